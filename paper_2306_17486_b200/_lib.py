@@ -1,0 +1,136 @@
+"""ctypes binding of the C-ABI library ``libhelmsolve_b200.so`` (include/helmsolve_b200.h).
+
+The library is built in-tree for sm_100a (``make -C paper_2306_17486_b200`` or
+``__graft_entry__.build()``).  There is no fallback: if the library or a GPU is
+missing, every compute entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libhelmsolve_b200.so")
+
+HS_OK, HS_EDIMENSION, HS_ESINGULAR, HS_EBREAKDOWN, HS_ENONFINITE, HS_ECONFIG, HS_ECUDA = range(7)
+HS_APPLY_C64_F32, HS_APPLY_C64_F64, HS_APPLY_C128 = 0, 1, 2
+
+c_int_p = ctypes.POINTER(ctypes.c_int)
+c_double_p = ctypes.POINTER(ctypes.c_double)
+
+
+class HsLevel(ctypes.Structure):
+    _fields_ = [
+        ("nx", ctypes.c_int),
+        ("ny", ctypes.c_int),
+        ("h", ctypes.c_double),
+        ("wall_x", ctypes.c_double),
+        ("wall_y", ctypes.c_double),
+        ("mass", ctypes.c_void_p),
+    ]
+
+
+class HsHierarchy(ctypes.Structure):
+    _fields_ = [
+        ("num_levels", ctypes.c_int),
+        ("n_models", ctypes.c_int),
+        ("levels", HsLevel * 8),
+        ("relax_pre", ctypes.c_int),
+        ("relax_post", ctypes.c_int),
+        ("damping_pre", ctypes.c_double),
+        ("damping_post", ctypes.c_double),
+        ("coarse_iters", ctypes.c_int),
+        ("coarse_damping", ctypes.c_double),
+    ]
+
+
+class HsSolveArgs(ctypes.Structure):
+    _fields_ = [
+        ("B", ctypes.c_int),
+        ("max_iter", ctypes.c_int),
+        ("restart", ctypes.c_int),
+        ("b", ctypes.c_void_p),
+        ("x0", ctypes.c_void_p),
+        ("x", ctypes.c_void_p),
+        ("tol", ctypes.c_void_p),
+        ("c_true", ctypes.c_void_p),
+        ("model_of", ctypes.c_void_p),
+        ("hist", ctypes.c_void_p),
+        ("hist_len", ctypes.c_void_p),
+        ("iterations", ctypes.c_void_p),
+        ("converged", ctypes.c_void_p),
+        ("status", ctypes.c_void_p),
+    ]
+
+
+# (name, restype, argtypes) for every symbol include/helmsolve_b200.h declares
+_VP, _I, _D, _SZ = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_size_t
+SIGNATURES = {
+    "hs_abi_version": (_I, []),
+    "hs_last_error": (ctypes.c_char_p, []),
+    "hs_helm_apply": (_I, [_VP, _VP, _VP, _VP, _I, _I, _I, _D, _D, _D, _I, _VP]),
+    "hs_restrict": (_I, [_VP, _VP, _I, _I, _I, _I, _VP]),
+    "hs_prolong": (_I, [_VP, _VP, _I, _I, _I, _I, _I, _I, _VP]),
+    "hs_jacobi": (_I, [_VP, _VP, _VP, ctypes.POINTER(HsLevel), _VP, _I, _D, _VP]),
+    "hs_vcycle_workspace_bytes": (_SZ, [ctypes.POINTER(HsHierarchy), _I]),
+    "hs_vcycle": (_I, [ctypes.POINTER(HsHierarchy), _VP, _VP, _VP, _VP, _I, _VP, _SZ, _VP, _VP]),
+    "hs_fgmres_workspace_bytes": (_SZ, [ctypes.POINTER(HsHierarchy), _VP, _I, _I, _I, _I, _I]),
+    "hs_fgmres_solve": (_I, [ctypes.POINTER(HsHierarchy), _VP, ctypes.POINTER(HsSolveArgs), _VP, _SZ, _VP]),
+    "hs_net_create": (_I, [ctypes.POINTER(_VP), _VP]),
+    "hs_net_destroy": (None, [_VP]),
+    "hs_net_set_encodings": (_I, [_VP, _I, _VP]),
+    "hs_net_forward": (_I, [_VP, _VP, _VP, _VP, _I, _VP, _SZ, _VP]),
+    "hs_net_workspace_bytes": (_SZ, [_VP, _I]),
+    "hs_green_spectrum": (_I, [_VP, _I, _I, _I, _VP, _VP]),
+    "hs_implicit_apply": (_I, [_VP, _VP, _VP, _I, _I, _I, _I, _VP]),
+    "hs_conv2d": (_I, [_VP, _VP, _VP, _VP, _I, _I, _I, _I, _I, _I, _I, _VP]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load():
+    """Load (once) and return the ctypes library; raises if it is not built."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(
+                    f"{LIB_PATH} is not built; run `make -C {HERE}` (needs nvcc, sm_100a)"
+                )
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name, None)
+                if fn is None:
+                    continue  # checked by tests/test_abi.py against the header
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+        return _lib
+
+
+def last_error() -> str:
+    msg = load().hs_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, what: str):
+    """Map an HS_* return code onto the reference's exception classes."""
+    if rc == HS_OK:
+        return
+    from . import errors
+
+    msg = f"{what}: {last_error()}"
+    if rc == HS_EDIMENSION:
+        raise errors.DimensionError(msg)
+    if rc == HS_ESINGULAR:
+        raise errors.SingularityError(msg)
+    if rc == HS_EBREAKDOWN:
+        raise errors.SolverError(msg)
+    if rc == HS_ENONFINITE:
+        raise errors.NumericalError(msg)
+    if rc == HS_ECONFIG:
+        raise errors.ConfigurationError(msg)
+    raise RuntimeError(msg)

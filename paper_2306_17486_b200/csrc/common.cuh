@@ -1,0 +1,101 @@
+// Shared device helpers for the B200 Helmholtz FGMRES path.
+//
+// Layout conventions:
+//   * a field is (nx, ny) row-major, iy fastest, exactly the reference's
+//     ``data[ix, iy]`` C order (fields.py:5-12); a batch is (B, nx, ny);
+//   * complex64 is interleaved float2, complex128 interleaved double2;
+//   * outside the grid every field is zero (Dirichlet padding, fields.py:191-199).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define HS_DEV __device__ __forceinline__
+
+// ------------------------------------------------------------------ complex
+
+HS_DEV float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+HS_DEV float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+HS_DEV float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+HS_DEV float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a / b for complex b (fp32; |b| is O(1/h^2) so no scaling is needed)
+HS_DEV float2 cdiv(float2 a, float2 b) {
+  float inv = 1.0f / (b.x * b.x + b.y * b.y);
+  return make_float2((a.x * b.x + a.y * b.y) * inv, (a.y * b.x - a.x * b.y) * inv);
+}
+
+HS_DEV double2 zadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+HS_DEV double2 zsub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+HS_DEV double2 zscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+// exact numpy-style complex product (no FMA contraction): (ac - bd) + (ad + bc) i
+HS_DEV double2 zmul(double2 a, double2 b) {
+  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
+                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+}
+// conj(a) * b
+HS_DEV double2 zcmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+HS_DEV double2 f2d(float2 a) { return make_double2((double)a.x, (double)a.y); }
+HS_DEV float2 d2f(double2 a) { return make_float2((float)a.x, (float)a.y); }
+
+// ------------------------------------------------------------------ reductions
+
+HS_DEV double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+HS_DEV float warp_sumf(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum of NV doubles per thread; result valid in every thread.
+// `scratch` must hold NV * (blockDim.x / 32) doubles.  Deterministic order.
+template <int NV>
+HS_DEV void block_sum(double (&v)[NV], double* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) scratch[i * nw + warp] = v[i];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += scratch[i * nw + w];
+    v[i] = s;
+  }
+  __syncthreads();
+}
+
+// Dynamic-count variant: n values per thread stored in v[0..n), n <= NMAX.
+template <int NMAX>
+HS_DEV void block_sum_n(double* v, int n, double* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = 0; i < n; ++i) v[i] = warp_sum(v[i]);
+  __syncthreads();
+  if (lane == 0)
+    for (int i = 0; i < n; ++i) scratch[i * nw + warp] = v[i];
+  __syncthreads();
+  for (int i = 0; i < n; ++i) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += scratch[i * nw + w];
+    v[i] = s;
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------ errors
+
+// status codes: HS_OK, HS_EDIMENSION, ... from the public header
+#include "../../include/helmsolve_b200.h"
+
+
+inline unsigned cdiv_u(long a, long b) { return (unsigned)((a + b - 1) / b); }

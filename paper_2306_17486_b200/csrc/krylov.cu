@@ -1,0 +1,399 @@
+// Batched device-resident flexible GMRES (krylov.py:39-146) for the outer
+// Helmholtz solve.  Every RHS carries its own window position, Hessenberg
+// matrix, Givens rotations and history, so RHS that converge (or restart
+// after the drift guard, krylov.py:140-141) simply drop out of later steps.
+//
+// Precision recipe: the basis V and Z are complex64, the
+// true-operator matvec A z and the true residual b - A x are evaluated in
+// fp64 from the stored values, every reduction accumulates in fp64, the
+// Hessenberg/Givens work is fp64 and the iterate x is complex128.
+//
+// w = A z_j is never stored: each Gram-Schmidt pass recomputes it in fp64
+// registers from z_j (8 B/node) and the L2-resident medium.  V_{j+1} is written
+// unnormalised with its scale 1/h_{j+1,j} kept per RHS, saving the
+// normalisation sweep.
+#include <algorithm>
+
+#include "common.cuh"
+#include "krylov.h"
+
+namespace hs {
+
+namespace {
+
+constexpr int NT = 256;
+constexpr int KC = 12;            // basis vectors per chunk in a dot pass
+constexpr int PST = 2 * KC + 1;   // doubles per partial record
+constexpr int kChunks = (kMaxRestart + KC - 1) / KC;
+
+enum Mode { DOT = 0, ORTH = 1, REDOT = 2, ORTH2 = 3 };
+
+HS_DEV double2 ldz(const float2* p) {
+  float2 v = *p;
+  return make_double2((double)v.x, (double)v.y);
+}
+
+// (A u)(p) of the TRUE operator (shift 1 + 0i, no wall), fp64, summation
+// order of neg_laplacian (fields.py:191-199) then minus c u (fields.py:208-210).
+template <typename LD>
+HS_DEV double2 apply_true(LD ld, const double2* __restrict__ c, int nx, int ny, int p, int i, int j, double h2) {
+  double2 u = ld(p);
+  double2 z0 = make_double2(0.0, 0.0);
+  double2 xp = i + 1 < nx ? ld(p + ny) : z0;
+  double2 xm = i > 0 ? ld(p - ny) : z0;
+  double2 yp = j + 1 < ny ? ld(p + 1) : z0;
+  double2 ym = j > 0 ? ld(p - 1) : z0;
+  double lr = __dsub_rn(__dsub_rn(__dsub_rn(__dsub_rn(4.0 * u.x, xp.x), xm.x), yp.x), ym.x);
+  double li = __dsub_rn(__dsub_rn(__dsub_rn(__dsub_rn(4.0 * u.y, xp.y), xm.y), yp.y), ym.y);
+  double2 cu = zmul(c[p], u);
+  return make_double2(__dsub_rn(__ddiv_rn(lr, h2), cu.x), __dsub_rn(__ddiv_rn(li, h2), cu.y));
+}
+
+// Deterministic two-level reduction: block partials, then the last block of
+// each RHS folds them in block order and runs `finish`.
+HS_DEV bool arrive_last(int* counter, int total) {
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1) == total - 1);
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    if (threadIdx.x == 0) *counter = 0;
+  }
+  return s_last;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(NT) k_arnoldi(SolveDims d, SolveBuffers s, int nchunks) {
+  __shared__ double red[PST * (NT / 32)];
+  __shared__ double2 s_coef[kMaxRestart + 1];
+  const int blk = blockIdx.x, chunk = blockIdx.y, b = blockIdx.z;
+  RhsState& S = s.st[b];
+  const int active = S.active;
+  const int reorth = S.reorth;
+  if (!active) return;
+  if ((MODE == REDOT || MODE == ORTH2) && !reorth) return;
+  const int j = S.j, J = j + 1, m = d.restart;
+  const int N = (int)d.N;
+  const float2* Vb = s.V + (long long)b * (m + 1) * N;
+  const float2* zb = s.Z + ((long long)b * m + j) * N;
+  const double2* c = s.c_true + (long long)(s.model_of ? s.model_of[b] : 0) * N;
+  if (MODE != DOT) {
+    for (int k = threadIdx.x; k < J; k += NT) s_coef[k] = zscale(S.hcol[k], S.vscale[k]);
+    __syncthreads();
+  }
+  const int k0 = chunk * KC;
+  double acc[PST];
+#pragma unroll
+  for (int t = 0; t < PST; ++t) acc[t] = 0.0;
+  int bad = 0;
+  auto ldz_b = [&](int q) { return ldz(zb + q); };
+  for (int p = blk * NT + threadIdx.x; p < N; p += d.nblk * NT) {
+    const int i = p / d.ny, jj = p - i * d.ny;
+    double2 w = apply_true(ldz_b, c, d.nx, d.ny, p, i, jj, d.h2);
+    if (MODE == DOT) {
+      if (!isfinite(w.x) || !isfinite(w.y)) bad = 1;
+      if (chunk == 0) acc[2 * KC] += w.x * w.x + w.y * w.y;
+    } else {
+      for (int k = 0; k < J; ++k) {
+        double2 v = ldz(Vb + (long long)k * N + p);
+        double2 cv = zmul(s_coef[k], v);
+        w = zsub(w, cv);
+      }
+    }
+    if (MODE == DOT || MODE == REDOT) {
+#pragma unroll
+      for (int kk = 0; kk < KC; ++kk) {
+        if (k0 + kk < J) {
+          double2 dv = zcmul(ldz(Vb + (long long)(k0 + kk) * N + p), w);
+          acc[2 * kk] += dv.x;
+          acc[2 * kk + 1] += dv.y;
+        }
+      }
+    } else {
+      const_cast<float2*>(Vb)[(long long)J * N + p] = d2f(w);
+      acc[2 * KC] += w.x * w.x + w.y * w.y;
+    }
+  }
+  if (MODE == DOT && bad) atomicOr(&S.nonfinite, 1);
+  block_sum<PST>(acc, red);
+  double* part = s.partial + (((long long)b * nchunks + chunk) * d.nblk + blk) * PST;
+  if (threadIdx.x < PST) part[threadIdx.x] = acc[threadIdx.x];
+  if (!arrive_last(&s.counter[b], nchunks * d.nblk)) return;
+  // ---- finish (one block per RHS)
+  const double* pb = s.partial + (long long)b * nchunks * d.nblk * PST;
+  if (MODE == DOT || MODE == REDOT) {
+    for (int t = threadIdx.x; t < 2 * J; t += NT) {
+      const int k = t >> 1, ch = k / KC, slot = 2 * (k % KC) + (t & 1);
+      double sum = 0.0;
+      for (int q = 0; q < d.nblk; ++q) sum += pb[((long long)ch * d.nblk + q) * PST + slot];
+      red[t] = sum * S.vscale[k];
+    }
+    if (MODE == DOT && threadIdx.x == 0) {
+      double nn = 0.0;
+      for (int q = 0; q < d.nblk; ++q) nn += pb[(long long)q * PST + 2 * KC];
+      S.wn = sqrt(nn);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < J; k += NT) {
+      double2 v = make_double2(red[2 * k], red[2 * k + 1]);
+      S.hcol[k] = MODE == DOT ? v : zadd(S.hcol[k], v);
+    }
+  } else if (threadIdx.x == 0) {
+    double nn = 0.0;
+    for (int q = 0; q < d.nblk; ++q) nn += pb[(long long)q * PST + 2 * KC];
+    S.hn = sqrt(nn);
+    if (MODE == ORTH) S.reorth = S.hn < 0.25 * S.wn;  // krylov.py:105
+  }
+}
+
+// Hessenberg column, Givens rotation, estimate, stopping tests (krylov.py:112-135)
+__global__ void k_givens(SolveDims d, SolveBuffers s) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= d.B) return;
+  RhsState& S = s.st[b];
+  if (!S.active) return;
+  if (S.nonfinite) {
+    S.status = HS_ENONFINITE;
+    S.active = 0;
+    return;
+  }
+  const int j = S.j;
+  double2 col[kMaxRestart + 1];
+  for (int k = 0; k <= j; ++k) col[k] = S.hcol[k];
+  for (int k = 0; k < j; ++k) {
+    double2 a = col[k], bb = col[k + 1], sk = S.sn[k];
+    col[k] = zadd(zscale(a, S.cs[k]), zmul(sk, bb));
+    col[k + 1] = zadd(zmul(make_double2(-sk.x, sk.y), a), zscale(bb, S.cs[k]));
+  }
+  const double hn = S.hn;
+  double2 a = col[j];
+  double cr;
+  double2 sr, rr;
+  const double mag = hypot(a.x, a.y);  // krylov.py:29-36
+  if (mag == 0.0) {
+    cr = 0.0;
+    sr = make_double2(1.0, 0.0);
+    rr = make_double2(hn, 0.0);
+  } else {
+    const double t = hypot(mag, hn);
+    const double2 ph = make_double2(a.x / mag, a.y / mag);
+    cr = mag / t;
+    sr = zscale(ph, hn / t);
+    rr = zscale(ph, t);
+  }
+  S.cs[j] = cr;
+  S.sn[j] = sr;
+  col[j] = rr;
+  for (int k = 0; k <= j; ++k) S.H[k * kMaxRestart + j] = col[k];
+  const double2 gj = S.g[j];
+  S.g[j] = zscale(gj, cr);
+  S.g[j + 1] = zmul(make_double2(-sr.x, sr.y), gj);
+  S.iter += 1;
+  S.j = j + 1;
+  const double est = hypot(S.g[j + 1].x, S.g[j + 1].y) / S.beta0;
+  s.hist[(long long)b * d.hist_stride + S.iter] = est;
+  S.hist_len = S.iter + 1;
+  if (est <= S.tol) {
+    S.conv_est = 1;
+    S.window_end = 1;
+  } else if (hn <= 1e-14 * fmax(1.0, S.wn)) {
+    S.status = HS_EBREAKDOWN;  // krylov.py:130-134
+    S.active = 0;
+    return;
+  } else {
+    S.vscale[j + 1] = 1.0 / hn;
+    if (S.j == S.m) S.window_end = 1;
+  }
+  if (S.window_end) {  // y = R^{-1} g (krylov.py:149-153)
+    const int n = S.j;
+    for (int r = n - 1; r >= 0; --r) {
+      double2 acc = S.g[r];
+      for (int k = r + 1; k < n; ++k) acc = zsub(acc, zmul(S.H[r * kMaxRestart + k], S.y[k]));
+      const double2 dd = S.H[r * kMaxRestart + r];
+      const double den = dd.x * dd.x + dd.y * dd.y;
+      S.y[r] = make_double2((acc.x * dd.x + acc.y * dd.y) / den, (acc.y * dd.x - acc.x * dd.y) / den);
+    }
+  }
+}
+
+// x += Z y at the end of a window (krylov.py:136-137)
+__global__ void __launch_bounds__(NT) k_xupdate(SolveDims d, SolveBuffers s) {
+  __shared__ double2 s_y[kMaxRestart];
+  const int b = blockIdx.y;
+  RhsState& S = s.st[b];
+  if (!S.active || !S.window_end) return;
+  const int n = S.j, N = (int)d.N;
+  for (int k = threadIdx.x; k < n; k += NT) s_y[k] = S.y[k];
+  __syncthreads();
+  const float2* Zb = s.Z + (long long)b * d.restart * N;
+  double2* xb = s.x + (long long)b * N;
+  for (int p = blockIdx.x * NT + threadIdx.x; p < N; p += d.nblk * NT) {
+    double2 t = make_double2(0.0, 0.0);
+    for (int k = 0; k < n; ++k) t = zadd(t, zmul(s_y[k], ldz(Zb + (long long)k * N + p)));
+    xb[p] = zadd(xb[p], t);
+  }
+}
+
+HS_DEV void start_window(RhsState& S, const SolveDims& d, double beta) {
+  S.m = min(min(d.restart, d.max_iter), d.max_iter - S.iter);  // krylov.py:79,83
+  S.j = 0;
+  S.vscale[0] = 1.0 / beta;
+  S.g[0] = make_double2(beta, 0.0);
+  for (int k = 1; k <= kMaxRestart; ++k) S.g[k] = make_double2(0.0, 0.0);
+  S.window_end = 0;
+  S.conv_est = 0;
+  S.reorth = 0;
+}
+
+// r = b - A x (fp64), V_0 = r (unnormalised); INIT: beta0 and the first window,
+// else the drift guard and restart logic of krylov.py:138-143.
+template <bool INIT>
+__global__ void __launch_bounds__(NT) k_residual(SolveDims d, SolveBuffers s, int use_x) {
+  __shared__ double red[NT / 32];
+  const int blk = blockIdx.x, b = blockIdx.y;
+  RhsState& S = s.st[b];
+  if (!S.active) return;
+  if (!INIT && !S.window_end) return;
+  const int N = (int)d.N, m = d.restart;
+  const double2* xb = s.x + (long long)b * N;
+  const double2* bb = s.b + (long long)b * N;
+  const double2* c = s.c_true + (long long)(s.model_of ? s.model_of[b] : 0) * N;
+  float2* V0 = s.V + (long long)b * (m + 1) * N;
+  double acc[1] = {0.0};
+  auto ldx = [&](int q) { return xb[q]; };
+  for (int p = blk * NT + threadIdx.x; p < N; p += d.nblk * NT) {
+    double2 r = bb[p];
+    if (use_x) {
+      const int i = p / d.ny, jj = p - i * d.ny;
+      r = zsub(r, apply_true(ldx, c, d.nx, d.ny, p, i, jj, d.h2));
+    }
+    V0[p] = d2f(r);
+    acc[0] += r.x * r.x + r.y * r.y;
+  }
+  block_sum<1>(acc, red);
+  double* part = s.partial + (long long)b * kChunks * d.nblk * PST + blk;
+  if (threadIdx.x == 0) part[0] = acc[0];
+  if (!arrive_last(&s.counter[b], d.nblk)) return;
+  if (threadIdx.x != 0) return;
+  const double* pb = s.partial + (long long)b * kChunks * d.nblk * PST;
+  double rr = 0.0;
+  for (int q = 0; q < d.nblk; ++q) rr += pb[q];
+  const double rn = sqrt(rr);
+  double* hist = s.hist + (long long)b * d.hist_stride;
+  if (INIT) {
+    S.beta0 = rn;
+    hist[0] = 1.0;
+    S.hist_len = 1;
+    if (rn == 0.0) {  // krylov.py:73-75
+      hist[1] = 0.0;
+      S.hist_len = 2;
+      S.converged = 1;
+      S.active = 0;
+      return;
+    }
+    if (1.0 <= S.tol) {  // krylov.py:76-77
+      S.converged = 1;
+      S.active = 0;
+      return;
+    }
+    start_window(S, d, rn);
+    return;
+  }
+  const double true_rel = rn / S.beta0;
+  if (S.conv_est && true_rel > S.tol) S.conv_est = 0;  // drift guard
+  if (S.conv_est) {
+    hist[S.iter] = true_rel;
+    S.converged = 1;
+    S.active = 0;
+  } else if (S.iter >= d.max_iter) {
+    S.active = 0;
+  } else {
+    start_window(S, d, rn);
+  }
+}
+
+__global__ void k_init_state(SolveDims d, SolveBuffers s, const double* tol) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= d.B) return;
+  RhsState& S = s.st[b];
+  S.active = 1;
+  S.j = 0;
+  S.m = 0;
+  S.iter = 0;
+  S.status = 0;
+  S.nonfinite = 0;
+  S.reorth = 0;
+  S.window_end = 0;
+  S.conv_est = 0;
+  S.converged = 0;
+  S.hist_len = 0;
+  S.tol = tol[b];
+  S.beta0 = 0.0;
+  s.counter[b] = 0;
+}
+
+__global__ void k_zero_x(SolveDims d, SolveBuffers s) {
+  long long n = (long long)d.B * d.N;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x)
+    s.x[p] = make_double2(0.0, 0.0);
+}
+
+__global__ void k_prep(SolveDims d, SolveBuffers s) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= d.B) return;
+  const RhsState& S = s.st[b];
+  const long long N = d.N;
+  if (S.active) {
+    s.vin[b] = s.V + ((long long)b * (d.restart + 1) + S.j) * N;
+    s.vin_scale[b] = (float)S.vscale[S.j];
+    s.zout[b] = s.Z + ((long long)b * d.restart + S.j) * N;
+  } else {
+    s.vin[b] = nullptr;
+    s.vin_scale[b] = 0.f;
+    s.zout[b] = nullptr;
+  }
+}
+
+__global__ void k_count_active(SolveDims d, SolveBuffers s) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  for (int b = threadIdx.x; b < d.B; b += blockDim.x)
+    if (s.st[b].active) atomicAdd(&cnt, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) *s.n_active = cnt;
+}
+
+}  // namespace
+
+size_t krylov_partial_doubles(const SolveDims& d) { return (size_t)d.B * kChunks * d.nblk * PST; }
+
+void krylov_init(const SolveDims& d, const SolveBuffers& s, const double* tol, bool have_x0,
+                 cudaStream_t stream) {
+  k_init_state<<<cdiv_u(d.B, 128), 128, 0, stream>>>(d, s, tol);
+  if (!have_x0) k_zero_x<<<592, 256, 0, stream>>>(d, s);
+  k_residual<true><<<dim3(d.nblk, d.B), NT, 0, stream>>>(d, s, have_x0 ? 1 : 0);
+}
+
+void krylov_prep(const SolveDims& d, const SolveBuffers& s, cudaStream_t stream) {
+  k_prep<<<cdiv_u(d.B, 128), 128, 0, stream>>>(d, s);
+}
+
+void krylov_after_precond(const SolveDims& d, const SolveBuffers& s, cudaStream_t stream) {
+  const int nch = (std::min(d.restart, d.max_iter) + KC - 1) / KC;
+  k_arnoldi<DOT><<<dim3(d.nblk, nch, d.B), NT, 0, stream>>>(d, s, nch);
+  k_arnoldi<ORTH><<<dim3(d.nblk, 1, d.B), NT, 0, stream>>>(d, s, 1);
+  k_arnoldi<REDOT><<<dim3(d.nblk, nch, d.B), NT, 0, stream>>>(d, s, nch);
+  k_arnoldi<ORTH2><<<dim3(d.nblk, 1, d.B), NT, 0, stream>>>(d, s, 1);
+  k_givens<<<cdiv_u(d.B, 64), 64, 0, stream>>>(d, s);
+  k_xupdate<<<dim3(d.nblk, d.B), NT, 0, stream>>>(d, s);
+  k_residual<false><<<dim3(d.nblk, d.B), NT, 0, stream>>>(d, s, 1);
+}
+
+void krylov_count_active(const SolveDims& d, const SolveBuffers& s, cudaStream_t stream) {
+  k_count_active<<<1, 256, 0, stream>>>(d, s);
+}
+
+}  // namespace hs

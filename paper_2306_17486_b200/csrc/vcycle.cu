@@ -1,0 +1,493 @@
+// Shifted-Laplacian V(1,1)-cycle kernels (multigrid.py:218-274), batched over
+// right-hand sides.  Each non-coarsest level costs two fused, shared-memory
+// tiled passes over HBM:
+//
+//   k_vc_down : u1 = u0 + w_pre (rhs - A u0)/diag       (jacobi_relax, :218-229)
+//               res = rhs - A u1                         (:270)
+//               coarse_rhs = R res                       (restrict_full_weighting, :64-78)
+//   k_vc_up   : u2 = u1 + P e_coarse                     (prolong_bilinear, :81-114, :273)
+//               u3 = u2 + w_post (rhs - A u2)/diag       (:274)
+//
+// u1 is recomputed in k_vc_up instead of being stored (cheaper: it needs only
+// rhs, the medium and u0, which k_vc_up reads anyway).
+// The coarsest level runs k_coarse_gmres: the reference's 10-step GMRES with
+// a damped-Jacobi preconditioner (coarse_solve, :232-244), one CTA per RHS,
+// basis kept in an L2-resident workspace, fp64 reductions.
+#include "common.cuh"
+#include "level.cuh"
+#include "vcycle.h"
+
+namespace hs {
+
+HS_DEV int floordiv2(int a) { return a >= 0 ? a / 2 : -((1 - a) / 2); }
+
+HS_DEV const float2* vin_ptr(const VecIn& v, int b) { return v.tab ? v.tab[b] : v.base + (long long)b * v.bstride; }
+HS_DEV float2* vout_ptr(const VecOut& v, int b) { return v.tab ? v.tab[b] : v.base + (long long)b * v.bstride; }
+
+// zero-padded region load: s[a*ry + c] = g[(ox+a)*ny + (oy+c)] * scale
+HS_DEV void load_region(float2* s, int rx, int ry, const float2* __restrict__ g, int nx, int ny, int ox,
+                        int oy, float scale) {
+  for (int t = threadIdx.x; t < rx * ry; t += blockDim.x) {
+    int a = t / ry, c = t - a * ry;
+    int i = ox + a, j = oy + c;
+    float2 v = make_float2(0.f, 0.f);
+    if (i >= 0 && i < nx && j >= 0 && j < ny) v = g[(long long)i * ny + j];
+    s[t] = cscale(v, scale);
+  }
+}
+
+// ------------------------------------------------------------------ down leg
+
+template <int CX, int CY>
+__global__ void __launch_bounds__(256) k_vc_down(LevelDev L, int ncx, int ncy, VecIn rhs_in, VecIn u0_in,
+                                                 const float2* const* active, const int* model_of,
+                                                 float w_pre, float2* __restrict__ coarse_out) {
+  constexpr int RX = 2 * CX + 3, RY = 2 * CY + 3;
+  constexpr int UX = RX + 2, UY = RY + 2;
+  __shared__ float2 s_rhs[RX * RY];
+  __shared__ float2 s_c[RX * RY];
+  __shared__ float2 s_u1[RX * RY];
+  __shared__ float2 s_u0[UX * UY];
+  const int b = blockIdx.y;
+  if (active && active[b] == nullptr) return;
+  const int tiles_y = (ncy + CY - 1) / CY;
+  const int K0 = (blockIdx.x / tiles_y) * CX, L0 = (blockIdx.x % tiles_y) * CY;
+  const int ox = 2 * K0 - 1, oy = 2 * L0 - 1;
+  const long long N = (long long)L.nx * L.ny;
+  const int model = model_of ? model_of[b] : 0;
+  const float2* rhs = vin_ptr(rhs_in, b);
+  const float rs = rhs_in.scale ? rhs_in.scale[b] : 1.f;
+  const float2* u0 = (u0_in.tab || u0_in.base) ? vin_ptr(u0_in, b) : nullptr;
+  load_region(s_rhs, RX, RY, rhs, L.nx, L.ny, ox, oy, rs);
+  load_region(s_c, RX, RY, L.mass + model * N, L.nx, L.ny, ox, oy, 1.f);
+  if (u0) load_region(s_u0, UX, UY, u0, L.nx, L.ny, ox - 1, oy - 1, u0_in.scale ? u0_in.scale[b] : 1.f);
+  __syncthreads();
+  // pre-smoothing on the region (one damped Jacobi sweep)
+  for (int t = threadIdx.x; t < RX * RY; t += blockDim.x) {
+    int a = t / RY, c = t - a * RY;
+    int i = ox + a, j = oy + c;
+    float2 u1 = make_float2(0.f, 0.f);
+    if (i >= 0 && i < L.nx && j >= 0 && j < L.ny) {
+      float2 cc = s_c[t];
+      float2 d = level_diag(L, cc, i, j);
+      if (u0) {
+        const float2* q = s_u0 + (a + 1) * UY + (c + 1);
+        float2 au = level_apply(L, cc, i, j, q[0], q[UY], q[-UY], q[1], q[-1]);
+        u1 = cadd(q[0], cscale(cdiv(csub(s_rhs[t], au), d), w_pre));
+      } else {
+        u1 = cscale(cdiv(s_rhs[t], d), w_pre);
+      }
+    }
+    s_u1[t] = u1;
+  }
+  __syncthreads();
+  // residual on the interior of the region, in place over s_rhs
+  for (int t = threadIdx.x; t < (RX - 2) * (RY - 2); t += blockDim.x) {
+    int a = t / (RY - 2) + 1, c = t % (RY - 2) + 1;
+    int i = ox + a, j = oy + c;
+    int p = a * RY + c;
+    float2 r = make_float2(0.f, 0.f);
+    if (i >= 0 && i < L.nx && j >= 0 && j < L.ny) {
+      const float2* q = s_u1 + p;
+      r = csub(s_rhs[p], level_apply(L, s_c[p], i, j, q[0], q[RY], q[-RY], q[1], q[-1]));
+    }
+    s_rhs[p] = r;
+  }
+  __syncthreads();
+  // full-weighting restriction centred on fine 2K+1
+  const float fw[3] = {0.25f, 0.5f, 0.25f};
+  for (int t = threadIdx.x; t < CX * CY; t += blockDim.x) {
+    int k = t / CY, l = t - k * CY;
+    int K = K0 + k, Lq = L0 + l;
+    if (K >= ncx || Lq >= ncy) continue;
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < 3; ++u)
+#pragma unroll
+      for (int v = 0; v < 3; ++v) acc = cadd(acc, cscale(s_rhs[(2 * k + 1 + u) * RY + 2 * l + 1 + v], fw[u] * fw[v]));
+    coarse_out[(long long)b * ncx * ncy + (long long)K * ncy + Lq] = acc;
+  }
+}
+
+// ------------------------------------------------------------------ up leg
+
+template <int FX, int FY>
+__global__ void __launch_bounds__(256) k_vc_up(LevelDev L, int ncx, int ncy, VecIn rhs_in, VecIn u0_in,
+                                               const float2* const* active, const int* model_of, float w_pre,
+                                               float w_post, const float2* __restrict__ ecoarse, VecOut out) {
+  constexpr int RX = FX + 2, RY = FY + 2;
+  constexpr int UX = FX + 4, UY = FY + 4;
+  constexpr int EX = FX / 2 + 3, EY = FY / 2 + 3;
+  __shared__ float2 s_rhs[RX * RY];
+  __shared__ float2 s_c[RX * RY];
+  __shared__ float2 s_u2[RX * RY];
+  __shared__ float2 s_u0[UX * UY];
+  __shared__ float2 s_e[EX * EY];
+  const int b = blockIdx.y;
+  if (active && active[b] == nullptr) return;
+  const int tiles_y = (L.ny + FY - 1) / FY;
+  const int x0 = (blockIdx.x / tiles_y) * FX, y0 = (blockIdx.x % tiles_y) * FY;
+  const long long N = (long long)L.nx * L.ny;
+  const int model = model_of ? model_of[b] : 0;
+  const float2* rhs = vin_ptr(rhs_in, b);
+  const float rs = rhs_in.scale ? rhs_in.scale[b] : 1.f;
+  const float2* u0 = (u0_in.tab || u0_in.base) ? vin_ptr(u0_in, b) : nullptr;
+  const int kx0 = floordiv2(x0 - 3), ky0 = floordiv2(y0 - 3);
+  load_region(s_rhs, RX, RY, rhs, L.nx, L.ny, x0 - 1, y0 - 1, rs);
+  load_region(s_c, RX, RY, L.mass + model * N, L.nx, L.ny, x0 - 1, y0 - 1, 1.f);
+  load_region(s_e, EX, EY, ecoarse + (long long)b * ncx * ncy, ncx, ncy, kx0, ky0, 1.f);
+  if (u0) load_region(s_u0, UX, UY, u0, L.nx, L.ny, x0 - 2, y0 - 2, u0_in.scale ? u0_in.scale[b] : 1.f);
+  __syncthreads();
+  for (int t = threadIdx.x; t < RX * RY; t += blockDim.x) {
+    int a = t / RY, c = t - a * RY;
+    int i = x0 - 1 + a, j = y0 - 1 + c;
+    float2 u2 = make_float2(0.f, 0.f);
+    if (i >= 0 && i < L.nx && j >= 0 && j < L.ny) {
+      float2 cc = s_c[t];
+      float2 d = level_diag(L, cc, i, j);
+      float2 u1;
+      if (u0) {
+        const float2* q = s_u0 + (a + 1) * UY + (c + 1);
+        float2 au = level_apply(L, cc, i, j, q[0], q[UY], q[-UY], q[1], q[-1]);
+        u1 = cadd(q[0], cscale(cdiv(csub(s_rhs[t], au), d), w_pre));
+      } else {
+        u1 = cscale(cdiv(s_rhs[t], d), w_pre);
+      }
+      // P e: coarse K contributes to fine i when i - 2K in {0, 1, 2}
+      int kxa = (i & 1) ? (i - 1) / 2 : i / 2 - 1, kxb = (i & 1) ? kxa : i / 2;
+      int kya = (j & 1) ? (j - 1) / 2 : j / 2 - 1, kyb = (j & 1) ? kya : j / 2;
+      float2 pe = make_float2(0.f, 0.f);
+      for (int K = kxa; K <= kxb; ++K) {
+        float wx = prolong_w(i - 2 * K);
+        for (int Q = kya; Q <= kyb; ++Q) {
+          float wy = prolong_w(j - 2 * Q);
+          pe = cadd(pe, cscale(s_e[(K - kx0) * EY + (Q - ky0)], wx * wy));
+        }
+      }
+      u2 = cadd(u1, pe);
+    }
+    s_u2[t] = u2;
+  }
+  __syncthreads();
+  float2* dst = vout_ptr(out, b);
+  for (int t = threadIdx.x; t < FX * FY; t += blockDim.x) {
+    int a = t / FY + 1, c = t % FY + 1;
+    int i = x0 - 1 + a, j = y0 - 1 + c;
+    if (i >= L.nx || j >= L.ny) continue;
+    int p = a * RY + c;
+    const float2* q = s_u2 + p;
+    float2 cc = s_c[p];
+    float2 au = level_apply(L, cc, i, j, q[0], q[RY], q[-RY], q[1], q[-1]);
+    float2 u3 = cadd(q[0], cscale(cdiv(csub(s_rhs[p], au), level_diag(L, cc, i, j)), w_post));
+    dst[(long long)i * L.ny + j] = u3;
+  }
+}
+
+// ------------------------------------------------------------ coarsest level
+//
+// GMRES(m) with M = damping/diag and x0 = 0, tol 1e-12 (coarse_solve,
+// multigrid.py:232-244 -> krylov.py:39-146).  One CTA per RHS.  V_0 is the rhs
+// itself (scale 1/beta0); V_k, k >= 1, live unnormalised in `vws` with their
+// scales 1/h_{k,k-1} in shared memory.  Dot products accumulate in fp64 and
+// are reduced deterministically; the Hessenberg/Givens work is fp64 on
+// thread 0.  Breakdown / non-finite conditions are written to `status`.
+
+constexpr int kCoarseThreads = 512;
+
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse_gmres(LevelDev L, const float2* __restrict__ rhs_base,
+                                                                 float2* __restrict__ x_out, float2* vws,
+                                                                 float2* sws, const float2* const* active,
+                                                                 const int* model_of, int m, float damping,
+                                                                 int* status) {
+  constexpr int NACC = 2 * (kCoarseMaxIters + 1) + 1;
+  __shared__ double red[NACC * (kCoarseThreads / 32)];
+  __shared__ double2 H[(kCoarseMaxIters + 1) * kCoarseMaxIters];
+  __shared__ double2 gv[kCoarseMaxIters + 1], sn[kCoarseMaxIters], yv[kCoarseMaxIters];
+  __shared__ double cs[kCoarseMaxIters], vs[kCoarseMaxIters + 1];
+  __shared__ double2 hc[kCoarseMaxIters + 1];
+  __shared__ int s_flag, s_jend;
+  const int b = blockIdx.x;
+  if (active && active[b] == nullptr) return;
+  const int nx = L.nx, ny = L.ny;
+  const long long N = (long long)nx * ny;
+  const float2* rhs = rhs_base + b * N;
+  float2* V = vws + (long long)b * (m + 1) * N;  // slots 1..m used
+  float2* S = sws + b * N;
+  float2* x = x_out + b * N;
+  const float2* mass = L.mass + (model_of ? model_of[b] : 0) * N;
+  auto vec = [&](int k) -> const float2* { return k == 0 ? rhs : V + k * N; };
+
+  // Jacobi scale s = damping / diag and beta0 = ||rhs||
+  double acc[NACC];
+  acc[0] = 0.0;
+  for (long long p = threadIdx.x; p < N; p += blockDim.x) {
+    int i = (int)(p / ny), j = (int)(p - (long long)i * ny);
+    S[p] = cdiv(make_float2(damping, 0.f), level_diag(L, mass[p], i, j));
+    float2 r = rhs[p];
+    acc[0] += (double)r.x * r.x + (double)r.y * r.y;
+  }
+  block_sum_n<NACC>(acc, 1, red);
+  const double beta0 = sqrt(acc[0]);
+  if (beta0 == 0.0) {
+    for (long long p = threadIdx.x; p < N; p += blockDim.x) x[p] = make_float2(0.f, 0.f);
+    return;
+  }
+  if (threadIdx.x == 0) {
+    vs[0] = 1.0 / beta0;
+    gv[0] = make_double2(beta0, 0.0);
+    s_flag = 0;
+    s_jend = m;
+  }
+  __syncthreads();  // S visible block-wide (global writes by this CTA, read via L1/L2)
+  __threadfence_block();
+
+  for (int j = 0; j < m; ++j) {
+    const float2* vj = vec(j);
+    float2* W = V + (j + 1) * N;
+    const float sj = (float)vs[j];
+    // pass A: w = A (S .* v_j), dots with v_0..v_j, ||w||^2
+    for (int k = 0; k < 2 * (j + 1) + 1; ++k) acc[k] = 0.0;
+    int bad = 0;
+    for (long long p = threadIdx.x; p < N; p += blockDim.x) {
+      int i = (int)(p / ny), jj = (int)(p - (long long)i * ny);
+      auto zat = [&](int ii, int jq) -> float2 {
+        if (ii < 0 || ii >= nx || jq < 0 || jq >= ny) return make_float2(0.f, 0.f);
+        long long q = (long long)ii * ny + jq;
+        return cscale(cmul(S[q], vj[q]), sj);
+      };
+      float2 w = level_apply(L, mass[p], i, jj, zat(i, jj), zat(i + 1, jj), zat(i - 1, jj), zat(i, jj + 1),
+                             zat(i, jj - 1));
+      if (!isfinite(w.x) || !isfinite(w.y)) bad = 1;
+      W[p] = w;
+      double2 wd = f2d(w);
+      acc[0] += wd.x * wd.x + wd.y * wd.y;
+#pragma unroll
+      for (int k = 0; k <= kCoarseMaxIters; ++k) {
+        if (k <= j) {
+          double2 d = zcmul(f2d(vec(k)[p]), wd);
+          acc[1 + 2 * k] += d.x;
+          acc[2 + 2 * k] += d.y;
+        }
+      }
+    }
+    if (bad) atomicOr(&s_flag, 1);
+    block_sum_n<NACC>(acc, 2 * (j + 1) + 1, red);
+    if (s_flag) {
+      if (threadIdx.x == 0) atomicCAS(status, 0, HS_ENONFINITE);
+      return;
+    }
+    const double wn = sqrt(acc[0]);
+    if (threadIdx.x == 0)
+      for (int k = 0; k <= j; ++k) {
+        hc[k] = make_double2(acc[1 + 2 * k] * vs[k], acc[2 + 2 * k] * vs[k]);
+        H[k * kCoarseMaxIters + j] = hc[k];
+      }
+    __syncthreads();
+    double hn2 = 0.0;
+    for (int pass = 0; pass < 2; ++pass) {
+      // w -= sum_k hc_k v_k ; ||w||^2   (hc = first-pass coefficients, then the extra part)
+      acc[0] = 0.0;
+      for (long long p = threadIdx.x; p < N; p += blockDim.x) {
+        float2 w = W[p];
+        for (int k = 0; k <= j; ++k) {
+          double2 hk = hc[k];
+          float2 coef = make_float2((float)(hk.x * vs[k]), (float)(hk.y * vs[k]));
+          w = csub(w, cmul(coef, vec(k)[p]));
+        }
+        W[p] = w;
+        acc[0] += (double)w.x * w.x + (double)w.y * w.y;
+      }
+      block_sum_n<NACC>(acc, 1, red);
+      hn2 = acc[0];
+      if (pass == 1 || sqrt(hn2) >= 0.25 * wn) break;
+      // one re-orthogonalisation pass (krylov.py:105-111): extra = V^H w
+      for (int k = 0; k < 2 * (j + 1); ++k) acc[k] = 0.0;
+      for (long long p = threadIdx.x; p < N; p += blockDim.x) {
+        double2 wd = f2d(W[p]);
+        for (int k = 0; k <= j; ++k) {
+          double2 d = zcmul(f2d(vec(k)[p]), wd);
+          acc[2 * k] += d.x;
+          acc[2 * k + 1] += d.y;
+        }
+      }
+      block_sum_n<NACC>(acc, 2 * (j + 1), red);
+      if (threadIdx.x == 0)
+        for (int k = 0; k <= j; ++k) {
+          hc[k] = make_double2(acc[2 * k] * vs[k], acc[2 * k + 1] * vs[k]);
+          H[k * kCoarseMaxIters + j] = zadd(H[k * kCoarseMaxIters + j], hc[k]);
+        }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      const double hn = sqrt(hn2);
+      double2 col[kCoarseMaxIters + 1];
+      for (int k = 0; k <= j; ++k) col[k] = H[k * kCoarseMaxIters + j];
+      for (int k = 0; k < j; ++k) {
+        double2 a = col[k], bb = col[k + 1];
+        double2 s = sn[k];
+        col[k] = zadd(zscale(a, cs[k]), zmul(s, bb));
+        col[k + 1] = zadd(zmul(make_double2(-s.x, s.y), a), zscale(bb, cs[k]));
+      }
+      double2 a = col[j];
+      double c;
+      double2 s, rr;
+      double mag = hypot(a.x, a.y);
+      if (mag == 0.0) {
+        c = 0.0;
+        s = make_double2(1.0, 0.0);
+        rr = make_double2(hn, 0.0);
+      } else {
+        double t = hypot(mag, hn);
+        double2 ph = make_double2(a.x / mag, a.y / mag);
+        c = mag / t;
+        s = zscale(ph, hn / t);
+        rr = zscale(ph, t);
+      }
+      cs[j] = c;
+      sn[j] = s;
+      col[j] = rr;
+      for (int k = 0; k <= j; ++k) H[k * kCoarseMaxIters + j] = col[k];
+      double2 gj = gv[j];
+      gv[j] = zscale(gj, c);
+      gv[j + 1] = zmul(make_double2(-s.x, s.y), gj);
+      const double est = hypot(gv[j + 1].x, gv[j + 1].y) / beta0;
+      if (est <= 1e-12) {
+        s_jend = j + 1;
+        s_flag = 2;
+      } else if (hn <= 1e-14 * fmax(1.0, wn)) {
+        s_flag = 3;
+      }
+      vs[j + 1] = 1.0 / hn;
+    }
+    __syncthreads();
+    if (s_flag == 2) break;
+    if (s_flag == 3) {
+      if (threadIdx.x == 0) atomicCAS(status, 0, HS_EBREAKDOWN);
+      return;
+    }
+  }
+  // y = R^{-1} g ; x = sum_k y_k S v_k
+  const int jend = s_jend;
+  if (threadIdx.x == 0) {
+    for (int i = jend - 1; i >= 0; --i) {
+      double2 acc2 = gv[i];
+      for (int k = i + 1; k < jend; ++k) acc2 = zsub(acc2, zmul(H[i * kCoarseMaxIters + k], yv[k]));
+      double2 d = H[i * kCoarseMaxIters + i];
+      double den = d.x * d.x + d.y * d.y;
+      yv[i] = make_double2((acc2.x * d.x + acc2.y * d.y) / den, (acc2.y * d.x - acc2.x * d.y) / den);
+    }
+  }
+  __syncthreads();
+  for (long long p = threadIdx.x; p < N; p += blockDim.x) {
+    float2 sum = make_float2(0.f, 0.f);
+    for (int k = 0; k < jend; ++k) {
+      float2 yk = make_float2((float)(yv[k].x * vs[k]), (float)(yv[k].y * vs[k]));
+      sum = cadd(sum, cmul(yk, vec(k)[p]));
+    }
+    x[p] = cmul(S[p], sum);
+  }
+}
+
+}  // namespace hs
+
+// ------------------------------------------------------------------ host side
+
+namespace hs {
+
+namespace {
+constexpr int kDownCX = 8, kDownCY = 32;
+constexpr int kUpFX = 16, kUpFY = 64;
+
+__global__ void k_gather_scaled(VecIn in, const float2* const* active, float2* out, long long N) {
+  const int b = blockIdx.y;
+  if (active && active[b] == nullptr) return;
+  const float2* src = vin_ptr(in, b);
+  const float s = in.scale ? in.scale[b] : 1.f;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x)
+    out[b * N + p] = cscale(src[p], s);
+}
+
+__global__ void k_scatter(const float2* in, const float2* const* active, VecOut out, long long N) {
+  const int b = blockIdx.y;
+  if (active && active[b] == nullptr) return;
+  float2* dst = vout_ptr(out, b);
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x)
+    dst[p] = in[b * N + p];
+}
+
+size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
+}  // namespace
+
+size_t vcycle_workspace_bytes(const Hierarchy& H, int B) {
+  size_t total = 0;
+  for (int l = 1; l < H.num_levels; ++l) {
+    size_t n = (size_t)H.lv[l].nx * H.lv[l].ny;
+    total += 2 * align_up(n * B * sizeof(float2));  // rhs_l and e_l
+  }
+  const LevelDev& C = H.lv[H.num_levels - 1];
+  size_t nc = (size_t)C.nx * C.ny;
+  total += align_up(nc * B * (H.coarse_iters + 1) * sizeof(float2));  // coarse basis
+  total += align_up(nc * B * sizeof(float2));                          // coarse Jacobi scale
+  if (H.num_levels == 1) total += 2 * align_up(nc * B * sizeof(float2));
+  return total;
+}
+
+void vcycle(const Hierarchy& H, VecIn rhs, VecIn u0, VecOut out, const float2* const* active,
+            const int* model_of, int B, void* ws, int* status, cudaStream_t stream) {
+  char* p = static_cast<char*>(ws);
+  float2* lrhs[kMaxLevels] = {nullptr};
+  float2* lerr[kMaxLevels] = {nullptr};
+  for (int l = 1; l < H.num_levels; ++l) {
+    size_t n = (size_t)H.lv[l].nx * H.lv[l].ny;
+    lrhs[l] = reinterpret_cast<float2*>(p);
+    p += align_up(n * B * sizeof(float2));
+    lerr[l] = reinterpret_cast<float2*>(p);
+    p += align_up(n * B * sizeof(float2));
+  }
+  const int Lc = H.num_levels - 1;
+  const LevelDev& C = H.lv[Lc];
+  size_t nc = (size_t)C.nx * C.ny;
+  float2* cV = reinterpret_cast<float2*>(p);
+  p += align_up(nc * B * (H.coarse_iters + 1) * sizeof(float2));
+  float2* cS = reinterpret_cast<float2*>(p);
+  p += align_up(nc * B * sizeof(float2));
+
+  if (H.num_levels == 1) {
+    // multigrid.py:266-267: a one-level hierarchy is just the coarse solve (u0 ignored)
+    float2* tmp_in = reinterpret_cast<float2*>(p);
+    p += align_up(nc * B * sizeof(float2));
+    float2* tmp_out = reinterpret_cast<float2*>(p);
+    dim3 g(cdiv_u(nc, 256 * 4), B);
+    k_gather_scaled<<<g, 256, 0, stream>>>(rhs, active, tmp_in, (long long)nc);
+    k_coarse_gmres<<<B, kCoarseThreads, 0, stream>>>(C, tmp_in, tmp_out, cV, cS, active, model_of,
+                                                     H.coarse_iters, H.coarse_damping, status);
+    k_scatter<<<g, 256, 0, stream>>>(tmp_out, active, out, (long long)nc);
+    return;
+  }
+  // down legs
+  for (int l = 0; l < Lc; ++l) {
+    const LevelDev& F = H.lv[l];
+    const int ncx = H.lv[l + 1].nx, ncy = H.lv[l + 1].ny;
+    VecIn in = l == 0 ? rhs : VecIn{nullptr, lrhs[l], (long long)F.nx * F.ny, nullptr};
+    VecIn uz = l == 0 ? u0 : VecIn{nullptr, nullptr, 0, nullptr};
+    dim3 g(cdiv_u(ncx, kDownCX) * cdiv_u(ncy, kDownCY), B);
+    k_vc_down<kDownCX, kDownCY><<<g, 256, 0, stream>>>(F, ncx, ncy, in, uz, active, model_of, H.w_pre,
+                                                        lrhs[l + 1]);
+  }
+  // coarsest
+  k_coarse_gmres<<<B, kCoarseThreads, 0, stream>>>(C, lrhs[Lc], lerr[Lc], cV, cS, active, model_of,
+                                                   H.coarse_iters, H.coarse_damping, status);
+  // up legs
+  for (int l = Lc - 1; l >= 0; --l) {
+    const LevelDev& F = H.lv[l];
+    const int ncx = H.lv[l + 1].nx, ncy = H.lv[l + 1].ny;
+    VecIn in = l == 0 ? rhs : VecIn{nullptr, lrhs[l], (long long)F.nx * F.ny, nullptr};
+    VecIn uz = l == 0 ? u0 : VecIn{nullptr, nullptr, 0, nullptr};
+    VecOut o = l == 0 ? out : VecOut{nullptr, lerr[l], (long long)F.nx * F.ny};
+    dim3 g(cdiv_u(F.nx, kUpFX) * cdiv_u(F.ny, kUpFY), B);
+    k_vc_up<kUpFX, kUpFY><<<g, 256, 0, stream>>>(F, ncx, ncy, in, uz, active, model_of, H.w_pre, H.w_post,
+                                                 lerr[l + 1], o);
+  }
+}
+
+}  // namespace hs

@@ -1,0 +1,40 @@
+"""Device plumbing: torch CUDA tensors as the buffers handed to the C ABI.
+
+PyTorch only provides memory, streams and host<->device copies here; all
+arithmetic on the hot path runs in the library's own kernels.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("helmsolve_b200 needs a CUDA device (B200, sm_100a); none is visible")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def to_device(a, dtype: torch.dtype) -> torch.Tensor:
+    """numpy array or tensor -> contiguous CUDA tensor of ``dtype``."""
+    dev = require_cuda()
+    if isinstance(a, torch.Tensor):
+        return a.to(device=dev, dtype=dtype).contiguous()
+    arr = np.ascontiguousarray(a)
+    return torch.from_numpy(arr).to(device=dev, dtype=dtype).contiguous()
+
+
+def pinned(shape, dtype: torch.dtype) -> torch.Tensor:
+    return torch.empty(shape, dtype=dtype, pin_memory=True)
+
+
+def workspace(nbytes: int) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=require_cuda())

@@ -1,0 +1,302 @@
+"""Flexible GMRES and the solve protocols (mirror of ``helmsolve.krylov``).
+
+* ``fgmres`` keeps the reference's callable interface (``krylov.py:39-146``)
+  for arbitrary operators: the Krylov basis, Gram-Schmidt and the iterate live
+  on the GPU, the user callables are invoked once per iteration (with numpy
+  arrays if ``b`` was numpy, CUDA tensors otherwise).
+* ``solve_helmholtz`` / ``solve_with_learned_preconditioner``
+  (``krylov.py:156-246``) and ``solve_batch`` route to the native batched
+  engine (``hs_fgmres_solve``), which runs whole solves on the device.
+"""
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import DimensionError, NumericalError, SolverError
+from .fields import TRUE_SHIFT, ComplexField, SlownessModel
+
+
+@dataclass
+class SolveReport:
+    """Iterations and relative-residual trace of one solve (krylov.py:19-26)."""
+
+    iterations: int
+    relative_residual_history: list[float] = field(repr=False)
+    converged: bool = False
+    wall_time: float = 0.0
+
+
+def _givens(a: complex, b: float):
+    """(c, s, r): [c s; -conj(s) c] maps (a, b) to (r, 0), complex a, real b >= 0 (krylov.py:29-36)."""
+    if a == 0:
+        return 0.0, 1.0 + 0.0j, b
+    mag = abs(a)
+    t = math.hypot(mag, b)
+    return mag / t, (a / mag) * (b / t), (a / mag) * t
+
+
+def _solve_upper(R, g):
+    """Back substitution on the rotated Hessenberg matrix (krylov.py:149-153)."""
+    n = len(g)
+    y = np.zeros(n, dtype=np.complex128)
+    for i in range(n - 1, -1, -1):
+        y[i] = (g[i] - R[i, i + 1 :] @ y[i + 1 :]) / R[i, i]
+    return y
+
+
+def fgmres(apply_A, apply_M, b, x0=None, tol: float = 1e-7, max_iter: int = 250, restart: int | None = 10):
+    """Restarted, right-preconditioned flexible GMRES on arrays of any shape (krylov.py:39-146).
+
+    Stops when ||b - A x|| / ||b - A x0|| <= tol or after ``max_iter``
+    preconditioner applications.  Same control flow as the reference: CGS
+    with a conditional second pass, complex Givens rotations, the estimate
+    relative to the initial residual, and the drift guard at window ends.
+    """
+    import torch
+
+    from .device import require_cuda
+
+    if tol <= 0:
+        raise ValueError(f"tol must be positive, got {tol}")
+    if max_iter < 1:
+        raise ValueError(f"max_iter must be >= 1, got {max_iter}")
+    start = time.perf_counter()
+    dev = require_cuda()
+    host = not isinstance(b, torch.Tensor)
+    bd = (torch.from_numpy(np.asarray(b, dtype=np.complex128)) if host else b).to(dev, torch.complex128)
+    shape = tuple(bd.shape)
+    n = bd.numel()
+
+    def call(fn, v):
+        out = fn(v.reshape(shape).cpu().numpy() if host else v.reshape(shape))
+        t = torch.from_numpy(np.asarray(out, dtype=np.complex128)) if host else out
+        return t.to(dev, torch.complex128).reshape(-1)
+
+    if x0 is None:
+        x = torch.zeros(n, dtype=torch.complex128, device=dev)
+        r = bd.reshape(-1).clone()
+    else:
+        if tuple(np.shape(x0)) != shape:
+            raise DimensionError(f"x0 {tuple(np.shape(x0))} does not match b {shape}")
+        x = (torch.from_numpy(np.asarray(x0, dtype=np.complex128)) if host else x0).to(dev, torch.complex128)
+        x = x.reshape(-1).clone()
+        r = bd.reshape(-1) - call(apply_A, x)
+    beta0 = float(torch.linalg.vector_norm(r))
+    history = [1.0]
+
+    def result(xv, it, conv):
+        out = xv.reshape(shape)
+        return (out.cpu().numpy() if host else out), SolveReport(it, history, conv, time.perf_counter() - start)
+
+    if beta0 == 0.0:
+        history.append(0.0)
+        return result(x, 0, True)
+    if 1.0 <= tol:
+        return result(x, 0, True)
+    window = max_iter if restart is None else min(restart, max_iter)
+    iterations, converged = 0, False
+    while iterations < max_iter and not converged:
+        m = min(window, max_iter - iterations)
+        beta = float(torch.linalg.vector_norm(r))
+        V = torch.empty((m + 1, n), dtype=torch.complex128, device=dev)
+        Z = torch.empty((m, n), dtype=torch.complex128, device=dev)
+        H = np.zeros((m + 1, m), dtype=np.complex128)
+        rot = []
+        g = np.zeros(m + 1, dtype=np.complex128)
+        g[0] = beta
+        V[0] = r / beta
+        j = 0
+        while j < m:
+            z = call(apply_M, V[j])
+            w = call(apply_A, z)
+            if not bool(torch.isfinite(w).all()):
+                raise NumericalError(f"non-finite Krylov vector at iteration {iterations + 1}")
+            Z[j] = z
+            before = float(torch.linalg.vector_norm(w))
+            coeffs = V[: j + 1].conj() @ w
+            w = w - coeffs @ V[: j + 1]
+            h_next = float(torch.linalg.vector_norm(w))
+            if h_next < 0.25 * before:
+                extra = V[: j + 1].conj() @ w
+                coeffs = coeffs + extra
+                w = w - extra @ V[: j + 1]
+                h_next = float(torch.linalg.vector_norm(w))
+            col = coeffs.cpu().numpy()
+            for k, (c, s) in enumerate(rot):
+                col[k], col[k + 1] = c * col[k] + s * col[k + 1], -np.conj(s) * col[k] + c * col[k + 1]
+            c, s, rr = _givens(col[j], h_next)
+            rot.append((c, s))
+            col[j] = rr
+            H[: j + 1, j] = col
+            gj = g[j]
+            g[j], g[j + 1] = c * gj, -np.conj(s) * gj
+            iterations += 1
+            j += 1
+            estimate = abs(g[j]) / beta0
+            history.append(estimate)
+            if estimate <= tol:
+                converged = True
+                break
+            if h_next <= 1e-14 * max(1.0, before):
+                raise SolverError(
+                    f"Arnoldi breakdown at iteration {iterations} with relative residual {estimate:.3e}"
+                )
+            V[j] = w / h_next
+        y = torch.from_numpy(_solve_upper(H[:j, :j], g[:j])).to(dev)
+        x = x + y @ Z[:j]
+        r = bd.reshape(-1) - call(apply_A, x)
+        true_rel = float(torch.linalg.vector_norm(r)) / beta0
+        if converged and true_rel > tol:
+            converged = False  # the estimate drifted below tol early; keep iterating
+        if converged:
+            history[-1] = true_rel
+    return result(x, iterations, converged)
+
+
+# -------------------------------------------------------------- solve entry points
+
+
+def _engine_for(model: SlownessModel, hierarchy, net=None):
+    from .engine import Engine
+    from .multigrid import DeviceHierarchy, build_hierarchy
+
+    if hierarchy is None:
+        hierarchy = build_hierarchy(model)
+    key = ("_engine", id(model), id(net))
+    cached = hierarchy.__dict__.get(key)
+    if cached is None or cached[0] is not model:
+        dh = DeviceHierarchy([hierarchy], true_models=[model])
+        cached = (model, Engine(dh, net))
+        object.__setattr__(hierarchy, key, cached)
+    return cached[1]
+
+
+def solve_helmholtz(model: SlownessModel, b: ComplexField, hierarchy=None, tol: float = 1e-7, max_iter: int = 250,
+                    restart: int | None = 10) -> tuple[ComplexField, SolveReport]:
+    """FGMRES on the true operator with the V-cycle preconditioner (krylov.py:156-177)."""
+    import torch
+
+    from .engine import raise_for_status
+
+    if tol <= 0:
+        raise ValueError(f"tol must be positive, got {tol}")
+    if max_iter < 1:
+        raise ValueError(f"max_iter must be >= 1, got {max_iter}")
+    start = time.perf_counter()
+    eng = _engine_for(model, hierarchy)
+    bd = torch.from_numpy(np.ascontiguousarray(b.data))[None]
+    res = eng.fgmres(bd, None, tol, max_iter, restart)
+    raise_for_status(res)
+    x = res.x[0].cpu().numpy()
+    rep = SolveReport(int(res.iterations[0]), res.histories[0], bool(res.converged[0]), time.perf_counter() - start)
+    return ComplexField(x, b.h), rep
+
+
+def solve_with_learned_preconditioner(model: SlownessModel, b: ComplexField, net, encodings=None, tol: float = 1e-7,
+                                      max_iter: int = 250, restart: int | None = 10, warmup_iters: int = 3,
+                                      hierarchy=None) -> tuple[ComplexField, SolveReport]:
+    """V-cycle warm-up, then FGMRES with M(r) = v_cycle(r, net(r)) (krylov.py:180-246)."""
+    from .network import precompute_encodings
+
+    start = time.perf_counter()
+    if encodings is None:
+        encodings = precompute_encodings(net, model)
+    xs, reports = solve_batch([model], np.asarray(b.data)[None], net=net, encodings=[encodings], tol=tol,
+                              max_iter=max_iter, restart=restart, warmup_iters=warmup_iters,
+                              hierarchies=None if hierarchy is None else [hierarchy])
+    reports[0].wall_time = time.perf_counter() - start
+    return ComplexField(xs[0], b.h), reports[0]
+
+
+def solve_batch(models, rhs, model_of=None, net=None, encodings=None, tol: float = 1e-7, max_iter: int = 250,
+                restart: int | None = 10, warmup_iters: int = 3, hierarchies=None, num_levels: int = 3,
+                jacobi_damping=None, coarse_iters: int = 10, return_device: bool = False, raise_errors=True):
+    """Data-parallel solve of many RHS over one or more slowness models of equal shape.
+
+    ``rhs`` is (B, nx, ny) (numpy or CUDA tensor); ``model_of[i]`` names the
+    model of RHS i.  ``net is None``: the V-cycle-only protocol of
+    ``solve_helmholtz`` for every RHS; otherwise the warm-up + net->V-cycle
+    protocol of ``solve_with_learned_preconditioner`` (krylov.py:214-245).
+    Returns (x, reports): x (B, nx, ny) complex128 and one SolveReport per RHS.
+    """
+    import torch
+
+    from .device import require_cuda, to_device
+    from .engine import Engine, raise_for_status
+    from .multigrid import CHEBYSHEV_DAMPING, DeviceHierarchy, build_hierarchy
+
+    if tol <= 0:
+        raise ValueError(f"tol must be positive, got {tol}")
+    if max_iter < 1:
+        raise ValueError(f"max_iter must be >= 1, got {max_iter}")
+    start = time.perf_counter()
+    dev = require_cuda()
+    models = list(models)
+    if hierarchies is None:
+        damp = CHEBYSHEV_DAMPING if jacobi_damping is None else jacobi_damping
+        hierarchies = [build_hierarchy(m, num_levels=num_levels, jacobi_damping=damp, coarse_iters=coarse_iters)
+                       for m in models]
+    dh = DeviceHierarchy(hierarchies, true_models=models)
+    bd = to_device(rhs, torch.complex128)
+    B = bd.shape[0]
+    owner = np.zeros(B, dtype=np.int32) if model_of is None else np.asarray(model_of, dtype=np.int32)
+    owner_d = torch.from_numpy(owner).to(dev)
+    net_dev = None
+    if net is not None:
+        from .network import device_network
+
+        net_dev = device_network(net, models, encodings, dh)
+    eng = Engine(dh, net_dev)
+
+    if net is None:
+        res = eng.fgmres(bd, None, tol, max_iter, restart, owner_d)
+        reports = [SolveReport(int(res.iterations[i]), res.histories[i], bool(res.converged[i]), 0.0)
+                   for i in range(B)]
+        status = res.status
+        x = res.x
+    else:
+        # phase 1: V-cycle warm-up from zero (krylov.py:215-220)
+        r1 = eng.fgmres(bd, None, tol, min(warmup_iters, max_iter), restart, owner_d)
+        x = r1.x.clone()
+        status = r1.status.copy()
+        reports = [SolveReport(int(r1.iterations[i]), r1.histories[i], bool(r1.converged[i]), 0.0)
+                   for i in range(B)]
+        cont = [i for i in range(B) if not (r1.converged[i] or r1.iterations[i] >= max_iter) and not status[i]]
+        if cont:
+            idx = torch.tensor(cont, device=dev)
+            from .fields import apply_operator
+
+            # rel1 = ||b - A x1|| / ||b|| in fp64 on the device (krylov.py:222-223)
+            resid = torch.stack([
+                bd[i] - apply_operator(x[i], models[owner[i]]) for i in cont
+            ])
+            rel1 = (torch.linalg.vector_norm(resid.reshape(len(cont), -1), dim=1)
+                    / torch.linalg.vector_norm(bd[idx].reshape(len(cont), -1), dim=1)).cpu().numpy()
+            it1 = int(r1.iterations[cont[0]])
+            r2 = eng.fgmres(bd[idx], x[idx], tol / rel1, max_iter - it1, restart, owner_d[idx], use_net=True)
+            x[idx] = r2.x
+            for k, i in enumerate(cont):
+                reports[i] = SolveReport(
+                    reports[i].iterations + int(r2.iterations[k]),
+                    reports[i].relative_residual_history + [e * rel1[k] for e in r2.histories[k][1:]],
+                    bool(r2.converged[k]), 0.0)
+                status[i] = r2.status[k]
+                r2.iterations[k] += it1
+            if raise_errors:
+                for k in range(len(cont)):
+                    raise_for_status(r2, k)
+    wall = time.perf_counter() - start
+    for rep in reports:
+        rep.wall_time = wall
+    if raise_errors:
+        from .engine import BatchResult
+
+        chk = BatchResult(x, [r.relative_residual_history for r in reports],
+                          np.array([r.iterations for r in reports]), None, np.asarray(status))
+        for i in range(B):
+            raise_for_status(chk, i)
+    return (x if return_device else x.cpu().numpy()), reports
