@@ -171,7 +171,7 @@ def _engine_for(model: SlownessModel, hierarchy, net=None):
     if cached is None or cached[0] is not model:
         dh = DeviceHierarchy([hierarchy], true_models=[model])
         cached = (model, Engine(dh, net))
-        object.__setattr__(hierarchy, key, cached)
+        hierarchy.__dict__[key] = cached
     return cached[1]
 
 

@@ -81,15 +81,15 @@ def test_vcycle_matches_reference(tag):
     assert relerr(z1, g[f"z1_{tag}"]) < 2e-5
 
 
-def test_vcycle_linearity_and_zero(rng):
+def test_vcycle_homogeneity_and_zero(rng):
+    # GMRES on the coarsest level makes the cycle homogeneous (v(a r) = a v(r)) but
+    # not additive: the Krylov polynomial depends on the rhs (same in the reference).
     m = fields.slowness_model(rng.uniform(0.25, 1.0, (33, 33)), layer_width=4)
     H = multigrid.build_hierarchy(m)
     assert np.all(multigrid.v_cycle(np.zeros((33, 33), complex), None, H) == 0)
     a = complex_noise(rng, (33, 33))
-    b = complex_noise(rng, (33, 33))
-    za, zb = multigrid.v_cycle(a, None, H), multigrid.v_cycle(b, None, H)
-    zab = multigrid.v_cycle(2.0 * a - 1j * b, None, H)
-    assert relerr(zab, 2.0 * za - 1j * zb) < 1e-5
+    za = multigrid.v_cycle(a, None, H)
+    assert relerr(multigrid.v_cycle((2.0 - 1j) * a, None, H), (2.0 - 1j) * za) < 1e-5
 
 
 def test_batched_vcycle_over_two_models(rng):
