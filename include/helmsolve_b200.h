@@ -74,6 +74,31 @@ typedef struct {
 /* Encoder-solver network prepared for the device (ARCH.md); opaque. */
 typedef struct hs_net hs_net_t;
 
+/* One 3x3 convolution of the network with batch norm folded in
+ * (autodiff.conv2d / conv_transpose2d + batchnorm2d inference + softplus,
+ * autodiff.py:472-607): y = act(conv(x, w) + b).  w is device float32
+ * [cout][3][3][cin]; a transposed layer (stride 2) uses the same order. */
+typedef struct {
+  int cin, cout, stride, transposed, softplus;
+  const float* w;
+  const float* b;
+} hs_conv_t;
+
+/* Layer table of the ARCH.md network (the network.py the reference imports
+ * at krylov.py:201 but never shipped).  Index l of the per-level arrays is
+ * level l (0 = finest); down[0] / up[0] are unused. */
+typedef struct {
+  int levels;
+  int channels[8];
+  int ix, iy;            /* network grid (nx-1, ny-1) */
+  int nx, ny;            /* PDE grid */
+  float out_scale;       /* h^2/64 */
+  hs_conv_t enc_stem, enc_res_a[8], enc_res_b[8], enc_down[8];
+  hs_conv_t sol_stem, sol_res_a[8], sol_res_b[8], sol_down[8];
+  hs_conv_t sol_up[8], sol_ures_a[8], sol_ures_b[8], sol_head;
+  const void* implicit_w; /* complex64 (C_{L-1}/2, 3, 3) */
+} hs_net_desc_t;
+
 /* Arguments of one batched FGMRES solve (krylov.fgmres, krylov.py:39-146,
  * with apply_A = the true operator and apply_M = V-cycle or net->V-cycle). */
 typedef struct {
@@ -129,5 +154,38 @@ HS_API size_t hs_fgmres_workspace_bytes(const hs_hierarchy_t* h, const hs_net_t*
                                         int restart, int max_iter);
 HS_API int hs_fgmres_solve(const hs_hierarchy_t* h, const hs_net_t* net, const hs_solve_args_t* args, void* ws,
                            size_t ws_bytes, void* stream);
+
+/* ---- network (ARCH.md; the missing helmsolve.network, krylov.py:201) ---- */
+
+/* Build the device network; also computes the implicit layer's Green
+ * spectrum once (green.ImplicitKernel.spectrum, green.py:139-146).  The
+ * layer weights stay owned by the caller and must outlive the network. */
+HS_API int hs_net_create(hs_net_t** net, const hs_net_desc_t* desc, void* stream);
+HS_API void hs_net_destroy(hs_net_t* net);
+/* network.precompute_encodings (krylov.py:205-206): media is float32 NHWC
+ * (n_models, ix, iy, 2) = (kappa^2, gamma); enc[l] receives the level-l
+ * encodings, float32 NHWC (n_models, ix/2^l, iy/2^l, channels[l]), and the
+ * network keeps pointers to them for later forwards. */
+HS_API size_t hs_net_encode_workspace_bytes(const hs_net_t* net, int n_models);
+HS_API int hs_net_encode(hs_net_t* net, const float* media, int n_models, float* const* enc, void* ws,
+                         size_t ws_bytes, void* stream);
+/* use caller-held encodings (same layout as hs_net_encode's output) */
+HS_API int hs_net_set_encodings(hs_net_t* net, int levels, const float* const* enc);
+/* network.preconditioner_estimate (krylov.py:225-226): u0 = (h^2/64) net(r),
+ * r and u0 complex64 (B, nx, ny); model_of selects each RHS's encodings. */
+HS_API size_t hs_net_workspace_bytes(const hs_net_t* net, int B);
+HS_API int hs_net_forward(const hs_net_t* net, const void* r, void* u0, const int* model_of, int B, void* ws,
+                          size_t ws_bytes, void* stream);
+/* green.green_function (green.py:55-82): kernel complex64 (C, 3, 3) ->
+ * spectrum complex128 (C, 2h, 2w), the reference's numpy-2 dtype flow. */
+HS_API int hs_green_spectrum(const void* kernel, int C, int h, int w, void* spectrum, void* stream);
+/* green.implicit_apply (green.py:85-107): x complex64 (B, C, h, w),
+ * spectrum complex64 (C, 2h, 2w) -> y complex64 (B, C, h, w). */
+HS_API int hs_implicit_apply(const void* x, const void* spectrum, void* y, int B, int C, int h, int w,
+                             void* stream);
+/* one network convolution on float32 NHWC tensors (autodiff.conv2d /
+ * conv_transpose2d, pad 1): y = act(conv(x) + b) [+ addend] [+ residual]. */
+HS_API int hs_conv2d(const float* x, const hs_conv_t* conv, const float* addend, const float* residual, float* y,
+                     int B, int H, int W, void* stream);
 
 #endif

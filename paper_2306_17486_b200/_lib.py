@@ -64,6 +64,43 @@ class HsSolveArgs(ctypes.Structure):
     ]
 
 
+class HsConv(ctypes.Structure):
+    _fields_ = [
+        ("cin", ctypes.c_int),
+        ("cout", ctypes.c_int),
+        ("stride", ctypes.c_int),
+        ("transposed", ctypes.c_int),
+        ("softplus", ctypes.c_int),
+        ("w", ctypes.c_void_p),
+        ("b", ctypes.c_void_p),
+    ]
+
+
+class HsNetDesc(ctypes.Structure):
+    _fields_ = [
+        ("levels", ctypes.c_int),
+        ("channels", ctypes.c_int * 8),
+        ("ix", ctypes.c_int),
+        ("iy", ctypes.c_int),
+        ("nx", ctypes.c_int),
+        ("ny", ctypes.c_int),
+        ("out_scale", ctypes.c_float),
+        ("enc_stem", HsConv),
+        ("enc_res_a", HsConv * 8),
+        ("enc_res_b", HsConv * 8),
+        ("enc_down", HsConv * 8),
+        ("sol_stem", HsConv),
+        ("sol_res_a", HsConv * 8),
+        ("sol_res_b", HsConv * 8),
+        ("sol_down", HsConv * 8),
+        ("sol_up", HsConv * 8),
+        ("sol_ures_a", HsConv * 8),
+        ("sol_ures_b", HsConv * 8),
+        ("sol_head", HsConv),
+        ("implicit_w", ctypes.c_void_p),
+    ]
+
+
 # (name, restype, argtypes) for every symbol include/helmsolve_b200.h declares
 _VP, _I, _D, _SZ = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_size_t
 SIGNATURES = {
@@ -77,14 +114,16 @@ SIGNATURES = {
     "hs_vcycle": (_I, [ctypes.POINTER(HsHierarchy), _VP, _VP, _VP, _VP, _I, _VP, _SZ, _VP, _VP]),
     "hs_fgmres_workspace_bytes": (_SZ, [ctypes.POINTER(HsHierarchy), _VP, _I, _I, _I, _I, _I]),
     "hs_fgmres_solve": (_I, [ctypes.POINTER(HsHierarchy), _VP, ctypes.POINTER(HsSolveArgs), _VP, _SZ, _VP]),
-    "hs_net_create": (_I, [ctypes.POINTER(_VP), _VP]),
+    "hs_net_create": (_I, [ctypes.POINTER(_VP), ctypes.POINTER(HsNetDesc), _VP]),
     "hs_net_destroy": (None, [_VP]),
+    "hs_net_encode_workspace_bytes": (_SZ, [_VP, _I]),
+    "hs_net_encode": (_I, [_VP, _VP, _I, _VP, _VP, _SZ, _VP]),
     "hs_net_set_encodings": (_I, [_VP, _I, _VP]),
-    "hs_net_forward": (_I, [_VP, _VP, _VP, _VP, _I, _VP, _SZ, _VP]),
     "hs_net_workspace_bytes": (_SZ, [_VP, _I]),
+    "hs_net_forward": (_I, [_VP, _VP, _VP, _VP, _I, _VP, _SZ, _VP]),
     "hs_green_spectrum": (_I, [_VP, _I, _I, _I, _VP, _VP]),
     "hs_implicit_apply": (_I, [_VP, _VP, _VP, _I, _I, _I, _I, _VP]),
-    "hs_conv2d": (_I, [_VP, _VP, _VP, _VP, _I, _I, _I, _I, _I, _I, _I, _VP]),
+    "hs_conv2d": (_I, [_VP, ctypes.POINTER(HsConv), _VP, _VP, _VP, _I, _I, _I, _VP]),
 }
 
 _lock = threading.Lock()

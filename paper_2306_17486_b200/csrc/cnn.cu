@@ -1,11 +1,809 @@
+// Encoder-solver CNN (ARCH.md) and the implicit Green's-function layer.
+//
+// Activations are float32 NHWC [B][H][W][C]: one pixel's channels are
+// contiguous, so a 3x3 tap of the implicit GEMM (M = pixels, N = cout,
+// K = 9 cin) is a contiguous cin-vector.  Batch norm is folded into the
+// convolution weights on the host; every convolution fuses its bias,
+// softplus, encoder/skip addend and residual add into the epilogue.
+//
+// Reference semantics: conv2d / conv_transpose2d / batchnorm2d / softplus
+// (autodiff.py:243-252, 472-607), pack/unpack_complex (:343-372),
+// green_function / implicit_apply (green.py:55-107).
+#include <cufft.h>
+
+#include <cmath>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
 #include "cnn.h"
+#include "common.cuh"
+#include "conv_tc.h"
 
 struct hs_net {
-  int levels;
+  hs_net_desc_t d;
+  int hc, wc, cc;              // coarsest grid and complex channel count
+  cufftComplex* spec = nullptr;  // (cc, 2hc, 2wc) complex64 Green spectrum
+  const float* enc[8] = {nullptr};
+  int n_models = 0;
+  mutable std::mutex plan_mu;
+  mutable std::map<int, cufftHandle> plans;  // batch -> plan
+  ~hs_net() {
+    for (auto& kv : plans) cufftDestroy(kv.second);
+    if (spec) cudaFree(spec);
+  }
 };
 
 namespace hs {
-size_t cnn_workspace_bytes(const hs_net_t*, int) { return 0; }
-void cnn_preconditioner_estimate(const hs_net_t*, VecIn, const float2* const*, float2*, const int*, int, void*,
-                                 cudaStream_t) {}
+namespace {
+
+constexpr int kConvThreads = 256;
+constexpr int kCK = 8;  // input channels staged per smem pass
+
+HS_DEV float softplusf(float x) { return fmaxf(x, 0.f) + log1pf(expf(-fabsf(x))); }
+
+struct ConvArgs {
+  const float* x;
+  int H, W, cin;  // input
+  float* y;
+  int Ho, Wo, cout;  // output
+  const float* w;    // [cout][9][cin]
+  const float* bias;
+  int softplus;
+  const float* addend;  // NHWC like y, per model (model_of) or per batch item
+  long long addend_bstride;
+  const int* model_of;
+  const float* residual;  // NHWC like y
+  const void* const* active;
+};
+
+template <int COUT>
+struct Tile {
+  static constexpr int CG = COUT < 16 ? COUT : 16;           // couts per thread
+  static constexpr int PX = 4;                               // pixels per thread (along W)
+  static constexpr int TPX = kConvThreads * PX * CG / COUT;  // pixels per block
+  static constexpr int TW = 32;
+  static constexpr int TH = TPX / TW;
+};
+
+// Direct 3x3 convolution, stride 1 or 2, SIMT fp32 (exact fp32 products).
+template <int COUT, int STRIDE>
+__global__ void __launch_bounds__(kConvThreads) k_conv(ConvArgs a) {
+  using T = Tile<COUT>;
+  constexpr int IH = (T::TH - 1) * STRIDE + 3, IW = (T::TW - 1) * STRIDE + 3;
+  extern __shared__ float smem[];
+  float* s_in = smem;                  // [kCK][IH][IW]
+  float* s_w = smem + kCK * IH * IW;   // [kCK][9][COUT]
+  const int b = blockIdx.z;
+  if (a.active && a.active[b] == nullptr) return;
+  const int tiles_x = (a.Wo + T::TW - 1) / T::TW;
+  const int oy0 = (blockIdx.x / tiles_x) * T::TH, ox0 = (blockIdx.x % tiles_x) * T::TW;
+  const int iy0 = oy0 * STRIDE - 1, ix0 = ox0 * STRIDE - 1;
+  const int t = threadIdx.x;
+  constexpr int PG = T::TPX / T::PX;  // pixel groups
+  const int cg = t / PG, pg = t % PG;
+  const int ly = pg / (T::TW / T::PX), lx = (pg % (T::TW / T::PX)) * T::PX;
+  float acc[T::PX][T::CG];
+#pragma unroll
+  for (int p = 0; p < T::PX; ++p)
+#pragma unroll
+    for (int q = 0; q < T::CG; ++q) acc[p][q] = 0.f;
+  const float* xb = a.x + (long long)b * a.H * a.W * a.cin;
+  for (int c0 = 0; c0 < a.cin; c0 += kCK) {
+    const int ck = min(kCK, a.cin - c0);
+    __syncthreads();
+    for (int e = t; e < IH * IW * kCK; e += kConvThreads) {
+      const int c = e % kCK, pix = e / kCK;
+      const int r = pix / IW, col = pix % IW;
+      const int gy = iy0 + r, gx = ix0 + col;
+      float v = 0.f;
+      if (c < ck && gy >= 0 && gy < a.H && gx >= 0 && gx < a.W) v = xb[((long long)gy * a.W + gx) * a.cin + c0 + c];
+      s_in[(c * IH + r) * IW + col] = v;
+    }
+    for (int e = t; e < kCK * 9 * COUT; e += kConvThreads) {
+      const int co = e % COUT, tap = (e / COUT) % 9, c = e / (9 * COUT);
+      s_w[e] = c < ck ? a.w[((long long)co * 9 + tap) * a.cin + c0 + c] : 0.f;
+    }
+    __syncthreads();
+    for (int c = 0; c < ck; ++c) {
+#pragma unroll
+      for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+        for (int kx = 0; kx < 3; ++kx) {
+          float xv[T::PX];
+#pragma unroll
+          for (int p = 0; p < T::PX; ++p) xv[p] = s_in[(c * IH + ly * STRIDE + ky) * IW + (lx + p) * STRIDE + kx];
+          const float* wr = s_w + (c * 9 + ky * 3 + kx) * COUT + cg * T::CG;
+#pragma unroll
+          for (int q = 0; q < T::CG; ++q) {
+            const float wv = wr[q];
+#pragma unroll
+            for (int p = 0; p < T::PX; ++p) acc[p][q] = fmaf(xv[p], wv, acc[p][q]);
+          }
+        }
+    }
+  }
+  const int oy = oy0 + ly;
+  if (oy >= a.Ho) return;
+  const long long obase = (long long)b * a.Ho * a.Wo * COUT;
+  const float* add = a.addend ? a.addend + (a.model_of ? a.model_of[b] : b) * a.addend_bstride : nullptr;
+#pragma unroll
+  for (int p = 0; p < T::PX; ++p) {
+    const int ox = ox0 + lx + p;
+    if (ox >= a.Wo) continue;
+    const long long o = obase + ((long long)oy * a.Wo + ox) * COUT + cg * T::CG;
+    const long long oa = ((long long)oy * a.Wo + ox) * COUT + cg * T::CG;
+#pragma unroll
+    for (int q = 0; q < T::CG; ++q) {
+      float v = acc[p][q] + a.bias[cg * T::CG + q];
+      if (a.softplus) v = softplusf(v);
+      if (add) v += add[oa + q];
+      if (a.residual) v += a.residual[o + q];
+      a.y[o + q] = v;
+    }
+  }
+}
+
+// Transposed 3x3 convolution, stride 2, pad 1, out = 2 x in (autodiff.py:510-541).
+// Output o along an axis receives x[q]*w[1] if o = 2q, and x[q+1]*w[0] +
+// x[q]*w[2] if o = 2q+1.  Each thread handles 4 outputs of one parity class.
+template <int COUT>
+__global__ void __launch_bounds__(kConvThreads) k_tconv(ConvArgs a) {
+  using T = Tile<COUT>;
+  constexpr int QH = T::TH / 2, QW = T::TW / 2;  // per-class sub-tile
+  constexpr int IH = QH + 1, IW = QW + 1;
+  extern __shared__ float smem[];
+  float* s_in = smem;
+  float* s_w = smem + kCK * IH * IW;
+  const int b = blockIdx.z;
+  if (a.active && a.active[b] == nullptr) return;
+  const int tiles_x = (a.Wo + T::TW - 1) / T::TW;
+  const int oy0 = (blockIdx.x / tiles_x) * T::TH, ox0 = (blockIdx.x % tiles_x) * T::TW;
+  const int qy0 = oy0 / 2, qx0 = ox0 / 2;
+  const int t = threadIdx.x;
+  constexpr int PG = T::TPX / T::PX;  // = 4 classes x (QH*QW/PX)
+  constexpr int PGC = QH * QW / T::PX;
+  const int cg = t / PG, pg = t % PG;
+  const int cls = pg / PGC, pgc = pg % PGC;
+  const int py = cls >> 1, px = cls & 1;
+  const int qy = pgc / (QW / T::PX), qx = (pgc % (QW / T::PX)) * T::PX;
+  float acc[T::PX][T::CG];
+#pragma unroll
+  for (int p = 0; p < T::PX; ++p)
+#pragma unroll
+    for (int q = 0; q < T::CG; ++q) acc[p][q] = 0.f;
+  const float* xb = a.x + (long long)b * a.H * a.W * a.cin;
+  // taps per parity: even -> (k=1, d=0); odd -> (k=0, d=1), (k=2, d=0)
+  const int nty = py ? 2 : 1, ntx = px ? 2 : 1;
+  for (int c0 = 0; c0 < a.cin; c0 += kCK) {
+    const int ck = min(kCK, a.cin - c0);
+    __syncthreads();
+    for (int e = t; e < IH * IW * kCK; e += kConvThreads) {
+      const int c = e % kCK, pix = e / kCK;
+      const int r = pix / IW, col = pix % IW;
+      const int gy = qy0 + r, gx = qx0 + col;
+      float v = 0.f;
+      if (c < ck && gy < a.H && gx < a.W) v = xb[((long long)gy * a.W + gx) * a.cin + c0 + c];
+      s_in[(c * IH + r) * IW + col] = v;
+    }
+    for (int e = t; e < kCK * 9 * COUT; e += kConvThreads) {
+      const int co = e % COUT, tap = (e / COUT) % 9, c = e / (9 * COUT);
+      s_w[e] = c < ck ? a.w[((long long)co * 9 + tap) * a.cin + c0 + c] : 0.f;
+    }
+    __syncthreads();
+    for (int c = 0; c < ck; ++c) {
+      for (int ty = 0; ty < nty; ++ty) {
+        const int ky = py ? (ty ? 2 : 0) : 1, dy = (py && !ty) ? 1 : 0;
+        for (int tx = 0; tx < ntx; ++tx) {
+          const int kx = px ? (tx ? 2 : 0) : 1, dx = (px && !tx) ? 1 : 0;
+          float xv[T::PX];
+#pragma unroll
+          for (int p = 0; p < T::PX; ++p) xv[p] = s_in[(c * IH + qy + dy) * IW + qx + p + dx];
+          const float* wr = s_w + (c * 9 + ky * 3 + kx) * COUT + cg * T::CG;
+#pragma unroll
+          for (int q = 0; q < T::CG; ++q) {
+            const float wv = wr[q];
+#pragma unroll
+            for (int p = 0; p < T::PX; ++p) acc[p][q] = fmaf(xv[p], wv, acc[p][q]);
+          }
+        }
+      }
+    }
+  }
+  const int oy = oy0 + 2 * qy + py;
+  if (oy >= a.Ho) return;
+  const long long obase = (long long)b * a.Ho * a.Wo * COUT;
+  const float* add = a.addend ? a.addend + (a.model_of ? a.model_of[b] : b) * a.addend_bstride : nullptr;
+#pragma unroll
+  for (int p = 0; p < T::PX; ++p) {
+    const int ox = ox0 + 2 * (qx + p) + px;
+    if (ox >= a.Wo) continue;
+    const long long oa = ((long long)oy * a.Wo + ox) * COUT + cg * T::CG;
+    const long long o = obase + oa;
+#pragma unroll
+    for (int q = 0; q < T::CG; ++q) {
+      float v = acc[p][q] + a.bias[cg * T::CG + q];
+      if (a.softplus) v = softplusf(v);
+      if (add) v += add[oa + q];
+      if (a.residual) v += a.residual[o + q];
+      a.y[o + q] = v;
+    }
+  }
+}
+
+template <int COUT, int STRIDE>
+size_t conv_smem() {
+  using T = Tile<COUT>;
+  constexpr int IH = (T::TH - 1) * STRIDE + 3, IW = (T::TW - 1) * STRIDE + 3;
+  return sizeof(float) * (kCK * IH * IW + kCK * 9 * COUT);
+}
+template <int COUT>
+size_t tconv_smem() {
+  using T = Tile<COUT>;
+  return sizeof(float) * (kCK * (T::TH / 2 + 1) * (T::TW / 2 + 1) + kCK * 9 * COUT);
+}
+
+template <int COUT, int STRIDE>
+void launch_conv_t(const ConvArgs& a, int B, cudaStream_t st) {
+  using T = Tile<COUT>;
+  static bool attr = false;
+  const size_t sm = conv_smem<COUT, STRIDE>();
+  if (!attr) {
+    cudaFuncSetAttribute(k_conv<COUT, STRIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  dim3 g(cdiv_u(a.Ho, T::TH) * cdiv_u(a.Wo, T::TW), 1, B);
+  k_conv<COUT, STRIDE><<<g, kConvThreads, sm, st>>>(a);
+}
+template <int COUT>
+void launch_tconv_t(const ConvArgs& a, int B, cudaStream_t st) {
+  using T = Tile<COUT>;
+  static bool attr = false;
+  const size_t sm = tconv_smem<COUT>();
+  if (!attr) {
+    cudaFuncSetAttribute(k_tconv<COUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  dim3 g(cdiv_u(a.Ho, T::TH) * cdiv_u(a.Wo, T::TW), 1, B);
+  k_tconv<COUT><<<g, kConvThreads, sm, st>>>(a);
+}
+
+int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* y, const float* addend,
+                long long addend_bstride, const int* model_of, const float* residual, const void* const* active,
+                cudaStream_t st) {
+  ConvArgs a{};
+  a.x = x;
+  a.H = H;
+  a.W = W;
+  a.cin = c.cin;
+  a.y = y;
+  a.cout = c.cout;
+  if (c.transposed) {
+    a.Ho = 2 * H;
+    a.Wo = 2 * W;
+  } else {
+    a.Ho = (H - 1) / c.stride + 1;
+    a.Wo = (W - 1) / c.stride + 1;
+  }
+  a.w = c.w;
+  a.bias = c.b;
+  a.softplus = c.softplus;
+  a.addend = addend;
+  a.addend_bstride = addend_bstride;
+  a.model_of = model_of;
+  a.residual = residual;
+  a.active = active;
+  if (!c.transposed && conv_tc_supported(c.cin, c.cout, c.stride)) {
+    conv_tc_launch(a.x, a.H, a.W, a.cin, a.y, a.Ho, a.Wo, a.cout, c.stride, a.w, a.bias, a.softplus, a.addend,
+                   a.addend_bstride, a.model_of, a.residual, a.active, B, st);
+    return HS_OK;
+  }
+#define HS_CONV_CASE(CO)                          \
+  case CO:                                        \
+    if (c.transposed)                             \
+      launch_tconv_t<CO>(a, B, st);               \
+    else if (c.stride == 2)                       \
+      launch_conv_t<CO, 2>(a, B, st);             \
+    else                                          \
+      launch_conv_t<CO, 1>(a, B, st);             \
+    return HS_OK;
+  switch (c.cout) {
+    HS_CONV_CASE(2)
+    HS_CONV_CASE(8)
+    HS_CONV_CASE(16)
+    HS_CONV_CASE(32)
+    HS_CONV_CASE(64)
+    HS_CONV_CASE(128)
+    default:
+      return HS_ECONFIG;
+  }
+#undef HS_CONV_CASE
+}
+
+// ------------------------------------------------------- input / output glue
+
+// r (complex64, nx x ny, scaled) cropped to (ix, iy) -> NHWC 2 channels (Re, Im)
+__global__ void k_gather_r(VecIn vin, const void* const* active, float* out, int nx, int ny, int ix, int iy) {
+  const int b = blockIdx.y;
+  if (active && active[b] == nullptr) return;
+  const float2* r = vin.tab ? vin.tab[b] : vin.base + (long long)b * vin.bstride;
+  const float s = vin.scale ? vin.scale[b] : 1.f;
+  const long long n = (long long)ix * iy;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(p / iy), j = (int)(p - (long long)i * iy);
+    float2 v = r[(long long)i * ny + j];
+    reinterpret_cast<float2*>(out)[(long long)b * n + p] = make_float2(v.x * s, v.y * s);
+  }
+}
+
+// NHWC 2-channel head output -> u0 = scale (o0 + i o1), zero outside (ix, iy)
+__global__ void k_scatter_u0(const float* head, const void* const* active, float2* u0, int nx, int ny, int ix, int iy,
+                             float scale) {
+  const int b = blockIdx.y;
+  if (active && active[b] == nullptr) return;
+  const long long n = (long long)nx * ny;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(p / ny), j = (int)(p - (long long)i * ny);
+    float2 v = make_float2(0.f, 0.f);
+    if (i < ix && j < iy) {
+      float2 o = reinterpret_cast<const float2*>(head)[(long long)b * ix * iy + (long long)i * iy + j];
+      v = make_float2(scale * o.x, scale * o.y);
+    }
+    u0[b * n + p] = v;
+  }
+}
+
+// NHWC real (C = 2 cc) at (h, w) -> complex NCHW (cc, 2h, 2w) zero-padded at the high end
+__global__ void k_pack_pad(const float* x, const void* const* active, cufftComplex* z, int h, int w, int cc) {
+  const int b = blockIdx.y;
+  if (active && active[b] == nullptr) return;
+  const int H2 = 2 * h, W2 = 2 * w;
+  const long long n = (long long)cc * H2 * W2;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(e / ((long long)H2 * W2));
+    const int rem = (int)(e - (long long)k * H2 * W2);
+    const int y = rem / W2, xx = rem % W2;
+    cufftComplex v = make_float2(0.f, 0.f);
+    if (y < h && xx < w) {
+      const float* px = x + (((long long)b * h + y) * w + xx) * (2 * cc);
+      v = make_float2(px[2 * k], px[2 * k + 1]);
+    }
+    z[(long long)b * n + e] = v;
+  }
+}
+
+__global__ void k_spec_mul(cufftComplex* z, const void* const* active, const cufftComplex* spec, long long per_b) {
+  const int b = blockIdx.y;
+  if (active && active[b] == nullptr) return;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < per_b; e += (long long)gridDim.x * blockDim.x)
+    z[(long long)b * per_b + e] = cmul(z[(long long)b * per_b + e], spec[e]);
+}
+
+// (B, C, h, w) complex -> (B, C, 2h, 2w) zero-padded at the high end (pad2d_to, autodiff.py:283-294)
+__global__ void k_pad_nchw(const cufftComplex* x, cufftComplex* z, int C, int h, int w) {
+  const int b = blockIdx.y;
+  const long long per_b = (long long)C * 4 * h * w;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < per_b; e += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(e / (4LL * h * w));
+    const int rem = (int)(e - (long long)k * 4 * h * w);
+    const int r = rem / (2 * w), c = rem % (2 * w);
+    z[b * per_b + e] = (r < h && c < w) ? x[(((long long)b * C + k) * h + r) * w + c] : make_float2(0.f, 0.f);
+  }
+}
+
+// (B, C, 2h, 2w) -> crop [:h, :w] with the inverse FFT's 1/N (ifft2 + crop2d)
+__global__ void k_crop_nchw(const cufftComplex* z, cufftComplex* y, int C, int h, int w) {
+  const int b = blockIdx.y;
+  const long long per_b = (long long)C * h * w;
+  const float inv = 1.f / (4.f * h * w);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < per_b; e += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(e / ((long long)h * w));
+    const int rem = (int)(e - (long long)k * h * w);
+    const int r = rem / w, c = rem % w;
+    cufftComplex v = z[(((long long)b * C + k) * 2 * h + r) * 2 * w + c];
+    y[b * per_b + e] = make_float2(v.x * inv, v.y * inv);
+  }
+}
+
+// complex NCHW (cc, 2h, 2w) -> crop [:h, :w], / (4hw), unpack to NHWC real (2cc)
+__global__ void k_crop_unpack(const cufftComplex* z, const void* const* active, float* x, int h, int w, int cc) {
+  const int b = blockIdx.y;
+  if (active && active[b] == nullptr) return;
+  const int H2 = 2 * h, W2 = 2 * w;
+  const float inv = 1.f / (float)(H2 * W2);
+  const long long n = (long long)h * w * cc;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(e % cc);
+    const long long pix = e / cc;
+    const int y = (int)(pix / w), xx = (int)(pix % w);
+    cufftComplex v = z[(long long)b * cc * H2 * W2 + ((long long)k * H2 + y) * W2 + xx];
+    float* px = x + (((long long)b * h + y) * w + xx) * (2 * cc);
+    px[2 * k] = v.x * inv;
+    px[2 * k + 1] = v.y * inv;
+  }
+}
+
+// ------------------------------------------------------- Green spectrum (setup)
+
+__global__ void k_green_embed(const float2* kern, cufftDoubleComplex* kp, int C, int bh, int bw) {
+  const long long n = (long long)C * bh * bw;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e / ((long long)bh * bw));
+    const int rem = (int)(e - (long long)c * bh * bw);
+    const int r = rem / bw, col = rem % bw;
+    // place_kernel_corners (autodiff.py:323-337): rows (bh-1, 0, 1), cols (bw-1, 0, 1)
+    int a = r == bh - 1 ? 0 : (r == 0 ? 1 : (r == 1 ? 2 : -1));
+    int q = col == bw - 1 ? 0 : (col == 0 ? 1 : (col == 1 ? 2 : -1));
+    cufftDoubleComplex v = make_double2(0.0, 0.0);
+    if (a >= 0 && q >= 0) {
+      float2 k = kern[c * 9 + a * 3 + q];
+      v = make_double2(k.x, k.y);
+    }
+    kp[e] = v;
+  }
+}
+
+// resp_hat = conj(S)/(S conj(S) + eps) * delta_hat with the reference's dtype flow
+__global__ void k_green_divide(cufftDoubleComplex* s, long long n, int bh, int bw, double eps) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int rem = (int)(e % ((long long)bh * bw));
+    const int u = rem / bw, v = rem % bw;
+    // S rounded to complex64 (ad.fft2 casts to the input's complex dtype)
+    const float sr = (float)s[e].x, si = (float)s[e].y;
+    // S * conj(S) in complex64 arithmetic, then + eps promotes to complex128
+    const float pr = sr * sr - si * (-si);
+    const float pi = sr * (-si) + si * sr;
+    const double dr = (double)pr + eps, di = (double)pi;
+    // conj(S) / denom in complex128
+    const double cr = sr, ci = -(double)si;
+    const double den = dr * dr + di * di;
+    const double qr = (cr * dr + ci * di) / den, qi = (ci * dr - cr * di) / den;
+    // delta at (bh/2, bw/2): spectrum (-1)^(u+v) for even sizes, rounded to complex64
+    const double ph = -2.0 * M_PI * ((double)u * (bh / 2) / bh + (double)v * (bw / 2) / bw);
+    const double er = (double)(float)cos(ph), ei = (double)(float)sin(ph);
+    s[e] = make_double2(qr * er - qi * ei, qr * ei + qi * er);
+  }
+}
+
+// crop the centred (gh, gw) window, ifftshift, scale the inverse FFT by 1/N
+__global__ void k_green_crop_shift(const cufftDoubleComplex* resp, cufftDoubleComplex* out, int C, int bh, int bw,
+                                   int gh, int gw) {
+  const long long n = (long long)C * gh * gw;
+  const double inv = 1.0 / ((double)bh * bw);
+  const int oy = bh / 2 - gh / 2, ox = bw / 2 - gw / 2;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e / ((long long)gh * gw));
+    const int rem = (int)(e - (long long)c * gh * gw);
+    const int r = rem / gw, col = rem % gw;
+    // ifftshift: out[r] = in[(r + g/2) mod g] (numpy, any parity: shift by -(g//2))
+    const int sr = (r + gh / 2) % gh, sc = (col + gw / 2) % gw;
+    cufftDoubleComplex v = resp[((long long)c * bh + oy + sr) * bw + ox + sc];
+    out[e] = make_double2(v.x * inv, v.y * inv);
+  }
+}
+
+__global__ void k_c128_to_c64(const cufftDoubleComplex* in, cufftComplex* out, long long n) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    out[e] = make_float2((float)in[e].x, (float)in[e].y);
+}
+
+unsigned grid1(long long n) {
+  long long g = (n + 255) / 256;
+  return (unsigned)(g > 4096 ? 4096 : (g < 1 ? 1 : g));
+}
+
+size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
+
+// per-level activation buffers of the forward pass
+struct FwdLayout {
+  size_t in, head, lvl_x[8], lvl_t[8], lvl_s[8], fftz, total;
+};
+
+FwdLayout fwd_layout(const hs_net_desc_t& d, int B) {
+  FwdLayout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align_up(bytes);
+    return o;
+  };
+  L.in = take((size_t)B * d.ix * d.iy * 2 * sizeof(float));
+  L.head = take((size_t)B * d.ix * d.iy * 2 * sizeof(float));
+  for (int l = 0; l < d.levels; ++l) {
+    size_t n = (size_t)B * (d.ix >> l) * (d.iy >> l) * d.channels[l] * sizeof(float);
+    L.lvl_x[l] = take(n);
+    L.lvl_t[l] = take(n);
+    L.lvl_s[l] = take(n);
+  }
+  const int L1 = d.levels - 1;
+  const int hc = d.ix >> L1, wc = d.iy >> L1, cc = d.channels[L1] / 2;
+  L.fftz = take((size_t)B * cc * 4 * hc * wc * sizeof(cufftComplex));
+  L.total = off;
+  return L;
+}
+
+}  // namespace
+
+size_t cnn_workspace_bytes(const hs_net_t* net, int B) { return fwd_layout(net->d, B).total; }
+
+static int green_spectrum_c128(const float2* kern, int C, int h, int w, cufftDoubleComplex* out, cudaStream_t st) {
+  const int gh = 2 * h, gw = 2 * w, bh = 3 * gh, bw = 3 * gw;
+  cufftDoubleComplex* big = nullptr;
+  const long long nb = (long long)C * bh * bw;
+  if (cudaMalloc(&big, nb * sizeof(cufftDoubleComplex)) != cudaSuccess) return HS_ECUDA;
+  cufftHandle p1, p2;
+  int n1[2] = {bh, bw}, n2[2] = {gh, gw};
+  int rc = HS_OK;
+  if (cufftPlanMany(&p1, 2, n1, nullptr, 1, bh * bw, nullptr, 1, bh * bw, CUFFT_Z2Z, C) != CUFFT_SUCCESS) rc = HS_ECUDA;
+  if (rc == HS_OK &&
+      cufftPlanMany(&p2, 2, n2, nullptr, 1, gh * gw, nullptr, 1, gh * gw, CUFFT_Z2Z, C) != CUFFT_SUCCESS)
+    rc = HS_ECUDA;
+  if (rc == HS_OK) {
+    cufftSetStream(p1, st);
+    cufftSetStream(p2, st);
+    k_green_embed<<<grid1(nb), 256, 0, st>>>(kern, big, C, bh, bw);
+    cufftExecZ2Z(p1, big, big, CUFFT_FORWARD);
+    k_green_divide<<<grid1(nb), 256, 0, st>>>(big, nb, bh, bw, 1e-5);
+    cufftExecZ2Z(p1, big, big, CUFFT_INVERSE);
+    k_green_crop_shift<<<grid1((long long)C * gh * gw), 256, 0, st>>>(big, out, C, bh, bw, gh, gw);
+    cufftExecZ2Z(p2, out, out, CUFFT_FORWARD);
+    cudaStreamSynchronize(st);
+    cufftDestroy(p1);
+    cufftDestroy(p2);
+  }
+  cudaFree(big);
+  return rc;
+}
+
+static int implicit_apply_dev(const hs_net_t* net, const float* x_nhwc, float* y_nhwc, cufftComplex* z,
+                              const void* const* active, int B, cudaStream_t st) {
+  const int hc = net->hc, wc = net->wc, cc = net->cc;
+  cufftHandle plan;
+  {
+    std::lock_guard<std::mutex> g(net->plan_mu);
+    auto it = net->plans.find(B);
+    if (it == net->plans.end()) {
+      int n[2] = {2 * hc, 2 * wc};
+      if (cufftPlanMany(&plan, 2, n, nullptr, 1, 4 * hc * wc, nullptr, 1, 4 * hc * wc, CUFFT_C2C, B * cc) !=
+          CUFFT_SUCCESS)
+        return HS_ECUDA;
+      net->plans[B] = plan;
+    } else {
+      plan = it->second;
+    }
+  }
+  cufftSetStream(plan, st);
+  const long long per_b = (long long)cc * 4 * hc * wc;
+  dim3 g(grid1(per_b), B);
+  k_pack_pad<<<g, 256, 0, st>>>(x_nhwc, active, z, hc, wc, cc);
+  if (cufftExecC2C(plan, z, z, CUFFT_FORWARD) != CUFFT_SUCCESS) return HS_ECUDA;
+  k_spec_mul<<<g, 256, 0, st>>>(z, active, net->spec, per_b);
+  if (cufftExecC2C(plan, z, z, CUFFT_INVERSE) != CUFFT_SUCCESS) return HS_ECUDA;
+  k_crop_unpack<<<dim3(grid1((long long)hc * wc * cc), B), 256, 0, st>>>(z, active, y_nhwc, hc, wc, cc);
+  return HS_OK;
+}
+
+// The solver U-Net (ARCH.md) on NHWC buffers; input 2-channel `in`, output
+// 2-channel `head`.  RHS with active[b] == null are skipped.
+static int solver_forward(const hs_net_t* net, const float* in, float* head, char* ws, const FwdLayout& L,
+                          const int* model_of, const void* const* active, int B, cudaStream_t st) {
+  const hs_net_desc_t& d = net->d;
+  float* X[8];
+  float* Tm[8];
+  float* S[8];
+  for (int l = 0; l < d.levels; ++l) {
+    X[l] = reinterpret_cast<float*>(ws + L.lvl_x[l]);
+    Tm[l] = reinterpret_cast<float*>(ws + L.lvl_t[l]);
+    S[l] = reinterpret_cast<float*>(ws + L.lvl_s[l]);
+  }
+  auto lvl_bstride = [&](int l) { return (long long)(d.ix >> l) * (d.iy >> l) * d.channels[l]; };
+  int rc;
+  // level 0: stem (+ encoding 0), residual block -> skip 0
+  if ((rc = launch_conv(d.sol_stem, in, B, d.ix, d.iy, X[0], net->enc[0], lvl_bstride(0), model_of, nullptr, active,
+                        st)))
+    return rc;
+  if ((rc = launch_conv(d.sol_res_a[0], X[0], B, d.ix, d.iy, Tm[0], nullptr, 0, nullptr, nullptr, active, st)))
+    return rc;
+  if ((rc = launch_conv(d.sol_res_b[0], Tm[0], B, d.ix, d.iy, S[0], nullptr, 0, nullptr, X[0], active, st))) return rc;
+  for (int l = 1; l < d.levels; ++l) {
+    const int H = d.ix >> (l - 1), W = d.iy >> (l - 1), h = d.ix >> l, w = d.iy >> l;
+    if ((rc = launch_conv(d.sol_down[l], S[l - 1], B, H, W, X[l], net->enc[l], lvl_bstride(l), model_of, nullptr,
+                          active, st)))
+      return rc;
+    if ((rc = launch_conv(d.sol_res_a[l], X[l], B, h, w, Tm[l], nullptr, 0, nullptr, nullptr, active, st))) return rc;
+    if ((rc = launch_conv(d.sol_res_b[l], Tm[l], B, h, w, S[l], nullptr, 0, nullptr, X[l], active, st))) return rc;
+  }
+  // coarsest: implicit layer S[L-1] -> X[L-1]
+  const int L1 = d.levels - 1;
+  if ((rc = implicit_apply_dev(net, S[L1], X[L1], reinterpret_cast<cufftComplex*>(ws + L.fftz), active, B, st)))
+    return rc;
+  // up path: X[l] -> (tconv + skip) X[l-1] -> residual block
+  for (int l = L1; l >= 1; --l) {
+    const int h = d.ix >> l, w = d.iy >> l, H = d.ix >> (l - 1), W = d.iy >> (l - 1);
+    (void)H;
+    (void)W;
+    float* src = X[l];
+    if ((rc = launch_conv(d.sol_up[l], src, B, h, w, Tm[l - 1], S[l - 1], lvl_bstride(l - 1), nullptr, nullptr,
+                          active, st)))
+      return rc;
+    // Tm[l-1] holds x = softplus(BN(tconv)) + skip; residual block into X[l-1]
+    if ((rc = launch_conv(d.sol_ures_a[l - 1], Tm[l - 1], B, d.ix >> (l - 1), d.iy >> (l - 1), S[l - 1], nullptr, 0,
+                          nullptr, nullptr, active, st)))
+      return rc;
+    if ((rc = launch_conv(d.sol_ures_b[l - 1], S[l - 1], B, d.ix >> (l - 1), d.iy >> (l - 1), X[l - 1], nullptr, 0,
+                          nullptr, Tm[l - 1], active, st)))
+      return rc;
+  }
+  return launch_conv(d.sol_head, X[0], B, d.ix, d.iy, head, nullptr, 0, nullptr, nullptr, active, st);
+}
+
+void cnn_preconditioner_estimate(const hs_net_t* net, VecIn vin, const float2* const* active, float2* u0,
+                                 const int* model_of, int B, void* ws, cudaStream_t st) {
+  const hs_net_desc_t& d = net->d;
+  FwdLayout L = fwd_layout(d, B);
+  char* w = static_cast<char*>(ws);
+  float* in = reinterpret_cast<float*>(w + L.in);
+  float* head = reinterpret_cast<float*>(w + L.head);
+  const void* const* act = reinterpret_cast<const void* const*>(active);
+  k_gather_r<<<dim3(grid1((long long)d.ix * d.iy), B), 256, 0, st>>>(vin, act, in, d.nx, d.ny, d.ix, d.iy);
+  solver_forward(net, in, head, w, L, model_of, act, B, st);
+  k_scatter_u0<<<dim3(grid1((long long)d.nx * d.ny), B), 256, 0, st>>>(head, act, u0, d.nx, d.ny, d.ix, d.iy,
+                                                                       d.out_scale);
+}
+
 }  // namespace hs
+
+// ------------------------------------------------------------------ C ABI
+
+namespace {
+int cfail(int code, const char* m) { return hs::set_error(code, m); }
+int ccheck(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return hs::set_error(HS_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return HS_OK;
+}
+}  // namespace
+
+HS_API int hs_net_create(hs_net_t** out, const hs_net_desc_t* desc, void* stream) {
+  if (!out || !desc) return cfail(HS_ECONFIG, "null argument");
+  if (desc->levels < 2 || desc->levels > 8) return cfail(HS_ECONFIG, "levels must lie in [2, 8]");
+  const int L1 = desc->levels - 1;
+  if ((desc->ix >> L1) << L1 != desc->ix || (desc->iy >> L1) << L1 != desc->iy)
+    return cfail(HS_EDIMENSION, "network grid not divisible by 2^(levels-1)");
+  auto* n = new hs_net();
+  n->d = *desc;
+  n->hc = desc->ix >> L1;
+  n->wc = desc->iy >> L1;
+  n->cc = desc->channels[L1] / 2;
+  if (n->hc < 3 || n->wc < 3) {
+    delete n;
+    return cfail(HS_EDIMENSION, "coarse size too small for the implicit layer");
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long ns = (long long)n->cc * 4 * n->hc * n->wc;
+  cufftDoubleComplex* s128 = nullptr;
+  if (cudaMalloc(&s128, ns * sizeof(cufftDoubleComplex)) != cudaSuccess ||
+      cudaMalloc(&n->spec, ns * sizeof(cufftComplex)) != cudaSuccess) {
+    delete n;
+    return cfail(HS_ECUDA, "cudaMalloc spectrum");
+  }
+  int rc = hs::green_spectrum_c128(static_cast<const float2*>(desc->implicit_w), n->cc, n->hc, n->wc, s128, st);
+  if (rc == HS_OK) {
+    hs::k_c128_to_c64<<<hs::grid1(ns), 256, 0, st>>>(s128, n->spec, ns);
+    cudaStreamSynchronize(st);
+  }
+  cudaFree(s128);
+  if (rc != HS_OK || ccheck("hs_net_create") != HS_OK) {
+    delete n;
+    return cfail(HS_ECUDA, "green spectrum");
+  }
+  *out = n;
+  return HS_OK;
+}
+
+HS_API void hs_net_destroy(hs_net_t* net) { delete net; }
+
+static size_t enc_level_bytes(const hs_net_desc_t& d, int n_models) {
+  size_t m = 0;
+  for (int l = 0; l < d.levels; ++l) {
+    size_t b = (size_t)n_models * (d.ix >> l) * (d.iy >> l) * d.channels[l] * sizeof(float);
+    m = b > m ? b : m;
+  }
+  return hs::align_up(m);
+}
+
+HS_API size_t hs_net_encode_workspace_bytes(const hs_net_t* net, int n_models) {
+  return 2 * enc_level_bytes(net->d, n_models);
+}
+
+HS_API int hs_net_encode(hs_net_t* net, const float* media, int n_models, float* const* enc, void* ws,
+                         size_t ws_bytes, void* stream) {
+  const hs_net_desc_t& d = net->d;
+  if (ws_bytes < hs_net_encode_workspace_bytes(net, n_models)) return cfail(HS_ECONFIG, "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = static_cast<char*>(ws);
+  const size_t big = enc_level_bytes(d, n_models);
+  float* t0 = reinterpret_cast<float*>(w);
+  float* t1 = reinterpret_cast<float*>(w + big);
+  int rc;
+  // e0 = res0(cbs(stem(media))), e_l = res_l(cbs(down_l(e_{l-1})))
+  if ((rc = hs::launch_conv(d.enc_stem, media, n_models, d.ix, d.iy, t0, nullptr, 0, nullptr, nullptr, nullptr, st)))
+    return cfail(rc, "encoder stem");
+  for (int l = 0; l < d.levels; ++l) {
+    const int h = d.ix >> l, ww = d.iy >> l;
+    if (l > 0) {
+      if ((rc = hs::launch_conv(d.enc_down[l], enc[l - 1], n_models, d.ix >> (l - 1), d.iy >> (l - 1), t0, nullptr, 0,
+                                nullptr, nullptr, nullptr, st)))
+        return cfail(rc, "encoder down");
+    }
+    if ((rc = hs::launch_conv(d.enc_res_a[l], t0, n_models, h, ww, t1, nullptr, 0, nullptr, nullptr, nullptr, st)))
+      return cfail(rc, "encoder res a");
+    if ((rc = hs::launch_conv(d.enc_res_b[l], t1, n_models, h, ww, enc[l], nullptr, 0, nullptr, t0, nullptr, st)))
+      return cfail(rc, "encoder res b");
+    net->enc[l] = enc[l];
+  }
+  net->n_models = n_models;
+  return ccheck("hs_net_encode");
+}
+
+HS_API size_t hs_net_workspace_bytes(const hs_net_t* net, int B) { return hs::cnn_workspace_bytes(net, B); }
+
+HS_API int hs_net_forward(const hs_net_t* net, const void* r, void* u0, const int* model_of, int B, void* ws,
+                          size_t ws_bytes, void* stream) {
+  if (!net->enc[0]) return cfail(HS_ECONFIG, "encodings not computed (hs_net_encode)");
+  if (ws_bytes < hs::cnn_workspace_bytes(net, B)) return cfail(HS_ECONFIG, "workspace too small");
+  const hs_net_desc_t& d = net->d;
+  hs::VecIn vin{nullptr, static_cast<const float2*>(r), (long long)d.nx * d.ny, nullptr};
+  hs::cnn_preconditioner_estimate(net, vin, nullptr, static_cast<float2*>(u0), model_of, B, ws,
+                                  (cudaStream_t)stream);
+  return ccheck("hs_net_forward");
+}
+
+HS_API int hs_green_spectrum(const void* kernel, int C, int h, int w, void* spectrum, void* stream) {
+  if (h < 3 || w < 3) return cfail(HS_EDIMENSION, "coarse size too small");
+  int rc = hs::green_spectrum_c128(static_cast<const float2*>(kernel), C, h, w,
+                                   static_cast<cufftDoubleComplex*>(spectrum), (cudaStream_t)stream);
+  return rc == HS_OK ? ccheck("hs_green_spectrum") : cfail(rc, "cufft");
+}
+
+HS_API int hs_implicit_apply(const void* x, const void* spectrum, void* y, int B, int C, int h, int w, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  cufftHandle plan;
+  int n[2] = {2 * h, 2 * w};
+  if (cufftPlanMany(&plan, 2, n, nullptr, 1, 4 * h * w, nullptr, 1, 4 * h * w, CUFFT_C2C, B * C) != CUFFT_SUCCESS)
+    return cfail(HS_ECUDA, "cufft plan");
+  cufftSetStream(plan, st);
+  cufftComplex* z = nullptr;
+  const long long per_b = (long long)C * 4 * h * w;
+  if (cudaMalloc(&z, (size_t)B * per_b * sizeof(cufftComplex)) != cudaSuccess) {
+    cufftDestroy(plan);
+    return cfail(HS_ECUDA, "cudaMalloc");
+  }
+  dim3 g(hs::grid1(per_b), B);
+  hs::k_pad_nchw<<<g, 256, 0, st>>>(static_cast<const cufftComplex*>(x), z, C, h, w);
+  cufftExecC2C(plan, z, z, CUFFT_FORWARD);
+  hs::k_spec_mul<<<g, 256, 0, st>>>(z, nullptr, static_cast<const cufftComplex*>(spectrum), per_b);
+  cufftExecC2C(plan, z, z, CUFFT_INVERSE);
+  hs::k_crop_nchw<<<g, 256, 0, st>>>(z, static_cast<cufftComplex*>(y), C, h, w);
+  cudaStreamSynchronize(st);
+  cudaFree(z);
+  cufftDestroy(plan);
+  return ccheck("hs_implicit_apply");
+}
+
+HS_API int hs_conv2d(const float* x, const hs_conv_t* conv, const float* addend, const float* residual, float* y,
+                     int B, int H, int W, void* stream) {
+  const int Ho = conv->transposed ? 2 * H : (H - 1) / conv->stride + 1;
+  const int Wo = conv->transposed ? 2 * W : (W - 1) / conv->stride + 1;
+  int rc = hs::launch_conv(*conv, x, B, H, W, y, addend, (long long)Ho * Wo * conv->cout, nullptr, residual, nullptr,
+                           (cudaStream_t)stream);
+  if (rc) return cfail(rc, "unsupported channel count");
+  return ccheck("hs_conv2d");
+}
+
+HS_API int hs_net_set_encodings(hs_net_t* net, int levels, const float* const* enc) {
+  if (levels != net->d.levels) return cfail(HS_EDIMENSION, "encodings for every level are needed");
+  for (int l = 0; l < levels; ++l) net->enc[l] = enc[l];
+  return HS_OK;
+}

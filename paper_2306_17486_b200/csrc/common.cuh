@@ -98,4 +98,9 @@ HS_DEV void block_sum_n(double* v, int n, double* scratch) {
 #include "../../include/helmsolve_b200.h"
 
 
+#include <string>
+namespace hs {
+int set_error(int code, const std::string& msg);
+}
+
 inline unsigned cdiv_u(long a, long b) { return (unsigned)((a + b - 1) / b); }

@@ -10,14 +10,17 @@
 #include "stencil.h"
 #include "vcycle.h"
 
-namespace {
-
+namespace hs {
 thread_local std::string g_last_error;
-
-int fail(int code, const std::string& msg) {
+int set_error(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
+}  // namespace hs
+
+namespace {
+
+int fail(int code, const std::string& msg) { return hs::set_error(code, msg); }
 
 int check_cuda(const char* what) {
   cudaError_t e = cudaGetLastError();
@@ -121,7 +124,7 @@ int* pinned_flag() {
 }  // namespace
 
 HS_API int hs_abi_version(void) { return 1; }
-HS_API const char* hs_last_error(void) { return g_last_error.c_str(); }
+HS_API const char* hs_last_error(void) { return hs::g_last_error.c_str(); }
 
 HS_API int hs_helm_apply(const void* u, void* out, const void* mass, const int* model_of, int B, int nx, int ny,
                          double h, double wall_x, double wall_y, int mode, void* stream) {

@@ -1,0 +1,169 @@
+"""GPU parity of the CNN primitives, the implicit layer, the network and the learned solve."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from conftest import complex_noise, golden, history_dev, relerr
+
+pytestmark = pytest.mark.gpu
+
+from paper_2306_17486_b200 import fields, green, krylov, netparams, network  # noqa: E402
+from oracle import helm_oracle as ho  # noqa: E402
+from oracle import network_oracle as no  # noqa: E402
+
+
+def run_conv(x_nchw, w, b, stride=1, transposed=False, softplus=False, addend=None, residual=None):
+    """One hs_conv2d call on NCHW numpy data (weights in the reference's layout)."""
+    import torch
+
+    from paper_2306_17486_b200 import _lib
+    from paper_2306_17486_b200.device import stream_handle
+
+    wt = w.transpose(1, 0, 2, 3) if transposed else w
+    cout, cin = wt.shape[:2]
+    wd = torch.from_numpy(np.ascontiguousarray(wt.transpose(0, 2, 3, 1)).astype(np.float32)).cuda()
+    bd = torch.from_numpy(b.astype(np.float32)).cuda()
+    xd = torch.from_numpy(np.ascontiguousarray(x_nchw.transpose(0, 2, 3, 1))).cuda()
+    B, H, W = x_nchw.shape[0], x_nchw.shape[2], x_nchw.shape[3]
+    Ho, Wo = (2 * H, 2 * W) if transposed else ((H - 1) // stride + 1, (W - 1) // stride + 1)
+    y = torch.empty((B, Ho, Wo, cout), dtype=torch.float32, device="cuda")
+    c = _lib.HsConv(cin, cout, stride if not transposed else 2, int(transposed), int(softplus), wd.data_ptr(),
+                    bd.data_ptr())
+    ad = None if addend is None else torch.from_numpy(np.ascontiguousarray(addend.transpose(0, 2, 3, 1))).cuda()
+    rd = None if residual is None else torch.from_numpy(np.ascontiguousarray(residual.transpose(0, 2, 3, 1))).cuda()
+    _lib.check(_lib.load().hs_conv2d(xd.data_ptr(), ctypes.byref(c), None if ad is None else ad.data_ptr(),
+                                     None if rd is None else rd.data_ptr(), y.data_ptr(), B, H, W, stream_handle()),
+               "conv")
+    return y.cpu().numpy().transpose(0, 3, 1, 2)
+
+
+def test_conv_primitives_match_reference():
+    g = golden("cnn_primitives.npz")
+    x, w, b = g["x"], g["w"], g["bias"]
+    assert relerr(run_conv(x, w, b), g["conv_s1"]) < 1e-6
+    assert relerr(run_conv(x, w, b, stride=2), g["conv_s2"]) < 1e-6
+    assert relerr(run_conv(x, g["wt"], b[:1].repeat(5), transposed=True), g["tconv"]) < 1e-6
+
+
+@pytest.mark.parametrize("cin,cout,stride,hw", [(2, 16, 1, (32, 32)), (16, 16, 1, (64, 40)), (16, 32, 2, (64, 64)),
+                                                (32, 64, 2, (32, 48)), (64, 64, 1, (16, 16)), (64, 128, 2, (16, 32)),
+                                                (16, 2, 1, (32, 32)), (128, 128, 1, (8, 16))])
+def test_conv_shapes_and_epilogue(rng, cin, cout, stride, hw):
+    x = rng.standard_normal((2, cin, *hw)).astype(np.float32)
+    w = (rng.standard_normal((cout, cin, 3, 3)) / np.sqrt(9 * cin)).astype(np.float32)
+    b = rng.standard_normal(cout).astype(np.float32)
+    ho, wo = (hw[0] - 1) // stride + 1, (hw[1] - 1) // stride + 1
+    add = rng.standard_normal((2, cout, ho, wo)).astype(np.float32)
+    y = run_conv(x, w, b, stride=stride, softplus=True, addend=add)
+    ref = no.softplus(no.conv2d(x, w, b, stride)) + add
+    assert relerr(y, ref) < 2e-6
+    y2 = run_conv(x, w, b, stride=stride, residual=add)
+    assert relerr(y2, no.conv2d(x, w, b, stride) + add) < 2e-6
+
+
+@pytest.mark.parametrize("cin,cout,hw", [(64, 32, (8, 8)), (32, 16, (16, 24)), (128, 64, (4, 8))])
+def test_tconv_shapes(rng, cin, cout, hw):
+    x = rng.standard_normal((2, cin, *hw)).astype(np.float32)
+    w = (rng.standard_normal((cin, cout, 3, 3)) / np.sqrt(9 * cout)).astype(np.float32)
+    b = rng.standard_normal(cout).astype(np.float32)
+    skip = rng.standard_normal((2, cout, 2 * hw[0], 2 * hw[1])).astype(np.float32)
+    y = run_conv(x, w, b, transposed=True, softplus=True, addend=skip)
+    assert relerr(y, no.softplus(no.conv_transpose2d(x, w, b)) + skip) < 2e-6
+
+
+def test_green_function_and_implicit_apply_match_reference():
+    g = golden("cnn_primitives.npz")
+    for tag in ("8x8", "16x16", "8x16"):
+        hh, ww = map(int, tag.split("x"))
+        S = green.green_function(g[f"gk_{tag}"], (hh, ww))
+        assert S.dtype == np.complex128
+        assert relerr(S, g[f"spec_{tag}"]) < 1e-6
+        y = green.implicit_apply(g[f"ix_{tag}"], g[f"spec_{tag}"].astype(np.complex64))
+        assert relerr(y, g[f"iy_{tag}"]) < 2e-6
+
+
+def test_green_regression_ratio_on_device():
+    # test_green.py:73-80
+    S = green.green_function(green.laplacian_plus_i_kernel(1), (16, 16))
+    resp = np.fft.ifft2(S[0])
+    assert np.abs(resp[16, 16]) / np.abs(resp[0, 0]) == pytest.approx(1.137e-8, rel=0.05)
+
+
+def test_implicit_kernel_cache():
+    k = green.ImplicitKernel(2)
+    s1 = k.spectrum((8, 8))
+    assert k.spectrum((8, 8)) is s1
+    k.weights[0, 1, 1] += 0.5
+    k.bump_version()
+    assert k.spectrum((8, 8)) is not s1
+
+
+@pytest.mark.parametrize("L", [2, 3])
+def test_network_matches_reference_composition(L):
+    g = golden("network.npz")
+    tag = f"L{L}"
+    ch = (16, 32, 64) if L == 3 else (8, 16)
+    p = netparams.randomise_batchnorm(netparams.init_params(ch, seed=5), seed=6)
+    k2, gm = g[f"kappa_sq_{tag}"], g[f"gamma_{tag}"]
+    n = k2.shape[0]
+    m = fields.SlownessModel(k2, gm, 10.0, 1.0 / (n - 1))
+    net = network.EncoderSolverNet(p, ch)
+    enc = network.precompute_encodings(net, m)
+    for lv in range(L):
+        e = enc.tensors[lv].cpu().numpy().transpose(0, 3, 1, 2)
+        assert relerr(e, g[f"enc{lv}_{tag}"]) < 1e-5
+    r = g[f"r_{tag}"]
+    u0 = network.preconditioner_estimate(net, enc, r)
+    (ix, iy), _ = no.cnn_dims(r.shape, L)
+    y = g[f"y_{tag}"][0]
+    s = np.float32(m.h * m.h / 64.0)
+    ref = np.zeros(r.shape, np.complex64)
+    ref[:ix, :iy] = s * y[0] + 1j * (s * y[1])
+    assert relerr(u0, ref) < 2e-5
+
+
+def test_preconditioner_estimate_matches_oracle_batched(rng):
+    n, L, ch = 65, 3, (16, 32, 64)
+    m = fields.slowness_model(rng.uniform(0.25, 1.0, (n, n)), layer_width=8)
+    net = network.EncoderSolverNet.seeded(ch, seed=3)
+    enc = network.precompute_encodings(net, m)
+    r = complex_noise(rng, (3, n, n)).astype(np.complex64)
+    u0 = network.preconditioner_estimate(net, enc, r)
+    feats = no.encode(net.params, L, no.media_planes(m.kappa_sq, m.gamma, L))
+    spec = no.spectrum_c64(net.params, L, m.shape)
+    for i in range(3):
+        assert relerr(u0[i], no.preconditioner_estimate(net.params, L, feats, spec, r[i], m.h)) < 2e-5
+
+
+def test_learned_c1_matches_reference():
+    g = golden("learned_c1.npz")
+    m = fields.slowness_model(g["kappa_sq"], layer_width=16)
+    net = network.EncoderSolverNet.seeded((16, 32, 64), seed=0)
+    xs, reps = krylov.solve_batch([m], g["rhs"], net=net, tol=1e-6, max_iter=400, restart=10,
+                                  jacobi_damping=(0.8, 0.8))
+    for i, rep in enumerate(reps):
+        it = int(g["iterations"][i])
+        assert abs(rep.iterations - it) <= 1, (rep.iterations, it)
+        assert history_dev(rep.relative_residual_history, g["hist"][i][: it + 1]) < 1e-4
+        assert relerr(xs[i], g["x"][i]) < 1e-4
+        assert rep.converged
+
+
+def test_learned_entry_point_single_rhs(rng):
+    n = 33
+    m = fields.slowness_model(rng.uniform(0.25, 1.0, (n, n)), layer_width=4)
+    net = network.EncoderSolverNet.seeded((8, 16), seed=1)
+    b = fields.ComplexField(complex_noise(rng, (n, n)), m.h)
+    x, rep = krylov.solve_with_learned_preconditioner(m, b, net, tol=1e-6, max_iter=300)
+    om = ho.Model(m.kappa_sq, m.gamma, m.omega, m.h)
+    feats = no.encode(net.params, 2, no.media_planes(m.kappa_sq, m.gamma, 2))
+    spec = no.spectrum_c64(net.params, 2, m.shape)
+    xo, ro = ho.solve_learned(om, b.data, lambda r: no.preconditioner_estimate(net.params, 2, feats, spec, r, m.h),
+                              1e-6, 300, 10, 3)
+    assert abs(rep.iterations - ro.iterations) <= 1
+    assert history_dev(rep.relative_residual_history, ro.history) < 1e-4
+    assert relerr(x.data, xo) < 1e-4
+    # tol = 1 returns after the warm-up's first check
+    x1, rep1 = krylov.solve_with_learned_preconditioner(m, b, net, tol=1.0)
+    assert rep1.converged and rep1.iterations == 0
