@@ -54,6 +54,7 @@ struct ConvArgs {
   const float* addend;  // NHWC like y, per model (model_of) or per batch item
   long long addend_bstride;
   const int* model_of;
+  int addend_per_model;  // 1: addend indexed by model_of[b] (encodings), 0: by b (skips)
   const float* residual;  // NHWC like y
   const void* const* active;
 };
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(kConvThreads) k_conv(ConvArgs a) {
   const int oy = oy0 + ly;
   if (oy >= a.Ho) return;
   const long long obase = (long long)b * a.Ho * a.Wo * COUT;
-  const float* add = a.addend ? a.addend + (a.model_of ? a.model_of[b] : b) * a.addend_bstride : nullptr;
+  const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[b] : 0) : b) * a.addend_bstride : nullptr;
 #pragma unroll
   for (int p = 0; p < T::PX; ++p) {
     const int ox = ox0 + lx + p;
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(kConvThreads) k_tconv(ConvArgs a) {
   const int oy = oy0 + 2 * qy + py;
   if (oy >= a.Ho) return;
   const long long obase = (long long)b * a.Ho * a.Wo * COUT;
-  const float* add = a.addend ? a.addend + (a.model_of ? a.model_of[b] : b) * a.addend_bstride : nullptr;
+  const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[b] : 0) : b) * a.addend_bstride : nullptr;
 #pragma unroll
   for (int p = 0; p < T::PX; ++p) {
     const int ox = ox0 + 2 * (qx + p) + px;
@@ -271,7 +272,7 @@ void launch_tconv_t(const ConvArgs& a, int B, cudaStream_t st) {
 
 int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* y, const float* addend,
                 long long addend_bstride, const int* model_of, const float* residual, const void* const* active,
-                cudaStream_t st) {
+                cudaStream_t st, bool model_of_addend = false) {
   ConvArgs a{};
   a.x = x;
   a.H = H;
@@ -292,6 +293,7 @@ int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* 
   a.addend = addend;
   a.addend_bstride = addend_bstride;
   a.model_of = model_of;
+  a.addend_per_model = addend && model_of_addend;
   a.residual = residual;
   a.active = active;
   if (!c.transposed && conv_tc_supported(c.cin, c.cout, c.stride)) {
@@ -310,6 +312,8 @@ int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* 
     return HS_OK;
   switch (c.cout) {
     HS_CONV_CASE(2)
+    HS_CONV_CASE(4)
+    HS_CONV_CASE(5)
     HS_CONV_CASE(8)
     HS_CONV_CASE(16)
     HS_CONV_CASE(32)
@@ -601,7 +605,7 @@ static int solver_forward(const hs_net_t* net, const float* in, float* head, cha
   int rc;
   // level 0: stem (+ encoding 0), residual block -> skip 0
   if ((rc = launch_conv(d.sol_stem, in, B, d.ix, d.iy, X[0], net->enc[0], lvl_bstride(0), model_of, nullptr, active,
-                        st)))
+                        st, true)))
     return rc;
   if ((rc = launch_conv(d.sol_res_a[0], X[0], B, d.ix, d.iy, Tm[0], nullptr, 0, nullptr, nullptr, active, st)))
     return rc;
@@ -609,7 +613,7 @@ static int solver_forward(const hs_net_t* net, const float* in, float* head, cha
   for (int l = 1; l < d.levels; ++l) {
     const int H = d.ix >> (l - 1), W = d.iy >> (l - 1), h = d.ix >> l, w = d.iy >> l;
     if ((rc = launch_conv(d.sol_down[l], S[l - 1], B, H, W, X[l], net->enc[l], lvl_bstride(l), model_of, nullptr,
-                          active, st)))
+                          active, st, true)))
       return rc;
     if ((rc = launch_conv(d.sol_res_a[l], X[l], B, h, w, Tm[l], nullptr, 0, nullptr, nullptr, active, st))) return rc;
     if ((rc = launch_conv(d.sol_res_b[l], Tm[l], B, h, w, S[l], nullptr, 0, nullptr, X[l], active, st))) return rc;
