@@ -169,6 +169,16 @@ HS_API void hs_net_destroy(hs_net_t* net);
 HS_API size_t hs_net_encode_workspace_bytes(const hs_net_t* net, int n_models);
 HS_API int hs_net_encode(hs_net_t* net, const float* media, int n_models, float* const* enc, void* ws,
                          size_t ws_bytes, void* stream);
+/* ---- tracing (the reference only reports SolveReport.wall_time) ---- */
+/* tags: 0 every conv (work = flops), 1 level-0 16-channel convs, 2 V-cycle
+ * (work = algorithmic bytes), 3 Gram-Schmidt dot pass (bytes), 4 network
+ * forward, 5 implicit layer, 6 finest-level V-cycle up-leg kernel (bytes). */
+HS_API void hs_profile_enable(unsigned tag_mask);
+HS_API void hs_profile_reset(void);
+HS_API int hs_profile_query(int tag, double* total_ms, double* total_work, long long* count);
+/* kernels launched by the library since the last hs_profile_reset */
+HS_API long long hs_launch_count(void);
+
 /* use caller-held encodings (same layout as hs_net_encode's output) */
 HS_API int hs_net_set_encodings(hs_net_t* net, int levels, const float* const* enc);
 /* network.preconditioner_estimate (krylov.py:225-226): u0 = (h^2/64) net(r),

@@ -1,0 +1,78 @@
+"""CPU ORACLE timing (bench.py's cpu_baseline leg and --impl reference arm only).
+
+Times the numpy restatement of the reference path (oracle/helm_oracle.py +
+oracle/network_oracle.py) on the host cores: P worker processes, each running
+a bounded number of FGMRES iterations of one RHS of the workload with the same
+preconditioner protocol as the GPU run.  Throughput in RHS/s is extrapolated
+from seconds per iteration and the workload's iterations per RHS (measured by
+the GPU run on the same seeded inputs, parity-checked against this oracle).
+"""
+from __future__ import annotations
+
+import os
+import time
+
+import numpy as np
+
+_STATE = {}
+
+
+def _setup(config: str, learned: bool, rhs_per_model: int):
+    from oracle import helm_oracle as ho
+    from oracle import network_oracle as no
+    from paper_2306_17486_b200 import netparams, problems
+
+    cfg = problems.make_config(config, rhs_per_model=rhs_per_model)
+    models = [ho.Model(m.kappa_sq, m.gamma, m.omega, m.h) for m in cfg.models]
+    hiers = [ho.build_hierarchy(m, damping=cfg.jacobi_damping, num_levels=cfg.mg_levels) for m in models]
+    nets = None
+    if learned:
+        L = len(cfg.cnn_channels)
+        p = netparams.init_params(cfg.cnn_channels, seed=0)
+        spec = no.spectrum_c64(p, L, cfg.shape)
+        nets = [(p, L, no.encode(p, L, no.media_planes(m.kappa_sq, m.gamma, L)), spec) for m in models]
+    _STATE.update(cfg=cfg, models=models, hiers=hiers, nets=nets)
+
+
+def _worker(args):
+    config, learned, rhs_per_model, index, iters = args
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    if not _STATE:
+        _setup(config, learned, rhs_per_model)
+    from oracle import helm_oracle as ho
+    from oracle import network_oracle as no
+
+    cfg = _STATE["cfg"]
+    b = cfg.rhs[index % cfg.rhs.shape[0]]
+    mi = int(cfg.model_of_rhs[index % cfg.rhs.shape[0]])
+    m, H = _STATE["models"][mi], _STATE["hiers"][mi]
+    A = lambda u: ho.helmholtz(u, m)  # noqa: E731
+    # phase 1: V-cycle-only iterations (the whole solve, or the learned protocol's warm-up)
+    t0 = time.perf_counter()
+    x1, r1 = ho.fgmres(A, lambda r: ho.v_cycle(r, None, H), b, None, 1e-30, 3 if learned else iters, cfg.restart)
+    t_v = (time.perf_counter() - t0) / max(r1.iterations, 1)
+    if not learned:
+        return t_v, 0.0
+    # phase 2: net -> V-cycle iterations (krylov.py:225-236)
+    p, L, feats, spec = _STATE["nets"][mi]
+    t0 = time.perf_counter()
+    _, r2 = ho.fgmres(A, lambda r: ho.v_cycle(r, no.preconditioner_estimate(p, L, feats, spec, r, m.h), H),
+                      b, x1, 1e-30, iters, cfg.restart)
+    return t_v, (time.perf_counter() - t0) / max(r2.iterations, 1)
+
+
+def sample(config: str, learned: bool, workers: int, iters: int, rhs_per_model: int | None = None):
+    """(seconds per V-cycle iteration, seconds per learned iteration) with `workers` busy processes."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("fork")
+    args = [(config, learned, rhs_per_model, i, iters) for i in range(workers)]
+    with ctx.Pool(workers) as pool:
+        res = pool.map(_worker, args)
+    return float(np.mean([r[0] for r in res])), float(np.mean([r[1] for r in res]))
+
+
+def rhs_per_second(t_v: float, t_l: float, workers: int, mean_iters: float, learned: bool, warmup: int = 3):
+    """Extrapolated whole-RHS throughput of `workers` concurrent processes."""
+    per_rhs = (warmup * t_v + max(mean_iters - warmup, 0.0) * t_l) if learned else mean_iters * t_v
+    return workers / per_rhs

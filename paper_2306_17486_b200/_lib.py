@@ -124,6 +124,10 @@ SIGNATURES = {
     "hs_green_spectrum": (_I, [_VP, _I, _I, _I, _VP, _VP]),
     "hs_implicit_apply": (_I, [_VP, _VP, _VP, _I, _I, _I, _I, _VP]),
     "hs_conv2d": (_I, [_VP, ctypes.POINTER(HsConv), _VP, _VP, _VP, _I, _I, _I, _VP]),
+    "hs_profile_enable": (None, [ctypes.c_uint]),
+    "hs_profile_reset": (None, []),
+    "hs_profile_query": (_I, [_I, c_double_p, c_double_p, ctypes.POINTER(ctypes.c_longlong)]),
+    "hs_launch_count": (ctypes.c_longlong, []),
 }
 
 _lock = threading.Lock()
@@ -148,6 +152,16 @@ def load():
                 fn.argtypes = args
             _lib = lib
         return _lib
+
+
+PROF_CONV, PROF_CONV_L0, PROF_VCYCLE, PROF_ARNOLDI, PROF_CNN, PROF_IMPLICIT, PROF_VC_UP0 = range(7)
+
+
+def profile_query(tag: int):
+    """(total_ms, total_work, launches) of a tag since the last reset."""
+    ms, work, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong()
+    check(load().hs_profile_query(tag, ctypes.byref(ms), ctypes.byref(work), ctypes.byref(n)), "profile")
+    return ms.value, work.value, n.value
 
 
 def last_error() -> str:

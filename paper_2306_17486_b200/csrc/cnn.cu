@@ -20,6 +20,7 @@
 #include "cnn.h"
 #include "common.cuh"
 #include "conv_tc.h"
+#include "prof.h"
 
 struct hs_net {
   hs_net_desc_t d;
@@ -294,6 +295,20 @@ int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* 
   a.addend_bstride = addend_bstride;
   a.model_of = model_of;
   a.addend_per_model = addend && model_of_addend;
+  prof::count(1);
+  struct Scope {
+    int s1, s2;
+    cudaStream_t st;
+    double work;
+    ~Scope() {
+      prof::stop(s2, st, work);
+      prof::stop(s1, st, work);
+    }
+  };
+  const double flops =
+      2.0 * 9.0 * c.cin * c.cout * (c.transposed ? (double)H * W : (double)a.Ho * a.Wo) * prof::active_hint(B);
+  const bool l0 = c.cin == 16 && c.cout == 16 && c.stride == 1 && !c.transposed;
+  Scope scope{prof::start(prof::CONV, st), l0 ? prof::start(prof::CONV_L0, st) : -1, st, flops};
   a.residual = residual;
   a.active = active;
   if (!c.transposed && conv_tc_supported(c.cin, c.cout, c.stride)) {
@@ -620,8 +635,10 @@ static int solver_forward(const hs_net_t* net, const float* in, float* head, cha
   }
   // coarsest: implicit layer S[L-1] -> X[L-1]
   const int L1 = d.levels - 1;
-  if ((rc = implicit_apply_dev(net, S[L1], X[L1], reinterpret_cast<cufftComplex*>(ws + L.fftz), active, B, st)))
-    return rc;
+  const int islot = prof::start(prof::IMPLICIT, st);
+  rc = implicit_apply_dev(net, S[L1], X[L1], reinterpret_cast<cufftComplex*>(ws + L.fftz), active, B, st);
+  prof::stop(islot, st, 0.0);
+  if (rc) return rc;
   // up path: X[l] -> (tconv + skip) X[l-1] -> residual block
   for (int l = L1; l >= 1; --l) {
     const int h = d.ix >> l, w = d.iy >> l, H = d.ix >> (l - 1), W = d.iy >> (l - 1);
@@ -650,10 +667,13 @@ void cnn_preconditioner_estimate(const hs_net_t* net, VecIn vin, const float2* c
   float* in = reinterpret_cast<float*>(w + L.in);
   float* head = reinterpret_cast<float*>(w + L.head);
   const void* const* act = reinterpret_cast<const void* const*>(active);
+  const int slot = prof::start(prof::CNN, st);
   k_gather_r<<<dim3(grid1((long long)d.ix * d.iy), B), 256, 0, st>>>(vin, act, in, d.nx, d.ny, d.ix, d.iy);
   solver_forward(net, in, head, w, L, model_of, act, B, st);
   k_scatter_u0<<<dim3(grid1((long long)d.nx * d.ny), B), 256, 0, st>>>(head, act, u0, d.nx, d.ny, d.ix, d.iy,
                                                                        d.out_scale);
+  prof::count(5);  // gather, scatter, pack, spectral multiply, crop (cuFFT kernels not counted)
+  prof::stop(slot, st, 0.0);
 }
 
 }  // namespace hs

@@ -16,6 +16,7 @@
 
 #include "common.cuh"
 #include "krylov.h"
+#include "prof.h"
 
 namespace hs {
 
@@ -381,9 +382,16 @@ void krylov_prep(const SolveDims& d, const SolveBuffers& s, cudaStream_t stream)
   k_prep<<<cdiv_u(d.B, 128), 128, 0, stream>>>(d, s);
 }
 
-void krylov_after_precond(const SolveDims& d, const SolveBuffers& s, cudaStream_t stream) {
+void krylov_after_precond(const SolveDims& d, const SolveBuffers& s, int j_hint, cudaStream_t stream) {
   const int nch = (std::min(d.restart, d.max_iter) + KC - 1) / KC;
+  // algorithmic bytes of the dot pass: z_j (8N) + v_0..v_j (8N each) per RHS,
+  // the complex128 true-operator mass (16N) once per model
+  const double N = (double)d.N;
+  const double dot_bytes = prof::active_hint(d.B) * 8.0 * N * (j_hint + 2) + d.n_models * 16.0 * N;
+  const int slot = prof::start(prof::ARNOLDI, stream);
   k_arnoldi<DOT><<<dim3(d.nblk, nch, d.B), NT, 0, stream>>>(d, s, nch);
+  prof::stop(slot, stream, dot_bytes);
+  prof::count(7);
   k_arnoldi<ORTH><<<dim3(d.nblk, 1, d.B), NT, 0, stream>>>(d, s, 1);
   k_arnoldi<REDOT><<<dim3(d.nblk, nch, d.B), NT, 0, stream>>>(d, s, nch);
   k_arnoldi<ORTH2><<<dim3(d.nblk, 1, d.B), NT, 0, stream>>>(d, s, 1);

@@ -65,7 +65,7 @@ void krylov_init(const SolveDims& d, const SolveBuffers& s, const double* tol, b
 // pointer tables for the preconditioner of the current step
 void krylov_prep(const SolveDims& d, const SolveBuffers& s, cudaStream_t stream);
 // everything after z_j = M v_j: Arnoldi, Givens, window end
-void krylov_after_precond(const SolveDims& d, const SolveBuffers& s, cudaStream_t stream);
+void krylov_after_precond(const SolveDims& d, const SolveBuffers& s, int j_hint, cudaStream_t stream);
 void krylov_count_active(const SolveDims& d, const SolveBuffers& s, cudaStream_t stream);
 
 }  // namespace hs

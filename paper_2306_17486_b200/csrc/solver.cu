@@ -7,6 +7,7 @@
 #include "cnn.h"
 #include "common.cuh"
 #include "krylov.h"
+#include "prof.h"
 #include "stencil.h"
 #include "vcycle.h"
 
@@ -245,12 +246,16 @@ HS_API int hs_fgmres_solve(const hs_hierarchy_t* h, const hs_net_t* net, const h
 
   int* flag = pinned_flag();
   const int kCheckEvery = 4;
+  int done_steps = 0;
   for (int step = 0; step <= a->max_iter + 2 * kCheckEvery; step += kCheckEvery) {
     hs::krylov_count_active(d, s, st);
+    hs::prof::count(1);
     cudaMemcpyAsync(flag, s.n_active, sizeof(int), cudaMemcpyDeviceToHost, st);
     if (cudaStreamSynchronize(st) != cudaSuccess) return check_cuda("fgmres poll");
     if (*flag == 0) break;
-    for (int k = 0; k < kCheckEvery; ++k) {
+    hs::prof::active_now.store(*flag);
+    for (int k = 0; k < kCheckEvery; ++k, ++done_steps) {
+      hs::prof::count(1);
       hs::krylov_prep(d, s, st);
       hs::VecIn vin{s.vin, nullptr, 0, s.vin_scale};
       hs::VecOut zout{s.zout, nullptr, 0};
@@ -260,10 +265,12 @@ HS_API int hs_fgmres_solve(const hs_hierarchy_t* h, const hs_net_t* net, const h
         uz = hs::VecIn{nullptr, u0, N, nullptr};
       }
       hs::vcycle(H, vin, uz, zout, s.vin, a->model_of, a->B, vws, vstatus, st);
-      hs::krylov_after_precond(d, s, st);
+      hs::krylov_after_precond(d, s, done_steps % window, st);
     }
     if ((rc = check_cuda("fgmres step")) != HS_OK) return rc;
   }
+  hs::prof::active_now.store(0);
+  hs::prof::count(1);
   k_finalize<<<cdiv_u(a->B, 128), 128, 0, st>>>(d, s, a->hist_len, a->iterations, a->converged, a->status, vstatus);
   return check_cuda("fgmres finalize");
 }

@@ -15,6 +15,7 @@
 // basis kept in an L2-resident workspace, fp64 reductions.
 #include "common.cuh"
 #include "level.cuh"
+#include "prof.h"
 #include "vcycle.h"
 
 namespace hs {
@@ -464,6 +465,14 @@ void vcycle(const Hierarchy& H, VecIn rhs, VecIn u0, VecOut out, const float2* c
     k_scatter<<<g, 256, 0, stream>>>(tmp_out, active, out, (long long)nc);
     return;
   }
+  // Algorithmic HBM bytes: per RHS and non-coarsest level,
+  // down = rhs 8N + coarse 2N, up = rhs 8N + e 2N + out 8N (+ u0 8N twice at
+  // level 0); the complex64 medium (8N) is read once per slowness model per
+  // kernel (it is shared by every RHS of that model and stays in L2).
+  const bool has_u0 = (u0.tab || u0.base);
+  const double nact = prof::active_hint(B);
+  double vc_bytes = 0.0;
+  const int vslot = prof::start(prof::VCYCLE, stream);
   // down legs
   for (int l = 0; l < Lc; ++l) {
     const LevelDev& F = H.lv[l];
@@ -473,10 +482,13 @@ void vcycle(const Hierarchy& H, VecIn rhs, VecIn u0, VecOut out, const float2* c
     dim3 g(cdiv_u(ncx, kDownCX) * cdiv_u(ncy, kDownCY), B);
     k_vc_down<kDownCX, kDownCY><<<g, 256, 0, stream>>>(F, ncx, ncy, in, uz, active, model_of, H.w_pre,
                                                         lrhs[l + 1]);
+    const double N = (double)F.nx * F.ny;
+    vc_bytes += nact * (10.0 * N + ((l == 0 && has_u0) ? 8.0 * N : 0.0)) + H.n_models * 8.0 * N;
   }
   // coarsest
   k_coarse_gmres<<<B, kCoarseThreads, 0, stream>>>(C, lrhs[Lc], lerr[Lc], cV, cS, active, model_of,
                                                    H.coarse_iters, H.coarse_damping, status);
+  vc_bytes += nact * 16.0 * (double)nc + H.n_models * 8.0 * (double)nc;
   // up legs
   for (int l = Lc - 1; l >= 0; --l) {
     const LevelDev& F = H.lv[l];
@@ -485,9 +497,16 @@ void vcycle(const Hierarchy& H, VecIn rhs, VecIn u0, VecOut out, const float2* c
     VecIn uz = l == 0 ? u0 : VecIn{nullptr, nullptr, 0, nullptr};
     VecOut o = l == 0 ? out : VecOut{nullptr, lerr[l], (long long)F.nx * F.ny};
     dim3 g(cdiv_u(F.nx, kUpFX) * cdiv_u(F.ny, kUpFY), B);
+    const double N = (double)F.nx * F.ny;
+    const double up_bytes = nact * (18.0 * N + ((l == 0 && has_u0) ? 8.0 * N : 0.0)) + H.n_models * 8.0 * N;
+    const int uslot = l == 0 ? prof::start(prof::VC_UP0, stream) : -1;
     k_vc_up<kUpFX, kUpFY><<<g, 256, 0, stream>>>(F, ncx, ncy, in, uz, active, model_of, H.w_pre, H.w_post,
                                                  lerr[l + 1], o);
+    prof::stop(uslot, stream, up_bytes);
+    vc_bytes += up_bytes;
   }
+  prof::stop(vslot, stream, vc_bytes);
+  prof::count(2 * Lc + 1);
 }
 
 }  // namespace hs

@@ -212,91 +212,100 @@ def solve_with_learned_preconditioner(model: SlownessModel, b: ComplexField, net
     return ComplexField(xs[0], b.h), reports[0]
 
 
+class BatchSolver:
+    """Device-resident solver for many RHS over one or more equal-shape slowness models.
+
+    Setup (hierarchies, device media, network encodings and Green spectrum)
+    happens once here; ``solve`` then runs the whole batch on the GPU.
+    ``net is None`` gives the V-cycle-only protocol of ``solve_helmholtz``;
+    otherwise the warm-up + net->V-cycle protocol of
+    ``solve_with_learned_preconditioner`` (krylov.py:214-245) for every RHS.
+    """
+
+    def __init__(self, models, net=None, encodings=None, hierarchies=None, num_levels: int = 3,
+                 jacobi_damping=None, coarse_iters: int = 10):
+        from .engine import Engine
+        from .multigrid import CHEBYSHEV_DAMPING, DeviceHierarchy, build_hierarchy
+
+        self.models = list(models)
+        if hierarchies is None:
+            damp = CHEBYSHEV_DAMPING if jacobi_damping is None else jacobi_damping
+            hierarchies = [build_hierarchy(m, num_levels=num_levels, jacobi_damping=damp,
+                                           coarse_iters=coarse_iters) for m in self.models]
+        self.hierarchies = list(hierarchies)
+        self.dh = DeviceHierarchy(self.hierarchies, true_models=self.models)
+        self.net = net
+        net_dev = None
+        if net is not None:
+            from .network import device_network
+
+            net_dev = device_network(net, self.models, encodings, self.dh)
+        self.engine = Engine(self.dh, net_dev)
+
+    def solve(self, rhs, model_of=None, tol: float = 1e-7, max_iter: int = 250, restart: int | None = 10,
+              warmup_iters: int = 3, return_device: bool = False, raise_errors: bool = True):
+        """x (B, nx, ny) complex128 and one SolveReport per RHS."""
+        import torch
+
+        from .device import require_cuda, to_device
+        from .engine import BatchResult, raise_for_status
+        from .fields import apply_operator
+
+        if tol <= 0:
+            raise ValueError(f"tol must be positive, got {tol}")
+        if max_iter < 1:
+            raise ValueError(f"max_iter must be >= 1, got {max_iter}")
+        start = time.perf_counter()
+        dev = require_cuda()
+        bd = to_device(rhs, torch.complex128)
+        B = bd.shape[0]
+        owner = np.zeros(B, dtype=np.int32) if model_of is None else np.asarray(model_of, dtype=np.int32)
+        owner_d = torch.from_numpy(owner).to(dev)
+        eng = self.engine
+        if self.net is None:
+            res = eng.fgmres(bd, None, tol, max_iter, restart, owner_d)
+            reports = [SolveReport(int(res.iterations[i]), res.histories[i], bool(res.converged[i]), 0.0)
+                       for i in range(B)]
+            status, x = res.status, res.x
+        else:
+            # phase 1: V-cycle warm-up from zero (krylov.py:215-220)
+            r1 = eng.fgmres(bd, None, tol, min(warmup_iters, max_iter), restart, owner_d)
+            x = r1.x
+            status = r1.status.copy()
+            reports = [SolveReport(int(r1.iterations[i]), r1.histories[i], bool(r1.converged[i]), 0.0)
+                       for i in range(B)]
+            cont = [i for i in range(B) if not (r1.converged[i] or r1.iterations[i] >= max_iter) and not status[i]]
+            if cont:
+                idx = torch.tensor(cont, device=dev)
+                # rel1 = ||b - A x1|| / ||b|| in fp64 on the device (krylov.py:222-223)
+                num = torch.empty(len(cont), dtype=torch.float64, device=dev)
+                for k, i in enumerate(cont):
+                    num[k] = torch.linalg.vector_norm(bd[i] - apply_operator(x[i], self.models[owner[i]]))
+                den = torch.linalg.vector_norm(bd[idx].reshape(len(cont), -1), dim=1)
+                rel1 = (num / den).cpu().numpy()
+                it1 = int(r1.iterations[cont[0]])
+                r2 = eng.fgmres(bd[idx], x[idx], tol / rel1, max_iter - it1, restart, owner_d[idx], use_net=True)
+                x[idx] = r2.x
+                for k, i in enumerate(cont):
+                    reports[i] = SolveReport(
+                        reports[i].iterations + int(r2.iterations[k]),
+                        reports[i].relative_residual_history + [e * rel1[k] for e in r2.histories[k][1:]],
+                        bool(r2.converged[k]), 0.0)
+                    status[i] = r2.status[k]
+        wall = time.perf_counter() - start
+        for rep in reports:
+            rep.wall_time = wall
+        if raise_errors:
+            chk = BatchResult(x, [r.relative_residual_history for r in reports],
+                              np.array([r.iterations for r in reports]), None, np.asarray(status))
+            for i in range(B):
+                raise_for_status(chk, i)
+        return (x if return_device else x.cpu().numpy()), reports
+
+
 def solve_batch(models, rhs, model_of=None, net=None, encodings=None, tol: float = 1e-7, max_iter: int = 250,
                 restart: int | None = 10, warmup_iters: int = 3, hierarchies=None, num_levels: int = 3,
                 jacobi_damping=None, coarse_iters: int = 10, return_device: bool = False, raise_errors=True):
-    """Data-parallel solve of many RHS over one or more slowness models of equal shape.
-
-    ``rhs`` is (B, nx, ny) (numpy or CUDA tensor); ``model_of[i]`` names the
-    model of RHS i.  ``net is None``: the V-cycle-only protocol of
-    ``solve_helmholtz`` for every RHS; otherwise the warm-up + net->V-cycle
-    protocol of ``solve_with_learned_preconditioner`` (krylov.py:214-245).
-    Returns (x, reports): x (B, nx, ny) complex128 and one SolveReport per RHS.
-    """
-    import torch
-
-    from .device import require_cuda, to_device
-    from .engine import Engine, raise_for_status
-    from .multigrid import CHEBYSHEV_DAMPING, DeviceHierarchy, build_hierarchy
-
-    if tol <= 0:
-        raise ValueError(f"tol must be positive, got {tol}")
-    if max_iter < 1:
-        raise ValueError(f"max_iter must be >= 1, got {max_iter}")
-    start = time.perf_counter()
-    dev = require_cuda()
-    models = list(models)
-    if hierarchies is None:
-        damp = CHEBYSHEV_DAMPING if jacobi_damping is None else jacobi_damping
-        hierarchies = [build_hierarchy(m, num_levels=num_levels, jacobi_damping=damp, coarse_iters=coarse_iters)
-                       for m in models]
-    dh = DeviceHierarchy(hierarchies, true_models=models)
-    bd = to_device(rhs, torch.complex128)
-    B = bd.shape[0]
-    owner = np.zeros(B, dtype=np.int32) if model_of is None else np.asarray(model_of, dtype=np.int32)
-    owner_d = torch.from_numpy(owner).to(dev)
-    net_dev = None
-    if net is not None:
-        from .network import device_network
-
-        net_dev = device_network(net, models, encodings, dh)
-    eng = Engine(dh, net_dev)
-
-    if net is None:
-        res = eng.fgmres(bd, None, tol, max_iter, restart, owner_d)
-        reports = [SolveReport(int(res.iterations[i]), res.histories[i], bool(res.converged[i]), 0.0)
-                   for i in range(B)]
-        status = res.status
-        x = res.x
-    else:
-        # phase 1: V-cycle warm-up from zero (krylov.py:215-220)
-        r1 = eng.fgmres(bd, None, tol, min(warmup_iters, max_iter), restart, owner_d)
-        x = r1.x.clone()
-        status = r1.status.copy()
-        reports = [SolveReport(int(r1.iterations[i]), r1.histories[i], bool(r1.converged[i]), 0.0)
-                   for i in range(B)]
-        cont = [i for i in range(B) if not (r1.converged[i] or r1.iterations[i] >= max_iter) and not status[i]]
-        if cont:
-            idx = torch.tensor(cont, device=dev)
-            from .fields import apply_operator
-
-            # rel1 = ||b - A x1|| / ||b|| in fp64 on the device (krylov.py:222-223)
-            resid = torch.stack([
-                bd[i] - apply_operator(x[i], models[owner[i]]) for i in cont
-            ])
-            rel1 = (torch.linalg.vector_norm(resid.reshape(len(cont), -1), dim=1)
-                    / torch.linalg.vector_norm(bd[idx].reshape(len(cont), -1), dim=1)).cpu().numpy()
-            it1 = int(r1.iterations[cont[0]])
-            r2 = eng.fgmres(bd[idx], x[idx], tol / rel1, max_iter - it1, restart, owner_d[idx], use_net=True)
-            x[idx] = r2.x
-            for k, i in enumerate(cont):
-                reports[i] = SolveReport(
-                    reports[i].iterations + int(r2.iterations[k]),
-                    reports[i].relative_residual_history + [e * rel1[k] for e in r2.histories[k][1:]],
-                    bool(r2.converged[k]), 0.0)
-                status[i] = r2.status[k]
-                r2.iterations[k] += it1
-            if raise_errors:
-                for k in range(len(cont)):
-                    raise_for_status(r2, k)
-    wall = time.perf_counter() - start
-    for rep in reports:
-        rep.wall_time = wall
-    if raise_errors:
-        from .engine import BatchResult
-
-        chk = BatchResult(x, [r.relative_residual_history for r in reports],
-                          np.array([r.iterations for r in reports]), None, np.asarray(status))
-        for i in range(B):
-            raise_for_status(chk, i)
-    return (x if return_device else x.cpu().numpy()), reports
+    """Data-parallel solve of many RHS (see BatchSolver); returns (x, reports)."""
+    solver = BatchSolver(models, net, encodings, hierarchies, num_levels, jacobi_damping, coarse_iters)
+    return solver.solve(rhs, model_of, tol, max_iter, restart, warmup_iters, return_device, raise_errors)

@@ -130,29 +130,35 @@ class ProblemSet:
         return self.models[0].shape
 
 
-def make_config(name: str, rhs_per_model: int | None = None, models: int | None = None) -> ProblemSet:
-    """Build one of BASELINE.json's configs C1..C5."""
+def make_config(name: str, rhs_per_model: int | None = None, models: int | None = None,
+                seed_offset: int = 0) -> ProblemSet:
+    """Build one of BASELINE.json's configs C1..C5.
+
+    ``seed_offset`` shifts every seed (a distinct, same-sized instance per
+    data-parallel rank); 0 gives the fixtures' inputs.
+    """
     name = name.upper()
+    so = 1000 * seed_offset
     if name == "C1":
         n, sig, abl, nm, nr = 129, 8.0, 16, 1, 4
-        ks = [smooth_random_kappa_sq((n, n), sig, 0)]
+        ks = [smooth_random_kappa_sq((n, n), sig, so)]
         lv, ch, rs = 3, (16, 32, 64), 10
     elif name == "C2":
         n, sig, abl, nm, nr = 257, 12.0, 20, 4, 32
         nm = models or nm
-        ks = [smooth_random_kappa_sq((n, n), sig, s) for s in range(nm)]
+        ks = [smooth_random_kappa_sq((n, n), sig, s + so) for s in range(nm)]
         lv, ch, rs = 3, (16, 32, 64), 10
     elif name == "C3":
         shape, abl, nm, nr = (513, 1025), 32, 1, 64
-        ks = [layered_kappa_sq(shape, 0)]
+        ks = [layered_kappa_sq(shape, so)]
         lv, ch, rs = 4, (16, 32, 64, 128), 20
     elif name == "C4":
         shape, abl, nm, nr = (1025, 2049), 32, 1, 128
-        ks = [smooth_random_kappa_sq(shape, 24.0, 0)]
+        ks = [smooth_random_kappa_sq(shape, 24.0, so)]
         lv, ch, rs = 4, (16, 32, 64, 128), 20
     elif name == "C5":
         shape, abl, nm, nr = (2049, 4097), 48, 1, 256
-        ks = [salt_kappa_sq(shape, 0)]
+        ks = [salt_kappa_sq(shape, so)]
         lv, ch, rs = 5, (16, 32, 64, 128, 128), 30
     else:
         raise ValueError(f"unknown config {name}")
@@ -163,10 +169,10 @@ def make_config(name: str, rhs_per_model: int | None = None, models: int | None 
     for m in range(len(mods)):
         if name == "C3":
             half = nr // 2
-            rhs.append(point_sources(shape, half, 100 + m, abl))
-            rhs.append(complex_gaussian_rhs(shape, nr - half, 200 + m))
+            rhs.append(point_sources(shape, half, 100 + m + so, abl))
+            rhs.append(complex_gaussian_rhs(shape, nr - half, 200 + m + so))
         else:
-            rhs.append(point_sources(shape, nr, 100 + m, abl))
+            rhs.append(point_sources(shape, nr, 100 + m + so, abl))
         owner += [m] * nr
     return ProblemSet(
         name,
