@@ -178,6 +178,8 @@ HS_API void hs_profile_reset(void);
 HS_API int hs_profile_query(int tag, double* total_ms, double* total_work, long long* count);
 /* kernels launched by the library since the last hs_profile_reset */
 HS_API long long hs_launch_count(void);
+/* 1 (default): tcgen05 3xTF32 convolutions where the shape allows; 0: SIMT fp32 only */
+HS_API void hs_set_conv_path(int tensor_cores);
 
 /* use caller-held encodings (same layout as hs_net_encode's output) */
 HS_API int hs_net_set_encodings(hs_net_t* net, int levels, const float* const* enc);

@@ -128,6 +128,7 @@ SIGNATURES = {
     "hs_profile_reset": (None, []),
     "hs_profile_query": (_I, [_I, c_double_p, c_double_p, ctypes.POINTER(ctypes.c_longlong)]),
     "hs_launch_count": (ctypes.c_longlong, []),
+    "hs_set_conv_path": (None, [_I]),
 }
 
 _lock = threading.Lock()

@@ -311,9 +311,9 @@ int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* 
   Scope scope{prof::start(prof::CONV, st), l0 ? prof::start(prof::CONV_L0, st) : -1, st, flops};
   a.residual = residual;
   a.active = active;
-  if (!c.transposed && conv_tc_supported(c.cin, c.cout, c.stride)) {
-    conv_tc_launch(a.x, a.H, a.W, a.cin, a.y, a.Ho, a.Wo, a.cout, c.stride, a.w, a.bias, a.softplus, a.addend,
-                   a.addend_bstride, a.model_of, a.residual, a.active, B, st);
+  if (conv_tc_supported(c.cin, c.cout, c.stride, c.transposed, H, W, a.Wo)) {
+    conv_tc_launch(a.x, a.H, a.W, a.cin, a.y, a.Ho, a.Wo, a.cout, c.stride, c.transposed, a.w, a.bias, a.softplus,
+                   a.addend, a.addend_bstride, a.addend_per_model, a.model_of, a.residual, a.active, B, st);
     return HS_OK;
   }
 #define HS_CONV_CASE(CO)                          \

@@ -1,10 +1,12 @@
-// tcgen05 (5th-gen tensor core) implicit-GEMM convolution, 3xTF32.
+// tcgen05 (5th-gen tensor core) implicit-GEMM 3x3 convolution, 3xTF32.
 #pragma once
 #include <cuda_runtime.h>
 
 namespace hs {
-bool conv_tc_supported(int cin, int cout, int stride);
+extern bool conv_tc_enabled;  // hs_set_conv_path() toggles it (tests compare both paths)
+bool conv_tc_supported(int cin, int cout, int stride, int transposed, int H, int W, int Wo);
 void conv_tc_launch(const float* x, int H, int W, int cin, float* y, int Ho, int Wo, int cout, int stride,
-                    const float* w, const float* bias, int softplus, const float* addend, long long addend_bstride,
-                    const int* model_of, const float* residual, const void* const* active, int B, cudaStream_t st);
+                    int transposed, const float* w, const float* bias, int softplus, const float* addend,
+                    long long addend_bstride, int addend_per_model, const int* model_of, const float* residual,
+                    const void* const* active, int B, cudaStream_t st);
 }  // namespace hs

@@ -91,3 +91,9 @@ HS_API int hs_profile_query(int tag, double* total_ms, double* total_work, long 
   *count = n;
   return HS_OK;
 }
+
+namespace hs {
+extern bool conv_tc_enabled;
+}
+/* 1 = tcgen05 convolutions where supported (default), 0 = SIMT everywhere (tests) */
+HS_API void hs_set_conv_path(int tensor_cores) { hs::conv_tc_enabled = tensor_cores != 0; }

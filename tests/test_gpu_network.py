@@ -72,6 +72,42 @@ def test_tconv_shapes(rng, cin, cout, hw):
     assert relerr(y, no.softplus(no.conv_transpose2d(x, w, b)) + skip) < 2e-6
 
 
+@pytest.mark.parametrize("cin,cout,mode,hw", [(16, 16, 0, (6, 128)), (16, 16, 0, (5, 256)), (32, 32, 0, (4, 128)),
+                                               (16, 32, 1, (6, 256)), (32, 16, 2, (3, 128)), (32, 16, 2, (2, 256))])
+def test_tcgen05_conv_matches_oracle(rng, cin, cout, mode, hw):
+    """The tcgen05 3xTF32 path (taken for widths that are multiples of 128) against the fp32 oracle."""
+    from paper_2306_17486_b200 import _lib
+
+    x = rng.standard_normal((3, cin, *hw)).astype(np.float32)
+    if mode == 2:
+        w = (rng.standard_normal((cin, cout, 3, 3)) / np.sqrt(9 * cout)).astype(np.float32)
+        out_hw = (2 * hw[0], 2 * hw[1])
+    else:
+        w = (rng.standard_normal((cout, cin, 3, 3)) / np.sqrt(9 * cin)).astype(np.float32)
+        s = 2 if mode == 1 else 1
+        out_hw = ((hw[0] - 1) // s + 1, (hw[1] - 1) // s + 1)
+    b = rng.standard_normal(cout).astype(np.float32)
+    add = rng.standard_normal((3, cout, *out_hw)).astype(np.float32)
+    lib = _lib.load()
+    try:
+        for tc in (1, 0):
+            lib.hs_set_conv_path(tc)
+            if mode == 2:
+                y = run_conv(x, w, b, transposed=True, softplus=True, addend=add)
+                ref = no.softplus(no.conv_transpose2d(x.astype(np.float64), w.astype(np.float64), b)) + add
+            else:
+                y = run_conv(x, w, b, stride=2 if mode == 1 else 1, softplus=True, addend=add)
+                ref = no.softplus(no.conv2d(x.astype(np.float64), w.astype(np.float64), b,
+                                            2 if mode == 1 else 1)) + add
+            assert relerr(y, ref) < 2e-6, (tc, relerr(y, ref))
+            y2 = run_conv(x, w, b, stride=2 if mode == 1 else 1, transposed=mode == 2, residual=add)
+            ref2 = (no.conv_transpose2d(x.astype(np.float64), w.astype(np.float64), b) if mode == 2 else
+                    no.conv2d(x.astype(np.float64), w.astype(np.float64), b, 2 if mode == 1 else 1)) + add
+            assert relerr(y2, ref2) < 2e-6, (tc, relerr(y2, ref2))
+    finally:
+        lib.hs_set_conv_path(1)
+
+
 def test_green_function_and_implicit_apply_match_reference():
     g = golden("cnn_primitives.npz")
     for tag in ("8x8", "16x16", "8x16"):
