@@ -1,25 +1,26 @@
 // tcgen05 implicit-GEMM 3x3 convolution with 3xTF32 (fp32-class) accuracy.
 //
 // GEMM view of one output tile: D[m][n] = sum_k A[m][k] B[n][k] with m = 128
-// consecutive output pixels of one row, n = cout, k = (tap, cin).  The input
-// rows the tile needs are staged ONCE in shared memory in the UMMA K-major
-// "interleaved" canonical layout (core matrix = 8 pixels x 16 bytes, pixels
-// consecutive at 16-byte pitch, channel chunks LBO apart).  Because pixels
-// sit at a 16-byte pitch, the A operand of tap (ky, kx) is the same buffer
-// with the descriptor start address moved by (ky * row_pixels + kx) * 16
-// bytes: no im2col copies.  Stride-2 convolutions store each input row
-// de-interleaved (even columns, then odd columns) so every tap is again a
-// unit-pitch window; the transposed convolution is split into its two
-// column-parity classes (1 and 2 taps) with two TMEM accumulators.
+// consecutive output pixels of one row, n = cout, k = (tap, cin).  Input rows
+// are staged in shared memory in the UMMA K-major "interleaved" canonical
+// layout (core matrix = 8 pixels x 16 bytes, pixels consecutive at a 16-byte
+// pitch, 4-channel chunks LBO apart).  Because pixels sit at a 16-byte pitch,
+// the A operand of tap (ky, kx) is just the staged row with the descriptor
+// start address moved by kx * 16 bytes: no im2col copies.  Stride-2
+// convolutions stage each input row de-interleaved (even columns, then odd
+// columns) so every tap is again a unit-pitch window; the transposed
+// convolution is split into its two column-parity classes (1 and 2 taps)
+// with two TMEM accumulators.
+//
+// Streaming: a CTA owns a band of output rows of one 128-pixel column block
+// and walks it top to bottom.  Input rows live in a ring of shared-memory
+// slots, so each input row is loaded and split once per band (one new row per
+// output row at stride 1).  The MMAs of row t run while the CTA prefetches the
+// rows of t+1 and drains row t-1's accumulator (two TMEM accumulators).
 //
 // Precision: every fp32 operand x is split into tf32 hi = rna(x) and
 // lo = rna(x - hi); the MMA accumulates hi*hi + hi*lo + lo*hi in fp32 TMEM
 // (relative error ~1e-6, fp32 class; SURVEY.md §0.5 rules out 1xTF32/BF16).
-//
-// Roles: all 128 threads fill shared memory; thread 0 issues the MMAs and
-// commits them to an mbarrier; the 4 warps then read their 32 TMEM lanes
-// (tcgen05.ld) and run the fused epilogue (bias, softplus, encoder/skip
-// addend, residual).  CTAs are persistent over tiles; weights stay resident.
 #include <cstdio>
 
 #include "common.cuh"
@@ -28,8 +29,9 @@
 namespace hs {
 namespace {
 
-constexpr int kTcThreads = 128;
-constexpr int kM = 128;  // pixels per tile (UMMA M)
+constexpr int kNT = 256;  // threads per CTA (8 warps)
+constexpr int kM = 128;   // pixels per tile (UMMA M)
+constexpr int kBand = 32; // output rows per work unit
 
 HS_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -90,16 +92,14 @@ HS_DEV void split3(float4 v, uint4& hi, uint4& lo) {
   lo.w = tf32_rna(v.w - __uint_as_float(hi.w));
 }
 
-HS_DEV void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
+HS_DEV void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 HS_DEV float softplus_f(float x) { return fmaxf(x, 0.f) + log1pf(expf(-fabsf(x))); }
@@ -124,218 +124,307 @@ struct TcArgs {
 // MODE 0: stride 1; MODE 1: stride 2; MODE 2: transposed stride 2 (out = 2 x in)
 template <int MODE>
 struct Geo {
-  static constexpr int NR = MODE == 2 ? 2 : 3;                 // staged input rows
-  static constexpr int RW = MODE == 0 ? kM + 2 : (MODE == 1 ? 2 * kM + 1 : kM + 1);  // pixels per row
-  static constexpr int XPL = NR * RW;                          // pixels per channel-chunk plane
-  static constexpr int NACC = MODE == 2 ? 2 : 1;               // accumulators (column-parity classes)
+  static constexpr int RW = MODE == 0 ? kM + 2 : (MODE == 1 ? 2 * kM + 1 : kM + 1);  // pixels per staged row
+  static constexpr int NS = MODE == 0 ? 4 : (MODE == 1 ? 5 : 3);                     // ring slots
+  static constexpr int NACC = MODE == 2 ? 2 : 1;  // accumulators per tile (column-parity classes)
 };
 
 template <int CIN, int COUT, int MODE>
-struct Smem {
-  static constexpr int KCH = CIN / 4;
+struct Cfg {
+  static constexpr int KCH = CIN / 4;                                    // 16-byte channel chunks
+  static constexpr int XPL = Geo<MODE>::NS * Geo<MODE>::RW;              // pixels per chunk plane
   static constexpr size_t W_BYTES = (size_t)9 * KCH * COUT * 16;
-  static constexpr size_t X_BYTES = (size_t)KCH * Geo<MODE>::XPL * 16;
+  static constexpr size_t X_BYTES = (size_t)KCH * XPL * 16;
   static constexpr size_t TOTAL = 2 * W_BYTES + 2 * X_BYTES + 64;
+  static constexpr int EPT = (Geo<MODE>::RW * KCH + kNT - 1) / kNT;     // row elements per thread
+  static constexpr int ACOLS = COUT * Geo<MODE>::NACC;                   // TMEM columns per accumulator
+  static constexpr int NCOLS_RAW = 2 * ACOLS;
+  static constexpr int NCOLS = NCOLS_RAW <= 32 ? 32 : (NCOLS_RAW <= 64 ? 64 : (NCOLS_RAW <= 128 ? 128 : 256));
+};
+
+// input column of staged pixel p in a row of column block xb
+template <int MODE>
+HS_DEV int stage_col(int xb, int p) {
+  if (MODE == 0) return xb * kM - 1 + p;
+  if (MODE == 1) return p < kM ? 2 * (xb * kM + p) : 2 * (xb * kM + (p - kM)) - 1;
+  return xb * kM + p;
+}
+
+template <int CIN, int COUT, int MODE>
+struct RowPrefetch {
+  float4 v[Cfg<CIN, COUT, MODE>::EPT];
+  int gy;
 };
 
 template <int CIN, int COUT, int MODE>
-__global__ void __launch_bounds__(kTcThreads) k_conv_tc(TcArgs a) {
-  using G = Geo<MODE>;
-  using S = Smem<CIN, COUT, MODE>;
-  constexpr int KCH = S::KCH;
+HS_DEV void row_load(RowPrefetch<CIN, COUT, MODE>& pf, const float* xb_ptr, int H, int W, int xb, int gy) {
+  using C = Cfg<CIN, COUT, MODE>;
+  constexpr int RW = Geo<MODE>::RW;
+  pf.gy = gy;
+#pragma unroll
+  for (int i = 0; i < C::EPT; ++i) {
+    const int e = threadIdx.x + i * kNT;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (e < RW * C::KCH) {
+      const int c = e / RW, p = e - c * RW;
+      const int gx = stage_col<MODE>(xb, p);
+      if (gy >= 0 && gy < H && gx >= 0 && gx < W)
+        v = __ldg(reinterpret_cast<const float4*>(xb_ptr + ((size_t)gy * W + gx) * CIN + 4 * c));
+    }
+    pf.v[i] = v;
+  }
+}
+
+template <int CIN, int COUT, int MODE>
+HS_DEV void row_store(const RowPrefetch<CIN, COUT, MODE>& pf, unsigned char* x_hi, unsigned char* x_lo) {
+  using C = Cfg<CIN, COUT, MODE>;
+  constexpr int RW = Geo<MODE>::RW, NS = Geo<MODE>::NS;
+  const int slot = ((pf.gy % NS) + NS) % NS;
+#pragma unroll
+  for (int i = 0; i < C::EPT; ++i) {
+    const int e = threadIdx.x + i * kNT;
+    if (e < RW * C::KCH) {
+      const int c = e / RW, p = e - c * RW;
+      uint4 hi, lo;
+      split3(pf.v[i], hi, lo);
+      const size_t off = ((size_t)c * C::XPL + slot * RW + p) * 16;
+      *reinterpret_cast<uint4*>(x_hi + off) = hi;
+      *reinterpret_cast<uint4*>(x_lo + off) = lo;
+    }
+  }
+}
+
+// input rows a tile needs: [lo, hi]
+template <int MODE>
+HS_DEV void tile_rows(int oy, int& lo, int& hi) {
+  if (MODE == 0) {
+    lo = oy - 1;
+    hi = oy + 1;
+  } else if (MODE == 1) {
+    lo = 2 * oy - 1;
+    hi = 2 * oy + 1;
+  } else {
+    lo = oy >> 1;
+    hi = (oy >> 1) + 1;
+  }
+}
+
+template <int CIN, int COUT, int MODE>
+HS_DEV void issue_mmas(int oy, uint32_t d0, uint32_t xh, uint32_t xl, uint32_t wh, uint32_t wl) {
+  using C = Cfg<CIN, COUT, MODE>;
+  constexpr int RW = Geo<MODE>::RW, NS = Geo<MODE>::NS;
+  constexpr uint32_t X_LBO = C::XPL * 16, W_LBO = COUT * 16;
+  constexpr uint32_t IDESC = idesc_tf32(kM, COUT);
+  auto slot_of = [](int gy) { return ((gy % NS) + NS) % NS; };
+  for (int acc = 0; acc < Geo<MODE>::NACC; ++acc) {
+    const uint32_t d = d0 + acc * COUT;
+    uint32_t first = 1;
+    for (int ky = 0; ky < 3; ++ky) {
+      for (int kx = 0; kx < 3; ++kx) {
+        int gy, px;  // staged input row and pixel offset feeding this tap
+        if (MODE == 0) {
+          gy = oy - 1 + ky;
+          px = kx;
+        } else if (MODE == 1) {
+          gy = 2 * oy - 1 + ky;
+          px = kx == 1 ? 0 : (kx == 0 ? kM : kM + 1);
+        } else {
+          // out row 2q: ky = 1 at row q; out row 2q+1: ky = 0 at q+1, ky = 2 at q
+          // out col 2q (acc 0): kx = 1 at q; out col 2q+1 (acc 1): kx = 0 at q+1, kx = 2 at q
+          const int py = oy & 1, q = oy >> 1;
+          if (py == 0 && ky != 1) continue;
+          if (py == 1 && ky == 1) continue;
+          if (acc == 0 && kx != 1) continue;
+          if (acc == 1 && kx == 1) continue;
+          gy = (py && ky == 0) ? q + 1 : q;
+          px = (acc && kx == 0) ? 1 : 0;
+        }
+        const uint32_t xo = (uint32_t)(slot_of(gy) * RW + px) * 16;
+        const uint32_t wo = (uint32_t)((ky * 3 + kx) * C::KCH * COUT * 16);
+#pragma unroll
+        for (int kk = 0; kk < C::KCH / 2; ++kk) {
+          const uint32_t xk = xo + kk * 2 * X_LBO, wk = wo + kk * 2 * W_LBO;
+          const uint64_t ah = umma_desc(xh + xk, X_LBO, 128), al = umma_desc(xl + xk, X_LBO, 128);
+          const uint64_t bh = umma_desc(wh + wk, W_LBO, 128), bl = umma_desc(wl + wk, W_LBO, 128);
+          mma_tf32(d, ah, bh, IDESC, first ? 0u : 1u);
+          first = 0;
+          mma_tf32(d, ah, bl, IDESC, 1u);
+          mma_tf32(d, al, bh, IDESC, 1u);
+        }
+      }
+    }
+  }
+}
+
+// warp w drains TMEM lane quarter (w % 4) (= tile pixels 32(w%4) + lane), column half (w / 4)
+template <int CIN, int COUT, int MODE>
+HS_DEV void epilogue(const TcArgs& a, uint32_t d0, int b, int oy, int xb) {
+  constexpr int HALF = COUT / 2;  // 8, 16, 32 or 64 columns per warp
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int m = quarter * 32 + lane;
+  const float* add =
+      a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[b] : 0) : b) * a.addend_bstride : nullptr;
+  for (int acc = 0; acc < Geo<MODE>::NACC; ++acc) {
+    const int ox = MODE == 2 ? 2 * (xb * kM + m) + acc : xb * kM + m;
+    const size_t pix = (size_t)oy * a.Wo + ox;
+    const size_t obase = (size_t)b * a.Ho * a.Wo * COUT + pix * COUT;
+#pragma unroll
+    for (int n0 = half * HALF; n0 < (half + 1) * HALF; n0 += 8) {
+      float4 ad[2], rs[2];
+      if (add) {
+        ad[0] = __ldg(reinterpret_cast<const float4*>(add + pix * COUT + n0));
+        ad[1] = __ldg(reinterpret_cast<const float4*>(add + pix * COUT + n0 + 4));
+      }
+      if (a.residual) {
+        rs[0] = __ldg(reinterpret_cast<const float4*>(a.residual + obase + n0));
+        rs[1] = __ldg(reinterpret_cast<const float4*>(a.residual + obase + n0 + 4));
+      }
+      float v[8];
+      tmem_ld8(d0 + ((uint32_t)(quarter * 32) << 16) + acc * COUT + n0, v);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        float t = v[u] + __ldg(a.bias + n0 + u);
+        if (a.softplus) t = softplus_f(t);
+        if (add) t += (&ad[u >> 2].x)[u & 3];
+        if (a.residual) t += (&rs[u >> 2].x)[u & 3];
+        v[u] = t;
+      }
+      *reinterpret_cast<float4*>(a.y + obase + n0) = make_float4(v[0], v[1], v[2], v[3]);
+      *reinterpret_cast<float4*>(a.y + obase + n0 + 4) = make_float4(v[4], v[5], v[6], v[7]);
+    }
+  }
+}
+
+template <int CIN, int COUT, int MODE>
+__global__ void __launch_bounds__(kNT) k_conv_tc(TcArgs a) {
+  using C = Cfg<CIN, COUT, MODE>;
+  constexpr int KCH = C::KCH;
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* w_hi = smem;
-  unsigned char* w_lo = smem + S::W_BYTES;
-  unsigned char* x_hi = smem + 2 * S::W_BYTES;
-  unsigned char* x_lo = x_hi + S::X_BYTES;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(x_lo + S::X_BYTES);
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(mbar + 1);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  unsigned char* w_lo = smem + C::W_BYTES;
+  unsigned char* x_hi = smem + 2 * C::W_BYTES;
+  unsigned char* x_lo = x_hi + C::X_BYTES;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(x_lo + C::X_BYTES);  // [2]
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(mbar + 2);
+  const int tid = threadIdx.x, warp = tid >> 5;
 
   // ---- weights: [cout][tap][cin] fp32 -> hi/lo tf32, layout (tap, chunk, n) x 16 B
-  for (int e = tid; e < 9 * KCH * COUT; e += kTcThreads) {
+  for (int e = tid; e < 9 * KCH * COUT; e += kNT) {
     const int n = e % COUT, c = (e / COUT) % KCH, t = e / (COUT * KCH);
-    const float4 v = *reinterpret_cast<const float4*>(a.w + ((size_t)n * 9 + t) * CIN + 4 * c);
+    const float4 v = __ldg(reinterpret_cast<const float4*>(a.w + ((size_t)n * 9 + t) * CIN + 4 * c));
     uint4 hi, lo;
     split3(v, hi, lo);
     const size_t off = ((size_t)(t * KCH + c) * COUT + n) * 16;
     *reinterpret_cast<uint4*>(w_hi + off) = hi;
     *reinterpret_cast<uint4*>(w_lo + off) = lo;
   }
-  constexpr int NCOLS_RAW = COUT * G::NACC;
-  constexpr int NCOLS = NCOLS_RAW <= 32 ? 32 : (NCOLS_RAW <= 64 ? 64 : (NCOLS_RAW <= 128 ? 128 : 256));
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
-                 "r"(NCOLS));
+                 "r"(C::NCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid == 0) mbar_init(smem_u32(mbar), 1);
+  if (tid == 0) {
+    mbar_init(smem_u32(&mbar[0]), 1);
+    mbar_init(smem_u32(&mbar[1]), 1);
+  }
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
-  constexpr uint32_t IDESC = idesc_tf32(kM, COUT);
-  uint32_t phase = 0;
+  const uint32_t xh = smem_u32(x_hi), xl = smem_u32(x_lo), wh = smem_u32(w_hi), wl = smem_u32(w_lo);
+  uint32_t phase[2] = {0u, 0u};
 
-  // tiles: MODE 0/1 -> (b, oy, x-block of kM outputs); MODE 2 -> (b, oy, q-block of kM inputs)
   const int xblocks = MODE == 2 ? a.W / kM : a.Wo / kM;
-  const long long ntiles = (long long)a.B * a.Ho * xblocks;
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int xb = (int)(tile % xblocks);
-    const int oy = (int)((tile / xblocks) % a.Ho);
-    const int b = (int)(tile / ((long long)xblocks * a.Ho));
+  const int nbands = (a.Ho + kBand - 1) / kBand;
+  const long long nunits = (long long)a.B * xblocks * nbands;
+  for (long long unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
+    const int xb = (int)(unit % xblocks);
+    const int band = (int)((unit / xblocks) % nbands);
+    const int b = (int)(unit / ((long long)xblocks * nbands));
     if (a.active && a.active[b] == nullptr) continue;  // uniform per CTA
     const float* xb_ptr = a.x + (size_t)b * a.H * a.W * CIN;
-    // ---- stage input rows (hi/lo) in the interleaved layout
-    for (int e = tid; e < KCH * G::XPL; e += kTcThreads) {
-      const int P = e % G::XPL, c = e / G::XPL;
-      const int r = P / G::RW, p = P % G::RW;
-      int gy, gx;
-      if (MODE == 0) {
-        gy = oy - 1 + r;
-        gx = xb * kM - 1 + p;
-      } else if (MODE == 1) {
-        gy = 2 * oy - 1 + r;
-        gx = p < kM ? 2 * (xb * kM + p) : 2 * (xb * kM + (p - kM)) - 1;
-      } else {
-        gy = (oy >> 1) + r;
-        gx = xb * kM + p;
-      }
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W)
-        v = *reinterpret_cast<const float4*>(xb_ptr + ((size_t)gy * a.W + gx) * CIN + 4 * c);
-      uint4 hi, lo;
-      split3(v, hi, lo);
-      const size_t off = ((size_t)c * G::XPL + P) * 16;
-      *reinterpret_cast<uint4*>(x_hi + off) = hi;
-      *reinterpret_cast<uint4*>(x_lo + off) = lo;
+    const int oy0 = band * kBand, oy1 = min(a.Ho, oy0 + kBand);
+    // prologue: stage every input row of the first tile
+    int lo, hi;
+    tile_rows<MODE>(oy0, lo, hi);
+    for (int gy = lo; gy <= hi; ++gy) {
+      RowPrefetch<CIN, COUT, MODE> pf;
+      row_load<CIN, COUT, MODE>(pf, xb_ptr, a.H, a.W, xb, gy);
+      row_store<CIN, COUT, MODE>(pf, x_hi, x_lo);
     }
+    int staged_hi = hi;
     fence_async_smem();
-    __syncthreads();
-    // ---- MMAs (one thread)
-    if (tid == 0) {
-      tc_fence_after();
-      const uint32_t xh = smem_u32(x_hi), xl = smem_u32(x_lo), wh = smem_u32(w_hi), wl = smem_u32(w_lo);
-      constexpr uint32_t X_LBO = G::XPL * 16, W_LBO = COUT * 16;
-      for (int acc = 0; acc < G::NACC; ++acc) {
-        uint32_t first = 1;
-        const int py = oy & 1;
-        // tap list of this accumulator: (ky, kx, input pixel offset in the staged rows)
-        int nt = 0, tky[9], tkx[9], toff[9];
-        if (MODE == 0) {
-          for (int ky = 0; ky < 3; ++ky)
-            for (int kx = 0; kx < 3; ++kx) {
-              tky[nt] = ky;
-              tkx[nt] = kx;
-              toff[nt++] = ky * G::RW + kx;
-            }
-        } else if (MODE == 1) {
-          for (int ky = 0; ky < 3; ++ky)
-            for (int kx = 0; kx < 3; ++kx) {
-              tky[nt] = ky;
-              tkx[nt] = kx;
-              toff[nt++] = ky * G::RW + (kx == 1 ? 0 : (kx == 0 ? kM : kM + 1));
-            }
-        } else {
-          // rows: py = 0 -> ky = 1 at row qy (r = 0); py = 1 -> ky = 0 at qy+1 (r = 1), ky = 2 at qy (r = 0)
-          // cols: px = 0 -> kx = 1 at q; px = 1 -> kx = 0 at q+1, kx = 2 at q
-          const int nky = py ? 2 : 1, nkx = acc ? 2 : 1;
-          for (int i = 0; i < nky; ++i)
-            for (int j = 0; j < nkx; ++j) {
-              const int ky = py ? (i ? 2 : 0) : 1, r = (py && !i) ? 1 : 0;
-              const int kx = acc ? (j ? 2 : 0) : 1, dx = (acc && !j) ? 1 : 0;
-              tky[nt] = ky;
-              tkx[nt] = kx;
-              toff[nt++] = r * G::RW + dx;
-            }
-        }
-        const uint32_t d = tmem + acc * COUT;
-        for (int t = 0; t < nt; ++t) {
-          const int tap = tky[t] * 3 + tkx[t];
-          const uint32_t xo = toff[t] * 16, wo = tap * KCH * COUT * 16;
-#pragma unroll
-          for (int kk = 0; kk < KCH / 2; ++kk) {
-            const uint32_t xk = xo + kk * 2 * X_LBO, wk = wo + kk * 2 * W_LBO;
-            const uint64_t ah = umma_desc(xh + xk, X_LBO, 128), al = umma_desc(xl + xk, X_LBO, 128);
-            const uint64_t bh = umma_desc(wh + wk, W_LBO, 128), bl = umma_desc(wl + wk, W_LBO, 128);
-            mma_tf32(d, ah, bh, IDESC, first ? 0u : 1u);
-            first = 0;
-            mma_tf32(d, ah, bl, IDESC, 1u);
-            mma_tf32(d, al, bh, IDESC, 1u);
-          }
-        }
-      }
-      mma_commit(smem_u32(mbar));
-    }
-    mbar_wait(smem_u32(mbar), phase);
-    phase ^= 1u;
-    tc_fence_after();
-    // ---- epilogue: warp w owns TMEM lanes / tile pixels [32w, 32w + 32)
-    const int m = warp * 32 + lane;
-    const float* add = a.addend
-                           ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[b] : 0) : b) * a.addend_bstride
-                           : nullptr;
-    for (int acc = 0; acc < G::NACC; ++acc) {
-      const int ox = MODE == 2 ? 2 * (xb * kM + m) + acc : xb * kM + m;
-      const size_t pix = (size_t)oy * a.Wo + ox;
-      const size_t obase = (size_t)b * a.Ho * a.Wo * COUT + pix * COUT;
-#pragma unroll
-      for (int n0 = 0; n0 < COUT; n0 += 16) {
-        float v[16];
-        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + acc * COUT + n0, v);
-#pragma unroll
-        for (int q = 0; q < 16; q += 4) {
-          float4 o;
-          float* po = &o.x;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            float t = v[q + u] + a.bias[n0 + q + u];
-            if (a.softplus) t = softplus_f(t);
-            po[u] = t;
-          }
-          if (add) {
-            const float4 ad = *reinterpret_cast<const float4*>(add + pix * COUT + n0 + q);
-            o.x += ad.x;
-            o.y += ad.y;
-            o.z += ad.z;
-            o.w += ad.w;
-          }
-          if (a.residual) {
-            const float4 rs = *reinterpret_cast<const float4*>(a.residual + obase + n0 + q);
-            o.x += rs.x;
-            o.y += rs.y;
-            o.z += rs.z;
-            o.w += rs.w;
-          }
-          *reinterpret_cast<float4*>(a.y + obase + n0 + q) = o;
-        }
-      }
-    }
     tc_fence_before();
-    __syncthreads();  // TMEM and staged rows are free for the next tile
+    __syncthreads();
+    for (int oy = oy0; oy < oy1; ++oy) {
+      const int t = oy - oy0, s = t & 1;
+      // (A) MMAs of row oy into accumulator s
+      if (tid == 0) {
+        tc_fence_after();
+        issue_mmas<CIN, COUT, MODE>(oy, tmem + s * C::ACOLS, xh, xl, wh, wl);
+        mma_commit(smem_u32(&mbar[s]));
+      }
+      // (B) prefetch the new input rows of row oy+1 (at most two)
+      RowPrefetch<CIN, COUT, MODE> pf0, pf1;
+      int nnew = 0;
+      if (oy + 1 < oy1) {
+        tile_rows<MODE>(oy + 1, lo, hi);
+        if (hi > staged_hi) {
+          row_load<CIN, COUT, MODE>(pf0, xb_ptr, a.H, a.W, xb, staged_hi + 1);
+          nnew = 1;
+          if (hi > staged_hi + 1) {
+            row_load<CIN, COUT, MODE>(pf1, xb_ptr, a.H, a.W, xb, staged_hi + 2);
+            nnew = 2;
+          }
+        }
+      }
+      // (C) drain row oy-1 (its MMAs overlapped with (A)/(B))
+      if (t > 0) {
+        mbar_wait(smem_u32(&mbar[s ^ 1]), phase[s ^ 1]);
+        phase[s ^ 1] ^= 1u;
+        tc_fence_after();
+        epilogue<CIN, COUT, MODE>(a, tmem + (s ^ 1) * C::ACOLS, b, oy - 1, xb);
+      }
+      // (D) rows for oy+1 overwrite slots only rows <= oy-1's inputs used (their MMAs are complete)
+      if (nnew >= 1) row_store<CIN, COUT, MODE>(pf0, x_hi, x_lo);
+      if (nnew >= 2) row_store<CIN, COUT, MODE>(pf1, x_hi, x_lo);
+      staged_hi += nnew;
+      fence_async_smem();
+      tc_fence_before();
+      __syncthreads();
+    }
+    // drain the last row
+    const int tl = oy1 - 1 - oy0, sl = tl & 1;
+    mbar_wait(smem_u32(&mbar[sl]), phase[sl]);
+    phase[sl] ^= 1u;
+    tc_fence_after();
+    epilogue<CIN, COUT, MODE>(a, tmem + sl * C::ACOLS, b, oy1 - 1, xb);
+    tc_fence_before();
+    __syncthreads();
   }
   if (warp == 0) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NCOLS));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::NCOLS));
   }
 }
 
 template <int CIN, int COUT, int MODE>
 void launch_tc(const TcArgs& a, cudaStream_t st) {
-  using S = Smem<CIN, COUT, MODE>;
+  using C = Cfg<CIN, COUT, MODE>;
   static int grid_cap = 0;
   if (!grid_cap) {
-    cudaFuncSetAttribute(k_conv_tc<CIN, COUT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::TOTAL);
+    cudaFuncSetAttribute(k_conv_tc<CIN, COUT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::TOTAL);
     int per_sm = 0, sms = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_conv_tc<CIN, COUT, MODE>, kTcThreads, S::TOTAL);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_conv_tc<CIN, COUT, MODE>, kNT, C::TOTAL);
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
   const long long xblocks = MODE == 2 ? a.W / kM : a.Wo / kM;
-  const long long ntiles = (long long)a.B * a.Ho * xblocks;
-  const int grid = (int)(ntiles < grid_cap ? ntiles : grid_cap);
-  k_conv_tc<CIN, COUT, MODE><<<grid, kTcThreads, S::TOTAL, st>>>(a);
+  const long long nunits = (long long)a.B * xblocks * ((a.Ho + kBand - 1) / kBand);
+  const int grid = (int)(nunits < grid_cap ? nunits : grid_cap);
+  k_conv_tc<CIN, COUT, MODE><<<grid, kNT, C::TOTAL, st>>>(a);
 }
 
 }  // namespace
@@ -343,6 +432,7 @@ void launch_tc(const TcArgs& a, cudaStream_t st) {
 bool conv_tc_enabled = true;
 
 bool conv_tc_supported(int cin, int cout, int stride, int transposed, int H, int W, int Wo) {
+  (void)H;
   if (!conv_tc_enabled) return false;
   const int mode = transposed ? 2 : (stride == 2 ? 1 : 0);
   const int width = mode == 2 ? W : Wo;
@@ -350,7 +440,6 @@ bool conv_tc_supported(int cin, int cout, int stride, int transposed, int H, int
   if (mode == 0) return (cin == 16 && cout == 16) || (cin == 32 && cout == 32);
   if (mode == 1) return cin == 16 && cout == 32;
   return cin == 32 && cout == 16;
-  (void)H;
 }
 
 void conv_tc_launch(const float* x, int H, int W, int cin, float* y, int Ho, int Wo, int cout, int stride,
