@@ -12,16 +12,25 @@
 // convolution is split into its two column-parity classes (1 and 2 taps)
 // with two TMEM accumulators.
 //
-// Streaming: a CTA owns a band of output rows of one 128-pixel column block
-// and walks it top to bottom.  Input rows live in a ring of shared-memory
-// slots, so each input row is loaded and split once per band (one new row per
-// output row at stride 1).  The MMAs of row t run while the CTA prefetches the
-// rows of t+1 and drains row t-1's accumulator (two TMEM accumulators).
+// Warp-specialised pipeline (one persistent CTA per SM, weights resident):
+//   warp 6 (1 lane)  producer : cp.async.bulk of raw NHWC input rows into a
+//                               ring of raw slots (mbarrier tx-count)
+//   warps 4-5        converters: raw fp32 -> tf32 hi/lo split, re-laid out
+//                               into the staged ring (smem -> smem)
+//   warp 7 (1 lane)  MMA issuer: 3xTF32 tcgen05.mma per tile into one of
+//                               four TMEM accumulators; commits release
+//                               staged rows and hand accumulators on
+//   warps 0-3        epilogue  : tcgen05.ld of their TMEM lane quarter, then
+//                               bias, softplus, encoder/skip addend,
+//                               residual, NHWC stores
+// A CTA walks a band of output rows of one 128-pixel column block top to
+// bottom, so every input row is fetched and split once per band.
 //
 // Precision: every fp32 operand x is split into tf32 hi = rna(x) and
 // lo = rna(x - hi); the MMA accumulates hi*hi + hi*lo + lo*hi in fp32 TMEM
 // (relative error ~1e-6, fp32 class; SURVEY.md §0.5 rules out 1xTF32/BF16).
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "conv_tc.h"
@@ -29,9 +38,12 @@
 namespace hs {
 namespace {
 
-constexpr int kNT = 256;  // threads per CTA (8 warps)
+constexpr int kNT = 256;  // 8 warps
 constexpr int kM = 128;   // pixels per tile (UMMA M)
 constexpr int kBand = 32; // output rows per work unit
+constexpr int kNA = 4;    // TMEM accumulators in flight
+constexpr int kEpiWarps = 4, kCvtWarp0 = 4, kCvtWarps = 2, kProdWarp = 6, kMmaWarp = 7;
+constexpr int kCvtThreads = 32 * kCvtWarps;
 
 HS_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -70,7 +82,22 @@ HS_DEV void mbar_wait(uint32_t mbar, uint32_t phase) {
       "r"(phase));
 }
 
+HS_DEV void mbar_arrive(uint32_t mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar) : "memory");
+}
+
+HS_DEV void mbar_arrive_tx(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+
+HS_DEV void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+
 HS_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+HS_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 HS_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 HS_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -92,15 +119,12 @@ HS_DEV void split3(float4 v, uint4& hi, uint4& lo) {
   lo.w = tf32_rna(v.w - __uint_as_float(hi.w));
 }
 
-HS_DEV void tmem_ld8(uint32_t taddr, float (&v)[8]) {
-  uint32_t r[8];
+HS_DEV void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
+HS_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 HS_DEV float softplus_f(float x) { return fmaxf(x, 0.f) + log1pf(expf(-fabsf(x))); }
 
@@ -119,82 +143,32 @@ struct TcArgs {
   const float* residual;
   const void* const* active;
   int B;
+  int dbg;  // debug: bit0 no bulk copies, bit1 no MMAs, bit2 no TMEM loads
 };
 
 // MODE 0: stride 1; MODE 1: stride 2; MODE 2: transposed stride 2 (out = 2 x in)
-template <int MODE>
-struct Geo {
-  static constexpr int RW = MODE == 0 ? kM + 2 : (MODE == 1 ? 2 * kM + 1 : kM + 1);  // pixels per staged row
-  static constexpr int NS = MODE == 0 ? 4 : (MODE == 1 ? 5 : 3);                     // ring slots
-  static constexpr int NACC = MODE == 2 ? 2 : 1;  // accumulators per tile (column-parity classes)
-};
-
 template <int CIN, int COUT, int MODE>
 struct Cfg {
-  static constexpr int KCH = CIN / 4;                                    // 16-byte channel chunks
-  static constexpr int XPL = Geo<MODE>::NS * Geo<MODE>::RW;              // pixels per chunk plane
+  static constexpr int KCH = CIN / 4;                                              // 16-byte channel chunks
+  static constexpr int RW = MODE == 0 ? kM + 2 : (MODE == 1 ? 2 * kM + 1 : kM + 1); // pixels per staged row
+  static constexpr int NACC = MODE == 2 ? 2 : 1;  // accumulators per tile (column-parity classes)
+  // staged (split) ring and raw ring depths, sized to fit 227 KB
+  static constexpr int NS = (MODE == 0 && CIN == 16) ? 5 : (MODE == 1 ? 4 : 3);
+  static constexpr int NR = (MODE == 0 && CIN == 16) ? 4 : 2;
+  static constexpr int XPL0 = NS * RW;
+  static constexpr int XPL = XPL0 + ((9 - (XPL0 & 7)) & 7);  // == 1 mod 8: conflict-free chunk planes
+  static constexpr int RAW_BYTES = RW * CIN * 4;
   static constexpr size_t W_BYTES = (size_t)9 * KCH * COUT * 16;
   static constexpr size_t X_BYTES = (size_t)KCH * XPL * 16;
-  static constexpr size_t TOTAL = 2 * W_BYTES + 2 * X_BYTES + 64;
-  static constexpr int EPT = (Geo<MODE>::RW * KCH + kNT - 1) / kNT;     // row elements per thread
-  static constexpr int ACOLS = COUT * Geo<MODE>::NACC;                   // TMEM columns per accumulator
-  static constexpr int NCOLS_RAW = 2 * ACOLS;
+  static constexpr size_t R_BYTES = (size_t)NR * RAW_BYTES;
+  static constexpr int NBAR = 2 * NR + 2 * NS + 2 * kNA;
+  static constexpr size_t TOTAL = 2 * W_BYTES + 2 * X_BYTES + R_BYTES + 8 * NBAR + 16;
+  static constexpr int ACOLS = COUT * NACC;  // TMEM columns per accumulator
+  static constexpr int NCOLS_RAW = kNA * ACOLS;
   static constexpr int NCOLS = NCOLS_RAW <= 32 ? 32 : (NCOLS_RAW <= 64 ? 64 : (NCOLS_RAW <= 128 ? 128 : 256));
 };
 
-// input column of staged pixel p in a row of column block xb
-template <int MODE>
-HS_DEV int stage_col(int xb, int p) {
-  if (MODE == 0) return xb * kM - 1 + p;
-  if (MODE == 1) return p < kM ? 2 * (xb * kM + p) : 2 * (xb * kM + (p - kM)) - 1;
-  return xb * kM + p;
-}
-
-template <int CIN, int COUT, int MODE>
-struct RowPrefetch {
-  float4 v[Cfg<CIN, COUT, MODE>::EPT];
-  int gy;
-};
-
-template <int CIN, int COUT, int MODE>
-HS_DEV void row_load(RowPrefetch<CIN, COUT, MODE>& pf, const float* xb_ptr, int H, int W, int xb, int gy) {
-  using C = Cfg<CIN, COUT, MODE>;
-  constexpr int RW = Geo<MODE>::RW;
-  pf.gy = gy;
-#pragma unroll
-  for (int i = 0; i < C::EPT; ++i) {
-    const int e = threadIdx.x + i * kNT;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (e < RW * C::KCH) {
-      const int c = e / RW, p = e - c * RW;
-      const int gx = stage_col<MODE>(xb, p);
-      if (gy >= 0 && gy < H && gx >= 0 && gx < W)
-        v = __ldg(reinterpret_cast<const float4*>(xb_ptr + ((size_t)gy * W + gx) * CIN + 4 * c));
-    }
-    pf.v[i] = v;
-  }
-}
-
-template <int CIN, int COUT, int MODE>
-HS_DEV void row_store(const RowPrefetch<CIN, COUT, MODE>& pf, unsigned char* x_hi, unsigned char* x_lo) {
-  using C = Cfg<CIN, COUT, MODE>;
-  constexpr int RW = Geo<MODE>::RW, NS = Geo<MODE>::NS;
-  const int slot = ((pf.gy % NS) + NS) % NS;
-#pragma unroll
-  for (int i = 0; i < C::EPT; ++i) {
-    const int e = threadIdx.x + i * kNT;
-    if (e < RW * C::KCH) {
-      const int c = e / RW, p = e - c * RW;
-      uint4 hi, lo;
-      split3(pf.v[i], hi, lo);
-      const size_t off = ((size_t)c * C::XPL + slot * RW + p) * 16;
-      *reinterpret_cast<uint4*>(x_hi + off) = hi;
-      *reinterpret_cast<uint4*>(x_lo + off) = lo;
-    }
-  }
-}
-
-// input rows a tile needs: [lo, hi]
+// input rows a tile (output row oy) needs: [lo, hi]
 template <int MODE>
 HS_DEV void tile_rows(int oy, int& lo, int& hi) {
   if (MODE == 0) {
@@ -209,107 +183,128 @@ HS_DEV void tile_rows(int oy, int& lo, int& hi) {
   }
 }
 
+// first input column of the raw row segment of column block xb
+template <int MODE>
+HS_DEV int raw_x0(int xb) {
+  return MODE == 0 ? xb * kM - 1 : (MODE == 1 ? 2 * xb * kM - 1 : xb * kM);
+}
+
+// raw pixel p -> staged pixel (stride 2 de-interleaves even / odd columns)
+template <int MODE>
+HS_DEV int staged_px(int p) {
+  if (MODE != 1) return p;
+  return (p & 1) ? (p - 1) >> 1 : kM + (p >> 1);  // col 2x0-1+p: odd p -> even col
+}
+
+struct Unit {
+  int b, xb, oy0, oy1, glo, ghi;  // rows [oy0, oy1), input rows [glo, ghi]
+};
+
+template <int MODE>
+HS_DEV bool unit_at(const TcArgs& a, long long u, Unit& U) {
+  const int xblocks = MODE == 2 ? a.W / kM : a.Wo / kM;
+  const int nbands = (a.Ho + kBand - 1) / kBand;
+  U.xb = (int)(u % xblocks);
+  const int band = (int)((u / xblocks) % nbands);
+  U.b = (int)(u / ((long long)xblocks * nbands));
+  U.oy0 = band * kBand;
+  U.oy1 = min(a.Ho, U.oy0 + kBand);
+  int lo, hi;
+  tile_rows<MODE>(U.oy0, lo, hi);
+  U.glo = lo;
+  tile_rows<MODE>(U.oy1 - 1, lo, hi);
+  U.ghi = hi;
+  return !(a.active && a.active[U.b] == nullptr);
+}
+
+template <int MODE>
+__host__ __device__ inline long long num_units(const TcArgs& a) {
+  const int xblocks = MODE == 2 ? a.W / kM : a.Wo / kM;
+  return (long long)a.B * xblocks * ((a.Ho + kBand - 1) / kBand);
+}
+
+// Descriptor bases (the start-address field is in 16-byte units in the low
+// bits, so moving a window is a 64-bit add of offset >> 4).
+struct DescBase {
+  uint64_t xh, xl, wh, wl;
+};
+
 template <int CIN, int COUT, int MODE>
-HS_DEV void issue_mmas(int oy, uint32_t d0, uint32_t xh, uint32_t xl, uint32_t wh, uint32_t wl) {
+HS_DEV void tap_mmas(uint32_t d, const DescBase& db, uint32_t x_units, uint32_t w_units, uint32_t& first) {
   using C = Cfg<CIN, COUT, MODE>;
-  constexpr int RW = Geo<MODE>::RW, NS = Geo<MODE>::NS;
-  constexpr uint32_t X_LBO = C::XPL * 16, W_LBO = COUT * 16;
+  constexpr uint32_t X_STEP = 2 * C::XPL, W_STEP = 2 * COUT;  // two 16-byte chunks per K step
   constexpr uint32_t IDESC = idesc_tf32(kM, COUT);
-  auto slot_of = [](int gy) { return ((gy % NS) + NS) % NS; };
-  for (int acc = 0; acc < Geo<MODE>::NACC; ++acc) {
-    const uint32_t d = d0 + acc * COUT;
-    uint32_t first = 1;
-    for (int ky = 0; ky < 3; ++ky) {
-      for (int kx = 0; kx < 3; ++kx) {
-        int gy, px;  // staged input row and pixel offset feeding this tap
-        if (MODE == 0) {
-          gy = oy - 1 + ky;
-          px = kx;
-        } else if (MODE == 1) {
-          gy = 2 * oy - 1 + ky;
-          px = kx == 1 ? 0 : (kx == 0 ? kM : kM + 1);
-        } else {
-          // out row 2q: ky = 1 at row q; out row 2q+1: ky = 0 at q+1, ky = 2 at q
-          // out col 2q (acc 0): kx = 1 at q; out col 2q+1 (acc 1): kx = 0 at q+1, kx = 2 at q
-          const int py = oy & 1, q = oy >> 1;
-          if (py == 0 && ky != 1) continue;
-          if (py == 1 && ky == 1) continue;
-          if (acc == 0 && kx != 1) continue;
-          if (acc == 1 && kx == 1) continue;
-          gy = (py && ky == 0) ? q + 1 : q;
-          px = (acc && kx == 0) ? 1 : 0;
-        }
-        const uint32_t xo = (uint32_t)(slot_of(gy) * RW + px) * 16;
-        const uint32_t wo = (uint32_t)((ky * 3 + kx) * C::KCH * COUT * 16);
 #pragma unroll
-        for (int kk = 0; kk < C::KCH / 2; ++kk) {
-          const uint32_t xk = xo + kk * 2 * X_LBO, wk = wo + kk * 2 * W_LBO;
-          const uint64_t ah = umma_desc(xh + xk, X_LBO, 128), al = umma_desc(xl + xk, X_LBO, 128);
-          const uint64_t bh = umma_desc(wh + wk, W_LBO, 128), bl = umma_desc(wl + wk, W_LBO, 128);
-          mma_tf32(d, ah, bh, IDESC, first ? 0u : 1u);
-          first = 0;
-          mma_tf32(d, ah, bl, IDESC, 1u);
-          mma_tf32(d, al, bh, IDESC, 1u);
-        }
-      }
-    }
+  for (int kk = 0; kk < C::KCH / 2; ++kk) {
+    const uint64_t xo = x_units + kk * X_STEP, wo = w_units + kk * W_STEP;
+    mma_tf32(d, db.xh + xo, db.wh + wo, IDESC, first ? 0u : 1u);
+    first = 0;
+    mma_tf32(d, db.xh + xo, db.wl + wo, IDESC, 1u);
+    mma_tf32(d, db.xl + xo, db.wh + wo, IDESC, 1u);
   }
 }
 
-// warp w drains TMEM lane quarter (w % 4) (= tile pixels 32(w%4) + lane), column half (w / 4)
-template <int CIN, int COUT, int MODE>
-HS_DEV void epilogue(const TcArgs& a, uint32_t d0, int b, int oy, int xb) {
-  constexpr int HALF = COUT / 2;  // 8, 16, 32 or 64 columns per warp
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int quarter = warp & 3, half = warp >> 2;
-  const int m = quarter * 32 + lane;
-  const float* add =
-      a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[b] : 0) : b) * a.addend_bstride : nullptr;
-  for (int acc = 0; acc < Geo<MODE>::NACC; ++acc) {
-    const int ox = MODE == 2 ? 2 * (xb * kM + m) + acc : xb * kM + m;
-    const size_t pix = (size_t)oy * a.Wo + ox;
-    const size_t obase = (size_t)b * a.Ho * a.Wo * COUT + pix * COUT;
-#pragma unroll
-    for (int n0 = half * HALF; n0 < (half + 1) * HALF; n0 += 8) {
-      float4 ad[2], rs[2];
-      if (add) {
-        ad[0] = __ldg(reinterpret_cast<const float4*>(add + pix * COUT + n0));
-        ad[1] = __ldg(reinterpret_cast<const float4*>(add + pix * COUT + n0 + 4));
-      }
-      if (a.residual) {
-        rs[0] = __ldg(reinterpret_cast<const float4*>(a.residual + obase + n0));
-        rs[1] = __ldg(reinterpret_cast<const float4*>(a.residual + obase + n0 + 4));
-      }
-      float v[8];
-      tmem_ld8(d0 + ((uint32_t)(quarter * 32) << 16) + acc * COUT + n0, v);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        float t = v[u] + __ldg(a.bias + n0 + u);
-        if (a.softplus) t = softplus_f(t);
-        if (add) t += (&ad[u >> 2].x)[u & 3];
-        if (a.residual) t += (&rs[u >> 2].x)[u & 3];
-        v[u] = t;
-      }
-      *reinterpret_cast<float4*>(a.y + obase + n0) = make_float4(v[0], v[1], v[2], v[3]);
-      *reinterpret_cast<float4*>(a.y + obase + n0 + 4) = make_float4(v[4], v[5], v[6], v[7]);
-    }
-  }
-}
-
-template <int CIN, int COUT, int MODE>
-__global__ void __launch_bounds__(kNT) k_conv_tc(TcArgs a) {
+// all MMAs of output row oy; slot(g) = staged slot holding input row g
+template <int CIN, int COUT, int MODE, typename SlotOf>
+HS_DEV void issue_mmas(int oy, uint32_t d0, const DescBase& db, SlotOf slot) {
   using C = Cfg<CIN, COUT, MODE>;
-  constexpr int KCH = C::KCH;
+  constexpr uint32_t WT = C::KCH * COUT;  // weight units per tap
+  auto row_units = [&](int g) { return (uint32_t)(slot(g) * C::RW); };
+  uint32_t first = 1;
+  if (MODE == 0 || MODE == 1) {
+    const int g0 = MODE == 0 ? oy - 1 : 2 * oy - 1;
+#pragma unroll
+    for (int ky = 0; ky < 3; ++ky) {
+      const uint32_t r = row_units(g0 + ky);
+#pragma unroll
+      for (int kx = 0; kx < 3; ++kx) {
+        const uint32_t px = MODE == 0 ? kx : (kx == 1 ? 0 : (kx == 0 ? kM : kM + 1));
+        tap_mmas<CIN, COUT, MODE>(d0, db, r + px, (ky * 3 + kx) * WT, first);
+      }
+    }
+    return;
+  }
+  // transposed: out row 2q <- (ky 1, row q); out row 2q+1 <- (ky 0, row q+1), (ky 2, row q)
+  //             out col 2q (acc 0) <- (kx 1, q); out col 2q+1 (acc 1) <- (kx 0, q+1), (kx 2, q)
+  const int q = oy >> 1;
+  const uint32_t rq = row_units(q), rq1 = row_units(q + 1);
+  if ((oy & 1) == 0) {
+    tap_mmas<CIN, COUT, MODE>(d0, db, rq, (1 * 3 + 1) * WT, first);
+    first = 1;
+    tap_mmas<CIN, COUT, MODE>(d0 + COUT, db, rq + 1, (1 * 3 + 0) * WT, first);
+    tap_mmas<CIN, COUT, MODE>(d0 + COUT, db, rq, (1 * 3 + 2) * WT, first);
+  } else {
+    tap_mmas<CIN, COUT, MODE>(d0, db, rq1, (0 * 3 + 1) * WT, first);
+    tap_mmas<CIN, COUT, MODE>(d0, db, rq, (2 * 3 + 1) * WT, first);
+    first = 1;
+    tap_mmas<CIN, COUT, MODE>(d0 + COUT, db, rq1 + 1, (0 * 3 + 0) * WT, first);
+    tap_mmas<CIN, COUT, MODE>(d0 + COUT, db, rq1, (0 * 3 + 2) * WT, first);
+    tap_mmas<CIN, COUT, MODE>(d0 + COUT, db, rq + 1, (2 * 3 + 0) * WT, first);
+    tap_mmas<CIN, COUT, MODE>(d0 + COUT, db, rq, (2 * 3 + 2) * WT, first);
+  }
+}
+
+template <int CIN, int COUT, int MODE>
+__global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
+  using C = Cfg<CIN, COUT, MODE>;
+  constexpr int KCH = C::KCH, NS = C::NS, NR = C::NR;
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* w_hi = smem;
   unsigned char* w_lo = smem + C::W_BYTES;
   unsigned char* x_hi = smem + 2 * C::W_BYTES;
   unsigned char* x_lo = x_hi + C::X_BYTES;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(x_lo + C::X_BYTES);  // [2]
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(mbar + 2);
-  const int tid = threadIdx.x, warp = tid >> 5;
+  unsigned char* raw = x_lo + C::X_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(raw + C::R_BYTES);
+  uint64_t* raw_full = bars;
+  uint64_t* raw_empty = raw_full + NR;
+  uint64_t* stg_full = raw_empty + NR;
+  uint64_t* stg_empty = stg_full + NS;
+  uint64_t* acc_full = stg_empty + NS;
+  uint64_t* acc_empty = acc_full + kNA;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(acc_empty + kNA);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  // ---- weights: [cout][tap][cin] fp32 -> hi/lo tf32, layout (tap, chunk, n) x 16 B
+  // ---- setup: resident weights (hi/lo), barriers, TMEM
   for (int e = tid; e < 9 * KCH * COUT; e += kNT) {
     const int n = e % COUT, c = (e / COUT) % KCH, t = e / (COUT * KCH);
     const float4 v = __ldg(reinterpret_cast<const float4*>(a.w + ((size_t)n * 9 + t) * CIN + 4 * c));
@@ -319,92 +314,192 @@ __global__ void __launch_bounds__(kNT) k_conv_tc(TcArgs a) {
     *reinterpret_cast<uint4*>(w_hi + off) = hi;
     *reinterpret_cast<uint4*>(w_lo + off) = lo;
   }
-  if (warp == 0) {
+  if (tid == 0) {
+    for (int i = 0; i < NR; ++i) {
+      mbar_init(smem_u32(&raw_full[i]), 1);
+      mbar_init(smem_u32(&raw_empty[i]), kCvtThreads);
+    }
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(smem_u32(&stg_full[i]), kCvtThreads);
+      mbar_init(smem_u32(&stg_empty[i]), 1);
+    }
+    for (int i = 0; i < kNA; ++i) {
+      mbar_init(smem_u32(&acc_full[i]), 1);
+      mbar_init(smem_u32(&acc_empty[i]), 32 * kEpiWarps);
+    }
+    if (!(a.dbg & 16)) fence_mbar_init();
+  }
+  if (warp == 0 && !(a.dbg & 8)) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
                  "r"(C::NCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 0) {
-    mbar_init(smem_u32(&mbar[0]), 1);
-    mbar_init(smem_u32(&mbar[1]), 1);
   }
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
-  const uint32_t xh = smem_u32(x_hi), xl = smem_u32(x_lo), wh = smem_u32(w_hi), wl = smem_u32(w_lo);
-  uint32_t phase[2] = {0u, 0u};
+  const long long nunits = num_units<MODE>(a);
 
-  const int xblocks = MODE == 2 ? a.W / kM : a.Wo / kM;
-  const int nbands = (a.Ho + kBand - 1) / kBand;
-  const long long nunits = (long long)a.B * xblocks * nbands;
-  for (long long unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
-    const int xb = (int)(unit % xblocks);
-    const int band = (int)((unit / xblocks) % nbands);
-    const int b = (int)(unit / ((long long)xblocks * nbands));
-    if (a.active && a.active[b] == nullptr) continue;  // uniform per CTA
-    const float* xb_ptr = a.x + (size_t)b * a.H * a.W * CIN;
-    const int oy0 = band * kBand, oy1 = min(a.Ho, oy0 + kBand);
-    // prologue: stage every input row of the first tile
-    int lo, hi;
-    tile_rows<MODE>(oy0, lo, hi);
-    for (int gy = lo; gy <= hi; ++gy) {
-      RowPrefetch<CIN, COUT, MODE> pf;
-      row_load<CIN, COUT, MODE>(pf, xb_ptr, a.H, a.W, xb, gy);
-      row_store<CIN, COUT, MODE>(pf, x_hi, x_lo);
-    }
-    int staged_hi = hi;
-    fence_async_smem();
-    tc_fence_before();
-    __syncthreads();
-    for (int oy = oy0; oy < oy1; ++oy) {
-      const int t = oy - oy0, s = t & 1;
-      // (A) MMAs of row oy into accumulator s
-      if (tid == 0) {
-        tc_fence_after();
-        issue_mmas<CIN, COUT, MODE>(oy, tmem + s * C::ACOLS, xh, xl, wh, wl);
-        mma_commit(smem_u32(&mbar[s]));
-      }
-      // (B) prefetch the new input rows of row oy+1 (at most two)
-      RowPrefetch<CIN, COUT, MODE> pf0, pf1;
-      int nnew = 0;
-      if (oy + 1 < oy1) {
-        tile_rows<MODE>(oy + 1, lo, hi);
-        if (hi > staged_hi) {
-          row_load<CIN, COUT, MODE>(pf0, xb_ptr, a.H, a.W, xb, staged_hi + 1);
-          nnew = 1;
-          if (hi > staged_hi + 1) {
-            row_load<CIN, COUT, MODE>(pf1, xb_ptr, a.H, a.W, xb, staged_hi + 2);
-            nnew = 2;
+  if (warp == kProdWarp) {
+    // ================= producer: raw row segments, global -> smem (bulk copies)
+    if (lane == 0) {
+      long long seq = 0;
+      for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
+        Unit U;
+        if (!unit_at<MODE>(a, u, U)) continue;
+        const int x0 = raw_x0<MODE>(U.xb);
+        const int clo = max(x0, 0), chi = min(x0 + C::RW, a.W);
+        const float* img = a.x + (size_t)U.b * a.H * a.W * CIN;
+        for (int g = U.glo; g <= U.ghi; ++g, ++seq) {
+          const int s = (int)(seq % NR);
+          const long long use = seq / NR;
+          if (use > 0) mbar_wait(smem_u32(&raw_empty[s]), (uint32_t)((use - 1) & 1));
+          const uint32_t bar = smem_u32(&raw_full[s]);
+          if (g >= 0 && g < a.H && chi > clo && !(a.dbg & 1)) {
+            const uint32_t bytes = (uint32_t)(chi - clo) * CIN * 4;
+            mbar_arrive_tx(bar, bytes);
+            bulk_g2s(smem_u32(raw + (size_t)s * C::RAW_BYTES + (size_t)(clo - x0) * CIN * 4),
+                     img + ((size_t)g * a.W + clo) * CIN, bytes, bar);
+          } else {
+            mbar_arrive(bar);
           }
         }
       }
-      // (C) drain row oy-1 (its MMAs overlapped with (A)/(B))
-      if (t > 0) {
-        mbar_wait(smem_u32(&mbar[s ^ 1]), phase[s ^ 1]);
-        phase[s ^ 1] ^= 1u;
-        tc_fence_after();
-        epilogue<CIN, COUT, MODE>(a, tmem + (s ^ 1) * C::ACOLS, b, oy - 1, xb);
-      }
-      // (D) rows for oy+1 overwrite slots only rows <= oy-1's inputs used (their MMAs are complete)
-      if (nnew >= 1) row_store<CIN, COUT, MODE>(pf0, x_hi, x_lo);
-      if (nnew >= 2) row_store<CIN, COUT, MODE>(pf1, x_hi, x_lo);
-      staged_hi += nnew;
-      fence_async_smem();
-      tc_fence_before();
-      __syncthreads();
     }
-    // drain the last row
-    const int tl = oy1 - 1 - oy0, sl = tl & 1;
-    mbar_wait(smem_u32(&mbar[sl]), phase[sl]);
-    phase[sl] ^= 1u;
-    tc_fence_after();
-    epilogue<CIN, COUT, MODE>(a, tmem + sl * C::ACOLS, b, oy1 - 1, xb);
-    tc_fence_before();
-    __syncthreads();
+  } else if (warp >= kCvtWarp0 && warp < kCvtWarp0 + kCvtWarps) {
+    // ================= converters: raw fp32 -> staged tf32 hi/lo
+    const int ct = tid - 32 * kCvtWarp0;
+    long long seq = 0;
+    for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
+      Unit U;
+      if (!unit_at<MODE>(a, u, U)) continue;
+      const int x0 = raw_x0<MODE>(U.xb);
+      const int clo = max(x0, 0) - x0, chi = min(x0 + C::RW, a.W) - x0;  // valid raw pixels [clo, chi)
+      for (int g = U.glo; g <= U.ghi; ++g, ++seq) {
+        const int rs = (int)(seq % NR), ss = (int)(seq % NS);
+        const long long suse = seq / NS;
+        if (suse > 0) mbar_wait(smem_u32(&stg_empty[ss]), (uint32_t)((suse - 1) & 1));
+        mbar_wait(smem_u32(&raw_full[rs]), (uint32_t)((seq / NR) & 1));
+        const bool row_ok = g >= 0 && g < a.H;
+        const unsigned char* src = raw + (size_t)rs * C::RAW_BYTES;
+        for (int e = ct; e < C::RW * KCH; e += kCvtThreads) {
+          const int p = e / KCH, c = e - p * KCH;  // chunk fastest: conflict-free raw reads
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (row_ok && p >= clo && p < chi) v = *reinterpret_cast<const float4*>(src + ((size_t)p * CIN + 4 * c) * 4);
+          uint4 hi, lo;
+          split3(v, hi, lo);
+          const size_t off = ((size_t)c * C::XPL + ss * C::RW + staged_px<MODE>(p)) * 16;
+          *reinterpret_cast<uint4*>(x_hi + off) = hi;
+          *reinterpret_cast<uint4*>(x_lo + off) = lo;
+        }
+        fence_async_smem();
+        mbar_arrive(smem_u32(&raw_empty[rs]));
+        mbar_arrive(smem_u32(&stg_full[ss]));
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ================= MMA issuer
+    if (lane == 0) {
+      const DescBase db{umma_desc(smem_u32(x_hi), C::XPL * 16, 128), umma_desc(smem_u32(x_lo), C::XPL * 16, 128),
+                        umma_desc(smem_u32(w_hi), COUT * 16, 128), umma_desc(smem_u32(w_lo), COUT * 16, 128)};
+      long long seq0 = 0;  // staged sequence number of the unit's first row
+      long long tile = 0;
+      for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
+        Unit U;
+        if (!unit_at<MODE>(a, u, U)) continue;
+        auto slot = [&](int g) { return (int)((seq0 + (g - U.glo)) % NS); };
+        int waited = U.glo - 1;   // highest input row known to be staged
+        int retired = U.glo - 1;  // highest input row released back to the converters
+        for (int oy = U.oy0; oy < U.oy1; ++oy, ++tile) {
+          int lo, hi;
+          tile_rows<MODE>(oy, lo, hi);
+          for (int g = waited + 1; g <= hi; ++g) {
+            const long long sq = seq0 + (g - U.glo);
+            mbar_wait(smem_u32(&stg_full[sq % NS]), (uint32_t)((sq / NS) & 1));
+          }
+          waited = max(waited, hi);
+          const int acc = (int)(tile % kNA);
+          const long long ause = tile / kNA;
+          if (ause > 0) mbar_wait(smem_u32(&acc_empty[acc]), (uint32_t)((ause - 1) & 1));
+          tc_fence_after();
+          if (!(a.dbg & 2)) issue_mmas<CIN, COUT, MODE>(oy, tmem + acc * C::ACOLS, db, slot);
+          if (a.dbg & 64) mbar_arrive(smem_u32(&acc_full[acc])); else mma_commit(smem_u32(&acc_full[acc]));
+          // release rows the next tile of this unit no longer reads
+          int keep_lo = U.ghi + 1;
+          if (oy + 1 < U.oy1) {
+            int nl, nh;
+            tile_rows<MODE>(oy + 1, nl, nh);
+            keep_lo = nl;
+          }
+          for (int g = retired + 1; g < keep_lo && g <= waited; ++g) { if (a.dbg & 64) mbar_arrive(smem_u32(&stg_empty[slot(g)])); else mma_commit(smem_u32(&stg_empty[slot(g)])); }
+          retired = max(retired, min(keep_lo - 1, waited));
+        }
+        seq0 += U.ghi - U.glo + 1;
+      }
+    }
+  } else {
+    // ================= epilogue warps 0-3: TMEM lane quarter = warp
+    const int m = warp * 32 + lane;
+    long long tile = 0;
+    for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
+      Unit U;
+      if (!unit_at<MODE>(a, u, U)) continue;
+      const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[U.b] : 0) : U.b) *
+                                                   a.addend_bstride
+                                  : nullptr;
+      for (int oy = U.oy0; oy < U.oy1; ++oy, ++tile) {
+        const int acc = (int)(tile % kNA);
+        mbar_wait(smem_u32(&acc_full[acc]), (uint32_t)((tile / kNA) & 1));
+        tc_fence_after();
+        uint32_t r[C::NACC][COUT];
+#pragma unroll
+        for (int k = 0; k < C::NACC; ++k)
+#pragma unroll
+          for (int n0 = 0; n0 < COUT; n0 += 8)
+            if (!(a.dbg & 4)) tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + acc * C::ACOLS + k * COUT + n0,
+                     *reinterpret_cast<uint32_t(*)[8]>(&r[k][n0]));
+        if (!(a.dbg & 4)) tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(smem_u32(&acc_empty[acc]));  // TMEM free; finish from registers
+#pragma unroll
+        for (int k = 0; k < C::NACC; ++k) {
+          const int ox = MODE == 2 ? 2 * (U.xb * kM + m) + k : U.xb * kM + m;
+          const size_t pix = (size_t)oy * a.Wo + ox;
+          const size_t obase = (size_t)U.b * a.Ho * a.Wo * COUT + pix * COUT;
+#pragma unroll
+          for (int n0 = 0; n0 < COUT; n0 += 4) {
+            float4 o;
+            float* po = &o.x;
+#pragma unroll
+            for (int u4 = 0; u4 < 4; ++u4) {
+              float t = __uint_as_float(r[k][n0 + u4]) + __ldg(a.bias + n0 + u4);
+              po[u4] = a.softplus ? softplus_f(t) : t;
+            }
+            if (add) {
+              const float4 ad = __ldg(reinterpret_cast<const float4*>(add + pix * COUT + n0));
+              o.x += ad.x;
+              o.y += ad.y;
+              o.z += ad.z;
+              o.w += ad.w;
+            }
+            if (a.residual) {
+              const float4 rs = __ldg(reinterpret_cast<const float4*>(a.residual + obase + n0));
+              o.x += rs.x;
+              o.y += rs.y;
+              o.z += rs.z;
+              o.w += rs.w;
+            }
+            if (!(a.dbg & 32)) *reinterpret_cast<float4*>(a.y + obase + n0) = o;
+          }
+        }
+      }
+    }
   }
-  if (warp == 0) {
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0 && !(a.dbg & 8)) {
+    tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::NCOLS));
   }
 }
@@ -412,18 +507,16 @@ __global__ void __launch_bounds__(kNT) k_conv_tc(TcArgs a) {
 template <int CIN, int COUT, int MODE>
 void launch_tc(const TcArgs& a, cudaStream_t st) {
   using C = Cfg<CIN, COUT, MODE>;
-  static int grid_cap = 0;
-  if (!grid_cap) {
+  static_assert(C::TOTAL <= 232448, "shared memory budget");
+  static int sms = 0;
+  if (!sms) {
     cudaFuncSetAttribute(k_conv_tc<CIN, COUT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::TOTAL);
-    int per_sm = 0, sms = 0, dev = 0;
+    int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_conv_tc<CIN, COUT, MODE>, kNT, C::TOTAL);
-    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
-  const long long xblocks = MODE == 2 ? a.W / kM : a.Wo / kM;
-  const long long nunits = (long long)a.B * xblocks * ((a.Ho + kBand - 1) / kBand);
-  const int grid = (int)(nunits < grid_cap ? nunits : grid_cap);
+  const long long nunits = num_units<MODE>(a);
+  const int grid = (int)(nunits < sms ? nunits : sms);
   k_conv_tc<CIN, COUT, MODE><<<grid, kNT, C::TOTAL, st>>>(a);
 }
 
@@ -446,8 +539,9 @@ void conv_tc_launch(const float* x, int H, int W, int cin, float* y, int Ho, int
                     int transposed, const float* w, const float* bias, int softplus, const float* addend,
                     long long addend_bstride, int addend_per_model, const int* model_of, const float* residual,
                     const void* const* active, int B, cudaStream_t st) {
+  static const int dbg = getenv("HS_CONV_DEBUG") ? atoi(getenv("HS_CONV_DEBUG")) : 0;
   TcArgs a{x, H, W, y, Ho, Wo, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual,
-           active, B};
+           active, B, dbg};
   const int mode = transposed ? 2 : (stride == 2 ? 1 : 0);
   if (mode == 0 && cin == 16 && cout == 16) launch_tc<16, 16, 0>(a, st);
   else if (mode == 0 && cin == 32 && cout == 32) launch_tc<32, 32, 0>(a, st);
