@@ -1,10 +1,10 @@
-// tcgen05 implicit-GEMM 3x3 convolution with 3xTF32 (fp32-class) accuracy.
+// tcgen05 implicit-GEMM 3x3 convolution with fp32-class accuracy (BF16x3).
 //
 // GEMM view of one output tile: D[m][n] = sum_k A[m][k] B[n][k] with m = 128
 // consecutive output pixels of one row, n = cout, k = (tap, cin).  Input rows
 // are staged in shared memory in the UMMA K-major "interleaved" canonical
 // layout (core matrix = 8 pixels x 16 bytes, pixels consecutive at a 16-byte
-// pitch, 4-channel chunks LBO apart).  Because pixels sit at a 16-byte pitch,
+// pitch, 8-channel chunks LBO apart).  Because pixels sit at a 16-byte pitch,
 // the A operand of tap (ky, kx) is just the staged row with the descriptor
 // start address moved by kx * 16 bytes: no im2col copies.  Stride-2
 // convolutions stage each input row de-interleaved (even columns, then odd
@@ -12,25 +12,30 @@
 // convolution is split into its two column-parity classes (1 and 2 taps)
 // with two TMEM accumulators.
 //
+// Precision (SURVEY.md §0.5 rules out plain TF32/BF16): every fp32 operand is
+// split exactly into three bf16 parts x = x0 + x1 + x2 (8+8+8 mantissa bits)
+// and the six products with weight >= 2^-16 are accumulated in fp32 TMEM:
+//   A0 [W0 | W1 | W2]  (N = 3 cout),  A1 [W0 | W1]  (N = 2 cout),  A2 W0  (N = cout)
+// The weight parts are stacked along N, so each activation part is read from
+// shared memory once per K step (cout = 16 makes these MMAs operand-bound,
+// not math-bound); the epilogue sums the three column groups.
+//
 // Warp-specialised pipeline (one persistent CTA per SM, weights resident):
-//   warp 6 (1 lane)  producer : cp.async.bulk of raw NHWC input rows into a
-//                               ring of raw slots (mbarrier tx-count)
-//   warps 4-5        converters: raw fp32 -> tf32 hi/lo split, re-laid out
-//                               into the staged ring (smem -> smem)
-//   warp 7 (1 lane)  MMA issuer: 3xTF32 tcgen05.mma per tile into one of
-//                               four TMEM accumulators; commits release
-//                               staged rows and hand accumulators on
+//   warp 6 (1 lane)  producer  : cp.async.bulk of raw NHWC input rows into a
+//                                ring of raw slots (mbarrier tx-count)
+//   warps 4-5        converters: raw fp32 -> bf16x3 split, re-laid out into
+//                                the staged ring (smem -> smem)
+//   warp 7 (1 lane)  MMA issuer: tcgen05.mma per tile into one of four TMEM
+//                                accumulators; commits release staged rows
+//                                and hand accumulators to the epilogue
 //   warps 0-3        epilogue  : tcgen05.ld of their TMEM lane quarter, then
-//                               bias, softplus, encoder/skip addend,
-//                               residual, NHWC stores
+//                                bias, softplus, encoder/skip addend,
+//                                residual, NHWC stores
 // A CTA walks a band of output rows of one 128-pixel column block top to
 // bottom, so every input row is fetched and split once per band.
-//
-// Precision: every fp32 operand x is split into tf32 hi = rna(x) and
-// lo = rna(x - hi); the MMA accumulates hi*hi + hi*lo + lo*hi in fp32 TMEM
-// (relative error ~1e-6, fp32 class; SURVEY.md §0.5 rules out 1xTF32/BF16).
+#include <cuda_bf16.h>
+
 #include <cstdio>
-#include <cstdlib>
 
 #include "common.cuh"
 #include "conv_tc.h"
@@ -53,15 +58,15 @@ HS_DEV uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
 }
 
-// instruction descriptor: D f32, A/B tf32, both K-major, M x N
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// instruction descriptor, kind::f16: D f32, A/B bf16, both K-major, M x N
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-HS_DEV void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+HS_DEV void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
@@ -101,22 +106,23 @@ HS_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluste
 HS_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 HS_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-HS_DEV uint32_t tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
-}
-
-// split x into tf32 hi + tf32 lo
-HS_DEV void split3(float4 v, uint4& hi, uint4& lo) {
-  hi.x = tf32_rna(v.x);
-  hi.y = tf32_rna(v.y);
-  hi.z = tf32_rna(v.z);
-  hi.w = tf32_rna(v.w);
-  lo.x = tf32_rna(v.x - __uint_as_float(hi.x));
-  lo.y = tf32_rna(v.y - __uint_as_float(hi.y));
-  lo.z = tf32_rna(v.z - __uint_as_float(hi.z));
-  lo.w = tf32_rna(v.w - __uint_as_float(hi.w));
+// exact three-way bf16 split of 8 floats into one 16-byte chunk per part
+HS_DEV void split_bf16x3(const float (&v)[8], uint4& p0, uint4& p1, uint4& p2) {
+  uint32_t w0[4], w1[4], w2[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float a = v[2 * i], b = v[2 * i + 1];
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    const float ra = a - __low2float(h), rb = b - __high2float(h);
+    const __nv_bfloat162 m = __floats2bfloat162_rn(ra, rb);
+    const __nv_bfloat162 l = __floats2bfloat162_rn(ra - __low2float(m), rb - __high2float(m));
+    w0[i] = *reinterpret_cast<const uint32_t*>(&h);
+    w1[i] = *reinterpret_cast<const uint32_t*>(&m);
+    w2[i] = *reinterpret_cast<const uint32_t*>(&l);
+  }
+  p0 = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+  p1 = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+  p2 = make_uint4(w2[0], w2[1], w2[2], w2[3]);
 }
 
 HS_DEV void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
@@ -143,34 +149,38 @@ struct TcArgs {
   const float* residual;
   const void* const* active;
   int B;
-  int dbg;  // debug: bit0 no bulk copies, bit1 no MMAs, bit2 no TMEM loads
 };
 
 // MODE 0: stride 1; MODE 1: stride 2; MODE 2: transposed stride 2 (out = 2 x in)
 template <int CIN, int COUT, int MODE>
 struct Cfg {
-  static constexpr int KCH = CIN / 4;                                              // 16-byte channel chunks
+  static constexpr int KC = CIN / 8;                                                // 16-byte chunks per part
+  static constexpr int KSTEPS = CIN / 16;                                           // MMA K steps per tap
   static constexpr int RW = MODE == 0 ? kM + 2 : (MODE == 1 ? 2 * kM + 1 : kM + 1); // pixels per staged row
   static constexpr int NACC = MODE == 2 ? 2 : 1;  // accumulators per tile (column-parity classes)
-  // staged (split) ring and raw ring depths, sized to fit 227 KB
-  static constexpr int NS = (MODE == 0 && CIN == 16) ? 5 : (MODE == 1 ? 4 : 3);
-  static constexpr int NR = (MODE == 0 && CIN == 16) ? 4 : 2;
+  static constexpr int NS = MODE == 0 ? (CIN == 16 ? 6 : 4) : (MODE == 1 ? 5 : 4);  // staged ring depth
+  static constexpr int NR = (MODE == 0 && CIN == 16) ? 4 : 2;                          // raw ring depth
   static constexpr int XPL0 = NS * RW;
   static constexpr int XPL = XPL0 + ((9 - (XPL0 & 7)) & 7);  // == 1 mod 8: conflict-free chunk planes
   static constexpr int RAW_BYTES = RW * CIN * 4;
-  static constexpr size_t W_BYTES = (size_t)9 * KCH * COUT * 16;
-  static constexpr size_t X_BYTES = (size_t)KCH * XPL * 16;
+  static constexpr int NW = 3 * COUT;                         // stacked weight rows [W0; W1; W2]
+  static constexpr size_t W_BYTES = (size_t)9 * KC * NW * 16;
+  static constexpr size_t XP_BYTES = (size_t)KC * XPL * 16;   // one activation part
   static constexpr size_t R_BYTES = (size_t)NR * RAW_BYTES;
   static constexpr int NBAR = 2 * NR + 2 * NS + 2 * kNA;
-  static constexpr size_t TOTAL = 2 * W_BYTES + 2 * X_BYTES + R_BYTES + 8 * NBAR + 16;
-  static constexpr int ACOLS = COUT * NACC;  // TMEM columns per accumulator
+  static constexpr size_t TOTAL = W_BYTES + 3 * XP_BYTES + R_BYTES + 8 * NBAR + 16;
+  static constexpr int ACOLS = NW * NACC;  // TMEM columns per accumulator
   static constexpr int NCOLS_RAW = kNA * ACOLS;
-  static constexpr int NCOLS = NCOLS_RAW <= 32 ? 32 : (NCOLS_RAW <= 64 ? 64 : (NCOLS_RAW <= 128 ? 128 : 256));
+  static constexpr int NCOLS = NCOLS_RAW <= 32    ? 32
+                               : NCOLS_RAW <= 64  ? 64
+                               : NCOLS_RAW <= 128 ? 128
+                               : NCOLS_RAW <= 256 ? 256
+                                                  : 512;
 };
 
 // input rows a tile (output row oy) needs: [lo, hi]
 template <int MODE>
-HS_DEV void tile_rows(int oy, int& lo, int& hi) {
+__host__ __device__ inline void tile_rows(int oy, int& lo, int& hi) {
   if (MODE == 0) {
     lo = oy - 1;
     hi = oy + 1;
@@ -193,12 +203,18 @@ HS_DEV int raw_x0(int xb) {
 template <int MODE>
 HS_DEV int staged_px(int p) {
   if (MODE != 1) return p;
-  return (p & 1) ? (p - 1) >> 1 : kM + (p >> 1);  // col 2x0-1+p: odd p -> even col
+  return (p & 1) ? (p - 1) >> 1 : kM + (p >> 1);  // column 2x0-1+p: odd p is an even column
 }
 
 struct Unit {
   int b, xb, oy0, oy1, glo, ghi;  // rows [oy0, oy1), input rows [glo, ghi]
 };
+
+template <int MODE>
+__host__ __device__ inline long long num_units(const TcArgs& a) {
+  const int xblocks = MODE == 2 ? a.W / kM : a.Wo / kM;
+  return (long long)a.B * xblocks * ((a.Ho + kBand - 1) / kBand);
+}
 
 template <int MODE>
 HS_DEV bool unit_at(const TcArgs& a, long long u, Unit& U) {
@@ -217,30 +233,24 @@ HS_DEV bool unit_at(const TcArgs& a, long long u, Unit& U) {
   return !(a.active && a.active[U.b] == nullptr);
 }
 
-template <int MODE>
-__host__ __device__ inline long long num_units(const TcArgs& a) {
-  const int xblocks = MODE == 2 ? a.W / kM : a.Wo / kM;
-  return (long long)a.B * xblocks * ((a.Ho + kBand - 1) / kBand);
-}
-
 // Descriptor bases (the start-address field is in 16-byte units in the low
 // bits, so moving a window is a 64-bit add of offset >> 4).
 struct DescBase {
-  uint64_t xh, xl, wh, wl;
+  uint64_t x[3], w;
 };
 
 template <int CIN, int COUT, int MODE>
 HS_DEV void tap_mmas(uint32_t d, const DescBase& db, uint32_t x_units, uint32_t w_units, uint32_t& first) {
   using C = Cfg<CIN, COUT, MODE>;
-  constexpr uint32_t X_STEP = 2 * C::XPL, W_STEP = 2 * COUT;  // two 16-byte chunks per K step
-  constexpr uint32_t IDESC = idesc_tf32(kM, COUT);
+  constexpr uint32_t X_STEP = 2 * C::XPL, W_STEP = 2 * C::NW;  // two 16-byte chunks per K step
+  constexpr uint32_t I0 = idesc_bf16(kM, 3 * COUT), I1 = idesc_bf16(kM, 2 * COUT), I2 = idesc_bf16(kM, COUT);
 #pragma unroll
-  for (int kk = 0; kk < C::KCH / 2; ++kk) {
-    const uint64_t xo = x_units + kk * X_STEP, wo = w_units + kk * W_STEP;
-    mma_tf32(d, db.xh + xo, db.wh + wo, IDESC, first ? 0u : 1u);
+  for (int kk = 0; kk < C::KSTEPS; ++kk) {
+    const uint64_t xo = x_units + kk * X_STEP, wo = db.w + w_units + kk * W_STEP;
+    mma_bf16(d, db.x[0] + xo, wo, I0, first ? 0u : 1u);
     first = 0;
-    mma_tf32(d, db.xh + xo, db.wl + wo, IDESC, 1u);
-    mma_tf32(d, db.xl + xo, db.wh + wo, IDESC, 1u);
+    mma_bf16(d, db.x[1] + xo, wo, I1, 1u);
+    mma_bf16(d, db.x[2] + xo, wo, I2, 1u);
   }
 }
 
@@ -248,7 +258,7 @@ HS_DEV void tap_mmas(uint32_t d, const DescBase& db, uint32_t x_units, uint32_t 
 template <int CIN, int COUT, int MODE, typename SlotOf>
 HS_DEV void issue_mmas(int oy, uint32_t d0, const DescBase& db, SlotOf slot) {
   using C = Cfg<CIN, COUT, MODE>;
-  constexpr uint32_t WT = C::KCH * COUT;  // weight units per tap
+  constexpr uint32_t WT = C::KC * C::NW;  // weight units per tap
   auto row_units = [&](int g) { return (uint32_t)(slot(g) * C::RW); };
   uint32_t first = 1;
   if (MODE == 0 || MODE == 1) {
@@ -268,32 +278,31 @@ HS_DEV void issue_mmas(int oy, uint32_t d0, const DescBase& db, SlotOf slot) {
   //             out col 2q (acc 0) <- (kx 1, q); out col 2q+1 (acc 1) <- (kx 0, q+1), (kx 2, q)
   const int q = oy >> 1;
   const uint32_t rq = row_units(q), rq1 = row_units(q + 1);
+  const uint32_t d1 = d0 + C::NW;
   if ((oy & 1) == 0) {
     tap_mmas<CIN, COUT, MODE>(d0, db, rq, (1 * 3 + 1) * WT, first);
     first = 1;
-    tap_mmas<CIN, COUT, MODE>(d0 + COUT, db, rq + 1, (1 * 3 + 0) * WT, first);
-    tap_mmas<CIN, COUT, MODE>(d0 + COUT, db, rq, (1 * 3 + 2) * WT, first);
+    tap_mmas<CIN, COUT, MODE>(d1, db, rq + 1, (1 * 3 + 0) * WT, first);
+    tap_mmas<CIN, COUT, MODE>(d1, db, rq, (1 * 3 + 2) * WT, first);
   } else {
     tap_mmas<CIN, COUT, MODE>(d0, db, rq1, (0 * 3 + 1) * WT, first);
     tap_mmas<CIN, COUT, MODE>(d0, db, rq, (2 * 3 + 1) * WT, first);
     first = 1;
-    tap_mmas<CIN, COUT, MODE>(d0 + COUT, db, rq1 + 1, (0 * 3 + 0) * WT, first);
-    tap_mmas<CIN, COUT, MODE>(d0 + COUT, db, rq1, (0 * 3 + 2) * WT, first);
-    tap_mmas<CIN, COUT, MODE>(d0 + COUT, db, rq + 1, (2 * 3 + 0) * WT, first);
-    tap_mmas<CIN, COUT, MODE>(d0 + COUT, db, rq, (2 * 3 + 2) * WT, first);
+    tap_mmas<CIN, COUT, MODE>(d1, db, rq1 + 1, (0 * 3 + 0) * WT, first);
+    tap_mmas<CIN, COUT, MODE>(d1, db, rq1, (0 * 3 + 2) * WT, first);
+    tap_mmas<CIN, COUT, MODE>(d1, db, rq + 1, (2 * 3 + 0) * WT, first);
+    tap_mmas<CIN, COUT, MODE>(d1, db, rq, (2 * 3 + 2) * WT, first);
   }
 }
 
 template <int CIN, int COUT, int MODE>
 __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
   using C = Cfg<CIN, COUT, MODE>;
-  constexpr int KCH = C::KCH, NS = C::NS, NR = C::NR;
+  constexpr int KC = C::KC, NS = C::NS, NR = C::NR, NW = C::NW;
   extern __shared__ __align__(128) unsigned char smem[];
-  unsigned char* w_hi = smem;
-  unsigned char* w_lo = smem + C::W_BYTES;
-  unsigned char* x_hi = smem + 2 * C::W_BYTES;
-  unsigned char* x_lo = x_hi + C::X_BYTES;
-  unsigned char* raw = x_lo + C::X_BYTES;
+  unsigned char* wst = smem;
+  unsigned char* xp[3] = {smem + C::W_BYTES, smem + C::W_BYTES + C::XP_BYTES, smem + C::W_BYTES + 2 * C::XP_BYTES};
+  unsigned char* raw = smem + C::W_BYTES + 3 * C::XP_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(raw + C::R_BYTES);
   uint64_t* raw_full = bars;
   uint64_t* raw_empty = raw_full + NR;
@@ -304,15 +313,17 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(acc_empty + kNA);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  // ---- setup: resident weights (hi/lo), barriers, TMEM
-  for (int e = tid; e < 9 * KCH * COUT; e += kNT) {
-    const int n = e % COUT, c = (e / COUT) % KCH, t = e / (COUT * KCH);
-    const float4 v = __ldg(reinterpret_cast<const float4*>(a.w + ((size_t)n * 9 + t) * CIN + 4 * c));
-    uint4 hi, lo;
-    split3(v, hi, lo);
-    const size_t off = ((size_t)(t * KCH + c) * COUT + n) * 16;
-    *reinterpret_cast<uint4*>(w_hi + off) = hi;
-    *reinterpret_cast<uint4*>(w_lo + off) = lo;
+  // ---- setup: resident weight stack [W0; W1; W2], layout (tap, chunk, row) x 16 B
+  for (int e = tid; e < 9 * KC * COUT; e += kNT) {
+    const int n = e % COUT, c = (e / COUT) % KC, t = e / (COUT * KC);
+    const float* src = a.w + ((size_t)n * 9 + t) * CIN + 8 * c;
+    const float4 v0 = __ldg(reinterpret_cast<const float4*>(src)), v1 = __ldg(reinterpret_cast<const float4*>(src + 4));
+    const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    uint4 p[3];
+    split_bf16x3(v, p[0], p[1], p[2]);
+#pragma unroll
+    for (int part = 0; part < 3; ++part)
+      *reinterpret_cast<uint4*>(wst + ((size_t)(t * KC + c) * NW + part * COUT + n) * 16) = p[part];
   }
   if (tid == 0) {
     for (int i = 0; i < NR; ++i) {
@@ -327,9 +338,9 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
       mbar_init(smem_u32(&acc_full[i]), 1);
       mbar_init(smem_u32(&acc_empty[i]), 32 * kEpiWarps);
     }
-    if (!(a.dbg & 16)) fence_mbar_init();
+    fence_mbar_init();
   }
-  if (warp == 0 && !(a.dbg & 8)) {
+  if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
                  "r"(C::NCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -356,7 +367,7 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
           const long long use = seq / NR;
           if (use > 0) mbar_wait(smem_u32(&raw_empty[s]), (uint32_t)((use - 1) & 1));
           const uint32_t bar = smem_u32(&raw_full[s]);
-          if (g >= 0 && g < a.H && chi > clo && !(a.dbg & 1)) {
+          if (g >= 0 && g < a.H && chi > clo) {
             const uint32_t bytes = (uint32_t)(chi - clo) * CIN * 4;
             mbar_arrive_tx(bar, bytes);
             bulk_g2s(smem_u32(raw + (size_t)s * C::RAW_BYTES + (size_t)(clo - x0) * CIN * 4),
@@ -368,7 +379,7 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
       }
     }
   } else if (warp >= kCvtWarp0 && warp < kCvtWarp0 + kCvtWarps) {
-    // ================= converters: raw fp32 -> staged tf32 hi/lo
+    // ================= converters: raw fp32 -> staged bf16x3
     const int ct = tid - 32 * kCvtWarp0;
     long long seq = 0;
     for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
@@ -383,15 +394,19 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
         mbar_wait(smem_u32(&raw_full[rs]), (uint32_t)((seq / NR) & 1));
         const bool row_ok = g >= 0 && g < a.H;
         const unsigned char* src = raw + (size_t)rs * C::RAW_BYTES;
-        for (int e = ct; e < C::RW * KCH; e += kCvtThreads) {
-          const int p = e / KCH, c = e - p * KCH;  // chunk fastest: conflict-free raw reads
-          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (row_ok && p >= clo && p < chi) v = *reinterpret_cast<const float4*>(src + ((size_t)p * CIN + 4 * c) * 4);
-          uint4 hi, lo;
-          split3(v, hi, lo);
+        for (int e = ct; e < C::RW * KC; e += kCvtThreads) {
+          const int p = e / KC, c = e - p * KC;  // chunk fastest: conflict-free raw reads
+          float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          if (row_ok && p >= clo && p < chi) {
+            const float4* s4 = reinterpret_cast<const float4*>(src + ((size_t)p * CIN + 8 * c) * 4);
+            const float4 v0 = s4[0], v1 = s4[1];
+            v[0] = v0.x, v[1] = v0.y, v[2] = v0.z, v[3] = v0.w, v[4] = v1.x, v[5] = v1.y, v[6] = v1.z, v[7] = v1.w;
+          }
+          uint4 p3[3];
+          split_bf16x3(v, p3[0], p3[1], p3[2]);
           const size_t off = ((size_t)c * C::XPL + ss * C::RW + staged_px<MODE>(p)) * 16;
-          *reinterpret_cast<uint4*>(x_hi + off) = hi;
-          *reinterpret_cast<uint4*>(x_lo + off) = lo;
+#pragma unroll
+          for (int part = 0; part < 3; ++part) *reinterpret_cast<uint4*>(xp[part] + off) = p3[part];
         }
         fence_async_smem();
         mbar_arrive(smem_u32(&raw_empty[rs]));
@@ -401,8 +416,10 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
   } else if (warp == kMmaWarp) {
     // ================= MMA issuer
     if (lane == 0) {
-      const DescBase db{umma_desc(smem_u32(x_hi), C::XPL * 16, 128), umma_desc(smem_u32(x_lo), C::XPL * 16, 128),
-                        umma_desc(smem_u32(w_hi), COUT * 16, 128), umma_desc(smem_u32(w_lo), COUT * 16, 128)};
+      DescBase db;
+#pragma unroll
+      for (int part = 0; part < 3; ++part) db.x[part] = umma_desc(smem_u32(xp[part]), C::XPL * 16, 128);
+      db.w = umma_desc(smem_u32(wst), NW * 16, 128);
       long long seq0 = 0;  // staged sequence number of the unit's first row
       long long tile = 0;
       for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
@@ -423,8 +440,8 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
           const long long ause = tile / kNA;
           if (ause > 0) mbar_wait(smem_u32(&acc_empty[acc]), (uint32_t)((ause - 1) & 1));
           tc_fence_after();
-          if (!(a.dbg & 2)) issue_mmas<CIN, COUT, MODE>(oy, tmem + acc * C::ACOLS, db, slot);
-          if (a.dbg & 64) mbar_arrive(smem_u32(&acc_full[acc])); else mma_commit(smem_u32(&acc_full[acc]));
+          issue_mmas<CIN, COUT, MODE>(oy, tmem + acc * C::ACOLS, db, slot);
+          mma_commit(smem_u32(&acc_full[acc]));
           // release rows the next tile of this unit no longer reads
           int keep_lo = U.ghi + 1;
           if (oy + 1 < U.oy1) {
@@ -432,7 +449,7 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
             tile_rows<MODE>(oy + 1, nl, nh);
             keep_lo = nl;
           }
-          for (int g = retired + 1; g < keep_lo && g <= waited; ++g) { if (a.dbg & 64) mbar_arrive(smem_u32(&stg_empty[slot(g)])); else mma_commit(smem_u32(&stg_empty[slot(g)])); }
+          for (int g = retired + 1; g < keep_lo && g <= waited; ++g) mma_commit(smem_u32(&stg_empty[slot(g)]));
           retired = max(retired, min(keep_lo - 1, waited));
         }
         seq0 += U.ghi - U.glo + 1;
@@ -452,14 +469,14 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
         const int acc = (int)(tile % kNA);
         mbar_wait(smem_u32(&acc_full[acc]), (uint32_t)((tile / kNA) & 1));
         tc_fence_after();
-        uint32_t r[C::NACC][COUT];
+        uint32_t r[C::NACC][NW];
 #pragma unroll
         for (int k = 0; k < C::NACC; ++k)
 #pragma unroll
-          for (int n0 = 0; n0 < COUT; n0 += 8)
-            if (!(a.dbg & 4)) tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + acc * C::ACOLS + k * COUT + n0,
+          for (int n0 = 0; n0 < NW; n0 += 8)
+            tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + acc * C::ACOLS + k * NW + n0,
                      *reinterpret_cast<uint32_t(*)[8]>(&r[k][n0]));
-        if (!(a.dbg & 4)) tmem_wait_ld();
+        tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(smem_u32(&acc_empty[acc]));  // TMEM free; finish from registers
 #pragma unroll
@@ -473,7 +490,10 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
             float* po = &o.x;
 #pragma unroll
             for (int u4 = 0; u4 < 4; ++u4) {
-              float t = __uint_as_float(r[k][n0 + u4]) + __ldg(a.bias + n0 + u4);
+              const int n = n0 + u4;
+              // the three column groups hold the x0-, x1- and x2-weighted partial sums
+              const float t = (__uint_as_float(r[k][n]) + __uint_as_float(r[k][COUT + n])) +
+                              __uint_as_float(r[k][2 * COUT + n]) + __ldg(a.bias + n);
               po[u4] = a.softplus ? softplus_f(t) : t;
             }
             if (add) {
@@ -490,7 +510,7 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
               o.z += rs.z;
               o.w += rs.w;
             }
-            if (!(a.dbg & 32)) *reinterpret_cast<float4*>(a.y + obase + n0) = o;
+            *reinterpret_cast<float4*>(a.y + obase + n0) = o;
           }
         }
       }
@@ -498,7 +518,7 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0 && !(a.dbg & 8)) {
+  if (warp == 0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::NCOLS));
   }
@@ -508,6 +528,7 @@ template <int CIN, int COUT, int MODE>
 void launch_tc(const TcArgs& a, cudaStream_t st) {
   using C = Cfg<CIN, COUT, MODE>;
   static_assert(C::TOTAL <= 232448, "shared memory budget");
+  static_assert(C::NCOLS_RAW <= 512, "TMEM budget");
   static int sms = 0;
   if (!sms) {
     cudaFuncSetAttribute(k_conv_tc<CIN, COUT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::TOTAL);
@@ -539,9 +560,8 @@ void conv_tc_launch(const float* x, int H, int W, int cin, float* y, int Ho, int
                     int transposed, const float* w, const float* bias, int softplus, const float* addend,
                     long long addend_bstride, int addend_per_model, const int* model_of, const float* residual,
                     const void* const* active, int B, cudaStream_t st) {
-  static const int dbg = getenv("HS_CONV_DEBUG") ? atoi(getenv("HS_CONV_DEBUG")) : 0;
   TcArgs a{x, H, W, y, Ho, Wo, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual,
-           active, B, dbg};
+           active, B};
   const int mode = transposed ? 2 : (stride == 2 ? 1 : 0);
   if (mode == 0 && cin == 16 && cout == 16) launch_tc<16, 16, 0>(a, st);
   else if (mode == 0 && cin == 32 && cout == 32) launch_tc<32, 32, 0>(a, st);
