@@ -467,6 +467,20 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
                                   : nullptr;
       for (int oy = U.oy0; oy < U.oy1; ++oy, ++tile) {
         const int acc = (int)(tile % kNA);
+        // addend / residual do not depend on the accumulator: fetch them before waiting on the MMA
+        float4 pre_add[C::NACC][COUT / 4], pre_res[C::NACC][COUT / 4];
+#pragma unroll
+        for (int k = 0; k < C::NACC; ++k) {
+          const int ox = MODE == 2 ? 2 * (U.xb * kM + m) + k : U.xb * kM + m;
+          const size_t pix = (size_t)oy * a.Wo + ox;
+          const size_t obase = (size_t)U.b * a.Ho * a.Wo * COUT + pix * COUT;
+#pragma unroll
+          for (int q = 0; q < COUT / 4; ++q) {
+            pre_add[k][q] = add ? __ldg(reinterpret_cast<const float4*>(add + pix * COUT) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+            pre_res[k][q] = a.residual ? __ldg(reinterpret_cast<const float4*>(a.residual + obase) + q)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
         mbar_wait(smem_u32(&acc_full[acc]), (uint32_t)((tile / kNA) & 1));
         tc_fence_after();
         uint32_t r[C::NACC][NW];
@@ -496,20 +510,11 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
                               __uint_as_float(r[k][2 * COUT + n]) + __ldg(a.bias + n);
               po[u4] = a.softplus ? softplus_f(t) : t;
             }
-            if (add) {
-              const float4 ad = __ldg(reinterpret_cast<const float4*>(add + pix * COUT + n0));
-              o.x += ad.x;
-              o.y += ad.y;
-              o.z += ad.z;
-              o.w += ad.w;
-            }
-            if (a.residual) {
-              const float4 rs = __ldg(reinterpret_cast<const float4*>(a.residual + obase + n0));
-              o.x += rs.x;
-              o.y += rs.y;
-              o.z += rs.z;
-              o.w += rs.w;
-            }
+            const float4 ad = pre_add[k][n0 / 4], rs = pre_res[k][n0 / 4];
+            o.x += ad.x + rs.x;
+            o.y += ad.y + rs.y;
+            o.z += ad.z + rs.z;
+            o.w += ad.w + rs.w;
             *reinterpret_cast<float4*>(a.y + obase + n0) = o;
           }
         }
