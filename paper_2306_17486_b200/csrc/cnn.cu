@@ -271,6 +271,88 @@ void launch_tconv_t(const ConvArgs& a, int B, cudaStream_t st) {
   k_tconv<COUT><<<g, kConvThreads, sm, st>>>(a);
 }
 
+// Thin convolutions, stride 1: the 2-channel stems (cin = 2) and the
+// 2-channel head (cout = 2).  One thread per output pixel, the 3x3 input
+// window straight from L1/L2 (neighbouring threads share it), weights in
+// shared memory; memory-bound on the wide side.
+template <int CIN, int COUT>
+__global__ void __launch_bounds__(256) k_conv_thin(ConvArgs a) {
+  __shared__ float s_w[COUT * 9 * CIN];  // [cout][tap][cin]
+  __shared__ float s_b[COUT];
+  for (int e = threadIdx.x; e < COUT * 9 * CIN; e += blockDim.x) s_w[e] = a.w[e];
+  for (int e = threadIdx.x; e < COUT; e += blockDim.x) s_b[e] = a.bias[e];
+  __syncthreads();
+  const int b = blockIdx.y;
+  if (a.active && a.active[b] == nullptr) return;
+  const long long npix = (long long)a.Ho * a.Wo;
+  const float* xb = a.x + (long long)b * a.H * a.W * CIN;
+  const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[b] : 0) : b) * a.addend_bstride
+                              : nullptr;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < npix;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int oy = (int)(p / a.Wo), ox = (int)(p - (long long)oy * a.Wo);
+    float acc[COUT];
+#pragma unroll
+    for (int n = 0; n < COUT; ++n) acc[n] = s_b[n];
+#pragma unroll
+    for (int ky = 0; ky < 3; ++ky) {
+      const int iy = oy + ky - 1;
+      if (iy < 0 || iy >= a.H) continue;
+#pragma unroll
+      for (int kx = 0; kx < 3; ++kx) {
+        const int ix = ox + kx - 1;
+        if (ix < 0 || ix >= a.W) continue;
+        const float* px = xb + ((long long)iy * a.W + ix) * CIN;
+        float xv[CIN];
+        if (CIN % 4 == 0) {
+#pragma unroll
+          for (int c = 0; c < CIN; c += 4) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(px + c));
+            xv[c] = v.x, xv[c + 1] = v.y, xv[c + 2] = v.z, xv[c + 3] = v.w;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < CIN; c += 2) {
+            const float2 v = __ldg(reinterpret_cast<const float2*>(px + c));
+            xv[c] = v.x, xv[c + 1] = v.y;
+          }
+        }
+        const int tap = ky * 3 + kx;
+#pragma unroll
+        for (int n = 0; n < COUT; ++n)
+#pragma unroll
+          for (int c = 0; c < CIN; ++c) acc[n] = fmaf(xv[c], s_w[(n * 9 + tap) * CIN + c], acc[n]);
+      }
+    }
+    const long long o = (long long)b * npix * COUT + p * COUT;
+#pragma unroll
+    for (int n = 0; n < COUT; n += 2) {
+      float2 v = make_float2(acc[n], acc[n + 1]);
+      if (a.softplus) v = make_float2(softplusf(v.x), softplusf(v.y));
+      if (add) {
+        const float2 ad = __ldg(reinterpret_cast<const float2*>(add + p * COUT + n));
+        v.x += ad.x;
+        v.y += ad.y;
+      }
+      if (a.residual) {
+        const float2 rs = __ldg(reinterpret_cast<const float2*>(a.residual + o + n));
+        v.x += rs.x;
+        v.y += rs.y;
+      }
+      *reinterpret_cast<float2*>(a.y + o + n) = v;
+    }
+  }
+}
+
+template <int CIN, int COUT>
+void launch_thin(const ConvArgs& a, int B, cudaStream_t st) {
+  const long long npix = (long long)a.Ho * a.Wo;
+  long long blocks = (npix + 255) / 256;
+  const long long cap = (8LL * 148 + B - 1) / B;
+  if (blocks > cap) blocks = cap;
+  k_conv_thin<CIN, COUT><<<dim3((unsigned)blocks, B), 256, 0, st>>>(a);
+}
+
 int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* y, const float* addend,
                 long long addend_bstride, const int* model_of, const float* residual, const void* const* active,
                 cudaStream_t st, bool model_of_addend = false) {
@@ -311,6 +393,12 @@ int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* 
   Scope scope{prof::start(prof::CONV, st), l0 ? prof::start(prof::CONV_L0, st) : -1, st, flops};
   a.residual = residual;
   a.active = active;
+  if (!c.transposed && c.stride == 1) {
+    if (c.cin == 2 && c.cout == 16) return launch_thin<2, 16>(a, B, st), HS_OK;
+    if (c.cin == 2 && c.cout == 8) return launch_thin<2, 8>(a, B, st), HS_OK;
+    if (c.cin == 16 && c.cout == 2) return launch_thin<16, 2>(a, B, st), HS_OK;
+    if (c.cin == 8 && c.cout == 2) return launch_thin<8, 2>(a, B, st), HS_OK;
+  }
   if (conv_tc_supported(c.cin, c.cout, c.stride, c.transposed, H, W, a.Wo)) {
     conv_tc_launch(a.x, a.H, a.W, a.cin, a.y, a.Ho, a.Wo, a.cout, c.stride, c.transposed, a.w, a.bias, a.softplus,
                    a.addend, a.addend_bstride, a.addend_per_model, a.model_of, a.residual, a.active, B, st);
