@@ -36,7 +36,10 @@ def _setup(config: str, learned: bool, rhs_per_model: int):
 
 def _worker(args):
     config, learned, rhs_per_model, index, iters = args
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    # one BLAS/FFT thread per worker process: the pool itself provides the parallelism
+    from threadpoolctl import threadpool_limits
+
+    threadpool_limits(1)
     if not _STATE:
         _setup(config, learned, rhs_per_model)
     from oracle import helm_oracle as ho
