@@ -183,6 +183,7 @@ def main():
 
     world, rank, local = dist_setup()
     from paper_2306_17486_b200 import _lib, krylov, network, problems
+    from paper_2306_17486_b200 import dist as hdist
     from paper_2306_17486_b200.device import to_device
 
     learned = args.precond == "learned"
@@ -227,17 +228,10 @@ def main():
     launches = int(lib.hs_launch_count())
     prof = {t: _lib.profile_query(t) for t in tags}
     lib.hs_profile_enable(0)
-    if world > 1:
-        import torch.distributed as dist
-
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        ti = torch.tensor([total_iters], device="cuda", dtype=torch.float64)
-        dist.all_reduce(ti)
-        total_iters = int(ti.item())
+    ms = hdist.reduce_scalar(ms, "max")  # max over ranks
+    total_iters = int(hdist.reduce_scalar(total_iters, "sum"))
     value = world * B * args.steps / (ms / 1e3)
-    applies = total_iters / (ms / 1e3) if world == 1 else total_iters / (ms / 1e3)
+    applies = total_iters / (ms / 1e3)
 
     # ---------------- e2e through the public API with pinned host buffers
     e2e = None
@@ -254,10 +248,7 @@ def main():
             d2h = x.nbytes + sum(8 * len(r.relative_residual_history) for r in reps)
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([el], device="cuda", dtype=torch.float64)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            el = float(t.item())
+        el = hdist.reduce_scalar(el, "max")
         e2e = {"value": world * B * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": int(rhs_pinned.numel() * 16),
                "d2h_bytes_per_step": int(d2h)}
 

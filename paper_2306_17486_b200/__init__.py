@@ -2,8 +2,26 @@
 
 Submodules mirror the reference package: ``errors``, ``fields``, ``multigrid``,
 ``krylov``, ``green``, ``network`` (the module the reference imports but never
-shipped), plus ``engine`` (batched device solve) and ``problems`` (seeded
-BASELINE inputs).  Compute runs in the in-tree C-ABI library
-``libhelmsolve_b200.so`` (sm_100a); there is no CPU fallback.
+shipped), plus ``engine`` (batched device solve), ``problems`` (seeded BASELINE
+inputs) and ``dist`` (data-parallel plumbing).  Compute runs in the in-tree
+C-ABI library ``libhelmsolve_b200.so`` (sm_100a); there is no CPU fallback.
 """
-__all__ = ["errors", "fields", "multigrid", "krylov", "green", "network", "engine", "problems", "netparams"]
+import importlib
+import sys
+
+__all__ = ["errors", "fields", "multigrid", "krylov", "green", "network", "engine", "problems", "netparams",
+           "dist", "install_as_helmsolve"]
+
+_MIRRORED = ("errors", "fields", "multigrid", "krylov", "green", "network")
+
+
+def install_as_helmsolve() -> None:
+    """Register this package as ``helmsolve`` (and ``helmsolve.<module>``) in sys.modules.
+
+    Code written against the reference (``from helmsolve.krylov import ...``)
+    then runs on the B200 path unchanged.
+    """
+    pkg = sys.modules[__name__]
+    sys.modules["helmsolve"] = pkg
+    for name in _MIRRORED:
+        sys.modules[f"helmsolve.{name}"] = importlib.import_module(f"{__name__}.{name}")

@@ -1,0 +1,57 @@
+"""Data-parallel plumbing: independent RHS / slowness models sharded over ranks.
+
+The solve has no exchange step: every (model, RHS) pair is
+independent, so ranks never communicate on the data path.  One process per
+GPU, ``torch.distributed`` (NCCL on GPUs, gloo in the CPU tests) is used only
+to time the job as the max over ranks and to gather per-RHS reports.
+"""
+from __future__ import annotations
+
+import os
+
+
+def rank_world() -> tuple[int, int, int]:
+    """(rank, world_size, local_rank) from the torchrun environment."""
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced [start, stop) share of n items for `rank`."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+    base, extra = divmod(n, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def _device():
+    import torch
+    import torch.distributed as dist
+
+    if dist.get_backend() == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def reduce_scalar(value: float, op: str = "max") -> float:
+    """All-reduce one float (max or sum) across ranks; identity without a process group."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_device())
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def gather_reports(local: list) -> list:
+    """Concatenate every rank's list (e.g. per-RHS SolveReports) in rank order."""
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return list(local)
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, list(local))
+    return [item for part in out for item in part]
