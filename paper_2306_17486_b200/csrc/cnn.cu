@@ -399,11 +399,10 @@ int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* 
     if (c.cin == 16 && c.cout == 2) return launch_thin<16, 2>(a, B, st), HS_OK;
     if (c.cin == 8 && c.cout == 2) return launch_thin<8, 2>(a, B, st), HS_OK;
   }
-  if (conv_tc_supported(c.cin, c.cout, c.stride, c.transposed, H, W, a.Wo)) {
-    conv_tc_launch(a.x, a.H, a.W, a.cin, a.y, a.Ho, a.Wo, a.cout, c.stride, c.transposed, a.w, a.bias, a.softplus,
-                   a.addend, a.addend_bstride, a.addend_per_model, a.model_of, a.residual, a.active, B, st);
+  if (conv_tc_supported(c.cin, c.cout, c.stride, c.transposed, H, W, a.Wo) &&
+      conv_tc_launch(a.x, a.H, a.W, a.cin, a.y, a.Ho, a.Wo, a.cout, c.stride, c.transposed, a.w, a.bias, a.softplus,
+                     a.addend, a.addend_bstride, a.addend_per_model, a.model_of, a.residual, a.active, B, st))
     return HS_OK;
-  }
 #define HS_CONV_CASE(CO)                          \
   case CO:                                        \
     if (c.transposed)                             \

@@ -1,23 +1,23 @@
 // tcgen05 implicit-GEMM 3x3 convolution with fp32-class accuracy (BF16x3).
 //
-// GEMM view of one output tile: D[m][n] = sum_k A[m][k] B[n][k] with m = 128
-// consecutive output pixels of one row, n = cout, k = (tap, cin).  Input rows
-// are staged in shared memory in the UMMA K-major "interleaved" canonical
-// layout (core matrix = 8 pixels x 16 bytes, pixels consecutive at a 16-byte
-// pitch, 8-channel chunks LBO apart).  Because pixels sit at a 16-byte pitch,
-// the A operand of tap (ky, kx) is just the staged row with the descriptor
-// start address moved by kx * 16 bytes: no im2col copies.  Stride-2
-// convolutions stage each input row de-interleaved (even columns, then odd
-// columns) so every tap is again a unit-pitch window; the transposed
-// convolution is split into its two column-parity classes (1 and 2 taps)
-// with two TMEM accumulators.
+// GEMM view of one output tile: D[m][n] = sum_k A[m][k] B[n][k] with m = MT
+// (128 or 64) consecutive output pixels of one row, n = output channels of
+// this CTA's cout slice, k = (tap, cin).  Input rows are staged in shared
+// memory in the UMMA K-major "interleaved" canonical layout (core matrix =
+// 8 pixels x 16 bytes, pixels consecutive at a 16-byte pitch, 8-channel chunks
+// LBO apart).  Because pixels sit at a 16-byte pitch, the A operand of tap
+// (ky, kx) is just the staged row with the descriptor start address moved by
+// kx * 16 bytes: no im2col copies.  Stride-2 convolutions stage each input
+// row de-interleaved (even columns, then odd columns) so every tap is again a
+// unit-pitch window; the transposed convolution is split into its two
+// column-parity classes (1 and 2 taps) with two TMEM accumulators.
 //
 // Precision (SURVEY.md §0.5 rules out plain TF32/BF16): every fp32 operand is
 // split exactly into three bf16 parts x = x0 + x1 + x2 (8+8+8 mantissa bits)
 // and the six products with weight >= 2^-16 are accumulated in fp32 TMEM:
-//   A0 [W0 | W1 | W2]  (N = 3 cout),  A1 [W0 | W1]  (N = 2 cout),  A2 W0  (N = cout)
+//   A0 [W0 | W1 | W2]  (N = 3 cs),  A1 [W0 | W1]  (N = 2 cs),  A2 W0  (N = cs)
 // The weight parts are stacked along N, so each activation part is read from
-// shared memory once per K step (cout = 16 makes these MMAs operand-bound,
+// shared memory once per K step (thin cout makes these MMAs operand-bound,
 // not math-bound); the epilogue sums the three column groups.
 //
 // Warp-specialised pipeline (one persistent CTA per SM, weights resident):
@@ -31,8 +31,11 @@
 //   warps 0-3        epilogue  : tcgen05.ld of their TMEM lane quarter, then
 //                                bias, softplus, encoder/skip addend,
 //                                residual, NHWC stores
-// A CTA walks a band of output rows of one 128-pixel column block top to
-// bottom, so every input row is fetched and split once per band.
+// A CTA walks a band of output rows of one MT-pixel column block top to
+// bottom, so every input row is fetched and split once per band.  Wide
+// layers split cout across CTAs (CS channels each) so the resident bf16x3
+// weights fit in shared memory.  M = 64 tiles use the half-lane TMEM layout
+// (tile row m -> lane 32*(m/16) + m%16).
 #include <cuda_bf16.h>
 
 #include <cstdio>
@@ -44,11 +47,11 @@ namespace hs {
 namespace {
 
 constexpr int kNT = 256;  // 8 warps
-constexpr int kM = 128;   // pixels per tile (UMMA M)
 constexpr int kBand = 32; // output rows per work unit
 constexpr int kNA = 4;    // TMEM accumulators in flight
 constexpr int kEpiWarps = 4, kCvtWarp0 = 4, kCvtWarps = 2, kProdWarp = 6, kMmaWarp = 7;
 constexpr int kCvtThreads = 32 * kCvtWarps;
+constexpr size_t kSmemMax = 232448;
 
 HS_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -151,26 +154,46 @@ struct TcArgs {
   int B;
 };
 
-// MODE 0: stride 1; MODE 1: stride 2; MODE 2: transposed stride 2 (out = 2 x in)
-template <int CIN, int COUT, int MODE>
+// MODE 0: stride 1; MODE 1: stride 2; MODE 2: transposed stride 2 (out = 2 x in).
+// MT: pixels per tile (UMMA M, 128 or 64); CS: output channels per CTA.
+template <int CIN, int COUT, int MODE, int MT, int CS>
 struct Cfg {
+  static constexpr int NSPLIT = COUT / CS;
   static constexpr int KC = CIN / 8;                                                // 16-byte chunks per part
   static constexpr int KSTEPS = CIN / 16;                                           // MMA K steps per tap
-  static constexpr int RW = MODE == 0 ? kM + 2 : (MODE == 1 ? 2 * kM + 1 : kM + 1); // pixels per staged row
+  static constexpr int RW = MODE == 0 ? MT + 2 : (MODE == 1 ? 2 * MT + 1 : MT + 1); // pixels per staged row
   static constexpr int NACC = MODE == 2 ? 2 : 1;  // accumulators per tile (column-parity classes)
-  static constexpr int NS = MODE == 0 ? (CIN == 16 ? 6 : 4) : (MODE == 1 ? 5 : 4);  // staged ring depth
-  static constexpr int NR = (MODE == 0 && CIN == 16) ? 4 : 2;                          // raw ring depth
+  static constexpr int RAW_BYTES = RW * CIN * 4;
+  static constexpr int NW = 3 * CS;                            // stacked weight rows [W0; W1; W2]
+  static constexpr size_t W_BYTES = (size_t)9 * KC * NW * 16;
+  static constexpr int NS_MIN = 3, NS_MAX = MODE == 0 ? 6 : (MODE == 1 ? 5 : 4);
+  static constexpr size_t row_stage_bytes(int ns) {
+    return (size_t)3 * KC * 16 * (ns * RW + ((9 - ((ns * RW) & 7)) & 7));
+  }
+  static constexpr size_t total(int ns, int nr) {
+    return W_BYTES + row_stage_bytes(ns) + (size_t)nr * RAW_BYTES + 8 * (2 * nr + 2 * ns + 2 * kNA) + 16;
+  }
+  // deepest rings that fit: raw ring 4..2, staged ring NS_MAX..3
+  static constexpr int pick_nr() {
+    for (int nr = 4; nr >= 2; --nr)
+      if (total(NS_MIN, nr) <= kSmemMax && total(NS_MAX < 4 ? NS_MAX : 4, nr) <= kSmemMax) return nr;
+    return 2;
+  }
+  static constexpr int NR = pick_nr();
+  static constexpr int pick_ns() {
+    for (int ns = NS_MAX; ns > NS_MIN; --ns)
+      if (total(ns, NR) <= kSmemMax) return ns;
+    return NS_MIN;
+  }
+  static constexpr int NS = pick_ns();
   static constexpr int XPL0 = NS * RW;
   static constexpr int XPL = XPL0 + ((9 - (XPL0 & 7)) & 7);  // == 1 mod 8: conflict-free chunk planes
-  static constexpr int RAW_BYTES = RW * CIN * 4;
-  static constexpr int NW = 3 * COUT;                         // stacked weight rows [W0; W1; W2]
-  static constexpr size_t W_BYTES = (size_t)9 * KC * NW * 16;
   static constexpr size_t XP_BYTES = (size_t)KC * XPL * 16;   // one activation part
   static constexpr size_t R_BYTES = (size_t)NR * RAW_BYTES;
-  static constexpr int NBAR = 2 * NR + 2 * NS + 2 * kNA;
-  static constexpr size_t TOTAL = W_BYTES + 3 * XP_BYTES + R_BYTES + 8 * NBAR + 16;
+  static constexpr size_t TOTAL = total(NS, NR);
   static constexpr int ACOLS = NW * NACC;  // TMEM columns per accumulator
-  static constexpr int NCOLS_RAW = kNA * ACOLS;
+  static constexpr int NA = 4 * ACOLS <= 512 ? 4 : 2;  // accumulators in flight (TMEM = 512 columns)
+  static constexpr int NCOLS_RAW = NA * ACOLS;
   static constexpr int NCOLS = NCOLS_RAW <= 32    ? 32
                                : NCOLS_RAW <= 64  ? 64
                                : NCOLS_RAW <= 128 ? 128
@@ -194,32 +217,34 @@ __host__ __device__ inline void tile_rows(int oy, int& lo, int& hi) {
 }
 
 // first input column of the raw row segment of column block xb
-template <int MODE>
+template <int MODE, int MT>
 HS_DEV int raw_x0(int xb) {
-  return MODE == 0 ? xb * kM - 1 : (MODE == 1 ? 2 * xb * kM - 1 : xb * kM);
+  return MODE == 0 ? xb * MT - 1 : (MODE == 1 ? 2 * xb * MT - 1 : xb * MT);
 }
 
 // raw pixel p -> staged pixel (stride 2 de-interleaves even / odd columns)
-template <int MODE>
+template <int MODE, int MT>
 HS_DEV int staged_px(int p) {
   if (MODE != 1) return p;
-  return (p & 1) ? (p - 1) >> 1 : kM + (p >> 1);  // column 2x0-1+p: odd p is an even column
+  return (p & 1) ? (p - 1) >> 1 : MT + (p >> 1);  // column 2x0-1+p: odd p is an even column
 }
 
 struct Unit {
-  int b, xb, oy0, oy1, glo, ghi;  // rows [oy0, oy1), input rows [glo, ghi]
+  int split, b, xb, oy0, oy1, glo, ghi;  // cout slice, rows [oy0, oy1), input rows [glo, ghi]
 };
 
-template <int MODE>
-__host__ __device__ inline long long num_units(const TcArgs& a) {
-  const int xblocks = MODE == 2 ? a.W / kM : a.Wo / kM;
-  return (long long)a.B * xblocks * ((a.Ho + kBand - 1) / kBand);
+template <int MODE, int MT>
+__host__ __device__ inline long long num_units(const TcArgs& a, int nsplit) {
+  const int xblocks = MODE == 2 ? a.W / MT : a.Wo / MT;
+  return (long long)nsplit * a.B * xblocks * ((a.Ho + kBand - 1) / kBand);
 }
 
-template <int MODE>
-HS_DEV bool unit_at(const TcArgs& a, long long u, Unit& U) {
-  const int xblocks = MODE == 2 ? a.W / kM : a.Wo / kM;
+template <int MODE, int MT>
+HS_DEV bool unit_at(const TcArgs& a, int nsplit, long long u, Unit& U) {
+  const int xblocks = MODE == 2 ? a.W / MT : a.Wo / MT;
   const int nbands = (a.Ho + kBand - 1) / kBand;
+  U.split = (int)(u % nsplit);  // slices of one band run side by side: the input rows are reused from L2
+  u /= nsplit;
   U.xb = (int)(u % xblocks);
   const int band = (int)((u / xblocks) % nbands);
   U.b = (int)(u / ((long long)xblocks * nbands));
@@ -239,11 +264,11 @@ struct DescBase {
   uint64_t x[3], w;
 };
 
-template <int CIN, int COUT, int MODE>
+template <typename C, int MT>
 HS_DEV void tap_mmas(uint32_t d, const DescBase& db, uint32_t x_units, uint32_t w_units, uint32_t& first) {
-  using C = Cfg<CIN, COUT, MODE>;
   constexpr uint32_t X_STEP = 2 * C::XPL, W_STEP = 2 * C::NW;  // two 16-byte chunks per K step
-  constexpr uint32_t I0 = idesc_bf16(kM, 3 * COUT), I1 = idesc_bf16(kM, 2 * COUT), I2 = idesc_bf16(kM, COUT);
+  constexpr int CS = C::NW / 3;
+  constexpr uint32_t I0 = idesc_bf16(MT, 3 * CS), I1 = idesc_bf16(MT, 2 * CS), I2 = idesc_bf16(MT, CS);
 #pragma unroll
   for (int kk = 0; kk < C::KSTEPS; ++kk) {
     const uint64_t xo = x_units + kk * X_STEP, wo = db.w + w_units + kk * W_STEP;
@@ -255,9 +280,8 @@ HS_DEV void tap_mmas(uint32_t d, const DescBase& db, uint32_t x_units, uint32_t 
 }
 
 // all MMAs of output row oy; slot(g) = staged slot holding input row g
-template <int CIN, int COUT, int MODE, typename SlotOf>
+template <typename C, int MODE, int MT, typename SlotOf>
 HS_DEV void issue_mmas(int oy, uint32_t d0, const DescBase& db, SlotOf slot) {
-  using C = Cfg<CIN, COUT, MODE>;
   constexpr uint32_t WT = C::KC * C::NW;  // weight units per tap
   auto row_units = [&](int g) { return (uint32_t)(slot(g) * C::RW); };
   uint32_t first = 1;
@@ -268,8 +292,8 @@ HS_DEV void issue_mmas(int oy, uint32_t d0, const DescBase& db, SlotOf slot) {
       const uint32_t r = row_units(g0 + ky);
 #pragma unroll
       for (int kx = 0; kx < 3; ++kx) {
-        const uint32_t px = MODE == 0 ? kx : (kx == 1 ? 0 : (kx == 0 ? kM : kM + 1));
-        tap_mmas<CIN, COUT, MODE>(d0, db, r + px, (ky * 3 + kx) * WT, first);
+        const uint32_t px = MODE == 0 ? kx : (kx == 1 ? 0 : (kx == 0 ? MT : MT + 1));
+        tap_mmas<C, MT>(d0, db, r + px, (ky * 3 + kx) * WT, first);
       }
     }
     return;
@@ -280,25 +304,25 @@ HS_DEV void issue_mmas(int oy, uint32_t d0, const DescBase& db, SlotOf slot) {
   const uint32_t rq = row_units(q), rq1 = row_units(q + 1);
   const uint32_t d1 = d0 + C::NW;
   if ((oy & 1) == 0) {
-    tap_mmas<CIN, COUT, MODE>(d0, db, rq, (1 * 3 + 1) * WT, first);
+    tap_mmas<C, MT>(d0, db, rq, (1 * 3 + 1) * WT, first);
     first = 1;
-    tap_mmas<CIN, COUT, MODE>(d1, db, rq + 1, (1 * 3 + 0) * WT, first);
-    tap_mmas<CIN, COUT, MODE>(d1, db, rq, (1 * 3 + 2) * WT, first);
+    tap_mmas<C, MT>(d1, db, rq + 1, (1 * 3 + 0) * WT, first);
+    tap_mmas<C, MT>(d1, db, rq, (1 * 3 + 2) * WT, first);
   } else {
-    tap_mmas<CIN, COUT, MODE>(d0, db, rq1, (0 * 3 + 1) * WT, first);
-    tap_mmas<CIN, COUT, MODE>(d0, db, rq, (2 * 3 + 1) * WT, first);
+    tap_mmas<C, MT>(d0, db, rq1, (0 * 3 + 1) * WT, first);
+    tap_mmas<C, MT>(d0, db, rq, (2 * 3 + 1) * WT, first);
     first = 1;
-    tap_mmas<CIN, COUT, MODE>(d1, db, rq1 + 1, (0 * 3 + 0) * WT, first);
-    tap_mmas<CIN, COUT, MODE>(d1, db, rq1, (0 * 3 + 2) * WT, first);
-    tap_mmas<CIN, COUT, MODE>(d1, db, rq + 1, (2 * 3 + 0) * WT, first);
-    tap_mmas<CIN, COUT, MODE>(d1, db, rq, (2 * 3 + 2) * WT, first);
+    tap_mmas<C, MT>(d1, db, rq1 + 1, (0 * 3 + 0) * WT, first);
+    tap_mmas<C, MT>(d1, db, rq1, (0 * 3 + 2) * WT, first);
+    tap_mmas<C, MT>(d1, db, rq + 1, (2 * 3 + 0) * WT, first);
+    tap_mmas<C, MT>(d1, db, rq, (2 * 3 + 2) * WT, first);
   }
 }
 
-template <int CIN, int COUT, int MODE>
+template <int CIN, int COUT, int MODE, int MT, int CS>
 __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
-  using C = Cfg<CIN, COUT, MODE>;
-  constexpr int KC = C::KC, NS = C::NS, NR = C::NR, NW = C::NW;
+  using C = Cfg<CIN, COUT, MODE, MT, CS>;
+  constexpr int KC = C::KC, NS = C::NS, NR = C::NR, NW = C::NW, NSPLIT = C::NSPLIT;
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* wst = smem;
   unsigned char* xp[3] = {smem + C::W_BYTES, smem + C::W_BYTES + C::XP_BYTES, smem + C::W_BYTES + 2 * C::XP_BYTES};
@@ -309,21 +333,25 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
   uint64_t* stg_full = raw_empty + NR;
   uint64_t* stg_empty = stg_full + NS;
   uint64_t* acc_full = stg_empty + NS;
-  uint64_t* acc_empty = acc_full + kNA;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(acc_empty + kNA);
+  uint64_t* acc_empty = acc_full + C::NA;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(acc_empty + C::NA);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long nunits = num_units<MODE, MT>(a, NSPLIT);
+  // a persistent CTA keeps one cout slice: its units are u = blockIdx.x + k gridDim.x
+  // with gridDim.x a multiple of NSPLIT, so u % NSPLIT is fixed per CTA
+  const int my_split = (int)(blockIdx.x % NSPLIT);
 
-  // ---- setup: resident weight stack [W0; W1; W2], layout (tap, chunk, row) x 16 B
-  for (int e = tid; e < 9 * KC * COUT; e += kNT) {
-    const int n = e % COUT, c = (e / COUT) % KC, t = e / (COUT * KC);
-    const float* src = a.w + ((size_t)n * 9 + t) * CIN + 8 * c;
+  // ---- setup: resident weight stack [W0; W1; W2] of this slice, layout (tap, chunk, row) x 16 B
+  for (int e = tid; e < 9 * KC * CS; e += kNT) {
+    const int n = e % CS, c = (e / CS) % KC, t = e / (CS * KC);
+    const float* src = a.w + ((size_t)(my_split * CS + n) * 9 + t) * CIN + 8 * c;
     const float4 v0 = __ldg(reinterpret_cast<const float4*>(src)), v1 = __ldg(reinterpret_cast<const float4*>(src + 4));
     const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
     uint4 p[3];
     split_bf16x3(v, p[0], p[1], p[2]);
 #pragma unroll
     for (int part = 0; part < 3; ++part)
-      *reinterpret_cast<uint4*>(wst + ((size_t)(t * KC + c) * NW + part * COUT + n) * 16) = p[part];
+      *reinterpret_cast<uint4*>(wst + ((size_t)(t * KC + c) * NW + part * CS + n) * 16) = p[part];
   }
   if (tid == 0) {
     for (int i = 0; i < NR; ++i) {
@@ -334,7 +362,7 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
       mbar_init(smem_u32(&stg_full[i]), kCvtThreads);
       mbar_init(smem_u32(&stg_empty[i]), 1);
     }
-    for (int i = 0; i < kNA; ++i) {
+    for (int i = 0; i < C::NA; ++i) {
       mbar_init(smem_u32(&acc_full[i]), 1);
       mbar_init(smem_u32(&acc_empty[i]), 32 * kEpiWarps);
     }
@@ -350,7 +378,6 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
-  const long long nunits = num_units<MODE>(a);
 
   if (warp == kProdWarp) {
     // ================= producer: raw row segments, global -> smem (bulk copies)
@@ -358,8 +385,8 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
       long long seq = 0;
       for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
         Unit U;
-        if (!unit_at<MODE>(a, u, U)) continue;
-        const int x0 = raw_x0<MODE>(U.xb);
+        if (!unit_at<MODE, MT>(a, NSPLIT, u, U)) continue;
+        const int x0 = raw_x0<MODE, MT>(U.xb);
         const int clo = max(x0, 0), chi = min(x0 + C::RW, a.W);
         const float* img = a.x + (size_t)U.b * a.H * a.W * CIN;
         for (int g = U.glo; g <= U.ghi; ++g, ++seq) {
@@ -384,8 +411,8 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
     long long seq = 0;
     for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
-      if (!unit_at<MODE>(a, u, U)) continue;
-      const int x0 = raw_x0<MODE>(U.xb);
+      if (!unit_at<MODE, MT>(a, NSPLIT, u, U)) continue;
+      const int x0 = raw_x0<MODE, MT>(U.xb);
       const int clo = max(x0, 0) - x0, chi = min(x0 + C::RW, a.W) - x0;  // valid raw pixels [clo, chi)
       for (int g = U.glo; g <= U.ghi; ++g, ++seq) {
         const int rs = (int)(seq % NR), ss = (int)(seq % NS);
@@ -404,7 +431,7 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
           }
           uint4 p3[3];
           split_bf16x3(v, p3[0], p3[1], p3[2]);
-          const size_t off = ((size_t)c * C::XPL + ss * C::RW + staged_px<MODE>(p)) * 16;
+          const size_t off = ((size_t)c * C::XPL + ss * C::RW + staged_px<MODE, MT>(p)) * 16;
 #pragma unroll
           for (int part = 0; part < 3; ++part) *reinterpret_cast<uint4*>(xp[part] + off) = p3[part];
         }
@@ -424,7 +451,7 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
       long long tile = 0;
       for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
         Unit U;
-        if (!unit_at<MODE>(a, u, U)) continue;
+        if (!unit_at<MODE, MT>(a, NSPLIT, u, U)) continue;
         auto slot = [&](int g) { return (int)((seq0 + (g - U.glo)) % NS); };
         int waited = U.glo - 1;   // highest input row known to be staged
         int retired = U.glo - 1;  // highest input row released back to the converters
@@ -436,11 +463,11 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
             mbar_wait(smem_u32(&stg_full[sq % NS]), (uint32_t)((sq / NS) & 1));
           }
           waited = max(waited, hi);
-          const int acc = (int)(tile % kNA);
-          const long long ause = tile / kNA;
+          const int acc = (int)(tile % C::NA);
+          const long long ause = tile / C::NA;
           if (ause > 0) mbar_wait(smem_u32(&acc_empty[acc]), (uint32_t)((ause - 1) & 1));
           tc_fence_after();
-          issue_mmas<CIN, COUT, MODE>(oy, tmem + acc * C::ACOLS, db, slot);
+          issue_mmas<C, MODE, MT>(oy, tmem + acc * C::ACOLS, db, slot);
           mma_commit(smem_u32(&acc_full[acc]));
           // release rows the next tile of this unit no longer reads
           int keep_lo = U.ghi + 1;
@@ -456,32 +483,43 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
       }
     }
   } else {
-    // ================= epilogue warps 0-3: TMEM lane quarter = warp
-    const int m = warp * 32 + lane;
+    // ================= epilogue warps 0-3: TMEM lane quarter = warp.
+    // M = 128: tile row m = TMEM lane m.  M = 64: rows 16w..16w+15 sit in the
+    // first 16 lanes of quarter w (the other 16 lanes are idle).
+    const bool lane_ok = MT == 128 || lane < 16;
+    const int m = MT == 128 ? warp * 32 + lane : warp * 16 + (lane & 15);
     long long tile = 0;
     for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
-      if (!unit_at<MODE>(a, u, U)) continue;
+      if (!unit_at<MODE, MT>(a, NSPLIT, u, U)) continue;
+      const int n_base = U.split * CS;
       const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[U.b] : 0) : U.b) *
                                                    a.addend_bstride
                                   : nullptr;
       for (int oy = U.oy0; oy < U.oy1; ++oy, ++tile) {
-        const int acc = (int)(tile % kNA);
-        // addend / residual do not depend on the accumulator: fetch them before waiting on the MMA
-        float4 pre_add[C::NACC][COUT / 4], pre_res[C::NACC][COUT / 4];
+        const int acc = (int)(tile % C::NA);
+        // addend + residual do not depend on the accumulator: fetch (and sum) them before waiting on the MMA
+        float4 pre[C::NACC][CS / 4];
 #pragma unroll
         for (int k = 0; k < C::NACC; ++k) {
-          const int ox = MODE == 2 ? 2 * (U.xb * kM + m) + k : U.xb * kM + m;
+          const int ox = MODE == 2 ? 2 * (U.xb * MT + m) + k : U.xb * MT + m;
           const size_t pix = (size_t)oy * a.Wo + ox;
-          const size_t obase = (size_t)U.b * a.Ho * a.Wo * COUT + pix * COUT;
+          const size_t obase = (size_t)U.b * a.Ho * a.Wo * COUT + pix * COUT + n_base;
 #pragma unroll
-          for (int q = 0; q < COUT / 4; ++q) {
-            pre_add[k][q] = add ? __ldg(reinterpret_cast<const float4*>(add + pix * COUT) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-            pre_res[k][q] = a.residual ? __ldg(reinterpret_cast<const float4*>(a.residual + obase) + q)
-                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int q = 0; q < CS / 4; ++q) {
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (add && lane_ok) v = __ldg(reinterpret_cast<const float4*>(add + pix * COUT + n_base) + q);
+            if (a.residual && lane_ok) {
+              const float4 rs = __ldg(reinterpret_cast<const float4*>(a.residual + obase) + q);
+              v.x += rs.x;
+              v.y += rs.y;
+              v.z += rs.z;
+              v.w += rs.w;
+            }
+            pre[k][q] = v;
           }
         }
-        mbar_wait(smem_u32(&acc_full[acc]), (uint32_t)((tile / kNA) & 1));
+        mbar_wait(smem_u32(&acc_full[acc]), (uint32_t)((tile / C::NA) & 1));
         tc_fence_after();
         uint32_t r[C::NACC][NW];
 #pragma unroll
@@ -493,28 +531,29 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(smem_u32(&acc_empty[acc]));  // TMEM free; finish from registers
+        if (!lane_ok) continue;
 #pragma unroll
         for (int k = 0; k < C::NACC; ++k) {
-          const int ox = MODE == 2 ? 2 * (U.xb * kM + m) + k : U.xb * kM + m;
+          const int ox = MODE == 2 ? 2 * (U.xb * MT + m) + k : U.xb * MT + m;
           const size_t pix = (size_t)oy * a.Wo + ox;
-          const size_t obase = (size_t)U.b * a.Ho * a.Wo * COUT + pix * COUT;
+          const size_t obase = (size_t)U.b * a.Ho * a.Wo * COUT + pix * COUT + n_base;
 #pragma unroll
-          for (int n0 = 0; n0 < COUT; n0 += 4) {
+          for (int n0 = 0; n0 < CS; n0 += 4) {
             float4 o;
             float* po = &o.x;
 #pragma unroll
             for (int u4 = 0; u4 < 4; ++u4) {
               const int n = n0 + u4;
               // the three column groups hold the x0-, x1- and x2-weighted partial sums
-              const float t = (__uint_as_float(r[k][n]) + __uint_as_float(r[k][COUT + n])) +
-                              __uint_as_float(r[k][2 * COUT + n]) + __ldg(a.bias + n);
+              const float t = (__uint_as_float(r[k][n]) + __uint_as_float(r[k][CS + n])) +
+                              __uint_as_float(r[k][2 * CS + n]) + __ldg(a.bias + n_base + n);
               po[u4] = a.softplus ? softplus_f(t) : t;
             }
-            const float4 ad = pre_add[k][n0 / 4], rs = pre_res[k][n0 / 4];
-            o.x += ad.x + rs.x;
-            o.y += ad.y + rs.y;
-            o.z += ad.z + rs.z;
-            o.w += ad.w + rs.w;
+            const float4 ad = pre[k][n0 / 4];
+            o.x += ad.x;
+            o.y += ad.y;
+            o.z += ad.z;
+            o.w += ad.w;
             *reinterpret_cast<float4*>(a.y + obase + n0) = o;
           }
         }
@@ -529,21 +568,36 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
   }
 }
 
-template <int CIN, int COUT, int MODE>
+template <int CIN, int COUT, int MODE, int MT, int CS>
 void launch_tc(const TcArgs& a, cudaStream_t st) {
-  using C = Cfg<CIN, COUT, MODE>;
-  static_assert(C::TOTAL <= 232448, "shared memory budget");
+  using C = Cfg<CIN, COUT, MODE, MT, CS>;
+  static_assert(C::TOTAL <= kSmemMax, "shared memory budget");
   static_assert(C::NCOLS_RAW <= 512, "TMEM budget");
+  static_assert(COUT % CS == 0 && CS % 16 == 0, "cout slices");
   static int sms = 0;
   if (!sms) {
-    cudaFuncSetAttribute(k_conv_tc<CIN, COUT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::TOTAL);
+    cudaFuncSetAttribute(k_conv_tc<CIN, COUT, MODE, MT, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::TOTAL);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const long long nunits = num_units<MODE>(a);
-  const int grid = (int)(nunits < sms ? nunits : sms);
-  k_conv_tc<CIN, COUT, MODE><<<grid, kNT, C::TOTAL, st>>>(a);
+  const long long nunits = num_units<MODE, MT>(a, C::NSPLIT);
+  long long grid = (sms / C::NSPLIT) * C::NSPLIT;  // a multiple of NSPLIT: fixed slice per CTA
+  if (nunits < grid) grid = nunits;
+  k_conv_tc<CIN, COUT, MODE, MT, CS><<<(unsigned)grid, kNT, C::TOTAL, st>>>(a);
+}
+
+// (cin, cout, mode) -> cout slice per CTA, or 0 if not on the tensor-core path
+int slice_for(int cin, int cout, int mode) {
+  if (mode == 0 && cin == 16 && cout == 16) return 16;
+  if (mode == 0 && cin == 32 && cout == 32) return 32;
+  if (mode == 0 && cin == 64 && cout == 64) return 32;
+  if (mode == 1 && cin == 16 && cout == 32) return 32;
+  if (mode == 1 && cin == 32 && cout == 64) return 32;
+  if (mode == 2 && cin == 32 && cout == 16) return 16;
+  if (mode == 2 && cin == 64 && cout == 32) return 32;
+  return 0;
 }
 
 }  // namespace
@@ -555,23 +609,34 @@ bool conv_tc_supported(int cin, int cout, int stride, int transposed, int H, int
   if (!conv_tc_enabled) return false;
   const int mode = transposed ? 2 : (stride == 2 ? 1 : 0);
   const int width = mode == 2 ? W : Wo;
-  if (width % kM) return false;
-  if (mode == 0) return (cin == 16 && cout == 16) || (cin == 32 && cout == 32);
-  if (mode == 1) return cin == 16 && cout == 32;
-  return cin == 32 && cout == 16;
+  if (width % 64) return false;
+  return slice_for(cin, cout, mode) > 0;
 }
 
-void conv_tc_launch(const float* x, int H, int W, int cin, float* y, int Ho, int Wo, int cout, int stride,
+bool conv_tc_launch(const float* x, int H, int W, int cin, float* y, int Ho, int Wo, int cout, int stride,
                     int transposed, const float* w, const float* bias, int softplus, const float* addend,
                     long long addend_bstride, int addend_per_model, const int* model_of, const float* residual,
                     const void* const* active, int B, cudaStream_t st) {
   TcArgs a{x, H, W, y, Ho, Wo, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual,
            active, B};
   const int mode = transposed ? 2 : (stride == 2 ? 1 : 0);
-  if (mode == 0 && cin == 16 && cout == 16) launch_tc<16, 16, 0>(a, st);
-  else if (mode == 0 && cin == 32 && cout == 32) launch_tc<32, 32, 0>(a, st);
-  else if (mode == 1 && cin == 16 && cout == 32) launch_tc<16, 32, 1>(a, st);
-  else if (mode == 2 && cin == 32 && cout == 16) launch_tc<32, 16, 2>(a, st);
+  const bool m128 = ((mode == 2 ? W : Wo) % 128) == 0;
+#define HS_TC(CI, CO, MD, CSL)                                           \
+  if (mode == MD && cin == CI && cout == CO) {                           \
+    if (m128) launch_tc<CI, CO, MD, 128, CSL>(a, st);                    \
+    else launch_tc<CI, CO, MD, 64, CSL>(a, st);                          \
+    return true;                                                         \
+  }
+  HS_TC(16, 16, 0, 16)
+  HS_TC(32, 32, 0, 32)
+  HS_TC(16, 32, 1, 32)
+  HS_TC(32, 16, 2, 16)
+  // 64-channel inputs / outputs: M = 64 tiles only (the M = 128 staging does not fit next to the weights)
+  if (mode == 0 && cin == 64 && cout == 64) return launch_tc<64, 64, 0, 64, 32>(a, st), true;
+  if (mode == 1 && cin == 32 && cout == 64) return launch_tc<32, 64, 1, 64, 32>(a, st), true;
+  if (mode == 2 && cin == 64 && cout == 32) return launch_tc<64, 32, 2, 64, 32>(a, st), true;
+#undef HS_TC
+  return false;
 }
 
 }  // namespace hs

@@ -73,7 +73,11 @@ def test_tconv_shapes(rng, cin, cout, hw):
 
 
 @pytest.mark.parametrize("cin,cout,mode,hw", [(16, 16, 0, (6, 128)), (16, 16, 0, (5, 256)), (32, 32, 0, (4, 128)),
-                                               (16, 32, 1, (6, 256)), (32, 16, 2, (3, 128)), (32, 16, 2, (2, 256))])
+                                               (16, 32, 1, (6, 256)), (32, 16, 2, (3, 128)), (32, 16, 2, (2, 256)),
+                                               # M = 64 tiles (64-wide levels) and cout split across CTAs
+                                               (16, 16, 0, (5, 64)), (32, 32, 0, (3, 64)), (64, 64, 0, (4, 64)),
+                                               (64, 64, 0, (3, 192)), (32, 64, 1, (5, 128)), (16, 32, 1, (4, 128)),
+                                               (64, 32, 2, (3, 64)), (32, 16, 2, (2, 64))])
 def test_tcgen05_conv_matches_oracle(rng, cin, cout, mode, hw):
     """The tcgen05 3xTF32 path (taken for widths that are multiples of 128) against the fp32 oracle."""
     from paper_2306_17486_b200 import _lib
