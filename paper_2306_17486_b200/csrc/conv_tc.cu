@@ -56,26 +56,34 @@ constexpr size_t kSmemMax = 232448;
 HS_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // UMMA shared-memory descriptor, K-major, SWIZZLE_NONE (version 1 = sm_100)
-HS_DEV uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
-}
+// low word: start address >> 4 (bits 0-13) | LBO >> 4 (bits 16-29); high word: SBO >> 4 | version 1 (bit 46)
+HS_DEV uint32_t desc_lo(uint32_t saddr, uint32_t lbo) { return ((saddr >> 4) & 0x3FFFu) | (((lbo >> 4) & 0x3FFFu) << 16); }
+constexpr uint32_t kDescHi = ((128u >> 4) & 0x3FFFu) | (1u << 14);  // SBO = 128 B (8 rows x 16 B)
 
 // instruction descriptor, kind::f16: D f32, A/B bf16, both K-major, M x N
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-HS_DEV void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+// The issuing warp runs converged and every operand is warp-uniform, so ptxas
+// keeps them in uniform registers; elect.sync picks the one issuing lane.
+// Descriptors are passed as (lo, hi) words: the start address lives in the
+// low word, the layout bits (LBO, SBO, version) in compile-time constants.
+HS_DEV void mma_bf16(uint32_t tmem_d, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo, uint32_t b_hi, uint32_t idesc,
+                     uint32_t accumulate) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 da, db;\n\t"
+      "mov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"
+      "setp.ne.b32 p, %6, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate));
 }
 
 HS_DEV void mma_commit(uint32_t mbar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar)
-               : "memory");
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(mbar)
+      : "memory");
 }
 
 HS_DEV void mbar_init(uint32_t mbar, uint32_t count) {
@@ -135,7 +143,14 @@ HS_DEV void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
 }
 HS_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-HS_DEV float softplus_f(float x) { return fmaxf(x, 0.f) + log1pf(expf(-fabsf(x))); }
+// softplus(x) = max(x, 0) + log1p(e), e = exp(-|x|) in (0, 1]: MUFU exp / log
+// with a short series for small e (absolute error ~2e-7, the fp32 class of
+// the reference's np.logaddexp; the tests hold the layer to 2e-6 relative).
+HS_DEV float softplus_f(float x) {
+  const float e = __expf(-fabsf(x));
+  const float series = e * fmaf(e, fmaf(e, fmaf(e, -0.25f, 0.33333334f), -0.5f), 1.0f);  // error < e^5 / 5
+  return fmaxf(x, 0.f) + (e < 0.03125f ? series : __logf(1.0f + e));
+}
 
 struct TcArgs {
   const float* x;
@@ -171,7 +186,7 @@ struct Cfg {
     return (size_t)3 * KC * 16 * (ns * RW + ((9 - ((ns * RW) & 7)) & 7));
   }
   static constexpr size_t total(int ns, int nr) {
-    return W_BYTES + row_stage_bytes(ns) + (size_t)nr * RAW_BYTES + 8 * (2 * nr + 2 * ns + 2 * kNA) + 16;
+    return W_BYTES + row_stage_bytes(ns) + (size_t)nr * RAW_BYTES + 8 * (2 * nr + 2 * ns + 2 * kNA) + 16 + 4 * CS;
   }
   // deepest rings that fit: raw ring 4..2, staged ring NS_MAX..3
   static constexpr int pick_nr() {
@@ -258,10 +273,10 @@ HS_DEV bool unit_at(const TcArgs& a, int nsplit, long long u, Unit& U) {
   return !(a.active && a.active[U.b] == nullptr);
 }
 
-// Descriptor bases (the start-address field is in 16-byte units in the low
-// bits, so moving a window is a 64-bit add of offset >> 4).
+// Descriptor bases: moving a window is a 32-bit add of offset >> 4 to the
+// low word (smem addresses < 256 KB never carry out of the 14-bit field).
 struct DescBase {
-  uint64_t x[3], w;
+  uint32_t x[3], w;
 };
 
 template <typename C, int MT>
@@ -271,11 +286,11 @@ HS_DEV void tap_mmas(uint32_t d, const DescBase& db, uint32_t x_units, uint32_t 
   constexpr uint32_t I0 = idesc_bf16(MT, 3 * CS), I1 = idesc_bf16(MT, 2 * CS), I2 = idesc_bf16(MT, CS);
 #pragma unroll
   for (int kk = 0; kk < C::KSTEPS; ++kk) {
-    const uint64_t xo = x_units + kk * X_STEP, wo = db.w + w_units + kk * W_STEP;
-    mma_bf16(d, db.x[0] + xo, wo, I0, first ? 0u : 1u);
+    const uint32_t xo = x_units + kk * X_STEP, wo = db.w + w_units + kk * W_STEP;
+    mma_bf16(d, db.x[0] + xo, kDescHi, wo, kDescHi, I0, first ? 0u : 1u);
     first = 0;
-    mma_bf16(d, db.x[1] + xo, wo, I1, 1u);
-    mma_bf16(d, db.x[2] + xo, wo, I2, 1u);
+    mma_bf16(d, db.x[1] + xo, kDescHi, wo, kDescHi, I1, 1u);
+    mma_bf16(d, db.x[2] + xo, kDescHi, wo, kDescHi, I2, 1u);
   }
 }
 
@@ -335,6 +350,7 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
   uint64_t* acc_full = stg_empty + NS;
   uint64_t* acc_empty = acc_full + C::NA;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(acc_empty + C::NA);
+  float* s_bias = reinterpret_cast<float*>(s_tmem + 4);  // this CTA's cout slice
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long nunits = num_units<MODE, MT>(a, NSPLIT);
   // a persistent CTA keeps one cout slice: its units are u = blockIdx.x + k gridDim.x
@@ -353,6 +369,7 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
     for (int part = 0; part < 3; ++part)
       *reinterpret_cast<uint4*>(wst + ((size_t)(t * KC + c) * NW + part * CS + n) * 16) = p[part];
   }
+  for (int n = tid; n < CS; n += kNT) s_bias[n] = a.bias[my_split * CS + n];
   if (tid == 0) {
     for (int i = 0; i < NR; ++i) {
       mbar_init(smem_u32(&raw_full[i]), 1);
@@ -442,11 +459,11 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
     }
   } else if (warp == kMmaWarp) {
     // ================= MMA issuer
-    if (lane == 0) {
+    {  // the whole warp walks the schedule; mma_bf16 / mma_commit elect one lane
       DescBase db;
 #pragma unroll
-      for (int part = 0; part < 3; ++part) db.x[part] = umma_desc(smem_u32(xp[part]), C::XPL * 16, 128);
-      db.w = umma_desc(smem_u32(wst), NW * 16, 128);
+      for (int part = 0; part < 3; ++part) db.x[part] = desc_lo(smem_u32(xp[part]), C::XPL * 16);
+      db.w = desc_lo(smem_u32(wst), NW * 16);
       long long seq0 = 0;  // staged sequence number of the unit's first row
       long long tile = 0;
       for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
@@ -521,14 +538,23 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
         }
         mbar_wait(smem_u32(&acc_full[acc]), (uint32_t)((tile / C::NA) & 1));
         tc_fence_after();
-        uint32_t r[C::NACC][NW];
+        // the three column groups hold the x0-, x1- and x2-weighted partial sums:
+        // sum them while draining TMEM (8 columns of each group per round trip)
+        float t[C::NACC][CS];
 #pragma unroll
         for (int k = 0; k < C::NACC; ++k)
 #pragma unroll
-          for (int n0 = 0; n0 < NW; n0 += 8)
-            tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + acc * C::ACOLS + k * NW + n0,
-                     *reinterpret_cast<uint32_t(*)[8]>(&r[k][n0]));
-        tmem_wait_ld();
+          for (int n0 = 0; n0 < CS; n0 += 8) {
+            uint32_t r0[8], r1[8], r2[8];
+            const uint32_t col = tmem + ((uint32_t)(warp * 32) << 16) + acc * C::ACOLS + k * NW + n0;
+            tmem_ld8(col, r0);
+            tmem_ld8(col + CS, r1);
+            tmem_ld8(col + 2 * CS, r2);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              t[k][n0 + j] = (__uint_as_float(r0[j]) + __uint_as_float(r1[j])) + __uint_as_float(r2[j]);
+          }
         tc_fence_before();
         mbar_arrive(smem_u32(&acc_empty[acc]));  // TMEM free; finish from registers
         if (!lane_ok) continue;
@@ -539,15 +565,13 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
           const size_t obase = (size_t)U.b * a.Ho * a.Wo * COUT + pix * COUT + n_base;
 #pragma unroll
           for (int n0 = 0; n0 < CS; n0 += 4) {
-            float4 o;
-            float* po = &o.x;
-#pragma unroll
-            for (int u4 = 0; u4 < 4; ++u4) {
-              const int n = n0 + u4;
-              // the three column groups hold the x0-, x1- and x2-weighted partial sums
-              const float t = (__uint_as_float(r[k][n]) + __uint_as_float(r[k][CS + n])) +
-                              __uint_as_float(r[k][2 * CS + n]) + __ldg(a.bias + n_base + n);
-              po[u4] = a.softplus ? softplus_f(t) : t;
+            const float4 bs = *reinterpret_cast<const float4*>(s_bias + n0);
+            float4 o = make_float4(t[k][n0] + bs.x, t[k][n0 + 1] + bs.y, t[k][n0 + 2] + bs.z, t[k][n0 + 3] + bs.w);
+            if (a.softplus) {
+              o.x = softplus_f(o.x);
+              o.y = softplus_f(o.y);
+              o.z = softplus_f(o.z);
+              o.w = softplus_f(o.w);
             }
             const float4 ad = pre[k][n0 / 4];
             o.x += ad.x;
