@@ -272,85 +272,174 @@ void launch_tconv_t(const ConvArgs& a, int B, cudaStream_t st) {
 }
 
 // Thin convolutions, stride 1: the 2-channel stems (cin = 2) and the
-// 2-channel head (cout = 2).  One thread per output pixel, the 3x3 input
-// window straight from L1/L2 (neighbouring threads share it), weights in
-// shared memory; memory-bound on the wide side.
+// 2-channel head (cout = 2).  Stems: one lane per output pixel, all cout
+// outputs in registers.  Heads: four lanes share a pixel, each folding in
+// cin / 4 input channels (partial sums reduced with shuffles), so a warp's
+// loads of the wide input cover 8 whole pixels, 512 contiguous bytes.  A
+// thread walks a band of kThinRows rows top to bottom: each input row (pixels
+// x-1, x, x+1) is read once and feeds the three output rows it touches, whose
+// sums stay in registers (rolling window); an output row is stored when its
+// last input row is in.  The next input row and the next output row's
+// addend / residual are loaded one iteration ahead.  Weights sit in shared
+// memory (warp-broadcast reads).
+constexpr int kThinRows = 16, kThinThreads = 128;
 template <int CIN, int COUT>
-__global__ void __launch_bounds__(256) k_conv_thin(ConvArgs a) {
-  __shared__ float s_w[COUT * 9 * CIN];  // [cout][tap][cin]
-  __shared__ float s_b[COUT];
-  for (int e = threadIdx.x; e < COUT * 9 * CIN; e += blockDim.x) s_w[e] = a.w[e];
-  for (int e = threadIdx.x; e < COUT; e += blockDim.x) s_b[e] = a.bias[e];
+__host__ __device__ constexpr int thin_lanes() { return CIN > COUT ? 4 : 1; }
+
+template <int N>
+HS_DEV void load_vec(const float* p, float* v) {
+  if constexpr (N % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < N; i += 4) {
+      const float4 t = __ldg(reinterpret_cast<const float4*>(p + i));
+      v[i] = t.x, v[i + 1] = t.y, v[i + 2] = t.z, v[i + 3] = t.w;
+    }
+  } else if constexpr (N == 2) {
+    const float2 t = __ldg(reinterpret_cast<const float2*>(p));
+    v[0] = t.x, v[1] = t.y;
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = __ldg(p + i);
+  }
+}
+
+template <int N>
+HS_DEV void store_vec(float* p, const float* v) {
+  if constexpr (N % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < N; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+  } else if constexpr (N == 2) {
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) p[i] = v[i];
+  }
+}
+
+template <int CIN, int COUT>
+__global__ void __launch_bounds__(kThinThreads) k_conv_thin(ConvArgs a) {
+  constexpr bool kSplitIn = CIN > COUT;              // head: lanes split cin; stem: lanes split cout
+  constexpr int L = thin_lanes<CIN, COUT>();
+  constexpr int GI = kSplitIn ? CIN / L : CIN;       // input channels per lane
+  constexpr int GO = kSplitIn ? COUT : COUT / L;     // output channels per lane
+  static_assert(GI * L == CIN || !kSplitIn, "lane split");
+  static_assert(GO * L == COUT || kSplitIn, "lane split");
+  __shared__ __align__(16) float s_w[9 * CIN * COUT];  // [tap][cin][cout]
+  for (int e = threadIdx.x; e < 9 * CIN * COUT; e += blockDim.x) {
+    const int n = e % COUT, c = (e / COUT) % CIN, t = e / (COUT * CIN);
+    s_w[e] = a.w[(n * 9 + t) * CIN + c];
+  }
   __syncthreads();
-  const int b = blockIdx.y;
+  const int b = blockIdx.z;
   if (a.active && a.active[b] == nullptr) return;
-  const long long npix = (long long)a.Ho * a.Wo;
+  const int q = threadIdx.x % L;
+  const int x = blockIdx.x * (kThinThreads / L) + threadIdx.x / L;
+  const bool x_ok = x < a.Wo;  // whole quads agree: shuffles stay within live lanes
+  const int ci0 = kSplitIn ? GI * q : 0, co0 = kSplitIn ? 0 : GO * q;
+  const int oy0 = blockIdx.y * kThinRows, oy1 = min(a.Ho, oy0 + kThinRows);
   const float* xb = a.x + (long long)b * a.H * a.W * CIN;
   const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[b] : 0) : b) * a.addend_bstride
                               : nullptr;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < npix;
-       p += (long long)gridDim.x * blockDim.x) {
-    const int oy = (int)(p / a.Wo), ox = (int)(p - (long long)oy * a.Wo);
-    float acc[COUT];
+  // acc[0]: output row iy - 1 (its ky = 2 tap), acc[1]: row iy (ky = 1), acc[2]: row iy + 1 (ky = 0);
+  // bias is added once, at the store (after the cin reduction for heads)
+  float acc[3][GO];
 #pragma unroll
-    for (int n = 0; n < COUT; ++n) acc[n] = s_b[n];
+  for (int r = 0; r < 3; ++r)
 #pragma unroll
-    for (int ky = 0; ky < 3; ++ky) {
-      const int iy = oy + ky - 1;
-      if (iy < 0 || iy >= a.H) continue;
+    for (int n = 0; n < GO; ++n) acc[r][n] = 0.f;
+  // the next input row's three pixel vectors are loaded one iteration ahead
+  auto load_row = [&](int iy, float(&xv)[3][GI]) {
 #pragma unroll
-      for (int kx = 0; kx < 3; ++kx) {
-        const int ix = ox + kx - 1;
-        if (ix < 0 || ix >= a.W) continue;
-        const float* px = xb + ((long long)iy * a.W + ix) * CIN;
-        float xv[CIN];
-        if (CIN % 4 == 0) {
+    for (int kx = 0; kx < 3; ++kx) {
+      const int ix = x + kx - 1;
+      if (x_ok && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W)
+        load_vec<GI>(xb + ((long long)iy * a.W + ix) * CIN + ci0, xv[kx]);
+      else
 #pragma unroll
-          for (int c = 0; c < CIN; c += 4) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(px + c));
-            xv[c] = v.x, xv[c + 1] = v.y, xv[c + 2] = v.z, xv[c + 3] = v.w;
-          }
-        } else {
+        for (int c = 0; c < GI; ++c) xv[kx][c] = 0.f;
+    }
+  };
+  // addend + residual of an output row, summed, fetched one row ahead as well
+  const bool store_lane = x_ok && (!kSplitIn || q == 0);
+  auto load_side = [&](int oy, float(&sd)[GO]) {
 #pragma unroll
-          for (int c = 0; c < CIN; c += 2) {
-            const float2 v = __ldg(reinterpret_cast<const float2*>(px + c));
-            xv[c] = v.x, xv[c + 1] = v.y;
-          }
+    for (int n = 0; n < GO; ++n) sd[n] = 0.f;
+    if (!store_lane || oy < oy0 || oy >= oy1) return;
+    const long long p = (long long)oy * a.Wo + x;
+    float t[GO];
+    if (add) {
+      load_vec<GO>(add + p * COUT + co0, t);
+#pragma unroll
+      for (int n = 0; n < GO; ++n) sd[n] += t[n];
+    }
+    if (a.residual) {
+      load_vec<GO>(a.residual + (long long)b * a.Ho * a.Wo * COUT + p * COUT + co0, t);
+#pragma unroll
+      for (int n = 0; n < GO; ++n) sd[n] += t[n];
+    }
+  };
+  float bias[GO];
+#pragma unroll
+  for (int n = 0; n < GO; ++n) bias[n] = __ldg(a.bias + co0 + n);
+  float nx[3][GI], nsd[GO];
+  load_row(oy0 - 1, nx);
+  load_side(oy0, nsd);  // not needed until iy = oy0 + 1
+  for (int iy = oy0 - 1; iy <= oy1; ++iy) {
+    float xv[3][GI], sd[GO];
+#pragma unroll
+    for (int kx = 0; kx < 3; ++kx)
+#pragma unroll
+      for (int c = 0; c < GI; ++c) xv[kx][c] = nx[kx][c];
+#pragma unroll
+    for (int n = 0; n < GO; ++n) sd[n] = nsd[n];
+    if (iy < oy1) load_row(iy + 1, nx);
+    if (iy >= oy0) load_side(iy, nsd);  // row iy is stored next iteration
+#pragma unroll
+    for (int kx = 0; kx < 3; ++kx)
+#pragma unroll
+      for (int ky = 0; ky < 3; ++ky) {
+        float* ac = acc[2 - ky];
+#pragma unroll
+        for (int c = 0; c < GI; ++c)
+#pragma unroll
+          for (int n = 0; n < GO; ++n) ac[n] = fmaf(xv[kx][c], s_w[((ky * 3 + kx) * CIN + ci0 + c) * COUT + co0 + n], ac[n]);
+      }
+    const int oy = iy - 1;  // complete: rows oy - 1, oy, oy + 1 are in
+    if (oy >= oy0 && oy < oy1) {
+      float v[GO];
+#pragma unroll
+      for (int n = 0; n < GO; ++n) {
+        v[n] = acc[0][n];
+        if (kSplitIn)
+#pragma unroll
+          for (int sh = 1; sh < L; sh <<= 1) v[n] += __shfl_xor_sync(0xffffffffu, v[n], sh);
+      }
+      if (store_lane) {
+        const long long o = (long long)b * a.Ho * a.Wo * COUT + ((long long)oy * a.Wo + x) * COUT + co0;
+#pragma unroll
+        for (int n = 0; n < GO; ++n) {
+          float t = v[n] + bias[n];
+          if (a.softplus) t = softplus_fast(t);
+          v[n] = t + sd[n];
         }
-        const int tap = ky * 3 + kx;
-#pragma unroll
-        for (int n = 0; n < COUT; ++n)
-#pragma unroll
-          for (int c = 0; c < CIN; ++c) acc[n] = fmaf(xv[c], s_w[(n * 9 + tap) * CIN + c], acc[n]);
+        store_vec<GO>(a.y + o, v);
       }
     }
-    const long long o = (long long)b * npix * COUT + p * COUT;
 #pragma unroll
-    for (int n = 0; n < COUT; n += 2) {
-      float2 v = make_float2(acc[n], acc[n + 1]);
-      if (a.softplus) v = make_float2(softplusf(v.x), softplusf(v.y));
-      if (add) {
-        const float2 ad = __ldg(reinterpret_cast<const float2*>(add + p * COUT + n));
-        v.x += ad.x;
-        v.y += ad.y;
-      }
-      if (a.residual) {
-        const float2 rs = __ldg(reinterpret_cast<const float2*>(a.residual + o + n));
-        v.x += rs.x;
-        v.y += rs.y;
-      }
-      *reinterpret_cast<float2*>(a.y + o + n) = v;
+    for (int n = 0; n < GO; ++n) {
+      acc[0][n] = acc[1][n];
+      acc[1][n] = acc[2][n];
+      acc[2][n] = 0.f;
     }
   }
 }
 
 template <int CIN, int COUT>
 void launch_thin(const ConvArgs& a, int B, cudaStream_t st) {
-  const long long npix = (long long)a.Ho * a.Wo;
-  long long blocks = (npix + 255) / 256;
-  const long long cap = (8LL * 148 + B - 1) / B;
-  if (blocks > cap) blocks = cap;
-  k_conv_thin<CIN, COUT><<<dim3((unsigned)blocks, B), 256, 0, st>>>(a);
+  constexpr int pix = kThinThreads / thin_lanes<CIN, COUT>();
+  const dim3 grid((unsigned)((a.Wo + pix - 1) / pix), (unsigned)((a.Ho + kThinRows - 1) / kThinRows),
+                  (unsigned)B);
+  k_conv_thin<CIN, COUT><<<grid, kThinThreads, 0, st>>>(a);
 }
 
 int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* y, const float* addend,

@@ -47,6 +47,15 @@ HS_DEV double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+// softplus(x) = max(x, 0) + log1p(e), e = exp(-|x|) in (0, 1]: MUFU exp / log
+// with a short series for small e (absolute error ~2e-7, the fp32 class of
+// the reference's np.logaddexp; the conv tests hold layers to 2e-6 relative).
+HS_DEV float softplus_fast(float x) {
+  const float e = __expf(-fabsf(x));
+  const float series = e * fmaf(e, fmaf(e, fmaf(e, -0.25f, 0.33333334f), -0.5f), 1.0f);  // error < e^5 / 5
+  return fmaxf(x, 0.f) + (e < 0.03125f ? series : __logf(1.0f + e));
+}
+
 HS_DEV float warp_sumf(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

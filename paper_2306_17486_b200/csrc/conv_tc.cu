@@ -21,14 +21,15 @@
 // not math-bound); the epilogue sums the three column groups.
 //
 // Warp-specialised pipeline (one persistent CTA per SM, weights resident):
-//   warp 6 (1 lane)  producer  : cp.async.bulk of raw NHWC input rows into a
+//   warp 10 (1 lane) producer  : cp.async.bulk of raw NHWC input rows into a
 //                                ring of raw slots (mbarrier tx-count)
-//   warps 4-5        converters: raw fp32 -> bf16x3 split, re-laid out into
+//   warps 8-9        converters: raw fp32 -> bf16x3 split, re-laid out into
 //                                the staged ring (smem -> smem)
-//   warp 7 (1 lane)  MMA issuer: tcgen05.mma per tile into one of four TMEM
+//   warp 11          MMA issuer: tcgen05.mma per tile into one of four TMEM
 //                                accumulators; commits release staged rows
 //                                and hand accumulators to the epilogue
-//   warps 0-3        epilogue  : tcgen05.ld of their TMEM lane quarter, then
+//   warps 0-7        epilogue  : tcgen05.ld of their TMEM lane quarter and
+//                                channel half, then
 //                                bias, softplus, encoder/skip addend,
 //                                residual, NHWC stores
 // A CTA walks a band of output rows of one MT-pixel column block top to
@@ -39,6 +40,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "conv_tc.h"
@@ -46,10 +48,11 @@
 namespace hs {
 namespace {
 
-constexpr int kNT = 256;  // 8 warps
+constexpr int kNT = 384;  // 12 warps
 constexpr int kBand = 32; // output rows per work unit
+constexpr int kPrefetch = 8;  // rows pulled into L2 ahead of the bulk copies / epilogue loads
 constexpr int kNA = 4;    // TMEM accumulators in flight
-constexpr int kEpiWarps = 4, kCvtWarp0 = 4, kCvtWarps = 2, kProdWarp = 6, kMmaWarp = 7;
+constexpr int kEpiWarps = 8, kCvtWarp0 = 8, kCvtWarps = 2, kProdWarp = 10, kMmaWarp = 11;
 constexpr int kCvtThreads = 32 * kCvtWarps;
 constexpr size_t kSmemMax = 232448;
 
@@ -112,6 +115,10 @@ HS_DEV void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mba
                : "memory");
 }
 
+HS_DEV void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 HS_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 HS_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 HS_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -143,15 +150,6 @@ HS_DEV void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
 }
 HS_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// softplus(x) = max(x, 0) + log1p(e), e = exp(-|x|) in (0, 1]: MUFU exp / log
-// with a short series for small e (absolute error ~2e-7, the fp32 class of
-// the reference's np.logaddexp; the tests hold the layer to 2e-6 relative).
-HS_DEV float softplus_f(float x) {
-  const float e = __expf(-fabsf(x));
-  const float series = e * fmaf(e, fmaf(e, fmaf(e, -0.25f, 0.33333334f), -0.5f), 1.0f);  // error < e^5 / 5
-  return fmaxf(x, 0.f) + (e < 0.03125f ? series : __logf(1.0f + e));
-}
-
 struct TcArgs {
   const float* x;
   int H, W;
@@ -167,6 +165,7 @@ struct TcArgs {
   const float* residual;
   const void* const* active;
   int B;
+  int dbg;  // experiment switch (HS_TC_DBG): 1 skip conversion, 2 skip MMAs, 4 skip epilogue math
 };
 
 // MODE 0: stride 1; MODE 1: stride 2; MODE 2: transposed stride 2 (out = 2 x in).
@@ -406,7 +405,33 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
         const int x0 = raw_x0<MODE, MT>(U.xb);
         const int clo = max(x0, 0), chi = min(x0 + C::RW, a.W);
         const float* img = a.x + (size_t)U.b * a.H * a.W * CIN;
+        // The raw ring holds only a few rows, too few bytes in flight to cover
+        // DRAM latency: rows kPrefetch ahead (input rows and the epilogue's
+        // addend / residual rows) are pulled into L2 with bulk prefetches.
+        const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[U.b] : 0) : U.b) *
+                                                     a.addend_bstride
+                                    : nullptr;
+        const float* res = a.residual ? a.residual + (size_t)U.b * a.Ho * a.Wo * COUT : nullptr;
+        const int ox0 = MODE == 2 ? 2 * U.xb * MT : U.xb * MT;
+        const uint32_t out_bytes = (uint32_t)(MODE == 2 ? 2 * MT : MT) * COUT * 4;
+        auto prefetch_in = [&](int g) {
+          if (g <= U.ghi && g >= 0 && g < a.H && chi > clo)
+            prefetch_l2(img + ((size_t)g * a.W + clo) * CIN, (uint32_t)(chi - clo) * CIN * 4);
+        };
+        int next_out = U.oy0;
+        auto prefetch_out = [&](int upto) {
+          for (; next_out < min(upto, U.oy1); ++next_out) {
+            const size_t off = ((size_t)next_out * a.Wo + ox0) * COUT;
+            if (add) prefetch_l2(add + off, out_bytes);
+            if (res) prefetch_l2(res + off, out_bytes);
+          }
+        };
+        for (int g = U.glo; g < U.glo + kPrefetch; ++g) prefetch_in(g);
+        prefetch_out(U.oy0 + kPrefetch);
         for (int g = U.glo; g <= U.ghi; ++g, ++seq) {
+          const int i = g - U.glo;
+          prefetch_in(g + kPrefetch);
+          prefetch_out(U.oy0 + (MODE == 0 ? i : (MODE == 1 ? i / 2 : 2 * i)) + kPrefetch);
           const int s = (int)(seq % NR);
           const long long use = seq / NR;
           if (use > 0) mbar_wait(smem_u32(&raw_empty[s]), (uint32_t)((use - 1) & 1));
@@ -438,7 +463,7 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
         mbar_wait(smem_u32(&raw_full[rs]), (uint32_t)((seq / NR) & 1));
         const bool row_ok = g >= 0 && g < a.H;
         const unsigned char* src = raw + (size_t)rs * C::RAW_BYTES;
-        for (int e = ct; e < C::RW * KC; e += kCvtThreads) {
+        for (int e = ct; e < ((a.dbg & 1) ? 0 : C::RW * KC); e += kCvtThreads) {
           const int p = e / KC, c = e - p * KC;  // chunk fastest: conflict-free raw reads
           float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
           if (row_ok && p >= clo && p < chi) {
@@ -484,7 +509,7 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
           const long long ause = tile / C::NA;
           if (ause > 0) mbar_wait(smem_u32(&acc_empty[acc]), (uint32_t)((ause - 1) & 1));
           tc_fence_after();
-          issue_mmas<C, MODE, MT>(oy, tmem + acc * C::ACOLS, db, slot);
+          if (!(a.dbg & 2)) issue_mmas<C, MODE, MT>(oy, tmem + acc * C::ACOLS, db, slot);
           mma_commit(smem_u32(&acc_full[acc]));
           // release rows the next tile of this unit no longer reads
           int keep_lo = U.ghi + 1;
@@ -500,30 +525,32 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
       }
     }
   } else {
-    // ================= epilogue warps 0-3: TMEM lane quarter = warp.
-    // M = 128: tile row m = TMEM lane m.  M = 64: rows 16w..16w+15 sit in the
-    // first 16 lanes of quarter w (the other 16 lanes are idle).
+    // ================= epilogue warps 0-7: TMEM lane quarter q = warp % 4 (the
+    // only lanes a warp may read), channel half h = warp / 4 of the slice.
+    // M = 128: tile row m = TMEM lane m.  M = 64: rows 16q..16q+15 sit in the
+    // first 16 lanes of quarter q (the other 16 lanes are idle).
+    constexpr int EH = CS / 2;
+    const int q4 = warp & 3, h = warp >> 2;
     const bool lane_ok = MT == 128 || lane < 16;
-    const int m = MT == 128 ? warp * 32 + lane : warp * 16 + (lane & 15);
+    const int m = MT == 128 ? q4 * 32 + lane : q4 * 16 + (lane & 15);
     long long tile = 0;
     for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
       if (!unit_at<MODE, MT>(a, NSPLIT, u, U)) continue;
-      const int n_base = U.split * CS;
+      const int n_base = U.split * CS + h * EH;
       const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[U.b] : 0) : U.b) *
                                                    a.addend_bstride
                                   : nullptr;
-      for (int oy = U.oy0; oy < U.oy1; ++oy, ++tile) {
-        const int acc = (int)(tile % C::NA);
-        // addend + residual do not depend on the accumulator: fetch (and sum) them before waiting on the MMA
-        float4 pre[C::NACC][CS / 4];
+      // addend + residual do not depend on the accumulator: row oy + 1 is
+      // fetched (and summed) while row oy waits on its MMAs
+      auto fetch = [&](int oy, float4(&p)[C::NACC][EH / 4]) {
 #pragma unroll
         for (int k = 0; k < C::NACC; ++k) {
           const int ox = MODE == 2 ? 2 * (U.xb * MT + m) + k : U.xb * MT + m;
           const size_t pix = (size_t)oy * a.Wo + ox;
           const size_t obase = (size_t)U.b * a.Ho * a.Wo * COUT + pix * COUT + n_base;
 #pragma unroll
-          for (int q = 0; q < CS / 4; ++q) {
+          for (int q = 0; q < EH / 4; ++q) {
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
             if (add && lane_ok) v = __ldg(reinterpret_cast<const float4*>(add + pix * COUT + n_base) + q);
             if (a.residual && lane_ok) {
@@ -533,20 +560,26 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
               v.z += rs.z;
               v.w += rs.w;
             }
-            pre[k][q] = v;
+            p[k][q] = v;
           }
         }
+      };
+      float4 pre[C::NACC][EH / 4], nxt[C::NACC][EH / 4];
+      fetch(U.oy0, pre);
+      for (int oy = U.oy0; oy < U.oy1; ++oy, ++tile) {
+        const int acc = (int)(tile % C::NA);
+        if (oy + 1 < U.oy1) fetch(oy + 1, nxt);
         mbar_wait(smem_u32(&acc_full[acc]), (uint32_t)((tile / C::NA) & 1));
         tc_fence_after();
         // the three column groups hold the x0-, x1- and x2-weighted partial sums:
         // sum them while draining TMEM (8 columns of each group per round trip)
-        float t[C::NACC][CS];
+        float t[C::NACC][EH];
 #pragma unroll
         for (int k = 0; k < C::NACC; ++k)
 #pragma unroll
-          for (int n0 = 0; n0 < CS; n0 += 8) {
+          for (int n0 = 0; n0 < EH; n0 += 8) {
             uint32_t r0[8], r1[8], r2[8];
-            const uint32_t col = tmem + ((uint32_t)(warp * 32) << 16) + acc * C::ACOLS + k * NW + n0;
+            const uint32_t col = tmem + ((uint32_t)(q4 * 32) << 16) + acc * C::ACOLS + k * NW + h * EH + n0;
             tmem_ld8(col, r0);
             tmem_ld8(col + CS, r1);
             tmem_ld8(col + 2 * CS, r2);
@@ -557,30 +590,35 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
           }
         tc_fence_before();
         mbar_arrive(smem_u32(&acc_empty[acc]));  // TMEM free; finish from registers
-        if (!lane_ok) continue;
+        if (lane_ok && !(a.dbg & 4)) {
 #pragma unroll
-        for (int k = 0; k < C::NACC; ++k) {
-          const int ox = MODE == 2 ? 2 * (U.xb * MT + m) + k : U.xb * MT + m;
-          const size_t pix = (size_t)oy * a.Wo + ox;
-          const size_t obase = (size_t)U.b * a.Ho * a.Wo * COUT + pix * COUT + n_base;
+          for (int k = 0; k < C::NACC; ++k) {
+            const int ox = MODE == 2 ? 2 * (U.xb * MT + m) + k : U.xb * MT + m;
+            const size_t pix = (size_t)oy * a.Wo + ox;
+            const size_t obase = (size_t)U.b * a.Ho * a.Wo * COUT + pix * COUT + n_base;
 #pragma unroll
-          for (int n0 = 0; n0 < CS; n0 += 4) {
-            const float4 bs = *reinterpret_cast<const float4*>(s_bias + n0);
-            float4 o = make_float4(t[k][n0] + bs.x, t[k][n0 + 1] + bs.y, t[k][n0 + 2] + bs.z, t[k][n0 + 3] + bs.w);
-            if (a.softplus) {
-              o.x = softplus_f(o.x);
-              o.y = softplus_f(o.y);
-              o.z = softplus_f(o.z);
-              o.w = softplus_f(o.w);
+            for (int n0 = 0; n0 < EH; n0 += 4) {
+              const float4 bs = *reinterpret_cast<const float4*>(s_bias + h * EH + n0);
+              float4 o = make_float4(t[k][n0] + bs.x, t[k][n0 + 1] + bs.y, t[k][n0 + 2] + bs.z, t[k][n0 + 3] + bs.w);
+              if (a.softplus) {
+                o.x = softplus_fast(o.x);
+                o.y = softplus_fast(o.y);
+                o.z = softplus_fast(o.z);
+                o.w = softplus_fast(o.w);
+              }
+              const float4 ad = pre[k][n0 / 4];
+              o.x += ad.x;
+              o.y += ad.y;
+              o.z += ad.z;
+              o.w += ad.w;
+              *reinterpret_cast<float4*>(a.y + obase + n0) = o;
             }
-            const float4 ad = pre[k][n0 / 4];
-            o.x += ad.x;
-            o.y += ad.y;
-            o.z += ad.z;
-            o.w += ad.w;
-            *reinterpret_cast<float4*>(a.y + obase + n0) = o;
           }
         }
+#pragma unroll
+        for (int k = 0; k < C::NACC; ++k)
+#pragma unroll
+          for (int q = 0; q < EH / 4; ++q) pre[k][q] = nxt[k][q];
       }
     }
   }
@@ -641,8 +679,9 @@ bool conv_tc_launch(const float* x, int H, int W, int cin, float* y, int Ho, int
                     int transposed, const float* w, const float* bias, int softplus, const float* addend,
                     long long addend_bstride, int addend_per_model, const int* model_of, const float* residual,
                     const void* const* active, int B, cudaStream_t st) {
+  static const int dbg = getenv("HS_TC_DBG") ? atoi(getenv("HS_TC_DBG")) : 0;
   TcArgs a{x, H, W, y, Ho, Wo, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual,
-           active, B};
+           active, B, dbg};
   const int mode = transposed ? 2 : (stride == 2 ? 1 : 0);
   const bool m128 = ((mode == 2 ? W : Wo) % 128) == 0;
 #define HS_TC(CI, CO, MD, CSL)                                           \
