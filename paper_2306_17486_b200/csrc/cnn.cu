@@ -20,12 +20,14 @@
 #include "cnn.h"
 #include "common.cuh"
 #include "conv_tc.h"
+#include "implicit.h"
 #include "prof.h"
 
 struct hs_net {
   hs_net_desc_t d;
   int hc, wc, cc;              // coarsest grid and complex channel count
-  cufftComplex* spec = nullptr;  // (cc, 2hc, 2wc) complex64 Green spectrum
+  cufftComplex* spec = nullptr;       // (cc, 2hc, 2wc) complex64 Green spectrum
+  cufftComplex* spec_perm = nullptr;  // the same in the fused kernel's order (implicit.cu), if supported
   const float* enc[8] = {nullptr};
   int n_models = 0;
   mutable std::mutex plan_mu;
@@ -33,6 +35,7 @@ struct hs_net {
   ~hs_net() {
     for (auto& kv : plans) cufftDestroy(kv.second);
     if (spec) cudaFree(spec);
+    if (spec_perm) cudaFree(spec_perm);
   }
 };
 
@@ -754,6 +757,10 @@ static int green_spectrum_c128(const float2* kern, int C, int h, int w, cufftDou
 static int implicit_apply_dev(const hs_net_t* net, const float* x_nhwc, float* y_nhwc, cufftComplex* z,
                               const void* const* active, int B, cudaStream_t st) {
   const int hc = net->hc, wc = net->wc, cc = net->cc;
+  if (net->spec_perm) {
+    const long long pix = (long long)hc * wc;
+    return implicit_fused(x_nhwc, pix * cc, 1, cc, y_nhwc, pix * cc, 1, cc, net->spec_perm, active, B, cc, hc, wc, st);
+  }
   cufftHandle plan;
   {
     std::lock_guard<std::mutex> g(net->plan_mu);
@@ -891,6 +898,10 @@ HS_API int hs_net_create(hs_net_t** out, const hs_net_desc_t* desc, void* stream
   int rc = hs::green_spectrum_c128(static_cast<const float2*>(desc->implicit_w), n->cc, n->hc, n->wc, s128, st);
   if (rc == HS_OK) {
     hs::k_c128_to_c64<<<hs::grid1(ns), 256, 0, st>>>(s128, n->spec, ns);
+    if (hs::implicit_fused_supported(n->hc, n->wc)) {
+      if (cudaMalloc(&n->spec_perm, ns * sizeof(cufftComplex)) != cudaSuccess) rc = HS_ECUDA;
+      else hs::implicit_permute_spectrum(n->spec, n->spec_perm, n->cc, n->hc, n->wc, st);
+    }
     cudaStreamSynchronize(st);
   }
   cudaFree(s128);
@@ -969,13 +980,24 @@ HS_API int hs_green_spectrum(const void* kernel, int C, int h, int w, void* spec
 
 HS_API int hs_implicit_apply(const void* x, const void* spectrum, void* y, int B, int C, int h, int w, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  const long long per_b = (long long)C * 4 * h * w;
+  if (hs::implicit_fused_supported(h, w)) {
+    void* sp = nullptr;
+    if (cudaMalloc(&sp, (size_t)per_b * sizeof(cufftComplex)) != cudaSuccess) return cfail(HS_ECUDA, "cudaMalloc");
+    hs::implicit_permute_spectrum(spectrum, sp, C, h, w, st);
+    const long long hw = (long long)h * w;
+    const int rc = hs::implicit_fused(x, C * hw, hw, 1, y, C * hw, hw, 1, sp, nullptr, B, C, h, w, st);
+    cudaStreamSynchronize(st);
+    cudaFree(sp);
+    if (rc) return cfail(rc, "implicit layer");
+    return ccheck("hs_implicit_apply");
+  }
   cufftHandle plan;
   int n[2] = {2 * h, 2 * w};
   if (cufftPlanMany(&plan, 2, n, nullptr, 1, 4 * h * w, nullptr, 1, 4 * h * w, CUFFT_C2C, B * C) != CUFFT_SUCCESS)
     return cfail(HS_ECUDA, "cufft plan");
   cufftSetStream(plan, st);
   cufftComplex* z = nullptr;
-  const long long per_b = (long long)C * 4 * h * w;
   if (cudaMalloc(&z, (size_t)B * per_b * sizeof(cufftComplex)) != cudaSuccess) {
     cufftDestroy(plan);
     return cfail(HS_ECUDA, "cudaMalloc");

@@ -123,6 +123,18 @@ def test_green_function_and_implicit_apply_match_reference():
         assert relerr(y, g[f"iy_{tag}"]) < 2e-6
 
 
+@pytest.mark.parametrize("hh,ww", [(32, 32), (64, 64), (32, 64), (64, 32), (128, 64)])
+def test_fused_implicit_layer_matches_oracle(hh, ww):
+    # sizes the fused one-kernel path (implicit.cu) handles; the oracle is green.py's pad/fft2/ifft2/crop
+    rng = np.random.default_rng(hh * 1000 + ww)
+    x = (rng.standard_normal((3, 5, hh, ww)) + 1j * rng.standard_normal((3, 5, hh, ww))).astype(np.complex64)
+    spec = (rng.standard_normal((5, 2 * hh, 2 * ww)) + 1j * rng.standard_normal((5, 2 * hh, 2 * ww)))
+    spec = spec.astype(np.complex64)
+    y = green.implicit_apply(x, spec)
+    ref = no.implicit_apply(x.astype(np.complex128), spec.astype(np.complex128))
+    assert relerr(y, ref) < 2e-6
+
+
 def test_green_regression_ratio_on_device():
     # test_green.py:73-80
     S = green.green_function(green.laplacian_plus_i_kernel(1), (16, 16))
