@@ -180,16 +180,16 @@ struct Cfg {
   static constexpr int RAW_BYTES = RW * CIN * 4;
   static constexpr int NW = 3 * CS;                            // stacked weight rows [W0; W1; W2]
   static constexpr size_t W_BYTES = (size_t)9 * KC * NW * 16;
-  static constexpr int NS_MIN = 3, NS_MAX = MODE == 0 ? 6 : (MODE == 1 ? 5 : 4);
+  static constexpr int NS_MIN = 3, NS_MAX = MODE == 0 ? 10 : (MODE == 1 ? 8 : 6);
   static constexpr size_t row_stage_bytes(int ns) {
     return (size_t)3 * KC * 16 * (ns * RW + ((9 - ((ns * RW) & 7)) & 7));
   }
   static constexpr size_t total(int ns, int nr) {
     return W_BYTES + row_stage_bytes(ns) + (size_t)nr * RAW_BYTES + 8 * (2 * nr + 2 * ns + 2 * kNA) + 16 + 4 * CS;
   }
-  // deepest rings that fit: raw ring 4..2, staged ring NS_MAX..3
+  // deepest rings that fit: raw ring 6..2, staged ring NS_MAX..3
   static constexpr int pick_nr() {
-    for (int nr = 4; nr >= 2; --nr)
+    for (int nr = 6; nr >= 2; --nr)
       if (total(NS_MIN, nr) <= kSmemMax && total(NS_MAX < 4 ? NS_MAX : 4, nr) <= kSmemMax) return nr;
     return 2;
   }
@@ -278,6 +278,50 @@ struct DescBase {
   uint32_t x[3], w;
 };
 
+// The three MMAs of one (tap, K step): activation parts x0, x1, x2 against
+// the stacked weights [W0|W1|W2] (N = 3 cs, 2 cs, cs).  One asm block, one
+// elect, immediates for the instruction descriptors and the descriptors'
+// high word: the per-MMA cost is a 64-bit move and the issue itself.
+template <uint32_t I0, uint32_t I1, uint32_t I2>
+HS_DEV void mma_parts3(uint32_t d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, t, e;\n\t.reg .b64 da, db;\n\t.reg .b32 hi, i0, i1, i2;\n\t"
+      "mov.b32 hi, %6;\n\tmov.b32 i0, %7;\n\tmov.b32 i1, %8;\n\tmov.b32 i2, %9;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, %5, %5;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "mov.b64 db, {%4, hi};\n\t"
+      "mov.b64 da, {%1, hi};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, i0, p;\n\t"
+      "mov.b64 da, {%2, hi};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, i1, t;\n\t"
+      "mov.b64 da, {%3, hi};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, i2, t;\n\t}\n" ::"r"(d),
+      "r"(a0), "r"(a1), "r"(a2), "r"(b), "r"(accumulate), "n"(kDescHi), "n"(I0), "n"(I1), "n"(I2));
+}
+
+// The nine MMAs of one filter row (taps kx = 0, 1, 2 of row ky, one K step):
+// one asm block whose descriptor arithmetic is all immediate adds, so ptxas
+// moves three values into uniform registers per nine MMAs.
+template <uint32_t I0, uint32_t I1, uint32_t I2, uint32_t PX0, uint32_t PX1, uint32_t PX2, uint32_t WT, uint32_t PS>
+HS_DEV void mma_row9(uint32_t d, uint32_t xbase, uint32_t wbase, uint32_t accumulate) {
+#define HS_MMA_PARTS(PX, P0)                                             \
+  "add.u32 al, %1, " PX ";\n\tmov.b64 da, {al, hi};\n\t"              \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, i0, " P0 ";\n\t" \
+  "add.u32 al, al, %12;\n\tmov.b64 da, {al, hi};\n\t"                 \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, i1, t;\n\t"      \
+  "add.u32 al, al, %12;\n\tmov.b64 da, {al, hi};\n\t"                 \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, i2, t;\n\t"
+  asm volatile(
+      "{\n\t.reg .pred p, t, e;\n\t.reg .b64 da, db;\n\t.reg .b32 hi, i0, i1, i2, al, bl;\n\t"
+      "mov.b32 hi, %4;\n\tmov.b32 i0, %5;\n\tmov.b32 i1, %6;\n\tmov.b32 i2, %7;\n\t"
+      "setp.ne.b32 p, %3, 0;\n\tsetp.eq.b32 t, %3, %3;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "mov.b64 db, {%2, hi};\n\t" HS_MMA_PARTS("%8", "p")
+      "add.u32 bl, %2, %11;\n\tmov.b64 db, {bl, hi};\n\t" HS_MMA_PARTS("%9", "t")
+      "add.u32 bl, %2, %13;\n\tmov.b64 db, {bl, hi};\n\t" HS_MMA_PARTS("%10", "t") "}\n" ::"r"(d),
+      "r"(xbase), "r"(wbase), "r"(accumulate), "n"(kDescHi), "n"(I0), "n"(I1), "n"(I2), "n"(PX0), "n"(PX1),
+      "n"(PX2), "n"(WT), "n"(PS), "n"(2 * WT));
+#undef HS_MMA_PARTS
+}
+
 template <typename C, int MT>
 HS_DEV void tap_mmas(uint32_t d, const DescBase& db, uint32_t x_units, uint32_t w_units, uint32_t& first) {
   constexpr uint32_t X_STEP = 2 * C::XPL, W_STEP = 2 * C::NW;  // two 16-byte chunks per K step
@@ -286,10 +330,8 @@ HS_DEV void tap_mmas(uint32_t d, const DescBase& db, uint32_t x_units, uint32_t 
 #pragma unroll
   for (int kk = 0; kk < C::KSTEPS; ++kk) {
     const uint32_t xo = x_units + kk * X_STEP, wo = db.w + w_units + kk * W_STEP;
-    mma_bf16(d, db.x[0] + xo, kDescHi, wo, kDescHi, I0, first ? 0u : 1u);
+    mma_parts3<I0, I1, I2>(d, db.x[0] + xo, db.x[1] + xo, db.x[2] + xo, wo, first ? 0u : 1u);
     first = 0;
-    mma_bf16(d, db.x[1] + xo, kDescHi, wo, kDescHi, I1, 1u);
-    mma_bf16(d, db.x[2] + xo, kDescHi, wo, kDescHi, I2, 1u);
   }
 }
 
@@ -301,15 +343,20 @@ HS_DEV void issue_mmas(int oy, uint32_t d0, const DescBase& db, SlotOf slot) {
   uint32_t first = 1;
   if (MODE == 0 || MODE == 1) {
     const int g0 = MODE == 0 ? oy - 1 : 2 * oy - 1;
+    constexpr int CS = C::NW / 3;
+    constexpr uint32_t I0 = idesc_bf16(MT, 3 * CS), I1 = idesc_bf16(MT, 2 * CS), I2 = idesc_bf16(MT, CS);
+    constexpr uint32_t PX0 = MODE == 0 ? 0 : MT, PX1 = MODE == 0 ? 1 : 0, PX2 = MODE == 0 ? 2 : MT + 1;
+    constexpr uint32_t PS = (uint32_t)(C::XP_BYTES / 16);  // activation part planes, 16-byte units
+    constexpr uint32_t X_STEP = 2 * C::XPL, W_STEP = 2 * C::NW;
 #pragma unroll
     for (int ky = 0; ky < 3; ++ky) {
       const uint32_t r = row_units(g0 + ky);
 #pragma unroll
-      for (int kx = 0; kx < 3; ++kx) {
-        const uint32_t px = MODE == 0 ? kx : (kx == 1 ? 0 : (kx == 0 ? MT : MT + 1));
-        tap_mmas<C, MT>(d0, db, r + px, (ky * 3 + kx) * WT, first);
-      }
+      for (int kk = 0; kk < C::KSTEPS; ++kk)
+        mma_row9<I0, I1, I2, PX0, PX1, PX2, WT, PS>(d0, db.x[0] + r + kk * X_STEP, db.w + ky * 3 * WT + kk * W_STEP,
+                                                    (ky | kk) ? 1u : 0u);
     }
+    (void)first;
     return;
   }
   // transposed: out row 2q <- (ky 1, row q); out row 2q+1 <- (ky 0, row q+1), (ky 2, row q)
@@ -489,27 +536,29 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
 #pragma unroll
       for (int part = 0; part < 3; ++part) db.x[part] = desc_lo(smem_u32(xp[part]), C::XPL * 16);
       db.w = desc_lo(smem_u32(wst), NW * 16);
-      long long seq0 = 0;  // staged sequence number of the unit's first row
-      long long tile = 0;
+      // 32-bit, warp-uniform bookkeeping: ptxas keeps MMA operands in uniform registers
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      uint32_t seq0 = 0;  // staged sequence number of the unit's first row
+      uint32_t tile = 0;
       for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
         Unit U;
         if (!unit_at<MODE, MT>(a, NSPLIT, u, U)) continue;
-        auto slot = [&](int g) { return (int)((seq0 + (g - U.glo)) % NS); };
+        auto slot = [&](int g) { return (int)((seq0 + (uint32_t)(g - U.glo)) % NS); };
         int waited = U.glo - 1;   // highest input row known to be staged
         int retired = U.glo - 1;  // highest input row released back to the converters
         for (int oy = U.oy0; oy < U.oy1; ++oy, ++tile) {
           int lo, hi;
           tile_rows<MODE>(oy, lo, hi);
           for (int g = waited + 1; g <= hi; ++g) {
-            const long long sq = seq0 + (g - U.glo);
-            mbar_wait(smem_u32(&stg_full[sq % NS]), (uint32_t)((sq / NS) & 1));
+            const uint32_t sq = seq0 + (uint32_t)(g - U.glo);
+            mbar_wait(smem_u32(&stg_full[sq % NS]), (sq / NS) & 1);
           }
           waited = max(waited, hi);
-          const int acc = (int)(tile % C::NA);
-          const long long ause = tile / C::NA;
-          if (ause > 0) mbar_wait(smem_u32(&acc_empty[acc]), (uint32_t)((ause - 1) & 1));
+          const uint32_t acc = tile % C::NA;
+          const uint32_t ause = tile / C::NA;
+          if (ause > 0) mbar_wait(smem_u32(&acc_empty[acc]), (ause - 1) & 1);
           tc_fence_after();
-          if (!(a.dbg & 2)) issue_mmas<C, MODE, MT>(oy, tmem + acc * C::ACOLS, db, slot);
+          if (!(a.dbg & 2)) issue_mmas<C, MODE, MT>(oy, tm + acc * C::ACOLS, db, slot);
           mma_commit(smem_u32(&acc_full[acc]));
           // release rows the next tile of this unit no longer reads
           int keep_lo = U.ghi + 1;
@@ -683,7 +732,7 @@ bool conv_tc_launch(const float* x, int H, int W, int cin, float* y, int Ho, int
   TcArgs a{x, H, W, y, Ho, Wo, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual,
            active, B, dbg};
   const int mode = transposed ? 2 : (stride == 2 ? 1 : 0);
-  const bool m128 = ((mode == 2 ? W : Wo) % 128) == 0;
+  const bool m128 = ((mode == 2 ? W : Wo) % 128) == 0 && !(dbg & 32);
 #define HS_TC(CI, CO, MD, CSL)                                           \
   if (mode == MD && cin == CI && cout == CO) {                           \
     if (m128) launch_tc<CI, CO, MD, 128, CSL>(a, st);                    \
