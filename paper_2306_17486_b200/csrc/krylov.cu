@@ -23,7 +23,7 @@ namespace hs {
 namespace {
 
 constexpr int NT = 256;
-constexpr int KC = 12;            // basis vectors per chunk in a dot pass
+constexpr int KC = 6;             // basis vectors per chunk in a dot pass (registers vs w recomputes)
 constexpr int PST = 2 * KC + 1;   // doubles per partial record
 constexpr int kChunks = (kMaxRestart + KC - 1) / KC;
 
@@ -36,8 +36,11 @@ HS_DEV double2 ldz(const float2* p) {
 
 // (A u)(p) of the TRUE operator (shift 1 + 0i, no wall), fp64, summation
 // order of neg_laplacian (fields.py:191-199) then minus c u (fields.py:208-210).
+// Division by h2 becomes a multiply by its exact reciprocal when h2 is a power
+// of two (bitwise identical; inv_h2 == 0 otherwise).
 template <typename LD>
-HS_DEV double2 apply_true(LD ld, const double2* __restrict__ c, int nx, int ny, int p, int i, int j, double h2) {
+HS_DEV double2 apply_true(LD ld, const double2* __restrict__ c, int nx, int ny, int p, int i, int j, double h2,
+                          double inv_h2) {
   double2 u = ld(p);
   double2 z0 = make_double2(0.0, 0.0);
   double2 xp = i + 1 < nx ? ld(p + ny) : z0;
@@ -47,7 +50,9 @@ HS_DEV double2 apply_true(LD ld, const double2* __restrict__ c, int nx, int ny, 
   double lr = __dsub_rn(__dsub_rn(__dsub_rn(__dsub_rn(4.0 * u.x, xp.x), xm.x), yp.x), ym.x);
   double li = __dsub_rn(__dsub_rn(__dsub_rn(__dsub_rn(4.0 * u.y, xp.y), xm.y), yp.y), ym.y);
   double2 cu = zmul(c[p], u);
-  return make_double2(__dsub_rn(__ddiv_rn(lr, h2), cu.x), __dsub_rn(__ddiv_rn(li, h2), cu.y));
+  const double qr = inv_h2 != 0.0 ? __dmul_rn(lr, inv_h2) : __ddiv_rn(lr, h2);
+  const double qi = inv_h2 != 0.0 ? __dmul_rn(li, inv_h2) : __ddiv_rn(li, h2);
+  return make_double2(__dsub_rn(qr, cu.x), __dsub_rn(qi, cu.y));
 }
 
 // Deterministic two-level reduction: block partials, then the last block of
@@ -92,7 +97,7 @@ __global__ void __launch_bounds__(NT) k_arnoldi(SolveDims d, SolveBuffers s, int
   auto ldz_b = [&](int q) { return ldz(zb + q); };
   for (int p = blk * NT + threadIdx.x; p < N; p += d.nblk * NT) {
     const int i = p / d.ny, jj = p - i * d.ny;
-    double2 w = apply_true(ldz_b, c, d.nx, d.ny, p, i, jj, d.h2);
+    double2 w = apply_true(ldz_b, c, d.nx, d.ny, p, i, jj, d.h2, d.inv_h2);
     if (MODE == DOT) {
       if (!isfinite(w.x) || !isfinite(w.y)) bad = 1;
       if (chunk == 0) acc[2 * KC] += w.x * w.x + w.y * w.y;
@@ -120,7 +125,9 @@ __global__ void __launch_bounds__(NT) k_arnoldi(SolveDims d, SolveBuffers s, int
   if (MODE == DOT && bad) atomicOr(&S.nonfinite, 1);
   block_sum<PST>(acc, red);
   double* part = s.partial + (((long long)b * nchunks + chunk) * d.nblk + blk) * PST;
-  if (threadIdx.x < PST) part[threadIdx.x] = acc[threadIdx.x];
+#pragma unroll
+  for (int t = 0; t < PST; ++t)  // constant indices keep acc[] in registers
+    if (threadIdx.x == t) part[t] = acc[t];
   if (!arrive_last(&s.counter[b], nchunks * d.nblk)) return;
   // ---- finish (one block per RHS)
   const double* pb = s.partial + (long long)b * nchunks * d.nblk * PST;
@@ -268,7 +275,7 @@ __global__ void __launch_bounds__(NT) k_residual(SolveDims d, SolveBuffers s, in
     double2 r = bb[p];
     if (use_x) {
       const int i = p / d.ny, jj = p - i * d.ny;
-      r = zsub(r, apply_true(ldx, c, d.nx, d.ny, p, i, jj, d.h2));
+      r = zsub(r, apply_true(ldx, c, d.nx, d.ny, p, i, jj, d.h2, d.inv_h2));
     }
     V0[p] = d2f(r);
     acc[0] += r.x * r.x + r.y * r.y;

@@ -33,6 +33,7 @@ struct SolveDims {
   int B, nx, ny, n_models;
   long long N;
   double h2;          // h*h of the finest grid
+  double inv_h2;      // 1/h2 when h2 is a power of two (x / h2 == x * inv_h2 exactly), else 0
   int restart;        // window length parameter (krylov.py:79)
   int max_iter;
   int nblk;           // blocks per RHS for the field-sweeping kernels

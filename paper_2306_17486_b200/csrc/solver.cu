@@ -5,6 +5,8 @@
 
 #include "../../include/helmsolve_b200.h"
 #include "cnn.h"
+#include <cmath>
+
 #include "common.cuh"
 #include "krylov.h"
 #include "prof.h"
@@ -76,7 +78,7 @@ __global__ void k_finalize(hs::SolveDims d, hs::SolveBuffers s, int* hist_len, i
 }
 
 int choose_nblk(long long N, int B) {
-  long long want = (4LL * 148 + B - 1) / B;
+  long long want = (8LL * 148 + B - 1) / B;
   long long cap = (N + 256 * 8 - 1) / (256 * 8);
   long long n = want < cap ? want : cap;
   return (int)(n < 1 ? 1 : n);
@@ -215,6 +217,10 @@ HS_API int hs_fgmres_solve(const hs_hierarchy_t* h, const hs_net_t* net, const h
   d.N = N;
   const double h0 = h->levels[0].h;
   d.h2 = h0 * h0;
+  {
+    int e = 0;
+    d.inv_h2 = std::frexp(d.h2, &e) == 0.5 ? 1.0 / d.h2 : 0.0;  // exact reciprocal of a power of two
+  }
   d.restart = window;
   d.max_iter = a->max_iter;
   d.nblk = choose_nblk(N, a->B);
