@@ -66,6 +66,8 @@ HS_DEV float warp_sumf(float v) {
 // `scratch` must hold NV * (blockDim.x / 32) doubles.  Deterministic order.
 template <int NV>
 HS_DEV void block_sum(double (&v)[NV], double* scratch) {
+  // scratch: NV * (nwarps + 1) doubles.  Warp sums, then thread i < NV folds
+  // value i over the warps in warp order (deterministic), then a broadcast.
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
   for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
@@ -75,12 +77,15 @@ HS_DEV void block_sum(double (&v)[NV], double* scratch) {
     for (int i = 0; i < NV; ++i) scratch[i * nw + warp] = v[i];
   }
   __syncthreads();
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
+  double* total = scratch + NV * nw;
+  for (int i = threadIdx.x; i < NV; i += blockDim.x) {
     double s = 0.0;
     for (int w = 0; w < nw; ++w) s += scratch[i * nw + w];
-    v[i] = s;
+    total[i] = s;
   }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = total[i];
   __syncthreads();
 }
 

@@ -72,7 +72,7 @@ HS_DEV bool arrive_last(int* counter, int total) {
 
 template <int MODE>
 __global__ void __launch_bounds__(NT) k_arnoldi(SolveDims d, SolveBuffers s, int nchunks) {
-  __shared__ double red[PST * (NT / 32)];
+  __shared__ double red[PST * (NT / 32 + 1)];
   __shared__ double2 s_coef[kMaxRestart + 1];
   const int blk = blockIdx.x, chunk = blockIdx.y, b = blockIdx.z;
   RhsState& S = s.st[b];
@@ -259,7 +259,7 @@ HS_DEV void start_window(RhsState& S, const SolveDims& d, double beta) {
 // else the drift guard and restart logic of krylov.py:138-143.
 template <bool INIT>
 __global__ void __launch_bounds__(NT) k_residual(SolveDims d, SolveBuffers s, int use_x) {
-  __shared__ double red[NT / 32];
+  __shared__ double red[NT / 32 + 1];
   const int blk = blockIdx.x, b = blockIdx.y;
   RhsState& S = s.st[b];
   if (!S.active) return;

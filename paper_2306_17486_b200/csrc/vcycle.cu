@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_gmres(LevelDev L, con
                                                                  const int* model_of, int m, float damping,
                                                                  int* status) {
   constexpr int NACC = 2 * (kCoarseMaxIters + 1) + 1;
-  __shared__ double red[NACC * (kCoarseThreads / 32)];
+  __shared__ double red[NACC * (kCoarseThreads / 32 + 1)];
   __shared__ double2 H[(kCoarseMaxIters + 1) * kCoarseMaxIters];
   __shared__ double2 gv[kCoarseMaxIters + 1], sn[kCoarseMaxIters], yv[kCoarseMaxIters];
   __shared__ double cs[kCoarseMaxIters], vs[kCoarseMaxIters + 1];
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_gmres(LevelDev L, con
     float2 r = rhs[p];
     acc[0] += (double)r.x * r.x + (double)r.y * r.y;
   }
-  block_sum_n<NACC>(acc, 1, red);
+  block_sum_n<NACC>(acc, 1, red);  // (acc[0] only: before acc[] is used with constant indices)
   const double beta0 = sqrt(acc[0]);
   if (beta0 == 0.0) {
     for (long long p = threadIdx.x; p < N; p += blockDim.x) x[p] = make_float2(0.f, 0.f);
@@ -247,7 +247,10 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_gmres(LevelDev L, con
     float2* W = V + (j + 1) * N;
     const float sj = (float)vs[j];
     // pass A: w = A (S .* v_j), dots with v_0..v_j, ||w||^2
-    for (int k = 0; k < 2 * (j + 1) + 1; ++k) acc[k] = 0.0;
+    // every acc[] index below is a compile-time constant (unrolled loops with
+    // k <= j guards), which keeps the partial sums in registers
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
     int bad = 0;
     for (long long p = threadIdx.x; p < N; p += blockDim.x) {
       int i = (int)(p / ny), jj = (int)(p - (long long)i * ny);
@@ -272,17 +275,19 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_gmres(LevelDev L, con
       }
     }
     if (bad) atomicOr(&s_flag, 1);
-    block_sum_n<NACC>(acc, 2 * (j + 1) + 1, red);
+    block_sum<NACC>(acc, red);
     if (s_flag) {
       if (threadIdx.x == 0) atomicCAS(status, 0, HS_ENONFINITE);
       return;
     }
     const double wn = sqrt(acc[0]);
     if (threadIdx.x == 0)
-      for (int k = 0; k <= j; ++k) {
-        hc[k] = make_double2(acc[1 + 2 * k] * vs[k], acc[2 + 2 * k] * vs[k]);
-        H[k * kCoarseMaxIters + j] = hc[k];
-      }
+#pragma unroll
+      for (int k = 0; k <= kCoarseMaxIters; ++k)
+        if (k <= j) {
+          hc[k] = make_double2(acc[1 + 2 * k] * vs[k], acc[2 + 2 * k] * vs[k]);
+          H[k * kCoarseMaxIters + j] = hc[k];
+        }
     __syncthreads();
     double hn2 = 0.0;
     for (int pass = 0; pass < 2; ++pass) {
@@ -298,25 +303,30 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_gmres(LevelDev L, con
         W[p] = w;
         acc[0] += (double)w.x * w.x + (double)w.y * w.y;
       }
-      block_sum_n<NACC>(acc, 1, red);
+      block_sum<1>(*reinterpret_cast<double(*)[1]>(acc), red);
       hn2 = acc[0];
       if (pass == 1 || sqrt(hn2) >= 0.25 * wn) break;
       // one re-orthogonalisation pass (krylov.py:105-111): extra = V^H w
-      for (int k = 0; k < 2 * (j + 1); ++k) acc[k] = 0.0;
+#pragma unroll
+      for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
       for (long long p = threadIdx.x; p < N; p += blockDim.x) {
         double2 wd = f2d(W[p]);
-        for (int k = 0; k <= j; ++k) {
-          double2 d = zcmul(f2d(vec(k)[p]), wd);
-          acc[2 * k] += d.x;
-          acc[2 * k + 1] += d.y;
-        }
+#pragma unroll
+        for (int k = 0; k <= kCoarseMaxIters; ++k)
+          if (k <= j) {
+            double2 d = zcmul(f2d(vec(k)[p]), wd);
+            acc[2 * k] += d.x;
+            acc[2 * k + 1] += d.y;
+          }
       }
-      block_sum_n<NACC>(acc, 2 * (j + 1), red);
+      block_sum<NACC>(acc, red);
       if (threadIdx.x == 0)
-        for (int k = 0; k <= j; ++k) {
-          hc[k] = make_double2(acc[2 * k] * vs[k], acc[2 * k + 1] * vs[k]);
-          H[k * kCoarseMaxIters + j] = zadd(H[k * kCoarseMaxIters + j], hc[k]);
-        }
+#pragma unroll
+        for (int k = 0; k <= kCoarseMaxIters; ++k)
+          if (k <= j) {
+            hc[k] = make_double2(acc[2 * k] * vs[k], acc[2 * k + 1] * vs[k]);
+            H[k * kCoarseMaxIters + j] = zadd(H[k * kCoarseMaxIters + j], hc[k]);
+          }
       __syncthreads();
     }
     if (threadIdx.x == 0) {
