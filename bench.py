@@ -43,6 +43,16 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+def load_traffic():
+    """DRAM bytes of one captured launch of the roofline kernel (ncu --set full, profiles/)."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "roofline_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -261,16 +271,18 @@ def main():
     # dominant kernel class: the network's convolutions (learned) or the finest V-cycle up-leg (MG only)
     if learned:
         # k_conv_tc<16,16,0>: the level-0 16->16 3x3 conv (8 of the 16 network convs per application run at
-        # level 0 and 4 of them are this kernel).  Arithmetic intensity 4608 flop / 192 B = 24 flop/B is far
-        # below the ridge (1621 TFLOP/s / 6.5 TB/s = 250), so its roof is HBM: algorithmic bytes per output
-        # pixel = 64 B input + 64 B addend-or-residual + 64 B output.
-        c_ms, c_flops, c_n = prof[_lib.PROF_CONV_L0]
-        c_bytes = c_flops / (2 * 9 * 16 * 16) * 192
+        # level 0 and 4 of them are this kernel).  Arithmetic intensity 4608 flop per output pixel over
+        # 128-192 B (input + output, + residual for the second conv of a residual block) = 24-36 flop/B is
+        # far below the ridge (1621 TFLOP/s / 6.5 TB/s = 250), so its roof is HBM.  The library's CONV_L0
+        # tag accumulates exactly those algorithmic bytes per launch (times the active RHS).
+        c_ms, c_bytes, c_n = prof[_lib.PROF_CONV_L0]
         achieved = c_bytes / (c_ms / 1e3) / 1e9 if c_ms > 0 else 0.0
+        traffic = load_traffic()
         roof = {"kernel": "k_conv_tc<16,16,0> (tcgen05 BF16x3 implicit-GEMM 3x3 conv, level 0)", "bound": "hbm",
                 "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "peak_note": f"{src} copy bandwidth; same kernel = {c_flops / (c_ms / 1e3) / 1e12:.1f} TFLOP/s "
-                             f"algorithmic", "launches": c_n, "ms_total": c_ms, "traffic": None}
+                "peak_note": f"{src} copy bandwidth", "launches": c_n, "ms_total": c_ms,
+                "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+                "traffic_note": traffic.get("note") if traffic else None}
     else:
         u_ms, u_bytes, u_n = prof[_lib.PROF_VC_UP0]
         achieved = u_bytes / (u_ms / 1e3) / 1e9 if u_ms > 0 else 0.0
@@ -284,7 +296,7 @@ def main():
     for t, (tms, work, n) in prof.items():
         breakdown[names[t]] = {"ms": round(tms, 3), "share": round(tms / ms, 4) if ms else None, "launches": n}
     for t, unit, scale in ((_lib.PROF_VCYCLE, "GB/s", 1e9), (_lib.PROF_ARNOLDI, "GB/s", 1e9),
-                           (_lib.PROF_VC_UP0, "GB/s", 1e9), (_lib.PROF_CONV_L0, "TFLOP/s", 1e12)):
+                           (_lib.PROF_VC_UP0, "GB/s", 1e9), (_lib.PROF_CONV_L0, "GB/s", 1e9)):
         tms, work, n = prof[t]
         if tms > 0:
             breakdown[names[t]]["achieved"] = round(work / (tms / 1e3) / scale, 2)

@@ -470,19 +470,22 @@ int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* 
   a.model_of = model_of;
   a.addend_per_model = addend && model_of_addend;
   prof::count(1);
-  struct Scope {
-    int s1, s2;
-    cudaStream_t st;
-    double work;
-    ~Scope() {
-      prof::stop(s2, st, work);
-      prof::stop(s1, st, work);
-    }
-  };
   const double flops =
       2.0 * 9.0 * c.cin * c.cout * (c.transposed ? (double)H * W : (double)a.Ho * a.Wo) * prof::active_hint(B);
   const bool l0 = c.cin == 16 && c.cout == 16 && c.stride == 1 && !c.transposed;
-  Scope scope{prof::start(prof::CONV, st), l0 ? prof::start(prof::CONV_L0, st) : -1, st, flops};
+  // CONV_L0 records algorithmic HBM bytes: input + output (+ addend) (+ residual), once each
+  const double l0_bytes = 4.0 * 16 * (double)H * W * (2 + (addend ? 1 : 0) + (residual ? 1 : 0)) *
+                          prof::active_hint(B);
+  struct Scope2 {
+    int s1, s2;
+    cudaStream_t st;
+    double w1, w2;
+    ~Scope2() {
+      prof::stop(s2, st, w2);
+      prof::stop(s1, st, w1);
+    }
+  };
+  Scope2 scope{prof::start(prof::CONV, st), l0 ? prof::start(prof::CONV_L0, st) : -1, st, flops, l0_bytes};
   a.residual = residual;
   a.active = active;
   if (!c.transposed && c.stride == 1) {
