@@ -185,7 +185,8 @@ struct Cfg {
     return (size_t)3 * KC * 16 * (ns * RW + ((9 - ((ns * RW) & 7)) & 7));
   }
   static constexpr size_t total(int ns, int nr) {
-    return W_BYTES + row_stage_bytes(ns) + (size_t)nr * RAW_BYTES + 8 * (2 * nr + 2 * ns + 2 * kNA) + 16 + 4 * CS;
+    return W_BYTES + row_stage_bytes(ns) + (size_t)nr * RAW_BYTES + 8 * (2 * nr + 2 * ns + 2 * kNA + 8) + 16 +
+           4 * CS;
   }
   // deepest rings that fit: raw ring 6..2, staged ring NS_MAX..3
   static constexpr int pick_nr() {
@@ -206,8 +207,18 @@ struct Cfg {
   static constexpr size_t R_BYTES = (size_t)NR * RAW_BYTES;
   static constexpr size_t TOTAL = total(NS, NR);
   static constexpr int ACOLS = NW * NACC;  // TMEM columns per accumulator
-  static constexpr int NA = 4 * ACOLS <= 512 ? 4 : 2;  // accumulators in flight (TMEM = 512 columns)
-  static constexpr int NCOLS_RAW = NA * ACOLS;
+  // A operand in TMEM (16-channel stride-1 layers): every staged row is copied
+  // once (tcgen05.cp) into a TMEM slot as its three tap views x three parts,
+  // 9 x 8 columns, and the 27 MMAs of a tile read only B from shared memory
+  // (otherwise each 4 KB A tile is re-read from smem by the three output rows
+  // that use it, and the per-MMA smem read bounds the kernel).
+  static constexpr int SLOT_COLS = 9 * 8;
+  static constexpr bool ATM = KSTEPS == 1 && MODE == 0 && MT == 128;
+  static constexpr int NA = 4 * ACOLS + (ATM ? 4 * SLOT_COLS : 0) <= 512 ? 4 : 2;  // accumulators in flight
+  static constexpr int AOFF = NA * ACOLS;                                         // first A slot column
+  static constexpr int NSA = ATM ? (512 - AOFF) / SLOT_COLS : 0;                  // TMEM A slots
+  static_assert(!ATM || NSA >= 4, "a tile reads three rows; one more slot keeps copies ahead");
+  static constexpr int NCOLS_RAW = ATM ? 512 : NA * ACOLS;
   static constexpr int NCOLS = NCOLS_RAW <= 32    ? 32
                                : NCOLS_RAW <= 64  ? 64
                                : NCOLS_RAW <= 128 ? 128
@@ -322,6 +333,45 @@ HS_DEV void mma_row9(uint32_t d, uint32_t xbase, uint32_t wbase, uint32_t accumu
 #undef HS_MMA_PARTS
 }
 
+// A-in-TMEM variants (Cfg::ATM).  cp_row9: copy one staged row into a TMEM
+// slot as tap views kx = 0, 1, 2 (start pixel PXkx) x parts 0, 1, 2, each a
+// 128-lane x 256-bit block (8 columns).  mma_row9_tm: the nine MMAs of filter
+// row ky reading those blocks; B (weights) stays in shared memory.
+template <uint32_t PX0, uint32_t PX1, uint32_t PX2, uint32_t PS>
+HS_DEV void cp_row9(uint32_t tbase, uint32_t sbase) {
+#define HS_CP_PARTS(PX, T0)                                                    \
+  "add.u32 sl, %1, " PX ";\n\tmov.b64 ds, {sl, hi};\n\t"                    \
+  "add.u32 ta, %0, " T0 ";\n\t@e tcgen05.cp.cta_group::1.128x256b [ta], ds;\n\t" \
+  "add.u32 sl, sl, %6;\n\tmov.b64 ds, {sl, hi};\n\t"                         \
+  "add.u32 ta, ta, 8;\n\t@e tcgen05.cp.cta_group::1.128x256b [ta], ds;\n\t"   \
+  "add.u32 sl, sl, %6;\n\tmov.b64 ds, {sl, hi};\n\t"                         \
+  "add.u32 ta, ta, 8;\n\t@e tcgen05.cp.cta_group::1.128x256b [ta], ds;\n\t"
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b64 ds;\n\t.reg .b32 hi, sl, ta;\n\t"
+      "mov.b32 hi, %2;\n\telect.sync _|e, 0xffffffff;\n\t"
+      HS_CP_PARTS("%3", "0") HS_CP_PARTS("%4", "24") HS_CP_PARTS("%5", "48") "}\n" ::"r"(tbase),
+      "r"(sbase), "n"(kDescHi), "n"(PX0), "n"(PX1), "n"(PX2), "n"(PS)
+      : "memory");
+#undef HS_CP_PARTS
+}
+
+template <uint32_t I0, uint32_t I1, uint32_t I2, uint32_t WT>
+HS_DEV void mma_row9_tm(uint32_t d, uint32_t abase, uint32_t wbase, uint32_t accumulate) {
+#define HS_MMA_TM(B0, P0)                                                           \
+  "add.u32 bl, %2, " B0 ";\n\tmov.b64 db, {bl, hi};\n\t"                          \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], db, i0, " P0 ";\n\tadd.u32 ta, ta, 8;\n\t" \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], db, i1, t;\n\tadd.u32 ta, ta, 8;\n\t"      \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], db, i2, t;\n\tadd.u32 ta, ta, 8;\n\t"
+  asm volatile(
+      "{\n\t.reg .pred p, t, e;\n\t.reg .b64 db;\n\t.reg .b32 hi, i0, i1, i2, bl, ta;\n\t"
+      "mov.b32 hi, %4;\n\tmov.b32 i0, %5;\n\tmov.b32 i1, %6;\n\tmov.b32 i2, %7;\n\t"
+      "setp.ne.b32 p, %3, 0;\n\tsetp.eq.b32 t, %3, %3;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "mov.b32 ta, %1;\n\t"
+      HS_MMA_TM("0", "p") HS_MMA_TM("%8", "t") HS_MMA_TM("%9", "t") "}\n" ::"r"(d), "r"(abase), "r"(wbase),
+      "r"(accumulate), "n"(kDescHi), "n"(I0), "n"(I1), "n"(I2), "n"(WT), "n"(2 * WT));
+#undef HS_MMA_TM
+}
+
 template <typename C, int MT>
 HS_DEV void tap_mmas(uint32_t d, const DescBase& db, uint32_t x_units, uint32_t w_units, uint32_t& first) {
   constexpr uint32_t X_STEP = 2 * C::XPL, W_STEP = 2 * C::NW;  // two 16-byte chunks per K step
@@ -395,7 +445,8 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
   uint64_t* stg_empty = stg_full + NS;
   uint64_t* acc_full = stg_empty + NS;
   uint64_t* acc_empty = acc_full + C::NA;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(acc_empty + C::NA);
+  uint64_t* a_empty = acc_empty + C::NA;  // TMEM A slots (C::ATM)
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(a_empty + 8);
   float* s_bias = reinterpret_cast<float*>(s_tmem + 4);  // this CTA's cout slice
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long nunits = num_units<MODE, MT>(a, NSPLIT);
@@ -429,6 +480,7 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
       mbar_init(smem_u32(&acc_full[i]), 1);
       mbar_init(smem_u32(&acc_empty[i]), 32 * kEpiWarps);
     }
+    for (int i = 0; i < C::NSA; ++i) mbar_init(smem_u32(&a_empty[i]), 1);
     fence_mbar_init();
   }
   if (warp == 0) {
@@ -540,6 +592,56 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
       const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
       uint32_t seq0 = 0;  // staged sequence number of the unit's first row
       uint32_t tile = 0;
+      if constexpr (C::ATM) {
+        // A in TMEM: each staged row is copied into a TMEM slot once (then its smem
+        // slot goes straight back to the converters); the MMAs read the slots
+        constexpr uint32_t WT = C::KC * C::NW;
+        constexpr uint32_t I0 = idesc_bf16(MT, 3 * CS), I1 = idesc_bf16(MT, 2 * CS), I2 = idesc_bf16(MT, CS);
+        constexpr uint32_t PS = (uint32_t)(C::XP_BYTES / 16);
+        for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
+          Unit U;
+          if (!unit_at<MODE, MT>(a, NSPLIT, u, U)) continue;
+          auto slot = [&](int g) { return (seq0 + (uint32_t)(g - U.glo)) % NS; };         // smem staged slot
+          auto tslot = [&](int g) { return (seq0 + (uint32_t)(g - U.glo)) % C::NSA; };   // TMEM A slot
+          int loaded = U.glo - 1;   // highest input row copied into TMEM
+          int retired = U.glo - 1;  // highest input row whose TMEM slot was released
+          for (int oy = U.oy0; oy < U.oy1; ++oy, ++tile) {
+            int lo, hi;
+            tile_rows<MODE>(oy, lo, hi);
+            for (int g = loaded + 1; g <= hi; ++g) {
+              const uint32_t sq = seq0 + (uint32_t)(g - U.glo);
+              mbar_wait(smem_u32(&stg_full[sq % NS]), (sq / NS) & 1);
+              const uint32_t tuse = sq / C::NSA;
+              if (tuse > 0) mbar_wait(smem_u32(&a_empty[sq % C::NSA]), (tuse - 1) & 1);
+              tc_fence_after();
+              cp_row9<0, 1, 2, PS>(tm + C::AOFF + tslot(g) * C::SLOT_COLS, db.x[0] + slot(g) * C::RW);
+              mma_commit(smem_u32(&stg_empty[sq % NS]));  // smem slot free once the copies land
+            }
+            loaded = max(loaded, hi);
+            const uint32_t acc = tile % C::NA;
+            const uint32_t ause = tile / C::NA;
+            if (ause > 0) mbar_wait(smem_u32(&acc_empty[acc]), (ause - 1) & 1);
+            tc_fence_after();
+            const uint32_t d0 = tm + acc * C::ACOLS;
+            if (!(a.dbg & 2)) {
+#pragma unroll
+              for (int ky = 0; ky < 3; ++ky)
+                mma_row9_tm<I0, I1, I2, WT>(d0, tm + C::AOFF + tslot(oy - 1 + ky) * C::SLOT_COLS,
+                                            db.w + ky * 3 * WT, ky ? 1u : 0u);
+            }
+            mma_commit(smem_u32(&acc_full[acc]));
+            int keep_lo = U.ghi + 1;
+            if (oy + 1 < U.oy1) {
+              int nl, nh;
+              tile_rows<MODE>(oy + 1, nl, nh);
+              keep_lo = nl;
+            }
+            for (int g = retired + 1; g < keep_lo && g <= loaded; ++g) mma_commit(smem_u32(&a_empty[tslot(g)]));
+            retired = max(retired, min(keep_lo - 1, loaded));
+          }
+          seq0 += U.ghi - U.glo + 1;
+        }
+      } else
       for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
         Unit U;
         if (!unit_at<MODE, MT>(a, NSPLIT, u, U)) continue;

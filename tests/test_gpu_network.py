@@ -72,7 +72,8 @@ def test_tconv_shapes(rng, cin, cout, hw):
     assert relerr(y, no.softplus(no.conv_transpose2d(x, w, b)) + skip) < 2e-6
 
 
-@pytest.mark.parametrize("cin,cout,mode,hw", [(16, 16, 0, (6, 128)), (16, 16, 0, (5, 256)), (32, 32, 0, (4, 128)),
+@pytest.mark.parametrize("cin,cout,mode,hw", [(16, 16, 0, (6, 128)), (16, 16, 0, (5, 256)), (16, 16, 0, (70, 128)),
+                                               (32, 32, 0, (4, 128)),
                                                (16, 32, 1, (6, 256)), (32, 16, 2, (3, 128)), (32, 16, 2, (2, 256)),
                                                # M = 64 tiles (64-wide levels) and cout split across CTAs
                                                (16, 16, 0, (5, 64)), (32, 32, 0, (3, 64)), (64, 64, 0, (4, 64)),
