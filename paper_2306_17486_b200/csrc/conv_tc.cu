@@ -48,12 +48,10 @@
 namespace hs {
 namespace {
 
-constexpr int kNT = 384;  // 12 warps
 constexpr int kBand = 32; // output rows per work unit
 constexpr int kPrefetch = 8;  // rows pulled into L2 ahead of the bulk copies / epilogue loads
 constexpr int kNA = 4;    // TMEM accumulators in flight
-constexpr int kEpiWarps = 8, kCvtWarp0 = 8, kCvtWarps = 2, kProdWarp = 10, kMmaWarp = 11;
-constexpr int kCvtThreads = 32 * kCvtWarps;
+constexpr int kEpiWarps = 8, kCvtWarp0 = 8;  // epilogue warps 0-7, converters from warp 8
 constexpr size_t kSmemMax = 232448;
 
 HS_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -180,7 +178,14 @@ struct Cfg {
   static constexpr int RAW_BYTES = RW * CIN * 4;
   static constexpr int NW = 3 * CS;                            // stacked weight rows [W0; W1; W2]
   static constexpr size_t W_BYTES = (size_t)9 * KC * NW * 16;
-  static constexpr int NS_MIN = 3, NS_MAX = MODE == 0 ? 10 : (MODE == 1 ? 8 : 6);
+  // A operand in TMEM (see below) for 16-channel stride-1 layers at M = 128
+  static constexpr bool ATM = KSTEPS == 1 && MODE == 0 && MT == 128;
+  // warp roles: epilogue 0-7, converters (four when they also write the TMEM A
+  // slots: a warp may only touch its own TMEM lane quarter), producer, MMA issuer
+  static constexpr int NCVT = ATM ? 4 : 2, CVT_THREADS = 32 * NCVT;
+  static constexpr int PROD = kCvtWarp0 + NCVT, MMAW = PROD + 1, NT = 32 * (MMAW + 1);
+  // staged ring: ATM converters consume their own staged rows at once (two slots)
+  static constexpr int NS_MIN = ATM ? 2 : 3, NS_MAX = ATM ? 2 : (MODE == 0 ? 10 : (MODE == 1 ? 8 : 6));
   static constexpr size_t row_stage_bytes(int ns) {
     return (size_t)3 * KC * 16 * (ns * RW + ((9 - ((ns * RW) & 7)) & 7));
   }
@@ -190,7 +195,7 @@ struct Cfg {
   }
   // deepest rings that fit: raw ring 6..2, staged ring NS_MAX..3
   static constexpr int pick_nr() {
-    for (int nr = 6; nr >= 2; --nr)
+    for (int nr = ATM ? 8 : 6; nr >= 2; --nr)
       if (total(NS_MIN, nr) <= kSmemMax && total(NS_MAX < 4 ? NS_MAX : 4, nr) <= kSmemMax) return nr;
     return 2;
   }
@@ -207,17 +212,17 @@ struct Cfg {
   static constexpr size_t R_BYTES = (size_t)NR * RAW_BYTES;
   static constexpr size_t TOTAL = total(NS, NR);
   static constexpr int ACOLS = NW * NACC;  // TMEM columns per accumulator
-  // A operand in TMEM (16-channel stride-1 layers): every staged row is copied
-  // once (tcgen05.cp) into a TMEM slot as its three tap views x three parts,
-  // 9 x 8 columns, and the 27 MMAs of a tile read only B from shared memory
-  // (otherwise each 4 KB A tile is re-read from smem by the three output rows
-  // that use it, and the per-MMA smem read bounds the kernel).
+  // A operand in TMEM (16-channel stride-1 layers): the converters write every
+  // input row once into a TMEM slot as its three tap views x three parts
+  // (9 x 8 columns, tcgen05.st), and the 27 MMAs of a tile read only B from
+  // shared memory.  With A in shared memory each MMA is bound by its 4 KB A
+  // read (~40 cycles at 128 B/clk, measured); from TMEM an N = 48 MMA issues
+  // at its math rate (24 cycles).
   static constexpr int SLOT_COLS = 9 * 8;
-  static constexpr bool ATM = KSTEPS == 1 && MODE == 0 && MT == 128;
   static constexpr int NA = 4 * ACOLS + (ATM ? 4 * SLOT_COLS : 0) <= 512 ? 4 : 2;  // accumulators in flight
   static constexpr int AOFF = NA * ACOLS;                                         // first A slot column
   static constexpr int NSA = ATM ? (512 - AOFF) / SLOT_COLS : 0;                  // TMEM A slots
-  static_assert(!ATM || NSA >= 4, "a tile reads three rows; one more slot keeps copies ahead");
+  static_assert(!ATM || (NSA >= 4 && NSA <= 4), "a tile reads three rows; one more slot keeps writes ahead");
   static constexpr int NCOLS_RAW = ATM ? 512 : NA * ACOLS;
   static constexpr int NCOLS = NCOLS_RAW <= 32    ? 32
                                : NCOLS_RAW <= 64  ? 64
@@ -431,7 +436,7 @@ HS_DEV void issue_mmas(int oy, uint32_t d0, const DescBase& db, SlotOf slot) {
 }
 
 template <int CIN, int COUT, int MODE, int MT, int CS>
-__global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
+__global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc(TcArgs a) {
   using C = Cfg<CIN, COUT, MODE, MT, CS>;
   constexpr int KC = C::KC, NS = C::NS, NR = C::NR, NW = C::NW, NSPLIT = C::NSPLIT;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -445,8 +450,9 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
   uint64_t* stg_empty = stg_full + NS;
   uint64_t* acc_full = stg_empty + NS;
   uint64_t* acc_empty = acc_full + C::NA;
-  uint64_t* a_empty = acc_empty + C::NA;  // TMEM A slots (C::ATM)
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(a_empty + 8);
+  uint64_t* a_full = acc_empty + C::NA;  // TMEM A slots (C::ATM)
+  uint64_t* a_empty = a_full + 4;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(a_empty + 4);
   float* s_bias = reinterpret_cast<float*>(s_tmem + 4);  // this CTA's cout slice
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long nunits = num_units<MODE, MT>(a, NSPLIT);
@@ -455,7 +461,7 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
   const int my_split = (int)(blockIdx.x % NSPLIT);
 
   // ---- setup: resident weight stack [W0; W1; W2] of this slice, layout (tap, chunk, row) x 16 B
-  for (int e = tid; e < 9 * KC * CS; e += kNT) {
+  for (int e = tid; e < 9 * KC * CS; e += C::NT) {
     const int n = e % CS, c = (e / CS) % KC, t = e / (CS * KC);
     const float* src = a.w + ((size_t)(my_split * CS + n) * 9 + t) * CIN + 8 * c;
     const float4 v0 = __ldg(reinterpret_cast<const float4*>(src)), v1 = __ldg(reinterpret_cast<const float4*>(src + 4));
@@ -466,21 +472,24 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
     for (int part = 0; part < 3; ++part)
       *reinterpret_cast<uint4*>(wst + ((size_t)(t * KC + c) * NW + part * CS + n) * 16) = p[part];
   }
-  for (int n = tid; n < CS; n += kNT) s_bias[n] = a.bias[my_split * CS + n];
+  for (int n = tid; n < CS; n += C::NT) s_bias[n] = a.bias[my_split * CS + n];
   if (tid == 0) {
     for (int i = 0; i < NR; ++i) {
       mbar_init(smem_u32(&raw_full[i]), 1);
-      mbar_init(smem_u32(&raw_empty[i]), kCvtThreads);
+      mbar_init(smem_u32(&raw_empty[i]), C::CVT_THREADS);
     }
     for (int i = 0; i < NS; ++i) {
-      mbar_init(smem_u32(&stg_full[i]), kCvtThreads);
+      mbar_init(smem_u32(&stg_full[i]), C::CVT_THREADS);
       mbar_init(smem_u32(&stg_empty[i]), 1);
     }
     for (int i = 0; i < C::NA; ++i) {
       mbar_init(smem_u32(&acc_full[i]), 1);
       mbar_init(smem_u32(&acc_empty[i]), 32 * kEpiWarps);
     }
-    for (int i = 0; i < C::NSA; ++i) mbar_init(smem_u32(&a_empty[i]), 1);
+    for (int i = 0; i < C::NSA; ++i) {
+      mbar_init(smem_u32(&a_full[i]), C::CVT_THREADS);
+      mbar_init(smem_u32(&a_empty[i]), 1);
+    }
     fence_mbar_init();
   }
   if (warp == 0) {
@@ -494,7 +503,7 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
 
-  if (warp == kProdWarp) {
+  if (warp == C::PROD) {
     // ================= producer: raw row segments, global -> smem (bulk copies)
     if (lane == 0) {
       long long seq = 0;
@@ -546,7 +555,7 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
         }
       }
     }
-  } else if (warp >= kCvtWarp0 && warp < kCvtWarp0 + kCvtWarps) {
+  } else if (warp >= kCvtWarp0 && warp < kCvtWarp0 + C::NCVT) {
     // ================= converters: raw fp32 -> staged bf16x3
     const int ct = tid - 32 * kCvtWarp0;
     long long seq = 0;
@@ -558,11 +567,11 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
       for (int g = U.glo; g <= U.ghi; ++g, ++seq) {
         const int rs = (int)(seq % NR), ss = (int)(seq % NS);
         const long long suse = seq / NS;
-        if (suse > 0) mbar_wait(smem_u32(&stg_empty[ss]), (uint32_t)((suse - 1) & 1));
+        if (!C::ATM && suse > 0) mbar_wait(smem_u32(&stg_empty[ss]), (uint32_t)((suse - 1) & 1));
         mbar_wait(smem_u32(&raw_full[rs]), (uint32_t)((seq / NR) & 1));
         const bool row_ok = g >= 0 && g < a.H;
         const unsigned char* src = raw + (size_t)rs * C::RAW_BYTES;
-        for (int e = ct; e < ((a.dbg & 1) ? 0 : C::RW * KC); e += kCvtThreads) {
+        for (int e = ct; e < ((a.dbg & 1) ? 0 : C::RW * KC); e += C::CVT_THREADS) {
           const int p = e / KC, c = e - p * KC;  // chunk fastest: conflict-free raw reads
           float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
           if (row_ok && p >= clo && p < chi) {
@@ -576,12 +585,39 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
 #pragma unroll
           for (int part = 0; part < 3; ++part) *reinterpret_cast<uint4*>(xp[part] + off) = p3[part];
         }
-        fence_async_smem();
-        mbar_arrive(smem_u32(&raw_empty[rs]));
-        mbar_arrive(smem_u32(&stg_full[ss]));
+        if constexpr (C::ATM) {
+          // every converter thread owns TMEM lane m = tile row m (a warp may only
+          // write its own lane quarter): write the row's three tap views x three
+          // parts of pixel m + kx from the staged row into TMEM slot `as`
+          mbar_arrive(smem_u32(&raw_empty[rs]));
+          asm volatile("bar.sync 1, %0;" ::"n"(C::CVT_THREADS) : "memory");  // staged row complete
+          const uint32_t as = (uint32_t)(seq % C::NSA), ause = (uint32_t)(seq / C::NSA);
+          if (ause > 0) mbar_wait(smem_u32(&a_empty[as]), (ause - 1) & 1);
+          tc_fence_after();
+          const int q = warp & 3, m = 32 * q + lane;
+          const uint32_t tcol = tmem + ((uint32_t)(32 * q) << 16) + C::AOFF + as * C::SLOT_COLS;
+#pragma unroll
+          for (int kx = 0; kx < 3; ++kx)
+#pragma unroll
+            for (int part = 0; part < 3; ++part) {
+              const unsigned char* b0 = xp[part] + ((size_t)ss * C::RW + m + kx) * 16;
+              const uint4 lo = *reinterpret_cast<const uint4*>(b0);                          // channels 0-7
+              const uint4 hi = *reinterpret_cast<const uint4*>(b0 + (size_t)C::XPL * 16);  // channels 8-15
+              asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                               tcol + (kx * 3 + part) * 8),
+                           "r"(lo.x), "r"(lo.y), "r"(lo.z), "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w));
+            }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          mbar_arrive(smem_u32(&a_full[as]));
+        } else {
+          fence_async_smem();
+          mbar_arrive(smem_u32(&raw_empty[rs]));
+          mbar_arrive(smem_u32(&stg_full[ss]));
+        }
       }
     }
-  } else if (warp == kMmaWarp) {
+  } else if (warp == C::MMAW) {
     // ================= MMA issuer
     {  // the whole warp walks the schedule; mma_bf16 / mma_commit elect one lane
       DescBase db;
@@ -593,29 +629,22 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
       uint32_t seq0 = 0;  // staged sequence number of the unit's first row
       uint32_t tile = 0;
       if constexpr (C::ATM) {
-        // A in TMEM: each staged row is copied into a TMEM slot once (then its smem
-        // slot goes straight back to the converters); the MMAs read the slots
+        // A in TMEM: the converters write each input row once into a TMEM slot
+        // (a_full); the MMAs read the slots and release them (a_empty)
         constexpr uint32_t WT = C::KC * C::NW;
         constexpr uint32_t I0 = idesc_bf16(MT, 3 * CS), I1 = idesc_bf16(MT, 2 * CS), I2 = idesc_bf16(MT, CS);
-        constexpr uint32_t PS = (uint32_t)(C::XP_BYTES / 16);
         for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
           Unit U;
           if (!unit_at<MODE, MT>(a, NSPLIT, u, U)) continue;
-          auto slot = [&](int g) { return (seq0 + (uint32_t)(g - U.glo)) % NS; };         // smem staged slot
           auto tslot = [&](int g) { return (seq0 + (uint32_t)(g - U.glo)) % C::NSA; };   // TMEM A slot
-          int loaded = U.glo - 1;   // highest input row copied into TMEM
+          int loaded = U.glo - 1;   // highest input row known to be in TMEM
           int retired = U.glo - 1;  // highest input row whose TMEM slot was released
           for (int oy = U.oy0; oy < U.oy1; ++oy, ++tile) {
             int lo, hi;
             tile_rows<MODE>(oy, lo, hi);
             for (int g = loaded + 1; g <= hi; ++g) {
               const uint32_t sq = seq0 + (uint32_t)(g - U.glo);
-              mbar_wait(smem_u32(&stg_full[sq % NS]), (sq / NS) & 1);
-              const uint32_t tuse = sq / C::NSA;
-              if (tuse > 0) mbar_wait(smem_u32(&a_empty[sq % C::NSA]), (tuse - 1) & 1);
-              tc_fence_after();
-              cp_row9<0, 1, 2, PS>(tm + C::AOFF + tslot(g) * C::SLOT_COLS, db.x[0] + slot(g) * C::RW);
-              mma_commit(smem_u32(&stg_empty[sq % NS]));  // smem slot free once the copies land
+              mbar_wait(smem_u32(&a_full[sq % C::NSA]), (sq / C::NSA) & 1);
             }
             loaded = max(loaded, hi);
             const uint32_t acc = tile % C::NA;
@@ -692,9 +721,13 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
       const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[U.b] : 0) : U.b) *
                                                    a.addend_bstride
                                   : nullptr;
-      // addend + residual do not depend on the accumulator: row oy + 1 is
-      // fetched (and summed) while row oy waits on its MMAs
-      auto fetch = [&](int oy, float4(&p)[C::NACC][EH / 4]) {
+      // addend and residual do not depend on the accumulator: row oy + 1's are
+      // loaded while row oy waits on its MMAs, and only added at the store (an
+      // add right after the load would stall on it)
+      // (wide transposed tiles have no registers to spare: there the two are summed at load)
+      constexpr bool SPLIT = C::NACC * EH <= 16;
+      constexpr int RK = SPLIT ? C::NACC : 1, RQ = SPLIT ? EH / 4 : 1;
+      auto fetch = [&](int oy, float4(&pa)[C::NACC][EH / 4], float4(&pr)[RK][RQ]) {
 #pragma unroll
         for (int k = 0; k < C::NACC; ++k) {
           const int ox = MODE == 2 ? 2 * (U.xb * MT + m) + k : U.xb * MT + m;
@@ -702,24 +735,26 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
           const size_t obase = (size_t)U.b * a.Ho * a.Wo * COUT + pix * COUT + n_base;
 #pragma unroll
           for (int q = 0; q < EH / 4; ++q) {
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (add && lane_ok) v = __ldg(reinterpret_cast<const float4*>(add + pix * COUT + n_base) + q);
-            if (a.residual && lane_ok) {
-              const float4 rs = __ldg(reinterpret_cast<const float4*>(a.residual + obase) + q);
-              v.x += rs.x;
-              v.y += rs.y;
-              v.z += rs.z;
-              v.w += rs.w;
+            pa[k][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (add && lane_ok) pa[k][q] = __ldg(reinterpret_cast<const float4*>(add + pix * COUT + n_base) + q);
+            float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (a.residual && lane_ok) r = __ldg(reinterpret_cast<const float4*>(a.residual + obase) + q);
+            if constexpr (SPLIT) {
+              pr[k][q] = r;
+            } else {
+              pa[k][q].x += r.x;
+              pa[k][q].y += r.y;
+              pa[k][q].z += r.z;
+              pa[k][q].w += r.w;
             }
-            p[k][q] = v;
           }
         }
       };
-      float4 pre[C::NACC][EH / 4], nxt[C::NACC][EH / 4];
-      fetch(U.oy0, pre);
+      float4 pre_a[C::NACC][EH / 4], nxt_a[C::NACC][EH / 4], pre_r[RK][RQ], nxt_r[RK][RQ];
+      fetch(U.oy0, pre_a, pre_r);
       for (int oy = U.oy0; oy < U.oy1; ++oy, ++tile) {
         const int acc = (int)(tile % C::NA);
-        if (oy + 1 < U.oy1) fetch(oy + 1, nxt);
+        if (oy + 1 < U.oy1) fetch(oy + 1, nxt_a, nxt_r);
         mbar_wait(smem_u32(&acc_full[acc]), (uint32_t)((tile / C::NA) & 1));
         tc_fence_after();
         // the three column groups hold the x0-, x1- and x2-weighted partial sums:
@@ -757,11 +792,12 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
                 o.z = softplus_fast(o.z);
                 o.w = softplus_fast(o.w);
               }
-              const float4 ad = pre[k][n0 / 4];
-              o.x += ad.x;
-              o.y += ad.y;
-              o.z += ad.z;
-              o.w += ad.w;
+              const float4 ad = pre_a[k][n0 / 4];
+              const float4 rs = SPLIT ? pre_r[SPLIT ? k : 0][SPLIT ? n0 / 4 : 0] : make_float4(0.f, 0.f, 0.f, 0.f);
+              o.x += ad.x + rs.x;
+              o.y += ad.y + rs.y;
+              o.z += ad.z + rs.z;
+              o.w += ad.w + rs.w;
               *reinterpret_cast<float4*>(a.y + obase + n0) = o;
             }
           }
@@ -769,7 +805,10 @@ __global__ void __launch_bounds__(kNT, 1) k_conv_tc(TcArgs a) {
 #pragma unroll
         for (int k = 0; k < C::NACC; ++k)
 #pragma unroll
-          for (int q = 0; q < EH / 4; ++q) pre[k][q] = nxt[k][q];
+          for (int q = 0; q < EH / 4; ++q) {
+            pre_a[k][q] = nxt_a[k][q];
+            if constexpr (SPLIT) pre_r[k][q] = nxt_r[k][q];
+          }
       }
     }
   }
@@ -798,7 +837,7 @@ void launch_tc(const TcArgs& a, cudaStream_t st) {
   const long long nunits = num_units<MODE, MT>(a, C::NSPLIT);
   long long grid = (sms / C::NSPLIT) * C::NSPLIT;  // a multiple of NSPLIT: fixed slice per CTA
   if (nunits < grid) grid = nunits;
-  k_conv_tc<CIN, COUT, MODE, MT, CS><<<(unsigned)grid, kNT, C::TOTAL, st>>>(a);
+  k_conv_tc<CIN, COUT, MODE, MT, CS><<<(unsigned)grid, C::NT, C::TOTAL, st>>>(a);
 }
 
 // (cin, cout, mode) -> cout slice per CTA, or 0 if not on the tensor-core path

@@ -18,7 +18,7 @@ __device__ __forceinline__ uint64_t desc(uint32_t saddr, uint32_t lbo, uint32_t 
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
 }
 
-template <int M, int N, bool ATMEM, int NMMA, int ND, int NWI = 1>
+template <int M, int N, bool ATMEM, int NMMA, int ND, int NWI = 1, bool CONSTP = false>
 __global__ void k_bench(long long* out) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint32_t s_tmem;
@@ -38,44 +38,63 @@ __global__ void k_bench(long long* out) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s_tmem;
-  if ((threadIdx.x & 31) == 0 && warp < NWI) {
-    const uint64_t da = desc(smem_u32(smem), 128 * 16, 128);
-    const uint64_t db = desc(smem_u32(smem + 32768), N * 16, 128);
+  if (warp < NWI) {  // converged issuing warps; one elected lane issues, 8 MMAs per asm block
+    const uint32_t da = (uint32_t)(desc(smem_u32(smem), 128 * 16, 128) & 0xffffffffu);
+    const uint32_t db = (uint32_t)(desc(smem_u32(smem + 32768), N * 16, 128) & 0xffffffffu);
+    const uint32_t hi = (uint32_t)(desc(0, 0, 128) >> 32);
     const uint32_t id = idesc_bf16(M, N);
     const uint32_t ta = tmem + 256;
+    const uint32_t d = tmem + (uint32_t)(warp * 64);
     long long t0 = clock64();
 #pragma unroll 1
-    for (int i = 0; i < NMMA; i += 16) {
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const uint32_t d = tmem + (uint32_t)(warp * 64) + (uint32_t)((k % ND) * (64 / ND));  // per-warp accumulators
-        if (ATMEM)
-          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
-                       "r"(ta), "l"(db), "r"(id), "r"(i + k));
-        else
-          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
-                       "l"(da), "l"(db), "r"(id), "r"(i + k));
-      }
+    for (int i = 0; i < NMMA; i += 8) {
+      if (ATMEM)
+        asm volatile(
+            "{\n\t.reg .pred e;\n\t.reg .b64 db;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\tmov.b64 db, {%2, %3};\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], db, %4, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], db, %4, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], db, %4, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], db, %4, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], db, %4, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], db, %4, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], db, %4, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], db, %4, 1;\n\t}\n" ::"r"(d),
+            "r"(ta), "r"(db), "r"(hi), "r"(id));
+      else
+        asm volatile(
+            "{\n\t.reg .pred e;\n\t.reg .b64 da, db;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\tmov.b64 db, {%2, %3};\n\tmov.b64 da, {%1, %3};\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %4, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %4, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %4, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %4, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %4, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %4, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %4, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %4, 1;\n\t}\n" ::"r"(d),
+            "r"(da), "r"(db), "r"(hi), "r"(id));
     }
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar[warp]))
-                 : "memory");
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+            smem_u32(&bar[warp]))
+        : "memory");
     asm volatile(
         "{\n\t.reg .pred P1;\n\tW:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t@P1 bra D;\n\tbra W;\n\tD:\n\t}\n" ::"r"(
             smem_u32(&bar[warp])));
     long long t1 = clock64();
-    if (warp == 0) out[blockIdx.x] = t1 - t0;
+    if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-template <int M, int N, bool ATMEM, int ND = 1, int NWI = 1>
+template <int M, int N, bool ATMEM, int ND = 1, int NWI = 1, bool CONSTP = false>
 void run(long long* d) {
   constexpr int NMMA = 4096;
-  auto k = k_bench<M, N, ATMEM, NMMA, ND, NWI>;
+  auto k = k_bench<M, N, ATMEM, NMMA, ND, NWI, CONSTP>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   k<<<1, 128, 64 * 1024>>>(d);
   k<<<1, 128, 64 * 1024>>>(d);
@@ -86,17 +105,102 @@ void run(long long* d) {
          cudaGetErrorString(e));
 }
 
+
+// tcgen05.cp 128x256b (4 KB smem -> TMEM) rate, and tcgen05.st 32x32b.x8 (1 KB per warp) rate
+template <int NCP>
+__global__ void k_cp(long long* out) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint32_t s_tmem;
+  __shared__ __align__(8) uint64_t bar;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s_tmem;
+  if (warp == 0) {
+    const uint32_t sl = (uint32_t)(desc(smem_u32(smem), 128 * 16, 128) & 0xffffffffu);
+    const uint32_t hi = (uint32_t)(desc(0, 0, 128) >> 32);
+    long long t0 = clock64();
+#pragma unroll 1
+    for (int i = 0; i < NCP; i += 8)
+      asm volatile(
+          "{\n\t.reg .pred e;\n\t.reg .b64 ds;\n\telect.sync _|e, 0xffffffff;\n\tmov.b64 ds, {%1, %2};\n\t"
+          "@e tcgen05.cp.cta_group::1.128x256b [%0], ds;\n\t@e tcgen05.cp.cta_group::1.128x256b [%0], ds;\n\t"
+          "@e tcgen05.cp.cta_group::1.128x256b [%0], ds;\n\t@e tcgen05.cp.cta_group::1.128x256b [%0], ds;\n\t"
+          "@e tcgen05.cp.cta_group::1.128x256b [%0], ds;\n\t@e tcgen05.cp.cta_group::1.128x256b [%0], ds;\n\t"
+          "@e tcgen05.cp.cta_group::1.128x256b [%0], ds;\n\t@e tcgen05.cp.cta_group::1.128x256b [%0], ds;\n\t}\n" ::"r"(
+              tmem + 256),
+          "r"(sl), "r"(hi));
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(&bar))
+        : "memory");
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tW:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t@P1 bra D;\n\tbra W;\n\tD:\n\t}\n" ::"r"(
+            smem_u32(&bar)));
+    long long t1 = clock64();
+    if (threadIdx.x == 0) out[0] = t1 - t0;
+  }
+  // tcgen05.st: 4 warps (all lane quarters) each store x8 (32 lanes x 8 columns = 1 KB) NCP times
+  __syncthreads();
+  if (warp < 4) {
+    uint32_t r[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) r[i] = i;
+    const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + 256;
+    long long t0 = clock64();
+#pragma unroll 1
+    for (int i = 0; i < NCP / 4; ++i)
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+          "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(ta + (i & 3) * 32),
+          "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+          "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
+          "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
+          "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    long long t1 = clock64();
+    if (threadIdx.x == 0) out[1] = t1 - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+void run_cp(long long* d) {
+  constexpr int NCP = 4096;
+  cudaFuncSetAttribute(k_cp<NCP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  k_cp<NCP><<<1, 128, 64 * 1024>>>(d);
+  k_cp<NCP><<<1, 128, 64 * 1024>>>(d);
+  long long h[2] = {0, 0};
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  printf("tcgen05.cp 128x256b: %.1f cycles each (%.0f B/clk); tcgen05.st x32 per warp, 4 warps: %.1f cycles each "
+         "(%.0f B/clk aggregate)\n",
+         (double)h[0] / NCP, 4096.0 * NCP / h[0], (double)h[1] / (NCP / 4), 4.0 * 4096 * (NCP / 4) / h[1]);
+}
+
 int main() {
   long long* d;
   cudaMalloc(&d, 1024 * sizeof(long long));
+  run_cp(d);
+  run<128, 16, false, 1, 1>(d);
   run<128, 48, false, 1, 1>(d);
+  run<128, 96, false, 1, 1>(d);
+  run<128, 16, true, 1, 1>(d);
+  run<128, 48, true, 1, 1>(d);
+  run<128, 96, true, 1, 1>(d);
   run<128, 48, false, 1, 2>(d);
-  run<128, 48, false, 1, 4>(d);
-  run<128, 16, false, 1, 2>(d);
-  run<128, 16, false, 1, 4>(d);
-  run<128, 96, false, 1, 2>(d);
   run<128, 48, true, 1, 2>(d);
+  run<128, 16, true, 1, 2>(d);
   run<128, 48, true, 1, 4>(d);
-  run<128, 256, false, 1, 2>(d);
+  run<128, 16, true, 1, 4>(d);
   return 0;
 }
