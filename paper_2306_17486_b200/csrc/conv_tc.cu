@@ -190,7 +190,7 @@ struct Cfg {
     return (size_t)3 * KC * 16 * (ns * RW + ((9 - ((ns * RW) & 7)) & 7));
   }
   static constexpr size_t total(int ns, int nr) {
-    return W_BYTES + row_stage_bytes(ns) + (size_t)nr * RAW_BYTES + 8 * (2 * nr + 2 * ns + 2 * kNA + 8) + 16 +
+    return W_BYTES + row_stage_bytes(ns) + (size_t)nr * RAW_BYTES + 8 * (2 * nr + 2 * ns + 2 * kNA + 12) + 16 +
            4 * CS;
   }
   // deepest rings that fit: raw ring 6..2, staged ring NS_MAX..3
@@ -219,10 +219,12 @@ struct Cfg {
   // read (~40 cycles at 128 B/clk, measured); from TMEM an N = 48 MMA issues
   // at its math rate (24 cycles).
   static constexpr int SLOT_COLS = 9 * 8;
-  static constexpr int NA = 4 * ACOLS + (ATM ? 4 * SLOT_COLS : 0) <= 512 ? 4 : 2;  // accumulators in flight
+  // accumulators in flight; ATM keeps two and gives TMEM to five A slots (a tile
+  // reads three rows, so the converters run two rows ahead of the MMAs)
+  static constexpr int NA = ATM ? 2 : (4 * ACOLS <= 512 ? 4 : 2);
   static constexpr int AOFF = NA * ACOLS;                                         // first A slot column
   static constexpr int NSA = ATM ? (512 - AOFF) / SLOT_COLS : 0;                  // TMEM A slots
-  static_assert(!ATM || (NSA >= 4 && NSA <= 4), "a tile reads three rows; one more slot keeps writes ahead");
+  static_assert(!ATM || (NSA >= 4 && NSA <= 6), "a tile reads three rows; spare slots keep writes ahead");
   static constexpr int NCOLS_RAW = ATM ? 512 : NA * ACOLS;
   static constexpr int NCOLS = NCOLS_RAW <= 32    ? 32
                                : NCOLS_RAW <= 64  ? 64
@@ -451,8 +453,8 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
   uint64_t* acc_full = stg_empty + NS;
   uint64_t* acc_empty = acc_full + C::NA;
   uint64_t* a_full = acc_empty + C::NA;  // TMEM A slots (C::ATM)
-  uint64_t* a_empty = a_full + 4;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(a_empty + 4);
+  uint64_t* a_empty = a_full + 6;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(a_empty + 6);
   float* s_bias = reinterpret_cast<float*>(s_tmem + 4);  // this CTA's cout slice
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long nunits = num_units<MODE, MT>(a, NSPLIT);
