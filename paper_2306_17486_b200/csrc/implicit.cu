@@ -32,20 +32,21 @@ constexpr int kImpThreads = 256;
 
 HS_DEV int br5(int l) { return __brev(l) >> 27; }
 
-// W_E^m = exp(-2 pi i m / E) for E in {2, 4, 8}: exact constants
+// a * W_E^m, W_E = exp(-2 pi i / E), E in {2, 4, 8}, m a compile-time constant
+// after unrolling: multiples of pi/2 are swaps / negations, odd multiples of
+// pi/4 one scaled add (no multiplications by 0 or 1 survive)
 template <int E>
-HS_DEV float2 wE(int m) {
+HS_DEV float2 mul_wE(float2 a, int m) {
   constexpr float s = 0.70710678118654752f;
-  const int q = (m * (8 / E)) & 7;  // in units of 2 pi / 8
-  switch (q) {
-    case 0: return make_float2(1.f, 0.f);
-    case 1: return make_float2(s, -s);
-    case 2: return make_float2(0.f, -1.f);
-    case 3: return make_float2(-s, -s);
-    case 4: return make_float2(-1.f, 0.f);
-    case 5: return make_float2(-s, s);
-    case 6: return make_float2(0.f, 1.f);
-    default: return make_float2(s, s);
+  switch ((m * (8 / E)) & 7) {  // in units of 2 pi / 8
+    case 0: return a;
+    case 1: return make_float2(s * (a.x + a.y), s * (a.y - a.x));    // (1 - i) / sqrt2
+    case 2: return make_float2(a.y, -a.x);                          // -i
+    case 3: return make_float2(s * (a.y - a.x), -s * (a.x + a.y));   // (-1 - i) / sqrt2
+    case 4: return make_float2(-a.x, -a.y);                         // -1
+    case 5: return make_float2(-s * (a.x + a.y), s * (a.x - a.y));   // (-1 + i) / sqrt2
+    case 6: return make_float2(-a.y, a.x);                          // i
+    default: return make_float2(s * (a.x - a.y), s * (a.x + a.y));  // (1 + i) / sqrt2
   }
 }
 
@@ -66,17 +67,21 @@ HS_DEV void fft_fwd(float2 (&a)[E], int lane, const float2* tw) {
   for (int k1 = 0; k1 < E; ++k1) {
     float2 s = a[0];
 #pragma unroll
-    for (int j = 1; j < NZ; ++j) s = cadd(s, cmul(a[j], wE<E>(j * k1)));
+    for (int j = 1; j < NZ; ++j) s = cadd(s, mul_wE<E>(a[j], j * k1));
     b[k1] = k1 == 0 ? s : cmul(s, tw[lane * k1]);
   }
+  // radix-2 DIF across lanes.  top lane: b + v; bottom lane: (v - b) w.  Written
+  // branch-free as (v + sg b) * w' with sg = +-1 and w' = 1 on the top lane.
 #pragma unroll
   for (int half = 16; half >= 1; half >>= 1) {
     const bool top = (lane & half) == 0;
-    const float2 w = tw[(lane & (half - 1)) * (N / (2 * half))];
+    const float sg = top ? 1.f : -1.f;
+    const float2 w = top ? make_float2(1.f, 0.f) : tw[(lane & (half - 1)) * (N / (2 * half))];
 #pragma unroll
     for (int k1 = 0; k1 < E; ++k1) {
       const float2 v = shfl_xor2(b[k1], half);
-      b[k1] = top ? cadd(b[k1], v) : cmul(csub(v, b[k1]), w);
+      const float2 t = make_float2(fmaf(sg, b[k1].x, v.x), fmaf(sg, b[k1].y, v.y));
+      b[k1] = cmul(t, w);
     }
   }
 #pragma unroll
@@ -87,14 +92,19 @@ HS_DEV void fft_fwd(float2 (&a)[E], int lane, const float2* tw) {
 template <int E, int NOUT>
 HS_DEV void fft_inv(float2 (&a)[E], int lane, const float2* tw) {
   constexpr int N = 32 * E;
+  // radix-2 DIT across lanes, the transpose of the DIF above: with s the top
+  // lane's value and d the bottom's, top <- s + d conj(w), bottom <- s - d conj(w)
 #pragma unroll
   for (int half = 1; half <= 16; half <<= 1) {
     const bool top = (lane & half) == 0;
+    const float sg = top ? 1.f : -1.f;
     const float2 w = tw[(lane & (half - 1)) * (N / (2 * half))];
 #pragma unroll
     for (int k1 = 0; k1 < E; ++k1) {
       const float2 v = shfl_xor2(a[k1], half);
-      a[k1] = top ? cadd(a[k1], cmulc(v, w)) : csub(v, cmulc(a[k1], w));
+      const float2 s = top ? a[k1] : v, d = top ? v : a[k1];
+      const float2 dw = cmulc(d, w);
+      a[k1] = make_float2(fmaf(sg, dw.x, s.x), fmaf(sg, dw.y, s.y));
     }
   }
 #pragma unroll
@@ -104,7 +114,7 @@ HS_DEV void fft_inv(float2 (&a)[E], int lane, const float2* tw) {
   for (int j = 0; j < NOUT; ++j) {
     float2 s = a[0];
 #pragma unroll
-    for (int k1 = 1; k1 < E; ++k1) s = cadd(s, cmulc(a[k1], wE<E>(j * k1)));
+    for (int k1 = 1; k1 < E; ++k1) s = cadd(s, mul_wE<E>(a[k1], (E - (j * k1) % E) % E));  // conj twiddle
     x[j] = s;
   }
 #pragma unroll

@@ -18,7 +18,7 @@ __device__ __forceinline__ uint64_t desc(uint32_t saddr, uint32_t lbo, uint32_t 
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
 }
 
-template <int M, int N, bool ATMEM, int NMMA, int ND, int NWI = 1, bool CONSTP = false>
+template <int M, int N, bool ATMEM, int NMMA, int ND, int NWI = 1, bool CONSTP = false, int AOFS = 0>
 __global__ void k_bench(long long* out) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint32_t s_tmem;
@@ -39,7 +39,7 @@ __global__ void k_bench(long long* out) {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s_tmem;
   if (warp < NWI) {  // converged issuing warps; one elected lane issues, 8 MMAs per asm block
-    const uint32_t da = (uint32_t)(desc(smem_u32(smem), 128 * 16, 128) & 0xffffffffu);
+    const uint32_t da = (uint32_t)(desc(smem_u32(smem) + AOFS, 128 * 16 + AOFS, 128) & 0xffffffffu);
     const uint32_t db = (uint32_t)(desc(smem_u32(smem + 32768), N * 16, 128) & 0xffffffffu);
     const uint32_t hi = (uint32_t)(desc(0, 0, 128) >> 32);
     const uint32_t id = idesc_bf16(M, N);
@@ -91,17 +91,17 @@ __global__ void k_bench(long long* out) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-template <int M, int N, bool ATMEM, int ND = 1, int NWI = 1, bool CONSTP = false>
+template <int M, int N, bool ATMEM, int ND = 1, int NWI = 1, bool CONSTP = false, int AOFS = 0>
 void run(long long* d) {
   constexpr int NMMA = 4096;
-  auto k = k_bench<M, N, ATMEM, NMMA, ND, NWI, CONSTP>;
+  auto k = k_bench<M, N, ATMEM, NMMA, ND, NWI, CONSTP, AOFS>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   k<<<1, 128, 64 * 1024>>>(d);
   k<<<1, 128, 64 * 1024>>>(d);
   long long h = 0;
   cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
   cudaError_t e = cudaDeviceSynchronize();
-  printf("M=%3d N=%3d A=%s acc=%d warps=%d: %6.1f cycles per MMA per warp (%s)\n", M, N, ATMEM ? "tmem" : "smem", ND, NWI, (double)h / NMMA,
+  printf("M=%3d N=%3d A=%s acc=%d warps=%d aofs=%d: %6.1f cycles per MMA per warp (%s)\n", M, N, ATMEM ? "tmem" : "smem", ND, NWI, AOFS, (double)h / NMMA,
          cudaGetErrorString(e));
 }
 
@@ -187,20 +187,111 @@ void run_cp(long long* d) {
          (double)h[0] / NCP, 4096.0 * NCP / h[0], (double)h[1] / (NCP / 4), 4.0 * 4096 * (NCP / 4) / h[1]);
 }
 
+
+constexpr uint32_t kDescHi = ((128u >> 4) & 0x3FFFu) | (1u << 14);
+template <uint32_t I0, uint32_t I1, uint32_t I2, uint32_t PX0, uint32_t PX1, uint32_t PX2, uint32_t WT, uint32_t PS>
+__device__ __forceinline__ void mma_row9(uint32_t d, uint32_t xbase, uint32_t wbase, uint32_t accumulate) {
+#define HS_MMA_PARTS(PX, P0)                                             \
+  "add.u32 al, %1, " PX ";\n\tmov.b64 da, {al, hi};\n\t"              \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, i0, " P0 ";\n\t" \
+  "add.u32 al, al, %12;\n\tmov.b64 da, {al, hi};\n\t"                 \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, i1, t;\n\t"      \
+  "add.u32 al, al, %12;\n\tmov.b64 da, {al, hi};\n\t"                 \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, i2, t;\n\t"
+  asm volatile(
+      "{\n\t.reg .pred p, t, e;\n\t.reg .b64 da, db;\n\t.reg .b32 hi, i0, i1, i2, al, bl;\n\t"
+      "mov.b32 hi, %4;\n\tmov.b32 i0, %5;\n\tmov.b32 i1, %6;\n\tmov.b32 i2, %7;\n\t"
+      "setp.ne.b32 p, %3, 0;\n\tsetp.eq.b32 t, %3, %3;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "mov.b64 db, {%2, hi};\n\t" HS_MMA_PARTS("%8", "p")
+      "add.u32 bl, %2, %11;\n\tmov.b64 db, {bl, hi};\n\t" HS_MMA_PARTS("%9", "t")
+      "add.u32 bl, %2, %13;\n\tmov.b64 db, {bl, hi};\n\t" HS_MMA_PARTS("%10", "t") "}\n" ::"r"(d),
+      "r"(xbase), "r"(wbase), "r"(accumulate), "n"(kDescHi), "n"(I0), "n"(I1), "n"(I2), "n"(PX0), "n"(PX1),
+      "n"(PX2), "n"(WT), "n"(PS), "n"(2 * WT));
+#undef HS_MMA_PARTS
+}
+
+// the conv kernel's issue pattern: filter-row asm blocks of nine MMAs (N = 3cs, 2cs, cs)
+template <int CS, int COMMIT_EVERY>
+__global__ void k_row9(long long* out, int reps) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint32_t s_tmem;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bar2[4];
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    for (int i = 0; i < 4; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar2[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s_tmem;
+  if (warp == 0) {
+    constexpr uint32_t I0 = idesc_bf16(128, 3 * CS), I1 = idesc_bf16(128, 2 * CS), I2 = idesc_bf16(128, CS);
+    const uint32_t xb = (uint32_t)(desc(smem_u32(smem), 400 * 16, 128) & 0xffffffffu);
+    const uint32_t wb = (uint32_t)(desc(smem_u32(smem + 65536), 3 * CS * 16, 128) & 0xffffffffu);
+    long long t0 = clock64();
+#pragma unroll 1
+    for (int i = 0; i < reps; ++i) {
+      mma_row9<I0, I1, I2, 0, 1, 2, 2 * 3 * CS, 1200>(tmem + (i / COMMIT_EVERY % 4) * 96, xb + (i & 3) * 130, wb, 1);
+      if (COMMIT_EVERY && i % COMMIT_EVERY == COMMIT_EVERY - 1) {
+        asm volatile(
+            "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+                smem_u32(&bar2[(i / COMMIT_EVERY) & 3]))
+            : "memory");
+        asm volatile(
+            "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+                smem_u32(&bar2[(i / COMMIT_EVERY + 1) & 3]))
+            : "memory");
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      }
+    }
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(&bar))
+        : "memory");
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tW:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t@P1 bra D;\n\tbra W;\n\tD:\n\t}\n" ::"r"(
+            smem_u32(&bar)));
+    long long t1 = clock64();
+    if (threadIdx.x == 0) out[0] = t1 - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+template <int CS, int CE = 0>
+void run_row9(long long* d) {
+  const int reps = 1024;
+  cudaFuncSetAttribute(k_row9<CS, CE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  k_row9<CS, CE><<<1, 128, 200 * 1024>>>(d, reps);
+  k_row9<CS, CE><<<1, 128, 200 * 1024>>>(d, reps);
+  long long h = 0;
+  cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  printf("row9 asm, cs=%d (N = %d/%d/%d), 2 commits+fence every %d blocks: %.1f cycles per MMA (%s)\n", CS, 3 * CS, 2 * CS, CS, CE, (double)h / (9 * reps),
+         cudaGetErrorString(cudaDeviceSynchronize()));
+}
+
 int main() {
   long long* d;
   cudaMalloc(&d, 1024 * sizeof(long long));
-  run_cp(d);
-  run<128, 16, false, 1, 1>(d);
-  run<128, 48, false, 1, 1>(d);
-  run<128, 96, false, 1, 1>(d);
-  run<128, 16, true, 1, 1>(d);
-  run<128, 48, true, 1, 1>(d);
-  run<128, 96, true, 1, 1>(d);
-  run<128, 48, false, 1, 2>(d);
-  run<128, 48, true, 1, 2>(d);
-  run<128, 16, true, 1, 2>(d);
-  run<128, 48, true, 1, 4>(d);
-  run<128, 16, true, 1, 4>(d);
+  run_row9<16>(d);
+  run_row9<32>(d);
+  run_row9<32, 6>(d);
+  run_row9<16, 3>(d);
+  run<128, 48, false, 1, 1, false, 0>(d);
+  run<128, 48, false, 1, 1, false, 16>(d);
+  run<128, 48, false, 1, 1, false, 32>(d);
+  run<128, 96, false, 1, 1, false, 0>(d);
+  run<128, 96, false, 1, 1, false, 16>(d);
+  run<128, 96, false, 1, 1, false, 48>(d);
   return 0;
 }
