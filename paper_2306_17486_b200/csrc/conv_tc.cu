@@ -800,7 +800,8 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
               o.y += ad.y + rs.y;
               o.z += ad.z + rs.z;
               o.w += ad.w + rs.w;
-              *reinterpret_cast<float4*>(a.y + obase + n0) = o;
+              if (!(a.dbg & 64)) *reinterpret_cast<float4*>(a.y + obase + n0) = o;
+              else if (o.x == 1234.5f) a.y[0] = o.y;
             }
           }
         }
