@@ -44,11 +44,11 @@
 
 #include "common.cuh"
 #include "conv_tc.h"
+#include "prof.h"
 
 namespace hs {
 namespace {
 
-constexpr int kBand = 32; // output rows per work unit
 constexpr int kPrefetch = 8;  // rows pulled into L2 ahead of the bulk copies / epilogue loads
 constexpr int kNA = 4;    // TMEM accumulators in flight
 constexpr int kEpiWarps = 8, kCvtWarp0 = 8;  // epilogue warps 0-7, converters from warp 8
@@ -163,7 +163,8 @@ struct TcArgs {
   const float* residual;
   const void* const* active;
   int B;
-  int dbg;  // experiment switch (HS_TC_DBG): 1 skip conversion, 2 skip MMAs, 4 skip epilogue math
+  int band;  // output rows per work unit (a CTA walks a band of one column block top to bottom)
+  int dbg;   // experiment switch (HS_TC_DBG): 1 skip conversion, 2 skip MMAs, 4 skip epilogue math, 64 skip stores
 };
 
 // MODE 0: stride 1; MODE 1: stride 2; MODE 2: transposed stride 2 (out = 2 x in).
@@ -268,20 +269,20 @@ struct Unit {
 template <int MODE, int MT>
 __host__ __device__ inline long long num_units(const TcArgs& a, int nsplit) {
   const int xblocks = MODE == 2 ? a.W / MT : a.Wo / MT;
-  return (long long)nsplit * a.B * xblocks * ((a.Ho + kBand - 1) / kBand);
+  return (long long)nsplit * a.B * xblocks * ((a.Ho + a.band - 1) / a.band);
 }
 
 template <int MODE, int MT>
 HS_DEV bool unit_at(const TcArgs& a, int nsplit, long long u, Unit& U) {
   const int xblocks = MODE == 2 ? a.W / MT : a.Wo / MT;
-  const int nbands = (a.Ho + kBand - 1) / kBand;
+  const int nbands = (a.Ho + a.band - 1) / a.band;
   U.split = (int)(u % nsplit);  // slices of one band run side by side: the input rows are reused from L2
   u /= nsplit;
   U.xb = (int)(u % xblocks);
   const int band = (int)((u / xblocks) % nbands);
   U.b = (int)(u / ((long long)xblocks * nbands));
-  U.oy0 = band * kBand;
-  U.oy1 = min(a.Ho, U.oy0 + kBand);
+  U.oy0 = band * a.band;
+  U.oy1 = min(a.Ho, U.oy0 + a.band);
   int lo, hi;
   tile_rows<MODE>(U.oy0, lo, hi);
   U.glo = lo;
@@ -837,10 +838,18 @@ void launch_tc(const TcArgs& a, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const long long nunits = num_units<MODE, MT>(a, C::NSPLIT);
   long long grid = (sms / C::NSPLIT) * C::NSPLIT;  // a multiple of NSPLIT: fixed slice per CTA
+  // Band height: tall bands re-read fewer halo rows, but units are handed out
+  // round-robin, so with few units per CTA the last wave idles.  Halve the band
+  // (down to 8 rows) until the RHS still iterating give every CTA >= 6 units.
+  TcArgs b = a;
+  const double act = prof::active_hint(a.B);
+  const int xblocks = MODE == 2 ? a.W / MT : a.Wo / MT;
+  b.band = 32;
+  while (b.band > 8 && C::NSPLIT * act * xblocks * ((a.Ho + b.band - 1) / b.band) < 6.0 * grid) b.band /= 2;
+  const long long nunits = num_units<MODE, MT>(b, C::NSPLIT);
   if (nunits < grid) grid = nunits;
-  k_conv_tc<CIN, COUT, MODE, MT, CS><<<(unsigned)grid, C::NT, C::TOTAL, st>>>(a);
+  k_conv_tc<CIN, COUT, MODE, MT, CS><<<(unsigned)grid, C::NT, C::TOTAL, st>>>(b);
 }
 
 // (cin, cout, mode) -> cout slice per CTA, or 0 if not on the tensor-core path
@@ -874,7 +883,7 @@ bool conv_tc_launch(const float* x, int H, int W, int cin, float* y, int Ho, int
                     const void* const* active, int B, cudaStream_t st) {
   static const int dbg = getenv("HS_TC_DBG") ? atoi(getenv("HS_TC_DBG")) : 0;
   TcArgs a{x, H, W, y, Ho, Wo, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual,
-           active, B, dbg};
+           active, B, 32, dbg};
   const int mode = transposed ? 2 : (stride == 2 ? 1 : 0);
   const bool m128 = ((mode == 2 ? W : Wo) % 128) == 0 && !(dbg & 32);
 #define HS_TC(CI, CO, MD, CSL)                                           \
