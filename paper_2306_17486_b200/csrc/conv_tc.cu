@@ -164,7 +164,8 @@ struct TcArgs {
   const void* const* active;
   int B;
   int band;  // output rows per work unit (a CTA walks a band of one column block top to bottom)
-  int dbg;   // experiment switch (HS_TC_DBG): 1 skip conversion, 2 skip MMAs, 4 skip epilogue math, 64 skip stores
+  int dbg;   // experiment switch (HS_TC_DBG): 1 skip conversion, 2 skip MMAs, 4 skip epilogue math, 64 skip
+             // stores, 128 skip input loads, 256 skip addend loads
 };
 
 // MODE 0: stride 1; MODE 1: stride 2; MODE 2: transposed stride 2 (out = 2 x in).
@@ -547,7 +548,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
           const long long use = seq / NR;
           if (use > 0) mbar_wait(smem_u32(&raw_empty[s]), (uint32_t)((use - 1) & 1));
           const uint32_t bar = smem_u32(&raw_full[s]);
-          if (g >= 0 && g < a.H && chi > clo) {
+          if (g >= 0 && g < a.H && chi > clo && !(a.dbg & 128)) {
             const uint32_t bytes = (uint32_t)(chi - clo) * CIN * 4;
             mbar_arrive_tx(bar, bytes);
             bulk_g2s(smem_u32(raw + (size_t)s * C::RAW_BYTES + (size_t)(clo - x0) * CIN * 4),
@@ -739,7 +740,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
 #pragma unroll
           for (int q = 0; q < EH / 4; ++q) {
             pa[k][q] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (add && lane_ok) pa[k][q] = __ldg(reinterpret_cast<const float4*>(add + pix * COUT + n_base) + q);
+            if (add && lane_ok && !(a.dbg & 256)) pa[k][q] = __ldg(reinterpret_cast<const float4*>(add + pix * COUT + n_base) + q);
             float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
             if (a.residual && lane_ok) r = __ldg(reinterpret_cast<const float4*>(a.residual + obase) + q);
             if constexpr (SPLIT) {
