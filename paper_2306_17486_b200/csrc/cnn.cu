@@ -61,6 +61,25 @@ struct ConvArgs {
   int addend_per_model;  // 1: addend indexed by model_of[b] (encodings), 0: by b (skips)
   const float* residual;  // NHWC like y
   const void* const* active;
+  // thin kernels only: the stem may read the complex Krylov vector directly and
+  // the head may write the complex preconditioner estimate directly
+  // (gather / scatter fused away)
+  VecIn cx;  // complex input (cin == 2) when cx_ld > 0: row r, column c at r * cx_ld + c, times scale[b]
+  int cx_ld;
+  float2* cy;  // complex output (cout == 2): value at (r, c) -> cy[b * cy_n + r * cy_ld + c]
+  long long cy_n;
+  int cy_ld, cy_h, cy_w;  // the output covers (cy_h, cy_w); outside (Ho, Wo) it is zero
+  float cy_scale;
+};
+
+// optional complex I/O for the thin stem / head (see ConvArgs)
+struct ThinIO {
+  VecIn in;
+  int in_ld;
+  float2* out;
+  long long out_n;
+  int out_ld, out_h, out_w;
+  float out_scale;
 };
 
 template <int COUT>
@@ -337,10 +356,15 @@ __global__ void __launch_bounds__(kThinThreads) k_conv_thin(ConvArgs a) {
   if (a.active && a.active[b] == nullptr) return;
   const int q = threadIdx.x % L;
   const int x = blockIdx.x * (kThinThreads / L) + threadIdx.x / L;
-  const bool x_ok = x < a.Wo;  // whole quads agree: shuffles stay within live lanes
+  const bool cout_c = COUT == 2 && a.cy != nullptr;     // complex output (head -> u0)
+  const int Hl = cout_c ? a.cy_h : a.Ho, Wl = cout_c ? a.cy_w : a.Wo;  // extents walked
+  const bool x_ok = x < Wl;  // whole lane groups agree: shuffles stay within live lanes
   const int ci0 = kSplitIn ? GI * q : 0, co0 = kSplitIn ? 0 : GO * q;
-  const int oy0 = blockIdx.y * kThinRows, oy1 = min(a.Ho, oy0 + kThinRows);
-  const float* xb = a.x + (long long)b * a.H * a.W * CIN;
+  const int oy0 = blockIdx.y * kThinRows, oy1 = min(Hl, oy0 + kThinRows);
+  const float* xb = a.x ? a.x + (long long)b * a.H * a.W * CIN : nullptr;
+  const bool cin_c = CIN == 2 && a.cx_ld > 0;  // complex input (Krylov vector -> stem)
+  const float2* xc = cin_c ? (a.cx.tab ? a.cx.tab[b] : a.cx.base + (long long)b * a.cx.bstride) : nullptr;
+  const float xcs = cin_c && a.cx.scale ? a.cx.scale[b] : 1.f;
   const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[b] : 0) : b) * a.addend_bstride
                               : nullptr;
   // acc[0]: output row iy - 1 (its ky = 2 tap), acc[1]: row iy (ky = 1), acc[2]: row iy + 1 (ky = 0);
@@ -355,9 +379,15 @@ __global__ void __launch_bounds__(kThinThreads) k_conv_thin(ConvArgs a) {
 #pragma unroll
     for (int kx = 0; kx < 3; ++kx) {
       const int ix = x + kx - 1;
-      if (x_ok && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W)
-        load_vec<GI>(xb + ((long long)iy * a.W + ix) * CIN + ci0, xv[kx]);
-      else
+      if (x_ok && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W) {
+        if (cin_c) {
+          const float2 v = xc[(long long)iy * a.cx_ld + ix];
+          xv[kx][0] = v.x * xcs;
+          xv[kx][GI > 1 ? 1 : 0] = v.y * xcs;
+        } else {
+          load_vec<GI>(xb + ((long long)iy * a.W + ix) * CIN + ci0, xv[kx]);
+        }
+      } else
 #pragma unroll
         for (int c = 0; c < GI; ++c) xv[kx][c] = 0.f;
     }
@@ -425,7 +455,13 @@ __global__ void __launch_bounds__(kThinThreads) k_conv_thin(ConvArgs a) {
           if (a.softplus) t = softplus_fast(t);
           v[n] = t + sd[n];
         }
-        store_vec<GO>(a.y + o, v);
+        if (cout_c) {
+          const bool valid = oy < a.Ho && x < a.Wo;
+          a.cy[(long long)b * a.cy_n + (long long)oy * a.cy_ld + x] =
+              valid ? make_float2(a.cy_scale * v[0], a.cy_scale * v[GO > 1 ? 1 : 0]) : make_float2(0.f, 0.f);
+        } else {
+          store_vec<GO>(a.y + o, v);
+        }
       }
     }
 #pragma unroll
@@ -440,15 +476,30 @@ __global__ void __launch_bounds__(kThinThreads) k_conv_thin(ConvArgs a) {
 template <int CIN, int COUT>
 void launch_thin(const ConvArgs& a, int B, cudaStream_t st) {
   constexpr int pix = kThinThreads / thin_lanes<CIN, COUT>();
-  const dim3 grid((unsigned)((a.Wo + pix - 1) / pix), (unsigned)((a.Ho + kThinRows - 1) / kThinRows),
+  const int Hl = a.cy ? a.cy_h : a.Ho, Wl = a.cy ? a.cy_w : a.Wo;
+  const dim3 grid((unsigned)((Wl + pix - 1) / pix), (unsigned)((Hl + kThinRows - 1) / kThinRows),
                   (unsigned)B);
   k_conv_thin<CIN, COUT><<<grid, kThinThreads, 0, st>>>(a);
 }
 
 int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* y, const float* addend,
                 long long addend_bstride, const int* model_of, const float* residual, const void* const* active,
-                cudaStream_t st, bool model_of_addend = false) {
+                cudaStream_t st, bool model_of_addend = false, const ThinIO* io = nullptr) {
   ConvArgs a{};
+  if (io) {  // complex Krylov-vector input (stem) and / or complex u0 output (head): thin kernels only
+    if (io->in_ld > 0 && c.cin == 2) {
+      a.cx = io->in;
+      a.cx_ld = io->in_ld;
+    }
+    if (io->out && c.cout == 2) {
+      a.cy = io->out;
+      a.cy_n = io->out_n;
+      a.cy_ld = io->out_ld;
+      a.cy_h = io->out_h;
+      a.cy_w = io->out_w;
+      a.cy_scale = io->out_scale;
+    }
+  }
   a.x = x;
   a.H = H;
   a.W = W;
@@ -488,6 +539,8 @@ int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* 
   Scope2 scope{prof::start(prof::CONV, st), l0 ? prof::start(prof::CONV_L0, st) : -1, st, flops, l0_bytes};
   a.residual = residual;
   a.active = active;
+  if ((a.cx_ld > 0 || a.cy) && !(!c.transposed && c.stride == 1 && (c.cin == 2 || c.cout == 2)))
+    return HS_ECONFIG;  // complex I/O is fused into the thin stem / head only
   if (!c.transposed && c.stride == 1) {
     if (c.cin == 2 && c.cout == 16) return launch_thin<2, 16>(a, B, st), HS_OK;
     if (c.cin == 2 && c.cout == 8) return launch_thin<2, 8>(a, B, st), HS_OK;
@@ -523,37 +576,6 @@ int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* 
 }
 
 // ------------------------------------------------------- input / output glue
-
-// r (complex64, nx x ny, scaled) cropped to (ix, iy) -> NHWC 2 channels (Re, Im)
-__global__ void k_gather_r(VecIn vin, const void* const* active, float* out, int nx, int ny, int ix, int iy) {
-  const int b = blockIdx.y;
-  if (active && active[b] == nullptr) return;
-  const float2* r = vin.tab ? vin.tab[b] : vin.base + (long long)b * vin.bstride;
-  const float s = vin.scale ? vin.scale[b] : 1.f;
-  const long long n = (long long)ix * iy;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(p / iy), j = (int)(p - (long long)i * iy);
-    float2 v = r[(long long)i * ny + j];
-    reinterpret_cast<float2*>(out)[(long long)b * n + p] = make_float2(v.x * s, v.y * s);
-  }
-}
-
-// NHWC 2-channel head output -> u0 = scale (o0 + i o1), zero outside (ix, iy)
-__global__ void k_scatter_u0(const float* head, const void* const* active, float2* u0, int nx, int ny, int ix, int iy,
-                             float scale) {
-  const int b = blockIdx.y;
-  if (active && active[b] == nullptr) return;
-  const long long n = (long long)nx * ny;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(p / ny), j = (int)(p - (long long)i * ny);
-    float2 v = make_float2(0.f, 0.f);
-    if (i < ix && j < iy) {
-      float2 o = reinterpret_cast<const float2*>(head)[(long long)b * ix * iy + (long long)i * iy + j];
-      v = make_float2(scale * o.x, scale * o.y);
-    }
-    u0[b * n + p] = v;
-  }
-}
 
 // NHWC real (C = 2 cc) at (h, w) -> complex NCHW (cc, 2h, 2w) zero-padded at the high end
 __global__ void k_pack_pad(const float* x, const void* const* active, cufftComplex* z, int h, int w, int cc) {
@@ -762,6 +784,7 @@ static int implicit_apply_dev(const hs_net_t* net, const float* x_nhwc, float* y
   const int hc = net->hc, wc = net->wc, cc = net->cc;
   if (net->spec_perm) {
     const long long pix = (long long)hc * wc;
+    prof::count(1);
     return implicit_fused(x_nhwc, pix * cc, 1, cc, y_nhwc, pix * cc, 1, cc, net->spec_perm, active, B, cc, hc, wc, st);
   }
   cufftHandle plan;
@@ -781,6 +804,7 @@ static int implicit_apply_dev(const hs_net_t* net, const float* x_nhwc, float* y
   cufftSetStream(plan, st);
   const long long per_b = (long long)cc * 4 * hc * wc;
   dim3 g(grid1(per_b), B);
+  prof::count(3);  // pack, spectral multiply, crop (cuFFT kernels not counted)
   k_pack_pad<<<g, 256, 0, st>>>(x_nhwc, active, z, hc, wc, cc);
   if (cufftExecC2C(plan, z, z, CUFFT_FORWARD) != CUFFT_SUCCESS) return HS_ECUDA;
   k_spec_mul<<<g, 256, 0, st>>>(z, active, net->spec, per_b);
@@ -791,7 +815,8 @@ static int implicit_apply_dev(const hs_net_t* net, const float* x_nhwc, float* y
 
 // The solver U-Net (ARCH.md) on NHWC buffers; input 2-channel `in`, output
 // 2-channel `head`.  RHS with active[b] == null are skipped.
-static int solver_forward(const hs_net_t* net, const float* in, float* head, char* ws, const FwdLayout& L,
+static int solver_forward(const hs_net_t* net, const float* in, float* head, const ThinIO* io, char* ws,
+                          const FwdLayout& L,
                           const int* model_of, const void* const* active, int B, cudaStream_t st) {
   const hs_net_desc_t& d = net->d;
   float* X[8];
@@ -806,7 +831,7 @@ static int solver_forward(const hs_net_t* net, const float* in, float* head, cha
   int rc;
   // level 0: stem (+ encoding 0), residual block -> skip 0
   if ((rc = launch_conv(d.sol_stem, in, B, d.ix, d.iy, X[0], net->enc[0], lvl_bstride(0), model_of, nullptr, active,
-                        st, true)))
+                        st, true, io)))
     return rc;
   if ((rc = launch_conv(d.sol_res_a[0], X[0], B, d.ix, d.iy, Tm[0], nullptr, 0, nullptr, nullptr, active, st)))
     return rc;
@@ -842,24 +867,22 @@ static int solver_forward(const hs_net_t* net, const float* in, float* head, cha
                           nullptr, Tm[l - 1], active, st)))
       return rc;
   }
-  return launch_conv(d.sol_head, X[0], B, d.ix, d.iy, head, nullptr, 0, nullptr, nullptr, active, st);
+  return launch_conv(d.sol_head, X[0], B, d.ix, d.iy, head, nullptr, 0, nullptr, nullptr, active, st, false, io);
 }
 
-void cnn_preconditioner_estimate(const hs_net_t* net, VecIn vin, const float2* const* active, float2* u0,
-                                 const int* model_of, int B, void* ws, cudaStream_t st) {
+int cnn_preconditioner_estimate(const hs_net_t* net, VecIn vin, const float2* const* active, float2* u0,
+                                const int* model_of, int B, void* ws, cudaStream_t st) {
   const hs_net_desc_t& d = net->d;
   FwdLayout L = fwd_layout(d, B);
   char* w = static_cast<char*>(ws);
-  float* in = reinterpret_cast<float*>(w + L.in);
-  float* head = reinterpret_cast<float*>(w + L.head);
   const void* const* act = reinterpret_cast<const void* const*>(active);
   const int slot = prof::start(prof::CNN, st);
-  k_gather_r<<<dim3(grid1((long long)d.ix * d.iy), B), 256, 0, st>>>(vin, act, in, d.nx, d.ny, d.ix, d.iy);
-  solver_forward(net, in, head, w, L, model_of, act, B, st);
-  k_scatter_u0<<<dim3(grid1((long long)d.nx * d.ny), B), 256, 0, st>>>(head, act, u0, d.nx, d.ny, d.ix, d.iy,
-                                                                       d.out_scale);
-  prof::count(5);  // gather, scatter, pack, spectral multiply, crop (cuFFT kernels not counted)
+  // the stem reads r[:ix, :iy] straight from the Krylov vector and the head writes
+  // u0 = (h^2/64) net(.) zero-padded to (nx, ny) (ARCH.md), so no gather / scatter pass
+  ThinIO io{vin, d.ny, u0, (long long)d.nx * d.ny, d.ny, d.nx, d.ny, d.out_scale};
+  const int rc = solver_forward(net, nullptr, nullptr, &io, w, L, model_of, act, B, st);
   prof::stop(slot, st, 0.0);
+  return rc;
 }
 
 }  // namespace hs
@@ -969,8 +992,9 @@ HS_API int hs_net_forward(const hs_net_t* net, const void* r, void* u0, const in
   if (ws_bytes < hs::cnn_workspace_bytes(net, B)) return cfail(HS_ECONFIG, "workspace too small");
   const hs_net_desc_t& d = net->d;
   hs::VecIn vin{nullptr, static_cast<const float2*>(r), (long long)d.nx * d.ny, nullptr};
-  hs::cnn_preconditioner_estimate(net, vin, nullptr, static_cast<float2*>(u0), model_of, B, ws,
-                                  (cudaStream_t)stream);
+  const int rc = hs::cnn_preconditioner_estimate(net, vin, nullptr, static_cast<float2*>(u0), model_of, B, ws,
+                                                 (cudaStream_t)stream);
+  if (rc) return cfail(rc, "network forward");
   return ccheck("hs_net_forward");
 }
 

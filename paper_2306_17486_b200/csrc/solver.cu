@@ -267,7 +267,9 @@ HS_API int hs_fgmres_solve(const hs_hierarchy_t* h, const hs_net_t* net, const h
       hs::VecOut zout{s.zout, nullptr, 0};
       hs::VecIn uz{nullptr, nullptr, 0, nullptr};
       if (net) {
-        hs::cnn_preconditioner_estimate(net, vin, s.vin, u0, a->model_of, a->B, base + L.netws, st);
+        if ((rc = hs::cnn_preconditioner_estimate(net, vin, s.vin, u0, a->model_of, a->B, base + L.netws, st)) !=
+            HS_OK)
+          return fail(rc, "network forward");
         uz = hs::VecIn{nullptr, u0, N, nullptr};
       }
       hs::vcycle(H, vin, uz, zout, s.vin, a->model_of, a->B, vws, vstatus, st);
