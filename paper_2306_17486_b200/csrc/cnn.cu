@@ -720,10 +720,10 @@ size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 
 // per-level activation buffers of the forward pass
 struct FwdLayout {
-  size_t in, head, lvl_x[8], lvl_t[8], lvl_s[8], fftz, total;
+  size_t lvl_x[8], lvl_t[8], lvl_s[8], fftz, total;
 };
 
-FwdLayout fwd_layout(const hs_net_desc_t& d, int B) {
+FwdLayout fwd_layout(const hs_net_desc_t& d, int B, bool fused_implicit) {
   FwdLayout L{};
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -731,8 +731,6 @@ FwdLayout fwd_layout(const hs_net_desc_t& d, int B) {
     off += align_up(bytes);
     return o;
   };
-  L.in = take((size_t)B * d.ix * d.iy * 2 * sizeof(float));
-  L.head = take((size_t)B * d.ix * d.iy * 2 * sizeof(float));
   for (int l = 0; l < d.levels; ++l) {
     size_t n = (size_t)B * (d.ix >> l) * (d.iy >> l) * d.channels[l] * sizeof(float);
     L.lvl_x[l] = take(n);
@@ -741,14 +739,17 @@ FwdLayout fwd_layout(const hs_net_desc_t& d, int B) {
   }
   const int L1 = d.levels - 1;
   const int hc = d.ix >> L1, wc = d.iy >> L1, cc = d.channels[L1] / 2;
-  L.fftz = take((size_t)B * cc * 4 * hc * wc * sizeof(cufftComplex));
+  // cuFFT fallback planes only where the fused implicit kernel does not apply
+  L.fftz = take(fused_implicit ? 0 : (size_t)B * cc * 4 * hc * wc * sizeof(cufftComplex));
   L.total = off;
   return L;
 }
 
 }  // namespace
 
-size_t cnn_workspace_bytes(const hs_net_t* net, int B) { return fwd_layout(net->d, B).total; }
+size_t cnn_workspace_bytes(const hs_net_t* net, int B) {
+  return fwd_layout(net->d, B, net->spec_perm != nullptr).total;
+}
 
 static int green_spectrum_c128(const float2* kern, int C, int h, int w, cufftDoubleComplex* out, cudaStream_t st) {
   const int gh = 2 * h, gw = 2 * w, bh = 3 * gh, bw = 3 * gw;
@@ -873,7 +874,7 @@ static int solver_forward(const hs_net_t* net, const float* in, float* head, con
 int cnn_preconditioner_estimate(const hs_net_t* net, VecIn vin, const float2* const* active, float2* u0,
                                 const int* model_of, int B, void* ws, cudaStream_t st) {
   const hs_net_desc_t& d = net->d;
-  FwdLayout L = fwd_layout(d, B);
+  FwdLayout L = fwd_layout(d, B, net->spec_perm != nullptr);
   char* w = static_cast<char*>(ws);
   const void* const* act = reinterpret_cast<const void* const*>(active);
   const int slot = prof::start(prof::CNN, st);
