@@ -94,9 +94,9 @@ HS_DEV void mbar_init(uint32_t mbar, uint32_t count) {
 HS_DEV void mbar_wait(uint32_t mbar, uint32_t phase) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}\n" ::"r"(mbar),
-      "r"(phase));
+      "r"(phase), "n"(20000));  // suspend-time hint (ns): waiting warps sleep instead of spinning
 }
 
 HS_DEV void mbar_arrive(uint32_t mbar) {
