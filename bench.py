@@ -172,6 +172,149 @@ def workload_config(args):
             "parallelism": f"rhs-sharded dp (independent instance per rank)"}
 
 
+DG_METRIC = "training pairs (r, e) generated/sec (257x257, k ~ U{2..20} V-cycle FGMRES iterations)"
+DG_UNIT = "pairs/s"
+
+
+def datagen_models(rank: int = 0):
+    """C2's four seeded slowness models with the training attenuation gamma0 = 0.05 (SPEC datagen)."""
+    from paper_2306_17486_b200 import datagen, fields, problems
+
+    cfg = problems.make_config("C2", rhs_per_model=1, seed_offset=rank)
+    return [fields.slowness_model(m.kappa_sq, gamma0=datagen.TRAINING_GAMMA0, layer_width=20) for m in cfg.models]
+
+
+def datagen_cpu(args, workers: int, per_worker: int = 1):
+    """Oracle datagen on the host cores: pairs/s (one process per core, per_worker pairs each)."""
+    from multiprocessing import get_context
+
+    t0 = time.perf_counter()
+    with get_context("fork").Pool(workers) as pool:
+        ks = pool.map(_dg_worker, [(i, per_worker) for i in range(workers)])
+    el = time.perf_counter() - t0
+    n = workers * per_worker
+    return n / el, (f"{workers} processes x {per_worker} pair(s) of the same draws (mean k "
+                    f"{np.mean(sum(ks, [])):.1f}), numpy oracle (oracle/datagen_oracle.py)")
+
+
+def _dg_worker(a):
+    from threadpoolctl import threadpool_limits
+
+    threadpool_limits(1)
+    from oracle import datagen_oracle as dg
+    from oracle import helm_oracle as ho
+
+    index, count = a
+    models = [ho.Model(m.kappa_sq, m.gamma, m.omega, m.h) for m in datagen_models()]
+    rng = np.random.default_rng(1000 + index)
+    ks = []
+    for j in range(count):
+        m = models[(index + j) % len(models)]
+        _, _, k = dg.generate_sample(m, rng)
+        ks.append(k)
+    return ks
+
+
+def run_datagen(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    cfg = {"workload": f"datagen: {args.samples} pairs per step over C2's 4 models (gamma0 0.05), 257x257, "
+                       f"x ~ CN(0,1), k ~ U{{2..20}} FGMRES(10)+V-cycle(MG3) iterations, r = A e",
+           "global_batch_per_gpu": args.samples, "parallelism": "sample-sharded dp (independent per rank)",
+           "l2": "per-step working set (x, b, e, r, Krylov bases: ~1.7 GB) far larger than L2"}
+    workers = args.cpu_workers or (os.cpu_count() or 1)
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        t0 = time.perf_counter()
+        vals = [datagen_cpu(args, workers)[0] for _ in range(args.warmup + args.steps)][args.warmup:]
+        value = float(np.mean(vals))
+        desc = datagen_cpu(args, workers)[1]
+        print(json.dumps({
+            "impl": "reference", "metric": DG_METRIC, "value": value, "unit": DG_UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * (time.perf_counter() - t0) / (args.steps + args.warmup + 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128/f64 (numpy oracle)",
+            "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": value, "unit": DG_UNIT, "cores": workers, "kind": "port", "sample": desc},
+            "e2e": {"value": value, "unit": DG_UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
+        return 0
+
+    import torch
+
+    world, rank, local = dist_setup()
+    from paper_2306_17486_b200 import _lib, datagen
+    from paper_2306_17486_b200 import dist as hdist
+
+    models = datagen_models(rank)
+    gen = datagen.PairGenerator(models)
+    shape = models[0].shape
+    rng = np.random.default_rng(2024 + rank)
+
+    def draw_batch():
+        d = [datagen._draw(rng, shape) for _ in range(args.samples)]
+        return np.stack([t[0] for t in d]), [t[1] for t in d], [i % len(models) for i in range(args.samples)]
+
+    batches = [draw_batch() for _ in range(args.warmup + args.steps)]
+    xdev = [torch.from_numpy(b[0]).cuda() for b in batches]
+    lib = _lib.load()
+    for i in range(args.warmup):
+        gen.pairs(xdev[i], batches[i][1], batches[i][2], return_device=True)
+    tags = [_lib.PROF_VCYCLE, _lib.PROF_ARNOLDI, _lib.PROF_VC_UP0]
+    lib.hs_profile_reset()
+    lib.hs_profile_enable(sum(1 << t for t in tags))
+    stream = torch.cuda.current_stream()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for i in range(args.warmup, args.warmup + args.steps):
+            gen.pairs(xdev[i], batches[i][1], batches[i][2], return_device=True)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = hdist.reduce_scalar(ev0.elapsed_time(ev1), "max")
+    launches = int(lib.hs_launch_count())
+    prof = {t: _lib.profile_query(t) for t in tags}
+    lib.hs_profile_enable(0)
+    value = world * args.samples * args.steps / (ms / 1e3)
+    # e2e: host x (pinned) in, host (r, e) out, every step
+    e2e = None
+    if not args.no_e2e:
+        xpin = [torch.from_numpy(batches[i][0]).pin_memory() for i in range(args.warmup, args.warmup + args.steps)]
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for j, i in enumerate(range(args.warmup, args.warmup + args.steps)):
+            r, e = gen.pairs(xpin[j], batches[i][1], batches[i][2])
+        el = hdist.reduce_scalar(time.perf_counter() - t0, "max")
+        e2e = {"value": world * args.samples * args.steps / el, "unit": DG_UNIT,
+               "h2d_bytes_per_step": int(xpin[0].numel() * 16), "d2h_bytes_per_step": int(r.nbytes + e.nbytes)}
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+    hbm, _, src = load_peaks()
+    u_ms, u_bytes, u_n = prof[_lib.PROF_VC_UP0]
+    ach = u_bytes / (u_ms / 1e3) / 1e9 if u_ms > 0 else 0.0
+    roof = {"kernel": "k_vc_up (finest level)", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+            "frac": ach / hbm, "peak_note": f"{src} copy bandwidth", "launches": u_n, "ms_total": u_ms, "traffic": None}
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        v, desc = datagen_cpu(args, workers)
+        cpu = {"value": v, "unit": DG_UNIT, "cores": workers, "kind": "port", "sample": desc}
+    print(json.dumps({
+        "metric": DG_METRIC, "value": value, "unit": DG_UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c64 basis/V-cycle, fp64 operator+reductions, c128 iterate",
+        "data": "synthetic (seeded)", "config": cfg, "mean_k": float(np.mean(sum((b[1] for b in batches), []))),
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary()}),
+        flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -185,7 +328,12 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workload", default="solve", choices=["solve", "datagen"],
+                    help="solve: the BASELINE metric (default); datagen: SURVEY 8f row 1, training pairs")
+    ap.add_argument("--samples", type=int, default=256, help="datagen: samples per step")
     args = ap.parse_args()
+    if args.workload == "datagen":
+        return run_datagen(args)
     if args.impl == "reference":
         return run_reference(args)
 

@@ -116,6 +116,8 @@ typedef struct {
   int* iterations;       /* (B,) out */
   int* converged;        /* (B,) out */
   int* status;           /* (B,) out: HS_OK / HS_EBREAKDOWN / HS_ENONFINITE */
+  const int* iter_cap;   /* (B,) device, per-RHS iteration cap (<= max_iter), or NULL: max_iter for every RHS
+                            (training-pair generation runs k ~ U{2..20} iterations per sample in one solve) */
 } hs_solve_args_t;
 
 /* version of the ABI (bumped on incompatible changes) */

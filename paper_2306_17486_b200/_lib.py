@@ -61,6 +61,7 @@ class HsSolveArgs(ctypes.Structure):
         ("iterations", ctypes.c_void_p),
         ("converged", ctypes.c_void_p),
         ("status", ctypes.c_void_p),
+        ("iter_cap", ctypes.c_void_p),
     ]
 
 

@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(NT) k_xupdate(SolveDims d, SolveBuffers s) {
 }
 
 HS_DEV void start_window(RhsState& S, const SolveDims& d, double beta) {
-  S.m = min(min(d.restart, d.max_iter), d.max_iter - S.iter);  // krylov.py:79,83
+  S.m = min(min(d.restart, S.cap), S.cap - S.iter);  // krylov.py:79,83
   S.j = 0;
   S.vscale[0] = 1.0 / beta;
   S.g[0] = make_double2(beta, 0.0);
@@ -315,14 +315,14 @@ __global__ void __launch_bounds__(NT) k_residual(SolveDims d, SolveBuffers s, in
     hist[S.iter] = true_rel;
     S.converged = 1;
     S.active = 0;
-  } else if (S.iter >= d.max_iter) {
+  } else if (S.iter >= S.cap) {
     S.active = 0;
   } else {
     start_window(S, d, rn);
   }
 }
 
-__global__ void k_init_state(SolveDims d, SolveBuffers s, const double* tol) {
+__global__ void k_init_state(SolveDims d, SolveBuffers s, const double* tol, const int* iter_cap) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= d.B) return;
   RhsState& S = s.st[b];
@@ -338,6 +338,7 @@ __global__ void k_init_state(SolveDims d, SolveBuffers s, const double* tol) {
   S.converged = 0;
   S.hist_len = 0;
   S.tol = tol[b];
+  S.cap = iter_cap ? min(max(iter_cap[b], 1), d.max_iter) : d.max_iter;
   S.beta0 = 0.0;
   s.counter[b] = 0;
 }
@@ -378,9 +379,9 @@ __global__ void k_count_active(SolveDims d, SolveBuffers s) {
 
 size_t krylov_partial_doubles(const SolveDims& d) { return (size_t)d.B * kChunks * d.nblk * PST; }
 
-void krylov_init(const SolveDims& d, const SolveBuffers& s, const double* tol, bool have_x0,
+void krylov_init(const SolveDims& d, const SolveBuffers& s, const double* tol, const int* iter_cap, bool have_x0,
                  cudaStream_t stream) {
-  k_init_state<<<cdiv_u(d.B, 128), 128, 0, stream>>>(d, s, tol);
+  k_init_state<<<cdiv_u(d.B, 128), 128, 0, stream>>>(d, s, tol, iter_cap);
   if (!have_x0) k_zero_x<<<592, 256, 0, stream>>>(d, s);
   k_residual<true><<<dim3(d.nblk, d.B), NT, 0, stream>>>(d, s, have_x0 ? 1 : 0);
 }

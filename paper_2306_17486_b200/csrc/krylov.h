@@ -18,7 +18,7 @@ struct RhsState {
   int conv_est;     // the Givens estimate met tol this window
   int converged;    // final flag (SolveReport.converged)
   int hist_len;     // entries written to the history
-  int pad;
+  int cap;          // this RHS's iteration cap (<= SolveDims::max_iter)
   double beta0, tol, wn, hn;
   double vscale[kMaxRestart + 1];   // v_k = vscale[k] * V_k (V stored unnormalised)
   double2 hcol[kMaxRestart + 1];    // Gram-Schmidt coefficients of this step (total)
@@ -61,7 +61,7 @@ struct SolveBuffers {
 size_t krylov_partial_doubles(const SolveDims& d);
 
 // initial residual: x <- x0 (or 0), r = b - A x, beta0, first window
-void krylov_init(const SolveDims& d, const SolveBuffers& s, const double* tol, bool have_x0,
+void krylov_init(const SolveDims& d, const SolveBuffers& s, const double* tol, const int* iter_cap, bool have_x0,
                  cudaStream_t stream);
 // pointer tables for the preconditioner of the current step
 void krylov_prep(const SolveDims& d, const SolveBuffers& s, cudaStream_t stream);

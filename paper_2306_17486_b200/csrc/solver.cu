@@ -126,7 +126,7 @@ int* pinned_flag() {
 
 }  // namespace
 
-HS_API int hs_abi_version(void) { return 1; }
+HS_API int hs_abi_version(void) { return 2; }  // 2: hs_solve_args_t.iter_cap
 HS_API const char* hs_last_error(void) { return hs::g_last_error.c_str(); }
 
 HS_API int hs_helm_apply(const void* u, void* out, const void* mass, const int* model_of, int B, int nx, int ny,
@@ -247,7 +247,7 @@ HS_API int hs_fgmres_solve(const hs_hierarchy_t* h, const hs_net_t* net, const h
 
   cudaMemsetAsync(vstatus, 0, sizeof(int), st);
   if (a->x0) cudaMemcpyAsync(a->x, a->x0, (size_t)a->B * N * sizeof(double2), cudaMemcpyDeviceToDevice, st);
-  hs::krylov_init(d, s, a->tol, a->x0 != nullptr, st);
+  hs::krylov_init(d, s, a->tol, a->iter_cap, a->x0 != nullptr, st);
   if ((rc = check_cuda("fgmres init")) != HS_OK) return rc;
 
   int* flag = pinned_flag();

@@ -43,7 +43,8 @@ class Engine:
         return self._ws
 
     def fgmres(self, b: torch.Tensor, x0: torch.Tensor | None, tol, max_iter: int, restart: int | None,
-               model_of: torch.Tensor | None = None, use_net: bool = False) -> BatchResult:
+               model_of: torch.Tensor | None = None, use_net: bool = False, iter_caps=None) -> BatchResult:
+        """One batched hs_fgmres_solve; ``iter_caps`` (B,) optionally caps each RHS below max_iter."""
         dev = require_cuda()
         b = b.to(device=dev, dtype=torch.complex128).contiguous()
         B = b.shape[0]
@@ -67,6 +68,10 @@ class Engine:
         args.hist = hist.data_ptr()
         args.hist_len, args.iterations = ints[0].data_ptr(), ints[1].data_ptr()
         args.converged, args.status = ints[2].data_ptr(), ints[3].data_ptr()
+        caps = None
+        if iter_caps is not None:
+            caps = torch.as_tensor(np.asarray(iter_caps, dtype=np.int32), device=dev)
+            args.iter_cap = caps.data_ptr()
         net_handle = self.net.handle if (use_net and self.net is not None) else None
         lib = _lib.load()
         nbytes = int(lib.hs_fgmres_workspace_bytes(ctypes.byref(self.dh.hs), net_handle, B, nx, ny,

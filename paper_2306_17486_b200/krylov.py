@@ -243,8 +243,12 @@ class BatchSolver:
         self.engine = Engine(self.dh, net_dev)
 
     def solve(self, rhs, model_of=None, tol: float = 1e-7, max_iter: int = 250, restart: int | None = 10,
-              warmup_iters: int = 3, return_device: bool = False, raise_errors: bool = True):
-        """x (B, nx, ny) complex128 and one SolveReport per RHS."""
+              warmup_iters: int = 3, return_device: bool = False, raise_errors: bool = True, iter_caps=None):
+        """x (B, nx, ny) complex128 and one SolveReport per RHS.
+
+        ``iter_caps`` (V-cycle protocol only): a per-RHS iteration cap <= max_iter, so samples that
+        need different iteration counts share one batched solve (training-pair generation).
+        """
         import torch
 
         from .device import require_cuda, to_device
@@ -262,8 +266,10 @@ class BatchSolver:
         owner = np.zeros(B, dtype=np.int32) if model_of is None else np.asarray(model_of, dtype=np.int32)
         owner_d = torch.from_numpy(owner).to(dev)
         eng = self.engine
+        if iter_caps is not None and self.net is not None:
+            raise ValueError("iter_caps applies to the V-cycle protocol only")
         if self.net is None:
-            res = eng.fgmres(bd, None, tol, max_iter, restart, owner_d)
+            res = eng.fgmres(bd, None, tol, max_iter, restart, owner_d, iter_caps=iter_caps)
             reports = [SolveReport(int(res.iterations[i]), res.histories[i], bool(res.converged[i]), 0.0)
                        for i in range(B)]
             status, x = res.status, res.x
