@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(kThinThreads) k_conv_thin(ConvArgs a) {
   constexpr int GO = kSplitIn ? COUT : COUT / L;     // output channels per lane
   static_assert(GI * L == CIN || !kSplitIn, "lane split");
   static_assert(GO * L == COUT || kSplitIn, "lane split");
-  __shared__ __align__(16) float s_w[9 * CIN * COUT];  // [tap][cin][cout]
+  __shared__ __align__(16) float s_w[9 * CIN * COUT + COUT];  // [tap][cin][cout], then the bias
   for (int e = threadIdx.x; e < 9 * CIN * COUT; e += blockDim.x) {
     const int n = e % COUT, c = (e / COUT) % CIN, t = e / (COUT * CIN);
     s_w[e] = a.w[(n * 9 + t) * CIN + c];
@@ -394,39 +394,39 @@ __global__ void __launch_bounds__(kThinThreads) k_conv_thin(ConvArgs a) {
   };
   // addend + residual of an output row, summed, fetched one row ahead as well
   const bool store_lane = x_ok && (!kSplitIn || q == 0);
+  // (a single side input is a plain load into sd: nothing waits on it until the store)
   auto load_side = [&](int oy, float(&sd)[GO]) {
 #pragma unroll
     for (int n = 0; n < GO; ++n) sd[n] = 0.f;
     if (!store_lane || oy < oy0 || oy >= oy1) return;
     const long long p = (long long)oy * a.Wo + x;
-    float t[GO];
-    if (add) {
+    const float* res = a.residual ? a.residual + (long long)b * a.Ho * a.Wo * COUT + p * COUT + co0 : nullptr;
+    if (add && !res) {
+      load_vec<GO>(add + p * COUT + co0, sd);
+    } else if (res && !add) {
+      load_vec<GO>(res, sd);
+    } else if (add && res) {
+      float t[GO], u[GO];
       load_vec<GO>(add + p * COUT + co0, t);
+      load_vec<GO>(res, u);
 #pragma unroll
-      for (int n = 0; n < GO; ++n) sd[n] += t[n];
-    }
-    if (a.residual) {
-      load_vec<GO>(a.residual + (long long)b * a.Ho * a.Wo * COUT + p * COUT + co0, t);
-#pragma unroll
-      for (int n = 0; n < GO; ++n) sd[n] += t[n];
+      for (int n = 0; n < GO; ++n) sd[n] = t[n] + u[n];
     }
   };
-  float bias[GO];
-#pragma unroll
-  for (int n = 0; n < GO; ++n) bias[n] = __ldg(a.bias + co0 + n);
-  float nx[3][GI], nsd[GO];
+  // bias from shared memory (broadcast) rather than GO more registers
+  float* s_bias = s_w + 9 * CIN * COUT;
+  for (int n = threadIdx.x; n < COUT; n += blockDim.x) s_bias[n] = a.bias[n];
+  __syncthreads();
+  float nx[3][GI];
   load_row(oy0 - 1, nx);
-  load_side(oy0, nsd);  // not needed until iy = oy0 + 1
   for (int iy = oy0 - 1; iy <= oy1; ++iy) {
     float xv[3][GI], sd[GO];
 #pragma unroll
     for (int kx = 0; kx < 3; ++kx)
 #pragma unroll
       for (int c = 0; c < GI; ++c) xv[kx][c] = nx[kx][c];
-#pragma unroll
-    for (int n = 0; n < GO; ++n) sd[n] = nsd[n];
     if (iy < oy1) load_row(iy + 1, nx);
-    if (iy >= oy0) load_side(iy, nsd);  // row iy is stored next iteration
+    load_side(iy - 1, sd);  // consumed by this iteration's store, after the row's FMAs
 #pragma unroll
     for (int kx = 0; kx < 3; ++kx)
 #pragma unroll
@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(kThinThreads) k_conv_thin(ConvArgs a) {
         const long long o = (long long)b * a.Ho * a.Wo * COUT + ((long long)oy * a.Wo + x) * COUT + co0;
 #pragma unroll
         for (int n = 0; n < GO; ++n) {
-          float t = v[n] + bias[n];
+          float t = v[n] + s_bias[co0 + n];
           if (a.softplus) t = softplus_fast(t);
           v[n] = t + sd[n];
         }
