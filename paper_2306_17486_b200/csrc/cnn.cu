@@ -294,19 +294,19 @@ void launch_tconv_t(const ConvArgs& a, int B, cudaStream_t st) {
 }
 
 // Thin convolutions, stride 1: the 2-channel stems (cin = 2) and the
-// 2-channel head (cout = 2).  Stems: one lane per output pixel, all cout
-// outputs in registers.  Heads: four lanes share a pixel, each folding in
-// cin / 4 input channels (partial sums reduced with shuffles), so a warp's
-// loads of the wide input cover 8 whole pixels, 512 contiguous bytes.  A
-// thread walks a band of kThinRows rows top to bottom: each input row (pixels
+// 2-channel head (cout = 2).  Two lanes share an output pixel and split its
+// wide side: stems give each lane cout / 2 output channels, heads give each
+// lane cin / 2 input channels (partial sums reduced with a shuffle) -- the
+// balance between per-lane work and registers (occupancy) that measured best.
+// A thread walks a band of kThinRows rows top to bottom: each input row (pixels
 // x-1, x, x+1) is read once and feeds the three output rows it touches, whose
 // sums stay in registers (rolling window); an output row is stored when its
-// last input row is in.  The next input row and the next output row's
-// addend / residual are loaded one iteration ahead.  Weights sit in shared
-// memory (warp-broadcast reads).
+// last input row is in.  The next input row is loaded one iteration ahead and
+// the row's addend / residual at the start of the iteration that stores it.
+// Weights and bias sit in shared memory (broadcast reads).
 constexpr int kThinRows = 16, kThinThreads = 128;
 template <int CIN, int COUT>
-__host__ __device__ constexpr int thin_lanes() { return CIN > COUT ? 4 : 1; }
+__host__ __device__ constexpr int thin_lanes() { return 2; }
 
 template <int N>
 HS_DEV void load_vec(const float* p, float* v) {
