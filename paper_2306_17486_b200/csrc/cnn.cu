@@ -304,7 +304,7 @@ void launch_tconv_t(const ConvArgs& a, int B, cudaStream_t st) {
 // last input row is in.  The next input row is loaded one iteration ahead and
 // the row's addend / residual at the start of the iteration that stores it.
 // Weights and bias sit in shared memory (broadcast reads).
-constexpr int kThinRows = 16, kThinThreads = 128;
+constexpr int kThinRows = 32, kThinThreads = 128;
 template <int CIN, int COUT>
 __host__ __device__ constexpr int thin_lanes() { return 2; }
 
