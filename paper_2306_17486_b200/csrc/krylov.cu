@@ -22,7 +22,7 @@ namespace hs {
 
 namespace {
 
-constexpr int NT = 256;
+constexpr int NT = 128;
 constexpr int KC = 6;             // basis vectors per chunk in a dot pass (registers vs w recomputes)
 constexpr int PST = 2 * KC + 1;   // doubles per partial record
 constexpr int kChunks = (kMaxRestart + KC - 1) / KC;

@@ -78,7 +78,7 @@ __global__ void k_finalize(hs::SolveDims d, hs::SolveBuffers s, int* hist_len, i
 }
 
 int choose_nblk(long long N, int B) {
-  long long want = (8LL * 148 + B - 1) / B;
+  long long want = (16LL * 148 + B - 1) / B;
   long long cap = (N + 256 * 8 - 1) / (256 * 8);
   long long n = want < cap ? want : cap;
   return (int)(n < 1 ? 1 : n);
