@@ -195,17 +195,18 @@ __global__ void __launch_bounds__(256) k_vc_up(LevelDev L, int ncx, int ncy, Vec
 
 constexpr int kCoarseThreads = 512;
 
+template <int MI>  // iteration capacity (coarse_iters <= MI): sizes the register partials
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_gmres(LevelDev L, const float2* __restrict__ rhs_base,
                                                                  float2* __restrict__ x_out, float2* vws,
                                                                  float2* sws, const float2* const* active,
                                                                  const int* model_of, int m, float damping,
                                                                  int* status) {
-  constexpr int NACC = 2 * (kCoarseMaxIters + 1) + 1;
+  constexpr int NACC = 2 * (MI + 1) + 1;
   __shared__ double red[NACC * (kCoarseThreads / 32 + 1)];
-  __shared__ double2 H[(kCoarseMaxIters + 1) * kCoarseMaxIters];
-  __shared__ double2 gv[kCoarseMaxIters + 1], sn[kCoarseMaxIters], yv[kCoarseMaxIters];
-  __shared__ double cs[kCoarseMaxIters], vs[kCoarseMaxIters + 1];
-  __shared__ double2 hc[kCoarseMaxIters + 1];
+  __shared__ double2 H[(MI + 1) * MI];
+  __shared__ double2 gv[MI + 1], sn[MI], yv[MI];
+  __shared__ double cs[MI], vs[MI + 1];
+  __shared__ double2 hc[MI + 1];
   __shared__ int s_flag, s_jend;
   const int b = blockIdx.x;
   if (active && active[b] == nullptr) return;
@@ -266,7 +267,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_gmres(LevelDev L, con
       double2 wd = f2d(w);
       acc[0] += wd.x * wd.x + wd.y * wd.y;
 #pragma unroll
-      for (int k = 0; k <= kCoarseMaxIters; ++k) {
+      for (int k = 0; k <= MI; ++k) {
         if (k <= j) {
           double2 d = zcmul(f2d(vec(k)[p]), wd);
           acc[1 + 2 * k] += d.x;
@@ -283,10 +284,10 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_gmres(LevelDev L, con
     const double wn = sqrt(acc[0]);
     if (threadIdx.x == 0)
 #pragma unroll
-      for (int k = 0; k <= kCoarseMaxIters; ++k)
+      for (int k = 0; k <= MI; ++k)
         if (k <= j) {
           hc[k] = make_double2(acc[1 + 2 * k] * vs[k], acc[2 + 2 * k] * vs[k]);
-          H[k * kCoarseMaxIters + j] = hc[k];
+          H[k * MI + j] = hc[k];
         }
     __syncthreads();
     double hn2 = 0.0;
@@ -312,7 +313,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_gmres(LevelDev L, con
       for (long long p = threadIdx.x; p < N; p += blockDim.x) {
         double2 wd = f2d(W[p]);
 #pragma unroll
-        for (int k = 0; k <= kCoarseMaxIters; ++k)
+        for (int k = 0; k <= MI; ++k)
           if (k <= j) {
             double2 d = zcmul(f2d(vec(k)[p]), wd);
             acc[2 * k] += d.x;
@@ -322,17 +323,17 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_gmres(LevelDev L, con
       block_sum<NACC>(acc, red);
       if (threadIdx.x == 0)
 #pragma unroll
-        for (int k = 0; k <= kCoarseMaxIters; ++k)
+        for (int k = 0; k <= MI; ++k)
           if (k <= j) {
             hc[k] = make_double2(acc[2 * k] * vs[k], acc[2 * k + 1] * vs[k]);
-            H[k * kCoarseMaxIters + j] = zadd(H[k * kCoarseMaxIters + j], hc[k]);
+            H[k * MI + j] = zadd(H[k * MI + j], hc[k]);
           }
       __syncthreads();
     }
     if (threadIdx.x == 0) {
       const double hn = sqrt(hn2);
-      double2 col[kCoarseMaxIters + 1];
-      for (int k = 0; k <= j; ++k) col[k] = H[k * kCoarseMaxIters + j];
+      double2 col[MI + 1];
+      for (int k = 0; k <= j; ++k) col[k] = H[k * MI + j];
       for (int k = 0; k < j; ++k) {
         double2 a = col[k], bb = col[k + 1];
         double2 s = sn[k];
@@ -357,7 +358,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_gmres(LevelDev L, con
       cs[j] = c;
       sn[j] = s;
       col[j] = rr;
-      for (int k = 0; k <= j; ++k) H[k * kCoarseMaxIters + j] = col[k];
+      for (int k = 0; k <= j; ++k) H[k * MI + j] = col[k];
       double2 gj = gv[j];
       gv[j] = zscale(gj, c);
       gv[j + 1] = zmul(make_double2(-s.x, s.y), gj);
@@ -382,8 +383,8 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_gmres(LevelDev L, con
   if (threadIdx.x == 0) {
     for (int i = jend - 1; i >= 0; --i) {
       double2 acc2 = gv[i];
-      for (int k = i + 1; k < jend; ++k) acc2 = zsub(acc2, zmul(H[i * kCoarseMaxIters + k], yv[k]));
-      double2 d = H[i * kCoarseMaxIters + i];
+      for (int k = i + 1; k < jend; ++k) acc2 = zsub(acc2, zmul(H[i * MI + k], yv[k]));
+      double2 d = H[i * MI + i];
       double den = d.x * d.x + d.y * d.y;
       yv[i] = make_double2((acc2.x * d.x + acc2.y * d.y) / den, (acc2.y * d.x - acc2.x * d.y) / den);
     }
@@ -397,6 +398,16 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_gmres(LevelDev L, con
     }
     x[p] = cmul(S[p], sum);
   }
+}
+
+// the reference's coarse solve runs 10 steps (multigrid.py:243); 16 is the supported maximum
+void launch_coarse(LevelDev L, const float2* rhs, float2* x, float2* vws, float2* sws, const float2* const* active,
+                   const int* model_of, int m, float damping, int* status, int B, cudaStream_t stream) {
+  if (m <= 10)
+    k_coarse_gmres<10><<<B, kCoarseThreads, 0, stream>>>(L, rhs, x, vws, sws, active, model_of, m, damping, status);
+  else
+    k_coarse_gmres<kCoarseMaxIters>
+        <<<B, kCoarseThreads, 0, stream>>>(L, rhs, x, vws, sws, active, model_of, m, damping, status);
 }
 
 }  // namespace hs
@@ -470,8 +481,7 @@ void vcycle(const Hierarchy& H, VecIn rhs, VecIn u0, VecOut out, const float2* c
     float2* tmp_out = reinterpret_cast<float2*>(p);
     dim3 g(cdiv_u(nc, 256 * 4), B);
     k_gather_scaled<<<g, 256, 0, stream>>>(rhs, active, tmp_in, (long long)nc);
-    k_coarse_gmres<<<B, kCoarseThreads, 0, stream>>>(C, tmp_in, tmp_out, cV, cS, active, model_of,
-                                                     H.coarse_iters, H.coarse_damping, status);
+    launch_coarse(C, tmp_in, tmp_out, cV, cS, active, model_of, H.coarse_iters, H.coarse_damping, status, B, stream);
     k_scatter<<<g, 256, 0, stream>>>(tmp_out, active, out, (long long)nc);
     return;
   }
@@ -496,8 +506,7 @@ void vcycle(const Hierarchy& H, VecIn rhs, VecIn u0, VecOut out, const float2* c
     vc_bytes += nact * (10.0 * N + ((l == 0 && has_u0) ? 8.0 * N : 0.0)) + H.n_models * 8.0 * N;
   }
   // coarsest
-  k_coarse_gmres<<<B, kCoarseThreads, 0, stream>>>(C, lrhs[Lc], lerr[Lc], cV, cS, active, model_of,
-                                                   H.coarse_iters, H.coarse_damping, status);
+  launch_coarse(C, lrhs[Lc], lerr[Lc], cV, cS, active, model_of, H.coarse_iters, H.coarse_damping, status, B, stream);
   vc_bytes += nact * 16.0 * (double)nc + H.n_models * 8.0 * (double)nc;
   // up legs
   for (int l = Lc - 1; l >= 0; --l) {
