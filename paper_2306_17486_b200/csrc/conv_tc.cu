@@ -49,7 +49,7 @@
 namespace hs {
 namespace {
 
-constexpr int kPrefetch = 8;  // rows pulled into L2 ahead of the bulk copies / epilogue loads
+constexpr int kPrefetch = 4;  // rows pulled into L2 ahead of the bulk copies / epilogue loads
 constexpr int kNA = 4;    // TMEM accumulators in flight
 constexpr int kEpiWarps = 8, kCvtWarp0 = 8;  // epilogue warps 0-7, converters from warp 8
 constexpr size_t kSmemMax = 232448;
@@ -184,7 +184,9 @@ struct Cfg {
   static constexpr bool ATM = KSTEPS == 1 && MODE == 0 && MT == 128;
   // warp roles: epilogue 0-7, converters (four when they also write the TMEM A
   // slots: a warp may only touch its own TMEM lane quarter), producer, MMA issuer
-  static constexpr int NCVT = ATM ? 4 : 2, CVT_THREADS = 32 * NCVT;
+  // four converter warps (measured best), except for the wide transposed tiles whose epilogue
+  // needs the registers a 14-warp CTA cannot give
+  static constexpr int NCVT = (MODE == 2 && CS * NACC > 32) ? 2 : 4, CVT_THREADS = 32 * NCVT;
   static constexpr int PROD = kCvtWarp0 + NCVT, MMAW = PROD + 1, NT = 32 * (MMAW + 1);
   // staged ring: ATM converters consume their own staged rows at once (two slots)
   static constexpr int NS_MIN = ATM ? 2 : 3, NS_MAX = ATM ? 2 : (MODE == 0 ? 10 : (MODE == 1 ? 8 : 6));
