@@ -187,7 +187,10 @@ struct Cfg {
   // four converter warps (measured best), except for the wide transposed tiles whose epilogue
   // needs the registers a 14-warp CTA cannot give
   static constexpr int NCVT = (MODE == 2 && CS * NACC > 32) ? 2 : 4, CVT_THREADS = 32 * NCVT;
-  static constexpr int PROD = kCvtWarp0 + NCVT, MMAW = PROD + 1, NT = 32 * (MMAW + 1);
+  // MMA issuer warps: one warp issues a tcgen05.mma every ~45 cycles; the M = 64
+  // layers (twice the MMAs per pixel) give alternate tiles to two issuers
+  static constexpr int NMW = (MT == 64 && MODE != 2) ? 2 : 1;  // measured: helps only the M = 64 layers
+  static constexpr int PROD = kCvtWarp0 + NCVT, MMAW = PROD + 1, NT = 32 * (MMAW + NMW);
   // staged ring: ATM converters consume their own staged rows at once (two slots)
   static constexpr int NS_MIN = ATM ? 2 : 3, NS_MAX = ATM ? 2 : (MODE == 0 ? 10 : (MODE == 1 ? 8 : 6));
   static constexpr size_t row_stage_bytes(int ns) {
@@ -486,7 +489,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
     }
     for (int i = 0; i < NS; ++i) {
       mbar_init(smem_u32(&stg_full[i]), C::CVT_THREADS);
-      mbar_init(smem_u32(&stg_empty[i]), 1);
+      mbar_init(smem_u32(&stg_empty[i]), C::NMW);  // every MMA warp releases every staged row
     }
     for (int i = 0; i < C::NA; ++i) {
       mbar_init(smem_u32(&acc_full[i]), 1);
@@ -623,7 +626,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
         }
       }
     }
-  } else if (warp == C::MMAW) {
+  } else if (warp >= C::MMAW && warp < C::MMAW + C::NMW) {
     // ================= MMA issuer
     {  // the whole warp walks the schedule; mma_bf16 / mma_commit elect one lane
       DescBase db;
@@ -683,12 +686,18 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
         auto slot = [&](int g) { return (int)((seq0 + (uint32_t)(g - U.glo)) % NS); };
         int waited = U.glo - 1;   // highest input row known to be staged
         int retired = U.glo - 1;  // highest input row released back to the converters
+        const int mw = warp - C::MMAW;  // this issuer takes the tiles with tile % NMW == mw
         for (int oy = U.oy0; oy < U.oy1; ++oy, ++tile) {
+          if ((int)(tile % C::NMW) != mw) continue;
           int lo, hi;
           tile_rows<MODE>(oy, lo, hi);
           for (int g = waited + 1; g <= hi; ++g) {
             const uint32_t sq = seq0 + (uint32_t)(g - U.glo);
             mbar_wait(smem_u32(&stg_full[sq % NS]), (sq / NS) & 1);
+            waited = g;
+            // rows below this tile were only read by the other issuer: release them at once,
+            // or the ring (3 slots on the 64-channel layers) cannot stage this tile's rows
+            for (; retired + 1 < lo && retired + 1 <= waited; ++retired) mma_commit(smem_u32(&stg_empty[slot(retired + 1)]));
           }
           waited = max(waited, hi);
           const uint32_t acc = tile % C::NA;
@@ -697,16 +706,25 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
           tc_fence_after();
           if (!(a.dbg & 2)) issue_mmas<C, MODE, MT>(oy, tm + acc * C::ACOLS, db, slot);
           mma_commit(smem_u32(&acc_full[acc]));
-          // release rows the next tile of this unit no longer reads
+          // release rows this issuer's next tile of the unit no longer reads (a row is
+          // released only after it was seen staged: an early arrival would complete the
+          // slot's previous phase)
           int keep_lo = U.ghi + 1;
-          if (oy + 1 < U.oy1) {
+          if (oy + C::NMW < U.oy1) {
             int nl, nh;
-            tile_rows<MODE>(oy + 1, nl, nh);
+            tile_rows<MODE>(oy + C::NMW, nl, nh);
             keep_lo = nl;
           }
           for (int g = retired + 1; g < keep_lo && g <= waited; ++g) mma_commit(smem_u32(&stg_empty[slot(g)]));
           retired = max(retired, min(keep_lo - 1, waited));
         }
+        // unit end: rows this issuer never read still need its release
+        for (int g = waited + 1; g <= U.ghi; ++g) {
+          const uint32_t sq = seq0 + (uint32_t)(g - U.glo);
+          mbar_wait(smem_u32(&stg_full[sq % NS]), (sq / NS) & 1);
+        }
+        waited = max(waited, U.ghi);
+        for (int g = retired + 1; g <= U.ghi; ++g) mma_commit(smem_u32(&stg_empty[slot(g)]));
         seq0 += U.ghi - U.glo + 1;
       }
     }
