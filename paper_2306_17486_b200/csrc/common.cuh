@@ -21,7 +21,7 @@ HS_DEV float2 cmul(float2 a, float2 b) {
 }
 // a / b for complex b (fp32; |b| is O(1/h^2) so no scaling is needed)
 HS_DEV float2 cdiv(float2 a, float2 b) {
-  float inv = 1.0f / (b.x * b.x + b.y * b.y);
+  float inv = __frcp_rn(b.x * b.x + b.y * b.y);  // correctly rounded, as 1.0f / x
   return make_float2((a.x * b.x + a.y * b.y) * inv, (a.y * b.x - a.x * b.y) * inv);
 }
 
