@@ -183,6 +183,19 @@ HS_API long long hs_launch_count(void);
 /* 1 (default): tcgen05 3xTF32 convolutions where the shape allows; 0: SIMT fp32 only */
 HS_API void hs_set_conv_path(int tensor_cores);
 
+/* ---- slowness-model preparation (SPEC.md datagen: load_slowness_corpus / gaussian_smooth,
+ *      reference SPEC.md:404-417,441).  fp64 fields (B, rows, cols), device pointers. */
+/* corner-aligned bilinear resize (B, hin, win) -> (B, hout, wout) */
+HS_API int hs_resize_bilinear(const double* in, double* out, int B, int hin, int win, int hout, int wout,
+                              void* stream);
+/* separable truncated Gaussian, radius ceil(3 sigma), edge-replicated; sigma = 0 is the identity.
+ * tmp: (B, nx, ny) scratch.  Blocks until done. */
+HS_API int hs_gaussian_smooth(const double* in, double* out, double* tmp, int B, int nx, int ny, double sigma,
+                              void* stream);
+/* affine map of each field onto [lo, hi]; a constant field maps to lo.  minmax: (B, 2) scratch out. */
+HS_API int hs_normalise_range(const double* in, double* out, double* minmax, int B, long long n, double lo,
+                              double hi, void* stream);
+
 /* use caller-held encodings (same layout as hs_net_encode's output) */
 HS_API int hs_net_set_encodings(hs_net_t* net, int levels, const float* const* enc);
 /* network.preconditioner_estimate (krylov.py:225-226): u0 = (h^2/64) net(r),

@@ -130,6 +130,9 @@ SIGNATURES = {
     "hs_profile_query": (_I, [_I, c_double_p, c_double_p, ctypes.POINTER(ctypes.c_longlong)]),
     "hs_launch_count": (ctypes.c_longlong, []),
     "hs_set_conv_path": (None, [_I]),
+    "hs_resize_bilinear": (_I, [_VP, _VP, _I, _I, _I, _I, _I, _VP]),
+    "hs_gaussian_smooth": (_I, [_VP, _VP, _VP, _I, _I, _I, _D, _VP]),
+    "hs_normalise_range": (_I, [_VP, _VP, _VP, _I, ctypes.c_longlong, _D, _D, _VP]),
 }
 
 _lock = threading.Lock()
