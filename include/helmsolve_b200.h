@@ -215,4 +215,36 @@ HS_API int hs_implicit_apply(const void* x, const void* spectrum, void* y, int B
 HS_API int hs_conv2d(const float* x, const hs_conv_t* conv, const float* addend, const float* residual, float* y,
                      int B, int H, int W, void* stream);
 
+/* ---- network training (SPEC.md `[MODULE] trainer`, reference SPEC.md:454-507).
+ * The reference has no trainer; one step is the SPEC mse_loss of u0 = (h^2/64) net(r) against the
+ * true error e, backward through the reference autodiff's rules (autodiff.py: conv2d :472-507,
+ * conv_transpose2d :510-544, batchnorm2d training :547-592, softplus :243-252, green.py:55-107),
+ * then Adam.  Parameters are one float32 vector in netparams.param_spec order (complex implicit
+ * kernels as (re, im) pairs), running batch-norm statistics included and updated in place. */
+typedef struct hs_trainer hs_trainer_t;
+typedef struct {
+  int levels;      /* L >= 2 */
+  int channels[8]; /* C_0 .. C_{L-1}, powers of two <= 256, C_{L-1} even */
+  int nx, ny;      /* node grid; the network grid is (nx-1, ny-1), divisible by 2^(L-1) */
+  int batch;       /* samples per step */
+  double h;        /* grid spacing of the u0 scale h^2/64 */
+} hs_train_desc_t;
+typedef struct {
+  float lr, beta1, beta2, eps; /* torch.optim.Adam defaults: 1e-3, 0.9, 0.999, 1e-8 */
+} hs_adam_t;
+/* floats in the flat parameter vector (0 for an invalid descriptor) */
+HS_API size_t hs_train_param_count(const hs_train_desc_t* desc);
+/* params: host float32 vector of hs_train_param_count floats */
+HS_API int hs_trainer_create(hs_trainer_t** out, const hs_train_desc_t* desc, const float* params, void* stream);
+HS_API void hs_trainer_destroy(hs_trainer_t* t);
+/* media: device float32 (n_models, 2, nx-1, ny-1) (kappa^2, gamma); model_of: HOST int (batch,);
+ * r, e: device complex128 (batch, nx, ny).  adam NULL = gradients only (no update).  loss (host,
+ * optional) receives the batch MSE and makes the call synchronous; HS_ENONFINITE on a non-finite loss. */
+HS_API int hs_trainer_step(hs_trainer_t* t, const float* media, int n_models, const int* model_of, const void* r,
+                           const void* e, const hs_adam_t* adam, double* loss, void* stream);
+/* which: 0 parameters, 1 last gradients, 2 Adam m, 3 Adam v; host float32 out */
+HS_API int hs_trainer_read(const hs_trainer_t* t, int which, float* host, void* stream);
+/* which: 0 parameters, 2 Adam m, 3 Adam v (checkpoint restore); step >= 0 sets Adam's step counter */
+HS_API int hs_trainer_write(hs_trainer_t* t, int which, const float* host, int step, void* stream);
+
 #endif

@@ -369,6 +369,96 @@ def fx_learned_c1(n_rhs):
          kappa_sq=m.kappa_sq)
 
 
+# ---------------------------------------- training step on reference autodiff
+
+
+def fx_train():
+    """Loss + every parameter gradient of one training step, from the reference's autodiff.
+
+    ARCH.md network composed from reference primitives with gradients ON, training-mode batch
+    norm (running buffers updated in place, autodiff.py:570-580), the Green spectrum built from
+    the trainable kernel Tensor (green.py:55-82), float64 throughout; loss = SPEC mse_loss of
+    u0 = (h^2/64) net(r) (zero-padded) against e.  Pins oracle/train_oracle.py.
+    """
+    from oracle import train_oracle as to
+
+    out = {}
+    rng = np.random.default_rng(29)
+    for tag, L, ch, n, B in [("a", 2, (4, 8), 17, 3), ("b", 3, (4, 8, 8), 33, 2)]:
+        params = to.as_float64(netparams.randomise_batchnorm(netparams.init_params(ch, seed=7), seed=8))
+        models = [rf.slowness_model(problems.smooth_random_kappa_sq((n, n), 3.0, s), layer_width=max(2, n // 8))
+                  for s in (1, 2)]
+        owner = np.arange(B) % 2
+        media = np.concatenate([no.media_planes(models[o].kappa_sq, models[o].gamma, L) for o in owner]
+                               ).astype(np.float64)
+        r = noise(rng, (B, n, n))
+        e = noise(rng, (B, n, n)) * 0.01
+        h = 1.0 / (n - 1)
+        T = ad.Tensor
+        tp = {k: T(v.copy(), requires_grad=True) for k, v in params.items() if to.trainable(k)}
+        stats = {k: v.copy() for k, v in params.items() if not to.trainable(k)}
+
+        def cbs(pre, x, stride=1, transposed=False, out_hw=None):
+            if transposed:
+                y = ad.conv_transpose2d(x, tp[pre + ".w"], tp[pre + ".b"], stride=2, pad=1, out_hw=out_hw)
+            else:
+                y = ad.conv2d(x, tp[pre + ".w"], tp[pre + ".b"], stride=stride)
+            y = ad.batchnorm2d(y, tp[pre + ".bn.gamma"], tp[pre + ".bn.beta"], stats[pre + ".bn.mean"],
+                               stats[pre + ".bn.var"], training=True)
+            return ad.softplus(y)
+
+        def res(pre, x):
+            return ad.add(x, ad.conv2d(cbs(pre + ".a", x), tp[pre + ".b.w"], tp[pre + ".b.b"]))
+
+        e0 = res("enc.res0", cbs("enc.stem", T(media)))
+        feats = [e0]
+        for lv in range(1, L):
+            e0 = res(f"enc.res{lv}", cbs(f"enc.down{lv}", e0, stride=2))
+            feats.append(e0)
+        (ix, iy), coarse = no.cnn_dims((n, n), L)
+        r2 = np.stack([r[:, :ix, :iy].real, r[:, :ix, :iy].imag], axis=1)
+        x = res("sol.res0", ad.add(cbs("sol.stem", T(r2)), feats[0]))
+        skips = [x]
+        for lv in range(1, L):
+            x = res(f"sol.res{lv}", ad.add(cbs(f"sol.down{lv}", x, stride=2), feats[lv]))
+            skips.append(x)
+        spec = rg.green_function(tp["sol.implicit.w"], coarse)
+        x = ad.unpack_complex(rg.implicit_apply(ad.pack_complex(x), spec))
+        for lv in range(L - 1, 0, -1):
+            s = skips[lv - 1]
+            x = res(f"sol.ures{lv - 1}", ad.add(cbs(f"sol.up{lv}", x, transposed=True, out_hw=s.data.shape[-2:]), s))
+        y = ad.conv2d(x, tp["sol.head.w"], tp["sol.head.b"])
+        sc = h * h / 64.0
+        tgt = np.stack([e[:, :ix, :iy].real, e[:, :ix, :iy].imag], axis=1)
+        d = ad.sub(ad.mul(y, sc), T(tgt))
+        pad = float(np.sum(np.abs(e) ** 2) - np.sum(np.abs(e[:, :ix, :iy]) ** 2))
+        loss = ad.add(ad.mul(ad.tsum(ad.mul(d, d)), 1.0 / B), pad / B)
+        loss.backward()
+        ref_grads = {k: t.grad for k, t in tp.items()}
+        # oracle restatement on the same inputs
+        po = {k: v.copy() for k, v in params.items()}
+        lo, go, _ = to.loss_and_grads(po, L, media, r, e, h)
+        el = abs(lo - float(loss.data)) / abs(float(loss.data))
+        assert el < 1e-12, el
+        worst = 0.0
+        for k, g in ref_grads.items():
+            er = relerr(go[k], g) if np.linalg.norm(g) > 1e-12 else float(np.abs(go[k] - g).max())
+            worst = max(worst, er)
+            assert er < 1e-9, (k, er)
+        for k in stats:
+            assert relerr(po[k], stats[k]) < 1e-12, k
+        print(f"  train {tag}: loss {float(loss.data):.6e}, oracle grads within {worst:.1e}")
+        out.update({f"media_{tag}": media, f"r_{tag}": r, f"e_{tag}": e, f"h_{tag}": h, f"loss_{tag}": float(loss.data),
+                    f"levels_{tag}": L, f"channels_{tag}": np.array(ch)})
+        for k, v in params.items():
+            out[f"p_{tag}_{k}"] = v
+        for k, g in ref_grads.items():
+            out[f"g_{tag}_{k}"] = g
+        for k, v in stats.items():
+            out[f"s_{tag}_{k}"] = v
+    save("train.npz", **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
@@ -377,7 +467,7 @@ def main():
     todo = {
         "fields": fx_fields, "transfers": fx_transfers, "hierarchy": fx_hierarchy, "vcycle": fx_vcycle,
         "solve_small": fx_solve_small, "solve_c1": fx_solve_c1, "cnn": fx_cnn_primitives, "network": fx_network,
-        "learned": lambda: fx_learned_c1(a.learned_rhs),
+        "learned": lambda: fx_learned_c1(a.learned_rhs), "train": fx_train,
     }
     for name, fn in todo.items():
         if a.only and name not in a.only.split(","):

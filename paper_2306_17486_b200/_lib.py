@@ -102,6 +102,21 @@ class HsNetDesc(ctypes.Structure):
     ]
 
 
+class HsTrainDesc(ctypes.Structure):
+    _fields_ = [
+        ("levels", ctypes.c_int),
+        ("channels", ctypes.c_int * 8),
+        ("nx", ctypes.c_int),
+        ("ny", ctypes.c_int),
+        ("batch", ctypes.c_int),
+        ("h", ctypes.c_double),
+    ]
+
+
+class HsAdam(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_float), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float), ("eps", ctypes.c_float)]
+
+
 # (name, restype, argtypes) for every symbol include/helmsolve_b200.h declares
 _VP, _I, _D, _SZ = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_size_t
 SIGNATURES = {
@@ -133,6 +148,12 @@ SIGNATURES = {
     "hs_resize_bilinear": (_I, [_VP, _VP, _I, _I, _I, _I, _I, _VP]),
     "hs_gaussian_smooth": (_I, [_VP, _VP, _VP, _I, _I, _I, _D, _VP]),
     "hs_normalise_range": (_I, [_VP, _VP, _VP, _I, ctypes.c_longlong, _D, _D, _VP]),
+    "hs_train_param_count": (_SZ, [ctypes.POINTER(HsTrainDesc)]),
+    "hs_trainer_create": (_I, [ctypes.POINTER(_VP), ctypes.POINTER(HsTrainDesc), _VP, _VP]),
+    "hs_trainer_destroy": (None, [_VP]),
+    "hs_trainer_step": (_I, [_VP, _VP, _I, _VP, _VP, _VP, ctypes.POINTER(HsAdam), c_double_p, _VP]),
+    "hs_trainer_read": (_I, [_VP, _I, _VP, _VP]),
+    "hs_trainer_write": (_I, [_VP, _I, _VP, _I, _VP]),
 }
 
 _lock = threading.Lock()
