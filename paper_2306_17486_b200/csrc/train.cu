@@ -27,6 +27,7 @@
 
 #include "../../include/helmsolve_b200.h"
 #include "common.cuh"
+#include "conv_tc.h"
 #include "prof.h"
 
 namespace hs {
@@ -65,11 +66,13 @@ struct TrConv {
 constexpr int kConvThreads = 128;
 constexpr int kCk = 32;
 
-template <int COB>
+// PX consecutive output pixels of one row per thread (Wo % PX == 0) x COB output channels:
+// weights staged in shared memory per 32-channel slice and read as broadcasts, reused PX times.
+template <int COB, int PX>
 __global__ void __launch_bounds__(kConvThreads) k_tr_conv(TrConv a) {
-  __shared__ float ws[9][kCk][COB];
+  __shared__ __align__(16) float ws[9][kCk][COB];
   const long long npix = (long long)a.B * a.Ho * a.Wo;
-  const long long pix = (long long)blockIdx.x * kConvThreads + threadIdx.x;
+  const long long pix = ((long long)blockIdx.x * kConvThreads + threadIdx.x) * PX;
   const int co0 = blockIdx.y * COB;
   const bool live = pix < npix;
   int n = 0, oy = 0, ox = 0;
@@ -79,22 +82,32 @@ __global__ void __launch_bounds__(kConvThreads) k_tr_conv(TrConv a) {
     oy = rem / a.Wo;
     ox = rem - oy * a.Wo;
   }
-  int iy[3], ix[3];
+  int iy[3], ix[PX][3];
 #pragma unroll
   for (int u = 0; u < 3; ++u) {
     if (a.trans) {
-      const int qy = oy + 1 - u, qx = ox + 1 - u;
+      const int qy = oy + 1 - u;
       iy[u] = (qy >= 0 && qy % a.s == 0 && qy / a.s < a.Hi) ? qy / a.s : -1;
-      ix[u] = (qx >= 0 && qx % a.s == 0 && qx / a.s < a.Wi) ? qx / a.s : -1;
+#pragma unroll
+      for (int j = 0; j < PX; ++j) {
+        const int qx = ox + j + 1 - u;
+        ix[j][u] = (qx >= 0 && qx % a.s == 0 && qx / a.s < a.Wi) ? qx / a.s : -1;
+      }
     } else {
-      const int qy = a.s * oy + u - 1, qx = a.s * ox + u - 1;
+      const int qy = a.s * oy + u - 1;
       iy[u] = (qy >= 0 && qy < a.Hi) ? qy : -1;
-      ix[u] = (qx >= 0 && qx < a.Wi) ? qx : -1;
+#pragma unroll
+      for (int j = 0; j < PX; ++j) {
+        const int qx = a.s * (ox + j) + u - 1;
+        ix[j][u] = (qx >= 0 && qx < a.Wi) ? qx : -1;
+      }
     }
   }
-  float acc[COB];
+  float acc[PX][COB];
 #pragma unroll
-  for (int k = 0; k < COB; ++k) acc[k] = 0.f;
+  for (int j = 0; j < PX; ++j)
+#pragma unroll
+    for (int k = 0; k < COB; ++k) acc[j][k] = 0.f;
   for (int c0 = 0; c0 < a.Ci; c0 += kCk) {
     const int ck = min(kCk, a.Ci - c0);
     __syncthreads();
@@ -109,29 +122,40 @@ __global__ void __launch_bounds__(kConvThreads) k_tr_conv(TrConv a) {
 #pragma unroll
     for (int u = 0; u < 3; ++u) {
       if (iy[u] < 0) continue;
+      const float* row = a.x + ((long long)n * a.Hi + iy[u]) * a.Wi * a.Ci + c0;
 #pragma unroll
       for (int v = 0; v < 3; ++v) {
-        if (ix[v] < 0) continue;
-        const float* px = a.x + (((long long)n * a.Hi + iy[u]) * a.Wi + ix[v]) * a.Ci + c0;
         const int t = u * 3 + v;
-        for (int c = 0; c < ck; ++c) {
-          const float xv = __ldg(px + c);
+        const float* px[PX];
 #pragma unroll
-          for (int k = 0; k < COB; ++k) acc[k] = fmaf(xv, ws[t][c][k], acc[k]);
+        for (int j = 0; j < PX; ++j) px[j] = ix[j][v] >= 0 ? row + (long long)ix[j][v] * a.Ci : nullptr;
+        for (int c = 0; c < ck; ++c) {
+          float xv[PX];
+#pragma unroll
+          for (int j = 0; j < PX; ++j) xv[j] = px[j] ? __ldg(px[j] + c) : 0.f;
+#pragma unroll
+          for (int k = 0; k < COB; ++k) {
+            const float wk = ws[t][c][k];
+#pragma unroll
+            for (int j = 0; j < PX; ++j) acc[j][k] = fmaf(xv[j], wk, acc[j][k]);
+          }
         }
       }
     }
   }
   if (!live) return;
-  float* py = a.y + pix * a.Co + co0;
 #pragma unroll
-  for (int k = 0; k < COB; ++k) {
-    if (co0 + k >= a.Co) break;
-    float v = acc[k];
-    if (a.bias) v += a.bias[co0 + k];
-    if (a.addend) v += a.addend[pix * a.Co + co0 + k];
-    if (a.accumulate) v += py[k];
-    py[k] = v;
+  for (int j = 0; j < PX; ++j) {
+    float* py = a.y + (pix + j) * a.Co + co0;
+#pragma unroll
+    for (int k = 0; k < COB; ++k) {
+      if (co0 + k >= a.Co) break;
+      float v = acc[j][k];
+      if (a.bias) v += a.bias[co0 + k];
+      if (a.addend) v += a.addend[(pix + j) * a.Co + co0 + k];
+      if (a.accumulate) v += py[k];
+      py[k] = v;
+    }
   }
 }
 
@@ -148,52 +172,113 @@ struct TrWgrad {
   long long chunk;
 };
 
+// Tile AT x BT of (a, b) pairs x 9 taps; a thread owns 4 consecutive a for one b (36 accumulators:
+// one 16-byte P read + 9 Q reads per 36 FMAs).  The 256 threads form KS = 256 / (AT BT / 4) groups that
+// take interleaved 16-pixel slices of the block's chunk (split-K inside the block), folded in shared
+// memory at the end in group order.
 constexpr int kWgPx = 16;
+constexpr int kWgSmem = 10240;  // floats of staging
 
-__global__ void __launch_bounds__(256) k_tr_wgrad(TrWgrad g) {
-  __shared__ float ps[kWgPx][16];
-  __shared__ float qs[kWgPx][9][16];
-  const int a0 = blockIdx.y * 16, b0 = blockIdx.z * 16;
-  const int ta = threadIdx.x >> 4, tb = threadIdx.x & 15;
+template <int AT, int BT>
+__global__ void __launch_bounds__(256, 2) k_tr_wgrad(TrWgrad g) {
+  constexpr int TPG = AT * BT / 4;  // threads per group
+  constexpr int KS = 256 / TPG;
+  constexpr int SP = KS * kWgPx;  // pixels staged per round
+  static_assert(SP * AT + SP * 9 * BT <= kWgSmem, "staging");
+  __shared__ __align__(16) float sm[kWgSmem];
+  __shared__ int4 pc[SP];
+  float* ps = sm;                // [SP][AT]
+  float* qs = sm + SP * AT;      // [SP][9][BT]
+  const int a0 = blockIdx.y * AT, b0 = blockIdx.z * BT;
+  const int grp = threadIdx.x / TPG, lt = threadIdx.x % TPG;
+  const int tb = lt % BT, ag = lt / BT;
   const long long plane = (long long)g.Hp * g.Wp;
   const long long npix = (long long)g.B * plane;
   const long long p0 = blockIdx.x * g.chunk, p1 = min(npix, p0 + g.chunk);
-  float acc[9];
+  float acc[4][9];
 #pragma unroll
-  for (int t = 0; t < 9; ++t) acc[t] = 0.f;
-  for (long long pb = p0; pb < p1; pb += kWgPx) {
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int t = 0; t < 9; ++t) acc[i][t] = 0.f;
+  for (long long pb = p0; pb < p1; pb += SP) {
     __syncthreads();
-    {
-      const int px = threadIdx.x >> 4, ai = threadIdx.x & 15;
-      const long long p = pb + px;
-      ps[px][ai] = (p < p1 && a0 + ai < g.A) ? g.P[p * g.A + a0 + ai] : 0.f;
-    }
-    for (int i = threadIdx.x; i < kWgPx * 9 * 16; i += 256) {
-      const int bi = i & 15, t = (i >> 4) % 9, px = i / 144;
-      const long long p = pb + px;
-      float v = 0.f;
-      if (p < p1 && b0 + bi < g.Bc) {
+    if (threadIdx.x < SP) {
+      const long long p = pb + threadIdx.x;
+      int4 c = make_int4(-1, 0, 0, 0);
+      if (p < p1) {
         const int n = (int)(p / plane);
         const int rem = (int)(p - n * plane);
-        const int oy = rem / g.Wp, ox = rem - oy * g.Wp;
-        const int qy = g.s * oy + t / 3 - 1, qx = g.s * ox + t % 3 - 1;
-        if (qy >= 0 && qy < g.Hq && qx >= 0 && qx < g.Wq)
-          v = g.Q[(((long long)n * g.Hq + qy) * g.Wq + qx) * g.Bc + b0 + bi];
+        c = make_int4(n, rem / g.Wp, rem % g.Wp, 0);
       }
-      qs[px][t][bi] = v;
+      pc[threadIdx.x] = c;
     }
     __syncthreads();
-#pragma unroll 4
-    for (int px = 0; px < kWgPx; ++px) {
-      const float pv = ps[px][ta];
+    for (int i = threadIdx.x; i < SP * AT; i += 256) {
+      const int px = i / AT, ai = i % AT;
+      ps[i] = (pc[px].x >= 0 && a0 + ai < g.A) ? g.P[(pb + px) * g.A + a0 + ai] : 0.f;
+    }
+    for (int i = threadIdx.x; i < SP * 9 * BT; i += 256) {
+      const int bi = i % BT, t = (i / BT) % 9, px = i / (9 * BT);
+      const int4 c = pc[px];
+      float v = 0.f;
+      if (c.x >= 0 && b0 + bi < g.Bc) {
+        const int qy = g.s * c.y + t / 3 - 1, qx = g.s * c.z + t % 3 - 1;
+        if (qy >= 0 && qy < g.Hq && qx >= 0 && qx < g.Wq)
+          v = g.Q[(((long long)c.x * g.Hq + qy) * g.Wq + qx) * g.Bc + b0 + bi];
+      }
+      qs[i] = v;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int k = 0; k < kWgPx; ++k) {
+      const int px = grp * kWgPx + k;
+      const float4 pa = *reinterpret_cast<const float4*>(ps + px * AT + 4 * ag);
 #pragma unroll
-      for (int t = 0; t < 9; ++t) acc[t] = fmaf(pv, qs[px][t][tb], acc[t]);
+      for (int t = 0; t < 9; ++t) {
+        const float q = qs[(px * 9 + t) * BT + tb];
+        acc[0][t] = fmaf(pa.x, q, acc[0][t]);
+        acc[1][t] = fmaf(pa.y, q, acc[1][t]);
+        acc[2][t] = fmaf(pa.z, q, acc[2][t]);
+        acc[3][t] = fmaf(pa.w, q, acc[3][t]);
+      }
     }
   }
-  if (a0 + ta < g.A && b0 + tb < g.Bc) {
-    float* out = g.part + (long long)blockIdx.x * g.A * g.Bc * 9 + ((long long)(a0 + ta) * g.Bc + b0 + tb) * 9;
+  // fold the KS groups in order
+  __syncthreads();
+  if (grp > 0) {
 #pragma unroll
-    for (int t = 0; t < 9; ++t) out[t] = acc[t];
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int t = 0; t < 9; ++t) sm[((grp - 1) * 36 + i * 9 + t) * TPG + lt] = acc[i][t];
+  }
+  __syncthreads();
+  if (grp == 0) {
+    for (int q = 1; q < KS; ++q)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int t = 0; t < 9; ++t) acc[i][t] += sm[((q - 1) * 36 + i * 9 + t) * TPG + lt];
+    const int b = b0 + tb;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int a = a0 + 4 * ag + i;
+      if (a < g.A && b < g.Bc) {
+        float* out = g.part + (long long)blockIdx.x * g.A * g.Bc * 9 + ((long long)a * g.Bc + b) * 9;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) out[t] = acc[i][t];
+      }
+    }
+  }
+}
+
+// stage 1 of the partial sum: part2[grp][i] = sum of chunks [grp * per, (grp + 1) * per), in order
+__global__ void k_tr_sum_parts1(const float* part, int nchunk, int per, long long n, float* part2) {
+  const int grp = blockIdx.y;
+  GRID_STRIDE(i, n) {
+    double s = 0.0;
+    const int c1 = min(nchunk, (grp + 1) * per);
+    for (int c = grp * per; c < c1; ++c) s += part[(long long)c * n + i];
+    part2[(long long)grp * n + i] = (float)s;
   }
 }
 
@@ -240,6 +325,7 @@ __global__ void __launch_bounds__(256) k_tr_chan(TrChan a) {
       gm = a.gamma[c];
       bt = a.beta[c];
     }
+#pragma unroll 4
     for (long long p = p0 + lane; p < p1; p += lanes) {
       const float z = a.z[p * a.C + c];
       if (a.op == kStats) {
@@ -284,14 +370,18 @@ struct TrChanFin {
   float* s1;
 };
 
+// one warp per channel: lanes take chunks lane, lane + 32, ... then a fixed shuffle tree (deterministic)
 __global__ void k_tr_chan_fin(TrChanFin f) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (c >= f.C) return;
   double q0 = 0.0, q1 = 0.0;
-  for (int k = 0; k < f.nchunk; ++k) {
+  for (int k = lane; k < f.nchunk; k += 32) {
     q0 += f.part[((long long)k * f.C + c) * 2];
     q1 += f.part[((long long)k * f.C + c) * 2 + 1];
   }
+  q0 = warp_sum(q0);
+  q1 = warp_sum(q1);
+  if (lane) return;
   const double m = (double)f.M;
   if (f.op == kStats) {
     const double mean = q0 / m;
@@ -570,12 +660,35 @@ __global__ void k_tr_adam(float* p, const float* g, float* m, float* v, long lon
   }
 }
 
+// ------------------------------------------------------------------ weight re-packing
+
+// dst[o][u][v][i] = src[o][i][u'][v'] (src_io = 0) or src[i][o][u'][v'] (src_io = 1), (u', v') = flip ? (2-u, 2-v) : (u, v)
+struct Repack {
+  const float* src;
+  float* dst;
+  int O, I, src_io, flip;
+};
+
+__global__ void k_tr_repack(const Repack* tab) {
+  const Repack r = tab[blockIdx.y];
+  const int n = r.O * r.I * 9;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int i = e % r.I, t = (e / r.I) % 9, o = e / (9 * r.I);
+    const int ts = r.flip ? 8 - t : t;
+    r.dst[e] = r.src_io ? r.src[((long long)i * r.O + o) * 9 + ts] : r.src[((long long)o * r.I + i) * 9 + ts];
+  }
+}
+
 // ------------------------------------------------------------------ the trainer
+
+enum Kind { kS1 = 0, kS2 = 1, kT2 = 2 };
 
 struct LayerP {
   size_t w = 0, b = 0, gamma = 0, beta = 0, mean = 0, var = 0;
-  int cin = 0, cout = 0;
+  int cin = 0, cout = 0, kind = 0;  // kind: kS1 / kS2 / kT2
   bool bn = false, transposed = false;
+  float* wf = nullptr;  // forward weights in the tensor-core layout [out][ky][kx][in] (re-packed per step)
+  float* wd = nullptr;  // data-gradient weights, same layout
   float* st_mean = nullptr;  // batch statistics of the current step
   float* st_inv = nullptr;
 };
@@ -605,6 +718,9 @@ struct hs_trainer {
   long long wg_part_cap = 0;
   double *loss_part = nullptr, *loss_dev = nullptr;
   int* model_dev = nullptr;
+  hs::Repack* repack = nullptr;  // device table, one entry per packed weight array
+  int n_repack = 0;
+  float* zero_bias = nullptr;
   cufftComplex *Xf = nullptr, *Yb = nullptr, *spec = nullptr;
   double2 *big1 = nullptr, *big2 = nullptr, *gG = nullptr;
   cufftHandle pB = 0, p1 = 0, p2 = 0;
@@ -628,11 +744,12 @@ namespace {
 // walk netparams.param_spec (netparams.py:31-53): the same order and sizes
 struct Spec {
   size_t off = 0;
-  LayerP conv(int co, int ci, bool transposed = false, bool bn = true) {
+  LayerP conv(int co, int ci, int kind, bool bn = true) {
     LayerP p;
     p.cin = ci;
     p.cout = co;
-    p.transposed = transposed;
+    p.kind = kind;
+    p.transposed = kind == kT2;
     p.bn = bn;
     p.w = off;
     off += (size_t)co * ci * 9;
@@ -658,23 +775,23 @@ void build_layout(hs_trainer* t) {
     LayerP* la = side ? t->sol_a : t->enc_a;
     LayerP* lb = side ? t->sol_b : t->enc_b;
     LayerP* ld = side ? t->sol_down : t->enc_down;
-    *stem = s.conv(C[0], 2);
-    la[0] = s.conv(C[0], C[0]);
-    lb[0] = s.conv(C[0], C[0], false, false);
+    *stem = s.conv(C[0], 2, kS1);
+    la[0] = s.conv(C[0], C[0], kS1);
+    lb[0] = s.conv(C[0], C[0], kS1, false);
     for (int lv = 1; lv < L; ++lv) {
-      ld[lv] = s.conv(C[lv], C[lv - 1]);
-      la[lv] = s.conv(C[lv], C[lv]);
-      lb[lv] = s.conv(C[lv], C[lv], false, false);
+      ld[lv] = s.conv(C[lv], C[lv - 1], kS2);
+      la[lv] = s.conv(C[lv], C[lv], kS1);
+      lb[lv] = s.conv(C[lv], C[lv], kS1, false);
     }
   }
   t->implicit = s.off;
   s.off += (size_t)(C[L - 1] / 2) * 9 * 2;
   for (int lv = L - 1; lv >= 1; --lv) {
-    t->up[lv] = s.conv(C[lv - 1], C[lv], true);
-    t->ures_a[lv] = s.conv(C[lv - 1], C[lv - 1]);
-    t->ures_b[lv] = s.conv(C[lv - 1], C[lv - 1], false, false);
+    t->up[lv] = s.conv(C[lv - 1], C[lv], kT2);
+    t->ures_a[lv] = s.conv(C[lv - 1], C[lv - 1], kS1);
+    t->ures_b[lv] = s.conv(C[lv - 1], C[lv - 1], kS1, false);
   }
-  t->head = s.conv(2, C[0], false, false);
+  t->head = s.conv(2, C[0], kS1, false);
   t->nparam = s.off;
 }
 
@@ -693,28 +810,46 @@ void conv_launch(const float* x, int Hi, int Wi, int Ci, float* y, int Ho, int W
                  cudaStream_t st) {
   TrConv a{x, Hi, Wi, Ci, y, Ho, Wo, Co, w, sco, sci, bias, addend, trans, s, accumulate, B};
   const long long npix = (long long)B * Ho * Wo;
-  const unsigned gx = (unsigned)((npix + kConvThreads - 1) / kConvThreads);
-  if (Co >= 16) k_tr_conv<16><<<dim3(gx, (Co + 15) / 16), kConvThreads, 0, st>>>(a);
-  else if (Co >= 8) k_tr_conv<8><<<dim3(gx, (Co + 7) / 8), kConvThreads, 0, st>>>(a);
-  else if (Co >= 4) k_tr_conv<4><<<dim3(gx, (Co + 3) / 4), kConvThreads, 0, st>>>(a);
-  else k_tr_conv<2><<<dim3(gx, (Co + 1) / 2), kConvThreads, 0, st>>>(a);
+  if (Wo % 4 == 0) {
+    const unsigned gx = (unsigned)((npix / 4 + kConvThreads - 1) / kConvThreads);
+    if (Co >= 16) k_tr_conv<16, 4><<<dim3(gx, (Co + 15) / 16), kConvThreads, 0, st>>>(a);
+    else if (Co >= 8) k_tr_conv<8, 4><<<dim3(gx, (Co + 7) / 8), kConvThreads, 0, st>>>(a);
+    else if (Co >= 4) k_tr_conv<4, 4><<<dim3(gx, (Co + 3) / 4), kConvThreads, 0, st>>>(a);
+    else k_tr_conv<2, 4><<<dim3(gx, (Co + 1) / 2), kConvThreads, 0, st>>>(a);
+  } else {
+    const unsigned gx = (unsigned)((npix + kConvThreads - 1) / kConvThreads);
+    if (Co >= 16) k_tr_conv<16, 1><<<dim3(gx, (Co + 15) / 16), kConvThreads, 0, st>>>(a);
+    else if (Co >= 8) k_tr_conv<8, 1><<<dim3(gx, (Co + 7) / 8), kConvThreads, 0, st>>>(a);
+    else if (Co >= 4) k_tr_conv<4, 1><<<dim3(gx, (Co + 3) / 4), kConvThreads, 0, st>>>(a);
+    else k_tr_conv<2, 1><<<dim3(gx, (Co + 1) / 2), kConvThreads, 0, st>>>(a);
+  }
   prof::count(1);
 }
 
 void wgrad_launch(hs_trainer* t, const float* P, int Hp, int Wp, int A, const float* Q, int Hq, int Wq, int Bc, int s,
                   float* out, cudaStream_t st) {
   const long long npix = (long long)t->B * Hp * Wp;
-  const int tiles = ((A + 15) / 16) * ((Bc + 15) / 16);
+  const int AT = A >= 32 ? 32 : 16, BT = Bc >= 32 ? 32 : 16;
+  const int tiles = ((A + AT - 1) / AT) * ((Bc + BT - 1) / BT);
   const long long per = (long long)A * Bc * 9;
-  long long nchunk = (4 * 148 + tiles - 1) / tiles;
-  nchunk = std::min(nchunk, std::max(1LL, npix / 64));
-  nchunk = std::min(nchunk, std::max(1LL, t->wg_part_cap / per));
+  long long nchunk = (3 * 148 + tiles - 1) / tiles;
+  nchunk = std::min(nchunk, std::max(1LL, npix / 256));
+  nchunk = std::min(nchunk, std::max(1LL, t->wg_part_cap / (2 * per)));
   const long long chunk = (npix + nchunk - 1) / nchunk;
   nchunk = (npix + chunk - 1) / chunk;
   TrWgrad g{P, Hp, Wp, A, Q, Hq, Wq, Bc, s, t->B, t->wg_part, chunk};
-  k_tr_wgrad<<<dim3((unsigned)nchunk, (A + 15) / 16, (Bc + 15) / 16), 256, 0, st>>>(g);
-  k_tr_sum_parts<<<g1(per), 256, 0, st>>>(t->wg_part, (int)nchunk, per, out);
-  prof::count(2);
+  const dim3 grid((unsigned)nchunk, (A + AT - 1) / AT, (Bc + BT - 1) / BT);
+  if (AT == 16 && BT == 16) k_tr_wgrad<16, 16><<<grid, 256, 0, st>>>(g);
+  else if (AT == 16) k_tr_wgrad<16, 32><<<grid, 256, 0, st>>>(g);
+  else if (BT == 16) k_tr_wgrad<32, 16><<<grid, 256, 0, st>>>(g);
+  else k_tr_wgrad<32, 32><<<grid, 256, 0, st>>>(g);
+  // deterministic two-stage sum of the chunk partials
+  const int per_grp = 16;
+  const int ngrp = (int)((nchunk + per_grp - 1) / per_grp);
+  float* part2 = t->wg_part + nchunk * per;
+  k_tr_sum_parts1<<<dim3(g1(per), ngrp), 256, 0, st>>>(t->wg_part, (int)nchunk, per_grp, per, part2);
+  k_tr_sum_parts<<<g1(per), 256, 0, st>>>(part2, ngrp, per, out);
+  prof::count(3);
 }
 
 // per-channel reduction + finalisation over an NHWC tensor of M pixels
@@ -739,36 +874,59 @@ void chan_launch(hs_trainer* t, int op, const float* z, const float* gy, long lo
     f.rmean = t->P + p->mean;
     f.rvar = t->P + p->var;
   }
-  k_tr_chan_fin<<<(C + 127) / 128, 128, 0, st>>>(f);
+  k_tr_chan_fin<<<(C + 7) / 8, 256, 0, st>>>(f);
   prof::count(2);
 }
 
-enum Kind { kS1 = 0, kS2 = 1, kT2 = 2 };
 
-// forward convolution of layer p (conv stride 1/2 or transposed stride 2) into y (+ bias, + addend)
+// forward convolution of layer p (conv stride 1/2 or transposed stride 2) into y (+ bias, + addend):
+// the tcgen05 implicit-GEMM kernel (conv_tc.cu, exact bf16x3 split) where the shape has one, else SIMT
 void conv_fwd(hs_trainer* t, const LayerP& p, int kind, const float* x, int Hi, int Wi, float* y, int Ho, int Wo,
               const float* addend, cudaStream_t st) {
   const float* w = t->P + p.w;
+  const int s = kind == kS1 ? 1 : 2, tr = kind == kT2;
+  if (p.wf && conv_tc_supported(p.cin, p.cout, s, tr, Hi, Wi, Wo) &&
+      conv_tc_launch(x, Hi, Wi, p.cin, y, Ho, Wo, p.cout, s, tr, p.wf, t->P + p.b, 0, addend,
+                     (long long)Ho * Wo * p.cout, 0, nullptr, nullptr, nullptr, t->B, st)) {
+    prof::count(1);
+    return;
+  }
   if (kind == kT2)
     conv_launch(x, Hi, Wi, p.cin, y, Ho, Wo, p.cout, w, 9, p.cout * 9, t->P + p.b, addend, 1, 2, 0, t->B, st);
   else
-    conv_launch(x, Hi, Wi, p.cin, y, Ho, Wo, p.cout, w, p.cin * 9, 9, t->P + p.b, addend, 0, kind == kS2 ? 2 : 1, 0,
-                t->B, st);
+    conv_launch(x, Hi, Wi, p.cin, y, Ho, Wo, p.cout, w, p.cin * 9, 9, t->P + p.b, addend, 0, s, 0, t->B, st);
+}
+
+// gx += data gradient: a stride-1 conv with flipped, transposed weights (conv s1), a transposed conv
+// (conv s2) or a stride-2 conv (transposed conv) -- on the tensor cores where the shape allows
+void dgrad(hs_trainer* t, const LayerP& p, int kind, const float* gz, int Ho, int Wo, float* gx, int Hi, int Wi,
+           cudaStream_t st) {
+  const float* w = t->P + p.w;
+  const int s = kind == kS1 ? 1 : 2;
+  // the adjoint's own shape: in = p.cout at (Ho, Wo), out = p.cin at (Hi, Wi); conv s1 -> conv s1,
+  // conv s2 -> transposed conv, transposed conv -> conv s2
+  const int astride = s, atr = kind == kS2;
+  if (p.wd && conv_tc_supported(p.cout, p.cin, astride, atr, Ho, Wo, Wi) &&
+      conv_tc_launch(gz, Ho, Wo, p.cout, gx, Hi, Wi, p.cin, astride, atr, p.wd, t->zero_bias, 0, nullptr, 0, 0,
+                     nullptr, gx, nullptr, t->B, st)) {
+    prof::count(1);
+    return;
+  }
+  if (kind == kT2)
+    conv_launch(gz, Ho, Wo, p.cout, gx, Hi, Wi, p.cin, w, p.cout * 9, 9, nullptr, nullptr, 0, 2, 1, t->B, st);
+  else
+    conv_launch(gz, Ho, Wo, p.cout, gx, Hi, Wi, p.cin, w, 9, p.cin * 9, nullptr, nullptr, 1, s, 1, t->B, st);
 }
 
 // backward of conv_fwd given the complete output gradient gz: weight / bias gradients (+=), gx (+=) if wanted
 void conv_bwd(hs_trainer* t, const LayerP& p, int kind, const float* x, int Hi, int Wi, const float* gz, int Ho,
               int Wo, float* gx, cudaStream_t st) {
-  const float* w = t->P + p.w;
   chan_launch(t, kSum, gz, nullptr, (long long)t->B * Ho * Wo, p.cout, &p, t->G + p.b, nullptr, st);
-  if (kind == kT2) {
+  if (kind == kT2)
     wgrad_launch(t, x, Hi, Wi, p.cin, gz, Ho, Wo, p.cout, 2, t->G + p.w, st);
-    if (gx) conv_launch(gz, Ho, Wo, p.cout, gx, Hi, Wi, p.cin, w, p.cout * 9, 9, nullptr, nullptr, 0, 2, 1, t->B, st);
-  } else {
-    const int s = kind == kS2 ? 2 : 1;
-    wgrad_launch(t, gz, Ho, Wo, p.cout, x, Hi, Wi, p.cin, s, t->G + p.w, st);
-    if (gx) conv_launch(gz, Ho, Wo, p.cout, gx, Hi, Wi, p.cin, w, 9, p.cin * 9, nullptr, nullptr, 1, s, 1, t->B, st);
-  }
+  else
+    wgrad_launch(t, gz, Ho, Wo, p.cout, x, Hi, Wi, p.cin, kind == kS2 ? 2 : 1, t->G + p.w, st);
+  if (gx) dgrad(t, p, kind, gz, Ho, Wo, gx, Hi, Wi, st);
 }
 
 // y = softplus(BN_train(conv(x) + b)) (+ addend); z keeps the pre-BN output
@@ -1041,6 +1199,27 @@ HS_API int hs_trainer_create(hs_trainer_t** out, const hs_train_desc_t* d, const
   t->scr_z = A(maxlev);
   t->s0 = A(256);
   t->s1 = A(256);
+  t->zero_bias = A(256);
+  // tensor-core weight layouts, re-packed from the parameters at the start of every step
+  std::vector<Repack> tab;
+  auto pack = [&](LayerP& p) {
+    if (!ok) return;
+    const size_t n = (size_t)p.cin * p.cout * 9;
+    p.wf = A(n);
+    p.wd = A(n);
+    tab.push_back({t->P + p.w, p.wf, p.cout, p.cin, p.kind == kT2 ? 1 : 0, 0});
+    if (p.kind == kS1) tab.push_back({t->P + p.w, p.wd, p.cin, p.cout, 1, 1});
+    else if (p.kind == kS2) tab.push_back({t->P + p.w, p.wd, p.cin, p.cout, 1, 0});
+    else tab.push_back({t->P + p.w, p.wd, p.cin, p.cout, 0, 0});
+  };
+  pack(t->enc_stem), pack(t->sol_stem), pack(t->head);
+  for (int l = 0; l < L; ++l) pack(t->enc_a[l]), pack(t->enc_b[l]), pack(t->sol_a[l]), pack(t->sol_b[l]);
+  for (int l = 1; l < L; ++l) pack(t->enc_down[l]), pack(t->sol_down[l]), pack(t->up[l]), pack(t->ures_a[l]),
+                              pack(t->ures_b[l]);
+  t->n_repack = (int)tab.size();
+  t->repack = dalloc<Repack>(t, tab.size());
+  ok = ok && t->repack;
+  if (ok) cudaMemcpy(t->repack, tab.data(), tab.size() * sizeof(Repack), cudaMemcpyHostToDevice);
   // batch statistics per BN layer
   auto stat = [&](LayerP& p) {
     if (!p.bn) return;
@@ -1086,6 +1265,7 @@ HS_API int hs_trainer_create(hs_trainer_t** out, const hs_train_desc_t* d, const
   cudaMemsetAsync(t->M, 0, t->nparam * sizeof(float), st);
   cudaMemsetAsync(t->V, 0, t->nparam * sizeof(float), st);
   cudaMemsetAsync(t->G, 0, t->nparam * sizeof(float), st);
+  cudaMemsetAsync(t->zero_bias, 0, 256 * sizeof(float), st);
   if (cudaStreamSynchronize(st) != cudaSuccess) {
     delete t;
     return tfail(HS_ECUDA, cudaGetErrorString(cudaGetLastError()));
@@ -1109,7 +1289,8 @@ HS_API int hs_trainer_step(hs_trainer_t* t, const float* media, int n_models, co
   const long long np = (long long)B * t->ix * t->iy;
   k_tr_media<<<g1(np * 2), 256, 0, st>>>(media, t->model_dev, t->media_b, B, t->ix, t->iy);
   k_tr_r2<<<g1(np), 256, 0, st>>>(static_cast<const double2*>(r), t->r2, B, t->d.nx, t->d.ny, t->ix, t->iy);
-  prof::count(2);
+  k_tr_repack<<<dim3(64, t->n_repack), 256, 0, st>>>(t->repack);
+  prof::count(3);
   int rc = green_fwd(t, st);
   if (!rc) rc = forward(t, st);
   if (rc) return tfail(rc, "training forward");
