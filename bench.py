@@ -315,6 +315,160 @@ def run_datagen(args):
     return 0
 
 
+TR_METRIC = "network training samples/sec (257x257, C2 network 16/32/64, batch 16: forward + MSE + backward + Adam)"
+TR_UNIT = "samples/s"
+FP32_SIMT_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # derived: SMs x FP32 FMA/clk x 2 x max SM clock
+
+
+def train_cpu(workers: int):
+    """Oracle training step (float64 numpy) on the host cores: samples/s, one process per core, batch 1 each."""
+    from multiprocessing import get_context
+
+    t0 = time.perf_counter()
+    with get_context("fork").Pool(workers) as pool:
+        pool.map(_tr_worker, range(workers))
+    el = time.perf_counter() - t0
+    return workers / el, (f"{workers} processes x 1 sample (a batch-1 step each: forward with training batch norm, "
+                          f"MSE, backward, Adam), 257x257, numpy oracle (oracle/train_oracle.py), single-threaded BLAS")
+
+
+def _tr_worker(i):
+    from threadpoolctl import threadpool_limits
+
+    threadpool_limits(1)
+    from oracle import train_oracle as to
+    from paper_2306_17486_b200 import netparams
+    from paper_2306_17486_b200 import train as tr
+
+    models = datagen_models()
+    rng = np.random.default_rng(500 + i)
+    n = models[0].shape
+    params = to.as_float64(netparams.init_params((16, 32, 64), 0))
+    media = tr.media_planes(models, 3)[[i % 4]].astype(np.float64)
+    r = rng.standard_normal((1,) + n) + 1j * rng.standard_normal((1,) + n)
+    e = rng.standard_normal((1,) + n) + 1j * rng.standard_normal((1,) + n)
+    to.train_step(params, 3, media, r, e, models[0].h, to.Adam(params))
+    return 0
+
+
+def run_train(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    B = args.train_batch
+    cfg = {"workload": f"train: C2's 4 models (gamma0 0.05), 257x257 grid, network 16/32/64 (3 levels, implicit "
+                       f"layer at 64x64), batch {B} datagen pairs (r, e) per step, training-mode batch norm, "
+                       f"MSE of u0 = (h^2/64) net(r) vs e, backward, Adam lr 1e-3",
+           "global_batch_per_gpu": B, "parallelism": "replicas only (independent trainer per rank, no gradient "
+                                                      "all-reduce; see DESIGN.md)",
+           "l2": "per-step working set (saved activations ~1.3 GB) far larger than L2"}
+    workers = args.cpu_workers or (os.cpu_count() or 1)
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        t0 = time.perf_counter()
+        vals = [train_cpu(workers)[0] for _ in range(args.warmup + args.steps)][args.warmup:]
+        value = float(np.mean(vals))
+        desc = train_cpu(workers)[1]
+        print(json.dumps({
+            "impl": "reference", "metric": TR_METRIC, "value": value, "unit": TR_UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * (time.perf_counter() - t0) / (args.steps + args.warmup + 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (numpy oracle)",
+            "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": value, "unit": TR_UNIT, "cores": workers, "kind": "port", "sample": desc},
+            "e2e": {"value": value, "unit": TR_UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
+        return 0
+
+    import torch
+
+    world, rank, local = dist_setup()
+    from paper_2306_17486_b200 import _lib, datagen, network
+    from paper_2306_17486_b200 import dist as hdist
+    from paper_2306_17486_b200 import train as tr
+
+    models = datagen_models(rank)
+    gen = datagen.PairGenerator(models)
+    n = models[0].shape
+    rng = np.random.default_rng(77 + rank)
+    pool = 4 * B
+    d = [datagen._draw(rng, n) for _ in range(pool)]
+    owner = np.arange(pool) % len(models)
+    r, e = gen.pairs(np.stack([t[0] for t in d]), [t[1] for t in d], owner, return_device=True)
+    media = torch.from_numpy(tr.media_planes(models, 3)).cuda()
+    net = network.EncoderSolverNet.seeded((16, 32, 64), seed=0)
+    trainer = tr.Trainer(net, n, models[0].h, B, lr=1e-3)
+    batches = [np.arange(s * B, (s + 1) * B) % pool for s in range(args.warmup + args.steps)]
+    bsel = [torch.from_numpy(b).cuda() for b in batches]
+    rb = [r.index_select(0, b).contiguous() for b in bsel]
+    eb = [e.index_select(0, b).contiguous() for b in bsel]
+    for i in range(args.warmup):
+        trainer.step(media, rb[i], eb[i], owner[batches[i]])
+    lib = _lib.load()
+    tags = [_lib.PROF_CONV, _lib.PROF_TRAIN_WGRAD]
+    lib.hs_profile_reset()
+    stream = torch.cuda.current_stream()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    losses = []
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for i in range(args.warmup, args.warmup + args.steps):
+            losses.append(trainer.step(media, rb[i], eb[i], owner[batches[i]]))
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = hdist.reduce_scalar(ev0.elapsed_time(ev1), "max")
+    launches = int(lib.hs_launch_count())
+    value = world * B * args.steps / (ms / 1e3)
+    # kernel shares, separate profiled pass (CUDA events around each tagged launch)
+    lib.hs_profile_enable(sum(1 << t for t in tags))
+    lib.hs_profile_reset()
+    for i in range(args.warmup, args.warmup + args.steps):
+        trainer.step(media, rb[i], eb[i], owner[batches[i]])
+    torch.cuda.synchronize()
+    prof = {t: _lib.profile_query(t) for t in tags}
+    lib.hs_profile_enable(0)
+    e2e = None
+    if not args.no_e2e:
+        rpin = [rb[i].cpu().pin_memory() for i in range(args.warmup, args.warmup + args.steps)]
+        epin = [eb[i].cpu().pin_memory() for i in range(args.warmup, args.warmup + args.steps)]
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for j, i in enumerate(range(args.warmup, args.warmup + args.steps)):
+            trainer.step(media, rpin[j], epin[j], owner[batches[i]])
+        el = hdist.reduce_scalar(time.perf_counter() - t0, "max")
+        e2e = {"value": world * B * args.steps / el, "unit": TR_UNIT,
+               "h2d_bytes_per_step": int(rpin[0].numel() * 16 * 2), "d2h_bytes_per_step": 8}
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+    w_ms, w_flops, w_n = prof[_lib.PROF_TRAIN_WGRAD]
+    c_ms, c_flops, c_n = prof[_lib.PROF_CONV]
+    ach = w_flops / (w_ms / 1e3) / 1e12 if w_ms > 0 else 0.0
+    roof = {"kernel": "k_tr_wgrad (+ its partial sums): weight gradients, the largest share of the step",
+            "bound": "fp32-simt", "achieved": ach, "peak": FP32_SIMT_TFLOPS, "unit": "TFLOP/s",
+            "frac": ach / FP32_SIMT_TFLOPS, "peak_note": "derived 148 SM x 128 FMA/clk x 2 x 1.965 GHz (no tensor cores)",
+            "launches": w_n, "ms_total": w_ms, "share_of_step": w_ms / ms,
+            "conv_ms_total": c_ms, "conv_tflops": c_flops / (c_ms / 1e3) / 1e12 if c_ms > 0 else 0.0,
+            "traffic": None}
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        v, desc = train_cpu(workers)
+        cpu = {"value": v, "unit": TR_UNIT, "cores": workers, "kind": "port", "sample": desc}
+    print(json.dumps({
+        "metric": TR_METRIC, "value": value, "unit": TR_UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp32 (tcgen05 convs: exact bf16x3 split, fp32 accumulate)",
+        "data": "synthetic (seeded datagen pairs, seeded init)", "config": cfg,
+        "loss_first_last": [losses[0], losses[-1]], "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches, "clocks": clk.summary()}), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -328,12 +482,16 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="solve", choices=["solve", "datagen"],
-                    help="solve: the BASELINE metric (default); datagen: SURVEY 8f row 1, training pairs")
+    ap.add_argument("--workload", default="solve", choices=["solve", "datagen", "train"],
+                    help="solve: the BASELINE metric (default); datagen: SURVEY 8f row 1, training pairs; "
+                         "train: SURVEY 8f row 2, network training steps")
+    ap.add_argument("--train-batch", type=int, default=16, help="train: samples per step")
     ap.add_argument("--samples", type=int, default=256, help="datagen: samples per step")
     args = ap.parse_args()
     if args.workload == "datagen":
         return run_datagen(args)
+    if args.workload == "train":
+        return run_train(args)
     if args.impl == "reference":
         return run_reference(args)
 

@@ -180,7 +180,7 @@ def load():
         return _lib
 
 
-PROF_CONV, PROF_CONV_L0, PROF_VCYCLE, PROF_ARNOLDI, PROF_CNN, PROF_IMPLICIT, PROF_VC_UP0 = range(7)
+PROF_CONV, PROF_CONV_L0, PROF_VCYCLE, PROF_ARNOLDI, PROF_CNN, PROF_IMPLICIT, PROF_VC_UP0, PROF_TRAIN_WGRAD = range(8)
 
 
 def profile_query(tag: int):

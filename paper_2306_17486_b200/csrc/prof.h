@@ -19,6 +19,7 @@ enum Tag {
   CNN = 4,        // one whole network forward
   IMPLICIT = 5,   // implicit layer
   VC_UP0 = 6,     // finest-level up-leg kernel (work = algorithmic bytes)
+  TRAIN_WGRAD = 7,  // training weight-gradient reductions (work = flops)
   NTAGS = 8
 };
 

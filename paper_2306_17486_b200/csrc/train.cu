@@ -172,78 +172,95 @@ struct TrWgrad {
   long long chunk;
 };
 
-// Tile AT x BT of (a, b) pairs x 9 taps; a thread owns 4 consecutive a for one b (36 accumulators:
-// one 16-byte P read + 9 Q reads per 36 FMAs).  The 256 threads form KS = 256 / (AT BT / 4) groups that
-// take interleaved 16-pixel slices of the block's chunk (split-K inside the block), folded in shared
-// memory at the end in group order.
+// Tile AT x BT of (a, b) pairs x 9 taps; a thread owns 4 consecutive a for one b (36 accumulators).
+// The 256 threads form KS = 256 / (AT BT / 4) groups that take interleaved 16-pixel slices of each
+// staged row segment (split-K inside the block), folded in shared memory at the end in group order.
 constexpr int kWgPx = 16;
 constexpr int kWgSmem = 10240;  // floats of staging
 
-template <int AT, int BT>
-__global__ void __launch_bounds__(256, 2) k_tr_wgrad(TrWgrad g) {
-  constexpr int TPG = AT * BT / 4;  // threads per group
+// A block owns whole P rows; each round stages one SP-pixel row segment of P
+// and the three Q rows it touches (s (SP - 1) + 3 columns) once, instead of 9 taps per pixel.  With
+// stride 1 a thread slides a 3-column register window along the row (3 Q reads per pixel).
+template <int AT, int BT, int S>
+__global__ void __launch_bounds__(256, 2) k_tr_wgrad_rows(TrWgrad g) {
+  constexpr int TPG = AT * BT / 4;
   constexpr int KS = 256 / TPG;
-  constexpr int SP = KS * kWgPx;  // pixels staged per round
-  static_assert(SP * AT + SP * 9 * BT <= kWgSmem, "staging");
+  constexpr int SP = KS * kWgPx;
+  constexpr int QC = S * (SP - 1) + 3;
   __shared__ __align__(16) float sm[kWgSmem];
-  __shared__ int4 pc[SP];
-  float* ps = sm;                // [SP][AT]
-  float* qs = sm + SP * AT;      // [SP][9][BT]
+  float* ps = sm;             // [SP][AT]
+  float* qs = sm + SP * AT;   // [3][QC][BT]
+  static_assert(SP * AT + 3 * QC * BT <= kWgSmem, "staging");
   const int a0 = blockIdx.y * AT, b0 = blockIdx.z * BT;
   const int grp = threadIdx.x / TPG, lt = threadIdx.x % TPG;
   const int tb = lt % BT, ag = lt / BT;
-  const long long plane = (long long)g.Hp * g.Wp;
-  const long long npix = (long long)g.B * plane;
-  const long long p0 = blockIdx.x * g.chunk, p1 = min(npix, p0 + g.chunk);
+  const long long nrows = (long long)g.B * g.Hp;
+  const long long r0 = blockIdx.x * g.chunk, r1 = min(nrows, r0 + g.chunk);
   float acc[4][9];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int t = 0; t < 9; ++t) acc[i][t] = 0.f;
-  for (long long pb = p0; pb < p1; pb += SP) {
-    __syncthreads();
-    if (threadIdx.x < SP) {
-      const long long p = pb + threadIdx.x;
-      int4 c = make_int4(-1, 0, 0, 0);
-      if (p < p1) {
-        const int n = (int)(p / plane);
-        const int rem = (int)(p - n * plane);
-        c = make_int4(n, rem / g.Wp, rem % g.Wp, 0);
+  for (long long row = r0; row < r1; ++row) {
+    const int n = (int)(row / g.Hp), oy = (int)(row % g.Hp);
+    for (int x0 = 0; x0 < g.Wp; x0 += SP) {
+      const int npx = min(SP, g.Wp - x0);
+      __syncthreads();
+      for (int i = threadIdx.x; i < SP * AT; i += 256) {
+        const int px = i / AT, ai = i % AT;
+        ps[i] = (px < npx && a0 + ai < g.A) ? g.P[(row * g.Wp + x0 + px) * g.A + a0 + ai] : 0.f;
       }
-      pc[threadIdx.x] = c;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < SP * AT; i += 256) {
-      const int px = i / AT, ai = i % AT;
-      ps[i] = (pc[px].x >= 0 && a0 + ai < g.A) ? g.P[(pb + px) * g.A + a0 + ai] : 0.f;
-    }
-    for (int i = threadIdx.x; i < SP * 9 * BT; i += 256) {
-      const int bi = i % BT, t = (i / BT) % 9, px = i / (9 * BT);
-      const int4 c = pc[px];
-      float v = 0.f;
-      if (c.x >= 0 && b0 + bi < g.Bc) {
-        const int qy = g.s * c.y + t / 3 - 1, qx = g.s * c.z + t % 3 - 1;
-        if (qy >= 0 && qy < g.Hq && qx >= 0 && qx < g.Wq)
-          v = g.Q[(((long long)c.x * g.Hq + qy) * g.Wq + qx) * g.Bc + b0 + bi];
+      for (int i = threadIdx.x; i < 3 * QC * BT; i += 256) {
+        const int bi = i % BT, j = (i / BT) % QC, u = i / (QC * BT);
+        const int qy = S * oy + u - 1, qx = S * x0 - 1 + j;
+        float v = 0.f;
+        if (j < S * (npx - 1) + 3 && qy >= 0 && qy < g.Hq && qx >= 0 && qx < g.Wq && b0 + bi < g.Bc)
+          v = g.Q[(((long long)n * g.Hq + qy) * g.Wq + qx) * g.Bc + b0 + bi];
+        qs[i] = v;
       }
-      qs[i] = v;
-    }
-    __syncthreads();
-#pragma unroll 2
-    for (int k = 0; k < kWgPx; ++k) {
-      const int px = grp * kWgPx + k;
-      const float4 pa = *reinterpret_cast<const float4*>(ps + px * AT + 4 * ag);
+      __syncthreads();
+      const int pb = grp * kWgPx;
+      if (S == 1) {
+        float wa[3], wb[3];
 #pragma unroll
-      for (int t = 0; t < 9; ++t) {
-        const float q = qs[(px * 9 + t) * BT + tb];
-        acc[0][t] = fmaf(pa.x, q, acc[0][t]);
-        acc[1][t] = fmaf(pa.y, q, acc[1][t]);
-        acc[2][t] = fmaf(pa.z, q, acc[2][t]);
-        acc[3][t] = fmaf(pa.w, q, acc[3][t]);
+        for (int u = 0; u < 3; ++u) {
+          wa[u] = qs[(u * QC + pb) * BT + tb];
+          wb[u] = qs[(u * QC + pb + 1) * BT + tb];
+        }
+#pragma unroll 4
+        for (int k = 0; k < kWgPx; ++k) {
+          const float4 pa = *reinterpret_cast<const float4*>(ps + (pb + k) * AT + 4 * ag);
+#pragma unroll
+          for (int u = 0; u < 3; ++u) {
+            const float wc = qs[(u * QC + pb + k + 2) * BT + tb];
+            const float q3[3] = {wa[u], wb[u], wc};
+#pragma unroll
+            for (int v = 0; v < 3; ++v) {
+              acc[0][u * 3 + v] = fmaf(pa.x, q3[v], acc[0][u * 3 + v]);
+              acc[1][u * 3 + v] = fmaf(pa.y, q3[v], acc[1][u * 3 + v]);
+              acc[2][u * 3 + v] = fmaf(pa.z, q3[v], acc[2][u * 3 + v]);
+              acc[3][u * 3 + v] = fmaf(pa.w, q3[v], acc[3][u * 3 + v]);
+            }
+            wa[u] = wb[u];
+            wb[u] = wc;
+          }
+        }
+      } else {
+#pragma unroll 2
+        for (int k = 0; k < kWgPx; ++k) {
+          const float4 pa = *reinterpret_cast<const float4*>(ps + (pb + k) * AT + 4 * ag);
+#pragma unroll
+          for (int t = 0; t < 9; ++t) {
+            const float q = qs[((t / 3) * QC + S * (pb + k) + t % 3) * BT + tb];
+            acc[0][t] = fmaf(pa.x, q, acc[0][t]);
+            acc[1][t] = fmaf(pa.y, q, acc[1][t]);
+            acc[2][t] = fmaf(pa.z, q, acc[2][t]);
+            acc[3][t] = fmaf(pa.w, q, acc[3][t]);
+          }
+        }
       }
     }
   }
-  // fold the KS groups in order
   __syncthreads();
   if (grp > 0) {
 #pragma unroll
@@ -828,27 +845,35 @@ void conv_launch(const float* x, int Hi, int Wi, int Ci, float* y, int Ho, int W
 
 void wgrad_launch(hs_trainer* t, const float* P, int Hp, int Wp, int A, const float* Q, int Hq, int Wq, int Bc, int s,
                   float* out, cudaStream_t st) {
-  const long long npix = (long long)t->B * Hp * Wp;
+  const long long nrows = (long long)t->B * Hp;
   const int AT = A >= 32 ? 32 : 16, BT = Bc >= 32 ? 32 : 16;
   const int tiles = ((A + AT - 1) / AT) * ((Bc + BT - 1) / BT);
   const long long per = (long long)A * Bc * 9;
   long long nchunk = (3 * 148 + tiles - 1) / tiles;
-  nchunk = std::min(nchunk, std::max(1LL, npix / 256));
+  nchunk = std::min(nchunk, nrows);
   nchunk = std::min(nchunk, std::max(1LL, t->wg_part_cap / (2 * per)));
-  const long long chunk = (npix + nchunk - 1) / nchunk;
-  nchunk = (npix + chunk - 1) / chunk;
+  const long long chunk = (nrows + nchunk - 1) / nchunk;  // rows per block
+  nchunk = (nrows + chunk - 1) / chunk;
   TrWgrad g{P, Hp, Wp, A, Q, Hq, Wq, Bc, s, t->B, t->wg_part, chunk};
+  const int slot = prof::start(prof::TRAIN_WGRAD, st);
   const dim3 grid((unsigned)nchunk, (A + AT - 1) / AT, (Bc + BT - 1) / BT);
-  if (AT == 16 && BT == 16) k_tr_wgrad<16, 16><<<grid, 256, 0, st>>>(g);
-  else if (AT == 16) k_tr_wgrad<16, 32><<<grid, 256, 0, st>>>(g);
-  else if (BT == 16) k_tr_wgrad<32, 16><<<grid, 256, 0, st>>>(g);
-  else k_tr_wgrad<32, 32><<<grid, 256, 0, st>>>(g);
+#define HS_WG(ATV, BTV)                                                          \
+  if (AT == ATV && BT == BTV) {                                                  \
+    if (s == 1) k_tr_wgrad_rows<ATV, BTV, 1><<<grid, 256, 0, st>>>(g);           \
+    else k_tr_wgrad_rows<ATV, BTV, 2><<<grid, 256, 0, st>>>(g);                  \
+  }
+  HS_WG(16, 16)
+  HS_WG(16, 32)
+  HS_WG(32, 16)
+  HS_WG(32, 32)
+#undef HS_WG
   // deterministic two-stage sum of the chunk partials
   const int per_grp = 16;
   const int ngrp = (int)((nchunk + per_grp - 1) / per_grp);
   float* part2 = t->wg_part + nchunk * per;
   k_tr_sum_parts1<<<dim3(g1(per), ngrp), 256, 0, st>>>(t->wg_part, (int)nchunk, per_grp, per, part2);
   k_tr_sum_parts<<<g1(per), 256, 0, st>>>(part2, ngrp, per, out);
+  prof::stop(slot, st, 18.0 * (double)nrows * Wp * A * Bc);
   prof::count(3);
 }
 
@@ -885,6 +910,13 @@ void conv_fwd(hs_trainer* t, const LayerP& p, int kind, const float* x, int Hi, 
               const float* addend, cudaStream_t st) {
   const float* w = t->P + p.w;
   const int s = kind == kS1 ? 1 : 2, tr = kind == kT2;
+  const double flops = 18.0 * t->B * (tr ? (double)Hi * Wi : (double)Ho * Wo) * p.cin * p.cout;
+  struct Scope {
+    int slot;
+    cudaStream_t st;
+    double w;
+    ~Scope() { prof::stop(slot, st, w); }
+  } scope{prof::start(prof::CONV, st), st, flops};
   if (p.wf && conv_tc_supported(p.cin, p.cout, s, tr, Hi, Wi, Wo) &&
       conv_tc_launch(x, Hi, Wi, p.cin, y, Ho, Wo, p.cout, s, tr, p.wf, t->P + p.b, 0, addend,
                      (long long)Ho * Wo * p.cout, 0, nullptr, nullptr, nullptr, t->B, st)) {
@@ -903,6 +935,13 @@ void dgrad(hs_trainer* t, const LayerP& p, int kind, const float* gz, int Ho, in
            cudaStream_t st) {
   const float* w = t->P + p.w;
   const int s = kind == kS1 ? 1 : 2;
+  const double flops = 18.0 * t->B * (kind == kT2 ? (double)Hi * Wi : (double)Ho * Wo) * p.cin * p.cout;
+  struct Scope {
+    int slot;
+    cudaStream_t st;
+    double w;
+    ~Scope() { prof::stop(slot, st, w); }
+  } scope{prof::start(prof::CONV, st), st, flops};
   // the adjoint's own shape: in = p.cout at (Ho, Wo), out = p.cin at (Hi, Wi); conv s1 -> conv s1,
   // conv s2 -> transposed conv, transposed conv -> conv s2
   const int astride = s, atr = kind == kS2;
