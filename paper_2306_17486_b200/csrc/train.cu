@@ -181,44 +181,76 @@ constexpr int kWgSmem = 10240;  // floats of staging
 // A block owns whole P rows; each round stages one SP-pixel row segment of P
 // and the three Q rows it touches (s (SP - 1) + 3 columns) once, instead of 9 taps per pixel.  With
 // stride 1 a thread slides a 3-column register window along the row (3 Q reads per pixel).
+HS_DEV void cp_async4(float* dst, const float* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int n = valid ? 4 : 0;  // src-size 0: the 4 bytes are zero-filled
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(n) : "memory");
+}
+HS_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+HS_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int AT, int BT, int S>
+struct WgCfg {
+  static constexpr int TPG = AT * BT / 4;
+  static constexpr int KS = 256 / TPG;
+  static constexpr int SP = KS * kWgPx;
+  static constexpr int QC = S * (SP - 1) + 3;
+  static constexpr int STAGE = SP * AT + 3 * QC * BT;  // floats per buffer
+  static constexpr int SMEM = 2 * STAGE * 4;           // double-buffered, bytes
+};
+
+// Rounds (row, SP-pixel segment) are staged with cp.async into two alternating buffers, so the
+// next round's loads overlap this round's FMAs.
 template <int AT, int BT, int S>
 __global__ void __launch_bounds__(256, 2) k_tr_wgrad_rows(TrWgrad g) {
-  constexpr int TPG = AT * BT / 4;
-  constexpr int KS = 256 / TPG;
-  constexpr int SP = KS * kWgPx;
-  constexpr int QC = S * (SP - 1) + 3;
-  __shared__ __align__(16) float sm[kWgSmem];
-  float* ps = sm;             // [SP][AT]
-  float* qs = sm + SP * AT;   // [3][QC][BT]
-  static_assert(SP * AT + 3 * QC * BT <= kWgSmem, "staging");
+  using C = WgCfg<AT, BT, S>;
+  constexpr int TPG = C::TPG, KS = C::KS, SP = C::SP, QC = C::QC;
+  extern __shared__ __align__(16) float sm[];
   const int a0 = blockIdx.y * AT, b0 = blockIdx.z * BT;
   const int grp = threadIdx.x / TPG, lt = threadIdx.x % TPG;
   const int tb = lt % BT, ag = lt / BT;
   const long long nrows = (long long)g.B * g.Hp;
   const long long r0 = blockIdx.x * g.chunk, r1 = min(nrows, r0 + g.chunk);
+  const int nseg = (g.Wp + SP - 1) / SP;
+  const long long nround = (r1 > r0 ? r1 - r0 : 0) * nseg;
+  auto issue = [&](long long k) {
+    float* ps = sm + (k & 1) * C::STAGE;
+    float* qs = ps + SP * AT;
+    const long long row = r0 + k / nseg;
+    const int x0 = (int)(k % nseg) * SP;
+    const int npx = min(SP, g.Wp - x0);
+    const int n = (int)(row / g.Hp), oy = (int)(row % g.Hp);
+    for (int i = threadIdx.x; i < SP * AT; i += 256) {
+      const int px = i / AT, ai = i % AT;
+      const bool ok = px < npx && a0 + ai < g.A;
+      cp_async4(ps + i, ok ? g.P + (row * g.Wp + x0 + px) * g.A + a0 + ai : g.P, ok);
+    }
+    for (int i = threadIdx.x; i < 3 * QC * BT; i += 256) {
+      const int bi = i % BT, j = (i / BT) % QC, u = i / (QC * BT);
+      const int qy = S * oy + u - 1, qx = S * x0 - 1 + j;
+      const bool ok = j < S * (npx - 1) + 3 && qy >= 0 && qy < g.Hq && qx >= 0 && qx < g.Wq && b0 + bi < g.Bc;
+      cp_async4(qs + i, ok ? g.Q + (((long long)n * g.Hq + qy) * g.Wq + qx) * g.Bc + b0 + bi : g.Q, ok);
+    }
+    cp_async_commit();
+  };
   float acc[4][9];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int t = 0; t < 9; ++t) acc[i][t] = 0.f;
-  for (long long row = r0; row < r1; ++row) {
-    const int n = (int)(row / g.Hp), oy = (int)(row % g.Hp);
-    for (int x0 = 0; x0 < g.Wp; x0 += SP) {
-      const int npx = min(SP, g.Wp - x0);
-      __syncthreads();
-      for (int i = threadIdx.x; i < SP * AT; i += 256) {
-        const int px = i / AT, ai = i % AT;
-        ps[i] = (px < npx && a0 + ai < g.A) ? g.P[(row * g.Wp + x0 + px) * g.A + a0 + ai] : 0.f;
-      }
-      for (int i = threadIdx.x; i < 3 * QC * BT; i += 256) {
-        const int bi = i % BT, j = (i / BT) % QC, u = i / (QC * BT);
-        const int qy = S * oy + u - 1, qx = S * x0 - 1 + j;
-        float v = 0.f;
-        if (j < S * (npx - 1) + 3 && qy >= 0 && qy < g.Hq && qx >= 0 && qx < g.Wq && b0 + bi < g.Bc)
-          v = g.Q[(((long long)n * g.Hq + qy) * g.Wq + qx) * g.Bc + b0 + bi];
-        qs[i] = v;
-      }
-      __syncthreads();
+  if (nround > 0) issue(0);
+  for (long long k = 0; k < nround; ++k) {
+    if (k + 1 < nround) {
+      issue(k + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    {
+      const float* ps = sm + (k & 1) * C::STAGE;
+      const float* qs = ps + SP * AT;
       const int pb = grp * kWgPx;
       if (S == 1) {
         float wa[3], wb[3];
@@ -228,11 +260,11 @@ __global__ void __launch_bounds__(256, 2) k_tr_wgrad_rows(TrWgrad g) {
           wb[u] = qs[(u * QC + pb + 1) * BT + tb];
         }
 #pragma unroll 4
-        for (int k = 0; k < kWgPx; ++k) {
-          const float4 pa = *reinterpret_cast<const float4*>(ps + (pb + k) * AT + 4 * ag);
+        for (int kk = 0; kk < kWgPx; ++kk) {
+          const float4 pa = *reinterpret_cast<const float4*>(ps + (pb + kk) * AT + 4 * ag);
 #pragma unroll
           for (int u = 0; u < 3; ++u) {
-            const float wc = qs[(u * QC + pb + k + 2) * BT + tb];
+            const float wc = qs[(u * QC + pb + kk + 2) * BT + tb];
             const float q3[3] = {wa[u], wb[u], wc};
 #pragma unroll
             for (int v = 0; v < 3; ++v) {
@@ -247,11 +279,11 @@ __global__ void __launch_bounds__(256, 2) k_tr_wgrad_rows(TrWgrad g) {
         }
       } else {
 #pragma unroll 2
-        for (int k = 0; k < kWgPx; ++k) {
-          const float4 pa = *reinterpret_cast<const float4*>(ps + (pb + k) * AT + 4 * ag);
+        for (int kk = 0; kk < kWgPx; ++kk) {
+          const float4 pa = *reinterpret_cast<const float4*>(ps + (pb + kk) * AT + 4 * ag);
 #pragma unroll
           for (int t = 0; t < 9; ++t) {
-            const float q = qs[((t / 3) * QC + S * (pb + k) + t % 3) * BT + tb];
+            const float q = qs[((t / 3) * QC + S * (pb + kk) + t % 3) * BT + tb];
             acc[0][t] = fmaf(pa.x, q, acc[0][t]);
             acc[1][t] = fmaf(pa.y, q, acc[1][t]);
             acc[2][t] = fmaf(pa.z, q, acc[2][t]);
@@ -260,6 +292,7 @@ __global__ void __launch_bounds__(256, 2) k_tr_wgrad_rows(TrWgrad g) {
         }
       }
     }
+    __syncthreads();  // this buffer is re-filled by round k + 2's issue
   }
   __syncthreads();
   if (grp > 0) {
@@ -843,6 +876,17 @@ void conv_launch(const float* x, int Hi, int Wi, int Ci, float* y, int Ho, int W
   prof::count(1);
 }
 
+template <int AT, int BT, int S>
+void launch_wg(dim3 grid, const TrWgrad& g, cudaStream_t st) {
+  using C = WgCfg<AT, BT, S>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_tr_wgrad_rows<AT, BT, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr = true;
+  }
+  k_tr_wgrad_rows<AT, BT, S><<<grid, 256, C::SMEM, st>>>(g);
+}
+
 void wgrad_launch(hs_trainer* t, const float* P, int Hp, int Wp, int A, const float* Q, int Hq, int Wq, int Bc, int s,
                   float* out, cudaStream_t st) {
   const long long nrows = (long long)t->B * Hp;
@@ -857,10 +901,10 @@ void wgrad_launch(hs_trainer* t, const float* P, int Hp, int Wp, int A, const fl
   TrWgrad g{P, Hp, Wp, A, Q, Hq, Wq, Bc, s, t->B, t->wg_part, chunk};
   const int slot = prof::start(prof::TRAIN_WGRAD, st);
   const dim3 grid((unsigned)nchunk, (A + AT - 1) / AT, (Bc + BT - 1) / BT);
-#define HS_WG(ATV, BTV)                                                          \
-  if (AT == ATV && BT == BTV) {                                                  \
-    if (s == 1) k_tr_wgrad_rows<ATV, BTV, 1><<<grid, 256, 0, st>>>(g);           \
-    else k_tr_wgrad_rows<ATV, BTV, 2><<<grid, 256, 0, st>>>(g);                  \
+#define HS_WG(ATV, BTV)                                                                       \
+  if (AT == ATV && BT == BTV) {                                                               \
+    if (s == 1) launch_wg<ATV, BTV, 1>(grid, g, st);                                          \
+    else launch_wg<ATV, BTV, 2>(grid, g, st);                                                 \
   }
   HS_WG(16, 16)
   HS_WG(16, 32)
