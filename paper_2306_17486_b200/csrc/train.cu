@@ -22,6 +22,7 @@
 #include <cufft.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <vector>
 
@@ -129,15 +130,35 @@ __global__ void __launch_bounds__(kConvThreads) k_tr_conv(TrConv a) {
         const float* px[PX];
 #pragma unroll
         for (int j = 0; j < PX; ++j) px[j] = ix[j][v] >= 0 ? row + (long long)ix[j][v] * a.Ci : nullptr;
-        for (int c = 0; c < ck; ++c) {
-          float xv[PX];
+        if ((a.Ci & 3) == 0) {  // 16-byte input loads, 4 channels at a time
+          for (int c = 0; c < ck; c += 4) {
+            float4 x4[PX];
 #pragma unroll
-          for (int j = 0; j < PX; ++j) xv[j] = px[j] ? __ldg(px[j] + c) : 0.f;
+            for (int j = 0; j < PX; ++j)
+              x4[j] = px[j] ? __ldg(reinterpret_cast<const float4*>(px[j] + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-          for (int k = 0; k < COB; ++k) {
-            const float wk = ws[t][c][k];
+            for (int cc = 0; cc < 4; ++cc)
 #pragma unroll
-            for (int j = 0; j < PX; ++j) acc[j][k] = fmaf(xv[j], wk, acc[j][k]);
+              for (int k = 0; k < COB; ++k) {
+                const float wk = ws[t][c + cc][k];
+#pragma unroll
+                for (int j = 0; j < PX; ++j) {
+                  const float xv = cc == 0 ? x4[j].x : cc == 1 ? x4[j].y : cc == 2 ? x4[j].z : x4[j].w;
+                  acc[j][k] = fmaf(xv, wk, acc[j][k]);
+                }
+              }
+          }
+        } else {
+          for (int c = 0; c < ck; ++c) {
+            float xv[PX];
+#pragma unroll
+            for (int j = 0; j < PX; ++j) xv[j] = px[j] ? __ldg(px[j] + c) : 0.f;
+#pragma unroll
+            for (int k = 0; k < COB; ++k) {
+              const float wk = ws[t][c][k];
+#pragma unroll
+              for (int j = 0; j < PX; ++j) acc[j][k] = fmaf(xv[j], wk, acc[j][k]);
+            }
           }
         }
       }
@@ -361,44 +382,69 @@ struct TrChan {
 
 HS_DEV float sigmoidf_(float a) { return 1.f / (1.f + __expf(-a)); }
 
+// V consecutive channels per thread (float4 loads when C % 4 == 0), pixel lanes strided; double sums
+template <int OP, int V>
 __global__ void __launch_bounds__(256) k_tr_chan(TrChan a) {
-  __shared__ double sm[2][256];
-  const int lanes = 256 / a.C;
-  const int c = threadIdx.x % a.C, lane = threadIdx.x / a.C;
-  double q0 = 0.0, q1 = 0.0;
+  using VT = typename std::conditional<V == 4, float4, float>::type;
+  __shared__ double sm[2][V][256];
+  const int G = a.C / V;  // channel groups
+  const int lanes = 256 / G;
+  const int cg = threadIdx.x % G, lane = threadIdx.x / G;
+  double q0[V], q1[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) q0[v] = q1[v] = 0.0;
   if (lane < lanes) {
     const long long p0 = blockIdx.x * a.chunk, p1 = min(a.M, p0 + a.chunk);
-    float mu = 0.f, iv = 0.f, gm = 0.f, bt = 0.f;
-    if (a.op == kBnBwd) {
-      mu = a.mean[c];
-      iv = a.inv[c];
-      gm = a.gamma[c];
-      bt = a.beta[c];
+    float mu[V], iv[V], gm[V], bt[V];
+    if (OP == kBnBwd) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        mu[v] = a.mean[cg * V + v];
+        iv[v] = a.inv[cg * V + v];
+        gm[v] = a.gamma[cg * V + v];
+        bt[v] = a.beta[cg * V + v];
+      }
     }
+    const VT* zv = reinterpret_cast<const VT*>(a.z);
+    const VT* gv = reinterpret_cast<const VT*>(a.gy);
 #pragma unroll 4
     for (long long p = p0 + lane; p < p1; p += lanes) {
-      const float z = a.z[p * a.C + c];
-      if (a.op == kStats) {
-        q0 += z;
-        q1 += (double)z * z;
-      } else if (a.op == kBnBwd) {
-        const float xh = (z - mu) * iv;
-        const float ga = a.gy[p * a.C + c] * sigmoidf_(fmaf(gm, xh, bt));
-        q0 += ga;
-        q1 += (double)ga * xh;
+      const VT zz = zv[p * G + cg];
+      const float* z = reinterpret_cast<const float*>(&zz);
+      if (OP == kStats) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          q0[v] += z[v];
+          q1[v] += (double)z[v] * z[v];
+        }
+      } else if (OP == kBnBwd) {
+        const VT gg = gv[p * G + cg];
+        const float* gy = reinterpret_cast<const float*>(&gg);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const float xh = (z[v] - mu[v]) * iv[v];
+          const float ga = gy[v] * sigmoidf_(fmaf(gm[v], xh, bt[v]));
+          q0[v] += ga;
+          q1[v] += (double)ga * xh;
+        }
       } else {
-        q0 += z;
+#pragma unroll
+        for (int v = 0; v < V; ++v) q0[v] += z[v];
       }
     }
   }
-  sm[0][threadIdx.x] = q0;
-  sm[1][threadIdx.x] = q1;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    sm[0][v][threadIdx.x] = q0[v];
+    sm[1][v][threadIdx.x] = q1[v];
+  }
   __syncthreads();
   if (threadIdx.x < a.C) {
+    const int c = threadIdx.x, g = c / V, v = c % V;
     double s0 = 0.0, s1 = 0.0;
     for (int l = 0; l < lanes; ++l) {
-      s0 += sm[0][l * a.C + c];
-      s1 += sm[1][l * a.C + c];
+      s0 += sm[0][v][l * G + g];
+      s1 += sm[1][v][l * G + g];
     }
     a.part[((long long)blockIdx.x * a.C + c) * 2] = s0;
     a.part[((long long)blockIdx.x * a.C + c) * 2 + 1] = s1;
@@ -924,7 +970,7 @@ void wgrad_launch(hs_trainer* t, const float* P, int Hp, int Wp, int A, const fl
 // per-channel reduction + finalisation over an NHWC tensor of M pixels
 void chan_launch(hs_trainer* t, int op, const float* z, const float* gy, long long M, int C, const LayerP* p,
                  float* g0, float* g1_, cudaStream_t st) {
-  long long nchunk = std::min<long long>(2 * 148, std::max(1LL, M / 256));
+  long long nchunk = std::min<long long>(4 * 148, std::max(1LL, M / 256));
   nchunk = std::min(nchunk, t->chan_part_cap / (2LL * C));
   const long long chunk = (M + nchunk - 1) / nchunk;
   nchunk = (M + chunk - 1) / chunk;
@@ -935,7 +981,15 @@ void chan_launch(hs_trainer* t, int op, const float* z, const float* gy, long lo
     a.gamma = t->P + p->gamma;
     a.beta = t->P + p->beta;
   }
-  k_tr_chan<<<(unsigned)nchunk, 256, 0, st>>>(a);
+#define HS_CH(OPV)                                                                          \
+  if (op == OPV) {                                                                          \
+    if (C % 4 == 0) k_tr_chan<OPV, 4><<<(unsigned)nchunk, 256, 0, st>>>(a);               \
+    else k_tr_chan<OPV, 1><<<(unsigned)nchunk, 256, 0, st>>>(a);                          \
+  }
+  HS_CH(kStats)
+  HS_CH(kBnBwd)
+  HS_CH(kSum)
+#undef HS_CH
   TrChanFin f{t->chan_part, (int)nchunk, C, M, op, nullptr, nullptr, nullptr, nullptr, g0, g1_, t->s0, t->s1};
   if (op == kStats) {
     f.mean = p->st_mean;
@@ -1312,7 +1366,7 @@ HS_API int hs_trainer_create(hs_trainer_t** out, const hs_train_desc_t* d, const
   stat(t->enc_stem), stat(t->sol_stem);
   for (int l = 0; l < L; ++l) stat(t->enc_a[l]), stat(t->sol_a[l]);
   for (int l = 1; l < L; ++l) stat(t->enc_down[l]), stat(t->sol_down[l]), stat(t->up[l]), stat(t->ures_a[l]);
-  t->chan_part_cap = 2LL * 2 * 148 * 256;
+  t->chan_part_cap = 2LL * 4 * 148 * 256;
   t->chan_part = dalloc<double>(t, t->chan_part_cap);
   t->wg_part_cap = 8LL << 20;
   t->wg_part = A(t->wg_part_cap);
