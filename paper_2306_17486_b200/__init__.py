@@ -10,9 +10,11 @@ import importlib
 import sys
 
 __all__ = ["errors", "fields", "multigrid", "krylov", "green", "network", "engine", "problems", "netparams",
-           "dist", "install_as_helmsolve"]
+           "dist", "datagen", "train", "corpus", "formats", "cli", "install_as_helmsolve"]
 
-_MIRRORED = ("errors", "fields", "multigrid", "krylov", "green", "network")
+# the reference's modules plus the ones its SPEC / pyproject name but it never shipped
+# (network: krylov.py:201; cli: pyproject.toml:15-16; datagen / trainer: SPEC.md:395-507)
+_MIRRORED = ("errors", "fields", "multigrid", "krylov", "green", "network", "cli", "datagen", "train")
 
 
 def install_as_helmsolve() -> None:

@@ -231,6 +231,7 @@ class TrainConfig:
 @dataclass
 class History:
     rows: list = field(default_factory=list)  # (epoch, size, train_mse, val_mse, lr)
+    state: dict | None = None  # final trainer state (checkpoint payload)
 
     def csv(self) -> str:
         lines = ["epoch,size,train_mse,val_mse,lr"]
@@ -296,4 +297,5 @@ def train(net: EncoderSolverNet, config: TrainConfig, corpora: dict, checkpoint=
         state = tr.state()
         if checkpoint and (epoch + 1) % config.epochs_per_size_block == 0:
             save_checkpoint(checkpoint, state, net.channels)
+    hist.state = state
     return EncoderSolverNet(unflatten(state["params"], net.channels), net.channels), hist
