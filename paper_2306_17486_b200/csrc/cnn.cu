@@ -30,6 +30,9 @@ struct hs_net {
   cufftComplex* spec_perm = nullptr;  // the same in the fused kernel's order (implicit.cu), if supported
   const float* enc[8] = {nullptr};
   int n_models = 0;
+  // host copies of the thin layers' weights ([tap][cin][cout], then the bias): passed to the
+  // thin kernels by value (kernel-parameter constant bank) -- 0 encoder stem, 1 solver stem, 2 head
+  std::vector<float> thin_w[3];
   mutable std::mutex plan_mu;
   mutable std::map<int, cufftHandle> plans;  // batch -> plan
   ~hs_net() {
@@ -80,6 +83,7 @@ struct ThinIO {
   long long out_n;
   int out_ld, out_h, out_w;
   float out_scale;
+  const float* host_w = nullptr;  // [tap][cin][cout] + bias on the host: the by-value thin kernels
 };
 
 template <int COUT>
@@ -482,6 +486,126 @@ void launch_thin(const ConvArgs& a, int B, cudaStream_t st) {
   k_conv_thin<CIN, COUT><<<grid, kThinThreads, 0, st>>>(a);
 }
 
+// Thin convolutions with the weights in the kernel-parameter constant bank: one thread per output
+// column walks kThinRows rows (rolling window as k_conv_thin) and owns every channel of its pixel,
+// so all weight indices are compile-time constants and each FFMA takes its weight straight from
+// the constant bank -- no shared-memory weight reads, no lane split, no shuffles.
+template <int CIN, int COUT>
+struct ThinW {
+  float w[9 * CIN * COUT];  // [tap][cin][cout]
+  float b[COUT];
+};
+
+template <int CIN, int COUT>
+__global__ void __launch_bounds__(kThinThreads) k_conv_thin1(ConvArgs a, const __grid_constant__ ThinW<CIN, COUT> wt) {
+  const int b = blockIdx.z;
+  if (a.active && a.active[b] == nullptr) return;
+  const int x = blockIdx.x * kThinThreads + threadIdx.x;
+  const bool cout_c = COUT == 2 && a.cy != nullptr;
+  const int Hl = cout_c ? a.cy_h : a.Ho, Wl = cout_c ? a.cy_w : a.Wo;
+  if (x >= Wl) return;
+  const int oy0 = blockIdx.y * kThinRows, oy1 = min(Hl, oy0 + kThinRows);
+  const float* xb = a.x ? a.x + (long long)b * a.H * a.W * CIN : nullptr;
+  const bool cin_c = CIN == 2 && a.cx_ld > 0;
+  const float2* xc = cin_c ? (a.cx.tab ? a.cx.tab[b] : a.cx.base + (long long)b * a.cx.bstride) : nullptr;
+  const float xcs = cin_c && a.cx.scale ? a.cx.scale[b] : 1.f;
+  const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[b] : 0) : b) * a.addend_bstride
+                              : nullptr;
+  float acc[3][COUT];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int n = 0; n < COUT; ++n) acc[r][n] = 0.f;
+  auto load_row = [&](int iy, float(&xv)[3][CIN]) {
+#pragma unroll
+    for (int kx = 0; kx < 3; ++kx) {
+      const int ix = x + kx - 1;
+      if (iy >= 0 && iy < a.H && ix >= 0 && ix < a.W) {
+        if (cin_c) {
+          const float2 v = xc[(long long)iy * a.cx_ld + ix];
+          xv[kx][0] = v.x * xcs;
+          xv[kx][CIN > 1 ? 1 : 0] = v.y * xcs;
+        } else {
+          load_vec<CIN>(xb + ((long long)iy * a.W + ix) * CIN, xv[kx]);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < CIN; ++c) xv[kx][c] = 0.f;
+      }
+    }
+  };
+  auto load_side = [&](int oy, float(&sd)[COUT]) {
+#pragma unroll
+    for (int n = 0; n < COUT; ++n) sd[n] = 0.f;
+    if (oy < oy0 || oy >= oy1 || oy >= a.Ho || x >= a.Wo) return;
+    const long long p = (long long)oy * a.Wo + x;
+    if (add) load_vec<COUT>(add + p * COUT, sd);
+    if (a.residual) {
+      float u[COUT];
+      load_vec<COUT>(a.residual + (long long)b * a.Ho * a.Wo * COUT + p * COUT, u);
+#pragma unroll
+      for (int n = 0; n < COUT; ++n) sd[n] += u[n];
+    }
+  };
+  float nx[3][CIN];
+  load_row(oy0 - 1, nx);
+  for (int iy = oy0 - 1; iy <= oy1; ++iy) {
+    float xv[3][CIN], sd[COUT];
+#pragma unroll
+    for (int kx = 0; kx < 3; ++kx)
+#pragma unroll
+      for (int c = 0; c < CIN; ++c) xv[kx][c] = nx[kx][c];
+    if (iy < oy1) load_row(iy + 1, nx);
+    load_side(iy - 1, sd);
+#pragma unroll
+    for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < 3; ++kx)
+#pragma unroll
+        for (int c = 0; c < CIN; ++c)
+#pragma unroll
+          for (int n = 0; n < COUT; ++n)
+            acc[2 - ky][n] = fmaf(xv[kx][c], wt.w[((ky * 3 + kx) * CIN + c) * COUT + n], acc[2 - ky][n]);
+    const int oy = iy - 1;
+    if (oy >= oy0 && oy < oy1) {
+      float v[COUT];
+#pragma unroll
+      for (int n = 0; n < COUT; ++n) {
+        float t = acc[0][n] + wt.b[n];
+        if (a.softplus) t = softplus_fast(t);
+        v[n] = t + sd[n];
+      }
+      if (cout_c) {
+        const bool valid = oy < a.Ho && x < a.Wo;
+        a.cy[(long long)b * a.cy_n + (long long)oy * a.cy_ld + x] =
+            valid ? make_float2(a.cy_scale * v[0], a.cy_scale * v[COUT > 1 ? 1 : 0]) : make_float2(0.f, 0.f);
+      } else if (oy < a.Ho) {
+        store_vec<COUT>(a.y + (long long)b * a.Ho * a.Wo * COUT + ((long long)oy * a.Wo + x) * COUT, v);
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < COUT; ++n) {
+      acc[0][n] = acc[1][n];
+      acc[1][n] = acc[2][n];
+      acc[2][n] = 0.f;
+    }
+  }
+}
+
+template <int CIN, int COUT>
+void launch_thin1(const ConvArgs& a, const float* host_w, int B, cudaStream_t st) {
+  ThinW<CIN, COUT> wt;
+  for (int i = 0; i < 9 * CIN * COUT; ++i) wt.w[i] = host_w[i];
+  for (int n = 0; n < COUT; ++n) wt.b[n] = host_w[9 * CIN * COUT + n];
+  const int Hl = a.cy ? a.cy_h : a.Ho, Wl = a.cy ? a.cy_w : a.Wo;
+  const dim3 grid((unsigned)((Wl + kThinThreads - 1) / kThinThreads), (unsigned)((Hl + kThinRows - 1) / kThinRows),
+                  (unsigned)B);
+  k_conv_thin1<CIN, COUT><<<grid, kThinThreads, 0, st>>>(a, wt);
+}
+
+// HS_THIN_SMEM=1 keeps the shared-memory thin kernels (A/B comparisons)
+const bool thin_smem_path = getenv("HS_THIN_SMEM") && atoi(getenv("HS_THIN_SMEM")) == 1;
+
 int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* y, const float* addend,
                 long long addend_bstride, const int* model_of, const float* residual, const void* const* active,
                 cudaStream_t st, bool model_of_addend = false, const ThinIO* io = nullptr) {
@@ -541,6 +665,12 @@ int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* 
   a.active = active;
   if ((a.cx_ld > 0 || a.cy) && !(!c.transposed && c.stride == 1 && (c.cin == 2 || c.cout == 2)))
     return HS_ECONFIG;  // complex I/O is fused into the thin stem / head only
+  if (!c.transposed && c.stride == 1 && io && io->host_w && !thin_smem_path) {
+    if (c.cin == 2 && c.cout == 16) return launch_thin1<2, 16>(a, io->host_w, B, st), HS_OK;
+    if (c.cin == 16 && c.cout == 2) return launch_thin1<16, 2>(a, io->host_w, B, st), HS_OK;
+    if (c.cin == 2 && c.cout == 8) return launch_thin1<2, 8>(a, io->host_w, B, st), HS_OK;
+    if (c.cin == 8 && c.cout == 2) return launch_thin1<8, 2>(a, io->host_w, B, st), HS_OK;
+  }
   if (!c.transposed && c.stride == 1) {
     if (c.cin == 2 && c.cout == 16) return launch_thin<2, 16>(a, B, st), HS_OK;
     if (c.cin == 2 && c.cout == 8) return launch_thin<2, 8>(a, B, st), HS_OK;
@@ -831,8 +961,11 @@ static int solver_forward(const hs_net_t* net, const float* in, float* head, con
   auto lvl_bstride = [&](int l) { return (long long)(d.ix >> l) * (d.iy >> l) * d.channels[l]; };
   int rc;
   // level 0: stem (+ encoding 0), residual block -> skip 0
+  ThinIO io_stem = io ? *io : ThinIO{}, io_head = io ? *io : ThinIO{};
+  io_stem.host_w = net->thin_w[1].empty() ? nullptr : net->thin_w[1].data();
+  io_head.host_w = net->thin_w[2].empty() ? nullptr : net->thin_w[2].data();
   if ((rc = launch_conv(d.sol_stem, in, B, d.ix, d.iy, X[0], net->enc[0], lvl_bstride(0), model_of, nullptr, active,
-                        st, true, io)))
+                        st, true, &io_stem)))
     return rc;
   if ((rc = launch_conv(d.sol_res_a[0], X[0], B, d.ix, d.iy, Tm[0], nullptr, 0, nullptr, nullptr, active, st)))
     return rc;
@@ -868,7 +1001,7 @@ static int solver_forward(const hs_net_t* net, const float* in, float* head, con
                           nullptr, Tm[l - 1], active, st)))
       return rc;
   }
-  return launch_conv(d.sol_head, X[0], B, d.ix, d.iy, head, nullptr, 0, nullptr, nullptr, active, st, false, io);
+  return launch_conv(d.sol_head, X[0], B, d.ix, d.iy, head, nullptr, 0, nullptr, nullptr, active, st, false, &io_head);
 }
 
 int cnn_preconditioner_estimate(const hs_net_t* net, VecIn vin, const float2* const* active, float2* u0,
@@ -915,6 +1048,25 @@ HS_API int hs_net_create(hs_net_t** out, const hs_net_desc_t* desc, void* stream
     return cfail(HS_EDIMENSION, "coarse size too small for the implicit layer");
   }
   cudaStream_t st = (cudaStream_t)stream;
+  // host copies of the thin layers ([cout][9][cin] on the device -> [tap][cin][cout] + bias)
+  const hs_conv_t* thin[3] = {&desc->enc_stem, &desc->sol_stem, &desc->sol_head};
+  for (int k = 0; k < 3; ++k) {
+    const hs_conv_t& c = *thin[k];
+    if (!c.w || !c.b || c.stride != 1 || c.transposed) continue;
+    const int ci = c.cin, co = c.cout, nw = 9 * ci * co;
+    std::vector<float> w(nw), b(co);
+    if (cudaMemcpy(w.data(), c.w, nw * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(b.data(), c.b, co * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      delete n;
+      return cfail(HS_ECUDA, "thin weights");
+    }
+    auto& h = n->thin_w[k];
+    h.assign(nw + co, 0.f);
+    for (int o = 0; o < co; ++o)
+      for (int t = 0; t < 9; ++t)
+        for (int i = 0; i < ci; ++i) h[(t * ci + i) * co + o] = w[(o * 9 + t) * ci + i];
+    for (int o = 0; o < co; ++o) h[nw + o] = b[o];
+  }
   const long long ns = (long long)n->cc * 4 * n->hc * n->wc;
   cufftDoubleComplex* s128 = nullptr;
   if (cudaMalloc(&s128, ns * sizeof(cufftDoubleComplex)) != cudaSuccess ||
@@ -966,7 +1118,10 @@ HS_API int hs_net_encode(hs_net_t* net, const float* media, int n_models, float*
   float* t1 = reinterpret_cast<float*>(w + big);
   int rc;
   // e0 = res0(cbs(stem(media))), e_l = res_l(cbs(down_l(e_{l-1})))
-  if ((rc = hs::launch_conv(d.enc_stem, media, n_models, d.ix, d.iy, t0, nullptr, 0, nullptr, nullptr, nullptr, st)))
+  hs::ThinIO io_enc{};
+  io_enc.host_w = net->thin_w[0].empty() ? nullptr : net->thin_w[0].data();
+  if ((rc = hs::launch_conv(d.enc_stem, media, n_models, d.ix, d.iy, t0, nullptr, 0, nullptr, nullptr, nullptr, st,
+                            false, &io_enc)))
     return cfail(rc, "encoder stem");
   for (int l = 0; l < d.levels; ++l) {
     const int h = d.ix >> l, ww = d.iy >> l;
