@@ -22,6 +22,8 @@
 // c = 32 k1 + l holds frequency k1 + E br5(l)); the spectrum is permuted into
 // the same order once, at network setup.  Twiddles come from a per-CTA table
 // built with sincospif (full fp32 accuracy).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "implicit.h"
 
@@ -192,6 +194,219 @@ __global__ void __launch_bounds__(kImpThreads) k_implicit(ImpArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Four-step variant for square grids (N = 32 E, E in {2, 4}): a line of N points is split as
+// n = l + 32 j (l < 32, j < E) and k = k1 + E m (k1 < E, m < 32):
+//   X[k1 + E m] = sum_l W_32^(l m) [ W_N^(l k1) sum_j x[l + 32 j] W_E^(j k1) ]
+// Step (a): one warp per line, lane l does the E-point DFT over j and the twiddle (registers).
+// Step (c): one THREAD per (line, k1) does the 32-point DFT over l entirely in registers
+// (radix-2, compile-time twiddles), through a padded shared-memory transpose.  No shuffles:
+// the warp-shuffle version spends most of its issue slots on the 5 cross-lane stages.
+// The column pass runs forward FFT, spectrum multiply and inverse FFT in the same thread's
+// registers; all data stay in natural frequency order (the spectrum is used as stored).
+
+// a * W_32^(+-k) for a compile-time k in [0, 16)
+template <bool INV>
+HS_DEV float2 tw32(float2 a, int k) {
+  constexpr float C[9] = {1.f,
+                          0.98078528040323044913f,
+                          0.92387953251128675613f,
+                          0.83146961230254523708f,
+                          0.70710678118654752440f,
+                          0.55557023301960222474f,
+                          0.38268343236508977173f,
+                          0.19509032201612826785f,
+                          0.f};
+  if (k == 0) return a;
+  if (k == 8) return INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
+  const float c = k < 8 ? C[k] : -C[16 - k];
+  const float sn = k < 8 ? C[8 - k] : C[k - 8];  // sin(pi k / 16)
+  // W^k = c - i sn (forward), c + i sn (inverse)
+  return INV ? make_float2(a.x * c - a.y * sn, a.y * c + a.x * sn) : make_float2(a.x * c + a.y * sn, a.y * c - a.x * sn);
+}
+
+HS_DEV constexpr int brev5(int m) {
+  return ((m & 1) << 4) | ((m & 2) << 2) | (m & 4) | ((m & 8) >> 2) | ((m & 16) >> 4);
+}
+
+// in-place 32-point DFT of v (natural order in, natural order out), unnormalised
+template <bool INV>
+HS_DEV void fft32(float2 (&v)[32]) {
+#pragma unroll
+  for (int hs = 16; hs >= 1; hs >>= 1) {  // radix-2 DIF stages
+#pragma unroll
+    for (int blk = 0; blk < 32; blk += 2 * hs)
+#pragma unroll
+      for (int j = 0; j < hs; ++j) {
+        const float2 a = v[blk + j], b = v[blk + j + hs];
+        v[blk + j] = cadd(a, b);
+        v[blk + j + hs] = tw32<INV>(csub(a, b), j * (16 / hs));
+      }
+  }
+  // bit-reversed -> natural (a compile-time register permutation)
+  float2 t[32];
+#pragma unroll
+  for (int m = 0; m < 32; ++m) t[m] = v[brev5(m)];
+#pragma unroll
+  for (int m = 0; m < 32; ++m) v[m] = t[m];
+}
+
+template <int E>
+struct Imp2 {
+  static constexpr int THREADS = 128;
+  static constexpr int N = 32 * E, h = N / 2, NZ = E / 2, LD = N + 1, TL = 33, LINES = THREADS / E;
+  static constexpr size_t SMEM = ((size_t)h * LD + (size_t)LINES * E * TL + N) * sizeof(float2);
+};
+
+template <int E>
+__global__ void __launch_bounds__(Imp2<E>::THREADS) k_implicit2(ImpArgs a) {
+  using G = Imp2<E>;
+  constexpr int N = G::N, h = G::h, NZ = G::NZ, LD = G::LD, TL = G::TL, LINES = G::LINES, NT = G::THREADS;
+  constexpr int NW = NT / 32;
+  extern __shared__ float2 smem_imp2[];
+  float2* S = smem_imp2;           // [h][LD]  row spectra (rows >= h of the padded input are zero)
+  float2* T = S + h * LD;          // [E][LINES][TL] transpose buffer
+  float2* tw = T + LINES * E * TL; // W_N^m
+  const int b = blockIdx.y, k = blockIdx.x;
+  if (a.active && a.active[b] == nullptr) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int m = threadIdx.x; m < N; m += NT) {
+    float sn, cs;
+    sincospif(-2.f * m / N, &sn, &cs);
+    tw[m] = make_float2(cs, sn);
+  }
+  const float2* xin = a.x + b * a.xb + k * a.xk;
+  float2* yout = a.y + b * a.yb + k * a.yk;
+  const float2* sp = a.spec + (long long)k * N * N;
+  const int tk = threadIdx.x / LINES, tl = threadIdx.x % LINES;  // step (c): (k1, line), lines fastest (banks)
+  __syncthreads();
+  // step (a) forward on a line held as q[j] = x[lane + 32 j] (j < NZ non-zero) -> T line
+  auto fwd_a = [&](float2(&q)[E], int line) {
+#pragma unroll
+    for (int k1 = 0; k1 < E; ++k1) {
+      float2 s = q[0];
+#pragma unroll
+      for (int j = 1; j < NZ; ++j) s = cadd(s, mul_wE<E>(q[j], j * k1));
+      T[(k1 * LINES + line) * TL + lane] = k1 == 0 ? s : cmul(s, tw[lane * k1]);
+    }
+  };
+  // step (a) inverse: T line -> q[j] = N x[lane + 32 j] for j < NZ
+  auto inv_a = [&](float2(&q)[E], int line) {
+    float2 y[E];
+#pragma unroll
+    for (int k1 = 0; k1 < E; ++k1) {
+      y[k1] = T[(k1 * LINES + line) * TL + lane];
+      if (k1) y[k1] = cmulc(y[k1], tw[lane * k1]);
+    }
+#pragma unroll
+    for (int j = 0; j < NZ; ++j) {
+      float2 s = y[0];
+#pragma unroll
+      for (int k1 = 1; k1 < E; ++k1) s = cadd(s, mul_wE<E>(y[k1], (E - (j * k1) % E) % E));
+      q[j] = s;
+    }
+  };
+  // 1. forward row transforms (h rows, LINES per chunk)
+  for (int r0 = 0; r0 < h; r0 += LINES) {
+    const int nl = min(LINES, h - r0);
+    {
+      // all of this warp's rows are loaded before any is transformed (loads in flight together)
+      constexpr int RPW = LINES / NW;
+      float2 q[RPW][E];
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) {
+        const int rr = warp + i * NW;
+#pragma unroll
+        for (int j = 0; j < E; ++j)
+          q[i][j] = (j < NZ && rr < nl) ? xin[(long long)((r0 + rr) * h + lane + 32 * j) * a.xp] : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int i = 0; i < RPW; ++i)
+        if (warp + i * NW < nl) fwd_a(q[i], warp + i * NW);
+    }
+    __syncthreads();
+    if (tl < nl) {
+      float2 v[32];
+#pragma unroll
+      for (int l = 0; l < 32; ++l) v[l] = T[(tk * LINES + tl) * TL + l];
+      fft32<false>(v);
+#pragma unroll
+      for (int m = 0; m < 32; ++m) S[(r0 + tl) * LD + tk + E * m] = v[m];
+    }
+    __syncthreads();
+  }
+  // 2. columns: forward, spectrum, inverse (rows < h kept)
+  for (int c0 = 0; c0 < N; c0 += LINES) {
+    const int nl = min(LINES, N - c0);
+    for (int cc = warp; cc < nl; cc += NW) {
+      float2 q[E];
+#pragma unroll
+      for (int j = 0; j < E; ++j) q[j] = j < NZ ? S[(lane + 32 * j) * LD + c0 + cc] : make_float2(0.f, 0.f);
+      fwd_a(q, cc);
+    }
+    __syncthreads();
+    if (tl < nl) {
+      float2 v[32];
+#pragma unroll
+      for (int l = 0; l < 32; ++l) v[l] = T[(tk * LINES + tl) * TL + l];
+      fft32<false>(v);
+      const float2* spc = sp + c0 + tl;
+#pragma unroll
+      for (int m = 0; m < 32; ++m) v[m] = cmul(v[m], __ldg(spc + (long long)(tk + E * m) * N));
+      fft32<true>(v);
+#pragma unroll
+      for (int l = 0; l < 32; ++l) T[(tk * LINES + tl) * TL + l] = v[l];
+    }
+    __syncthreads();
+    for (int cc = warp; cc < nl; cc += NW) {
+      float2 q[E];
+      inv_a(q, cc);
+#pragma unroll
+      for (int j = 0; j < NZ; ++j) S[(lane + 32 * j) * LD + c0 + cc] = q[j];
+    }
+    __syncthreads();
+  }
+  // 3. inverse row transforms (columns < h kept), 1 / N^2
+  const float inv = 1.f / ((float)N * (float)N);
+  for (int r0 = 0; r0 < h; r0 += LINES) {
+    const int nl = min(LINES, h - r0);
+    if (tl < nl) {
+      float2 v[32];
+#pragma unroll
+      for (int m = 0; m < 32; ++m) v[m] = S[(r0 + tl) * LD + tk + E * m];
+      fft32<true>(v);
+#pragma unroll
+      for (int l = 0; l < 32; ++l) T[(tk * LINES + tl) * TL + l] = v[l];
+    }
+    __syncthreads();
+    for (int rr = warp; rr < nl; rr += NW) {
+      float2 q[E];
+      inv_a(q, rr);
+#pragma unroll
+      for (int j = 0; j < NZ; ++j)
+        yout[(long long)((r0 + rr) * h + lane + 32 * j) * a.yp] = make_float2(q[j].x * inv, q[j].y * inv);
+    }
+    __syncthreads();
+  }
+}
+
+template <int E>
+void launch_imp2(const ImpArgs& a, int B, cudaStream_t st) {
+  const size_t sm = Imp2<E>::SMEM;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_implicit2<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  k_implicit2<E><<<dim3((unsigned)a.C, (unsigned)B), Imp2<E>::THREADS, sm, st>>>(a);
+}
+
+// the four-step kernel where it applies (square 64^2 / 128^2 padded grids); HS_IMP_V1=1 forces the old one
+bool use_v2(int h, int w) {
+  static const bool off = getenv("HS_IMP_V1") && atoi(getenv("HS_IMP_V1")) == 1;
+  return !off && h == w && (h == 32 || h == 64);
+}
+
 // natural spectrum [C][H2][W2] -> kernel order [C][c][k1'][l]: column c holds
 // frequency f = c/32 + EW br5(c%32), entry (k1', l) row frequency u = k1' + EH br5(l)
 __global__ void k_permute_spec(const float2* in, float2* out, int C, int H2, int W2) {
@@ -230,6 +445,10 @@ bool implicit_fused_supported(int h, int w) {
 
 void implicit_permute_spectrum(const void* spec, void* spec_perm, int C, int h, int w, cudaStream_t st) {
   const long long n = (long long)C * 4 * h * w;
+  if (use_v2(h, w)) {  // the four-step kernel reads the natural order
+    cudaMemcpyAsync(spec_perm, spec, n * sizeof(float2), cudaMemcpyDeviceToDevice, st);
+    return;
+  }
   const unsigned g = (unsigned)((n + 255) / 256 > 4096 ? 4096 : (n + 255) / 256);
   k_permute_spec<<<g, 256, 0, st>>>(static_cast<const float2*>(spec), static_cast<float2*>(spec_perm), C, 2 * h,
                                     2 * w);
@@ -242,6 +461,10 @@ int implicit_fused(const void* x, long long xb, long long xk, long long xp, void
   ImpArgs a{static_cast<const float2*>(x), xb, xk, xp, static_cast<float2*>(y), yb, yk, yp,
             static_cast<const float2*>(spec_perm), active, C};
   const int EW = w / 16, EH = h / 16;
+  if (use_v2(h, w)) {
+    if (EW == 2) return launch_imp2<2>(a, B, st), HS_OK;
+    if (EW == 4) return launch_imp2<4>(a, B, st), HS_OK;
+  }
 #define HS_IMP(A, Bq) \
   if (EW == A && EH == Bq) return launch_imp<A, Bq>(a, B, st), HS_OK;
   HS_IMP(2, 2)

@@ -284,9 +284,14 @@ class BatchSolver:
             if cont:
                 idx = torch.tensor(cont, device=dev)
                 # rel1 = ||b - A x1|| / ||b|| in fp64 on the device (krylov.py:222-223)
+                # (one batched operator application per slowness model)
                 num = torch.empty(len(cont), dtype=torch.float64, device=dev)
-                for k, i in enumerate(cont):
-                    num[k] = torch.linalg.vector_norm(bd[i] - apply_operator(x[i], self.models[owner[i]]))
+                cont_a = np.asarray(cont)
+                for m in np.unique(owner[cont_a]):
+                    sel = np.nonzero(owner[cont_a] == m)[0]
+                    ii = torch.from_numpy(cont_a[sel]).to(dev)
+                    res = bd[ii] - apply_operator(x[ii], self.models[int(m)])
+                    num[torch.from_numpy(sel).to(dev)] = torch.linalg.vector_norm(res.reshape(len(sel), -1), dim=1)
                 den = torch.linalg.vector_norm(bd[idx].reshape(len(cont), -1), dim=1)
                 rel1 = (num / den).cpu().numpy()
                 it1 = int(r1.iterations[cont[0]])
