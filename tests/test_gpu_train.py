@@ -162,3 +162,24 @@ def test_deterministic_gradients():
     a, b = g1.grads(), g2.grads()
     for k in a:
         assert np.array_equal(a[k], b[k]), k
+
+
+def test_gradients_match_oracle_four_levels_nonsquare():
+    # C3-style network (16, 32, 64, 128): 4 levels, implicit layer on a 4 x 8 coarse grid, 33 x 65 nodes
+    ch, B = (16, 32, 64, 128), 2
+    rng = np.random.default_rng(31)
+    from paper_2306_17486_b200 import fields
+
+    models = [fields.slowness_model(problems.smooth_random_kappa_sq((33, 65), 3.0, s), layer_width=4) for s in (1, 2)]
+    params = netparams.randomise_batchnorm(netparams.init_params(ch, seed=3), seed=4)
+    owner = np.arange(B) % 2
+    media = tr.media_planes(models, len(ch))
+    r = rng.standard_normal((B, 33, 65)) + 1j * rng.standard_normal((B, 33, 65))
+    e = 0.01 * (rng.standard_normal((B, 33, 65)) + 1j * rng.standard_normal((B, 33, 65)))
+    h = models[0].h
+    po = to.as_float64(params)
+    loss, og, _ = to.loss_and_grads(po, len(ch), media[owner].astype(np.float64), r, e, h)
+    t = tr.Trainer(network.EncoderSolverNet(params, ch), (33, 65), h, B)
+    lg = t.step(media, r, e, model_of=owner, update=False)
+    assert lg == pytest.approx(loss, rel=1e-5)
+    compare_grads(t.grads(), og, po)
