@@ -358,8 +358,8 @@ def run_train(args):
     cfg = {"workload": f"train: C2's 4 models (gamma0 0.05), 257x257 grid, network 16/32/64 (3 levels, implicit "
                        f"layer at 64x64), batch {B} datagen pairs (r, e) per step, training-mode batch norm, "
                        f"MSE of u0 = (h^2/64) net(r) vs e, backward, Adam lr 1e-3",
-           "global_batch_per_gpu": B, "parallelism": "replicas only (independent trainer per rank, no gradient "
-                                                      "all-reduce; see DESIGN.md)",
+           "global_batch_per_gpu": B, "parallelism": "data-parallel: batch B per rank, one NCCL all-reduce of the "
+                                                      "flat fp32 gradient vector per step (train.Trainer.step)",
            "l2": "per-step working set (saved activations ~1.3 GB) far larger than L2"}
     workers = args.cpu_workers or (os.cpu_count() or 1)
     if args.impl == "reference":

@@ -242,6 +242,12 @@ HS_API void hs_trainer_destroy(hs_trainer_t* t);
  * optional) receives the batch MSE and makes the call synchronous; HS_ENONFINITE on a non-finite loss. */
 HS_API int hs_trainer_step(hs_trainer_t* t, const float* media, int n_models, const int* model_of, const void* r,
                            const void* e, const hs_adam_t* adam, double* loss, void* stream);
+/* data-parallel training: copy the flat float32 gradient vector to (to_trainer = 0) or from (1)
+ * a caller DEVICE buffer, so an all-reduce can run between the backward pass (hs_trainer_step with
+ * adam = NULL) and hs_trainer_apply. */
+HS_API int hs_trainer_grads(hs_trainer_t* t, void* dev, int to_trainer, void* stream);
+/* one Adam step on the trainer's current gradient vector */
+HS_API int hs_trainer_apply(hs_trainer_t* t, const hs_adam_t* adam, void* stream);
 /* which: 0 parameters, 1 last gradients, 2 Adam m, 3 Adam v; host float32 out */
 HS_API int hs_trainer_read(const hs_trainer_t* t, int which, float* host, void* stream);
 /* which: 0 parameters, 2 Adam m, 3 Adam v (checkpoint restore); step >= 0 sets Adam's step counter */

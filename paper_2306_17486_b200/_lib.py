@@ -153,6 +153,8 @@ SIGNATURES = {
     "hs_trainer_destroy": (None, [_VP]),
     "hs_trainer_step": (_I, [_VP, _VP, _I, _VP, _VP, _VP, ctypes.POINTER(HsAdam), c_double_p, _VP]),
     "hs_trainer_read": (_I, [_VP, _I, _VP, _VP]),
+    "hs_trainer_grads": (_I, [_VP, _VP, _I, _VP]),
+    "hs_trainer_apply": (_I, [_VP, ctypes.POINTER(HsAdam), _VP]),
     "hs_trainer_write": (_I, [_VP, _I, _VP, _I, _VP]),
 }
 

@@ -1459,6 +1459,30 @@ HS_API int hs_trainer_step(hs_trainer_t* t, const float* media, int n_models, co
   return HS_OK;
 }
 
+// data-parallel training: copy the flat gradient vector to (to_trainer = 0) or from (1) a caller
+// device buffer, so an all-reduce (NCCL) can run between the backward pass and hs_trainer_apply
+HS_API int hs_trainer_grads(hs_trainer_t* t, void* dev, int to_trainer, void* stream) {
+  if (!t || !dev) return hs::tfail(HS_ECONFIG, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const cudaError_t e = to_trainer ? cudaMemcpyAsync(t->G, dev, t->nparam * sizeof(float), cudaMemcpyDeviceToDevice, st)
+                                   : cudaMemcpyAsync(dev, t->G, t->nparam * sizeof(float), cudaMemcpyDeviceToDevice, st);
+  return e == cudaSuccess ? HS_OK : hs::tfail(HS_ECUDA, cudaGetErrorString(e));
+}
+
+// one Adam step on the current gradient vector (after hs_trainer_step with adam = NULL)
+HS_API int hs_trainer_apply(hs_trainer_t* t, const hs_adam_t* adam, void* stream) {
+  if (!t || !adam) return hs::tfail(HS_ECONFIG, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  t->t += 1;
+  const float c1 = (float)(1.0 - std::pow((double)adam->beta1, t->t));
+  const float c2 = (float)(1.0 - std::pow((double)adam->beta2, t->t));
+  hs::k_tr_adam<<<hs::g1((long long)t->nparam), 256, 0, st>>>(t->P, t->G, t->M, t->V, (long long)t->nparam, adam->lr,
+                                                              adam->beta1, adam->beta2, adam->eps, c1, c2);
+  hs::prof::count(1);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? HS_OK : hs::tfail(HS_ECUDA, cudaGetErrorString(e));
+}
+
 // which: 0 parameters (incl. running statistics), 1 gradients of the last step, 2 Adam m, 3 Adam v
 HS_API int hs_trainer_read(const hs_trainer_t* t, int which, float* host, void* stream) {
   if (!t || !host || which < 0 || which > 3) return hs::tfail(HS_ECONFIG, "bad read request");

@@ -1,7 +1,9 @@
 """Data-parallel plumbing: independent RHS / slowness models sharded over ranks.
 
 The solve has no exchange step: every (model, RHS) pair is
-independent, so ranks never communicate on the data path.  One process per
+independent, so ranks never communicate on the data path.  Data-parallel
+training (train.py) has one: the flat gradient vector is averaged across ranks
+(``allreduce_mean``, one NCCL all-reduce per step) between backward and Adam.  One process per
 GPU, ``torch.distributed`` (NCCL on GPUs, gloo in the CPU tests) is used only
 to time the job as the max over ranks and to gather per-RHS reports.
 """
@@ -55,3 +57,21 @@ def gather_reports(local: list) -> list:
     out = [None] * dist.get_world_size()
     dist.all_gather_object(out, list(local))
     return [item for part in out for item in part]
+
+
+def world_size() -> int:
+    import torch.distributed as dist
+
+    return dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+
+
+def allreduce_mean(t):
+    """In-place average of a tensor across ranks (sum all-reduce / world); identity alone."""
+    import torch.distributed as dist
+
+    w = world_size()
+    if w == 1:
+        return t
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    t /= w
+    return t

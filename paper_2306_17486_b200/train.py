@@ -19,6 +19,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from . import dist as hdist
 from . import netparams
 from .errors import ConfigurationError, DimensionError, NumericalError
 from .network import EncoderSolverNet
@@ -138,13 +139,25 @@ class Trainer:
         owner = np.zeros(self.batch, dtype=np.int32) if model_of is None else np.asarray(model_of, dtype=np.int32)
         owner = np.ascontiguousarray(owner)
         loss = ctypes.c_double()
-        _lib.check(_lib.load().hs_trainer_step(self.handle, md.data_ptr(), int(md.shape[0]), owner.ctypes.data,
-                                               rd.data_ptr(), ed.data_ptr(),
-                                               ctypes.byref(self.adam) if update else None, ctypes.byref(loss),
-                                               stream_handle()), "training step")
+        lib = _lib.load()
+        data_parallel = update and hdist.world_size() > 1
+        _lib.check(lib.hs_trainer_step(self.handle, md.data_ptr(), int(md.shape[0]), owner.ctypes.data,
+                                       rd.data_ptr(), ed.data_ptr(),
+                                       ctypes.byref(self.adam) if update and not data_parallel else None,
+                                       ctypes.byref(loss), stream_handle()), "training step")
+        value = float(loss.value)
+        if data_parallel:
+            # data-parallel step: average the gradient vector over ranks (NCCL), then Adam
+            if getattr(self, "_gbuf", None) is None:
+                self._gbuf = torch.empty(self.n, dtype=torch.float32, device=rd.device)
+            _lib.check(lib.hs_trainer_grads(self.handle, self._gbuf.data_ptr(), 0, stream_handle()), "grads out")
+            hdist.allreduce_mean(self._gbuf)
+            _lib.check(lib.hs_trainer_grads(self.handle, self._gbuf.data_ptr(), 1, stream_handle()), "grads in")
+            _lib.check(lib.hs_trainer_apply(self.handle, ctypes.byref(self.adam), stream_handle()), "adam")
+            value = hdist.reduce_scalar(value, "sum") / hdist.world_size()
         if update:
             self.steps += 1
-        return float(loss.value)
+        return value
 
     def _read(self, which: int) -> np.ndarray:
         from . import _lib

@@ -75,3 +75,68 @@ def test_gloo_world_size_two():
         assert s == 4  # C1 has 4 RHS: 2 per rank
         assert [r for r, _, _ in allr] == [0, 0, 1, 1]
     assert res[0][3] == res[1][3]
+
+
+def _train_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import train_oracle as to
+    from paper_2306_17486_b200 import netparams
+    from paper_2306_17486_b200 import train as tr
+    from conftest import golden
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # data-parallel training step: each rank's gradient of ITS shard, averaged by the all-reduce
+        g = golden("train.npz")
+        ch = tuple(int(c) for c in g["channels_a"])
+        names = [n for n, *_ in netparams.param_spec(ch)]
+        params = {n: g[f"p_a_{n}"].copy() for n in names}
+        sl = slice(rank, rank + 1)  # ranks 0 and 1 take samples 0 and 1
+        loss, grads, _ = to.loss_and_grads(params, int(g["levels_a"]), g["media_a"][sl], g["r_a"][sl], g["e_a"][sl],
+                                           float(g["h_a"]))
+        vec = torch.from_numpy(tr.flatten({**params, **grads}, ch).astype(np.float32))
+        hdist.allreduce_mean(vec)
+        mean_loss = hdist.reduce_scalar(loss, "sum") / hdist.world_size()
+        q.put((rank, vec.numpy(), mean_loss))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_data_parallel_gradient_average():
+    import multiprocessing as mp
+
+    from conftest import golden
+    from oracle import train_oracle as to
+    from paper_2306_17486_b200 import netparams
+    from paper_2306_17486_b200 import train as tr
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_train_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in procs], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # serial reference: the mean of the two per-sample gradients
+    g = golden("train.npz")
+    ch = tuple(int(c) for c in g["channels_a"])
+    names = [n for n, *_ in netparams.param_spec(ch)]
+    vecs, losses = [], []
+    for r in range(2):
+        params = {n: g[f"p_a_{n}"].copy() for n in names}
+        sl = slice(r, r + 1)
+        loss, grads, _ = to.loss_and_grads(params, int(g["levels_a"]), g["media_a"][sl], g["r_a"][sl], g["e_a"][sl],
+                                           float(g["h_a"]))
+        vecs.append(tr.flatten({**params, **grads}, ch).astype(np.float32))
+        losses.append(loss)
+    want = (vecs[0] + vecs[1]) / 2
+    for rank, vec, mean_loss in res:
+        assert np.allclose(vec, want, rtol=1e-6, atol=1e-7)
+        assert mean_loss == pytest.approx(np.mean(losses), rel=1e-12)
+    assert np.array_equal(res[0][1], res[1][1])  # every rank holds the same averaged vector

@@ -183,3 +183,29 @@ def test_gradients_match_oracle_four_levels_nonsquare():
     lg = t.step(media, r, e, model_of=owner, update=False)
     assert lg == pytest.approx(loss, rel=1e-5)
     compare_grads(t.grads(), og, po)
+
+
+def test_split_step_equals_fused_step():
+    # the data-parallel sequence (backward, gradients out / in around an all-reduce, Adam) is the fused step
+    import ctypes
+
+    import torch
+
+    from paper_2306_17486_b200 import _lib
+    from paper_2306_17486_b200.device import stream_handle
+
+    g, ch, params = fixture("a")
+    B, n = g["r_a"].shape[:2]
+    a = tr.Trainer(network.EncoderSolverNet(f32(params), ch), (n, n), float(g["h_a"]), B)
+    b = tr.Trainer(network.EncoderSolverNet(f32(params), ch), (n, n), float(g["h_a"]), B)
+    la = a.step(g["media_a"], g["r_a"], g["e_a"], model_of=np.arange(B))
+    lb = b.step(g["media_a"], g["r_a"], g["e_a"], model_of=np.arange(B), update=False)
+    lib = _lib.load()
+    buf = torch.empty(b.n, dtype=torch.float32, device="cuda")
+    _lib.check(lib.hs_trainer_grads(b.handle, buf.data_ptr(), 0, stream_handle()), "out")
+    _lib.check(lib.hs_trainer_grads(b.handle, buf.data_ptr(), 1, stream_handle()), "in")
+    _lib.check(lib.hs_trainer_apply(b.handle, ctypes.byref(b.adam), stream_handle()), "apply")
+    assert la == lb
+    pa, pb = a.params(), b.params()
+    for k in pa:
+        assert np.array_equal(pa[k], pb[k]), k
