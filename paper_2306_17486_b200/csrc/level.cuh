@@ -14,6 +14,9 @@ struct LevelDev {
   float wall_x;   // 0 when the level has no wall on that axis
   float wall_y;
   const float2* mass;  // (n_models, nx, ny)
+  // derived once per solve by vcycle_prepare (null until then), (n_models, nx, ny):
+  const float2* diag;  // 4/h^2 - c + wall
+  const float2* dinv;  // 1 / diag
 };
 
 HS_DEV float wall_at(const LevelDev& L, int i, int j) {
@@ -36,6 +39,18 @@ HS_DEV float2 level_apply(const LevelDev& L, float2 c, int i, int j, float2 u, f
   float wl = wall_at(L, i, j);
   float2 cu = cmul(c, u);
   return make_float2(lap.x * L.inv_h2 - cu.x + wl * u.x, lap.y * L.inv_h2 - cu.y + wl * u.y);
+}
+
+// The same operator in diagonal form: (A u)(p) = diag u - (sum of the four
+// neighbours) / h^2, and one damped Jacobi sweep
+//   u + w (rhs - A u) / diag = (1 - w) u + w dinv (rhs + nb / h^2).
+HS_DEV float2 apply_dd(float2 d, float inv_h2, float2 u, float2 nb) {
+  return make_float2(fmaf(d.x, u.x, fmaf(-d.y, u.y, -nb.x * inv_h2)), fmaf(d.x, u.y, fmaf(d.y, u.x, -nb.y * inv_h2)));
+}
+HS_DEV float2 jacobi_dd(float2 di, float inv_h2, float w, float2 u, float2 rhs, float2 nb) {
+  const float2 t = make_float2(fmaf(nb.x, inv_h2, rhs.x), fmaf(nb.y, inv_h2, rhs.y));
+  const float2 q = cmul(di, t);
+  return make_float2(fmaf(1.f - w, u.x, w * q.x), fmaf(1.f - w, u.y, w * q.y));
 }
 
 // 1D prolongation weights of P = 4 R^T for fine index i against coarse K

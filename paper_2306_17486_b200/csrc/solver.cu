@@ -246,6 +246,7 @@ HS_API int hs_fgmres_solve(const hs_hierarchy_t* h, const hs_net_t* net, const h
   float2* u0 = net ? reinterpret_cast<float2*>(base + L.u0) : nullptr;
 
   cudaMemsetAsync(vstatus, 0, sizeof(int), st);
+  hs::vcycle_prepare(H, vws, st);
   if (a->x0) cudaMemcpyAsync(a->x, a->x0, (size_t)a->B * N * sizeof(double2), cudaMemcpyDeviceToDevice, st);
   hs::krylov_init(d, s, a->tol, a->iter_cap, a->x0 != nullptr, st);
   if ((rc = check_cuda("fgmres init")) != HS_OK) return rc;

@@ -13,6 +13,8 @@
 // The coarsest level runs k_coarse_gmres: the reference's 10-step GMRES with
 // a damped-Jacobi preconditioner (coarse_solve, :232-244), one CTA per RHS,
 // basis kept in an L2-resident workspace, fp64 reductions.
+#include <algorithm>
+
 #include "common.cuh"
 #include "level.cuh"
 #include "prof.h"
@@ -20,167 +22,318 @@
 
 namespace hs {
 
-HS_DEV int floordiv2(int a) { return a >= 0 ? a / 2 : -((1 - a) / 2); }
-
 HS_DEV const float2* vin_ptr(const VecIn& v, int b) { return v.tab ? v.tab[b] : v.base + (long long)b * v.bstride; }
 HS_DEV float2* vout_ptr(const VecOut& v, int b) { return v.tab ? v.tab[b] : v.base + (long long)b * v.bstride; }
 
-// zero-padded region load: s[a*ry + c] = g[(ox+a)*ny + (oy+c)] * scale
-HS_DEV void load_region(float2* s, int rx, int ry, const float2* __restrict__ g, int nx, int ny, int ox,
-                        int oy, float scale) {
-  for (int t = threadIdx.x; t < rx * ry; t += blockDim.x) {
-    int a = t / ry, c = t - a * ry;
-    int i = ox + a, j = oy + c;
-    float2 v = make_float2(0.f, 0.f);
-    if (i >= 0 && i < nx && j >= 0 && j < ny) v = g[(long long)i * ny + j];
-    s[t] = cscale(v, scale);
+// ------------------------------------------------------------------ row-marching warps
+//
+// Both legs run one warp per (column block, band of rows): every lane owns two
+// adjacent columns (ja even, jb = ja + 1) and the warp marches down the rows,
+// keeping the three-row stencil windows of every intermediate (u0, u1 / u2) in
+// registers.  Left / right neighbours come from the adjacent lanes by shuffle,
+// so each stencil stage shrinks the valid column range by one column per side;
+// the warp's outermost lanes are halo lanes whose results are discarded.  Each
+// input row is read once per warp (HBM once, the band and column halos hit L2),
+// nothing is staged in shared memory and there are no block barriers.
+
+struct Pair {
+  float2 a, b;  // columns ja, jb = ja + 1
+};
+
+HS_DEV float2 shfl_up1(float2 v) {
+  return make_float2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
+}
+HS_DEV float2 shfl_dn1(float2 v) {
+  return make_float2(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
+}
+
+// row i of a field at the lane's two columns, zero outside the grid, times s
+HS_DEV Pair ld_pair(const float2* __restrict__ g, int nx, int ny, int i, int ja, float s) {
+  Pair r{make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  if (i >= 0 && i < nx) {
+    const float2* p = g + (long long)i * ny;
+    if (ja >= 0 && ja < ny) r.a = cscale(p[ja], s);
+    if (ja + 1 >= 0 && ja + 1 < ny) r.b = cscale(p[ja + 1], s);
   }
+  return r;
+}
+
+HS_DEV float2 sum4(float2 a, float2 b, float2 c, float2 d) {
+  return make_float2((a.x + b.x) + (c.x + d.x), (a.y + b.y) + (c.y + d.y));
+}
+
+// neighbour sums of row i at both columns from rows up = i-1, mid = i, dn = i+1
+HS_DEV Pair nbsum_pair(const Pair& up, const Pair& mid, const Pair& dn) {
+  const float2 left = shfl_up1(mid.b), right = shfl_dn1(mid.a);
+  return Pair{sum4(up.a, dn.a, mid.b, left), sum4(up.b, dn.b, right, mid.a)};
+}
+
+// one damped Jacobi sweep at row i (diagonal form, level.cuh), from u = 0 when !U0
+template <bool U0>
+HS_DEV Pair jacobi_pair(const Pair& dinv, const Pair& rhs, float inv_h2, const Pair& up, const Pair& mid,
+                        const Pair& dn, float w) {
+  if (U0) {
+    const Pair nb = nbsum_pair(up, mid, dn);
+    return Pair{jacobi_dd(dinv.a, inv_h2, w, mid.a, rhs.a, nb.a), jacobi_dd(dinv.b, inv_h2, w, mid.b, rhs.b, nb.b)};
+  }
+  return Pair{cscale(cmul(dinv.a, rhs.a), w), cscale(cmul(dinv.b, rhs.b), w)};
+}
+
+HS_DEV Pair mask_pair(Pair v, bool row_ok, bool oka, bool okb) {
+  const float2 z = make_float2(0.f, 0.f);
+  if (!(row_ok && oka)) v.a = z;
+  if (!(row_ok && okb)) v.b = z;
+  return v;
+}
+
+constexpr int kVcWarps = 4;          // warps per block (independent)
+constexpr int kDownQ = 29;           // coarse columns per down-leg warp (lanes 1..29)
+constexpr int kUpCols = 60;          // fine columns per up-leg warp (lanes 1..30)
+constexpr int kRing = 4;             // rows in flight per warp (cp.async ring depth)
+
+// Row staging: every lane copies its own two columns of a row into a per-warp
+// shared-memory ring with 8-byte cp.async (zero-filled outside the grid) and
+// reads them back after cp.async.wait_group, so kRing - 1 rows of every input
+// stay in flight without holding registers.
+HS_DEV void cpa8(uint32_t dst, const float2* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0) : "memory");
+}
+HS_DEV void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+HS_DEV void cpa_wait_ring() { asm volatile("cp.async.wait_group %0;\n" ::"n"(kRing - 1) : "memory"); }
+
+HS_DEV void issue_pair(uint32_t dst, const float2* __restrict__ g, int nx, int ny, int i, int ja) {
+  const bool rok = i >= 0 && i < nx;
+  const bool oka = rok && ja >= 0 && ja < ny, okb = rok && ja + 1 >= 0 && ja + 1 < ny;
+  const long long off = (long long)i * ny + ja;
+  cpa8(dst, oka ? g + off : g, oka);
+  cpa8(dst + 8, okb ? g + off + 1 : g, okb);
+}
+
+HS_DEV Pair read_pair(const float2* slot, float s) {
+  const float4 v = *reinterpret_cast<const float4*>(slot);
+  return Pair{make_float2(v.x * s, v.y * s), make_float2(v.z * s, v.w * s)};
 }
 
 // ------------------------------------------------------------------ down leg
+//
+//   u1 = u0 + w_pre (rhs - A u0)/diag      (jacobi_relax, multigrid.py:218-229)
+//   r  = rhs - A u1                         (:270)
+//   coarse_rhs = R r                        (restrict_full_weighting, :64-78)
+//
+// Lane l owns fine columns (2Q, 2Q+1) with Q = Q0 - 1 + l, so its odd column is
+// the centre of coarse column Q; lanes 1..29 emit.  A warp covers coarse rows
+// [K0, K1): u1 rows 2K0-1 .. 2K1+1, r rows 2K0 .. 2K1.  Ring slot of u1 row s:
+// rhs, diag and dinv of row s, u0 row s + 1.
 
-template <int CX, int CY>
-__global__ void __launch_bounds__(256) k_vc_down(LevelDev L, int ncx, int ncy, VecIn rhs_in, VecIn u0_in,
-                                                 const float2* const* active, const int* model_of,
-                                                 float w_pre, float2* __restrict__ coarse_out) {
-  constexpr int RX = 2 * CX + 3, RY = 2 * CY + 3;
-  constexpr int UX = RX + 2, UY = RY + 2;
-  __shared__ float2 s_rhs[RX * RY];
-  __shared__ float2 s_c[RX * RY];
-  __shared__ float2 s_u1[RX * RY];
-  __shared__ float2 s_u0[UX * UY];
-  const int b = blockIdx.y;
+constexpr int kDownSlot = 4 * 64;  // float2 per warp and ring slot
+constexpr int kUpSlot = 4 * 64;
+
+template <bool U0>
+__global__ void __launch_bounds__(kVcWarps * 32) k_vc_down(LevelDev L, int ncx, int ncy, VecIn rhs_in, VecIn u0_in,
+                                                           const float2* const* active, const int* model_of,
+                                                           float w_pre, float2* __restrict__ coarse_out, int ncb,
+                                                           int band) {
+  extern __shared__ __align__(16) float2 vc_smem[];
+  const int lane = threadIdx.x & 31;
+  const int wid = blockIdx.y * kVcWarps + (threadIdx.x >> 5);
+  const int nbands = (ncx + band - 1) / band;
+  if (wid >= ncb * nbands) return;
+  const int b = blockIdx.x;
   if (active && active[b] == nullptr) return;
-  const int tiles_y = (ncy + CY - 1) / CY;
-  const int K0 = (blockIdx.x / tiles_y) * CX, L0 = (blockIdx.x % tiles_y) * CY;
-  const int ox = 2 * K0 - 1, oy = 2 * L0 - 1;
-  const long long N = (long long)L.nx * L.ny;
-  const int model = model_of ? model_of[b] : 0;
-  const float2* rhs = vin_ptr(rhs_in, b);
+  const int Q0 = (wid % ncb) * kDownQ, K0 = (wid / ncb) * band, K1 = min(ncx, K0 + band);
+  const int Q = Q0 - 1 + lane, ja = 2 * Q;
+  const int nx = L.nx, ny = L.ny;
+  const bool oka = ja >= 0 && ja < ny, okb = ja + 1 >= 0 && ja + 1 < ny;
+  const bool emit = lane >= 1 && lane <= kDownQ && Q < ncy;
+  const long long N = (long long)nx * ny;
+  const long long moff = (model_of ? model_of[b] : 0) * N;
+  const float2* __restrict__ dg = L.diag + moff;
+  const float2* __restrict__ di = L.dinv + moff;
+  const float ih2 = L.inv_h2;
+  const float2* __restrict__ rhs = vin_ptr(rhs_in, b);
   const float rs = rhs_in.scale ? rhs_in.scale[b] : 1.f;
-  const float2* u0 = (u0_in.tab || u0_in.base) ? vin_ptr(u0_in, b) : nullptr;
-  load_region(s_rhs, RX, RY, rhs, L.nx, L.ny, ox, oy, rs);
-  load_region(s_c, RX, RY, L.mass + model * N, L.nx, L.ny, ox, oy, 1.f);
-  if (u0) load_region(s_u0, UX, UY, u0, L.nx, L.ny, ox - 1, oy - 1, u0_in.scale ? u0_in.scale[b] : 1.f);
-  __syncthreads();
-  // pre-smoothing on the region (one damped Jacobi sweep)
-  for (int t = threadIdx.x; t < RX * RY; t += blockDim.x) {
-    int a = t / RY, c = t - a * RY;
-    int i = ox + a, j = oy + c;
-    float2 u1 = make_float2(0.f, 0.f);
-    if (i >= 0 && i < L.nx && j >= 0 && j < L.ny) {
-      float2 cc = s_c[t];
-      float2 d = level_diag(L, cc, i, j);
-      if (u0) {
-        const float2* q = s_u0 + (a + 1) * UY + (c + 1);
-        float2 au = level_apply(L, cc, i, j, q[0], q[UY], q[-UY], q[1], q[-1]);
-        u1 = cadd(q[0], cscale(cdiv(csub(s_rhs[t], au), d), w_pre));
+  const float2* __restrict__ u0 = U0 ? vin_ptr(u0_in, b) : nullptr;
+  const float us = (U0 && u0_in.scale) ? u0_in.scale[b] : 1.f;
+  float2* __restrict__ co = coarse_out + (long long)b * ncx * ncy;
+  float2* ring = vc_smem + (threadIdx.x >> 5) * kRing * kDownSlot;
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring) + lane * 16;
+
+  const int s0 = 2 * K0 - 1, s1 = 2 * K1 + 1;  // u1 rows
+  auto issue = [&](int s) {
+    if (s <= s1) {
+      const uint32_t d = ring_s + (((unsigned)(s - s0) % kRing) * kDownSlot * 8);
+      issue_pair(d, rhs, nx, ny, s, ja);
+      issue_pair(d + 512, dg, nx, ny, s, ja);
+      issue_pair(d + 1024, di, nx, ny, s, ja);
+      if (U0) issue_pair(d + 1536, u0, nx, ny, s + 1, ja);
+    }
+    cpa_commit();
+  };
+#pragma unroll
+  for (int k = 0; k < kRing - 1; ++k) issue(s0 + k);
+  const Pair z{make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  Pair u0m = z, u0c = z, u0p = z;
+  if (U0) {
+    u0c = ld_pair(u0, nx, ny, s0 - 1, ja, us);
+    u0p = ld_pair(u0, nx, ny, s0, ja, us);
+  }
+  Pair rh_m = z, dg_m = z, u1m2 = z, u1m1 = z;
+  float2 acc = make_float2(0.f, 0.f);
+  for (int s = s0; s <= s1; ++s) {
+    issue(s + kRing - 1);
+    cpa_wait_ring();
+    const float2* slot = ring + ((unsigned)(s - s0) % kRing) * kDownSlot + 2 * lane;
+    const Pair rh_c = read_pair(slot, rs), dg_c = read_pair(slot + 64, 1.f), di_c = read_pair(slot + 128, 1.f);
+    if (U0) {
+      u0m = u0c;
+      u0c = u0p;
+      u0p = read_pair(slot + 192, us);
+    }
+    const bool row_ok = s >= 0 && s < nx;
+    const Pair u1 = mask_pair(jacobi_pair<U0>(di_c, rh_c, ih2, u0m, u0c, u0p, w_pre), row_ok, oka, okb);
+    // residual of row i = s - 1 from u1 rows s-2, s-1, s
+    const int i = s - 1;
+    if (i >= 2 * K0) {
+      const Pair nb = nbsum_pair(u1m2, u1m1, u1);
+      Pair r;
+      r.a = csub(rh_m.a, apply_dd(dg_m.a, ih2, u1m1.a, nb.a));
+      r.b = csub(rh_m.b, apply_dd(dg_m.b, ih2, u1m1.b, nb.b));
+      r = mask_pair(r, i < nx, oka, okb);
+      // horizontal full weighting centred on the odd column jb
+      const float2 rr = shfl_dn1(r.a);
+      const float2 hr = cadd(cadd(cscale(r.a, 0.25f), cscale(r.b, 0.5f)), cscale(rr, 0.25f));
+      if ((i & 1) == 0) {
+        if (i > 2 * K0 && emit) co[(long long)(i / 2 - 1) * ncy + Q] = cadd(acc, cscale(hr, 0.25f));
+        acc = cscale(hr, 0.25f);
       } else {
-        u1 = cscale(cdiv(s_rhs[t], d), w_pre);
+        acc = cadd(acc, cscale(hr, 0.5f));
       }
     }
-    s_u1[t] = u1;
-  }
-  __syncthreads();
-  // residual on the interior of the region, in place over s_rhs
-  for (int t = threadIdx.x; t < (RX - 2) * (RY - 2); t += blockDim.x) {
-    int a = t / (RY - 2) + 1, c = t % (RY - 2) + 1;
-    int i = ox + a, j = oy + c;
-    int p = a * RY + c;
-    float2 r = make_float2(0.f, 0.f);
-    if (i >= 0 && i < L.nx && j >= 0 && j < L.ny) {
-      const float2* q = s_u1 + p;
-      r = csub(s_rhs[p], level_apply(L, s_c[p], i, j, q[0], q[RY], q[-RY], q[1], q[-1]));
-    }
-    s_rhs[p] = r;
-  }
-  __syncthreads();
-  // full-weighting restriction centred on fine 2K+1
-  const float fw[3] = {0.25f, 0.5f, 0.25f};
-  for (int t = threadIdx.x; t < CX * CY; t += blockDim.x) {
-    int k = t / CY, l = t - k * CY;
-    int K = K0 + k, Lq = L0 + l;
-    if (K >= ncx || Lq >= ncy) continue;
-    float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int u = 0; u < 3; ++u)
-#pragma unroll
-      for (int v = 0; v < 3; ++v) acc = cadd(acc, cscale(s_rhs[(2 * k + 1 + u) * RY + 2 * l + 1 + v], fw[u] * fw[v]));
-    coarse_out[(long long)b * ncx * ncy + (long long)K * ncy + Lq] = acc;
+    u1m2 = u1m1;
+    u1m1 = u1;
+    rh_m = rh_c;
+    dg_m = dg_c;
   }
 }
 
 // ------------------------------------------------------------------ up leg
+//
+//   u2 = u1 + P e_coarse                    (prolong_bilinear, multigrid.py:81-114, :273)
+//   u3 = u2 + w_post (rhs - A u2)/diag      (:274)
+// with u1 recomputed from rhs and u0 (cheaper than storing it).  Lane l owns
+// fine columns (c0 + 2l, c0 + 2l + 1), c0 = 60 cb - 2; lanes 1..30 emit.  A
+// warp covers fine rows [R0, R1): u2 rows R0-1 .. R1.  Ring slot of u2 row s:
+// rhs and dinv of row s, u0 row s + 1 and, for even s, coarse error row s / 2
+// at coarse column Q = ja / 2.
 
-template <int FX, int FY>
-__global__ void __launch_bounds__(256) k_vc_up(LevelDev L, int ncx, int ncy, VecIn rhs_in, VecIn u0_in,
-                                               const float2* const* active, const int* model_of, float w_pre,
-                                               float w_post, const float2* __restrict__ ecoarse, VecOut out) {
-  constexpr int RX = FX + 2, RY = FY + 2;
-  constexpr int UX = FX + 4, UY = FY + 4;
-  constexpr int EX = FX / 2 + 3, EY = FY / 2 + 3;
-  __shared__ float2 s_rhs[RX * RY];
-  __shared__ float2 s_c[RX * RY];
-  __shared__ float2 s_u2[RX * RY];
-  __shared__ float2 s_u0[UX * UY];
-  __shared__ float2 s_e[EX * EY];
-  const int b = blockIdx.y;
+// horizontally prolonged coarse row at the lane's columns from its value v at
+// column Q = ja / 2: even column ja takes (e[Q-1] + e[Q]) / 2, odd jb takes e[Q]
+HS_DEV Pair prolong_pair(float2 v) {
+  const float2 vm = shfl_up1(v);
+  return Pair{cscale(cadd(vm, v), 0.5f), v};
+}
+
+template <bool U0>
+__global__ void __launch_bounds__(kVcWarps * 32) k_vc_up(LevelDev L, int ncx, int ncy, VecIn rhs_in, VecIn u0_in,
+                                                         const float2* const* active, const int* model_of,
+                                                         float w_pre, float w_post, const float2* __restrict__ ecoarse,
+                                                         VecOut out, int ncb, int band) {
+  extern __shared__ __align__(16) float2 vc_smem[];
+  const int lane = threadIdx.x & 31;
+  const int wid = blockIdx.y * kVcWarps + (threadIdx.x >> 5);
+  const int nx = L.nx, ny = L.ny;
+  const int nbands = (nx + band - 1) / band;
+  if (wid >= ncb * nbands) return;
+  const int b = blockIdx.x;
   if (active && active[b] == nullptr) return;
-  const int tiles_y = (L.ny + FY - 1) / FY;
-  const int x0 = (blockIdx.x / tiles_y) * FX, y0 = (blockIdx.x % tiles_y) * FY;
-  const long long N = (long long)L.nx * L.ny;
-  const int model = model_of ? model_of[b] : 0;
-  const float2* rhs = vin_ptr(rhs_in, b);
+  const int c0 = (wid % ncb) * kUpCols - 2, R0 = (wid / ncb) * band, R1 = min(nx, R0 + band);
+  const int ja = c0 + 2 * lane, Q = ja / 2;  // c0 even, so ja / 2 is exact (Q = -1 only on a halo lane)
+  const bool oka = ja >= 0 && ja < ny, okb = ja + 1 >= 0 && ja + 1 < ny;
+  const bool emit = lane >= 1 && lane <= 30;
+  const bool okq = Q >= 0 && Q < ncy;
+  const long long N = (long long)nx * ny;
+  const float2* __restrict__ di = L.dinv + (model_of ? model_of[b] : 0) * N;
+  const float ih2 = L.inv_h2;
+  const float2* __restrict__ rhs = vin_ptr(rhs_in, b);
   const float rs = rhs_in.scale ? rhs_in.scale[b] : 1.f;
-  const float2* u0 = (u0_in.tab || u0_in.base) ? vin_ptr(u0_in, b) : nullptr;
-  const int kx0 = floordiv2(x0 - 3), ky0 = floordiv2(y0 - 3);
-  load_region(s_rhs, RX, RY, rhs, L.nx, L.ny, x0 - 1, y0 - 1, rs);
-  load_region(s_c, RX, RY, L.mass + model * N, L.nx, L.ny, x0 - 1, y0 - 1, 1.f);
-  load_region(s_e, EX, EY, ecoarse + (long long)b * ncx * ncy, ncx, ncy, kx0, ky0, 1.f);
-  if (u0) load_region(s_u0, UX, UY, u0, L.nx, L.ny, x0 - 2, y0 - 2, u0_in.scale ? u0_in.scale[b] : 1.f);
-  __syncthreads();
-  for (int t = threadIdx.x; t < RX * RY; t += blockDim.x) {
-    int a = t / RY, c = t - a * RY;
-    int i = x0 - 1 + a, j = y0 - 1 + c;
-    float2 u2 = make_float2(0.f, 0.f);
-    if (i >= 0 && i < L.nx && j >= 0 && j < L.ny) {
-      float2 cc = s_c[t];
-      float2 d = level_diag(L, cc, i, j);
-      float2 u1;
-      if (u0) {
-        const float2* q = s_u0 + (a + 1) * UY + (c + 1);
-        float2 au = level_apply(L, cc, i, j, q[0], q[UY], q[-UY], q[1], q[-1]);
-        u1 = cadd(q[0], cscale(cdiv(csub(s_rhs[t], au), d), w_pre));
-      } else {
-        u1 = cscale(cdiv(s_rhs[t], d), w_pre);
+  const float2* __restrict__ u0 = U0 ? vin_ptr(u0_in, b) : nullptr;
+  const float us = (U0 && u0_in.scale) ? u0_in.scale[b] : 1.f;
+  const float2* __restrict__ e = ecoarse + (long long)b * ncx * ncy;
+  float2* __restrict__ dst = vout_ptr(out, b);
+  float2* ring = vc_smem + (threadIdx.x >> 5) * kRing * kUpSlot;
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring) + lane * 16;
+
+  const int s0 = R0 - 1, s1 = R1;  // u2 rows
+  auto issue = [&](int s) {
+    if (s <= s1) {
+      const uint32_t d = ring_s + (((unsigned)(s - s0) % kRing) * kUpSlot * 8);
+      issue_pair(d, rhs, nx, ny, s, ja);
+      issue_pair(d + 512, di, nx, ny, s, ja);
+      if (U0) issue_pair(d + 1024, u0, nx, ny, s + 1, ja);
+      if ((s & 1) == 0) {
+        const int K = s / 2;
+        const bool ok = okq && K < ncx;
+        cpa8(d + 1536, ok ? e + (long long)K * ncy + Q : e, ok);
       }
-      // P e: coarse K contributes to fine i when i - 2K in {0, 1, 2}
-      int kxa = (i & 1) ? (i - 1) / 2 : i / 2 - 1, kxb = (i & 1) ? kxa : i / 2;
-      int kya = (j & 1) ? (j - 1) / 2 : j / 2 - 1, kyb = (j & 1) ? kya : j / 2;
-      float2 pe = make_float2(0.f, 0.f);
-      for (int K = kxa; K <= kxb; ++K) {
-        float wx = prolong_w(i - 2 * K);
-        for (int Q = kya; Q <= kyb; ++Q) {
-          float wy = prolong_w(j - 2 * Q);
-          pe = cadd(pe, cscale(s_e[(K - kx0) * EY + (Q - ky0)], wx * wy));
-        }
-      }
-      u2 = cadd(u1, pe);
     }
-    s_u2[t] = u2;
+    cpa_commit();
+  };
+#pragma unroll
+  for (int k = 0; k < kRing - 1; ++k) issue(s0 + k);
+  const Pair z{make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  Pair u0m = z, u0c = z, u0p = z;
+  if (U0) {
+    u0c = ld_pair(u0, nx, ny, s0 - 1, ja, us);
+    u0p = ld_pair(u0, nx, ny, s0, ja, us);
   }
-  __syncthreads();
-  float2* dst = vout_ptr(out, b);
-  for (int t = threadIdx.x; t < FX * FY; t += blockDim.x) {
-    int a = t / FY + 1, c = t % FY + 1;
-    int i = x0 - 1 + a, j = y0 - 1 + c;
-    if (i >= L.nx || j >= L.ny) continue;
-    int p = a * RY + c;
-    const float2* q = s_u2 + p;
-    float2 cc = s_c[p];
-    float2 au = level_apply(L, cc, i, j, q[0], q[RY], q[-RY], q[1], q[-1]);
-    float2 u3 = cadd(q[0], cscale(cdiv(csub(s_rhs[p], au), level_diag(L, cc, i, j)), w_post));
-    dst[(long long)i * L.ny + j] = u3;
+  Pair rh_m = z, di_m = z, u2m2 = z, u2m1 = z;
+  // hcur = prolonged coarse row below the first u2 row: K = (s0-1)/2 for odd s0,
+  // s0/2 - 1 for even s0 (s0 >= -1; K = -1 is a zero row)
+  Pair hcur = z;
+  {
+    const int K = (s0 & 1) ? (s0 - 1) / 2 : s0 / 2 - 1;
+    float2 v = make_float2(0.f, 0.f);
+    if (okq && K >= 0 && K < ncx) v = e[(long long)K * ncy + Q];
+    hcur = prolong_pair(v);
+  }
+  for (int s = s0; s <= s1; ++s) {
+    issue(s + kRing - 1);
+    cpa_wait_ring();
+    const float2* slot = ring + ((unsigned)(s - s0) % kRing) * kUpSlot + 2 * lane;
+    const Pair rh_c = read_pair(slot, rs), di_c = read_pair(slot + 64, 1.f);
+    if (U0) {
+      u0m = u0c;
+      u0c = u0p;
+      u0p = read_pair(slot + 128, us);
+    }
+    // P e at row s: odd s = 2K+1 -> h(K); even s = 2K -> (h(K-1) + h(K)) / 2
+    Pair pe;
+    if ((s & 1) == 0) {
+      const Pair hprev = hcur;
+      hcur = prolong_pair(slot[192]);
+      pe.a = cscale(cadd(hprev.a, hcur.a), 0.5f);
+      pe.b = cscale(cadd(hprev.b, hcur.b), 0.5f);
+    } else {
+      pe = hcur;
+    }
+    Pair u2 = jacobi_pair<U0>(di_c, rh_c, ih2, u0m, u0c, u0p, w_pre);
+    u2.a = cadd(u2.a, pe.a);
+    u2.b = cadd(u2.b, pe.b);
+    u2 = mask_pair(u2, s >= 0 && s < nx, oka, okb);
+    // post-smoothing of row i = s - 1 from u2 rows s-2, s-1, s
+    const int i = s - 1;
+    if (i >= R0) {
+      const Pair u3 = jacobi_pair<true>(di_m, rh_m, ih2, u2m2, u2m1, u2, w_post);
+      if (emit) {
+        float2* row = dst + (long long)i * ny;
+        if (oka) row[ja] = u3.a;
+        if (okb) row[ja + 1] = u3.b;
+      }
+    }
+    u2m2 = u2m1;
+    u2m1 = u2;
+    rh_m = rh_c;
+    di_m = di_c;
   }
 }
 
@@ -417,8 +570,20 @@ void launch_coarse(LevelDev L, const float2* rhs, float2* x, float2* vws, float2
 namespace hs {
 
 namespace {
-constexpr int kDownCX = 8, kDownCY = 32;
-constexpr int kUpFX = 16, kUpFY = 64;
+constexpr int kDownSmem = kVcWarps * kRing * kDownSlot * 8;
+constexpr int kUpSmem = kVcWarps * kRing * kUpSlot * 8;
+
+// rows per warp band: enough (column block, band) warps to fill every SM
+// ~32 warps deep over the batch, but never bands shorter than `min_rows`
+// (each band re-reads a few halo rows)
+int band_rows(int rows, int ncb, int B, int min_rows) {
+  const long target = 148L * 32;
+  long nb = (target + (long)ncb * B - 1) / ((long)ncb * B);
+  long cap = rows / min_rows;
+  if (nb > cap) nb = cap;
+  if (nb < 1) nb = 1;
+  return (int)((rows + nb - 1) / nb);
+}
 
 __global__ void k_gather_scaled(VecIn in, const float2* const* active, float2* out, long long N) {
   const int b = blockIdx.y;
@@ -438,10 +603,32 @@ __global__ void k_scatter(const float2* in, const float2* const* active, VecOut 
 }
 
 size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
+
+// diag / dinv planes of every level (vcycle_prepare), at the head of the workspace
+size_t planes_bytes(const Hierarchy& H) {
+  size_t total = 0;
+  for (int l = 0; l < H.num_levels; ++l) total += 2 * align_up((size_t)H.n_models * H.lv[l].nx * H.lv[l].ny * sizeof(float2));
+  return total;
+}
+
+// diag = 4/h^2 - c + wall (level_diag, fp32 as before) and dinv = 1 / diag
+// (fp64 division, rounded once) for every model of a level
+__global__ void k_level_planes(LevelDev L, int n_models, float2* diag, float2* dinv) {
+  const long long N = (long long)L.nx * L.ny, total = N * n_models;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long p = q % N;
+    const int i = (int)(p / L.ny), j = (int)(p - (long long)i * L.ny);
+    const float2 d = level_diag(L, L.mass[q], i, j);
+    const double den = (double)d.x * d.x + (double)d.y * d.y;
+    diag[q] = d;
+    dinv[q] = make_float2((float)(d.x / den), (float)(-d.y / den));
+  }
+}
 }  // namespace
 
 size_t vcycle_workspace_bytes(const Hierarchy& H, int B) {
-  size_t total = 0;
+  size_t total = planes_bytes(H);
   for (int l = 1; l < H.num_levels; ++l) {
     size_t n = (size_t)H.lv[l].nx * H.lv[l].ny;
     total += 2 * align_up(n * B * sizeof(float2));  // rhs_l and e_l
@@ -454,9 +641,26 @@ size_t vcycle_workspace_bytes(const Hierarchy& H, int B) {
   return total;
 }
 
-void vcycle(const Hierarchy& H, VecIn rhs, VecIn u0, VecOut out, const float2* const* active,
-            const int* model_of, int B, void* ws, int* status, cudaStream_t stream) {
+void vcycle_prepare(Hierarchy& H, void* ws, cudaStream_t stream) {
   char* p = static_cast<char*>(ws);
+  for (int l = 0; l < H.num_levels; ++l) {
+    LevelDev& L = H.lv[l];
+    const size_t n = (size_t)H.n_models * L.nx * L.ny;
+    float2* dg = reinterpret_cast<float2*>(p);
+    p += align_up(n * sizeof(float2));
+    float2* di = reinterpret_cast<float2*>(p);
+    p += align_up(n * sizeof(float2));
+    k_level_planes<<<(unsigned)std::min<size_t>(cdiv_u((long)n, 256), 4 * 148), 256, 0, stream>>>(L, H.n_models, dg, di);
+    L.diag = dg;
+    L.dinv = di;
+  }
+}
+
+void vcycle(const Hierarchy& H_in, VecIn rhs, VecIn u0, VecOut out, const float2* const* active,
+            const int* model_of, int B, void* ws, int* status, cudaStream_t stream) {
+  Hierarchy H = H_in;
+  if (!H.lv[0].dinv) vcycle_prepare(H, ws, stream);  // stand-alone call: derive the planes now
+  char* p = static_cast<char*>(ws) + planes_bytes(H);
   float2* lrhs[kMaxLevels] = {nullptr};
   float2* lerr[kMaxLevels] = {nullptr};
   for (int l = 1; l < H.num_levels; ++l) {
@@ -487,8 +691,8 @@ void vcycle(const Hierarchy& H, VecIn rhs, VecIn u0, VecOut out, const float2* c
   }
   // Algorithmic HBM bytes: per RHS and non-coarsest level,
   // down = rhs 8N + coarse 2N, up = rhs 8N + e 2N + out 8N (+ u0 8N twice at
-  // level 0); the complex64 medium (8N) is read once per slowness model per
-  // kernel (it is shared by every RHS of that model and stays in L2).
+  // level 0); the complex64 diag / dinv planes (16N down, 8N up) are read once
+  // per slowness model per kernel (shared by every RHS of that model, L2-hot).
   const bool has_u0 = (u0.tab || u0.base);
   const double nact = prof::active_hint(B);
   double vc_bytes = 0.0;
@@ -499,11 +703,17 @@ void vcycle(const Hierarchy& H, VecIn rhs, VecIn u0, VecOut out, const float2* c
     const int ncx = H.lv[l + 1].nx, ncy = H.lv[l + 1].ny;
     VecIn in = l == 0 ? rhs : VecIn{nullptr, lrhs[l], (long long)F.nx * F.ny, nullptr};
     VecIn uz = l == 0 ? u0 : VecIn{nullptr, nullptr, 0, nullptr};
-    dim3 g(cdiv_u(ncx, kDownCX) * cdiv_u(ncy, kDownCY), B);
-    k_vc_down<kDownCX, kDownCY><<<g, 256, 0, stream>>>(F, ncx, ncy, in, uz, active, model_of, H.w_pre,
-                                                        lrhs[l + 1]);
+    const int ncb = (int)cdiv_u(ncy, kDownQ);
+    const int band = band_rows(ncx, ncb, B, 4);
+    dim3 g(B, cdiv_u((long)ncb * cdiv_u(ncx, band), kVcWarps));  // RHS fastest: the planes stay L2-hot
+    if (uz.tab || uz.base)
+      k_vc_down<true><<<g, kVcWarps * 32, kDownSmem, stream>>>(F, ncx, ncy, in, uz, active, model_of, H.w_pre, lrhs[l + 1],
+                                                       ncb, band);
+    else
+      k_vc_down<false><<<g, kVcWarps * 32, kDownSmem, stream>>>(F, ncx, ncy, in, uz, active, model_of, H.w_pre,
+                                                        lrhs[l + 1], ncb, band);
     const double N = (double)F.nx * F.ny;
-    vc_bytes += nact * (10.0 * N + ((l == 0 && has_u0) ? 8.0 * N : 0.0)) + H.n_models * 8.0 * N;
+    vc_bytes += nact * (10.0 * N + ((l == 0 && has_u0) ? 8.0 * N : 0.0)) + H.n_models * 16.0 * N;
   }
   // coarsest
   launch_coarse(C, lrhs[Lc], lerr[Lc], cV, cS, active, model_of, H.coarse_iters, H.coarse_damping, status, B, stream);
@@ -515,12 +725,18 @@ void vcycle(const Hierarchy& H, VecIn rhs, VecIn u0, VecOut out, const float2* c
     VecIn in = l == 0 ? rhs : VecIn{nullptr, lrhs[l], (long long)F.nx * F.ny, nullptr};
     VecIn uz = l == 0 ? u0 : VecIn{nullptr, nullptr, 0, nullptr};
     VecOut o = l == 0 ? out : VecOut{nullptr, lerr[l], (long long)F.nx * F.ny};
-    dim3 g(cdiv_u(F.nx, kUpFX) * cdiv_u(F.ny, kUpFY), B);
+    const int ncb = (int)cdiv_u(F.ny, kUpCols);
+    const int band = band_rows(F.nx, ncb, B, 8);
+    dim3 g(B, cdiv_u((long)ncb * cdiv_u(F.nx, band), kVcWarps));
     const double N = (double)F.nx * F.ny;
     const double up_bytes = nact * (18.0 * N + ((l == 0 && has_u0) ? 8.0 * N : 0.0)) + H.n_models * 8.0 * N;
     const int uslot = l == 0 ? prof::start(prof::VC_UP0, stream) : -1;
-    k_vc_up<kUpFX, kUpFY><<<g, 256, 0, stream>>>(F, ncx, ncy, in, uz, active, model_of, H.w_pre, H.w_post,
-                                                 lerr[l + 1], o);
+    if (uz.tab || uz.base)
+      k_vc_up<true><<<g, kVcWarps * 32, kUpSmem, stream>>>(F, ncx, ncy, in, uz, active, model_of, H.w_pre, H.w_post,
+                                                     lerr[l + 1], o, ncb, band);
+    else
+      k_vc_up<false><<<g, kVcWarps * 32, kUpSmem, stream>>>(F, ncx, ncy, in, uz, active, model_of, H.w_pre, H.w_post,
+                                                      lerr[l + 1], o, ncb, band);
     prof::stop(uslot, stream, up_bytes);
     vc_bytes += up_bytes;
   }

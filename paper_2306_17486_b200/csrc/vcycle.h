@@ -39,6 +39,11 @@ struct Hierarchy {
 // Workspace (bytes) for a V-cycle over B right-hand sides.
 size_t vcycle_workspace_bytes(const Hierarchy& H, int B);
 
+// Derive the per-level diag / dinv planes into the head of `ws` and point H's
+// levels at them.  vcycle() does this itself when H is not prepared; a solve
+// that runs many V-cycles with one workspace prepares once.
+void vcycle_prepare(Hierarchy& H, void* ws, cudaStream_t stream);
+
 // z = V-cycle(rhs, u0) for every RHS whose `active` entry is non-null (or all
 // RHS when active == nullptr).  Asynchronous on `stream`.
 void vcycle(const Hierarchy& H, VecIn rhs, VecIn u0, VecOut out, const float2* const* active,
