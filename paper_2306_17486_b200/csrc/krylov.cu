@@ -81,6 +81,10 @@ __global__ void __launch_bounds__(NT) k_arnoldi(SolveDims d, SolveBuffers s, int
   if (!active) return;
   if ((MODE == REDOT || MODE == ORTH2) && !reorth) return;
   const int j = S.j, J = j + 1, m = d.restart;
+  // dot passes: only the chunks holding v_0..v_j do work (and take part in the
+  // last-block count); the rest exit before touching memory
+  const int live = (MODE == DOT || MODE == REDOT) ? min(nchunks, (J + KC - 1) / KC) : nchunks;
+  if (chunk >= live) return;
   const int N = (int)d.N;
   const float2* Vb = s.V + (long long)b * (m + 1) * N;
   const float2* zb = s.Z + ((long long)b * m + j) * N;
@@ -128,7 +132,7 @@ __global__ void __launch_bounds__(NT) k_arnoldi(SolveDims d, SolveBuffers s, int
 #pragma unroll
   for (int t = 0; t < PST; ++t)  // constant indices keep acc[] in registers
     if (threadIdx.x == t) part[t] = acc[t];
-  if (!arrive_last(&s.counter[b], nchunks * d.nblk)) return;
+  if (!arrive_last(&s.counter[b], live * d.nblk)) return;
   // ---- finish (one block per RHS)
   const double* pb = s.partial + (long long)b * nchunks * d.nblk * PST;
   if (MODE == DOT || MODE == REDOT) {
