@@ -553,10 +553,310 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_gmres(LevelDev L, con
   }
 }
 
+// Small coarsest grids (N <= 512 * 8 nodes: C1's 32^2, C2's 64^2): the same
+// GMRES with the vector being expanded kept on chip.  Each thread owns nodes
+// p = t + 512 u (u < 8) and keeps the unnormalised V_j of those nodes in
+// registers; z_j = S v_j / h is staged in shared memory so the stencil reads
+// its neighbours on chip; the operator is the diagonal form (diag / dinv
+// planes, level.cuh); the stored basis V_1..V_j is read back from the
+// L2-resident workspace two nodes x every k at a time, so each Gram-Schmidt
+// pass costs a few L2 round trips instead of one per node and vector.
+// Gram-Schmidt passes of the fast coarse GMRES over the thread's nodes, with
+// the number of basis vectors JJ a compile-time constant (dispatched on the
+// window position), so every loop is unrolled without guards.
+// dots: acc[1 + 2k] + i acc[2 + 2k] += conj(v_k) w, k < JJ (v_0 = rhs)
+template <int JJ, int NACC>
+HS_DEV void coarse_dots(double (&acc)[NACC], const float2* __restrict__ rhs, const float2* __restrict__ V, int N,
+                        const float2* ws) {
+  for (int p = threadIdx.x; p < N; p += blockDim.x) {
+    float2 q[JJ];
+    q[0] = rhs[p];
+#pragma unroll
+    for (int k = 1; k < JJ; ++k) q[k] = V[k * N + p];
+    const double2 wd = f2d(ws[p]);
+#pragma unroll
+    for (int k = 0; k < JJ; ++k) {
+      const double2 d = zcmul(f2d(q[k]), wd);
+      acc[1 + 2 * k] += d.x;
+      acc[2 + 2 * k] += d.y;
+    }
+  }
+}
+// orth: w -= sum_k coef_k v_k, k < JJ; returns the thread's part of ||w||^2
+template <int JJ>
+HS_DEV double coarse_orth(const float2* __restrict__ rhs, const float2* __restrict__ V, int N, float2* ws,
+                          const float2* coef) {
+  float2 c[JJ];
+#pragma unroll
+  for (int k = 0; k < JJ; ++k) c[k] = coef[k];
+  double nn = 0.0;
+  for (int p = threadIdx.x; p < N; p += blockDim.x) {
+    float2 q[JJ];
+    q[0] = rhs[p];
+#pragma unroll
+    for (int k = 1; k < JJ; ++k) q[k] = V[k * N + p];
+    float2 wv = ws[p];
+#pragma unroll
+    for (int k = 0; k < JJ; ++k) wv = csub(wv, cmul(c[k], q[k]));
+    ws[p] = wv;
+    nn += (double)wv.x * wv.x + (double)wv.y * wv.y;
+  }
+  return nn;
+}
+
+#define HS_COARSE_SWITCH(J, CALL) \
+  switch (J) {                    \
+    case 1: CALL(1); break;       \
+    case 2: CALL(2); break;       \
+    case 3: CALL(3); break;       \
+    case 4: CALL(4); break;       \
+    case 5: CALL(5); break;       \
+    case 6: CALL(6); break;       \
+    case 7: CALL(7); break;       \
+    case 8: CALL(8); break;       \
+    case 9: CALL(9); break;       \
+    default: CALL(10); break;     \
+  }
+
+constexpr int kCoarseFastNpt = 8;
+constexpr int kCoarseFastMax = kCoarseThreads * kCoarseFastNpt;
+
+template <int MI>
+__global__ void __launch_bounds__(kCoarseThreads, 1)
+    k_coarse_gmres_fast(LevelDev L, const float2* __restrict__ rhs_base, float2* __restrict__ x_out, float2* vws,
+                        const float2* const* active, const int* model_of, int m, float damping, int* status) {
+  constexpr int NACC = 2 * (MI + 1) + 1;
+  constexpr int NPT = kCoarseFastNpt;
+  __shared__ double red[NACC * (kCoarseThreads / 32 + 1)];
+  extern __shared__ __align__(16) float2 coarse_dyn[];
+  float2* zs = coarse_dyn;                   // z_j = S v_j / h_j
+  float2* ws = coarse_dyn + kCoarseFastMax;  // unnormalised V_j, then w
+  __shared__ double2 H[(MI + 1) * MI];
+  __shared__ double2 gv[MI + 1], sn[MI], yv[MI];
+  __shared__ double cs[MI], vs[MI + 1];
+  __shared__ double2 hc[MI + 1];
+  __shared__ float2 scoef[MI + 1];
+  __shared__ int s_flag, s_jend;
+  const int b = blockIdx.x;
+  if (active && active[b] == nullptr) return;
+  const int nx = L.nx, ny = L.ny, N = nx * ny;
+  const float ih2 = L.inv_h2;
+  const float2* rhs = rhs_base + (long long)b * N;
+  float2* V = vws + (long long)b * (m + 1) * N;  // slots 1..m used
+  float2* x = x_out + (long long)b * N;
+  const long long moff = (long long)(model_of ? model_of[b] : 0) * N;
+  const float2* __restrict__ dg = L.diag + moff;
+  const float2* __restrict__ di = L.dinv + moff;
+  auto vec = [&](int k) -> const float2* { return k == 0 ? rhs : V + (long long)k * N; };
+  const int t = threadIdx.x;
+
+  double acc[NACC];
+  acc[0] = 0.0;
+#pragma unroll
+  for (int u = 0; u < NPT; ++u) {
+    const int p = t + u * kCoarseThreads;
+    const float2 r = p < N ? rhs[p] : make_float2(0.f, 0.f);
+    if (p < N) ws[p] = r;
+    acc[0] += (double)r.x * r.x + (double)r.y * r.y;
+  }
+  block_sum_n<NACC>(acc, 1, red);
+  const double beta0 = sqrt(acc[0]);
+  if (beta0 == 0.0) {
+#pragma unroll
+    for (int u = 0; u < NPT; ++u) {
+      const int p = t + u * kCoarseThreads;
+      if (p < N) x[p] = make_float2(0.f, 0.f);
+    }
+    return;
+  }
+  if (t == 0) {
+    vs[0] = 1.0 / beta0;
+    gv[0] = make_double2(beta0, 0.0);
+    s_flag = 0;
+    s_jend = m;
+  }
+  __syncthreads();
+
+  for (int j = 0; j < m; ++j) {
+    const float sj = (float)vs[j];
+    // z_j = S v_j (S = damping / diag) into shared memory
+#pragma unroll
+    for (int u = 0; u < NPT; ++u) {
+      const int p = t + u * kCoarseThreads;
+      if (p < N) zs[p] = cscale(cmul(di[p], ws[p]), damping * sj);
+    }
+    __syncthreads();
+    // w = A z_j (diagonal form), ||w||^2
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
+    int bad = 0;
+#pragma unroll
+    for (int u = 0; u < NPT; ++u) {
+      const int p = t + u * kCoarseThreads;
+      float2 r = make_float2(0.f, 0.f);
+      if (p < N) {
+        const int i = p / ny, q = p - i * ny;
+        const float2 zero = make_float2(0.f, 0.f);
+        const float2 xp = i + 1 < nx ? zs[p + ny] : zero, xm = i > 0 ? zs[p - ny] : zero;
+        const float2 yp = q + 1 < ny ? zs[p + 1] : zero, ym = q > 0 ? zs[p - 1] : zero;
+        const float2 nb = make_float2((xp.x + xm.x) + (yp.x + ym.x), (xp.y + xm.y) + (yp.y + ym.y));
+        r = apply_dd(dg[p], ih2, zs[p], nb);
+      }
+      if (!isfinite(r.x) || !isfinite(r.y)) bad = 1;
+      if (p < N) ws[p] = r;
+      acc[0] += (double)r.x * r.x + (double)r.y * r.y;
+    }
+    // dots with v_0..v_j
+#define HS_DOTS(JJ) coarse_dots<JJ>(acc, rhs, V, N, ws)
+    HS_COARSE_SWITCH(j + 1, HS_DOTS)
+#undef HS_DOTS
+    __syncthreads();  // every thread is done with zs before the next step rewrites it
+    if (bad) atomicOr(&s_flag, 1);
+    block_sum<NACC>(acc, red);
+    if (s_flag) {
+      if (t == 0) atomicCAS(status, 0, HS_ENONFINITE);
+      return;
+    }
+    const double wn = sqrt(acc[0]);
+    if (t == 0)
+#pragma unroll
+      for (int k = 0; k <= MI; ++k)
+        if (k <= j) {
+          hc[k] = make_double2(acc[1 + 2 * k] * vs[k], acc[2 + 2 * k] * vs[k]);
+          H[k * MI + j] = hc[k];
+        }
+    __syncthreads();
+    double hn2 = 0.0;
+    for (int pass = 0; pass < 2; ++pass) {
+      // w -= sum_k hc_k v_k ; ||w||^2  (coefficients from shared memory)
+      if (t <= j) scoef[t] = make_float2((float)(hc[t].x * vs[t]), (float)(hc[t].y * vs[t]));
+      __syncthreads();
+#define HS_ORTH(JJ) acc[0] = coarse_orth<JJ>(rhs, V, N, ws, scoef)
+      HS_COARSE_SWITCH(j + 1, HS_ORTH)
+#undef HS_ORTH
+      block_sum<1>(*reinterpret_cast<double(*)[1]>(acc), red);
+      hn2 = acc[0];
+      if (pass == 1 || sqrt(hn2) >= 0.25 * wn) break;
+      // one re-orthogonalisation pass (krylov.py:105-111): extra = V^H w
+#pragma unroll
+      for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
+#pragma unroll 1
+      for (int u = 0; u < NPT; ++u) {
+        const int p = t + u * kCoarseThreads;
+        if (p >= N) continue;
+        const double2 wd = f2d(ws[p]);
+#pragma unroll
+        for (int k = 0; k <= MI; ++k)
+          if (k <= j) {
+            const double2 d = zcmul(f2d(vec(k)[p]), wd);
+            acc[2 * k] += d.x;
+            acc[2 * k + 1] += d.y;
+          }
+      }
+      block_sum<NACC>(acc, red);
+      if (t == 0)
+#pragma unroll
+        for (int k = 0; k <= MI; ++k)
+          if (k <= j) {
+            hc[k] = make_double2(acc[2 * k] * vs[k], acc[2 * k + 1] * vs[k]);
+            H[k * MI + j] = zadd(H[k * MI + j], hc[k]);
+          }
+      __syncthreads();
+    }
+    // store the unnormalised V_{j+1} for the later passes and the solution
+    if (j + 1 < m) {
+#pragma unroll
+      for (int u = 0; u < NPT; ++u) {
+        const int p = t + u * kCoarseThreads;
+        if (p < N) V[(long long)(j + 1) * N + p] = ws[p];
+      }
+    }
+    if (t == 0) {
+      const double hn = sqrt(hn2);
+      double2 col[MI + 1];
+      for (int k = 0; k <= j; ++k) col[k] = H[k * MI + j];
+      for (int k = 0; k < j; ++k) {
+        double2 a = col[k], bb = col[k + 1];
+        double2 s = sn[k];
+        col[k] = zadd(zscale(a, cs[k]), zmul(s, bb));
+        col[k + 1] = zadd(zmul(make_double2(-s.x, s.y), a), zscale(bb, cs[k]));
+      }
+      double2 a = col[j];
+      double c;
+      double2 s, rr;
+      double mag = hypot(a.x, a.y);
+      if (mag == 0.0) {
+        c = 0.0;
+        s = make_double2(1.0, 0.0);
+        rr = make_double2(hn, 0.0);
+      } else {
+        double tt = hypot(mag, hn);
+        double2 ph = make_double2(a.x / mag, a.y / mag);
+        c = mag / tt;
+        s = zscale(ph, hn / tt);
+        rr = zscale(ph, tt);
+      }
+      cs[j] = c;
+      sn[j] = s;
+      col[j] = rr;
+      for (int k = 0; k <= j; ++k) H[k * MI + j] = col[k];
+      double2 gj = gv[j];
+      gv[j] = zscale(gj, c);
+      gv[j + 1] = zmul(make_double2(-s.x, s.y), gj);
+      const double est = hypot(gv[j + 1].x, gv[j + 1].y) / beta0;
+      if (est <= 1e-12) {
+        s_jend = j + 1;
+        s_flag = 2;
+      } else if (hn <= 1e-14 * fmax(1.0, wn)) {
+        s_flag = 3;
+      }
+      vs[j + 1] = 1.0 / hn;
+    }
+    __syncthreads();
+    if (s_flag == 2) break;
+    if (s_flag == 3) {
+      if (t == 0) atomicCAS(status, 0, HS_EBREAKDOWN);
+      return;
+    }
+  }
+  // y = R^{-1} g ; x = S sum_k y_k v_k
+  const int jend = s_jend;
+  if (t == 0) {
+    for (int i = jend - 1; i >= 0; --i) {
+      double2 acc2 = gv[i];
+      for (int k = i + 1; k < jend; ++k) acc2 = zsub(acc2, zmul(H[i * MI + k], yv[k]));
+      double2 d = H[i * MI + i];
+      double den = d.x * d.x + d.y * d.y;
+      yv[i] = make_double2((acc2.x * d.x + acc2.y * d.y) / den, (acc2.y * d.x - acc2.x * d.y) / den);
+    }
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int u = 0; u < NPT; ++u) {
+    const int p = t + u * kCoarseThreads;
+    if (p >= N) continue;
+    float2 sum = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < MI; ++k)
+      if (k < jend) {
+        const float2 yk = make_float2((float)(yv[k].x * vs[k]), (float)(yv[k].y * vs[k]));
+        sum = cadd(sum, cmul(yk, vec(k)[p]));
+      }
+    x[p] = cmul(cscale(di[p], damping), sum);
+  }
+}
+
 // the reference's coarse solve runs 10 steps (multigrid.py:243); 16 is the supported maximum
 void launch_coarse(LevelDev L, const float2* rhs, float2* x, float2* vws, float2* sws, const float2* const* active,
                    const int* model_of, int m, float damping, int* status, int B, cudaStream_t stream) {
-  if (m <= 10)
+  if (m <= 10 && L.dinv && (long long)L.nx * L.ny <= kCoarseFastMax) {
+    constexpr int smem = 2 * kCoarseFastMax * sizeof(float2);
+    static bool attr = (cudaFuncSetAttribute(k_coarse_gmres_fast<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             smem) == cudaSuccess);
+    (void)attr;
+    k_coarse_gmres_fast<10><<<B, kCoarseThreads, smem, stream>>>(L, rhs, x, vws, active, model_of, m, damping, status);
+  }
+  else if (m <= 10)
     k_coarse_gmres<10><<<B, kCoarseThreads, 0, stream>>>(L, rhs, x, vws, sws, active, model_of, m, damping, status);
   else
     k_coarse_gmres<kCoarseMaxIters>
