@@ -712,7 +712,10 @@ __global__ void __launch_bounds__(kCoarseThreads, 1)
 #undef HS_DOTS
     __syncthreads();  // every thread is done with zs before the next step rewrites it
     if (bad) atomicOr(&s_flag, 1);
-    block_sum<NACC>(acc, red);
+    // reduce only the 2(j+1)+1 live partial sums
+#define HS_RED(JJ) block_sum<2 * JJ + 1>(*reinterpret_cast<double(*)[2 * JJ + 1]>(acc), red)
+    HS_COARSE_SWITCH(j + 1, HS_RED)
+#undef HS_RED
     if (s_flag) {
       if (t == 0) atomicCAS(status, 0, HS_ENONFINITE);
       return;
