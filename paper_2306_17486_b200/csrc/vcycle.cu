@@ -618,19 +618,17 @@ HS_DEV double coarse_orth(const float2* __restrict__ rhs, const float2* __restri
     default: CALL(10); break;     \
   }
 
-constexpr int kCoarseFastNpt = 8;
-constexpr int kCoarseFastMax = kCoarseThreads * kCoarseFastNpt;
+constexpr int kCoarseFastMax = kCoarseThreads * 16;  // C3's 4-level coarsest grid, 64 x 128
 
-template <int MI>
+template <int MI, int NPT>
 __global__ void __launch_bounds__(kCoarseThreads, 1)
     k_coarse_gmres_fast(LevelDev L, const float2* __restrict__ rhs_base, float2* __restrict__ x_out, float2* vws,
                         const float2* const* active, const int* model_of, int m, float damping, int* status) {
   constexpr int NACC = 2 * (MI + 1) + 1;
-  constexpr int NPT = kCoarseFastNpt;
   __shared__ double red[NACC * (kCoarseThreads / 32 + 1)];
   extern __shared__ __align__(16) float2 coarse_dyn[];
-  float2* zs = coarse_dyn;                   // z_j = S v_j / h_j
-  float2* ws = coarse_dyn + kCoarseFastMax;  // unnormalised V_j, then w
+  float2* zs = coarse_dyn;                           // z_j = S v_j / h_j
+  float2* ws = coarse_dyn + kCoarseThreads * NPT;  // unnormalised V_j, then w
   __shared__ double2 H[(MI + 1) * MI];
   __shared__ double2 gv[MI + 1], sn[MI], yv[MI];
   __shared__ double cs[MI], vs[MI + 1];
@@ -852,12 +850,17 @@ __global__ void __launch_bounds__(kCoarseThreads, 1)
 // the reference's coarse solve runs 10 steps (multigrid.py:243); 16 is the supported maximum
 void launch_coarse(LevelDev L, const float2* rhs, float2* x, float2* vws, float2* sws, const float2* const* active,
                    const int* model_of, int m, float damping, int* status, int B, cudaStream_t stream) {
-  if (m <= 10 && L.dinv && (long long)L.nx * L.ny <= kCoarseFastMax) {
-    constexpr int smem = 2 * kCoarseFastMax * sizeof(float2);
-    static bool attr = (cudaFuncSetAttribute(k_coarse_gmres_fast<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             smem) == cudaSuccess);
-    (void)attr;
-    k_coarse_gmres_fast<10><<<B, kCoarseThreads, smem, stream>>>(L, rhs, x, vws, active, model_of, m, damping, status);
+  const long long nc = (long long)L.nx * L.ny;
+  if (m <= 10 && L.dinv && nc <= kCoarseFastMax) {
+    auto launch = [&](auto kern, int npt) {
+      const int smem = 2 * kCoarseThreads * npt * (int)sizeof(float2);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      kern<<<B, kCoarseThreads, smem, stream>>>(L, rhs, x, vws, active, model_of, m, damping, status);
+    };
+    if (nc <= kCoarseThreads * 8)
+      launch(k_coarse_gmres_fast<10, 8>, 8);
+    else
+      launch(k_coarse_gmres_fast<10, 16>, 16);
   }
   else if (m <= 10)
     k_coarse_gmres<10><<<B, kCoarseThreads, 0, stream>>>(L, rhs, x, vws, sws, active, model_of, m, damping, status);
