@@ -23,11 +23,13 @@ namespace hs {
 namespace {
 
 constexpr int NT = 128;
-constexpr int KC = 6;             // basis vectors per chunk in a dot pass (registers vs w recomputes)
+constexpr int KC = 10;            // basis vectors per chunk in a dot pass (registers vs w recomputes)
 constexpr int PST = 2 * KC + 1;   // doubles per partial record
 constexpr int kChunks = (kMaxRestart + KC - 1) / KC;
 
-enum Mode { DOT = 0, ORTH = 1, REDOT = 2, ORTH2 = 3 };
+// ORTH is the orthogonalisation pass fused with the re-dot (for RHS predicted
+// to re-orthogonalise), ORTHP the plain one (the rest)
+enum Mode { DOT = 0, ORTH = 1, REDOT = 2, ORTH2 = 3, ORTHP = 4 };
 
 HS_DEV double2 ldz(const float2* p) {
   float2 v = *p;
@@ -89,7 +91,7 @@ HS_DEV void arn_sweep(const SolveDims& d, const ArnArgs& g, double (&acc)[PST], 
   auto ldz_b = [&](int q) { return ldz(g.zb + q); };
   for (int p = g.p0; p < g.N; p += g.stride) {
     const int i = p / d.ny, jj = p - i * d.ny;
-    if constexpr (MODE == DOT || MODE == REDOT) {
+    if constexpr (MODE == DOT || MODE == REDOT || MODE == ORTH) {
       float2 v[NV > 0 ? NV : 1];
 #pragma unroll
       for (int kk = 0; kk < NV; ++kk) v[kk] = g.Vb[(long long)(g.k0 + kk) * N + p];
@@ -99,6 +101,10 @@ HS_DEV void arn_sweep(const SolveDims& d, const ArnArgs& g, double (&acc)[PST], 
         if (g.chunk == 0) acc[2 * KC] += w.x * w.x + w.y * w.y;
       } else {
         for (int k = 0; k < g.J; ++k) w = zsub(w, zmul(g.coef[k], ldz(g.Vb + (long long)k * N + p)));
+        if (MODE == ORTH && g.chunk == 0) {
+          const_cast<float2*>(g.Vb)[(long long)g.J * N + p] = d2f(w);
+          acc[2 * KC] += w.x * w.x + w.y * w.y;
+        }
       }
 #pragma unroll
       for (int kk = 0; kk < NV; ++kk) {
@@ -133,10 +139,12 @@ __global__ void __launch_bounds__(NT) k_arnoldi(SolveDims d, SolveBuffers s, int
   const int reorth = S.reorth;
   if (!active) return;
   if ((MODE == REDOT || MODE == ORTH2) && !reorth) return;
+  if (MODE == REDOT && S.fused) return;  // the fused ORTH pass already added the re-dot
+  if ((MODE == ORTH && !S.fuse) || (MODE == ORTHP && S.fuse)) return;
   const int j = S.j, J = j + 1, m = d.restart;
   // dot passes: only the chunks holding v_0..v_j do work (and take part in the
   // last-block count); the rest exit before touching memory
-  const int live = (MODE == DOT || MODE == REDOT) ? min(nchunks, (J + KC - 1) / KC) : nchunks;
+  const int live = (MODE == DOT || MODE == REDOT || MODE == ORTH) ? min(nchunks, (J + KC - 1) / KC) : nchunks;
   if (chunk >= live) return;
   const int N = (int)d.N;
   const float2* Vb = s.V + (long long)b * (m + 1) * N;
@@ -152,7 +160,7 @@ __global__ void __launch_bounds__(NT) k_arnoldi(SolveDims d, SolveBuffers s, int
   for (int t = 0; t < PST; ++t) acc[t] = 0.0;
   int bad = 0;
   ArnArgs g{Vb, zb, c, s_coef, N, J, k0, chunk, blk * NT + (int)threadIdx.x, d.nblk * NT};
-  if (MODE == DOT || MODE == REDOT) {
+  if (MODE == DOT || MODE == REDOT || MODE == ORTH) {
     // vectors of this chunk, a compile-time count
     switch (min(KC, J - k0)) {
       case 1: arn_sweep<MODE, 1>(d, g, acc, bad); break;
@@ -160,7 +168,11 @@ __global__ void __launch_bounds__(NT) k_arnoldi(SolveDims d, SolveBuffers s, int
       case 3: arn_sweep<MODE, 3>(d, g, acc, bad); break;
       case 4: arn_sweep<MODE, 4>(d, g, acc, bad); break;
       case 5: arn_sweep<MODE, 5>(d, g, acc, bad); break;
-      default: arn_sweep<MODE, 6>(d, g, acc, bad); break;
+      case 6: arn_sweep<MODE, 6>(d, g, acc, bad); break;
+      case 7: arn_sweep<MODE, 7>(d, g, acc, bad); break;
+      case 8: arn_sweep<MODE, 8>(d, g, acc, bad); break;
+      case 9: arn_sweep<MODE, 9>(d, g, acc, bad); break;
+      default: arn_sweep<MODE, 10>(d, g, acc, bad); break;
     }
   } else {
     // w -= sum_k coef_k v_k over every k < J: the runtime loop measured faster
@@ -193,11 +205,34 @@ __global__ void __launch_bounds__(NT) k_arnoldi(SolveDims d, SolveBuffers s, int
       double2 v = make_double2(red[2 * k], red[2 * k + 1]);
       S.hcol[k] = MODE == DOT ? v : zadd(S.hcol[k], v);
     }
+  } else if (MODE == ORTH) {
+    // ||w||, the re-orthogonalisation test (krylov.py:105) and, when it fires,
+    // the second-pass coefficients V^H w: this pass formed exactly the w the
+    // re-dot would recompute (same operations, same order), so it dots it here
+    for (int t = threadIdx.x; t < 2 * J; t += NT) {
+      const int k = t >> 1, ch = k / KC, slot = 2 * (k % KC) + (t & 1);
+      double sum = 0.0;
+      for (int q = 0; q < d.nblk; ++q) sum += pb[((long long)ch * d.nblk + q) * PST + slot];
+      red[t] = sum * S.vscale[k];
+    }
+    if (threadIdx.x == 0) {
+      double nn = 0.0;
+      for (int q = 0; q < d.nblk; ++q) nn += pb[(long long)q * PST + 2 * KC];
+      S.hn = sqrt(nn);
+      S.reorth = S.hn < 0.25 * S.wn;
+      S.fused = 1;
+    }
+    __syncthreads();
+    if (S.reorth)
+      for (int k = threadIdx.x; k < J; k += NT) S.hcol[k] = zadd(S.hcol[k], make_double2(red[2 * k], red[2 * k + 1]));
   } else if (threadIdx.x == 0) {
     double nn = 0.0;
     for (int q = 0; q < d.nblk; ++q) nn += pb[(long long)q * PST + 2 * KC];
     S.hn = sqrt(nn);
-    if (MODE == ORTH) S.reorth = S.hn < 0.25 * S.wn;  // krylov.py:105
+    if (MODE == ORTHP) {
+      S.reorth = S.hn < 0.25 * S.wn;  // krylov.py:105
+      S.fused = 0;
+    }
   }
 }
 
@@ -207,6 +242,7 @@ __global__ void k_givens(SolveDims d, SolveBuffers s) {
   if (b >= d.B) return;
   RhsState& S = s.st[b];
   if (!S.active) return;
+  S.fuse = S.reorth;  // predict the next step's re-orthogonalisation from this one
   if (S.nonfinite) {
     S.status = HS_ENONFINITE;
     S.active = 0;
@@ -378,6 +414,8 @@ __global__ void k_init_state(SolveDims d, SolveBuffers s, const double* tol, con
   S.status = 0;
   S.nonfinite = 0;
   S.reorth = 0;
+  S.fuse = 0;
+  S.fused = 0;
   S.window_end = 0;
   S.conv_est = 0;
   S.converged = 0;
@@ -444,8 +482,9 @@ void krylov_after_precond(const SolveDims& d, const SolveBuffers& s, int j_hint,
   const int slot = prof::start(prof::ARNOLDI, stream);
   k_arnoldi<DOT><<<dim3(d.nblk, nch, d.B), NT, 0, stream>>>(d, s, nch);
   prof::stop(slot, stream, dot_bytes);
-  prof::count(7);
-  k_arnoldi<ORTH><<<dim3(d.nblk, 1, d.B), NT, 0, stream>>>(d, s, 1);
+  prof::count(8);
+  k_arnoldi<ORTH><<<dim3(d.nblk, nch, d.B), NT, 0, stream>>>(d, s, nch);  // + the re-dot (see its finish)
+  k_arnoldi<ORTHP><<<dim3(d.nblk, 1, d.B), NT, 0, stream>>>(d, s, 1);
   k_arnoldi<REDOT><<<dim3(d.nblk, nch, d.B), NT, 0, stream>>>(d, s, nch);
   k_arnoldi<ORTH2><<<dim3(d.nblk, 1, d.B), NT, 0, stream>>>(d, s, 1);
   k_givens<<<cdiv_u(d.B, 64), 64, 0, stream>>>(d, s);

@@ -14,6 +14,8 @@ struct RhsState {
   int status;       // HsStatus; 0 while fine
   int nonfinite;    // set by the Arnoldi pass when A z has a NaN/Inf
   int reorth;       // second Gram-Schmidt pass needed this step
+  int fuse;         // predicted re-orthogonalisation: the ORTH pass also forms the re-dot
+  int fused;        // whether this step's ORTH pass did
   int window_end;   // x update + true residual due this step
   int conv_est;     // the Givens estimate met tol this window
   int converged;    // final flag (SolveReport.converged)
