@@ -490,6 +490,19 @@ void launch_thin(const ConvArgs& a, int B, cudaStream_t st) {
 // column walks kThinRows rows (rolling window as k_conv_thin) and owns every channel of its pixel,
 // so all weight indices are compile-time constants and each FFMA takes its weight straight from
 // the constant bank -- no shared-memory weight reads, no lane split, no shuffles.
+// Packed fp32x2 FMA (sm_100 FFMA2): acc.{lo,hi} = fma(x, {w0, w1}, acc.{lo,hi}),
+// each half rounded exactly like fmaf, so results are bitwise those of two
+// scalar FMAs; ptxas takes the broadcast x as a .F32 operand and the weight
+// pair from uniform registers.
+HS_DEV void ffma2(unsigned long long& acc, float x, float w0, float w1) {
+  unsigned long long xx, ww;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(xx) : "f"(x));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(ww) : "f"(w0), "f"(w1));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(xx), "l"(ww));
+}
+HS_DEV float lo32(unsigned long long v) { return __uint_as_float((unsigned)(v & 0xffffffffull)); }
+HS_DEV float hi32(unsigned long long v) { return __uint_as_float((unsigned)(v >> 32)); }
+
 template <int CIN, int COUT>
 struct ThinW {
   float w[9 * CIN * COUT];  // [tap][cin][cout]
@@ -511,11 +524,12 @@ __global__ void __launch_bounds__(kThinThreads) k_conv_thin1(ConvArgs a, const _
   const float xcs = cin_c && a.cx.scale ? a.cx.scale[b] : 1.f;
   const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[b] : 0) : b) * a.addend_bstride
                               : nullptr;
-  float acc[3][COUT];
+  static_assert(COUT % 2 == 0, "packed accumulators");
+  unsigned long long acc[3][COUT / 2];  // output channel pairs, packed fp32x2
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
-    for (int n = 0; n < COUT; ++n) acc[r][n] = 0.f;
+    for (int n = 0; n < COUT / 2; ++n) acc[r][n] = 0ull;
   auto load_row = [&](int iy, float(&xv)[3][CIN]) {
 #pragma unroll
     for (int kx = 0; kx < 3; ++kx) {
@@ -564,14 +578,15 @@ __global__ void __launch_bounds__(kThinThreads) k_conv_thin1(ConvArgs a, const _
 #pragma unroll
         for (int c = 0; c < CIN; ++c)
 #pragma unroll
-          for (int n = 0; n < COUT; ++n)
-            acc[2 - ky][n] = fmaf(xv[kx][c], wt.w[((ky * 3 + kx) * CIN + c) * COUT + n], acc[2 - ky][n]);
+          for (int n = 0; n < COUT / 2; ++n)
+            ffma2(acc[2 - ky][n], xv[kx][c], wt.w[((ky * 3 + kx) * CIN + c) * COUT + 2 * n],
+                  wt.w[((ky * 3 + kx) * CIN + c) * COUT + 2 * n + 1]);
     const int oy = iy - 1;
     if (oy >= oy0 && oy < oy1) {
       float v[COUT];
 #pragma unroll
       for (int n = 0; n < COUT; ++n) {
-        float t = acc[0][n] + wt.b[n];
+        float t = ((n & 1) ? hi32(acc[0][n / 2]) : lo32(acc[0][n / 2])) + wt.b[n];
         if (a.softplus) t = softplus_fast(t);
         v[n] = t + sd[n];
       }
@@ -584,10 +599,10 @@ __global__ void __launch_bounds__(kThinThreads) k_conv_thin1(ConvArgs a, const _
       }
     }
 #pragma unroll
-    for (int n = 0; n < COUT; ++n) {
+    for (int n = 0; n < COUT / 2; ++n) {
       acc[0][n] = acc[1][n];
       acc[1][n] = acc[2][n];
-      acc[2][n] = 0.f;
+      acc[2][n] = 0ull;
     }
   }
 }
@@ -601,6 +616,127 @@ void launch_thin1(const ConvArgs& a, const float* host_w, int B, cudaStream_t st
   const dim3 grid((unsigned)((Wl + kThinThreads - 1) / kThinThreads), (unsigned)((Hl + kThinRows - 1) / kThinRows),
                   (unsigned)B);
   k_conv_thin1<CIN, COUT><<<grid, kThinThreads, 0, st>>>(a, wt);
+}
+
+template <int CIN, int COUT>
+__global__ void __launch_bounds__(kThinThreads) k_conv_thin1w(ConvArgs a, const __grid_constant__ ThinW<CIN, COUT> wt) {
+  // warp = a 32-column strip of one band of kThinRows rows; every lane loads
+  // only its own pixel and takes its left / right neighbours from the adjacent
+  // lanes (lanes 0 and 31 also load the one pixel outside the strip)
+  const int b = blockIdx.z;
+  if (a.active && a.active[b] == nullptr) return;
+  const int lane = threadIdx.x & 31;
+  const int x = blockIdx.x * 32 + lane;
+  const bool cout_c = COUT == 2 && a.cy != nullptr;
+  const int Hl = cout_c ? a.cy_h : a.Ho, Wl = cout_c ? a.cy_w : a.Wo;
+  const int oy0 = (blockIdx.y * (kThinThreads / 32) + (threadIdx.x >> 5)) * kThinRows, oy1 = min(Hl, oy0 + kThinRows);
+  if (oy0 >= Hl) return;  // whole warp
+  const bool xin = x < Wl;
+  const float* xb = a.x ? a.x + (long long)b * a.H * a.W * CIN : nullptr;
+  const bool cin_c = CIN == 2 && a.cx_ld > 0;
+  const float2* xc = cin_c ? (a.cx.tab ? a.cx.tab[b] : a.cx.base + (long long)b * a.cx.bstride) : nullptr;
+  const float xcs = cin_c && a.cx.scale ? a.cx.scale[b] : 1.f;
+  const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[b] : 0) : b) * a.addend_bstride
+                              : nullptr;
+  static_assert(COUT % 2 == 0, "packed accumulators");
+  unsigned long long acc[3][COUT / 2];  // output channel pairs, packed fp32x2
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int n = 0; n < COUT / 2; ++n) acc[r][n] = 0ull;
+  auto load_px = [&](int iy, int ix, float(&v)[CIN]) {
+    if (iy >= 0 && iy < a.H && ix >= 0 && ix < a.W) {
+      if (cin_c) {
+        const float2 t = xc[(long long)iy * a.cx_ld + ix];
+        v[0] = t.x * xcs;
+        v[CIN > 1 ? 1 : 0] = t.y * xcs;
+      } else {
+        load_vec<CIN>(xb + ((long long)iy * a.W + ix) * CIN, v);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < CIN; ++c) v[c] = 0.f;
+    }
+  };
+  // own pixel and (edge lanes) the outside neighbour of a row
+  auto load_row = [&](int iy, float(&own)[CIN], float(&edge)[CIN]) {
+    load_px(iy, x, own);
+    if (lane == 0) load_px(iy, x - 1, edge);
+    if (lane == 31) load_px(iy, x + 1, edge);
+  };
+  auto load_side = [&](int oy, float(&sd)[COUT]) {
+#pragma unroll
+    for (int n = 0; n < COUT; ++n) sd[n] = 0.f;
+    if (oy < oy0 || oy >= oy1 || oy >= a.Ho || x >= a.Wo) return;
+    const long long p = (long long)oy * a.Wo + x;
+    if (add) load_vec<COUT>(add + p * COUT, sd);
+    if (a.residual) {
+      float u[COUT];
+      load_vec<COUT>(a.residual + (long long)b * a.Ho * a.Wo * COUT + p * COUT, u);
+#pragma unroll
+      for (int n = 0; n < COUT; ++n) sd[n] += u[n];
+    }
+  };
+  float nown[CIN], nedge[CIN];
+#pragma unroll
+  for (int c = 0; c < CIN; ++c) nedge[c] = 0.f;
+  load_row(oy0 - 1, nown, nedge);
+  for (int iy = oy0 - 1; iy <= oy1; ++iy) {
+    float xv[3][CIN], sd[COUT];
+#pragma unroll
+    for (int c = 0; c < CIN; ++c) {
+      const float up = __shfl_up_sync(0xffffffffu, nown[c], 1), dn = __shfl_down_sync(0xffffffffu, nown[c], 1);
+      xv[0][c] = lane == 0 ? nedge[c] : up;
+      xv[1][c] = nown[c];
+      xv[2][c] = lane == 31 ? nedge[c] : dn;
+    }
+    if (iy < oy1) load_row(iy + 1, nown, nedge);
+    load_side(iy - 1, sd);
+#pragma unroll
+    for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < 3; ++kx)
+#pragma unroll
+        for (int c = 0; c < CIN; ++c)
+#pragma unroll
+          for (int n = 0; n < COUT / 2; ++n)
+            ffma2(acc[2 - ky][n], xv[kx][c], wt.w[((ky * 3 + kx) * CIN + c) * COUT + 2 * n],
+                  wt.w[((ky * 3 + kx) * CIN + c) * COUT + 2 * n + 1]);
+    const int oy = iy - 1;
+    if (oy >= oy0 && oy < oy1 && xin) {
+      float v[COUT];
+#pragma unroll
+      for (int n = 0; n < COUT; ++n) {
+        float t = ((n & 1) ? hi32(acc[0][n / 2]) : lo32(acc[0][n / 2])) + wt.b[n];
+        if (a.softplus) t = softplus_fast(t);
+        v[n] = t + sd[n];
+      }
+      if (cout_c) {
+        const bool valid = oy < a.Ho && x < a.Wo;
+        a.cy[(long long)b * a.cy_n + (long long)oy * a.cy_ld + x] =
+            valid ? make_float2(a.cy_scale * v[0], a.cy_scale * v[COUT > 1 ? 1 : 0]) : make_float2(0.f, 0.f);
+      } else if (oy < a.Ho) {
+        store_vec<COUT>(a.y + (long long)b * a.Ho * a.Wo * COUT + ((long long)oy * a.Wo + x) * COUT, v);
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < COUT / 2; ++n) {
+      acc[0][n] = acc[1][n];
+      acc[1][n] = acc[2][n];
+      acc[2][n] = 0ull;
+    }
+  }
+}
+
+template <int CIN, int COUT>
+void launch_thin1w(const ConvArgs& a, const float* host_w, int B, cudaStream_t st) {
+  ThinW<CIN, COUT> wt;
+  for (int i = 0; i < 9 * CIN * COUT; ++i) wt.w[i] = host_w[i];
+  for (int n = 0; n < COUT; ++n) wt.b[n] = host_w[9 * CIN * COUT + n];
+  const int Hl = a.cy ? a.cy_h : a.Ho, Wl = a.cy ? a.cy_w : a.Wo;
+  const int bands = (Hl + kThinRows - 1) / kThinRows, wpb = kThinThreads / 32;
+  const dim3 grid((unsigned)((Wl + 31) / 32), (unsigned)((bands + wpb - 1) / wpb), (unsigned)B);
+  k_conv_thin1w<CIN, COUT><<<grid, kThinThreads, 0, st>>>(a, wt);
 }
 
 // HS_THIN_SMEM=1 keeps the shared-memory thin kernels (A/B comparisons)
@@ -667,9 +803,9 @@ int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* 
     return HS_ECONFIG;  // complex I/O is fused into the thin stem / head only
   if (!c.transposed && c.stride == 1 && io && io->host_w && !thin_smem_path) {
     if (c.cin == 2 && c.cout == 16) return launch_thin1<2, 16>(a, io->host_w, B, st), HS_OK;
-    if (c.cin == 16 && c.cout == 2) return launch_thin1<16, 2>(a, io->host_w, B, st), HS_OK;
+    if (c.cin == 16 && c.cout == 2) return launch_thin1w<16, 2>(a, io->host_w, B, st), HS_OK;
     if (c.cin == 2 && c.cout == 8) return launch_thin1<2, 8>(a, io->host_w, B, st), HS_OK;
-    if (c.cin == 8 && c.cout == 2) return launch_thin1<8, 2>(a, io->host_w, B, st), HS_OK;
+    if (c.cin == 8 && c.cout == 2) return launch_thin1w<8, 2>(a, io->host_w, B, st), HS_OK;
   }
   if (!c.transposed && c.stride == 1) {
     if (c.cin == 2 && c.cout == 16) return launch_thin<2, 16>(a, B, st), HS_OK;

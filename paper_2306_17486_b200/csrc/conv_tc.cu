@@ -53,6 +53,12 @@ constexpr int kPrefetch = 4;  // rows pulled into L2 ahead of the bulk copies / 
 constexpr int kNA = 4;    // TMEM accumulators in flight
 constexpr int kEpiWarps = 8, kCvtWarp0 = 8;  // epilogue warps 0-7, converters from warp 8
 constexpr size_t kSmemMax = 232448;
+#ifndef HS_TC_ATM_NA
+#define HS_TC_ATM_NA 2
+#endif
+#ifndef HS_TC_CVT_GROUPS
+#define HS_TC_CVT_GROUPS 2
+#endif
 
 HS_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -186,7 +192,13 @@ struct Cfg {
   // slots: a warp may only touch its own TMEM lane quarter), producer, MMA issuer
   // four converter warps (measured best), except for the wide transposed tiles whose epilogue
   // needs the registers a 14-warp CTA cannot give
-  static constexpr int NCVT = (MODE == 2 && CS * NACC > 32) ? 2 : 4, CVT_THREADS = 32 * NCVT;
+  static constexpr int NCVT_BASE = (MODE == 2 && CS * NACC > 32) ? 2 : 4;
+  // ATM: two groups of four converter warps (one per TMEM lane quarter each)
+  // take alternate input rows, so two rows' convert -> stage -> TMEM chains
+  // overlap instead of running back to back
+  static constexpr int NCG = ATM ? HS_TC_CVT_GROUPS : 1;
+  static constexpr int NCVT = NCVT_BASE * NCG, CVT_THREADS = 32 * NCVT;
+  static constexpr int GCVT_THREADS = 32 * NCVT_BASE;  // threads of one converter group
   // MMA issuer warps: one warp issues a tcgen05.mma every ~45 cycles; the M = 64
   // layers (twice the MMAs per pixel) give alternate tiles to two issuers
   static constexpr int NMW = (MT == 64 && MODE != 2) ? 2 : 1;  // measured: helps only the M = 64 layers
@@ -228,7 +240,7 @@ struct Cfg {
   static constexpr int SLOT_COLS = 9 * 8;
   // accumulators in flight; ATM keeps two and gives TMEM to five A slots (a tile
   // reads three rows, so the converters run two rows ahead of the MMAs)
-  static constexpr int NA = ATM ? 2 : (4 * ACOLS <= 512 ? 4 : 2);
+  static constexpr int NA = ATM ? HS_TC_ATM_NA : (4 * ACOLS <= 512 ? 4 : 2);
   static constexpr int AOFF = NA * ACOLS;                                         // first A slot column
   static constexpr int NSA = ATM ? (512 - AOFF) / SLOT_COLS : 0;                  // TMEM A slots
   static_assert(!ATM || (NSA >= 4 && NSA <= 6), "a tile reads three rows; spare slots keep writes ahead");
@@ -485,7 +497,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
   if (tid == 0) {
     for (int i = 0; i < NR; ++i) {
       mbar_init(smem_u32(&raw_full[i]), 1);
-      mbar_init(smem_u32(&raw_empty[i]), C::CVT_THREADS);
+      mbar_init(smem_u32(&raw_empty[i]), C::GCVT_THREADS);
     }
     for (int i = 0; i < NS; ++i) {
       mbar_init(smem_u32(&stg_full[i]), C::CVT_THREADS);
@@ -496,7 +508,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
       mbar_init(smem_u32(&acc_empty[i]), 32 * kEpiWarps);
     }
     for (int i = 0; i < C::NSA; ++i) {
-      mbar_init(smem_u32(&a_full[i]), C::CVT_THREADS);
+      mbar_init(smem_u32(&a_full[i]), C::GCVT_THREADS);
       mbar_init(smem_u32(&a_empty[i]), 1);
     }
     fence_mbar_init();
@@ -566,7 +578,8 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
     }
   } else if (warp >= kCvtWarp0 && warp < kCvtWarp0 + C::NCVT) {
     // ================= converters: raw fp32 -> staged bf16x3
-    const int ct = tid - 32 * kCvtWarp0;
+    const int cg = (warp - kCvtWarp0) / C::NCVT_BASE;              // converter group: rows seq % NCG == cg
+    const int ct = tid - 32 * kCvtWarp0 - cg * C::GCVT_THREADS;    // thread within the group
     long long seq = 0;
     for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
@@ -574,13 +587,14 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
       const int x0 = raw_x0<MODE, MT>(U.xb);
       const int clo = max(x0, 0) - x0, chi = min(x0 + C::RW, a.W) - x0;  // valid raw pixels [clo, chi)
       for (int g = U.glo; g <= U.ghi; ++g, ++seq) {
+        if (C::NCG > 1 && (int)(seq % C::NCG) != cg) continue;
         const int rs = (int)(seq % NR), ss = (int)(seq % NS);
         const long long suse = seq / NS;
         if (!C::ATM && suse > 0) mbar_wait(smem_u32(&stg_empty[ss]), (uint32_t)((suse - 1) & 1));
         mbar_wait(smem_u32(&raw_full[rs]), (uint32_t)((seq / NR) & 1));
         const bool row_ok = g >= 0 && g < a.H;
         const unsigned char* src = raw + (size_t)rs * C::RAW_BYTES;
-        for (int e = ct; e < ((a.dbg & 1) ? 0 : C::RW * KC); e += C::CVT_THREADS) {
+        for (int e = ct; e < ((a.dbg & 1) ? 0 : C::RW * KC); e += C::GCVT_THREADS) {
           const int p = e / KC, c = e - p * KC;  // chunk fastest: conflict-free raw reads
           float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
           if (row_ok && p >= clo && p < chi) {
@@ -599,7 +613,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
           // write its own lane quarter): write the row's three tap views x three
           // parts of pixel m + kx from the staged row into TMEM slot `as`
           mbar_arrive(smem_u32(&raw_empty[rs]));
-          asm volatile("bar.sync 1, %0;" ::"n"(C::CVT_THREADS) : "memory");  // staged row complete
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + cg), "n"(C::GCVT_THREADS) : "memory");  // staged row complete
           const uint32_t as = (uint32_t)(seq % C::NSA), ause = (uint32_t)(seq / C::NSA);
           if (ause > 0) mbar_wait(smem_u32(&a_empty[as]), (ause - 1) & 1);
           tc_fence_after();
