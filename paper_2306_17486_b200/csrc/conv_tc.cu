@@ -188,6 +188,7 @@ struct Cfg {
   static constexpr size_t W_BYTES = (size_t)9 * KC * NW * 16;
   // A operand in TMEM (see below) for 16-channel stride-1 layers at M = 128
   static constexpr bool ATM = KSTEPS == 1 && MODE == 0 && MT == 128;
+  static constexpr int NCG_ = ATM ? HS_TC_CVT_GROUPS : 1;  // converter groups (see NCG)
   // warp roles: epilogue 0-7, converters (four when they also write the TMEM A
   // slots: a warp may only touch its own TMEM lane quarter), producer, MMA issuer
   // four converter warps (measured best), except for the wide transposed tiles whose epilogue
@@ -196,15 +197,18 @@ struct Cfg {
   // ATM: two groups of four converter warps (one per TMEM lane quarter each)
   // take alternate input rows, so two rows' convert -> stage -> TMEM chains
   // overlap instead of running back to back
-  static constexpr int NCG = ATM ? HS_TC_CVT_GROUPS : 1;
+  static constexpr int NCG = NCG_;
   static constexpr int NCVT = NCVT_BASE * NCG, CVT_THREADS = 32 * NCVT;
   static constexpr int GCVT_THREADS = 32 * NCVT_BASE;  // threads of one converter group
   // MMA issuer warps: one warp issues a tcgen05.mma every ~45 cycles; the M = 64
   // layers (twice the MMAs per pixel) give alternate tiles to two issuers
   static constexpr int NMW = (MT == 64 && MODE != 2) ? 2 : 1;  // measured: helps only the M = 64 layers
   static constexpr int PROD = kCvtWarp0 + NCVT, MMAW = PROD + 1, NT = 32 * (MMAW + NMW);
-  // staged ring: ATM converters consume their own staged rows at once (two slots)
-  static constexpr int NS_MIN = ATM ? 2 : 3, NS_MAX = ATM ? 2 : (MODE == 0 ? 10 : (MODE == 1 ? 8 : 6));
+  // staged ring: ATM converters consume their own staged rows at once; each
+  // converter group alternates between two slots, so a thread may convert the
+  // group's next row while a slower one still reads the previous (the group
+  // barrier of the next row orders the reuse)
+  static constexpr int NS_MIN = ATM ? 2 * NCG_ : 3, NS_MAX = ATM ? 2 * NCG_ : (MODE == 0 ? 10 : (MODE == 1 ? 8 : 6));
   static constexpr size_t row_stage_bytes(int ns) {
     return (size_t)3 * KC * 16 * (ns * RW + ((9 - ((ns * RW) & 7)) & 7));
   }
@@ -588,7 +592,8 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
       const int clo = max(x0, 0) - x0, chi = min(x0 + C::RW, a.W) - x0;  // valid raw pixels [clo, chi)
       for (int g = U.glo; g <= U.ghi; ++g, ++seq) {
         if (C::NCG > 1 && (int)(seq % C::NCG) != cg) continue;
-        const int rs = (int)(seq % NR), ss = (int)(seq % NS);
+        const int rs = (int)(seq % NR);
+        const int ss = C::ATM ? (int)(2 * cg + (seq / C::NCG) % 2) : (int)(seq % NS);
         const long long suse = seq / NS;
         if (!C::ATM && suse > 0) mbar_wait(smem_u32(&stg_empty[ss]), (uint32_t)((suse - 1) & 1));
         mbar_wait(smem_u32(&raw_full[rs]), (uint32_t)((seq / NR) & 1));

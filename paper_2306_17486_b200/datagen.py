@@ -56,7 +56,7 @@ class PairGenerator:
         """x (B, nx, ny) complex, k (B,) iteration counts, model_of (B,) -> (r, e) complex128."""
         import torch
 
-        from .device import to_device
+        from .device import to_device, to_host
         from .fields import apply_operator
 
         xd = to_device(x, torch.complex128)
@@ -82,7 +82,7 @@ class PairGenerator:
         r = per_model(lambda u, m: apply_operator(u, m), e)
         if return_device:
             return r, e
-        return r.cpu().numpy(), e.cpu().numpy()
+        return to_host(r), to_host(e)
 
 
 def generate_sample(model: SlownessModel, rng: np.random.Generator, generator: PairGenerator | None = None,

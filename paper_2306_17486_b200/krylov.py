@@ -180,6 +180,7 @@ def solve_helmholtz(model: SlownessModel, b: ComplexField, hierarchy=None, tol: 
     """FGMRES on the true operator with the V-cycle preconditioner (krylov.py:156-177)."""
     import torch
 
+    from .device import to_host
     from .engine import raise_for_status
 
     if tol <= 0:
@@ -191,7 +192,7 @@ def solve_helmholtz(model: SlownessModel, b: ComplexField, hierarchy=None, tol: 
     bd = torch.from_numpy(np.ascontiguousarray(b.data))[None]
     res = eng.fgmres(bd, None, tol, max_iter, restart)
     raise_for_status(res)
-    x = res.x[0].cpu().numpy()
+    x = to_host(res.x[0])
     rep = SolveReport(int(res.iterations[0]), res.histories[0], bool(res.converged[0]), time.perf_counter() - start)
     return ComplexField(x, b.h), rep
 
@@ -251,7 +252,7 @@ class BatchSolver:
         """
         import torch
 
-        from .device import require_cuda, to_device
+        from .device import require_cuda, to_device, to_host
         from .engine import BatchResult, raise_for_status
         from .fields import apply_operator
 
@@ -311,7 +312,7 @@ class BatchSolver:
                               np.array([r.iterations for r in reports]), None, np.asarray(status))
             for i in range(B):
                 raise_for_status(chk, i)
-        return (x if return_device else x.cpu().numpy()), reports
+        return (x if return_device else to_host(x)), reports
 
 
 def solve_batch(models, rhs, model_of=None, net=None, encodings=None, tol: float = 1e-7, max_iter: int = 250,
