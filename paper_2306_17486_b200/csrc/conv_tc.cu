@@ -527,6 +527,13 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
+  // Programmatic dependent launch: the set-up above (weights, barriers, TMEM)
+  // does not touch the previous kernel's data, so it overlaps that kernel's
+  // tail; every global read or write of activations comes after the wait.
+  // Triggering at once is safe because this grid is persistent (one CTA per
+  // SM, all resident): the next conv's CTAs only take SMs this grid leaves.
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == C::PROD) {
     // ================= producer: raw row segments, global -> smem (bulk copies)
@@ -889,7 +896,18 @@ void launch_tc(const TcArgs& a, cudaStream_t st) {
   while (b.band > 8 && C::NSPLIT * act * xblocks * ((a.Ho + b.band - 1) / b.band) < 6.0 * grid) b.band /= 2;
   const long long nunits = num_units<MODE, MT>(b, C::NSPLIT);
   if (nunits < grid) grid = nunits;
-  k_conv_tc<CIN, COUT, MODE, MT, CS><<<(unsigned)grid, C::NT, C::TOTAL, st>>>(b);
+  static const bool pdl = !(getenv("HS_NO_PDL") && atoi(getenv("HS_NO_PDL")) == 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(C::NT);
+  cfg.dynamicSmemBytes = C::TOTAL;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k_conv_tc<CIN, COUT, MODE, MT, CS>, b);
 }
 
 // (cin, cout, mode) -> cout slice per CTA, or 0 if not on the tensor-core path
