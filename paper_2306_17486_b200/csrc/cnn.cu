@@ -17,6 +17,8 @@
 #include <string>
 #include <vector>
 
+#include <type_traits>
+
 #include "cnn.h"
 #include "common.cuh"
 #include "conv_tc.h"
@@ -86,6 +88,25 @@ struct ThinIO {
   const float* host_w = nullptr;  // [tap][cin][cout] + bias on the host: the by-value thin kernels
 };
 
+// Packed fp32x2 FMA (sm_100 FFMA2): acc.{lo,hi} = fma(x, {w0, w1}, acc.{lo,hi}),
+// each half rounded exactly like fmaf, so results are bitwise those of two
+// scalar FMAs; ptxas takes the broadcast x as a .F32 operand and the weight
+// pair from uniform registers.
+HS_DEV void ffma2(unsigned long long& acc, float x, float w0, float w1) {
+  unsigned long long xx, ww;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(xx) : "f"(x));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(ww) : "f"(w0), "f"(w1));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(xx), "l"(ww));
+}
+HS_DEV float lo32(unsigned long long v) { return __uint_as_float((unsigned)(v & 0xffffffffull)); }
+HS_DEV float hi32(unsigned long long v) { return __uint_as_float((unsigned)(v >> 32)); }
+// channel q of a packed (PK) or scalar accumulator row
+template <bool PK, typename A>
+HS_DEV float acc_at(const A* row, int q) {
+  if constexpr (PK) return (q & 1) ? hi32(row[q / 2]) : lo32(row[q / 2]);
+  else return row[q];
+}
+
 template <int COUT>
 struct Tile {
   static constexpr int CG = COUT < 16 ? COUT : 16;           // couts per thread
@@ -102,7 +123,7 @@ __global__ void __launch_bounds__(kConvThreads) k_conv(ConvArgs a) {
   constexpr int IH = (T::TH - 1) * STRIDE + 3, IW = (T::TW - 1) * STRIDE + 3;
   extern __shared__ float smem[];
   float* s_in = smem;                  // [kCK][IH][IW]
-  float* s_w = smem + kCK * IH * IW;   // [kCK][9][COUT]
+  float* s_w = smem + ((kCK * IH * IW + 3) & ~3);  // [kCK][9][COUT], 16-byte aligned (paired loads)
   const int b = blockIdx.z;
   if (a.active && a.active[b] == nullptr) return;
   const int tiles_x = (a.Wo + T::TW - 1) / T::TW;
@@ -112,11 +133,15 @@ __global__ void __launch_bounds__(kConvThreads) k_conv(ConvArgs a) {
   constexpr int PG = T::TPX / T::PX;  // pixel groups
   const int cg = t / PG, pg = t % PG;
   const int ly = pg / (T::TW / T::PX), lx = (pg % (T::TW / T::PX)) * T::PX;
-  float acc[T::PX][T::CG];
+  // output-channel pairs packed fp32x2 (FFMA2) when CG is even; scalar otherwise
+  constexpr bool PK = T::CG % 2 == 0;
+  constexpr int NQ = PK ? T::CG / 2 : T::CG;
+  using AccT = typename std::conditional<PK, unsigned long long, float>::type;
+  AccT acc[T::PX][NQ];
 #pragma unroll
   for (int p = 0; p < T::PX; ++p)
 #pragma unroll
-    for (int q = 0; q < T::CG; ++q) acc[p][q] = 0.f;
+    for (int q = 0; q < NQ; ++q) acc[p][q] = AccT(0);
   const float* xb = a.x + (long long)b * a.H * a.W * a.cin;
   for (int c0 = 0; c0 < a.cin; c0 += kCK) {
     const int ck = min(kCK, a.cin - c0);
@@ -143,11 +168,20 @@ __global__ void __launch_bounds__(kConvThreads) k_conv(ConvArgs a) {
 #pragma unroll
           for (int p = 0; p < T::PX; ++p) xv[p] = s_in[(c * IH + ly * STRIDE + ky) * IW + (lx + p) * STRIDE + kx];
           const float* wr = s_w + (c * 9 + ky * 3 + kx) * COUT + cg * T::CG;
+          if constexpr (PK) {
 #pragma unroll
-          for (int q = 0; q < T::CG; ++q) {
-            const float wv = wr[q];
+            for (int q = 0; q < T::CG; q += 2) {
+              const float2 wv = *reinterpret_cast<const float2*>(wr + q);
 #pragma unroll
-            for (int p = 0; p < T::PX; ++p) acc[p][q] = fmaf(xv[p], wv, acc[p][q]);
+              for (int p = 0; p < T::PX; ++p) ffma2(acc[p][q / 2], xv[p], wv.x, wv.y);
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < T::CG; ++q) {
+              const float wv = wr[q];
+#pragma unroll
+              for (int p = 0; p < T::PX; ++p) acc[p][q] = fmaf(xv[p], wv, acc[p][q]);
+            }
           }
         }
     }
@@ -164,7 +198,7 @@ __global__ void __launch_bounds__(kConvThreads) k_conv(ConvArgs a) {
     const long long oa = ((long long)oy * a.Wo + ox) * COUT + cg * T::CG;
 #pragma unroll
     for (int q = 0; q < T::CG; ++q) {
-      float v = acc[p][q] + a.bias[cg * T::CG + q];
+      float v = acc_at<PK>(acc[p], q) + a.bias[cg * T::CG + q];
       if (a.softplus) v = softplusf(v);
       if (add) v += add[oa + q];
       if (a.residual) v += a.residual[o + q];
@@ -183,7 +217,7 @@ __global__ void __launch_bounds__(kConvThreads) k_tconv(ConvArgs a) {
   constexpr int IH = QH + 1, IW = QW + 1;
   extern __shared__ float smem[];
   float* s_in = smem;
-  float* s_w = smem + kCK * IH * IW;
+  float* s_w = smem + ((kCK * IH * IW + 3) & ~3);  // 16-byte aligned (paired weight loads)
   const int b = blockIdx.z;
   if (a.active && a.active[b] == nullptr) return;
   const int tiles_x = (a.Wo + T::TW - 1) / T::TW;
@@ -196,11 +230,15 @@ __global__ void __launch_bounds__(kConvThreads) k_tconv(ConvArgs a) {
   const int cls = pg / PGC, pgc = pg % PGC;
   const int py = cls >> 1, px = cls & 1;
   const int qy = pgc / (QW / T::PX), qx = (pgc % (QW / T::PX)) * T::PX;
-  float acc[T::PX][T::CG];
+  // output-channel pairs packed fp32x2 (FFMA2) when CG is even; scalar otherwise
+  constexpr bool PK = T::CG % 2 == 0;
+  constexpr int NQ = PK ? T::CG / 2 : T::CG;
+  using AccT = typename std::conditional<PK, unsigned long long, float>::type;
+  AccT acc[T::PX][NQ];
 #pragma unroll
   for (int p = 0; p < T::PX; ++p)
 #pragma unroll
-    for (int q = 0; q < T::CG; ++q) acc[p][q] = 0.f;
+    for (int q = 0; q < NQ; ++q) acc[p][q] = AccT(0);
   const float* xb = a.x + (long long)b * a.H * a.W * a.cin;
   // taps per parity: even -> (k=1, d=0); odd -> (k=0, d=1), (k=2, d=0)
   const int nty = py ? 2 : 1, ntx = px ? 2 : 1;
@@ -229,11 +267,20 @@ __global__ void __launch_bounds__(kConvThreads) k_tconv(ConvArgs a) {
 #pragma unroll
           for (int p = 0; p < T::PX; ++p) xv[p] = s_in[(c * IH + qy + dy) * IW + qx + p + dx];
           const float* wr = s_w + (c * 9 + ky * 3 + kx) * COUT + cg * T::CG;
+          if constexpr (PK) {
 #pragma unroll
-          for (int q = 0; q < T::CG; ++q) {
-            const float wv = wr[q];
+            for (int q = 0; q < T::CG; q += 2) {
+              const float2 wv = *reinterpret_cast<const float2*>(wr + q);
 #pragma unroll
-            for (int p = 0; p < T::PX; ++p) acc[p][q] = fmaf(xv[p], wv, acc[p][q]);
+              for (int p = 0; p < T::PX; ++p) ffma2(acc[p][q / 2], xv[p], wv.x, wv.y);
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < T::CG; ++q) {
+              const float wv = wr[q];
+#pragma unroll
+              for (int p = 0; p < T::PX; ++p) acc[p][q] = fmaf(xv[p], wv, acc[p][q]);
+            }
           }
         }
       }
@@ -251,7 +298,7 @@ __global__ void __launch_bounds__(kConvThreads) k_tconv(ConvArgs a) {
     const long long o = obase + oa;
 #pragma unroll
     for (int q = 0; q < T::CG; ++q) {
-      float v = acc[p][q] + a.bias[cg * T::CG + q];
+      float v = acc_at<PK>(acc[p], q) + a.bias[cg * T::CG + q];
       if (a.softplus) v = softplusf(v);
       if (add) v += add[oa + q];
       if (a.residual) v += a.residual[o + q];
@@ -264,12 +311,12 @@ template <int COUT, int STRIDE>
 size_t conv_smem() {
   using T = Tile<COUT>;
   constexpr int IH = (T::TH - 1) * STRIDE + 3, IW = (T::TW - 1) * STRIDE + 3;
-  return sizeof(float) * (kCK * IH * IW + kCK * 9 * COUT);
+  return sizeof(float) * (((kCK * IH * IW + 3) & ~3) + kCK * 9 * COUT);
 }
 template <int COUT>
 size_t tconv_smem() {
   using T = Tile<COUT>;
-  return sizeof(float) * (kCK * (T::TH / 2 + 1) * (T::TW / 2 + 1) + kCK * 9 * COUT);
+  return sizeof(float) * (((kCK * (T::TH / 2 + 1) * (T::TW / 2 + 1) + 3) & ~3) + kCK * 9 * COUT);
 }
 
 template <int COUT, int STRIDE>
@@ -490,18 +537,6 @@ void launch_thin(const ConvArgs& a, int B, cudaStream_t st) {
 // column walks kThinRows rows (rolling window as k_conv_thin) and owns every channel of its pixel,
 // so all weight indices are compile-time constants and each FFMA takes its weight straight from
 // the constant bank -- no shared-memory weight reads, no lane split, no shuffles.
-// Packed fp32x2 FMA (sm_100 FFMA2): acc.{lo,hi} = fma(x, {w0, w1}, acc.{lo,hi}),
-// each half rounded exactly like fmaf, so results are bitwise those of two
-// scalar FMAs; ptxas takes the broadcast x as a .F32 operand and the weight
-// pair from uniform registers.
-HS_DEV void ffma2(unsigned long long& acc, float x, float w0, float w1) {
-  unsigned long long xx, ww;
-  asm("mov.b64 %0, {%1, %1};" : "=l"(xx) : "f"(x));
-  asm("mov.b64 %0, {%1, %2};" : "=l"(ww) : "f"(w0), "f"(w1));
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(xx), "l"(ww));
-}
-HS_DEV float lo32(unsigned long long v) { return __uint_as_float((unsigned)(v & 0xffffffffull)); }
-HS_DEV float hi32(unsigned long long v) { return __uint_as_float((unsigned)(v >> 32)); }
 
 template <int CIN, int COUT>
 struct ThinW {
