@@ -47,23 +47,14 @@ HS_DEV double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-// softplus(x) = max(x, 0) + log1p(e), e = exp(-|x|) in (0, 1]: one MUFU exp,
-// then log1p(e) = e q(e) with q a degree-8 Chebyshev fit of log1p(e)/e on
-// [0, 1] evaluated by Horner in fp32 (max absolute error 1.2e-7 over [0, 1],
-// the fp32 class of the reference's np.logaddexp; FMA pipe instead of a second
-// MUFU op; the conv tests hold layers to 2e-6 relative).
+// softplus(x) = max(x, 0) + log1p(e), e = exp(-|x|) in (0, 1], as
+// max(x, 0) + ln2 * lg2(1 + e) with the MUFU ex2 / lg2 approximations: six
+// instructions.  Absolute error ~1e-7 (the rounding of 1 + e dominates; for
+// tiny e the result is exact to within e ulp-of-1), the fp32 class of the
+// reference's np.logaddexp; the conv tests hold layers to 2e-6 relative.
 HS_DEV float softplus_fast(float x) {
   const float e = __expf(-fabsf(x));
-  float q = 0.005253457929939032f;
-  q = fmaf(q, e, -0.02958850748836994f);
-  q = fmaf(q, e, 0.07836166769266129f);
-  q = fmaf(q, e, -0.13674770295619965f);
-  q = fmaf(q, e, 0.19111430644989014f);
-  q = fmaf(q, e, -0.24844369292259216f);
-  q = fmaf(q, e, 0.33319270610809326f);
-  q = fmaf(q, e, -0.49999502301216125f);
-  q = fmaf(q, e, 1.0f);
-  return fmaxf(x, 0.f) + e * q;
+  return fmaf(__log2f(1.0f + e), 0.69314718055994531f, fmaxf(x, 0.f));
 }
 
 HS_DEV float warp_sumf(float v) {

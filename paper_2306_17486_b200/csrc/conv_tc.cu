@@ -128,18 +128,38 @@ HS_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluste
 HS_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 HS_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
+// packed fp32x2 adds (FADD2), each half rounded exactly like a scalar add
+HS_DEV uint64_t pk2(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
+HS_DEV uint64_t pkf(float lo, float hi) { return pk2(__float_as_uint(lo), __float_as_uint(hi)); }
+HS_DEV float lo_f(uint64_t v) { return __uint_as_float((uint32_t)v); }
+HS_DEV float hi_f(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+HS_DEV uint64_t add2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+HS_DEV uint64_t sub2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 // exact three-way bf16 split of 8 floats into one 16-byte chunk per part
 HS_DEV void split_bf16x3(const float (&v)[8], uint4& p0, uint4& p1, uint4& p2) {
   uint32_t w0[4], w1[4], w2[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
+    // a pair at a time: the bf16x2 word widens to the pair of its floats with two
+    // bit ops, and the residuals are one packed subtract (FADD2), exact like the scalar ones
     const float a = v[2 * i], b = v[2 * i + 1];
     const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-    const float ra = a - __low2float(h), rb = b - __high2float(h);
-    const __nv_bfloat162 m = __floats2bfloat162_rn(ra, rb);
-    const __nv_bfloat162 l = __floats2bfloat162_rn(ra - __low2float(m), rb - __high2float(m));
-    w0[i] = *reinterpret_cast<const uint32_t*>(&h);
-    w1[i] = *reinterpret_cast<const uint32_t*>(&m);
+    const uint32_t hw = *reinterpret_cast<const uint32_t*>(&h);
+    const uint64_t r1 = sub2(pkf(a, b), pk2(hw << 16, hw & 0xffff0000u));
+    const __nv_bfloat162 m = __floats2bfloat162_rn(lo_f(r1), hi_f(r1));
+    const uint32_t mw = *reinterpret_cast<const uint32_t*>(&m);
+    const uint64_t r2 = sub2(r1, pk2(mw << 16, mw & 0xffff0000u));
+    const __nv_bfloat162 l = __floats2bfloat162_rn(lo_f(r2), hi_f(r2));
+    w0[i] = hw;
+    w1[i] = mw;
     w2[i] = *reinterpret_cast<const uint32_t*>(&l);
   }
   p0 = make_uint4(w0[0], w0[1], w0[2], w0[3]);
@@ -821,8 +841,11 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
             tmem_ld8(col + 2 * CS, r2);
             tmem_wait_ld();
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              t[k][n0 + j] = (__uint_as_float(r0[j]) + __uint_as_float(r1[j])) + __uint_as_float(r2[j]);
+            for (int j = 0; j < 8; j += 2) {  // (x0 + x1) + x2 partial sums, channel pairs packed (FADD2)
+              const uint64_t s = add2(add2(pk2(r0[j], r0[j + 1]), pk2(r1[j], r1[j + 1])), pk2(r2[j], r2[j + 1]));
+              t[k][n0 + j] = __uint_as_float((uint32_t)s);
+              t[k][n0 + j + 1] = __uint_as_float((uint32_t)(s >> 32));
+            }
           }
         tc_fence_before();
         mbar_arrive(smem_u32(&acc_empty[acc]));  // TMEM free; finish from registers
@@ -835,7 +858,9 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
 #pragma unroll
             for (int n0 = 0; n0 < EH; n0 += 4) {
               const float4 bs = *reinterpret_cast<const float4*>(s_bias + h * EH + n0);
-              float4 o = make_float4(t[k][n0] + bs.x, t[k][n0 + 1] + bs.y, t[k][n0 + 2] + bs.z, t[k][n0 + 3] + bs.w);
+              const uint64_t o01 = add2(pkf(t[k][n0], t[k][n0 + 1]), pkf(bs.x, bs.y));
+              const uint64_t o23 = add2(pkf(t[k][n0 + 2], t[k][n0 + 3]), pkf(bs.z, bs.w));
+              float4 o = make_float4(lo_f(o01), hi_f(o01), lo_f(o23), hi_f(o23));
               if (a.softplus) {
                 o.x = softplus_fast(o.x);
                 o.y = softplus_fast(o.y);
@@ -844,10 +869,11 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
               }
               const float4 ad = pre_a[k][n0 / 4];
               const float4 rs = SPLIT ? pre_r[SPLIT ? k : 0][SPLIT ? n0 / 4 : 0] : make_float4(0.f, 0.f, 0.f, 0.f);
-              o.x += ad.x + rs.x;
-              o.y += ad.y + rs.y;
-              o.z += ad.z + rs.z;
-              o.w += ad.w + rs.w;
+              {  // o + (addend + residual), packed
+                const uint64_t a01 = add2(pkf(ad.x, ad.y), pkf(rs.x, rs.y)), a23 = add2(pkf(ad.z, ad.w), pkf(rs.z, rs.w));
+                const uint64_t q01 = add2(pkf(o.x, o.y), a01), q23 = add2(pkf(o.z, o.w), a23);
+                o = make_float4(lo_f(q01), hi_f(q01), lo_f(q23), hi_f(q23));
+              }
               if (!(a.dbg & 64)) *reinterpret_cast<float4*>(a.y + obase + n0) = o;
               else if (o.x == 1234.5f) a.y[0] = o.y;
             }
