@@ -521,18 +521,18 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
   if (tid == 0) {
     for (int i = 0; i < NR; ++i) {
       mbar_init(smem_u32(&raw_full[i]), 1);
-      mbar_init(smem_u32(&raw_empty[i]), C::GCVT_THREADS);
+      mbar_init(smem_u32(&raw_empty[i]), C::NCVT_BASE);  // one arrival per converter warp
     }
     for (int i = 0; i < NS; ++i) {
-      mbar_init(smem_u32(&stg_full[i]), C::CVT_THREADS);
+      mbar_init(smem_u32(&stg_full[i]), C::NCVT);
       mbar_init(smem_u32(&stg_empty[i]), C::NMW);  // every MMA warp releases every staged row
     }
     for (int i = 0; i < C::NA; ++i) {
       mbar_init(smem_u32(&acc_full[i]), 1);
-      mbar_init(smem_u32(&acc_empty[i]), 32 * kEpiWarps);
+      mbar_init(smem_u32(&acc_empty[i]), kEpiWarps);  // one arrival per epilogue warp
     }
     for (int i = 0; i < C::NSA; ++i) {
-      mbar_init(smem_u32(&a_full[i]), C::GCVT_THREADS);
+      mbar_init(smem_u32(&a_full[i]), C::NCVT_BASE);
       mbar_init(smem_u32(&a_empty[i]), 1);
     }
     fence_mbar_init();
@@ -644,7 +644,8 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
           // every converter thread owns TMEM lane m = tile row m (a warp may only
           // write its own lane quarter): write the row's three tap views x three
           // parts of pixel m + kx from the staged row into TMEM slot `as`
-          mbar_arrive(smem_u32(&raw_empty[rs]));
+          __syncwarp();  // barriers count warps: a waiter wakes once per warp, not once per thread
+          if (lane == 0) mbar_arrive(smem_u32(&raw_empty[rs]));
           asm volatile("bar.sync %0, %1;" ::"r"(1 + cg), "n"(C::GCVT_THREADS) : "memory");  // staged row complete
           const uint32_t as = (uint32_t)(seq % C::NSA), ause = (uint32_t)(seq / C::NSA);
           if (ause > 0) mbar_wait(smem_u32(&a_empty[as]), (ause - 1) & 1);
@@ -664,11 +665,15 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
             }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
-          mbar_arrive(smem_u32(&a_full[as]));
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&a_full[as]));
         } else {
           fence_async_smem();
-          mbar_arrive(smem_u32(&raw_empty[rs]));
-          mbar_arrive(smem_u32(&stg_full[ss]));
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(smem_u32(&raw_empty[rs]));
+            mbar_arrive(smem_u32(&stg_full[ss]));
+          }
         }
       }
     }
@@ -848,7 +853,8 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
             }
           }
         tc_fence_before();
-        mbar_arrive(smem_u32(&acc_empty[acc]));  // TMEM free; finish from registers
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&acc_empty[acc]));  // TMEM free; finish from registers
         if (lane_ok && !(a.dbg & 4)) {
 #pragma unroll
           for (int k = 0; k < C::NACC; ++k) {
