@@ -52,9 +52,14 @@ HS_DEV double warp_sum(double v) {
 // instructions.  Absolute error ~1e-7 (the rounding of 1 + e dominates; for
 // tiny e the result is exact to within e ulp-of-1), the fp32 class of the
 // reference's np.logaddexp; the conv tests hold layers to 2e-6 relative.
+// The .ftz MUFU forms skip the denormal range scaling the plain ones add around
+// each MUFU op: the ex2 argument is <= 0 (a denormal result, x < -87, flushes to
+// 0, an absolute error below 1e-38) and the lg2 argument lies in [1, 2].
 HS_DEV float softplus_fast(float x) {
-  const float e = __expf(-fabsf(x));
-  return fmaf(__log2f(1.0f + e), 0.69314718055994531f, fmaxf(x, 0.f));
+  float e, l;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fabsf(x) * -1.4426950408889634f));
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(1.0f + e));
+  return fmaf(l, 0.69314718055994531f, fmaxf(x, 0.f));
 }
 
 HS_DEV float warp_sumf(float v) {
