@@ -779,7 +779,7 @@ const bool thin_smem_path = getenv("HS_THIN_SMEM") && atoi(getenv("HS_THIN_SMEM"
 
 int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* y, const float* addend,
                 long long addend_bstride, const int* model_of, const float* residual, const void* const* active,
-                cudaStream_t st, bool model_of_addend = false, const ThinIO* io = nullptr) {
+                cudaStream_t st, bool model_of_addend = false, const ThinIO* io = nullptr, bool planar_out = false) {
   ConvArgs a{};
   if (io) {  // complex Krylov-vector input (stem) and / or complex u0 output (head): thin kernels only
     if (io->in_ld > 0 && c.cin == 2) {
@@ -850,8 +850,10 @@ int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* 
   }
   if (conv_tc_supported(c.cin, c.cout, c.stride, c.transposed, H, W, a.Wo) &&
       conv_tc_launch(a.x, a.H, a.W, a.cin, a.y, a.Ho, a.Wo, a.cout, c.stride, c.transposed, a.w, a.bias, a.softplus,
-                     a.addend, a.addend_bstride, a.addend_per_model, a.model_of, a.residual, a.active, B, st))
+                     a.addend, a.addend_bstride, a.addend_per_model, a.model_of, a.residual, a.active, B, st,
+                     planar_out ? 1 : 0))
     return HS_OK;
+  if (planar_out) return HS_ECONFIG;  // only the tcgen05 epilogue writes the planar layout
 #define HS_CONV_CASE(CO)                          \
   case CO:                                        \
     if (c.transposed)                             \
@@ -1082,13 +1084,16 @@ static int green_spectrum_c128(const float2* kern, int C, int h, int w, cufftDou
 }
 
 static int implicit_apply_dev(const hs_net_t* net, const float* x_nhwc, float* y_nhwc, cufftComplex* z,
-                              const void* const* active, int B, cudaStream_t st) {
+                              const void* const* active, int B, cudaStream_t st, bool x_planar = false) {
   const int hc = net->hc, wc = net->wc, cc = net->cc;
   if (net->spec_perm) {
     const long long pix = (long long)hc * wc;
     prof::count(1);
-    return implicit_fused(x_nhwc, pix * cc, 1, cc, y_nhwc, pix * cc, 1, cc, net->spec_perm, active, B, cc, hc, wc, st);
+    // input NHWC (channel pairs at pixel stride cc) or complex-planar (pixel stride 1)
+    return implicit_fused(x_nhwc, pix * cc, x_planar ? pix : 1, x_planar ? 1 : cc, y_nhwc, pix * cc, 1, cc,
+                          net->spec_perm, active, B, cc, hc, wc, st);
   }
+  if (x_planar) return HS_ECONFIG;
   cufftHandle plan;
   {
     std::lock_guard<std::mutex> g(net->plan_mu);
@@ -1117,6 +1122,13 @@ static int implicit_apply_dev(const hs_net_t* net, const float* x_nhwc, float* y
 
 // The solver U-Net (ARCH.md) on NHWC buffers; input 2-channel `in`, output
 // 2-channel `head`.  RHS with active[b] == null are skipped.
+// whether the coarsest residual block writes the implicit layer's input complex-planar
+static bool coarse_planar(const hs_net_t* net, int h, int w) {
+  const hs_conv_t& c = net->d.sol_res_b[net->d.levels - 1];
+  return net->spec_perm != nullptr && !c.transposed && c.stride == 1 &&
+         conv_tc_supported(c.cin, c.cout, c.stride, c.transposed, h, w, w);
+}
+
 static int solver_forward(const hs_net_t* net, const float* in, float* head, const ThinIO* io, char* ws,
                           const FwdLayout& L,
                           const int* model_of, const void* const* active, int B, cudaStream_t st) {
@@ -1147,12 +1159,18 @@ static int solver_forward(const hs_net_t* net, const float* in, float* head, con
                           active, st, true)))
       return rc;
     if ((rc = launch_conv(d.sol_res_a[l], X[l], B, h, w, Tm[l], nullptr, 0, nullptr, nullptr, active, st))) return rc;
-    if ((rc = launch_conv(d.sol_res_b[l], Tm[l], B, h, w, S[l], nullptr, 0, nullptr, X[l], active, st))) return rc;
+    // the coarsest level's S feeds only the implicit layer: stored complex-planar
+    // there (coalesced FFT-line reads) when the fused kernel and the tcgen05 conv run
+    const bool planar = l == d.levels - 1 && coarse_planar(net, h, w);
+    if ((rc = launch_conv(d.sol_res_b[l], Tm[l], B, h, w, S[l], nullptr, 0, nullptr, X[l], active, st, false, nullptr,
+                          planar)))
+      return rc;
   }
   // coarsest: implicit layer S[L-1] -> X[L-1]
   const int L1 = d.levels - 1;
   const int islot = prof::start(prof::IMPLICIT, st);
-  rc = implicit_apply_dev(net, S[L1], X[L1], reinterpret_cast<cufftComplex*>(ws + L.fftz), active, B, st);
+  rc = implicit_apply_dev(net, S[L1], X[L1], reinterpret_cast<cufftComplex*>(ws + L.fftz), active, B, st,
+                          L1 > 0 && coarse_planar(net, d.ix >> L1, d.iy >> L1));
   prof::stop(islot, st, 0.0);
   if (rc) return rc;
   // up path: X[l] -> (tconv + skip) X[l-1] -> residual block

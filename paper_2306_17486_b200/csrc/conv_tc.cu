@@ -192,6 +192,7 @@ struct TcArgs {
   int band;  // output rows per work unit (a CTA walks a band of one column block top to bottom)
   int dbg;   // experiment switch (HS_TC_DBG): 1 skip conversion, 2 skip MMAs, 4 skip epilogue math, 64 skip
              // stores, 128 skip input loads, 256 skip addend loads
+  int planar;  // complex-planar output (conv_tc.h)
 };
 
 // MODE 0: stride 1; MODE 1: stride 2; MODE 2: transposed stride 2 (out = 2 x in).
@@ -880,7 +881,14 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
                 const uint64_t q01 = add2(pkf(o.x, o.y), a01), q23 = add2(pkf(o.z, o.w), a23);
                 o = make_float4(lo_f(q01), hi_f(q01), lo_f(q23), hi_f(q23));
               }
-              if (!(a.dbg & 64)) *reinterpret_cast<float4*>(a.y + obase + n0) = o;
+              if (a.planar) {  // two complex channels, each a coalesced float2 plane store
+                float2* yp = reinterpret_cast<float2*>(a.y) +
+                             ((size_t)U.b * (COUT / 2) + (n_base + n0) / 2) * ((size_t)a.Ho * a.Wo) + pix;
+                yp[0] = make_float2(o.x, o.y);
+                yp[(size_t)a.Ho * a.Wo] = make_float2(o.z, o.w);
+              } else if (!(a.dbg & 64)) {
+                *reinterpret_cast<float4*>(a.y + obase + n0) = o;
+              }
               else if (o.x == 1234.5f) a.y[0] = o.y;
             }
           }
@@ -970,10 +978,10 @@ bool conv_tc_supported(int cin, int cout, int stride, int transposed, int H, int
 bool conv_tc_launch(const float* x, int H, int W, int cin, float* y, int Ho, int Wo, int cout, int stride,
                     int transposed, const float* w, const float* bias, int softplus, const float* addend,
                     long long addend_bstride, int addend_per_model, const int* model_of, const float* residual,
-                    const void* const* active, int B, cudaStream_t st) {
+                    const void* const* active, int B, cudaStream_t st, int planar) {
   static const int dbg = getenv("HS_TC_DBG") ? atoi(getenv("HS_TC_DBG")) : 0;
   TcArgs a{x, H, W, y, Ho, Wo, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual,
-           active, B, 32, dbg};
+           active, B, 32, dbg, planar};
   const int mode = transposed ? 2 : (stride == 2 ? 1 : 0);
   const bool m128 = ((mode == 2 ? W : Wo) % 128) == 0 && !(dbg & 32);
 #define HS_TC(CI, CO, MD, CSL)                                           \
