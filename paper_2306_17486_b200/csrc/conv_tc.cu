@@ -56,6 +56,9 @@ constexpr size_t kSmemMax = 232448;
 #ifndef HS_TC_ATM_NA
 #define HS_TC_ATM_NA 2
 #endif
+#ifndef HS_TC_S2_CVT
+#define HS_TC_S2_CVT 6
+#endif
 #ifndef HS_TC_CVT_GROUPS
 #define HS_TC_CVT_GROUPS 2
 #endif
@@ -214,7 +217,9 @@ struct Cfg {
   // slots: a warp may only touch its own TMEM lane quarter), producer, MMA issuer
   // four converter warps (measured best), except for the wide transposed tiles whose epilogue
   // needs the registers a 14-warp CTA cannot give
-  static constexpr int NCVT_BASE = (MODE == 2 && CS * NACC > 32) ? 2 : 4;
+  // stride-2 layers convert two input rows per output row: six converter warps at M = 128
+  // (measured; the M = 64 ones with two MMA warps would spill)
+  static constexpr int NCVT_BASE = (MODE == 2 && CS * NACC > 32) ? 2 : (MODE == 1 && MT == 128 ? HS_TC_S2_CVT : 4);
   // ATM: two groups of four converter warps (one per TMEM lane quarter each)
   // take alternate input rows, so two rows' convert -> stage -> TMEM chains
   // overlap instead of running back to back
