@@ -6,7 +6,7 @@ from conftest import complex_noise, golden, relerr
 
 pytestmark = pytest.mark.gpu
 
-from paper_2306_17486_b200 import fields, multigrid  # noqa: E402
+from paper_2306_17486_b200 import fields, multigrid, problems  # noqa: E402
 from oracle import helm_oracle as ho  # noqa: E402
 
 
@@ -126,3 +126,23 @@ def test_jacobi_matches_oracle(rng):
     u, r = complex_noise(rng, lv.model.shape), complex_noise(rng, lv.model.shape)
     O = ho.Level(ho.Model(lv.model.kappa_sq, lv.model.gamma, lv.model.omega, lv.model.h), 1.0, 0.5, lv.wall)
     assert relerr(multigrid.jacobi_relax(u, r, lv, 2, 0.8), ho.jacobi(u, r, O, 2, 0.8)) < 1e-5
+
+
+@pytest.mark.parametrize("n,levels", [(257, 2), (129, 2)])
+def test_vcycle_large_coarse_grid_matches_oracle(rng, n, levels):
+    """Coarsest grids above the fast coarse kernel's 8192-node reach (C3 with 3 levels, C4, C5 use
+    128 x 256) take the L2-basis coarse GMRES; 129^2 with 2 levels (64^2) takes the 4096-node tier."""
+    import torch
+
+    from paper_2306_17486_b200.multigrid import DeviceHierarchy, run_vcycle
+
+    m = fields.slowness_model(problems.smooth_random_kappa_sq((n, n), 6.0, 11), layer_width=8)
+    H = multigrid.build_hierarchy(m, jacobi_damping=(0.8, 0.8), num_levels=levels)
+    rhs = complex_noise(rng, (2, n, n))
+    u0 = complex_noise(rng, (2, n, n), 1e-3)
+    dh = DeviceHierarchy([H])
+    owner = torch.zeros(2, dtype=torch.int32, device="cuda")
+    out = run_vcycle(dh, torch.from_numpy(rhs).cuda(), torch.from_numpy(u0).cuda(), owner).cpu().numpy()
+    O = ho.build_hierarchy(ho.Model(m.kappa_sq, m.gamma, m.omega, m.h), damping=(0.8, 0.8), num_levels=levels)
+    for i in range(2):
+        assert relerr(out[i], ho.v_cycle(rhs[i], u0[i], O)) < 2e-5
