@@ -338,6 +338,15 @@ __global__ void __launch_bounds__(Imp2<E>::THREADS) k_implicit2(ImpArgs a) {
   // 2. columns: forward, spectrum, inverse (rows < h kept)
   for (int c0 = 0; c0 < N; c0 += LINES) {
     const int nl = min(LINES, N - c0);
+    // this thread's 32 spectrum values, requested before step (a) and the barrier
+    // (the compiler does not move loads across __syncthreads; shared memory, not
+    // registers, bounds this kernel's occupancy)
+    float2 spv[32];
+    if (tl < nl) {
+      const float2* spc = sp + c0 + tl;
+#pragma unroll
+      for (int m = 0; m < 32; ++m) spv[m] = __ldg(spc + (long long)(tk + E * m) * N);
+    }
     for (int cc = warp; cc < nl; cc += NW) {
       float2 q[E];
 #pragma unroll
@@ -350,9 +359,8 @@ __global__ void __launch_bounds__(Imp2<E>::THREADS) k_implicit2(ImpArgs a) {
 #pragma unroll
       for (int l = 0; l < 32; ++l) v[l] = T[(tk * LINES + tl) * TL + l];
       fft32<false>(v);
-      const float2* spc = sp + c0 + tl;
 #pragma unroll
-      for (int m = 0; m < 32; ++m) v[m] = cmul(v[m], __ldg(spc + (long long)(tk + E * m) * N));
+      for (int m = 0; m < 32; ++m) v[m] = cmul(v[m], spv[m]);
       fft32<true>(v);
 #pragma unroll
       for (int l = 0; l < 32; ++l) T[(tk * LINES + tl) * TL + l] = v[l];
