@@ -306,24 +306,28 @@ __global__ void __launch_bounds__(Imp2<E>::THREADS) k_implicit2(ImpArgs a) {
       q[j] = s;
     }
   };
-  // 1. forward row transforms (h rows, LINES per chunk)
+  // 1. forward row transforms (h rows, LINES per chunk).  All of a warp's rows of a
+  // chunk are loaded together, and the next chunk's rows are requested before this
+  // chunk's barrier and step (c), so their latency overlaps the FFT work.
+  constexpr int RPW = LINES / NW;
+  float2 q[RPW][E];
+  auto load_rows = [&](int r0) {
+    const int nl = min(LINES, h - r0);
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      const int rr = warp + i * NW;
+#pragma unroll
+      for (int j = 0; j < E; ++j)
+        q[i][j] = (j < NZ && rr < nl) ? xin[(long long)((r0 + rr) * h + lane + 32 * j) * a.xp] : make_float2(0.f, 0.f);
+    }
+  };
+  load_rows(0);
   for (int r0 = 0; r0 < h; r0 += LINES) {
     const int nl = min(LINES, h - r0);
-    {
-      // all of this warp's rows are loaded before any is transformed (loads in flight together)
-      constexpr int RPW = LINES / NW;
-      float2 q[RPW][E];
 #pragma unroll
-      for (int i = 0; i < RPW; ++i) {
-        const int rr = warp + i * NW;
-#pragma unroll
-        for (int j = 0; j < E; ++j)
-          q[i][j] = (j < NZ && rr < nl) ? xin[(long long)((r0 + rr) * h + lane + 32 * j) * a.xp] : make_float2(0.f, 0.f);
-      }
-#pragma unroll
-      for (int i = 0; i < RPW; ++i)
-        if (warp + i * NW < nl) fwd_a(q[i], warp + i * NW);
-    }
+    for (int i = 0; i < RPW; ++i)
+      if (warp + i * NW < nl) fwd_a(q[i], warp + i * NW);
+    if (r0 + LINES < h) load_rows(r0 + LINES);
     __syncthreads();
     if (tl < nl) {
       float2 v[32];
