@@ -1,26 +1,31 @@
 #!/usr/bin/env python
 """Benchmark: Helmholtz RHS solved per second to relative residual 1e-6 (BASELINE.json metric).
 
-Workload (BASELINE.json configs[1], "C2"): 257x257 nodes (external 256^2),
-4 seeded smooth-random slowness models x 32 point-source RHS, 3-level V-cycle
-(damped Jacobi 0.8/0.8) + the 3-level 16/32/64 encoder-solver CNN with seeded
-weights, FGMRES(10) to 1e-6 (max 2000 iterations).  One "step" = one batched
-solve of all 128 RHS.  Synthetic seeded data (no datasets are available).
+Headline workload (BASELINE.json configs[2], "C3", the largest single-GPU configuration; C4/C5
+are specified across 8 GPUs): a 513x1025 grid (external 512x1024) with the layered-plus-10%-
+smoothed-noise slowness, omega for 10 points per wavelength, absorbing layer 32, 64 right-hand
+sides (32 point sources + 32 seeded complex Gaussians), FGMRES(20) to 1e-6 (max 2000 iterations),
+preconditioned by the 4-level V(1,1)-cycle (Jacobi 0.8/0.8) with the encoder-solver CNN
+(4 levels, 16/32/64/128 channels, seeded weights) as its initial guess -- the reference's
+solve_with_learned_preconditioner protocol (krylov.py:180-246).  BASELINE runs C3 twice; the
+multigrid-only run (solve_helmholtz, krylov.py:156-177) is reported in the same line under
+``mg_only``.  One "step" = one batched solve of all the RHS.  Synthetic seeded data.
 
 Arms
-  default           the B200 path (libhelmsolve_b200.so), N GPUs via torchrun,
-                    one independent C2 instance per rank (weak scaling), no
-                    collective on the data path; NCCL only for the max-over-ranks
-                    timing and the result gather.
-  --impl reference  the reference's CPU algorithm (the numpy oracle port of
-                    helmsolve; the reference is pure Python) on the host cores,
-                    rank 0 only.
+  default           the B200 path (libhelmsolve_b200.so).  With --gpus N > 1 (and no torchrun
+                    environment) the script re-launches itself under torch.distributed.run with
+                    one rank per GPU; each rank solves its contiguous share of the SAME 64 RHS
+                    (dist.shard_range, strong scaling), NCCL only for the max-over-ranks timing
+                    and the all-gather of the per-RHS reports (dist.sharded_solve).
+  --impl reference  the reference's CPU algorithm (the numpy oracle port of helmsolve; the
+                    reference is pure Python) on the host cores, rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,10 +38,6 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Helmholtz RHS solved/sec to rel-res 1e-6"
 UNIT = "RHS/s"
-# Mean FGMRES iterations per RHS of the C2 learned workload (seed offset 0),
-# measured by the B200 arm and matched by the oracle within +-1 (parity tests).
-# Used only to extrapolate the CPU arm's bounded sample to whole solves.
-C2_MEAN_ITERS = {"learned": 123.1, "vcycle": 113.2}
 
 
 def log(*a):
@@ -125,51 +126,94 @@ def dist_setup():
     return world, rank, local
 
 
-def cpu_leg(args, learned: bool, steps: int, warmup: int):
-    """Oracle port on the host cores: (value RHS/s per step list, description)."""
+CFG_TEXT = {
+    "C1": "129x129, 1 smooth-random model x 4 point sources, MG 3 levels, CNN 16/32/64, FGMRES(10)",
+    "C2": "257x257, 4 smooth-random models x 32 point sources, MG 3 levels, CNN 16/32/64, FGMRES(10)",
+    "C3": "513x1025, layered+10% noise model, 64 RHS (32 point + 32 complex Gaussian), MG 4 levels, "
+          "CNN 16/32/64/128 (implicit layer at 64x128), FGMRES(20)",
+    "C4": "1025x2049, smooth-random model, 128 point sources, MG 4 levels, CNN 16/32/64/128, FGMRES(20)",
+    "C5": "2049x4097, salt model, 256 point sources, MG 5 levels, CNN 16/32/64/128/128 (implicit at 128x256), "
+          "FGMRES(30)",
+}
+
+
+def workload_config(args, cfg=None, world=1):
+    """The config the line was measured on, derived from the ProblemSet itself (not hard-coded)."""
+    from paper_2306_17486_b200 import dist as hdist
+
+    if cfg is None:
+        from paper_2306_17486_b200 import problems
+
+        cfg = problems.make_config(args.config)
+    B = cfg.rhs.shape[0]
+    nx, ny = cfg.shape
+    learned = args.precond == "learned"
+    return {
+        "workload": f"{args.config} ({CFG_TEXT.get(args.config, '')}); headline precond: "
+                    f"{'MG + CNN (learned protocol)' if learned else 'MG only'}; tol {cfg.tol:g}",
+        "grid": f"{nx}x{ny}", "models": len(cfg.models), "rhs_total": B,
+        "rhs_per_gpu": [len(range(*hdist.shard_range(B, world, r))) for r in range(world)],
+        "mg_levels": cfg.mg_levels, "jacobi_damping": list(cfg.jacobi_damping),
+        "cnn_channels": list(cfg.cnn_channels) if learned else None, "restart": cfg.restart,
+        "max_iter": cfg.max_iter, "precond": args.precond,
+        "l2": "working set far larger than the 126 MB L2 (C3 Krylov bases 64 x 41 x 525k x 8 B = 11 GB); "
+              "no flush needed",
+        "parallelism": f"RHS-sharded across {world} GPU(s) (dist.shard_range), no data-path collective",
+    }
+
+
+def cpu_arm_value(arm, learned, iters, warm, config):
+    """One bounded CPU sample -> (RHS/s extrapolated with the REFERENCE's own iteration count, description)."""
     from oracle import cpu_bench
 
-    workers = args.cpu_workers or (os.cpu_count() or 1)
-    vals = []
-    t_v = t_l = 0.0
-    for s in range(warmup + steps):
-        t_v, t_l = cpu_bench.sample(args.config, learned, workers, args.cpu_iters, args.rhs_per_model)
-        if s >= warmup:
-            mean_iters = C2_MEAN_ITERS["learned" if learned else "vcycle"]
-            vals.append(cpu_bench.rhs_per_second(t_v, t_l, workers, mean_iters, learned))
-    desc = (f"{workers} processes x 1 RHS each, {args.cpu_iters} FGMRES iterations per phase "
-            f"(V-cycle {t_v * 1e3:.1f} ms/it, net+V-cycle {t_l * 1e3:.1f} ms/it), extrapolated to "
-            f"{C2_MEAN_ITERS['learned' if learned else 'vcycle']:.0f} iterations per RHS; numpy oracle port")
-    return vals, workers, desc
+    t_v, t_l = arm.sample(iters, warm)
+    mean_iters, n_ref = cpu_bench.reference_iterations(config, learned)
+    if mean_iters is None:
+        raise RuntimeError(f"no reference iteration count for {config} (tests/golden/configs_*.npz)")
+    v = cpu_bench.rhs_per_second(t_v, t_l, arm.workers, mean_iters, learned, warm)
+    desc = (f"{arm.workers} single-threaded processes x 1 RHS of {config}: "
+            + (f"{warm} V-cycle-only warm-up iterations ({t_v * 1e3:.0f} ms/it) + {iters} net+V-cycle iterations "
+               f"({t_l * 1e3:.0f} ms/it)" if learned else f"{iters} V-cycle iterations ({t_v * 1e3:.0f} ms/it)")
+            + f", extrapolated to {mean_iters:.1f} iterations per RHS = the reference's own mean over {n_ref} "
+              f"full C3 solves (tests/golden/configs_{config.lower()}.npz); numpy oracle port")
+    return v, desc
 
 
 def run_reference(args):
+    """--impl reference: the oracle port on the host cores, rank 0 only, bounded steps."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    from oracle import cpu_bench
+
     learned = args.precond == "learned"
+    workers = args.cpu_workers or (os.cpu_count() or 1)
+    arm = cpu_bench.CpuArm(args.config, learned, workers)
     t0 = time.perf_counter()
-    vals, workers, desc = cpu_leg(args, learned, args.steps, args.warmup)
+    for _ in range(args.warmup):  # untimed: pool set-up (oracle hierarchy, encodings) + one V-cycle iteration
+        arm.sample(0, 1)
+    t1 = time.perf_counter()
+    vals = []
+    desc = ""
+    for _ in range(args.steps):
+        v, desc = cpu_arm_value(arm, learned, 1, 3 if learned else 0, args.config) if learned else \
+            cpu_arm_value(arm, learned, 4, 0, args.config)
+        vals.append(v)
+    arm.close()
     value = float(np.mean(vals))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * (time.perf_counter() - t0) / (args.steps + args.warmup),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128/f64 (numpy oracle)",
-        "data": "synthetic", "config": workload_config(args),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": desc},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * (time.perf_counter() - t1) / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128/f64 (numpy oracle)",
+        "data": "synthetic", "config": workload_config(args, world=1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                         "sample": "each step: " + desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup_s": t1 - t0,
     }
     print(json.dumps(line), flush=True)
     return 0
-
-
-def workload_config(args):
-    return {"workload": f"{args.config}: 4 models x {args.rhs_per_model} RHS, 257x257, "
-                        f"{'MG3 + CNN 16/32/64' if args.precond == 'learned' else 'MG3 only'}, FGMRES(10), tol 1e-6",
-            "global_batch_per_gpu": 4 * args.rhs_per_model, "precond": args.precond,
-            "l2": "working set (Krylov basis ~1.4 GB/GPU) far larger than L2; no flush needed",
-            "parallelism": f"rhs-sharded dp (independent instance per rank)"}
 
 
 DG_METRIC = "training pairs (r, e) generated/sec (257x257, k ~ U{2..20} V-cycle FGMRES iterations)"
@@ -469,32 +513,60 @@ def run_train(args):
     return 0
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="C2")
-    ap.add_argument("--precond", default="learned", choices=["learned", "vcycle"])
-    ap.add_argument("--rhs-per-model", type=int, default=32)
-    ap.add_argument("--cpu-workers", type=int, default=0, help="0 = all host cores")
-    ap.add_argument("--cpu-iters", type=int, default=3)
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="solve", choices=["solve", "datagen", "train"],
-                    help="solve: the BASELINE metric (default); datagen: SURVEY 8f row 1, training pairs; "
-                         "train: SURVEY 8f row 2, network training steps")
-    ap.add_argument("--train-batch", type=int, default=16, help="train: samples per step")
-    ap.add_argument("--samples", type=int, default=256, help="datagen: samples per step")
-    args = ap.parse_args()
-    if args.workload == "datagen":
-        return run_datagen(args)
-    if args.workload == "train":
-        return run_train(args)
-    if args.impl == "reference":
-        return run_reference(args)
+def free_port() -> int:
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
 
+
+def relaunch(args) -> int:
+    """--gpus N without a torchrun environment: run this script under torch.distributed.run, N ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    log("relaunching under torchrun: " + " ".join(cmd))
+    return subprocess.call(cmd)
+
+
+# profiling tags: name, work unit ("bytes" -> GB/s, "flops" -> TFLOP/s)
+PROFILE_TAGS = (("convs", "CONV", "flops"), ("convs_l0_16ch", "CONV_L0", "bytes"), ("convs_wide", "CONV_WIDE", "flops"),
+                ("vcycle", "VCYCLE", "bytes"), ("arnoldi_dot", "ARNOLDI", "bytes"), ("cnn_forward", "CNN", None),
+                ("implicit_layer", "IMPLICIT", "bytes"), ("vc_up_l0", "VC_UP0", "bytes"))
+
+
+def profiled_pass(lib, solver, rhs_dev, kw, max_iter):
+    """Per-tag kernel times from a SEPARATE solve with CUDA events around every tagged launch.
+
+    Profiling events serialise the programmatic-dependent-launch chain of the convolutions, so they are
+    never on inside the timed region.  The pass solves the same batch truncated at ``max_iter``
+    iterations (warm-up phase + learned phase), which keeps the per-launch averages representative of
+    the full solve (every RHS is still active) at a fraction of its cost.
+    """
+    import torch
+
+    from paper_2306_17486_b200 import _lib
+
+    tags = [(n, getattr(_lib, "PROF_" + t), u) for n, t, u in PROFILE_TAGS if hasattr(_lib, "PROF_" + t)]
+    lib.hs_profile_reset()
+    lib.hs_profile_enable(sum(1 << t for _, t, _ in tags))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    solver.solve(rhs_dev, **dict(kw, max_iter=max_iter, raise_errors=False))
+    torch.cuda.synchronize()
+    wall_ms = 1e3 * (time.perf_counter() - t0)
+    prof = {n: (_lib.profile_query(t), u) for n, t, u in tags}
+    lib.hs_profile_enable(0)
+    out = {}
+    for n, ((tms, work, cnt), unit) in prof.items():
+        row = {"ms": round(tms, 3), "share": round(tms / wall_ms, 4) if wall_ms else None, "launches": cnt}
+        if tms > 0 and unit == "bytes":
+            row.update(achieved=round(work / (tms / 1e3) / 1e9, 2), unit="GB/s")
+        elif tms > 0 and unit == "flops":
+            row.update(achieved=round(work / (tms / 1e3) / 1e12, 2), unit="TFLOP/s")
+        out[n] = row
+    return out, wall_ms
+
+
+def run_solve(args):
     import torch
 
     world, rank, local = dist_setup()
@@ -503,70 +575,95 @@ def main():
     from paper_2306_17486_b200.device import to_device
 
     learned = args.precond == "learned"
-    cfg = problems.make_config(args.config, rhs_per_model=args.rhs_per_model, seed_offset=rank)
-    net = network.EncoderSolverNet.seeded(cfg.cnn_channels, seed=0) if learned else None
-    t_setup = time.perf_counter()
-    solver = krylov.BatchSolver(cfg.models, net, jacobi_damping=cfg.jacobi_damping, num_levels=cfg.mg_levels)
-    torch.cuda.synchronize()
-    t_setup = time.perf_counter() - t_setup
-    B = cfg.rhs.shape[0]
-    rhs_dev = to_device(cfg.rhs, torch.complex128)
-    owner = cfg.model_of_rhs
-    solve_kw = dict(model_of=owner, tol=cfg.tol, max_iter=cfg.max_iter, restart=cfg.restart, return_device=True)
+    cfg = problems.make_config(args.config)
+    B_all = cfg.rhs.shape[0]
+    lo, hi = hdist.shard_range(B_all, world, rank)
+    rhs_local, owner = cfg.rhs[lo:hi], cfg.model_of_rhs[lo:hi]
+    B = hi - lo
     lib = _lib.load()
 
-    for _ in range(args.warmup):
-        _, reps = solver.solve(rhs_dev, **solve_kw)
-    iters = np.array([r.iterations for r in reps], dtype=np.float64)
-    conv = all(r.converged for r in reps)
-    log(f"[rank {rank}] setup {t_setup:.2f}s, iterations mean {iters.mean():.1f} [{iters.min():.0f}..{iters.max():.0f}], "
-        f"converged {conv}")
+    def make_solver(use_net):
+        net = network.EncoderSolverNet.seeded(cfg.cnn_channels, seed=0) if use_net else None
+        return krylov.BatchSolver(cfg.models, net, jacobi_damping=cfg.jacobi_damping, num_levels=cfg.mg_levels)
 
-    # ---------------- timed region: device-resident inputs
-    tags = [_lib.PROF_CONV, _lib.PROF_CONV_L0, _lib.PROF_VCYCLE, _lib.PROF_ARNOLDI, _lib.PROF_CNN,
-            _lib.PROF_IMPLICIT, _lib.PROF_VC_UP0]
-    lib.hs_profile_reset()
-    lib.hs_profile_enable(sum(1 << t for t in tags))
-    stream = torch.cuda.current_stream()
-    if world > 1:
-        torch.distributed.barrier()
+    t_setup = time.perf_counter()
+    solver = make_solver(learned)
     torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    total_iters = 0
-    with ClockSampler(local) as clk:
+    t_setup = time.perf_counter() - t_setup
+    rhs_dev = to_device(rhs_local, torch.complex128)
+    kw = dict(model_of=owner, tol=cfg.tol, max_iter=cfg.max_iter, restart=cfg.restart, return_device=True)
+    stream = torch.cuda.current_stream()
+
+    def timed(slv, steps):
+        """device-timed steps (CUDA events, barrier + synchronize on both sides), max over ranks"""
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        its, reps = 0, None
         ev0.record(stream)
-        for _ in range(args.steps):
-            _, reps = solver.solve(rhs_dev, **solve_kw)
-            total_iters += sum(r.iterations for r in reps)
+        for _ in range(steps):
+            _, reps = slv.solve(rhs_dev, **kw)
+            its += sum(r.iterations for r in reps)
         ev1.record(stream)
         torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
-    launches = int(lib.hs_launch_count())
-    prof = {t: _lib.profile_query(t) for t in tags}
-    lib.hs_profile_enable(0)
-    ms = hdist.reduce_scalar(ms, "max")  # max over ranks
-    total_iters = int(hdist.reduce_scalar(total_iters, "sum"))
-    value = world * B * args.steps / (ms / 1e3)
-    applies = total_iters / (ms / 1e3)
+        if world > 1:
+            torch.distributed.barrier()
+        return hdist.reduce_scalar(ev0.elapsed_time(ev1), "max"), int(hdist.reduce_scalar(its, "sum")), reps
 
-    # ---------------- e2e through the public API with pinned host buffers
+    for _ in range(args.warmup):
+        solver.solve(rhs_dev, **kw)
+    lib.hs_profile_enable(0)
+    lib.hs_profile_reset()  # launch counter
+    with ClockSampler(local) as clk:
+        ms, total_iters, reps = timed(solver, args.steps)
+    launches = int(hdist.reduce_scalar(int(lib.hs_launch_count()), "sum"))
+    value = B_all * args.steps / (ms / 1e3)
+    applies = total_iters / (ms / 1e3)
+    # per-RHS results of the whole batch, gathered over ranks in batch order (NCCL all_gather)
+    rows = hdist.gather_reports(hdist.report_rows(reps))
+    iters = np.array([r[0] for r in rows], dtype=np.float64)
+    conv = all(r[2] for r in rows)
+    log(f"[rank {rank}] {B} RHS, setup {t_setup:.2f}s, {ms / args.steps:.1f} ms/step, iterations mean "
+        f"{iters.mean():.1f} [{iters.min():.0f}..{iters.max():.0f}], converged {conv}")
+
+    # ---------------- e2e through the public API: pinned host RHS in, host x and histories out, every step
     e2e = None
     if not args.no_e2e:
-        rhs_pinned = torch.from_numpy(np.ascontiguousarray(cfg.rhs)).pin_memory()
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        rhs_pinned = torch.from_numpy(np.ascontiguousarray(rhs_local)).pin_memory()
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         d2h = 0
-        for _ in range(args.steps):
-            x, reps = solver.solve(rhs_pinned, model_of=owner, tol=cfg.tol, max_iter=cfg.max_iter,
-                                   restart=cfg.restart, return_device=False)
-            d2h = x.nbytes + sum(8 * len(r.relative_residual_history) for r in reps)
+        for _ in range(e2e_steps):
+            x, reps_h = solver.solve(rhs_pinned, model_of=owner, tol=cfg.tol, max_iter=cfg.max_iter,
+                                     restart=cfg.restart, return_device=False)
+            d2h = x.nbytes + sum(8 * len(r.relative_residual_history) for r in reps_h)
         torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-        el = hdist.reduce_scalar(el, "max")
-        e2e = {"value": world * B * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": int(rhs_pinned.numel() * 16),
-               "d2h_bytes_per_step": int(d2h)}
+        el = hdist.reduce_scalar(time.perf_counter() - t0, "max")
+        e2e = {"value": B_all * e2e_steps / el, "unit": UNIT,
+               "h2d_bytes_per_step": int(hdist.reduce_scalar(rhs_pinned.numel() * 16, "sum")),
+               "d2h_bytes_per_step": int(hdist.reduce_scalar(d2h, "sum")), "steps": e2e_steps,
+               "path": "krylov.BatchSolver.solve(host numpy/pinned RHS, return_device=False)"}
+
+    # ---------------- breakdown / roofline from a separate profiled pass (never inside the timed region)
+    breakdown, prof_ms = profiled_pass(lib, solver, rhs_dev, kw, args.profile_iters)
+
+    # ---------------- the multigrid-only run of the same config (BASELINE runs C3 both ways)
+    mg_only = None
+    if learned and not args.no_mg:
+        mg_solver = make_solver(False)
+        for _ in range(args.warmup):
+            mg_solver.solve(rhs_dev, **kw)
+        ms_mg, its_mg, reps_mg = timed(mg_solver, args.steps)
+        rows_mg = hdist.gather_reports(hdist.report_rows(reps_mg))
+        it_mg = np.array([r[0] for r in rows_mg], dtype=np.float64)
+        mg_only = {"value": B_all * args.steps / (ms_mg / 1e3), "unit": UNIT, "ms_per_step": ms_mg / args.steps,
+                   "iterations_per_rhs": float(it_mg.mean()), "converged": all(r[2] for r in rows_mg),
+                   "precond_applies_per_s": its_mg / (ms_mg / 1e3)}
+        del mg_solver
 
     if rank != 0:
         if world > 1:
@@ -574,59 +671,101 @@ def main():
         return 0
 
     hbm, bf16, src = load_peaks()
-    # dominant kernel class: the network's convolutions (learned) or the finest V-cycle up-leg (MG only)
-    if learned:
-        # k_conv_tc<16,16,0>: the level-0 16->16 3x3 conv (8 of the 16 network convs per application run at
-        # level 0 and 4 of them are this kernel).  Arithmetic intensity 4608 flop per output pixel over
-        # 128-192 B (input + output, + residual for the second conv of a residual block) = 24-36 flop/B is
-        # far below the ridge (1621 TFLOP/s / 6.5 TB/s = 250), so its roof is HBM.  The library's CONV_L0
-        # tag accumulates exactly those algorithmic bytes per launch (times the active RHS).
-        c_ms, c_bytes, c_n = prof[_lib.PROF_CONV_L0]
-        achieved = c_bytes / (c_ms / 1e3) / 1e9 if c_ms > 0 else 0.0
-        traffic = load_traffic()
-        roof = {"kernel": "k_conv_tc<16,16,0> (tcgen05 BF16x3 implicit-GEMM 3x3 conv, level 0)", "bound": "hbm",
-                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "peak_note": f"{src} copy bandwidth", "launches": c_n, "ms_total": c_ms,
-                "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
-                "traffic_note": traffic.get("note") if traffic else None}
-    else:
-        u_ms, u_bytes, u_n = prof[_lib.PROF_VC_UP0]
-        achieved = u_bytes / (u_ms / 1e3) / 1e9 if u_ms > 0 else 0.0
-        roof = {"kernel": "k_vc_up (finest level)", "bound": "hbm", "achieved": achieved, "peak": hbm,
-                "unit": "GB/s", "frac": achieved / hbm, "peak_note": f"{src} copy bandwidth", "launches": u_n,
-                "ms_total": u_ms, "traffic": None}
-    breakdown = {}
-    names = {_lib.PROF_CONV: "convs", _lib.PROF_CONV_L0: "convs_l0_16ch", _lib.PROF_VCYCLE: "vcycle",
-             _lib.PROF_ARNOLDI: "arnoldi_dot", _lib.PROF_CNN: "cnn_forward", _lib.PROF_IMPLICIT: "implicit_layer",
-             _lib.PROF_VC_UP0: "vc_up_l0"}
-    for t, (tms, work, n) in prof.items():
-        breakdown[names[t]] = {"ms": round(tms, 3), "share": round(tms / ms, 4) if ms else None, "launches": n}
-    for t, unit, scale in ((_lib.PROF_VCYCLE, "GB/s", 1e9), (_lib.PROF_ARNOLDI, "GB/s", 1e9),
-                           (_lib.PROF_VC_UP0, "GB/s", 1e9), (_lib.PROF_CONV_L0, "GB/s", 1e9)):
-        tms, work, n = prof[t]
-        if tms > 0:
-            breakdown[names[t]]["achieved"] = round(work / (tms / 1e3) / scale, 2)
-            breakdown[names[t]]["unit"] = unit
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            bf16_sus = float(json.load(f).get("bf16_tflops_sustained", bf16))
+    except Exception:
+        bf16_sus = bf16
+    roof = roofline(breakdown, learned, hbm, bf16_sus, src)
 
     cpu = None
     if world == 1 and not args.no_cpu:
-        vals, workers, desc = cpu_leg(args, learned, 1, 0)
-        cpu = {"value": vals[0], "unit": UNIT, "cores": workers, "kind": "port", "sample": desc}
+        from oracle import cpu_bench
+
+        workers = args.cpu_workers or (os.cpu_count() or 1)
+        arm = cpu_bench.CpuArm(args.config, learned, workers)
+        v, desc = cpu_arm_value(arm, learned, 1 if learned else 4, 3 if learned else 0, args.config)
+        arm.close()
+        cpu = {"value": v, "unit": UNIT, "cores": workers, "kind": "port", "sample": desc}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "c64 basis/fp32 CNN, fp64 operator+reductions, c128 iterate",
-        "data": "synthetic (seeded generators; random-init seeded network)", "config": workload_config(args),
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "c64 basis/V-cycle, fp32-class CNN (BF16x3 tcgen05), fp64 operator+reductions, "
+                                      "c128 iterate",
+        "data": "synthetic (seeded generators; random-init seeded network)",
+        "config": workload_config(args, cfg, world),
         "precond_applies_per_s": applies, "iterations_per_rhs": float(iters.mean()),
-        "converged": conv, "setup_s": t_setup,
-        "roofline": roof, "breakdown": breakdown, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": launches, "clocks": clk.summary(),
+        "iterations_range": [int(iters.min()), int(iters.max())], "converged": conv, "setup_s": t_setup,
+        "mg_only": mg_only, "roofline": roof, "breakdown": breakdown,
+        "breakdown_note": f"separate profiled pass (CUDA events per tagged launch), same batch truncated at "
+                          f"{args.profile_iters} iterations, {prof_ms:.0f} ms wall; shares are of that pass",
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def roofline(breakdown, learned, hbm, bf16_sus, src):
+    """Roofline of the dominant kernel class of the profiled pass."""
+    traffic = load_traffic() or {}
+    if learned:
+        cands = {k: v for k, v in breakdown.items() if k in ("convs_l0_16ch", "convs_wide") and v.get("ms", 0) > 0}
+        name = max(cands, key=lambda k: cands[k]["ms"]) if cands else "convs_l0_16ch"
+    else:
+        name = "vc_up_l0"
+    row = breakdown.get(name, {})
+    ach = row.get("achieved", 0.0)
+    if name == "convs_wide":
+        # tensor-bound: algorithmic fp32-class flops; each is 6 bf16 tensor products (exact BF16x3 split)
+        peak = bf16_sus / 6.0
+        return {"kernel": "k_conv_wide (tcgen05 BF16x3 implicit-GEMM 3x3 convs, >= 64 channels)", "bound": "tensor",
+                "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak if peak else None,
+                "peak_note": f"{src} sustained bf16 {bf16_sus:.0f} TFLOP/s / 6 (six bf16 products per fp32-class "
+                             f"product)", "launches": row.get("launches"), "ms_total": row.get("ms"),
+                "traffic": traffic.get("wide_dram_bytes_per_launch"), "traffic_note": traffic.get("wide_note")}
+    kern = ("k_conv_tc<16,16,0> (tcgen05 BF16x3 implicit-GEMM 3x3 conv, level 0)" if learned
+            else "k_vc_up (finest level)")
+    return {"kernel": kern, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+            "frac": ach / hbm if hbm else None, "peak_note": f"{src} copy bandwidth",
+            "launches": row.get("launches"), "ms_total": row.get("ms"),
+            "traffic": traffic.get("dram_bytes_per_launch") if learned else None,
+            "traffic_note": traffic.get("note") if learned else None}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--precond", default="learned", choices=["learned", "vcycle"])
+    ap.add_argument("--cpu-workers", type=int, default=0, help="0 = all host cores")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-mg", action="store_true", help="skip the multigrid-only run of the learned config")
+    ap.add_argument("--e2e-steps", type=int, default=3, help="e2e steps (<= --steps)")
+    ap.add_argument("--profile-iters", type=int, default=24, help="iterations of the separate profiled pass")
+    ap.add_argument("--workload", default="solve", choices=["solve", "datagen", "train"],
+                    help="solve: the BASELINE metric (default); datagen: SURVEY 8f row 1, training pairs; "
+                         "train: SURVEY 8f row 2, network training steps")
+    ap.add_argument("--train-batch", type=int, default=16, help="train: samples per step")
+    ap.add_argument("--samples", type=int, default=256, help="datagen: samples per step")
+    args = ap.parse_args()
+    if args.warmup < 0 or args.steps < 1:
+        ap.error("--steps must be >= 1 and --warmup >= 0")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        return relaunch(args)
+    if args.workload == "datagen":
+        return run_datagen(args)
+    if args.workload == "train":
+        return run_train(args)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_solve(args)
 
 
 if __name__ == "__main__":

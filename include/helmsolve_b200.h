@@ -141,11 +141,12 @@ HS_API int hs_jacobi(const void* u, const void* rhs, void* out, const hs_level_t
 
 /* multigrid.v_cycle (multigrid.py:247-274) over B right-hand sides;
  * rhs/u0/out complex64 (B, nx0, ny0); u0 may be NULL.  A one-level hierarchy
- * is multigrid.coarse_solve (multigrid.py:232-244). `status` (device int,
- * may be NULL) receives HS_EBREAKDOWN / HS_ENONFINITE from the coarse GMRES. */
+ * is multigrid.coarse_solve (multigrid.py:232-244). */
 HS_API size_t hs_vcycle_workspace_bytes(const hs_hierarchy_t* h, int B);
 HS_API int hs_vcycle(const hs_hierarchy_t* h, const void* rhs, const void* u0, void* out, const int* model_of,
                      int B, void* ws, size_t ws_bytes, int* status, void* stream);
+/* status: B device ints, zeroed by the caller; status[b] receives HS_EBREAKDOWN / HS_ENONFINITE when RHS b's
+   coarse-grid GMRES fails (multigrid.py:232-244 -> krylov.py:96-99, :130-134) */
 
 /* krylov.fgmres specialised to the Helmholtz solve (krylov.py:39-146), the
  * engine behind krylov.solve_helmholtz (:156-177) and both phases of
@@ -180,7 +181,8 @@ HS_API void hs_profile_reset(void);
 HS_API int hs_profile_query(int tag, double* total_ms, double* total_work, long long* count);
 /* kernels launched by the library since the last hs_profile_reset */
 HS_API long long hs_launch_count(void);
-/* 1 (default): tcgen05 3xTF32 convolutions where the shape allows; 0: SIMT fp32 only */
+/* 1 (default): tcgen05 BF16x3 convolutions (exact three-way bf16 split, fp32 accumulate) where the shape
+   allows; 0: SIMT fp32 only (a test switch for A/B parity; it never skips work) */
 HS_API void hs_set_conv_path(int tensor_cores);
 
 /* ---- slowness-model preparation (SPEC.md datagen: load_slowness_corpus / gaussian_smooth,

@@ -182,7 +182,8 @@ def load():
         return _lib
 
 
-PROF_CONV, PROF_CONV_L0, PROF_VCYCLE, PROF_ARNOLDI, PROF_CNN, PROF_IMPLICIT, PROF_VC_UP0, PROF_TRAIN_WGRAD = range(8)
+(PROF_CONV, PROF_CONV_L0, PROF_VCYCLE, PROF_ARNOLDI, PROF_CNN, PROF_IMPLICIT, PROF_VC_UP0, PROF_TRAIN_WGRAD,
+ PROF_CONV_WIDE) = range(9)
 
 
 def profile_query(tag: int):

@@ -774,9 +774,6 @@ void launch_thin1w(const ConvArgs& a, const float* host_w, int B, cudaStream_t s
   k_conv_thin1w<CIN, COUT><<<grid, kThinThreads, 0, st>>>(a, wt);
 }
 
-// HS_THIN_SMEM=1 keeps the shared-memory thin kernels (A/B comparisons)
-const bool thin_smem_path = getenv("HS_THIN_SMEM") && atoi(getenv("HS_THIN_SMEM")) == 1;
-
 int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* y, const float* addend,
                 long long addend_bstride, const int* model_of, const float* residual, const void* const* active,
                 cudaStream_t st, bool model_of_addend = false, const ThinIO* io = nullptr, bool planar_out = false) {
@@ -822,6 +819,7 @@ int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* 
   // CONV_L0 records algorithmic HBM bytes: input + output (+ addend) (+ residual), once each
   const double l0_bytes = 4.0 * 16 * (double)H * W * (2 + (addend ? 1 : 0) + (residual ? 1 : 0)) *
                           prof::active_hint(B);
+  const bool wide = (c.cin >= 64 || c.cout >= 64) && c.cin > 2 && c.cout > 2;
   struct Scope2 {
     int s1, s2;
     cudaStream_t st;
@@ -831,12 +829,14 @@ int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* 
       prof::stop(s1, st, w1);
     }
   };
-  Scope2 scope{prof::start(prof::CONV, st), l0 ? prof::start(prof::CONV_L0, st) : -1, st, flops, l0_bytes};
+  Scope2 scope{prof::start(prof::CONV, st),
+               l0 ? prof::start(prof::CONV_L0, st) : (wide ? prof::start(prof::CONV_WIDE, st) : -1), st, flops,
+               l0 ? l0_bytes : flops};
   a.residual = residual;
   a.active = active;
   if ((a.cx_ld > 0 || a.cy) && !(!c.transposed && c.stride == 1 && (c.cin == 2 || c.cout == 2)))
     return HS_ECONFIG;  // complex I/O is fused into the thin stem / head only
-  if (!c.transposed && c.stride == 1 && io && io->host_w && !thin_smem_path) {
+  if (!c.transposed && c.stride == 1 && io && io->host_w) {
     if (c.cin == 2 && c.cout == 16) return launch_thin1<2, 16>(a, io->host_w, B, st), HS_OK;
     if (c.cin == 16 && c.cout == 2) return launch_thin1w<16, 2>(a, io->host_w, B, st), HS_OK;
     if (c.cin == 2 && c.cout == 8) return launch_thin1<2, 8>(a, io->host_w, B, st), HS_OK;
@@ -1171,7 +1171,9 @@ static int solver_forward(const hs_net_t* net, const float* in, float* head, con
   const int islot = prof::start(prof::IMPLICIT, st);
   rc = implicit_apply_dev(net, S[L1], X[L1], reinterpret_cast<cufftComplex*>(ws + L.fftz), active, B, st,
                           L1 > 0 && coarse_planar(net, d.ix >> L1, d.iy >> L1));
-  prof::stop(islot, st, 0.0);
+  // algorithmic bytes: complex64 input + output of every (RHS, complex channel) (the spectrum is L2-resident)
+  prof::stop(islot, st,
+             2.0 * 8.0 * (d.channels[L1] / 2) * (double)(d.ix >> L1) * (double)(d.iy >> L1) * prof::active_hint(B));
   if (rc) return rc;
   // up path: X[l] -> (tconv + skip) X[l-1] -> residual block
   for (int l = L1; l >= 1; --l) {

@@ -53,6 +53,18 @@ constexpr int kPrefetch = 4;  // rows pulled into L2 ahead of the bulk copies / 
 constexpr int kNA = 4;    // TMEM accumulators in flight
 constexpr int kEpiWarps = 8, kCvtWarp0 = 8;  // epilogue warps 0-7, converters from warp 8
 constexpr size_t kSmemMax = 232448;
+// Stage-removal probes for a separate measurement build only (tools/; `make PROBE=<mask>`): 1 skip
+// conversion, 2 skip MMAs, 4 skip epilogue math, 32 force M = 64, 64 skip stores, 128 skip input loads,
+// 256 skip addend loads.  The product build compiles with 0, so nothing read at run time can change
+// what a launch computes.
+#ifndef HS_TC_PROBE
+#define HS_TC_PROBE 0
+#endif
+constexpr int kProbe = HS_TC_PROBE;
+// programmatic dependent launch between chained convolutions (0 only in an A/B probe build)
+#ifndef HS_TC_PDL
+#define HS_TC_PDL 1
+#endif
 #ifndef HS_TC_ATM_NA
 #define HS_TC_ATM_NA 2
 #endif
@@ -193,8 +205,6 @@ struct TcArgs {
   const void* const* active;
   int B;
   int band;  // output rows per work unit (a CTA walks a band of one column block top to bottom)
-  int dbg;   // experiment switch (HS_TC_DBG): 1 skip conversion, 2 skip MMAs, 4 skip epilogue math, 64 skip
-             // stores, 128 skip input loads, 256 skip addend loads
   int planar;  // complex-planar output (conv_tc.h)
 };
 
@@ -602,7 +612,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
           const long long use = seq / NR;
           if (use > 0) mbar_wait(smem_u32(&raw_empty[s]), (uint32_t)((use - 1) & 1));
           const uint32_t bar = smem_u32(&raw_full[s]);
-          if (g >= 0 && g < a.H && chi > clo && !(a.dbg & 128)) {
+          if (g >= 0 && g < a.H && chi > clo && !(kProbe & 128)) {
             const uint32_t bytes = (uint32_t)(chi - clo) * CIN * 4;
             mbar_arrive_tx(bar, bytes);
             bulk_g2s(smem_u32(raw + (size_t)s * C::RAW_BYTES + (size_t)(clo - x0) * CIN * 4),
@@ -632,7 +642,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
         mbar_wait(smem_u32(&raw_full[rs]), (uint32_t)((seq / NR) & 1));
         const bool row_ok = g >= 0 && g < a.H;
         const unsigned char* src = raw + (size_t)rs * C::RAW_BYTES;
-        for (int e = ct; e < ((a.dbg & 1) ? 0 : C::RW * KC); e += C::GCVT_THREADS) {
+        for (int e = ct; e < ((kProbe & 1) ? 0 : C::RW * KC); e += C::GCVT_THREADS) {
           const int p = e / KC, c = e - p * KC;  // chunk fastest: conflict-free raw reads
           float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
           if (row_ok && p >= clo && p < chi) {
@@ -718,7 +728,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
             if (ause > 0) mbar_wait(smem_u32(&acc_empty[acc]), (ause - 1) & 1);
             tc_fence_after();
             const uint32_t d0 = tm + acc * C::ACOLS;
-            if (!(a.dbg & 2)) {
+            if (!(kProbe & 2)) {
 #pragma unroll
               for (int ky = 0; ky < 3; ++ky)
                 mma_row9_tm<I0, I1, I2, WT>(d0, tm + C::AOFF + tslot(oy - 1 + ky) * C::SLOT_COLS,
@@ -761,7 +771,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
           const uint32_t ause = tile / C::NA;
           if (ause > 0) mbar_wait(smem_u32(&acc_empty[acc]), (ause - 1) & 1);
           tc_fence_after();
-          if (!(a.dbg & 2)) issue_mmas<C, MODE, MT>(oy, tm + acc * C::ACOLS, db, slot);
+          if (!(kProbe & 2)) issue_mmas<C, MODE, MT>(oy, tm + acc * C::ACOLS, db, slot);
           mma_commit(smem_u32(&acc_full[acc]));
           // release rows this issuer's next tile of the unit no longer reads (a row is
           // released only after it was seen staged: an early arrival would complete the
@@ -817,7 +827,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
 #pragma unroll
           for (int q = 0; q < EH / 4; ++q) {
             pa[k][q] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (add && lane_ok && !(a.dbg & 256)) pa[k][q] = __ldg(reinterpret_cast<const float4*>(add + pix * COUT + n_base) + q);
+            if (add && lane_ok && !(kProbe & 256)) pa[k][q] = __ldg(reinterpret_cast<const float4*>(add + pix * COUT + n_base) + q);
             float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
             if (a.residual && lane_ok) r = __ldg(reinterpret_cast<const float4*>(a.residual + obase) + q);
             if constexpr (SPLIT) {
@@ -861,7 +871,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&acc_empty[acc]));  // TMEM free; finish from registers
-        if (lane_ok && !(a.dbg & 4)) {
+        if (lane_ok && !(kProbe & 4)) {
 #pragma unroll
           for (int k = 0; k < C::NACC; ++k) {
             const int ox = MODE == 2 ? 2 * (U.xb * MT + m) + k : U.xb * MT + m;
@@ -891,10 +901,9 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
                              ((size_t)U.b * (COUT / 2) + (n_base + n0) / 2) * ((size_t)a.Ho * a.Wo) + pix;
                 yp[0] = make_float2(o.x, o.y);
                 yp[(size_t)a.Ho * a.Wo] = make_float2(o.z, o.w);
-              } else if (!(a.dbg & 64)) {
+              } else if (!(kProbe & 64)) {
                 *reinterpret_cast<float4*>(a.y + obase + n0) = o;
               }
-              else if (o.x == 1234.5f) a.y[0] = o.y;
             }
           }
         }
@@ -941,7 +950,7 @@ void launch_tc(const TcArgs& a, cudaStream_t st) {
   while (b.band > 8 && C::NSPLIT * act * xblocks * ((a.Ho + b.band - 1) / b.band) < 6.0 * grid) b.band /= 2;
   const long long nunits = num_units<MODE, MT>(b, C::NSPLIT);
   if (nunits < grid) grid = nunits;
-  static const bool pdl = !(getenv("HS_NO_PDL") && atoi(getenv("HS_NO_PDL")) == 1);
+  constexpr bool pdl = HS_TC_PDL != 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(C::NT);
@@ -984,11 +993,10 @@ bool conv_tc_launch(const float* x, int H, int W, int cin, float* y, int Ho, int
                     int transposed, const float* w, const float* bias, int softplus, const float* addend,
                     long long addend_bstride, int addend_per_model, const int* model_of, const float* residual,
                     const void* const* active, int B, cudaStream_t st, int planar) {
-  static const int dbg = getenv("HS_TC_DBG") ? atoi(getenv("HS_TC_DBG")) : 0;
   TcArgs a{x, H, W, y, Ho, Wo, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual,
-           active, B, 32, dbg, planar};
+           active, B, 32, planar};
   const int mode = transposed ? 2 : (stride == 2 ? 1 : 0);
-  const bool m128 = ((mode == 2 ? W : Wo) % 128) == 0 && !(dbg & 32);
+  const bool m128 = ((mode == 2 ? W : Wo) % 128) == 0 && !(kProbe & 32);
 #define HS_TC(CI, CO, MD, CSL)                                           \
   if (mode == MD && cin == CI && cout == CO) {                           \
     if (m128) launch_tc<CI, CO, MD, 128, CSL>(a, st);                    \

@@ -1,4 +1,4 @@
-// tcgen05 (5th-gen tensor core) implicit-GEMM 3x3 convolution, 3xTF32.
+// tcgen05 (5th-gen tensor core) implicit-GEMM 3x3 convolution, BF16x3 (exact three-way bf16 split, six products, fp32 accumulate).
 #pragma once
 #include <cuda_runtime.h>
 

@@ -413,11 +413,8 @@ void launch_imp2(const ImpArgs& a, int B, cudaStream_t st) {
   k_implicit2<E><<<dim3((unsigned)a.C, (unsigned)B), Imp2<E>::THREADS, sm, st>>>(a);
 }
 
-// the four-step kernel where it applies (square 64^2 / 128^2 padded grids); HS_IMP_V1=1 forces the old one
-bool use_v2(int h, int w) {
-  static const bool off = getenv("HS_IMP_V1") && atoi(getenv("HS_IMP_V1")) == 1;
-  return !off && h == w && (h == 32 || h == 64);
-}
+// the four-step kernel where it applies (square 64^2 / 128^2 padded grids)
+bool use_v2(int h, int w) { return h == w && (h == 32 || h == 64); }
 
 // natural spectrum [C][H2][W2] -> kernel order [C][c][k1'][l]: column c holds
 // frequency f = c/32 + EW br5(c%32), entry (k1', l) row frequency u = k1' + EH br5(l)

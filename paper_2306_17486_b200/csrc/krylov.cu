@@ -243,6 +243,11 @@ __global__ void k_givens(SolveDims d, SolveBuffers s) {
   RhsState& S = s.st[b];
   if (!S.active) return;
   S.fuse = S.reorth;  // predict the next step's re-orthogonalisation from this one
+  if (s.vstatus && s.vstatus[b]) {  // this RHS's coarse solve failed: only it stops (the reference raises per solve)
+    S.status = s.vstatus[b];
+    S.active = 0;
+    return;
+  }
   if (S.nonfinite) {
     S.status = HS_ENONFINITE;
     S.active = 0;

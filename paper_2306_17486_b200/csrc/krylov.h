@@ -58,6 +58,7 @@ struct SolveBuffers {
   float* vin_scale;
   float2** zout;
   int* n_active;      // device scalar
+  const int* vstatus; // (B,) V-cycle status of each RHS (coarse GMRES), or null
 };
 
 size_t krylov_partial_doubles(const SolveDims& d);

@@ -17,10 +17,11 @@ enum Tag {
   VCYCLE = 2,     // one whole V-cycle (work = algorithmic bytes)
   ARNOLDI = 3,    // Gram-Schmidt dot pass (work = algorithmic bytes)
   CNN = 4,        // one whole network forward
-  IMPLICIT = 5,   // implicit layer
+  IMPLICIT = 5,   // implicit layer (work = algorithmic bytes: complex input + output)
   VC_UP0 = 6,     // finest-level up-leg kernel (work = algorithmic bytes)
   TRAIN_WGRAD = 7,  // training weight-gradient reductions (work = flops)
-  NTAGS = 8
+  CONV_WIDE = 8,  // 3x3 convolutions with >= 64 input or output channels, tensor-bound (work = flops)
+  NTAGS = 9
 };
 
 extern std::atomic<long long> launches;

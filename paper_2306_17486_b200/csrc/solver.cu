@@ -73,7 +73,7 @@ __global__ void k_finalize(hs::SolveDims d, hs::SolveBuffers s, int* hist_len, i
   iters[b] = S.iter;
   conv[b] = S.converged;
   int st = S.status;
-  if (st == 0 && vstatus && *vstatus) st = *vstatus;
+  if (st == 0 && vstatus && vstatus[b]) st = vstatus[b];  // this RHS's coarse-grid GMRES failed
   status[b] = st;
 }
 
@@ -109,7 +109,7 @@ SolveLayout layout(const hs::Hierarchy& H, const hs_net_t* net, int B, long long
   L.vin_scale = take((size_t)B * sizeof(float));
   L.zout = take((size_t)B * sizeof(void*));
   L.n_active = take(sizeof(int));
-  L.vstatus = take(sizeof(int));
+  L.vstatus = take((size_t)B * sizeof(int));  // per-RHS V-cycle status (coarse GMRES breakdown / NaN)
   L.vws = take(hs::vcycle_workspace_bytes(H, B));
   L.netws = net ? take(hs::cnn_workspace_bytes(net, B)) : 0;
   L.u0 = net ? take((size_t)B * N * sizeof(float2)) : 0;
@@ -245,7 +245,8 @@ HS_API int hs_fgmres_solve(const hs_hierarchy_t* h, const hs_net_t* net, const h
   void* vws = base + L.vws;
   float2* u0 = net ? reinterpret_cast<float2*>(base + L.u0) : nullptr;
 
-  cudaMemsetAsync(vstatus, 0, sizeof(int), st);
+  cudaMemsetAsync(vstatus, 0, (size_t)a->B * sizeof(int), st);
+  s.vstatus = vstatus;
   hs::vcycle_prepare(H, vws, st);
   if (a->x0) cudaMemcpyAsync(a->x, a->x0, (size_t)a->B * N * sizeof(double2), cudaMemcpyDeviceToDevice, st);
   hs::krylov_init(d, s, a->tol, a->iter_cap, a->x0 != nullptr, st);

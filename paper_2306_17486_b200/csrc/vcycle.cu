@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_gmres(LevelDev L, con
     if (bad) atomicOr(&s_flag, 1);
     block_sum<NACC>(acc, red);
     if (s_flag) {
-      if (threadIdx.x == 0) atomicCAS(status, 0, HS_ENONFINITE);
+      if (threadIdx.x == 0) atomicCAS(status + b, 0, HS_ENONFINITE);
       return;
     }
     const double wn = sqrt(acc[0]);
@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_gmres(LevelDev L, con
     __syncthreads();
     if (s_flag == 2) break;
     if (s_flag == 3) {
-      if (threadIdx.x == 0) atomicCAS(status, 0, HS_EBREAKDOWN);
+      if (threadIdx.x == 0) atomicCAS(status + b, 0, HS_EBREAKDOWN);
       return;
     }
   }
@@ -715,7 +715,7 @@ __global__ void __launch_bounds__(kCoarseThreads, 1)
     HS_COARSE_SWITCH(j + 1, HS_RED)
 #undef HS_RED
     if (s_flag) {
-      if (t == 0) atomicCAS(status, 0, HS_ENONFINITE);
+      if (t == 0) atomicCAS(status + b, 0, HS_ENONFINITE);
       return;
     }
     const double wn = sqrt(acc[0]);
@@ -816,7 +816,7 @@ __global__ void __launch_bounds__(kCoarseThreads, 1)
     __syncthreads();
     if (s_flag == 2) break;
     if (s_flag == 3) {
-      if (t == 0) atomicCAS(status, 0, HS_EBREAKDOWN);
+      if (t == 0) atomicCAS(status + b, 0, HS_EBREAKDOWN);
       return;
     }
   }

@@ -75,3 +75,31 @@ def allreduce_mean(t):
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     t /= w
     return t
+
+
+def report_rows(reports) -> list:
+    """SolveReports as plain (iterations, history, converged) tuples: the per-RHS result the gather carries."""
+    return [(int(r.iterations), [float(v) for v in r.relative_residual_history], bool(r.converged)) for r in reports]
+
+
+def sharded_solve(solve_fn, rhs, model_of):
+    """Solve this rank's contiguous share of a batch and gather every RHS's report in global order.
+
+    ``solve_fn(rhs_shard, model_of_shard) -> (x_shard, reports)`` runs the local batch (the device
+    ``BatchSolver.solve`` in production, the oracle in the CPU tests).  The shards are independent
+    (no exchange step inside a solve), so the only collective is the all-gather of the
+    per-RHS (iterations, history, converged) rows, in rank order, i.e. in the batch's own order.
+
+    Returns ``(rows, x_shard, (start, stop))`` with ``rows`` covering the whole batch on every rank.
+    """
+    rank, world = (0, 1)
+    try:
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            rank, world = dist.get_rank(), dist.get_world_size()
+    except ImportError:  # pragma: no cover
+        pass
+    start, stop = shard_range(len(rhs), world, rank)
+    x, reps = solve_fn(rhs[start:stop], model_of[start:stop])
+    return gather_reports(report_rows(reps)), x, (start, stop)

@@ -17,6 +17,8 @@ import torch
 from . import _lib
 from .device import require_cuda, stream_handle, workspace
 
+MAX_WINDOW = 32  # hs::kMaxRestart (csrc/krylov.h): per-RHS Hessenberg / Givens state lives in RhsState
+
 
 @dataclass
 class BatchResult:
@@ -32,9 +34,12 @@ class BatchResult:
 class Engine:
     """FGMRES over a DeviceHierarchy, optionally with the device network."""
 
-    def __init__(self, dh, net=None):
+    def __init__(self, dh, net=None, net_encodings=None):
         self.dh = dh
         self.net = net
+        # this engine's own per-level encodings (n_models, h_l, w_l, c_l): the DeviceNet is shared per
+        # (net, shape), so another solver may have pointed it at a different model set since
+        self.net_encodings = net_encodings
         self._ws = None
 
     def _workspace(self, nbytes: int) -> torch.Tensor:
@@ -53,7 +58,13 @@ class Engine:
             from .errors import DimensionError
 
             raise DimensionError(f"rhs {(nx, ny)} does not match hierarchy {self.dh.shape}")
-        window = max_iter if restart is None else restart
+        window = max_iter if restart is None else min(restart, max_iter)
+        if window > MAX_WINDOW:
+            from .errors import ConfigurationError
+
+            raise ConfigurationError(
+                f"FGMRES window {window} (restart={restart}, max_iter={max_iter}) exceeds the device solver's "
+                f"{MAX_WINDOW}-vector Hessenberg; pass restart <= {MAX_WINDOW} (BASELINE uses 10/20/30)")
         tol_t = torch.as_tensor(np.broadcast_to(np.asarray(tol, dtype=np.float64), (B,)).copy(), device=dev)
         x = torch.empty_like(b)
         x0c = None if x0 is None else x0.to(device=dev, dtype=torch.complex128).contiguous()
@@ -73,6 +84,8 @@ class Engine:
             caps = torch.as_tensor(np.asarray(iter_caps, dtype=np.int32), device=dev)
             args.iter_cap = caps.data_ptr()
         net_handle = self.net.handle if (use_net and self.net is not None) else None
+        if net_handle is not None and self.net_encodings is not None:
+            self.net.set_encodings(self.net_encodings)
         lib = _lib.load()
         nbytes = int(lib.hs_fgmres_workspace_bytes(ctypes.byref(self.dh.hs), net_handle, B, nx, ny,
                                                    int(window), int(max_iter)))

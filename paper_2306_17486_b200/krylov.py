@@ -236,12 +236,14 @@ class BatchSolver:
         self.hierarchies = list(hierarchies)
         self.dh = DeviceHierarchy(self.hierarchies, true_models=self.models)
         self.net = net
-        net_dev = None
+        net_dev, net_enc = None, None
         if net is not None:
             from .network import device_network
 
-            net_dev = device_network(net, self.models, encodings, self.dh)
-        self.engine = Engine(self.dh, net_dev)
+            # the DeviceNet is shared by every solver on this (net, shape); this solver keeps its own
+            # stacked encodings and the engine re-binds them before each solve
+            net_dev, net_enc = device_network(net, self.models, encodings, self.dh)
+        self.engine = Engine(self.dh, net_dev, net_enc)
 
     def solve(self, rhs, model_of=None, tol: float = 1e-7, max_iter: int = 250, restart: int | None = 10,
               warmup_iters: int = 3, return_device: bool = False, raise_errors: bool = True, iter_caps=None):

@@ -245,7 +245,7 @@ def run_vcycle(dh: DeviceHierarchy, rhs, u0=None, model_of=None):
     u0c = None if u0 is None else u0.to(torch.complex64).contiguous()
     ws_bytes = dh.workspace_bytes(B)
     ws = workspace(ws_bytes)
-    status = torch.zeros(1, dtype=torch.int32, device=rhs.device)
+    status = torch.zeros(B, dtype=torch.int32, device=rhs.device)  # per RHS
     lib = _lib.load()
     _lib.check(
         lib.hs_vcycle(ctypes.byref(dh.hs), rhs.data_ptr(), None if u0c is None else u0c.data_ptr(),
@@ -253,7 +253,8 @@ def run_vcycle(dh: DeviceHierarchy, rhs, u0=None, model_of=None):
                       ws_bytes, status.data_ptr(), stream_handle()),
         "v_cycle",
     )
-    code = int(status.item())
+    codes = status.cpu().numpy()
+    code = int(codes[np.nonzero(codes)[0][0]]) if codes.any() else 0
     if code:
         _lib.check(code, "coarse-grid GMRES")
     return out

@@ -228,4 +228,4 @@ def device_network(net: EncoderSolverNet, models, encodings, dh) -> DeviceNet:
     else:
         dn.set_encodings([torch.cat([e.tensors[lv] for e in encodings], dim=0).contiguous()
                           for lv in range(net.levels)])
-    return dn
+    return dn, list(dn.encodings)

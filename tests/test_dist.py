@@ -21,16 +21,6 @@ def test_shard_range_covers_everything_once():
         hdist.shard_range(4, 2, 2)
 
 
-def test_rank_instances_are_distinct_and_same_shaped():
-    a = problems.make_config("C1", seed_offset=0)
-    b = problems.make_config("C1", seed_offset=1)
-    assert a.rhs.shape == b.rhs.shape and a.shape == b.shape
-    assert not np.array_equal(a.models[0].kappa_sq, b.models[0].kappa_sq)
-    # seed offset 0 reproduces the fixtures' inputs
-    c = problems.make_config("C1")
-    assert np.array_equal(a.models[0].kappa_sq, c.models[0].kappa_sq)
-
-
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -39,25 +29,50 @@ def _free_port():
     return port
 
 
+def _oracle_problem():
+    """A small two-model batch of 5 RHS at 33^2 (the oracle stands in for the device solver on CPU)."""
+    from oracle import helm_oracle as ho
+
+    rng = np.random.default_rng(7)
+    models = [ho.make_model(problems.smooth_random_kappa_sq((33, 33), 3.0, s), layer_width=4) for s in (1, 2)]
+    rhs = rng.standard_normal((5, 33, 33)) + 1j * rng.standard_normal((5, 33, 33))
+    owner = np.array([0, 1, 1, 0, 1])
+    return models, rhs, owner
+
+
+def _oracle_solve_fn(models):
+    from oracle import helm_oracle as ho
+    from paper_2306_17486_b200.krylov import SolveReport
+
+    def solve(rhs, owner):
+        xs, reps = [], []
+        for b, o in zip(rhs, owner):
+            x, r = ho.solve_vcycle(models[int(o)], b, None, 1e-6, 200, 10)
+            xs.append(x)
+            reps.append(SolveReport(r.iterations, list(r.history), r.converged))
+        return np.array(xs), reps
+
+    return solve
+
+
 def _worker(rank, world, port, q):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        # each rank owns an independent instance and a shard of its RHS (no data-path collective)
-        cfg = problems.make_config("C1", seed_offset=rank)
-        lo, hi = hdist.shard_range(cfg.rhs.shape[0], world, rank)
-        local = [(rank, i, float(np.abs(cfg.rhs[i]).sum())) for i in range(lo, hi)]
+        # the bench's exact shard-and-gather path: this rank solves its share of ONE batch, the per-RHS
+        # reports are all-gathered in batch order; the max-over-ranks timing reduction
+        models, rhs, owner = _oracle_problem()
+        rows, x, (lo, hi) = hdist.sharded_solve(_oracle_solve_fn(models), rhs, owner)
         t = hdist.reduce_scalar(1.5 + rank, "max")
-        s = hdist.reduce_scalar(len(local), "sum")
-        allr = hdist.gather_reports(local)
-        q.put((rank, t, s, allr))
+        s = hdist.reduce_scalar(hi - lo, "sum")
+        q.put((rank, t, s, rows, (lo, hi), x))
     finally:
         dist.destroy_process_group()
 
 
-def test_gloo_world_size_two():
+def test_gloo_sharded_solve_equals_one_rank():
     import multiprocessing as mp
 
     ctx = mp.get_context("spawn")
@@ -66,15 +81,20 @@ def test_gloo_world_size_two():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=120) for _ in procs]
+    res = sorted([q.get(timeout=300) for _ in procs], key=lambda r: r[0])
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, t, s, allr in res:
+    models, rhs, owner = _oracle_problem()
+    rows1, x1, span1 = hdist.sharded_solve(_oracle_solve_fn(models), rhs, owner)  # no process group: one rank
+    assert span1 == (0, 5)
+    for rank, t, s, rows, (lo, hi), x in res:
         assert t == 2.5  # max over ranks
-        assert s == 4  # C1 has 4 RHS: 2 per rank
-        assert [r for r, _, _ in allr] == [0, 0, 1, 1]
-    assert res[0][3] == res[1][3]
+        assert s == 5  # every RHS solved exactly once
+        assert (lo, hi) == hdist.shard_range(5, 2, rank)
+        assert rows == rows1  # gathered reports == the one-rank run, in batch order
+        assert np.array_equal(x, x1[lo:hi])
+    assert [r[4] for r in res] == [(0, 3), (3, 5)]
 
 
 def _train_worker(rank, world, port, q):

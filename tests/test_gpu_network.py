@@ -80,7 +80,7 @@ def test_tconv_shapes(rng, cin, cout, hw):
                                                (64, 64, 0, (3, 192)), (32, 64, 1, (5, 128)), (16, 32, 1, (4, 128)),
                                                (64, 32, 2, (3, 64)), (32, 16, 2, (2, 64))])
 def test_tcgen05_conv_matches_oracle(rng, cin, cout, mode, hw):
-    """The tcgen05 3xTF32 path (taken for widths that are multiples of 128) against the fp32 oracle."""
+    """The tcgen05 BF16x3 path (widths that are multiples of 64) against the fp32 oracle."""
     from paper_2306_17486_b200 import _lib
 
     x = rng.standard_normal((3, cin, *hw)).astype(np.float32)
