@@ -355,16 +355,21 @@ def solve_vcycle(model: Model, b, hier=None, tol=1e-7, max_iter=250, restart=10)
 
 
 def solve_learned(model: Model, b, net_apply, tol=1e-7, max_iter=250, restart=10,
-                  warmup_iters=3, hier=None):
-    """krylov.py:180-246: V-cycle warm-up, then M(r) = v_cycle(r, u0 = net(r))."""
+                  warmup_iters=3, hier=None, round_z=None):
+    """krylov.py:180-246: V-cycle warm-up, then M(r) = v_cycle(r, u0 = net(r)).
+
+    ``round_z`` (precision-envelope experiments only, oracle/precision_envelope.py) post-processes
+    every preconditioner output z, e.g. rounding it to complex64 storage.
+    """
     hier = hier or build_hierarchy(model)
     A = lambda u: helmholtz(u, model)  # noqa: E731
-    x1, r1 = fgmres(A, lambda r: v_cycle(r, None, hier), b, None, tol,
+    rz = round_z or (lambda z: z)
+    x1, r1 = fgmres(A, lambda r: rz(v_cycle(r, None, hier)), b, None, tol,
                     min(warmup_iters, max_iter), restart)
     if r1.converged or r1.iterations >= max_iter:
         return x1, r1
     rel1 = np.linalg.norm(b - A(x1)) / np.linalg.norm(b)
-    x2, r2 = fgmres(A, lambda r: v_cycle(r, net_apply(r), hier), b, x1, tol / rel1,
+    x2, r2 = fgmres(A, lambda r: rz(v_cycle(r, net_apply(r), hier)), b, x1, tol / rel1,
                     max_iter - r1.iterations, restart)
     return x2, Report(r1.iterations + r2.iterations,
                       r1.history + [e * rel1 for e in r2.history[1:]], r2.converged)

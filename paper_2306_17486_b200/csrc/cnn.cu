@@ -848,6 +848,10 @@ int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* 
     if (c.cin == 16 && c.cout == 2) return launch_thin<16, 2>(a, B, st), HS_OK;
     if (c.cin == 8 && c.cout == 2) return launch_thin<8, 2>(a, B, st), HS_OK;
   }
+  if (conv_wide_launch(a.x, a.H, a.W, a.cin, a.y, a.Ho, a.Wo, a.cout, c.stride, c.transposed, a.w, a.bias,
+                       a.softplus, a.addend, a.addend_bstride, a.addend_per_model, a.model_of, a.residual, a.active, B,
+                       st, planar_out ? 1 : 0))
+    return HS_OK;
   if (conv_tc_supported(c.cin, c.cout, c.stride, c.transposed, H, W, a.Wo) &&
       conv_tc_launch(a.x, a.H, a.W, a.cin, a.y, a.Ho, a.Wo, a.cout, c.stride, c.transposed, a.w, a.bias, a.softplus,
                      a.addend, a.addend_bstride, a.addend_per_model, a.model_of, a.residual, a.active, B, st,
@@ -1126,7 +1130,8 @@ static int implicit_apply_dev(const hs_net_t* net, const float* x_nhwc, float* y
 static bool coarse_planar(const hs_net_t* net, int h, int w) {
   const hs_conv_t& c = net->d.sol_res_b[net->d.levels - 1];
   return net->spec_perm != nullptr && !c.transposed && c.stride == 1 &&
-         conv_tc_supported(c.cin, c.cout, c.stride, c.transposed, h, w, w);
+         (conv_wide_supported(c.cin, c.cout, c.stride, c.transposed, h, w, w) ||
+          conv_tc_supported(c.cin, c.cout, c.stride, c.transposed, h, w, w));
 }
 
 static int solver_forward(const hs_net_t* net, const float* in, float* head, const ThinIO* io, char* ws,

@@ -9,6 +9,14 @@ bool conv_tc_launch(const float* x, int H, int W, int cin, float* y, int Ho, int
                     int transposed, const float* w, const float* bias, int softplus, const float* addend,
                     long long addend_bstride, int addend_per_model, const int* model_of, const float* residual,
                     const void* const* active, int B, cudaStream_t st, int planar = 0);
+// K-streamed tcgen05 kernel for the >= 64-channel layers (conv_wide.cu): 64->64 / 128->128 stride 1,
+// 64->128 / 128->128 stride 2, 128->64 transposed, widths (transposed: input widths) that are
+// multiples of 128.  Same arguments and epilogue as conv_tc_launch.
+bool conv_wide_supported(int cin, int cout, int stride, int transposed, int H, int W, int Wo);
+bool conv_wide_launch(const float* x, int H, int W, int cin, float* y, int Ho, int Wo, int cout, int stride,
+                      int transposed, const float* w, const float* bias, int softplus, const float* addend,
+                      long long addend_bstride, int addend_per_model, const int* model_of, const float* residual,
+                      const void* const* active, int B, cudaStream_t st, int planar);
 // planar != 0: the output is stored complex-planar, channel pair (2c, 2c+1) of pixel p at
 // float2 index (b * cout/2 + c) * Ho * Wo + p (the implicit layer's coalesced input)
 }  // namespace hs

@@ -1,0 +1,500 @@
+// tcgen05 implicit-GEMM 3x3 convolution for the wide (>= 64-channel) layers, K-streamed.
+//
+// Serves the reference conv2d / conv_transpose2d (autodiff.py:472-541, _corr :407-421, _corr_t
+// :442-469) with batch norm folded (autodiff.py:595-607), softplus (:243-252) and the skip /
+// encoder / residual adds of the ARCH.md network, at the channel counts whose bf16x3 weights do
+// not fit in shared memory (9 x 128 x 128 x 3 parts x 2 B = 884 KB for a 128 -> 128 layer):
+// 64 -> 64 and 128 -> 128 (stride 1), 64 -> 128 and 128 -> 128 (stride 2), 128 -> 64 (transposed).
+//
+// GEMM view.  One tile = M = 128 output pixels of one row (transposed: 128 input columns, two
+// accumulators for the even / odd output columns) x N = cout, K = 9 taps x cin.  A pass covers R
+// tiles (consecutive output rows of one 128-column block of one RHS) and streams K in chunks of
+// 16 input channels:
+//   for chunk c:  for tap row ky:  for tap kx:  B piece (c, ky, kx) = 16 x cout weights x 3 parts
+//                                               for every tile using the tap: 3 (G = 3) or 5 MMAs
+// Precision (BF16x3, x = x0 + x1 + x2 exactly; the dropped products are below 2^-16).
+// The weight parts are stacked along N in every B piece ([W0 | W1 | W2], 3 cout rows per K plane),
+// and each tile keeps G fp32 TMEM column groups so that the leading products a0 w0 are the ONLY
+// terms of group 0: the tensor core's accumulation adds one rounding per K step to the large
+// partial sums, exactly like a plain fp32 dot product, and every correction term goes to a group
+// 2^8 smaller (measured: putting all six products in one accumulator made these layers 10x less
+// accurate than fp32 SIMT).  The epilogue sums g0 + (g1 [+ g2]).
+//   G = 3 (cout 64):  A0 x [W0 W1 W2] -> g0 g1 g2;  A1 x [W0 W1] -> g1 g2;  A2 x W0 -> g2
+//   G = 2 (cout 128, transposed): A0 x [W0 W1] -> g0 g1;  A0 x W2, A1 x W0, A1 x W1, A2 x W0 -> g1
+// (one UMMA has N <= 256, hence two groups for cout 128).
+//
+// Warp roles (one persistent CTA per SM):
+//   warps 0-7    epilogue: tcgen05.ld of lane quarter (warp % 4) x column half (warp / 4), bias,
+//                softplus, encoder / skip addend, residual, NHWC (or complex-planar) stores
+//   warps 8-11   A converters: input row chunks (RW pixels x 16 channels, fp32, L2-prefetched)
+//                -> exact bf16x3 split -> A ring (UMMA K-major interleaved layout, 16 B pixel pitch,
+//                so the A operand of tap kx is the staged row with its start address moved by kx)
+//   warps 12-15  B converters: weight pieces (cout x 16 channels of one tap) -> bf16x3 -> B ring
+//   warp 16      MMA issuer (one elected lane issues tcgen05.mma; commits release ring slots and
+//                hand the accumulators to the epilogue)
+// The weights are read as fp32 from L2 and split on the fly (4 B per weight instead of 6 B for a
+// pre-split copy); every activation element is read from HBM once (the first channel chunk of a
+// pass pulls the pass's input rows into L2 with bulk prefetches, the other chunks hit L2).
+#include <cuda_bf16.h>
+
+#include <cstdio>
+
+#include "common.cuh"
+#include "conv_tc.h"
+#include "prof.h"
+#include "tc_util.cuh"
+
+namespace hs {
+namespace {
+using namespace tc;
+
+constexpr int kWEpi = 8, kWAcv = 4, kWBcv = 4;
+constexpr int kWarpA0 = kWEpi, kWarpB0 = kWEpi + kWAcv, kWarpMma = kWEpi + kWAcv + kWBcv;
+constexpr int kWThreads = 32 * (kWarpMma + 1);
+constexpr size_t kWSmemMax = 232448;
+
+template <int CIN, int COUT, int MODE>
+struct WCfg {
+  static constexpr int MT = 128;                     // tile pixels (UMMA M)
+  static constexpr int NACC = MODE == 2 ? 2 : 1;     // accumulators per tile (transposed: column parity)
+  static constexpr int G = COUT <= 64 && NACC == 1 ? 3 : 2;  // column groups per accumulator (see above)
+  static constexpr int ACC_COLS = G * COUT;
+  // output rows (tiles) per pass: as many as TMEM holds, 4 at most (transposed: an even number)
+  static constexpr int R = NACC * ACC_COLS * 4 <= 512 ? 4 : 2;
+  static constexpr int SET_COLS = R * NACC * ACC_COLS;  // TMEM columns of one pass
+  static constexpr int NSETS = 2 * SET_COLS <= 512 ? 2 : 1;  // double-buffered when it fits
+  static constexpr int NCH = CIN / 16;               // K chunks
+  static constexpr int RW = MODE == 0 ? MT + 2 : (MODE == 1 ? 2 * MT + 1 : MT + 1);  // staged pixels per row
+  static constexpr int NROWS = MODE == 0 ? R + 2 : (MODE == 1 ? 2 * R + 1 : R / 2 + 1);  // input rows per pass
+  static constexpr uint32_t A_PLANE = (uint32_t)RW * 16;   // one (part, 8-channel half) plane
+  static constexpr uint32_t A_SLOT = 6 * A_PLANE;          // 3 parts x 2 halves
+  static constexpr uint32_t B_PLANE = (uint32_t)3 * COUT * 16;  // one 8-channel half: rows [W0 | W1 | W2]
+  static constexpr uint32_t B_SLOT = 2 * B_PLANE;
+  static constexpr int NBS = 6;                            // B ring slots
+  static constexpr size_t FIXED = (size_t)NBS * B_SLOT + 1024 + 4 * COUT;  // + barriers, bias
+  static constexpr int pick_nas() {
+    for (int n = NROWS + 4; n > NROWS; --n)
+      if (FIXED + (size_t)n * A_SLOT <= kWSmemMax) return n;
+    return NROWS;
+  }
+  static constexpr int NAS = pick_nas();                   // A ring slots (>= rows of one chunk)
+  static constexpr size_t TOTAL = FIXED + (size_t)NAS * A_SLOT;
+  static constexpr int NCOLS = NSETS * SET_COLS <= 128 ? 128 : (NSETS * SET_COLS <= 256 ? 256 : 512);
+  static_assert(NSETS * SET_COLS <= 512, "TMEM");
+  static_assert(TOTAL <= kWSmemMax, "shared memory");
+  static_assert(CIN % 16 == 0 && COUT % 32 == 0 && COUT <= 256, "shapes");
+};
+
+struct WArgs {
+  const float* x;
+  int H, W;
+  float* y;
+  int Ho, Wo;
+  const float* w;  // [cout][ky][kx][cin] (transposed layers in the same order, see cnn.h)
+  const float* bias;
+  int softplus;
+  const float* addend;
+  long long addend_bstride;
+  int addend_per_model;
+  const int* model_of;
+  const float* residual;
+  const void* const* active;
+  int B;
+  int planar;
+};
+
+struct Pass {
+  int b, xb, oy0;
+};
+
+template <int MODE, typename C>
+__host__ __device__ inline long long num_passes(const WArgs& a) {
+  const int xblocks = (MODE == 2 ? a.W : a.Wo) / C::MT;
+  return (long long)a.B * xblocks * ((a.Ho + C::R - 1) / C::R);
+}
+
+// pass u -> (b, column block, first output row); RHS slowest so neighbouring CTAs share input rows in L2
+template <int MODE, typename C>
+HS_DEV bool pass_at(const WArgs& a, long long u, Pass& P) {
+  const int xblocks = (MODE == 2 ? a.W : a.Wo) / C::MT;
+  const int bands = (a.Ho + C::R - 1) / C::R;
+  P.xb = (int)(u % xblocks);
+  P.oy0 = (int)((u / xblocks) % bands) * C::R;
+  P.b = (int)(u / ((long long)xblocks * bands));
+  return !(a.active && a.active[P.b] == nullptr);
+}
+
+// first input row of the pass and first input column of the staged segment
+template <int MODE>
+HS_DEV int first_row(int oy0) { return MODE == 0 ? oy0 - 1 : (MODE == 1 ? 2 * oy0 - 1 : oy0 >> 1); }
+template <int MODE>
+HS_DEV int first_col(int xb) { return MODE == 0 ? 128 * xb - 1 : (MODE == 1 ? 256 * xb - 1 : 128 * xb); }
+// raw pixel p of the segment -> staged pixel (stride 2 de-interleaves: even columns, then odd)
+template <int MODE>
+HS_DEV int staged(int p) {
+  if (MODE != 1) return p;
+  return (p & 1) ? (p - 1) >> 1 : 128 + (p >> 1);
+}
+
+// Tap usage.  For output row r of the pass (0..R-1) and tap (ky, kx): the input row (relative to
+// first_row), the staged start pixel of the A window and the accumulator parity, or -1 if unused.
+template <int MODE>
+HS_DEV int tap_row(int r, int ky) {
+  if (MODE == 0) return r + ky;
+  if (MODE == 1) return 2 * r + ky;
+  // transposed: out row 2q <- (ky 1, in row q); out row 2q+1 <- (ky 0, row q+1), (ky 2, row q)
+  if ((r & 1) == 0) return ky == 1 ? (r >> 1) : -1;
+  return ky == 0 ? (r >> 1) + 1 : (ky == 2 ? (r >> 1) : -1);
+}
+template <int MODE>
+HS_DEV int tap_px(int kx) {
+  if (MODE == 0) return kx;
+  if (MODE == 1) return kx == 0 ? 128 : (kx == 1 ? 0 : 129);
+  // transposed: out col 2q (acc 0) <- (kx 1, in col q); out col 2q+1 (acc 1) <- (kx 0, q+1), (kx 2, q)
+  return kx == 0 ? 1 : 0;
+}
+template <int MODE>
+HS_DEV int tap_acc(int kx) { return MODE == 2 ? (kx == 1 ? 0 : 1) : 0; }
+// the last tap row that reads input row i of a pass (its A slot is released after it)
+template <int MODE, int R>
+HS_DEV int last_ky(int i) {
+  int m = -1;
+  for (int r = 0; r < R; ++r)
+    for (int ky = 0; ky < 3; ++ky)
+      if (tap_row<MODE>(r, ky) == i) m = ky > m ? ky : m;
+  return m;
+}
+
+template <int CIN, int COUT, int MODE>
+__global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(WArgs a) {
+  using C = WCfg<CIN, COUT, MODE>;
+  constexpr int R = C::R, NCH = C::NCH, NAS = C::NAS, NBS = C::NBS, NROWS = C::NROWS;
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* bring = smem;
+  unsigned char* aring = smem + (size_t)NBS * C::B_SLOT;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(aring + (size_t)NAS * C::A_SLOT);
+  uint64_t* a_full = bars;
+  uint64_t* a_empty = a_full + NAS;
+  uint64_t* b_full = a_empty + NAS;
+  uint64_t* b_empty = b_full + NBS;
+  uint64_t* acc_full = b_empty + NBS;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  float* s_bias = reinterpret_cast<float*>(smem + (size_t)NBS * C::B_SLOT + (size_t)NAS * C::A_SLOT + 512);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long npass = num_passes<MODE, C>(a);
+
+  for (int n = tid; n < COUT; n += kWThreads) s_bias[n] = a.bias[n];
+  if (tid == 0) {
+    for (int i = 0; i < NAS; ++i) {
+      mbar_init(smem_u32(&a_full[i]), kWAcv);
+      mbar_init(smem_u32(&a_empty[i]), 1);
+    }
+    for (int i = 0; i < NBS; ++i) {
+      mbar_init(smem_u32(&b_full[i]), kWBcv);
+      mbar_init(smem_u32(&b_empty[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&acc_full[i]), 1);
+      mbar_init(smem_u32(&acc_empty[i]), kWEpi);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
+                 "r"(C::NCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *s_tmem;
+  // programmatic dependent launch: set-up above overlaps the previous kernel's tail (persistent grid)
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  if (warp >= kWarpA0 && warp < kWarpA0 + kWAcv) {
+    // ================= A converters: input row chunks -> bf16x3 A ring
+    const int t = tid - 32 * kWarpA0;
+    constexpr int NT = 32 * kWAcv;
+    uint32_t seq = 0;
+    for (long long u = blockIdx.x; u < npass; u += gridDim.x) {
+      Pass P;
+      if (!pass_at<MODE, C>(a, u, P)) continue;
+      const int g0 = first_row<MODE>(P.oy0), x0 = first_col<MODE>(P.xb);
+      const float* img = a.x + (size_t)P.b * a.H * a.W * CIN;
+      const int clo = max(x0, 0), chi = min(x0 + C::RW, a.W);
+      if (t == 0) {
+        // pull this pass's input rows (all channels) into L2: the later channel chunks hit L2
+        for (int i = 0; i < NROWS; ++i) {
+          const int g = g0 + i;
+          if (g >= 0 && g < a.H && chi > clo)
+            prefetch_l2(img + ((size_t)g * a.W + clo) * CIN, (uint32_t)(chi - clo) * CIN * 4);
+        }
+      }
+      for (int c = 0; c < NCH; ++c) {
+        for (int i = 0; i < NROWS; ++i, ++seq) {
+          const uint32_t s = seq % NAS, use = seq / NAS;
+          if (use > 0) mbar_wait(smem_u32(&a_empty[s]), (use - 1) & 1);
+          unsigned char* slot = aring + (size_t)s * C::A_SLOT;
+          const int g = g0 + i;
+          const bool row_ok = g >= 0 && g < a.H;
+          const float* src = img + (size_t)(row_ok ? g : 0) * a.W * CIN + 16 * c;
+          for (int e = t; e < 2 * C::RW; e += NT) {
+            const int p = e % C::RW, h = e / C::RW;  // pixel fastest: conflict-free 16-byte stores
+            const int col = x0 + p;
+            float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            if (row_ok && col >= 0 && col < a.W) {
+              const float4* s4 = reinterpret_cast<const float4*>(src + (size_t)col * CIN + 8 * h);
+              const float4 v0 = __ldg(s4), v1 = __ldg(s4 + 1);
+              v[0] = v0.x, v[1] = v0.y, v[2] = v0.z, v[3] = v0.w, v[4] = v1.x, v[5] = v1.y, v[6] = v1.z, v[7] = v1.w;
+            }
+            uint4 q0, q1, q2;
+            split_bf16x3(v, q0, q1, q2);
+            const size_t off = (size_t)h * C::A_PLANE + (size_t)staged<MODE>(p) * 16;
+            *reinterpret_cast<uint4*>(slot + off) = q0;
+            *reinterpret_cast<uint4*>(slot + 2 * C::A_PLANE + off) = q1;
+            *reinterpret_cast<uint4*>(slot + 4 * C::A_PLANE + off) = q2;
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&a_full[s]));
+        }
+      }
+    }
+  } else if (warp >= kWarpB0 && warp < kWarpB0 + kWBcv) {
+    // ================= B converters: weight pieces (c, ky, kx) -> bf16x3 B ring, in MMA order
+    const int t = tid - 32 * kWarpB0;
+    constexpr int NT = 32 * kWBcv;
+    uint32_t seq = 0;
+    for (long long u = blockIdx.x; u < npass; u += gridDim.x) {
+      Pass P;
+      if (!pass_at<MODE, C>(a, u, P)) continue;
+      for (int c = 0; c < NCH; ++c)
+        for (int tap = 0; tap < 9; ++tap, ++seq) {
+          const uint32_t s = seq % NBS, use = seq / NBS;
+          if (use > 0) mbar_wait(smem_u32(&b_empty[s]), (use - 1) & 1);
+          unsigned char* slot = bring + (size_t)s * C::B_SLOT;
+          for (int e = t; e < 2 * COUT; e += NT) {
+            const int n = e % COUT, h = e / COUT;
+            const float4* s4 = reinterpret_cast<const float4*>(a.w + ((size_t)n * 9 + tap) * CIN + 16 * c + 8 * h);
+            const float4 v0 = __ldg(s4), v1 = __ldg(s4 + 1);
+            const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+            uint4 q0, q1, q2;
+            split_bf16x3(v, q0, q1, q2);
+            const size_t off = (size_t)h * C::B_PLANE + (size_t)n * 16;  // part p at row p * cout + n
+            *reinterpret_cast<uint4*>(slot + off) = q0;
+            *reinterpret_cast<uint4*>(slot + off + (size_t)COUT * 16) = q1;
+            *reinterpret_cast<uint4*>(slot + off + (size_t)2 * COUT * 16) = q2;
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&b_full[s]));
+        }
+    }
+  } else if (warp == kWarpMma) {
+    // ================= MMA issuer
+    constexpr uint32_t I1 = idesc_bf16(128, COUT), I2 = idesc_bf16(128, 2 * COUT), I3 = idesc_bf16(128, 3 * COUT);
+    constexpr uint32_t WROW = (uint32_t)COUT * 16;  // byte offset of weight part p: p * WROW
+    const uint32_t a_base = smem_u32(aring), b_base = smem_u32(bring);
+    uint32_t aseq = 0, bseq = 0, pass = 0;
+    for (long long u = blockIdx.x; u < npass; u += gridDim.x) {
+      Pass P;
+      if (!pass_at<MODE, C>(a, u, P)) continue;
+      const uint32_t set = pass % C::NSETS, suse = pass / C::NSETS;
+      if (suse > 0) mbar_wait(smem_u32(&acc_empty[set]), (suse - 1) & 1);
+      tc_fence_after();
+      const uint32_t dset = tmem + set * C::SET_COLS;
+      uint32_t started = 0;  // bit (r * NACC + k): accumulator written
+      for (int c = 0; c < NCH; ++c) {
+        int have = -1;  // highest input row of this chunk known to be staged
+        for (int ky = 0; ky < 3; ++ky) {
+          for (int kx = 0; kx < 3; ++kx, ++bseq) {
+            const uint32_t bs = bseq % NBS;
+            mbar_wait(smem_u32(&b_full[bs]), (bseq / NBS) & 1);
+            const uint32_t bsl = b_base + bs * C::B_SLOT;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              const int i = tap_row<MODE>(r, ky);
+              if (i < 0) continue;
+              for (; have < i; ++have) {
+                const uint32_t sq = aseq + (uint32_t)(have + 1);
+                mbar_wait(smem_u32(&a_full[sq % NAS]), (sq / NAS) & 1);
+              }
+              tc_fence_after();
+              const uint32_t asl = a_base + ((aseq + (uint32_t)i) % NAS) * C::A_SLOT + (uint32_t)tap_px<MODE>(kx) * 16;
+              const int k = tap_acc<MODE>(kx);
+              const uint32_t bit = 1u << (r * C::NACC + k);
+              const uint32_t d = dset + (uint32_t)((r * C::NACC + k) * C::ACC_COLS);
+              const uint32_t a0 = desc_lo(asl, C::A_PLANE), a1 = desc_lo(asl + 2 * C::A_PLANE, C::A_PLANE),
+                             a2 = desc_lo(asl + 4 * C::A_PLANE, C::A_PLANE);
+              const uint32_t w0 = desc_lo(bsl, C::B_PLANE), w1 = desc_lo(bsl + WROW, C::B_PLANE),
+                             w2 = desc_lo(bsl + 2 * WROW, C::B_PLANE);
+              if constexpr (C::G == 3) {
+                mma_bf16(d, a0, kDescHi, w0, kDescHi, I3, (started & bit) ? 1u : 0u);  // g0 g1 g2 += a0 [w0 w1 w2]
+                mma_bf16(d + COUT, a1, kDescHi, w0, kDescHi, I2, 1u);                  // g1 g2 += a1 [w0 w1]
+                mma_bf16(d + 2 * COUT, a2, kDescHi, w0, kDescHi, I1, 1u);              // g2 += a2 w0
+              } else {
+                mma_bf16(d, a0, kDescHi, w0, kDescHi, I2, (started & bit) ? 1u : 0u);  // g0 g1 += a0 [w0 w1]
+                mma_bf16(d + COUT, a0, kDescHi, w2, kDescHi, I1, 1u);                  // g1 += a0 w2
+                mma_bf16(d + COUT, a1, kDescHi, w0, kDescHi, I1, 1u);                  // g1 += a1 w0
+                mma_bf16(d + COUT, a1, kDescHi, w1, kDescHi, I1, 1u);                  // g1 += a1 w1
+                mma_bf16(d + COUT, a2, kDescHi, w0, kDescHi, I1, 1u);                  // g1 += a2 w0
+              }
+              started |= bit;
+            }
+            mma_commit(smem_u32(&b_empty[bs]));  // the piece is free once these MMAs completed
+          }
+          // input rows whose last reader was this tap row go back to the converters
+          for (int i = 0; i < NROWS; ++i)
+            if (last_ky<MODE, R>(i) == ky) {
+              for (; have < i; ++have) {  // (a row no tap reads yet must still be seen staged first)
+                const uint32_t sq = aseq + (uint32_t)(have + 1);
+                mbar_wait(smem_u32(&a_full[sq % NAS]), (sq / NAS) & 1);
+              }
+              mma_commit(smem_u32(&a_empty[(aseq + (uint32_t)i) % NAS]));
+            }
+        }
+        aseq += NROWS;
+      }
+      mma_commit(smem_u32(&acc_full[set]));
+      ++pass;
+    }
+  } else if (warp < kWEpi) {
+    // ================= epilogue: lane quarter q (tile pixel m = 32 q + lane), column half hc
+    constexpr int EH = COUT / 2;
+    const int q4 = warp & 3, hc = warp >> 2;
+    const int m = 32 * q4 + lane;
+    uint32_t pass = 0;
+    for (long long u = blockIdx.x; u < npass; u += gridDim.x) {
+      Pass P;
+      if (!pass_at<MODE, C>(a, u, P)) continue;
+      const uint32_t set = pass % C::NSETS;
+      mbar_wait(smem_u32(&acc_full[set]), (pass / C::NSETS) & 1);
+      tc_fence_after();
+      const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[P.b] : 0) : P.b) *
+                                                   a.addend_bstride
+                                  : nullptr;
+      for (int r = 0; r < R; ++r) {
+        const int oy = P.oy0 + r;
+#pragma unroll
+        for (int k = 0; k < C::NACC; ++k) {
+          const int ox = MODE == 2 ? 2 * (128 * P.xb + m) + k : 128 * P.xb + m;
+          const size_t pix = (size_t)oy * a.Wo + ox;
+          const size_t obase = ((size_t)P.b * a.Ho * a.Wo + pix) * COUT + hc * EH;
+          const bool ok = oy < a.Ho;
+#pragma unroll
+          for (int n0 = 0; n0 < EH; n0 += 8) {
+            uint32_t v[8], v1[8], v2[8];
+            const uint32_t col = tmem + ((uint32_t)(32 * q4) << 16) + set * C::SET_COLS +
+                                 (uint32_t)((r * C::NACC + k) * C::ACC_COLS) + hc * EH + n0;
+            tmem_ld8(col, v);
+            tmem_ld8(col + COUT, v1);
+            if constexpr (C::G == 3) tmem_ld8(col + 2 * COUT, v2);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {  // g0 + (g1 [+ g2]): the corrections are summed first
+              const float corr = C::G == 3 ? __uint_as_float(v1[j]) + __uint_as_float(v2[j]) : __uint_as_float(v1[j]);
+              v[j] = __float_as_uint(__uint_as_float(v[j]) + corr);
+            }
+            if (!ok) continue;
+            float o[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              o[j] = __uint_as_float(v[j]) + s_bias[hc * EH + n0 + j];
+              if (a.softplus) o[j] = softplus_fast(o[j]);
+            }
+            if (add) {
+              const float4* ap = reinterpret_cast<const float4*>(add + pix * COUT + hc * EH + n0);
+              const float4 a0 = __ldg(ap), a1 = __ldg(ap + 1);
+              o[0] += a0.x, o[1] += a0.y, o[2] += a0.z, o[3] += a0.w, o[4] += a1.x, o[5] += a1.y, o[6] += a1.z,
+                  o[7] += a1.w;
+            }
+            if (a.residual) {
+              const float4* rp = reinterpret_cast<const float4*>(a.residual + obase + n0);
+              const float4 r0 = __ldg(rp), r1 = __ldg(rp + 1);
+              o[0] += r0.x, o[1] += r0.y, o[2] += r0.z, o[3] += r0.w, o[4] += r1.x, o[5] += r1.y, o[6] += r1.z,
+                  o[7] += r1.w;
+            }
+            if (a.planar) {  // channel pairs (2c, 2c+1) -> complex plane c (the implicit layer's input)
+              float2* yp = reinterpret_cast<float2*>(a.y) +
+                           ((size_t)P.b * (COUT / 2) + (hc * EH + n0) / 2) * ((size_t)a.Ho * a.Wo) + pix;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) yp[(size_t)j * a.Ho * a.Wo] = make_float2(o[2 * j], o[2 * j + 1]);
+            } else {
+              float4* yp = reinterpret_cast<float4*>(a.y + obase + n0);
+              yp[0] = make_float4(o[0], o[1], o[2], o[3]);
+              yp[1] = make_float4(o[4], o[5], o[6], o[7]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&acc_empty[set]));
+      ++pass;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::NCOLS));
+  }
+}
+
+template <int CIN, int COUT, int MODE>
+void launch_wide(const WArgs& a, cudaStream_t st) {
+  using C = WCfg<CIN, COUT, MODE>;
+  static int sms = 0;
+  if (!sms) {
+    cudaFuncSetAttribute(k_conv_wide<CIN, COUT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::TOTAL);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  long long grid = sms;
+  const long long np = num_passes<MODE, C>(a);
+  if (np < grid) grid = np;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kWThreads);
+  cfg.dynamicSmemBytes = C::TOTAL;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_conv_wide<CIN, COUT, MODE>, a);
+}
+
+}  // namespace
+
+bool conv_wide_supported(int cin, int cout, int stride, int transposed, int H, int W, int Wo) {
+  (void)H;
+  if (!conv_tc_enabled) return false;
+  const int mode = transposed ? 2 : (stride == 2 ? 1 : 0);
+  if ((mode == 2 ? W : Wo) % 128) return false;
+  return (mode == 0 && ((cin == 64 && cout == 64) || (cin == 128 && cout == 128))) ||
+         (mode == 1 && ((cin == 64 && cout == 128) || (cin == 128 && cout == 128))) ||
+         (mode == 2 && cin == 128 && cout == 64);
+}
+
+bool conv_wide_launch(const float* x, int H, int W, int cin, float* y, int Ho, int Wo, int cout, int stride,
+                      int transposed, const float* w, const float* bias, int softplus, const float* addend,
+                      long long addend_bstride, int addend_per_model, const int* model_of, const float* residual,
+                      const void* const* active, int B, cudaStream_t st, int planar) {
+  if (!conv_wide_supported(cin, cout, stride, transposed, H, W, Wo)) return false;
+  WArgs a{x, H, W, y, Ho, Wo, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual,
+          active, B, planar};
+  const int mode = transposed ? 2 : (stride == 2 ? 1 : 0);
+  if (mode == 0 && cin == 64) return launch_wide<64, 64, 0>(a, st), true;
+  if (mode == 0 && cin == 128) return launch_wide<128, 128, 0>(a, st), true;
+  if (mode == 1 && cin == 64) return launch_wide<64, 128, 1>(a, st), true;
+  if (mode == 1 && cin == 128) return launch_wide<128, 128, 1>(a, st), true;
+  if (mode == 2 && cout == 64) return launch_wide<128, 64, 2>(a, st), true;
+  return false;
+}
+
+}  // namespace hs
