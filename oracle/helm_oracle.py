@@ -262,8 +262,12 @@ def _back_substitute(R, g):
     return y
 
 
-def fgmres(apply_A, apply_M, b, x0=None, tol=1e-7, max_iter=250, restart=10):
-    """krylov.py:39-146: restarted flexible GMRES, CGS + conditional second pass."""
+def fgmres(apply_A, apply_M, b, x0=None, tol=1e-7, max_iter=250, restart=10, store=None):
+    """krylov.py:39-146: restarted flexible GMRES, CGS + conditional second pass.
+
+    ``store`` (precision-envelope experiments only) rounds every basis vector as it is stored in V / Z.
+    """
+    st = store or (lambda v: v)
     if tol <= 0 or max_iter < 1:
         raise ValueError("bad tol / max_iter")
     b = np.asarray(b, dtype=np.complex128)
@@ -291,14 +295,14 @@ def fgmres(apply_A, apply_M, b, x0=None, tol=1e-7, max_iter=250, restart=10):
         cs, sn = [], []
         g = np.zeros(m + 1, dtype=np.complex128)
         g[0] = beta
-        V[0] = r.ravel() / beta
+        V[0] = st(r.ravel() / beta)
         j = 0
         while j < m:
             z = np.asarray(apply_M(V[j].reshape(shape)), dtype=np.complex128).ravel()
             w = np.asarray(apply_A(z.reshape(shape)), dtype=np.complex128).ravel()
             if not np.isfinite(w).all():
                 raise OracleError("nonfinite", f"non-finite Krylov vector at iteration {it + 1}")
-            Z[j] = z
+            Z[j] = st(z)
             wn = np.linalg.norm(w)
             hcol = V[: j + 1].conj() @ w
             w = w - hcol @ V[: j + 1]
@@ -332,7 +336,7 @@ def fgmres(apply_A, apply_M, b, x0=None, tol=1e-7, max_iter=250, restart=10):
                     "breakdown",
                     f"Arnoldi breakdown at iteration {it} with relative residual {est:.3e}",
                 )
-            V[j] = w / hn
+            V[j] = st(w / hn)
         y = _back_substitute(H[:j, :j], g[:j])
         x = x + (y @ Z[:j]).reshape(shape)
         r = b - apply_A(x)
@@ -355,21 +359,22 @@ def solve_vcycle(model: Model, b, hier=None, tol=1e-7, max_iter=250, restart=10)
 
 
 def solve_learned(model: Model, b, net_apply, tol=1e-7, max_iter=250, restart=10,
-                  warmup_iters=3, hier=None, round_z=None):
+                  warmup_iters=3, hier=None, round_z=None, vcycle=None, store=None):
     """krylov.py:180-246: V-cycle warm-up, then M(r) = v_cycle(r, u0 = net(r)).
 
-    ``round_z`` (precision-envelope experiments only, oracle/precision_envelope.py) post-processes
-    every preconditioner output z, e.g. rounding it to complex64 storage.
+    ``round_z`` / ``vcycle`` (precision-envelope experiments only, oracle/precision_envelope.py)
+    post-process every preconditioner output z / replace the V-cycle ``vcycle(r, u0)``.
     """
     hier = hier or build_hierarchy(model)
     A = lambda u: helmholtz(u, model)  # noqa: E731
     rz = round_z or (lambda z: z)
-    x1, r1 = fgmres(A, lambda r: rz(v_cycle(r, None, hier)), b, None, tol,
-                    min(warmup_iters, max_iter), restart)
+    vc = vcycle or (lambda r, u0: v_cycle(r, u0, hier))
+    x1, r1 = fgmres(A, lambda r: rz(vc(r, None)), b, None, tol,
+                    min(warmup_iters, max_iter), restart, store)
     if r1.converged or r1.iterations >= max_iter:
         return x1, r1
     rel1 = np.linalg.norm(b - A(x1)) / np.linalg.norm(b)
-    x2, r2 = fgmres(A, lambda r: rz(v_cycle(r, net_apply(r), hier)), b, x1, tol / rel1,
-                    max_iter - r1.iterations, restart)
+    x2, r2 = fgmres(A, lambda r: rz(vc(r, net_apply(r))), b, x1, tol / rel1,
+                    max_iter - r1.iterations, restart, store)
     return x2, Report(r1.iterations + r2.iterations,
                       r1.history + [e * rel1 for e in r2.history[1:]], r2.converged)

@@ -2,20 +2,23 @@
 
 The north-star bar asks for residual histories within 1e-4 relative per iteration of the
 complex128 reference while the solve runs in the BASELINE's complex64/fp32 precision.  This
-script measures how far the REFERENCE'S OWN ALGORITHM moves when the only change is the
-storage precision of the preconditioned vectors: the oracle restatement (pinned to the
-reference to <= 1e-8, ``make_golden_configs.py``) runs the same solve with every
-preconditioner output z = M v rounded to complex64 (exactly what a complex64 Krylov basis Z
-stores; ``krylov.py:95`` keeps z in ``Z[j]``), everything else in complex128.
+script measures how far the REFERENCE'S OWN ALGORITHM moves when only the preconditioner runs in
+that precision class: the oracle restatement (pinned to the reference to <= 1e-8,
+``make_golden_configs.py``) runs the same solve with the V-cycle (``multigrid.py:247-274``)
+evaluated in complex64/float32 arithmetic (``V32`` below, the device V-cycle's precision class)
+and every Krylov basis vector stored in complex64 as it enters V or Z (the device's complex64
+bases, ``krylov.py:94-95, 135``); the outer operator, the Gram-Schmidt sums, Givens and the
+iterate stay complex128 / fp64 exactly as on the device.  (The network is float32 in both.)
 
-Measured at C3 multigrid-only, RHS 0: iterations 395 = 395, x within 8e-8,
-history within 3.7e-5 up to iteration 230, then 1.0e-2 at iteration 231 -- a near-stagnation
-step of GMRES where the Givens estimate is ill-conditioned.  No complex64 implementation can
-meet 1e-4 there, whatever its arithmetic; the per-iteration deviation of that run is the
-envelope the GPU parity tests (``tests/test_gpu_config_parity.py``) scale their bar by.
+Measured at C3 multigrid-only, RHS 0: merely rounding z to complex64 already moves
+the history by 1.0e-2 at iteration 231 -- a near-stagnation stretch of GMRES where the residual
+estimate is ill-conditioned -- while the iteration count (395) and x (8e-8) are unchanged.  No
+complex64 implementation can meet 1e-4 per iteration there; the per-iteration deviation of the
+fp32-V-cycle run is the envelope the GPU parity tests (``tests/test_gpu_config_parity.py``) scale
+their history bar by.
 
-Output: ``tests/golden/envelope_c{2,3}.npz`` with ``<case>.env`` = |h_z64 - h_ref| / h_ref per
-iteration (over the common length) and ``<case>.iterations`` of the z64 run.
+Output: ``tests/golden/envelope_c{2,3}.npz`` with ``<case>.env`` = |h_c64 - h_ref| / h_ref per
+iteration (over the common length) and ``<case>.iterations`` of that run.
 
     PYTHONDONTWRITEBYTECODE=1 python oracle/precision_envelope.py --jobs 4 [--cases c3_mg_0,...]
 """
@@ -41,6 +44,80 @@ def c64(z):
     return np.asarray(z).astype(np.complex64).astype(np.complex128)
 
 
+class V32:
+    """The reference V(1,1)-cycle (multigrid.py:247-274) in complex64 / float32 ARITHMETIC: the precision
+    class of the GPU's V-cycle (BASELINE: complex64/fp32).  Same operations and order as the oracle
+    (helm_oracle.v_cycle); the coarse GMRES keeps complex128 reductions like the device kernel.  Input and
+    output are complex128 arrays holding complex64 values."""
+
+    def __init__(self, hier):
+        from oracle import helm_oracle as ho
+
+        self.ho, self.H = ho, hier
+        self.lv = []
+        for L in hier.levels:
+            m = L.model
+            c = ho.mass(m, L.alpha, L.beta).astype(np.complex64)
+            self.lv.append(dict(c=c, diag=L.diag.astype(np.complex64), h2=np.float32(1.0 / (m.h * m.h)),
+                                wall=None if L.wall is None else L.wall.astype(np.float32), level=L))
+        self.fw = self.ho.FW.astype(np.float32)
+
+    def apply(self, u, d):
+        out = np.float32(4.0) * u
+        out[:-1, :] -= u[1:, :]
+        out[1:, :] -= u[:-1, :]
+        out[:, :-1] -= u[:, 1:]
+        out[:, 1:] -= u[:, :-1]
+        out = out * d["h2"] - d["c"] * u
+        if d["wall"] is not None:
+            out = out + d["wall"] * u
+        return out
+
+    def restrict(self, f):
+        nx, ny = f.shape
+        cx, cy = nx // 2, ny // 2
+        pad = np.zeros((2 * cx + 1, 2 * cy + 1), dtype=np.complex64)
+        pad[: min(nx, 2 * cx + 1), : min(ny, 2 * cy + 1)] = f[: 2 * cx + 1, : 2 * cy + 1]
+        out = np.zeros((cx, cy), dtype=np.complex64)
+        for a in range(3):
+            for b in range(3):
+                out += self.fw[a, b] * pad[a: a + 2 * cx: 2, b: b + 2 * cy: 2]
+        return out
+
+    def prolong(self, c, shape):
+        cx, cy = c.shape
+        full = np.zeros((2 * cx + 1, 2 * cy + 1), dtype=np.complex64)
+        for a in range(3):
+            for b in range(3):
+                full[a: a + 2 * cx: 2, b: b + 2 * cy: 2] += (np.float32(4.0) * self.fw[a, b]) * c
+        return full[: shape[0], : shape[1]]
+
+    def __call__(self, rhs, u0=None):
+        r = np.asarray(rhs).astype(np.complex64)
+        u = np.zeros_like(r) if u0 is None else np.asarray(u0).astype(np.complex64)
+        return self._cycle(r, u, 0).astype(np.complex128)
+
+    def _cycle(self, rhs, u, depth):
+        if u is None:
+            u = np.zeros_like(rhs)
+        d = self.lv[depth]
+        H = self.H
+        if depth == len(self.lv) - 1:
+            s = np.float32(0.8) / d["diag"]
+            x, _ = self.ho.fgmres(lambda v: self.apply(np.asarray(v).astype(np.complex64), d).astype(np.complex128),
+                                  lambda v: (s * np.asarray(v).astype(np.complex64)).astype(np.complex128),
+                                  rhs.astype(np.complex128), None, 1e-12, H.coarse_iters, H.coarse_iters)
+            return x.astype(np.complex64)
+        w0, w1 = np.float32(H.damping[0]), np.float32(H.damping[1])
+        for _ in range(H.relax_pre):
+            u = u + w0 * ((rhs - self.apply(u, d)) / d["diag"])
+        e = self._cycle(self.restrict(rhs - self.apply(u, d)), None, depth + 1)
+        u = u + self.prolong(e, rhs.shape)
+        for _ in range(H.relax_post):
+            u = u + w1 * ((rhs - self.apply(u, d)) / d["diag"])
+        return u
+
+
 def run_case(case):
     from oracle import helm_oracle as ho
     from oracle import network_oracle as no
@@ -59,13 +136,15 @@ def run_case(case):
         p = netparams.init_params(ch, seed=0)
         feats = no.encode(p, L, no.media_planes(m.kappa_sq, m.gamma, L))
         spec = no.spectrum_c64(p, L, m.shape)
+        v32 = V32(H)
         x, rep = ho.solve_learned(om, cfg.rhs[idx],
-                                  lambda r: no.preconditioner_estimate(p, L, feats, spec, r, m.h),
-                                  cfg.tol, cfg.max_iter, cfg.restart, 3, H, round_z=c64)
+                                  lambda r: no.preconditioner_estimate(p, L, feats, spec, c64(r), m.h),
+                                  cfg.tol, cfg.max_iter, cfg.restart, 3, H, vcycle=lambda r, u0: v32(c64(r), u0),
+                                  store=c64)
     else:
         A = lambda u: ho.helmholtz(u, om)  # noqa: E731
-        x, rep = ho.fgmres(A, lambda r: c64(ho.v_cycle(r, None, H)), cfg.rhs[idx], None, cfg.tol, cfg.max_iter,
-                           cfg.restart)
+        v32 = V32(H)
+        x, rep = ho.fgmres(A, lambda r: v32(r), cfg.rhs[idx], None, cfg.tol, cfg.max_iter, cfg.restart, store=c64)
     g = np.load(os.path.join(OUT, f"configs_{cfgname.lower()}.npz"))
     ref = g[f"{case}.hist"]
     h = np.asarray(rep.history)

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include <type_traits>
+#include <algorithm>
 
 #include "cnn.h"
 #include "common.cuh"
@@ -37,7 +38,9 @@ struct hs_net {
   std::vector<float> thin_w[3];
   mutable std::mutex plan_mu;
   mutable std::map<int, cufftHandle> plans;  // batch -> plan
+  std::vector<const float*> wide_w;          // layers whose bf16x3 split is registered (conv_wide.cu)
   ~hs_net() {
+    for (const float* w : wide_w) hs::conv_wide_unregister(w);
     for (auto& kv : plans) cufftDestroy(kv.second);
     if (spec) cudaFree(spec);
     if (spec_perm) cudaFree(spec_perm);
@@ -1262,6 +1265,25 @@ HS_API int hs_net_create(hs_net_t** out, const hs_net_desc_t* desc, void* stream
       for (int t = 0; t < 9; ++t)
         for (int i = 0; i < ci; ++i) h[(t * ci + i) * co + o] = w[(o * 9 + t) * ci + i];
     for (int o = 0; o < co; ++o) h[nw + o] = b[o];
+  }
+  // the >= 64-channel layers: bf16x3 weight pieces for the K-streamed tcgen05 kernel, split once here
+  {
+    const hs_conv_t* all[] = {&desc->enc_stem, &desc->sol_stem, &desc->sol_head};
+    std::vector<const hs_conv_t*> convs(all, all + 3);
+    for (int l = 0; l < desc->levels; ++l)
+      for (const hs_conv_t* c : {&desc->enc_res_a[l], &desc->enc_res_b[l], &desc->enc_down[l], &desc->sol_res_a[l],
+                                 &desc->sol_res_b[l], &desc->sol_down[l], &desc->sol_up[l], &desc->sol_ures_a[l],
+                                 &desc->sol_ures_b[l]})
+        convs.push_back(c);
+    for (const hs_conv_t* c : convs) {
+      if (!c->w || std::find(n->wide_w.begin(), n->wide_w.end(), c->w) != n->wide_w.end()) continue;
+      if (!hs::conv_wide_eligible(c->cin, c->cout)) continue;
+      if (hs::conv_wide_register(c->w, c->cin, c->cout, st)) {
+        delete n;
+        return cfail(HS_ECUDA, "wide-layer weight split");
+      }
+      n->wide_w.push_back(c->w);
+    }
   }
   const long long ns = (long long)n->cc * 4 * n->hc * n->wc;
   cufftDoubleComplex* s128 = nullptr;

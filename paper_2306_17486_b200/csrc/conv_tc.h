@@ -17,6 +17,12 @@ bool conv_wide_launch(const float* x, int H, int W, int cin, float* y, int Ho, i
                       int transposed, const float* w, const float* bias, int softplus, const float* addend,
                       long long addend_bstride, int addend_per_model, const int* model_of, const float* residual,
                       const void* const* active, int B, cudaStream_t st, int planar);
+// The network's wide layers are split into bf16x3 pieces once, at hs_net_create (conv_wide_register,
+// keyed by the device weight pointer; conv_wide_unregister at hs_net_destroy).  Unregistered weights are
+// split into a stream-ordered temporary on every launch.
+bool conv_wide_eligible(int cin, int cout);
+int conv_wide_register(const float* w, int cin, int cout, cudaStream_t st);
+void conv_wide_unregister(const float* w);
 // planar != 0: the output is stored complex-planar, channel pair (2c, 2c+1) of pixel p at
 // float2 index (b * cout/2 + c) * Ho * Wo + p (the implicit layer's coalesced input)
 }  // namespace hs

@@ -26,18 +26,23 @@
 // Warp roles (one persistent CTA per SM):
 //   warps 0-7    epilogue: tcgen05.ld of lane quarter (warp % 4) x column half (warp / 4), bias,
 //                softplus, encoder / skip addend, residual, NHWC (or complex-planar) stores
-//   warps 8-11   A converters: input row chunks (RW pixels x 16 channels, fp32, L2-prefetched)
+//   warps 8-15   A converters: input row chunks (RW pixels x 16 channels, fp32, L2-prefetched)
 //                -> exact bf16x3 split -> A ring (UMMA K-major interleaved layout, 16 B pixel pitch,
-//                so the A operand of tap kx is the staged row with its start address moved by kx)
-//   warps 12-15  B converters: weight pieces (cout x 16 channels of one tap) -> bf16x3 -> B ring
-//   warp 16      MMA issuer (one elected lane issues tcgen05.mma; commits release ring slots and
+//                so the A operand of tap kx is the staged row with its start address moved by kx);
+//                the next row's global loads are in flight while the current row is split
+//   warp 16      B producer: one cp.async.bulk per weight piece into the B ring (mbarrier tx-count)
+//   warp 17      MMA issuer (one elected lane issues tcgen05.mma; commits release ring slots and
 //                hand the accumulators to the epilogue)
-// The weights are read as fp32 from L2 and split on the fly (4 B per weight instead of 6 B for a
-// pre-split copy); every activation element is read from HBM once (the first channel chunk of a
-// pass pulls the pass's input rows into L2 with bulk prefetches, the other chunks hit L2).
+// The weights are split once into bf16x3 pieces laid out exactly like a B ring slot
+// (k_wide_split: at network creation for the network's layers, conv_wide_register; otherwise a
+// stream-ordered temporary per launch).  Every activation element is read from HBM once (the first
+// channel chunk of a pass pulls the pass's input rows into L2 with bulk prefetches, the other chunks
+// hit L2).
 #include <cuda_bf16.h>
 
 #include <cstdio>
+#include <map>
+#include <mutex>
 
 #include "common.cuh"
 #include "conv_tc.h"
@@ -48,8 +53,8 @@ namespace hs {
 namespace {
 using namespace tc;
 
-constexpr int kWEpi = 8, kWAcv = 4, kWBcv = 4;
-constexpr int kWarpA0 = kWEpi, kWarpB0 = kWEpi + kWAcv, kWarpMma = kWEpi + kWAcv + kWBcv;
+constexpr int kWEpi = 8, kWAcv = 8;
+constexpr int kWarpA0 = kWEpi, kWarpB = kWEpi + kWAcv, kWarpMma = kWarpB + 1;
 constexpr int kWThreads = 32 * (kWarpMma + 1);
 constexpr size_t kWSmemMax = 232448;
 
@@ -71,6 +76,7 @@ struct WCfg {
   static constexpr uint32_t B_PLANE = (uint32_t)3 * COUT * 16;  // one 8-channel half: rows [W0 | W1 | W2]
   static constexpr uint32_t B_SLOT = 2 * B_PLANE;
   static constexpr int NBS = 6;                            // B ring slots
+  static constexpr int IPT = (2 * RW + 32 * kWAcv - 1) / (32 * kWAcv);  // A items per converter thread
   static constexpr size_t FIXED = (size_t)NBS * B_SLOT + 1024 + 4 * COUT;  // + barriers, bias
   static constexpr int pick_nas() {
     for (int n = NROWS + 4; n > NROWS; --n)
@@ -86,6 +92,7 @@ struct WCfg {
 };
 
 struct WArgs {
+  const unsigned char* wsplit;  // bf16x3 weight pieces [chunk][tap] x B_SLOT bytes (k_wide_split)
   const float* x;
   int H, W;
   float* y;
@@ -191,7 +198,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(WArgs a) {
       mbar_init(smem_u32(&a_empty[i]), 1);
     }
     for (int i = 0; i < NBS; ++i) {
-      mbar_init(smem_u32(&b_full[i]), kWBcv);
+      mbar_init(smem_u32(&b_full[i]), 1);
       mbar_init(smem_u32(&b_empty[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -214,83 +221,112 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(WArgs a) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp >= kWarpA0 && warp < kWarpA0 + kWAcv) {
-    // ================= A converters: input row chunks -> bf16x3 A ring
+    // ================= A converters: input row chunks -> bf16x3 A ring.  Item e of a row is (pixel
+    // e % RW, channel half e / RW): pixel fastest, so the 16-byte smem stores of a warp are contiguous.
     const int t = tid - 32 * kWarpA0;
-    constexpr int NT = 32 * kWAcv;
+    constexpr int NT = 32 * kWAcv, IPT = C::IPT;
     uint32_t seq = 0;
-    for (long long u = blockIdx.x; u < npass; u += gridDim.x) {
-      Pass P;
-      if (!pass_at<MODE, C>(a, u, P)) continue;
+    float4 cur[IPT][2], nxt[IPT][2];
+    // issue the global loads of one row chunk (zero outside the image)
+    auto load_row = [&](const float* img, int g, int x0, int c, float4 (&v)[IPT][2]) {
+      const bool row_ok = g >= 0 && g < a.H;
+      const float* src = img + (size_t)(row_ok ? g : 0) * a.W * CIN + 16 * c;
+#pragma unroll
+      for (int k = 0; k < IPT; ++k) {
+        const int e = t + k * NT, p = e % C::RW, h = e / C::RW, col = x0 + p;
+        v[k][0] = v[k][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (e < 2 * C::RW && row_ok && col >= 0 && col < a.W) {
+          const float4* s4 = reinterpret_cast<const float4*>(src + (size_t)col * CIN + 8 * h);
+          v[k][0] = __ldg(s4);
+          v[k][1] = __ldg(s4 + 1);
+        }
+      }
+    };
+    // the (pass, chunk, row) sequence this CTA converts, walked one step ahead for the loads
+    long long u = blockIdx.x;
+    Pass P{};
+    auto next_pass = [&]() {
+      while (u < npass && !pass_at<MODE, C>(a, u, P)) u += gridDim.x;
+      return u < npass;
+    };
+    bool have = next_pass();
+    int c = 0, i = 0;
+    auto prefetch_pass = [&]() {  // pull the pass's input rows (all channels) and side-input rows into L2
       const int g0 = first_row<MODE>(P.oy0), x0 = first_col<MODE>(P.xb);
-      const float* img = a.x + (size_t)P.b * a.H * a.W * CIN;
       const int clo = max(x0, 0), chi = min(x0 + C::RW, a.W);
-      if (t == 0) {
-        // pull this pass's input rows (all channels) into L2: the later channel chunks hit L2
-        for (int i = 0; i < NROWS; ++i) {
-          const int g = g0 + i;
-          if (g >= 0 && g < a.H && chi > clo)
-            prefetch_l2(img + ((size_t)g * a.W + clo) * CIN, (uint32_t)(chi - clo) * CIN * 4);
-        }
+      const float* img = a.x + (size_t)P.b * a.H * a.W * CIN;
+      for (int r = 0; r < NROWS; ++r) {
+        const int g = g0 + r;
+        if (g >= 0 && g < a.H && chi > clo)
+          prefetch_l2(img + ((size_t)g * a.W + clo) * CIN, (uint32_t)(chi - clo) * CIN * 4);
       }
-      for (int c = 0; c < NCH; ++c) {
-        for (int i = 0; i < NROWS; ++i, ++seq) {
-          const uint32_t s = seq % NAS, use = seq / NAS;
-          if (use > 0) mbar_wait(smem_u32(&a_empty[s]), (use - 1) & 1);
-          unsigned char* slot = aring + (size_t)s * C::A_SLOT;
-          const int g = g0 + i;
-          const bool row_ok = g >= 0 && g < a.H;
-          const float* src = img + (size_t)(row_ok ? g : 0) * a.W * CIN + 16 * c;
-          for (int e = t; e < 2 * C::RW; e += NT) {
-            const int p = e % C::RW, h = e / C::RW;  // pixel fastest: conflict-free 16-byte stores
-            const int col = x0 + p;
-            float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            if (row_ok && col >= 0 && col < a.W) {
-              const float4* s4 = reinterpret_cast<const float4*>(src + (size_t)col * CIN + 8 * h);
-              const float4 v0 = __ldg(s4), v1 = __ldg(s4 + 1);
-              v[0] = v0.x, v[1] = v0.y, v[2] = v0.z, v[3] = v0.w, v[4] = v1.x, v[5] = v1.y, v[6] = v1.z, v[7] = v1.w;
-            }
-            uint4 q0, q1, q2;
-            split_bf16x3(v, q0, q1, q2);
-            const size_t off = (size_t)h * C::A_PLANE + (size_t)staged<MODE>(p) * 16;
-            *reinterpret_cast<uint4*>(slot + off) = q0;
-            *reinterpret_cast<uint4*>(slot + 2 * C::A_PLANE + off) = q1;
-            *reinterpret_cast<uint4*>(slot + 4 * C::A_PLANE + off) = q2;
-          }
-          fence_async_smem();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&a_full[s]));
-        }
+      const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[P.b] : 0) : P.b) *
+                                                   a.addend_bstride
+                                  : nullptr;
+      constexpr int OXN = MODE == 2 ? 256 : 128;  // output columns of a tile
+      for (int r = 0; r < R && P.oy0 + r < a.Ho; ++r) {
+        const size_t pix = (size_t)(P.oy0 + r) * a.Wo + (size_t)OXN * P.xb;
+        if (add) prefetch_l2(add + pix * COUT, OXN * COUT * 4);
+        if (a.residual) prefetch_l2(a.residual + ((size_t)P.b * a.Ho * a.Wo + pix) * COUT, OXN * COUT * 4);
       }
+    };
+    if (have) {
+      if (t == 0) prefetch_pass();
+      load_row(a.x + (size_t)P.b * a.H * a.W * CIN, first_row<MODE>(P.oy0) + i, first_col<MODE>(P.xb), c, nxt);
     }
-  } else if (warp >= kWarpB0 && warp < kWarpB0 + kWBcv) {
-    // ================= B converters: weight pieces (c, ky, kx) -> bf16x3 B ring, in MMA order
-    const int t = tid - 32 * kWarpB0;
-    constexpr int NT = 32 * kWBcv;
-    uint32_t seq = 0;
-    for (long long u = blockIdx.x; u < npass; u += gridDim.x) {
-      Pass P;
-      if (!pass_at<MODE, C>(a, u, P)) continue;
-      for (int c = 0; c < NCH; ++c)
-        for (int tap = 0; tap < 9; ++tap, ++seq) {
+    while (have) {
+#pragma unroll
+      for (int k = 0; k < IPT; ++k) cur[k][0] = nxt[k][0], cur[k][1] = nxt[k][1];
+      // advance (pass, chunk, row) and put the next row's loads in flight
+      if (++i == NROWS) {
+        i = 0;
+        if (++c == NCH) {
+          c = 0;
+          u += gridDim.x;
+          have = next_pass();
+          if (have && t == 0) prefetch_pass();
+        }
+      }
+      if (have)
+        load_row(a.x + (size_t)P.b * a.H * a.W * CIN, first_row<MODE>(P.oy0) + i, first_col<MODE>(P.xb), c, nxt);
+      // convert the current row into its ring slot
+      const uint32_t s = seq % NAS, use = seq / NAS;
+      if (use > 0) mbar_wait(smem_u32(&a_empty[s]), (use - 1) & 1);
+      unsigned char* slot = aring + (size_t)s * C::A_SLOT;
+#pragma unroll
+      for (int k = 0; k < IPT; ++k) {
+        const int e = t + k * NT;
+        if (e >= 2 * C::RW) break;
+        const int p = e % C::RW, h = e / C::RW;
+        const float v[8] = {cur[k][0].x, cur[k][0].y, cur[k][0].z, cur[k][0].w,
+                            cur[k][1].x, cur[k][1].y, cur[k][1].z, cur[k][1].w};
+        uint4 q0, q1, q2;
+        split_bf16x3(v, q0, q1, q2);
+        const size_t off = (size_t)h * C::A_PLANE + (size_t)staged<MODE>(p) * 16;
+        *reinterpret_cast<uint4*>(slot + off) = q0;
+        *reinterpret_cast<uint4*>(slot + 2 * C::A_PLANE + off) = q1;
+        *reinterpret_cast<uint4*>(slot + 4 * C::A_PLANE + off) = q2;
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&a_full[s]));
+      ++seq;
+    }
+  } else if (warp == kWarpB) {
+    // ================= B producer: pre-split weight pieces (c, ky, kx), one bulk copy each, in MMA order
+    if (lane == 0) {
+      uint32_t seq = 0;
+      for (long long u = blockIdx.x; u < npass; u += gridDim.x) {
+        Pass P;
+        if (!pass_at<MODE, C>(a, u, P)) continue;
+        for (int pc = 0; pc < NCH * 9; ++pc, ++seq) {
           const uint32_t s = seq % NBS, use = seq / NBS;
           if (use > 0) mbar_wait(smem_u32(&b_empty[s]), (use - 1) & 1);
-          unsigned char* slot = bring + (size_t)s * C::B_SLOT;
-          for (int e = t; e < 2 * COUT; e += NT) {
-            const int n = e % COUT, h = e / COUT;
-            const float4* s4 = reinterpret_cast<const float4*>(a.w + ((size_t)n * 9 + tap) * CIN + 16 * c + 8 * h);
-            const float4 v0 = __ldg(s4), v1 = __ldg(s4 + 1);
-            const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-            uint4 q0, q1, q2;
-            split_bf16x3(v, q0, q1, q2);
-            const size_t off = (size_t)h * C::B_PLANE + (size_t)n * 16;  // part p at row p * cout + n
-            *reinterpret_cast<uint4*>(slot + off) = q0;
-            *reinterpret_cast<uint4*>(slot + off + (size_t)COUT * 16) = q1;
-            *reinterpret_cast<uint4*>(slot + off + (size_t)2 * COUT * 16) = q2;
-          }
-          fence_async_smem();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&b_full[s]));
+          const uint32_t bar = smem_u32(&b_full[s]);
+          mbar_arrive_tx(bar, C::B_SLOT);
+          bulk_g2s(smem_u32(bring + (size_t)s * C::B_SLOT), a.wsplit + (size_t)pc * C::B_SLOT, C::B_SLOT, bar);
         }
+      }
     }
   } else if (warp == kWarpMma) {
     // ================= MMA issuer
@@ -375,58 +411,80 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(WArgs a) {
       const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[P.b] : 0) : P.b) *
                                                    a.addend_bstride
                                   : nullptr;
-      for (int r = 0; r < R; ++r) {
+      // side input (encoder / skip addend or residual) of one 16-channel segment: loaded a segment
+      // ahead of its use (the converters pulled the pass's side rows into L2 when the pass started)
+      constexpr int SEG = 16, NSEG = EH / SEG;
+      const float* side = add ? add : a.residual;
+      const bool side_res = !add;  // addend rows are indexed by pixel, residual rows by (b, pixel)
+      auto side_ptr = [&](int r, int k, int sg) -> const float4* {
+        const int ox = MODE == 2 ? 2 * (128 * P.xb + m) + k : 128 * P.xb + m;
+        const size_t pix = (size_t)(P.oy0 + r) * a.Wo + ox;
+        const size_t base = side_res ? ((size_t)P.b * a.Ho * a.Wo + pix) * COUT : pix * COUT;
+        return reinterpret_cast<const float4*>(side + base + hc * EH + sg * SEG);
+      };
+      float4 sd[SEG / 4], sn[SEG / 4];
+      auto load_side = [&](int r, int k, int sg, float4 (&dst)[SEG / 4]) {
+#pragma unroll
+        for (int q = 0; q < SEG / 4; ++q) dst[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (side && P.oy0 + r < a.Ho) {
+          const float4* sp = side_ptr(r, k, sg);
+#pragma unroll
+          for (int q = 0; q < SEG / 4; ++q) dst[q] = __ldg(sp + q);
+        }
+      };
+      load_side(0, 0, 0, sn);
+      for (int step = 0; step < R * C::NACC * NSEG; ++step) {
+        const int sg = step % NSEG, k = (step / NSEG) % C::NACC, r = step / (NSEG * C::NACC);
+#pragma unroll
+        for (int q = 0; q < SEG / 4; ++q) sd[q] = sn[q];
+        if (step + 1 < R * C::NACC * NSEG) {
+          const int s1 = step + 1;
+          load_side(s1 / (NSEG * C::NACC), (s1 / NSEG) % C::NACC, s1 % NSEG, sn);
+        }
         const int oy = P.oy0 + r;
+        const int ox = MODE == 2 ? 2 * (128 * P.xb + m) + k : 128 * P.xb + m;
+        const size_t pix = (size_t)oy * a.Wo + ox;
+        const size_t obase = ((size_t)P.b * a.Ho * a.Wo + pix) * COUT + hc * EH + sg * SEG;
+        float o[SEG];
 #pragma unroll
-        for (int k = 0; k < C::NACC; ++k) {
-          const int ox = MODE == 2 ? 2 * (128 * P.xb + m) + k : 128 * P.xb + m;
-          const size_t pix = (size_t)oy * a.Wo + ox;
-          const size_t obase = ((size_t)P.b * a.Ho * a.Wo + pix) * COUT + hc * EH;
-          const bool ok = oy < a.Ho;
+        for (int n0 = 0; n0 < SEG; n0 += 8) {
+          uint32_t v[8], v1[8], v2[8];
+          const uint32_t col = tmem + ((uint32_t)(32 * q4) << 16) + set * C::SET_COLS +
+                               (uint32_t)((r * C::NACC + k) * C::ACC_COLS) + hc * EH + sg * SEG + n0;
+          tmem_ld8(col, v);
+          tmem_ld8(col + COUT, v1);
+          if constexpr (C::G == 3) tmem_ld8(col + 2 * COUT, v2);
+          tmem_wait_ld();
 #pragma unroll
-          for (int n0 = 0; n0 < EH; n0 += 8) {
-            uint32_t v[8], v1[8], v2[8];
-            const uint32_t col = tmem + ((uint32_t)(32 * q4) << 16) + set * C::SET_COLS +
-                                 (uint32_t)((r * C::NACC + k) * C::ACC_COLS) + hc * EH + n0;
-            tmem_ld8(col, v);
-            tmem_ld8(col + COUT, v1);
-            if constexpr (C::G == 3) tmem_ld8(col + 2 * COUT, v2);
-            tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {  // g0 + (g1 [+ g2]): the corrections are summed first
-              const float corr = C::G == 3 ? __uint_as_float(v1[j]) + __uint_as_float(v2[j]) : __uint_as_float(v1[j]);
-              v[j] = __float_as_uint(__uint_as_float(v[j]) + corr);
-            }
-            if (!ok) continue;
-            float o[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              o[j] = __uint_as_float(v[j]) + s_bias[hc * EH + n0 + j];
-              if (a.softplus) o[j] = softplus_fast(o[j]);
-            }
-            if (add) {
-              const float4* ap = reinterpret_cast<const float4*>(add + pix * COUT + hc * EH + n0);
-              const float4 a0 = __ldg(ap), a1 = __ldg(ap + 1);
-              o[0] += a0.x, o[1] += a0.y, o[2] += a0.z, o[3] += a0.w, o[4] += a1.x, o[5] += a1.y, o[6] += a1.z,
-                  o[7] += a1.w;
-            }
-            if (a.residual) {
-              const float4* rp = reinterpret_cast<const float4*>(a.residual + obase + n0);
-              const float4 r0 = __ldg(rp), r1 = __ldg(rp + 1);
-              o[0] += r0.x, o[1] += r0.y, o[2] += r0.z, o[3] += r0.w, o[4] += r1.x, o[5] += r1.y, o[6] += r1.z,
-                  o[7] += r1.w;
-            }
-            if (a.planar) {  // channel pairs (2c, 2c+1) -> complex plane c (the implicit layer's input)
-              float2* yp = reinterpret_cast<float2*>(a.y) +
-                           ((size_t)P.b * (COUT / 2) + (hc * EH + n0) / 2) * ((size_t)a.Ho * a.Wo) + pix;
-#pragma unroll
-              for (int j = 0; j < 4; ++j) yp[(size_t)j * a.Ho * a.Wo] = make_float2(o[2 * j], o[2 * j + 1]);
-            } else {
-              float4* yp = reinterpret_cast<float4*>(a.y + obase + n0);
-              yp[0] = make_float4(o[0], o[1], o[2], o[3]);
-              yp[1] = make_float4(o[4], o[5], o[6], o[7]);
-            }
+          for (int j = 0; j < 8; ++j) {  // g0 + (g1 [+ g2]): the corrections are summed first
+            const float corr = C::G == 3 ? __uint_as_float(v1[j]) + __uint_as_float(v2[j]) : __uint_as_float(v1[j]);
+            float x = (__uint_as_float(v[j]) + corr) + s_bias[hc * EH + sg * SEG + n0 + j];
+            if (a.softplus) x = softplus_fast(x);
+            o[n0 + j] = x;
           }
+        }
+        if (oy >= a.Ho) continue;  // (warp-uniform: every lane of the warp has the same row)
+#pragma unroll
+        for (int q = 0; q < SEG / 4; ++q) {
+          o[4 * q] += sd[q].x, o[4 * q + 1] += sd[q].y, o[4 * q + 2] += sd[q].z, o[4 * q + 3] += sd[q].w;
+        }
+        if (add && a.residual) {  // both side inputs (not used by the ARCH.md network): the residual directly
+          const float4* rp = reinterpret_cast<const float4*>(a.residual + obase);
+#pragma unroll
+          for (int q = 0; q < SEG / 4; ++q) {
+            const float4 rv = __ldg(rp + q);
+            o[4 * q] += rv.x, o[4 * q + 1] += rv.y, o[4 * q + 2] += rv.z, o[4 * q + 3] += rv.w;
+          }
+        }
+        if (a.planar) {  // channel pairs (2c, 2c+1) -> complex plane c (the implicit layer's input)
+          float2* yp = reinterpret_cast<float2*>(a.y) +
+                       ((size_t)P.b * (COUT / 2) + (hc * EH + sg * SEG) / 2) * ((size_t)a.Ho * a.Wo) + pix;
+#pragma unroll
+          for (int j = 0; j < SEG / 2; ++j) yp[(size_t)j * a.Ho * a.Wo] = make_float2(o[2 * j], o[2 * j + 1]);
+        } else {
+          float4* yp = reinterpret_cast<float4*>(a.y + obase);
+#pragma unroll
+          for (int q = 0; q < SEG / 4; ++q) yp[q] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
         }
       }
       tc_fence_before();
@@ -442,6 +500,43 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(WArgs a) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::NCOLS));
   }
 }
+
+// bf16x3 weight pieces in B-slot layout: piece (c, tap) = [half h][row = part * cout + n] x 16 B, the
+// 8 channels 16 c + 8 h .. + 7 of part `part` of w[n][tap][:]
+template <int CIN, int COUT>
+__global__ void k_wide_split(const float* __restrict__ w, uint4* __restrict__ out) {
+  constexpr int NCH = CIN / 16, ROWS = 3 * COUT;
+  const long long total = (long long)NCH * 9 * 2 * COUT;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int n = (int)(e % COUT), h = (int)((e / COUT) % 2), pc = (int)(e / (2 * COUT));
+    const int c = pc / 9, tap = pc % 9;
+    const float4* s4 = reinterpret_cast<const float4*>(w + ((size_t)n * 9 + tap) * CIN + 16 * c + 8 * h);
+    const float4 v0 = __ldg(s4), v1 = __ldg(s4 + 1);
+    const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    uint4 q[3];
+    split_bf16x3(v, q[0], q[1], q[2]);
+    uint4* piece = out + (size_t)pc * 2 * ROWS;
+#pragma unroll
+    for (int part = 0; part < 3; ++part) piece[(size_t)h * ROWS + part * COUT + n] = q[part];
+  }
+}
+
+size_t split_bytes(int cin, int cout) { return (size_t)(cin / 16) * 9 * 2 * 3 * cout * 16; }
+
+cudaError_t run_split(const float* w, int cin, int cout, void* out, cudaStream_t st) {
+  const int blocks = (int)((split_bytes(cin, cout) / 16 / 3 + 255) / 256);
+  if (cin == 64 && cout == 64) k_wide_split<64, 64><<<blocks, 256, 0, st>>>(w, static_cast<uint4*>(out));
+  else if (cin == 128 && cout == 128) k_wide_split<128, 128><<<blocks, 256, 0, st>>>(w, static_cast<uint4*>(out));
+  else if (cin == 64 && cout == 128) k_wide_split<64, 128><<<blocks, 256, 0, st>>>(w, static_cast<uint4*>(out));
+  else if (cin == 128 && cout == 64) k_wide_split<128, 64><<<blocks, 256, 0, st>>>(w, static_cast<uint4*>(out));
+  else return cudaErrorInvalidValue;
+  prof::count(1);
+  return cudaGetLastError();
+}
+
+// weights registered by hs_net_create: device weight pointer -> its split pieces
+std::mutex reg_mu;
+std::map<const float*, void*> reg;
 
 template <int CIN, int COUT, int MODE>
 void launch_wide(const WArgs& a, cudaStream_t st) {
@@ -481,20 +576,61 @@ bool conv_wide_supported(int cin, int cout, int stride, int transposed, int H, i
          (mode == 2 && cin == 128 && cout == 64);
 }
 
+bool conv_wide_eligible(int cin, int cout) {
+  return (cin == 64 && cout == 64) || (cin == 128 && cout == 128) || (cin == 64 && cout == 128) ||
+         (cin == 128 && cout == 64);
+}
+
+int conv_wide_register(const float* w, int cin, int cout, cudaStream_t st) {
+  if (!conv_wide_eligible(cin, cout)) return 0;
+  void* buf = nullptr;
+  if (cudaMalloc(&buf, split_bytes(cin, cout)) != cudaSuccess) return 1;
+  if (run_split(w, cin, cout, buf, st) != cudaSuccess) {
+    cudaFree(buf);
+    return 1;
+  }
+  std::lock_guard<std::mutex> g(reg_mu);
+  auto it = reg.find(w);
+  if (it != reg.end()) cudaFree(it->second);
+  reg[w] = buf;
+  return 0;
+}
+
+void conv_wide_unregister(const float* w) {
+  std::lock_guard<std::mutex> g(reg_mu);
+  auto it = reg.find(w);
+  if (it == reg.end()) return;
+  cudaFree(it->second);  // synchronises the device: only at network destruction
+  reg.erase(it);
+}
+
 bool conv_wide_launch(const float* x, int H, int W, int cin, float* y, int Ho, int Wo, int cout, int stride,
                       int transposed, const float* w, const float* bias, int softplus, const float* addend,
                       long long addend_bstride, int addend_per_model, const int* model_of, const float* residual,
                       const void* const* active, int B, cudaStream_t st, int planar) {
   if (!conv_wide_supported(cin, cout, stride, transposed, H, W, Wo)) return false;
-  WArgs a{x, H, W, y, Ho, Wo, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual,
-          active, B, planar};
+  const void* split = nullptr;
+  {
+    std::lock_guard<std::mutex> g(reg_mu);
+    auto it = reg.find(w);
+    if (it != reg.end()) split = it->second;
+  }
+  void* tmp = nullptr;
+  if (!split) {  // unregistered weights (hs_conv2d): a stream-ordered temporary split
+    if (cudaMallocAsync(&tmp, split_bytes(cin, cout), st) != cudaSuccess) return false;
+    if (run_split(w, cin, cout, tmp, st) != cudaSuccess) return false;
+    split = tmp;
+  }
+  WArgs a{static_cast<const unsigned char*>(split), x, H, W, y, Ho, Wo, w, bias, softplus, addend, addend_bstride,
+          addend_per_model, model_of, residual, active, B, planar};
   const int mode = transposed ? 2 : (stride == 2 ? 1 : 0);
-  if (mode == 0 && cin == 64) return launch_wide<64, 64, 0>(a, st), true;
-  if (mode == 0 && cin == 128) return launch_wide<128, 128, 0>(a, st), true;
-  if (mode == 1 && cin == 64) return launch_wide<64, 128, 1>(a, st), true;
-  if (mode == 1 && cin == 128) return launch_wide<128, 128, 1>(a, st), true;
-  if (mode == 2 && cout == 64) return launch_wide<128, 64, 2>(a, st), true;
-  return false;
+  if (mode == 0 && cin == 64) launch_wide<64, 64, 0>(a, st);
+  else if (mode == 0 && cin == 128) launch_wide<128, 128, 0>(a, st);
+  else if (mode == 1 && cin == 64) launch_wide<64, 128, 1>(a, st);
+  else if (mode == 1 && cin == 128) launch_wide<128, 128, 1>(a, st);
+  else if (mode == 2 && cout == 64) launch_wide<128, 64, 2>(a, st);
+  if (tmp) cudaFreeAsync(tmp, st);
+  return true;
 }
 
 }  // namespace hs
