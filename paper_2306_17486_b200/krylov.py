@@ -159,6 +159,52 @@ def fgmres(apply_A, apply_M, b, x0=None, tol: float = 1e-7, max_iter: int = 250,
 
 # -------------------------------------------------------------- solve entry points
 
+MAX_FUSED_WINDOW = 32  # engine.MAX_WINDOW: the batched device solver's per-RHS Hessenberg
+
+
+def _needs_generic(hierarchy, restart, max_iter) -> bool:
+    """Settings the fused batched solver does not implement (the reference accepts them all).
+
+    Restart windows beyond 32 vectors (``restart=None`` means one window of ``max_iter``) and V-cycles
+    other than V(1,1) with <= 16 coarse steps run the generic device FGMRES above with the device
+    operator and V-cycle as its callables -- the reference's own composition (krylov.py:170-176,
+    :215-236), on the GPU, one RHS at a time.
+    """
+    from .multigrid import fused_cycle
+
+    window = max_iter if restart is None else min(restart, max_iter)
+    return window > MAX_FUSED_WINDOW or (hierarchy is not None and not fused_cycle(hierarchy))
+
+
+def _generic_solve(model, b, hierarchy, tol, max_iter, restart, net=None, encodings=None, warmup_iters=3):
+    """solve_helmholtz / solve_with_learned_preconditioner through ``fgmres`` with device callables.
+
+    ``b`` is a complex128 CUDA tensor (nx, ny); returns (x tensor, SolveReport).
+    """
+    import torch
+
+    from .fields import apply_operator
+    from .multigrid import v_cycle
+
+    def A(v):
+        return apply_operator(v, model)
+
+    if net is None:
+        return fgmres(A, lambda r: v_cycle(r, None, hierarchy), b, None, tol, max_iter, restart)
+    from .network import preconditioner_estimate
+
+    x1, r1 = fgmres(A, lambda r: v_cycle(r, None, hierarchy), b, None, tol, min(warmup_iters, max_iter), restart)
+    if r1.converged or r1.iterations >= max_iter:
+        return x1, r1
+    rel1 = float(torch.linalg.vector_norm(b - A(x1)) / torch.linalg.vector_norm(b))
+
+    def M(r):
+        return v_cycle(r, preconditioner_estimate(net, encodings, r).to(torch.complex128), hierarchy)
+
+    x2, r2 = fgmres(A, M, b, x1, tol / rel1, max_iter - r1.iterations, restart)
+    hist = r1.relative_residual_history + [e * rel1 for e in r2.relative_residual_history[1:]]
+    return x2, SolveReport(r1.iterations + r2.iterations, hist, r2.converged)
+
 
 def _engine_for(model: SlownessModel, hierarchy, net=None):
     from .engine import Engine
@@ -188,8 +234,16 @@ def solve_helmholtz(model: SlownessModel, b: ComplexField, hierarchy=None, tol: 
     if max_iter < 1:
         raise ValueError(f"max_iter must be >= 1, got {max_iter}")
     start = time.perf_counter()
+    if _needs_generic(hierarchy, restart, max_iter):
+        from .device import to_device
+        from .multigrid import build_hierarchy
+
+        H = hierarchy if hierarchy is not None else build_hierarchy(model)
+        x, rep = _generic_solve(model, to_device(np.asarray(b.data), torch.complex128), H, tol, max_iter, restart)
+        rep.wall_time = time.perf_counter() - start
+        return ComplexField(to_host(x), b.h), rep
     eng = _engine_for(model, hierarchy)
-    bd = torch.from_numpy(np.ascontiguousarray(b.data))[None]
+    bd = torch.from_numpy(np.array(b.data))[None]
     res = eng.fgmres(bd, None, tol, max_iter, restart)
     raise_for_status(res)
     x = to_host(res.x[0])
@@ -244,6 +298,18 @@ class BatchSolver:
             # stacked encodings and the engine re-binds them before each solve
             net_dev, net_enc = device_network(net, self.models, encodings, self.dh)
         self.engine = Engine(self.dh, net_dev, net_enc)
+        self._encodings = encodings
+        self._enc_cache = {}
+
+    def _encodings_for(self, m: int):
+        """Encodings of model m for the generic (unfused) path."""
+        from .network import precompute_encodings
+
+        if self._encodings is not None and self._encodings[m] is not None:
+            return self._encodings[m]
+        if m not in self._enc_cache:
+            self._enc_cache[m] = precompute_encodings(self.net, self.models[m])
+        return self._enc_cache[m]
 
     def solve(self, rhs, model_of=None, tol: float = 1e-7, max_iter: int = 250, restart: int | None = 10,
               warmup_iters: int = 3, return_device: bool = False, raise_errors: bool = True, iter_caps=None):
@@ -267,6 +333,26 @@ class BatchSolver:
         bd = to_device(rhs, torch.complex128)
         B = bd.shape[0]
         owner = np.zeros(B, dtype=np.int32) if model_of is None else np.asarray(model_of, dtype=np.int32)
+        if _needs_generic(self.hierarchies[0], restart, max_iter):
+            if iter_caps is not None:
+                raise ValueError("iter_caps needs the fused solver (restart <= 32, V(1,1), <= 16 coarse steps)")
+            from .network import precompute_encodings
+
+            xs, reports = [], []
+            for i in range(B):
+                m = int(owner[i])
+                enc = None
+                if self.net is not None:
+                    enc = self._encodings_for(m)
+                x, rep = _generic_solve(self.models[m], bd[i], self.hierarchies[m], tol, max_iter, restart,
+                                        self.net, enc, warmup_iters)
+                xs.append(x)
+                reports.append(rep)
+            x = torch.stack(xs)
+            wall = time.perf_counter() - start
+            for rep in reports:
+                rep.wall_time = wall
+            return (x if return_device else to_host(x)), reports
         owner_d = torch.from_numpy(owner).to(dev)
         eng = self.engine
         if iter_caps is not None and self.net is not None:

@@ -334,6 +334,8 @@ def jacobi_relax(u, rhs, level: Level, sweeps: int, damping: float = 0.8):
     from .device import stream_handle
 
     was_np = not isinstance(u, torch.Tensor)
+    if sweeps <= 0:  # the reference loop body never runs: u comes back unchanged
+        return u
     cur = _as_device_complex(u, torch.complex64)
     r = _as_device_complex(rhs, torch.complex64)
     if tuple(cur.shape[-2:]) != tuple(level.model.shape):
@@ -355,11 +357,67 @@ def jacobi_relax(u, rhs, level: Level, sweeps: int, damping: float = 0.8):
     return out.cpu().numpy() if was_np else out
 
 
+COARSE_MAX_ITERS = 16  # hs::kCoarseMaxIters (csrc/vcycle.h)
+
+
+def fused_cycle(hierarchy: GridHierarchy) -> bool:
+    """Whether the fused device V-cycle (csrc/vcycle.cu) implements these cycle settings.
+
+    It fuses exactly one pre- and one post-smoothing sweep into the down / up legs and keeps the
+    coarse GMRES basis on chip for up to 16 steps (BASELINE: V(1,1), 10 coarse steps).  Any other
+    ``relax_pre`` / ``relax_post`` / ``coarse_iters`` the reference accepts (multigrid.py:185-193)
+    runs the general device cycle below instead.
+    """
+    return hierarchy.relax_pre == 1 and hierarchy.relax_post == 1 and 1 <= hierarchy.coarse_iters <= COARSE_MAX_ITERS
+
+
+def _v_cycle_general(rhs, u0, hierarchy: GridHierarchy):
+    """V(relax_pre, relax_post) cycle from the device primitives, any sweep / coarse-step counts.
+
+    The reference's recursion (multigrid.py:264-274) on CUDA tensors: damped Jacobi (hs_jacobi), the
+    level operator in fp64 (hs_helm_apply), full-weighting restriction and bilinear prolongation
+    (hs_restrict / hs_prolong), the coarse solve (fused kernel or, beyond 16 steps, the generic device
+    FGMRES).  Batched (B, nx, ny) or single (nx, ny) complex128 tensors in and out.
+    """
+    import torch
+
+    def cycle(r, u, depth):
+        lv = hierarchy.levels[depth]
+        if depth == len(hierarchy.levels) - 1:
+            return coarse_solve(r, lv, hierarchy.coarse_iters)
+        w0, w1 = hierarchy.jacobi_damping
+        u = jacobi_relax(u, r, lv, hierarchy.relax_pre, w0).to(torch.complex128)
+        rc = restrict_full_weighting(r - lv.apply(u)).to(torch.complex128)
+        e = cycle(rc, torch.zeros_like(rc), depth + 1)
+        u = u + prolong_bilinear(e, tuple(r.shape[-2:])).to(torch.complex128)
+        return jacobi_relax(u, r, lv, hierarchy.relax_post, w1).to(torch.complex128)
+
+    if len(hierarchy.levels) == 1:  # multigrid.py:266-267: u0 ignored
+        return coarse_solve(rhs, hierarchy.levels[0], hierarchy.coarse_iters)
+    return cycle(rhs, torch.zeros_like(rhs) if u0 is None else u0, 0)
+
+
 def coarse_solve(rhs, level: Level, iters: int = 10, damping: float = 0.8):
     """GMRES(iters) with a damped-Jacobi preconditioner, zero guess (multigrid.py:232-244)."""
     import torch
 
     was_np = not isinstance(rhs, torch.Tensor)
+    if iters > COARSE_MAX_ITERS:
+        # The fused coarse kernel keeps its GMRES basis on chip for up to 16 steps.  Longer runs (the
+        # reference's own tests use 20-40, test_multigrid.py:201-229) take the generic device FGMRES
+        # (krylov.fgmres: complex128 basis on the GPU, the level operator in fp64) with the same
+        # arguments as multigrid.py:243: tol 1e-12, max_iter = restart = iters, M = damping / diag.
+        from .device import to_device
+        from .krylov import fgmres
+
+        s = to_device(damping / np.asarray(level.diag), torch.complex128)
+        b = rhs if not was_np else to_device(np.asarray(rhs), torch.complex128)
+        b = b.to(torch.complex128)
+        if b.dim() > 2:
+            x = torch.stack([coarse_solve(bi, level, iters, damping) for bi in b])
+        else:
+            x, _ = fgmres(level.apply, lambda r: s * r, b, None, 1e-12, iters, iters)
+        return x.cpu().numpy() if was_np else x
     one = GridHierarchy((level,), coarse_iters=iters)
     dh = DeviceHierarchy([one])
     dh.hs.coarse_damping = float(damping)
@@ -384,6 +442,10 @@ def v_cycle(rhs, u0, hierarchy: GridHierarchy):
     if u0 is not None and tuple(np.shape(u0)) != tuple(np.shape(rhs)):
         raise DimensionError(f"u0 {tuple(np.shape(u0))} does not match rhs {tuple(np.shape(rhs))}")
     was_np = not isinstance(rhs, torch.Tensor)
+    if not fused_cycle(hierarchy):
+        out = _v_cycle_general(_as_device_complex(rhs, torch.complex128),
+                               None if u0 is None else _as_device_complex(u0, torch.complex128), hierarchy)
+        return out.cpu().numpy() if was_np else out
     r = _as_device_complex(rhs, torch.complex64)
     u = None if u0 is None else _as_device_complex(u0, torch.complex64)
     batched = r.dim() > 2
