@@ -26,19 +26,22 @@
 // Warp roles (one persistent CTA per SM):
 //   warps 0-7    epilogue: tcgen05.ld of lane quarter (warp % 4) x column half (warp / 4), bias,
 //                softplus, encoder / skip addend, residual, NHWC (or complex-planar) stores
-//   warps 8-15   A converters: input row chunks (RW pixels x 16 channels, fp32, L2-prefetched)
-//                -> exact bf16x3 split -> A ring (UMMA K-major interleaved layout, 16 B pixel pitch,
-//                so the A operand of tap kx is the staged row with its start address moved by kx);
-//                the next row's global loads are in flight while the current row is split
+//   warps 8-15   A converters: raw fp32 row chunks (RW pixels x 16 channels) -> exact bf16x3 split
+//                -> A ring (UMMA K-major interleaved layout, 16 B pixel pitch, so the A operand of tap
+//                kx is the staged row with its start address moved by kx)
 //   warp 16      B producer: one cp.async.bulk per weight piece into the B ring (mbarrier tx-count)
-//   warp 17      MMA issuer (one elected lane issues tcgen05.mma; commits release ring slots and
+//   warp 17      A producer: one TMA tensor load (cp.async.bulk.tensor.4d, box 16 ch x 130 px of the
+//                NHWC activation, zero-filled outside the image) per row chunk into a raw ring
+//   warp 18      MMA issuer (one elected lane issues tcgen05.mma; commits release ring slots and
 //                hand the accumulators to the epilogue)
 // The weights are split once into bf16x3 pieces laid out exactly like a B ring slot
 // (k_wide_split: at network creation for the network's layers, conv_wide_register; otherwise a
 // stream-ordered temporary per launch).  Every activation element is read from HBM once (the first
 // channel chunk of a pass pulls the pass's input rows into L2 with bulk prefetches, the other chunks
 // hit L2).
+#include <cuda.h>
 #include <cuda_bf16.h>
+#include <cudaTypedefs.h>
 
 #include <cstdio>
 #include <map>
@@ -53,8 +56,26 @@ namespace hs {
 namespace {
 using namespace tc;
 
-constexpr int kWEpi = 8, kWAcv = 8;
-constexpr int kWarpA0 = kWEpi, kWarpB = kWEpi + kWAcv, kWarpMma = kWarpB + 1;
+// measurement-variant switches (tools/_variants only; the product build uses the defaults):
+// HS_WIDE_PROBE bit 1 skips the epilogue's side loads / math / stores, bit 2 the MMAs, bit 4 the
+// A conversion, bit 8 the B pipeline (no weight copies, no B waits); HS_WIDE_G64 = column groups for cout 64 (3, or 2 to double-buffer the accumulators)
+#ifndef HS_WIDE_PROBE
+#define HS_WIDE_PROBE 0
+#endif
+#ifndef HS_WIDE_G64
+#define HS_WIDE_G64 3
+#endif
+#ifndef HS_WIDE_RD_MAX
+#define HS_WIDE_RD_MAX 8
+#endif
+#ifndef HS_WIDE_NAS_EXTRA
+#define HS_WIDE_NAS_EXTRA 4
+#endif
+#ifndef HS_WIDE_ACV
+#define HS_WIDE_ACV 8
+#endif
+constexpr int kWEpi = 8, kWAcv = HS_WIDE_ACV;
+constexpr int kWarpA0 = kWEpi, kWarpB = kWEpi + kWAcv, kWarpAP = kWarpB + 1, kWarpMma = kWarpAP + 1;
 constexpr int kWThreads = 32 * (kWarpMma + 1);
 constexpr size_t kWSmemMax = 232448;
 
@@ -62,7 +83,7 @@ template <int CIN, int COUT, int MODE>
 struct WCfg {
   static constexpr int MT = 128;                     // tile pixels (UMMA M)
   static constexpr int NACC = MODE == 2 ? 2 : 1;     // accumulators per tile (transposed: column parity)
-  static constexpr int G = COUT <= 64 && NACC == 1 ? 3 : 2;  // column groups per accumulator (see above)
+  static constexpr int G = COUT <= 64 && NACC == 1 ? HS_WIDE_G64 : 2;  // column groups per accumulator (see above)
   static constexpr int ACC_COLS = G * COUT;
   // output rows (tiles) per pass: as many as TMEM holds, 4 at most (transposed: an even number)
   static constexpr int R = NACC * ACC_COLS * 4 <= 512 ? 4 : 2;
@@ -75,12 +96,28 @@ struct WCfg {
   static constexpr uint32_t A_SLOT = 6 * A_PLANE;          // 3 parts x 2 halves
   static constexpr uint32_t B_PLANE = (uint32_t)3 * COUT * 16;  // one 8-channel half: rows [W0 | W1 | W2]
   static constexpr uint32_t B_SLOT = 2 * B_PLANE;
-  static constexpr int NBS = 6;                            // B ring slots
   static constexpr int IPT = (2 * RW + 32 * kWAcv - 1) / (32 * kWAcv);  // A items per converter thread
-  static constexpr size_t FIXED = (size_t)NBS * B_SLOT + 1024 + 4 * COUT;  // + barriers, bias
+  // B ring: the bulk copies of the weight pieces are latency-bound (a few KB each from L2), so the
+  // ring is made as deep as shared memory allows once the A ring has NROWS + 3 slots (16 at most)
+  // raw fp32 ring filled by the A producer's TMA loads: one slot = NLOAD boxes of 130 pixels x 16
+  // channels (64 B per pixel; stride 2 needs 257 pixels, two boxes)
+  static constexpr int BOXW = 130, NLOAD = MODE == 1 ? 2 : 1;
+  static constexpr size_t RAW_SLOT = (size_t)NLOAD * BOXW * 64;  // a multiple of 128 (TMA destination)
+  // B ring slots (measured: a deeper ring is slower, the weight copies are not the limiter); the
+  // stride-2 layers' 257-pixel rows need the space
+  static constexpr int NBS = MODE == 1 ? 4 : 6;
+  static constexpr int pick_rd() {
+    for (int n = HS_WIDE_RD_MAX; n > 2; --n)
+      if (1024 + (size_t)n * RAW_SLOT + (size_t)NBS * B_SLOT + (size_t)(NROWS + 2) * A_SLOT <= kWSmemMax) return n;
+    return 2;
+  }
+  static constexpr int RD = pick_rd();
+  static constexpr size_t BASE = 1024 + RD * RAW_SLOT;  // raw ring, barriers (512 B), bias (<= 512 B)
+  static constexpr size_t FIXED = BASE + (size_t)NBS * B_SLOT;
   static constexpr int pick_nas() {
-    for (int n = NROWS + 4; n > NROWS; --n)
+    for (int n = NROWS + HS_WIDE_NAS_EXTRA; n > NROWS; --n)
       if (FIXED + (size_t)n * A_SLOT <= kWSmemMax) return n;
+    // (stride 2: the 257-pixel rows leave room for NROWS + 1 slots at most)
     return NROWS;
   }
   static constexpr int NAS = pick_nas();                   // A ring slots (>= rows of one chunk)
@@ -89,6 +126,7 @@ struct WCfg {
   static_assert(NSETS * SET_COLS <= 512, "TMEM");
   static_assert(TOTAL <= kWSmemMax, "shared memory");
   static_assert(CIN % 16 == 0 && COUT % 32 == 0 && COUT <= 256, "shapes");
+  static_assert(RAW_SLOT % 128 == 0 && RW <= NLOAD * BOXW, "raw ring");
 };
 
 struct WArgs {
@@ -173,12 +211,14 @@ HS_DEV int last_ky(int i) {
 }
 
 template <int CIN, int COUT, int MODE>
-__global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(WArgs a) {
+__global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(const __grid_constant__ WArgs a,
+                                                             const __grid_constant__ CUtensorMap tmx) {
   using C = WCfg<CIN, COUT, MODE>;
-  constexpr int R = C::R, NCH = C::NCH, NAS = C::NAS, NBS = C::NBS, NROWS = C::NROWS;
-  extern __shared__ __align__(128) unsigned char smem[];
-  unsigned char* bring = smem;
-  unsigned char* aring = smem + (size_t)NBS * C::B_SLOT;
+  constexpr int R = C::R, NCH = C::NCH, NAS = C::NAS, NBS = C::NBS, NROWS = C::NROWS, RD = C::RD;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* araw = smem;  // TMA destinations first: 128-byte aligned
+  unsigned char* bring = araw + (size_t)RD * C::RAW_SLOT;
+  unsigned char* aring = bring + (size_t)NBS * C::B_SLOT;
   uint64_t* bars = reinterpret_cast<uint64_t*>(aring + (size_t)NAS * C::A_SLOT);
   uint64_t* a_full = bars;
   uint64_t* a_empty = a_full + NAS;
@@ -186,8 +226,10 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(WArgs a) {
   uint64_t* b_empty = b_full + NBS;
   uint64_t* acc_full = b_empty + NBS;
   uint64_t* acc_empty = acc_full + 2;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  float* s_bias = reinterpret_cast<float*>(smem + (size_t)NBS * C::B_SLOT + (size_t)NAS * C::A_SLOT + 512);
+  uint64_t* raw_full = acc_empty + 2;
+  uint64_t* raw_empty = raw_full + RD;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(raw_empty + RD);
+  float* s_bias = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(bars) + 512);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long npass = num_passes<MODE, C>(a);
 
@@ -200,6 +242,10 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(WArgs a) {
     for (int i = 0; i < NBS; ++i) {
       mbar_init(smem_u32(&b_full[i]), 1);
       mbar_init(smem_u32(&b_empty[i]), 1);
+    }
+    for (int i = 0; i < RD; ++i) {
+      mbar_init(smem_u32(&raw_full[i]), 1);
+      mbar_init(smem_u32(&raw_empty[i]), kWAcv);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&acc_full[i]), 1);
@@ -220,101 +266,93 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(WArgs a) {
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
-  if (warp >= kWarpA0 && warp < kWarpA0 + kWAcv) {
-    // ================= A converters: input row chunks -> bf16x3 A ring.  Item e of a row is (pixel
+  auto pass_of = [&](long long& u, Pass& P) {  // first active pass at or after u
+    while (u < npass && !pass_at<MODE, C>(a, u, P)) u += gridDim.x;
+    return u < npass;
+  };
+  if (warp == kWarpAP) {
+    // ================= A producer: TMA row-chunk loads (pass, chunk, row) into the raw ring
+    if (lane == 0) {
+      uint32_t seq = 0;
+      Pass P;
+      for (long long u = blockIdx.x; pass_of(u, P); u += gridDim.x) {
+        const int g0 = first_row<MODE>(P.oy0), x0 = first_col<MODE>(P.xb);
+        {  // all channels of the pass's input rows and its side-input rows into L2: later chunks hit L2
+          const int clo = max(x0, 0), chi = min(x0 + C::RW, a.W);
+          const float* img = a.x + (size_t)P.b * a.H * a.W * CIN;
+          for (int r = 0; r < NROWS; ++r) {
+            const int g = g0 + r;
+            if (g >= 0 && g < a.H && chi > clo)
+              prefetch_l2(img + ((size_t)g * a.W + clo) * CIN, (uint32_t)(chi - clo) * CIN * 4);
+          }
+          const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[P.b] : 0) : P.b) *
+                                                       a.addend_bstride
+                                      : nullptr;
+          constexpr int OXN = MODE == 2 ? 256 : 128;  // output columns of a tile
+          for (int r = 0; r < R && P.oy0 + r < a.Ho; ++r) {
+            const size_t pix = (size_t)(P.oy0 + r) * a.Wo + (size_t)OXN * P.xb;
+            if (add) prefetch_l2(add + pix * COUT, OXN * COUT * 4);
+            if (a.residual) prefetch_l2(a.residual + ((size_t)P.b * a.Ho * a.Wo + pix) * COUT, OXN * COUT * 4);
+          }
+        }
+        for (int c = 0; c < NCH; ++c)
+          for (int i = 0; i < NROWS; ++i, ++seq) {
+            const uint32_t s = seq % RD, use = seq / RD;
+            if (use > 0) mbar_wait(smem_u32(&raw_empty[s]), (use - 1) & 1);
+            const uint32_t bar = smem_u32(&raw_full[s]);
+            mbar_arrive_tx(bar, (uint32_t)C::RAW_SLOT);
+#pragma unroll
+            for (int l = 0; l < C::NLOAD; ++l)  // coordinates (channel, column, row, RHS); outside -> zeros
+              asm volatile(
+                  "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+                  "%4, %5}], [%6];" ::"r"(smem_u32(araw + (size_t)s * C::RAW_SLOT + (size_t)l * C::BOXW * 64)),
+                  "l"(reinterpret_cast<uint64_t>(&tmx)), "r"(16 * c), "r"(x0 + l * C::BOXW), "r"(g0 + i), "r"(P.b),
+                  "r"(bar)
+                  : "memory");
+          }
+      }
+    }
+  } else if (warp >= kWarpA0 && warp < kWarpA0 + kWAcv) {
+    // ================= A converters: raw row chunks -> bf16x3 A ring.  Item e of a row is (pixel
     // e % RW, channel half e / RW): pixel fastest, so the 16-byte smem stores of a warp are contiguous.
     const int t = tid - 32 * kWarpA0;
     constexpr int NT = 32 * kWAcv, IPT = C::IPT;
     uint32_t seq = 0;
-    float4 cur[IPT][2], nxt[IPT][2];
-    // issue the global loads of one row chunk (zero outside the image)
-    auto load_row = [&](const float* img, int g, int x0, int c, float4 (&v)[IPT][2]) {
-      const bool row_ok = g >= 0 && g < a.H;
-      const float* src = img + (size_t)(row_ok ? g : 0) * a.W * CIN + 16 * c;
+    Pass P;
+    for (long long u = blockIdx.x; pass_of(u, P); u += gridDim.x)
+      for (int c = 0; c < NCH; ++c)
+        for (int i = 0; i < NROWS; ++i, ++seq) {
+          const uint32_t rs = seq % RD;
+          mbar_wait(smem_u32(&raw_full[rs]), (seq / RD) & 1);
+          const uint32_t s = seq % NAS, use = seq / NAS;
+          if (use > 0) mbar_wait(smem_u32(&a_empty[s]), (use - 1) & 1);
+          unsigned char* slot = aring + (size_t)s * C::A_SLOT;
+          const unsigned char* raw = araw + (size_t)rs * C::RAW_SLOT;
 #pragma unroll
-      for (int k = 0; k < IPT; ++k) {
-        const int e = t + k * NT, p = e % C::RW, h = e / C::RW, col = x0 + p;
-        v[k][0] = v[k][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (e < 2 * C::RW && row_ok && col >= 0 && col < a.W) {
-          const float4* s4 = reinterpret_cast<const float4*>(src + (size_t)col * CIN + 8 * h);
-          v[k][0] = __ldg(s4);
-          v[k][1] = __ldg(s4 + 1);
+          for (int k = 0; k < ((HS_WIDE_PROBE & 4) ? 0 : IPT); ++k) {
+            const int e = t + k * NT;
+            if (e >= 2 * C::RW) break;
+            const int p = e % C::RW, h = e / C::RW;
+            const float4 v0 = *reinterpret_cast<const float4*>(raw + (size_t)p * 64 + h * 32);
+            const float4 v1 = *reinterpret_cast<const float4*>(raw + (size_t)p * 64 + h * 32 + 16);
+            const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+            uint4 q0, q1, q2;
+            split_bf16x3(v, q0, q1, q2);
+            const size_t off = (size_t)h * C::A_PLANE + (size_t)staged<MODE>(p) * 16;
+            *reinterpret_cast<uint4*>(slot + off) = q0;
+            *reinterpret_cast<uint4*>(slot + 2 * C::A_PLANE + off) = q1;
+            *reinterpret_cast<uint4*>(slot + 4 * C::A_PLANE + off) = q2;
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(smem_u32(&a_full[s]));
+            mbar_arrive(smem_u32(&raw_empty[rs]));
+          }
         }
-      }
-    };
-    // the (pass, chunk, row) sequence this CTA converts, walked one step ahead for the loads
-    long long u = blockIdx.x;
-    Pass P{};
-    auto next_pass = [&]() {
-      while (u < npass && !pass_at<MODE, C>(a, u, P)) u += gridDim.x;
-      return u < npass;
-    };
-    bool have = next_pass();
-    int c = 0, i = 0;
-    auto prefetch_pass = [&]() {  // pull the pass's input rows (all channels) and side-input rows into L2
-      const int g0 = first_row<MODE>(P.oy0), x0 = first_col<MODE>(P.xb);
-      const int clo = max(x0, 0), chi = min(x0 + C::RW, a.W);
-      const float* img = a.x + (size_t)P.b * a.H * a.W * CIN;
-      for (int r = 0; r < NROWS; ++r) {
-        const int g = g0 + r;
-        if (g >= 0 && g < a.H && chi > clo)
-          prefetch_l2(img + ((size_t)g * a.W + clo) * CIN, (uint32_t)(chi - clo) * CIN * 4);
-      }
-      const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[P.b] : 0) : P.b) *
-                                                   a.addend_bstride
-                                  : nullptr;
-      constexpr int OXN = MODE == 2 ? 256 : 128;  // output columns of a tile
-      for (int r = 0; r < R && P.oy0 + r < a.Ho; ++r) {
-        const size_t pix = (size_t)(P.oy0 + r) * a.Wo + (size_t)OXN * P.xb;
-        if (add) prefetch_l2(add + pix * COUT, OXN * COUT * 4);
-        if (a.residual) prefetch_l2(a.residual + ((size_t)P.b * a.Ho * a.Wo + pix) * COUT, OXN * COUT * 4);
-      }
-    };
-    if (have) {
-      if (t == 0) prefetch_pass();
-      load_row(a.x + (size_t)P.b * a.H * a.W * CIN, first_row<MODE>(P.oy0) + i, first_col<MODE>(P.xb), c, nxt);
-    }
-    while (have) {
-#pragma unroll
-      for (int k = 0; k < IPT; ++k) cur[k][0] = nxt[k][0], cur[k][1] = nxt[k][1];
-      // advance (pass, chunk, row) and put the next row's loads in flight
-      if (++i == NROWS) {
-        i = 0;
-        if (++c == NCH) {
-          c = 0;
-          u += gridDim.x;
-          have = next_pass();
-          if (have && t == 0) prefetch_pass();
-        }
-      }
-      if (have)
-        load_row(a.x + (size_t)P.b * a.H * a.W * CIN, first_row<MODE>(P.oy0) + i, first_col<MODE>(P.xb), c, nxt);
-      // convert the current row into its ring slot
-      const uint32_t s = seq % NAS, use = seq / NAS;
-      if (use > 0) mbar_wait(smem_u32(&a_empty[s]), (use - 1) & 1);
-      unsigned char* slot = aring + (size_t)s * C::A_SLOT;
-#pragma unroll
-      for (int k = 0; k < IPT; ++k) {
-        const int e = t + k * NT;
-        if (e >= 2 * C::RW) break;
-        const int p = e % C::RW, h = e / C::RW;
-        const float v[8] = {cur[k][0].x, cur[k][0].y, cur[k][0].z, cur[k][0].w,
-                            cur[k][1].x, cur[k][1].y, cur[k][1].z, cur[k][1].w};
-        uint4 q0, q1, q2;
-        split_bf16x3(v, q0, q1, q2);
-        const size_t off = (size_t)h * C::A_PLANE + (size_t)staged<MODE>(p) * 16;
-        *reinterpret_cast<uint4*>(slot + off) = q0;
-        *reinterpret_cast<uint4*>(slot + 2 * C::A_PLANE + off) = q1;
-        *reinterpret_cast<uint4*>(slot + 4 * C::A_PLANE + off) = q2;
-      }
-      fence_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&a_full[s]));
-      ++seq;
-    }
   } else if (warp == kWarpB) {
     // ================= B producer: pre-split weight pieces (c, ky, kx), one bulk copy each, in MMA order
-    if (lane == 0) {
+    if (lane == 0 && !(HS_WIDE_PROBE & 8)) {
       uint32_t seq = 0;
       for (long long u = blockIdx.x; u < npass; u += gridDim.x) {
         Pass P;
@@ -347,7 +385,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(WArgs a) {
         for (int ky = 0; ky < 3; ++ky) {
           for (int kx = 0; kx < 3; ++kx, ++bseq) {
             const uint32_t bs = bseq % NBS;
-            mbar_wait(smem_u32(&b_full[bs]), (bseq / NBS) & 1);
+            if (!(HS_WIDE_PROBE & 8)) mbar_wait(smem_u32(&b_full[bs]), (bseq / NBS) & 1);
             const uint32_t bsl = b_base + bs * C::B_SLOT;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -366,7 +404,8 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(WArgs a) {
                              a2 = desc_lo(asl + 4 * C::A_PLANE, C::A_PLANE);
               const uint32_t w0 = desc_lo(bsl, C::B_PLANE), w1 = desc_lo(bsl + WROW, C::B_PLANE),
                              w2 = desc_lo(bsl + 2 * WROW, C::B_PLANE);
-              if constexpr (C::G == 3) {
+              if constexpr ((HS_WIDE_PROBE & 2) != 0) {
+              } else if constexpr (C::G == 3) {
                 mma_bf16(d, a0, kDescHi, w0, kDescHi, I3, (started & bit) ? 1u : 0u);  // g0 g1 g2 += a0 [w0 w1 w2]
                 mma_bf16(d + COUT, a1, kDescHi, w0, kDescHi, I2, 1u);                  // g1 g2 += a1 [w0 w1]
                 mma_bf16(d + 2 * COUT, a2, kDescHi, w0, kDescHi, I1, 1u);              // g2 += a2 w0
@@ -379,7 +418,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(WArgs a) {
               }
               started |= bit;
             }
-            mma_commit(smem_u32(&b_empty[bs]));  // the piece is free once these MMAs completed
+            if (!(HS_WIDE_PROBE & 8)) mma_commit(smem_u32(&b_empty[bs]));  // the piece is free once its MMAs completed
           }
           // input rows whose last reader was this tap row go back to the converters
           for (int i = 0; i < NROWS; ++i)
@@ -432,6 +471,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(WArgs a) {
           for (int q = 0; q < SEG / 4; ++q) dst[q] = __ldg(sp + q);
         }
       };
+      if (HS_WIDE_PROBE & 1) side = nullptr;  // probe build only
       load_side(0, 0, 0, sn);
       for (int step = 0; step < R * C::NACC * NSEG; ++step) {
         const int sg = step % NSEG, k = (step / NSEG) % C::NACC, r = step / (NSEG * C::NACC);
@@ -463,7 +503,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(WArgs a) {
             o[n0 + j] = x;
           }
         }
-        if (oy >= a.Ho) continue;  // (warp-uniform: every lane of the warp has the same row)
+        if (oy >= a.Ho || (HS_WIDE_PROBE & 1)) continue;  // (warp-uniform: every lane has the same row)
 #pragma unroll
         for (int q = 0; q < SEG / 4; ++q) {
           o[4 * q] += sd[q].x, o[4 * q + 1] += sd[q].y, o[4 * q + 2] += sd[q].z, o[4 * q + 3] += sd[q].w;
@@ -538,8 +578,29 @@ cudaError_t run_split(const float* w, int cin, int cout, void* out, cudaStream_t
 std::mutex reg_mu;
 std::map<const float*, void*> reg;
 
+// TMA descriptor of the NHWC activation x: 4-D (channel, column, row, RHS), box 16 channels x 130
+// columns x 1 x 1, fp32, zero fill outside the tensor (the convolution's padding and halo)
+bool make_tmap(CUtensorMap* tm, const float* x, int cin, int H, int W, int B) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[4] = {(cuuint64_t)cin, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
+  const cuuint64_t strides[3] = {(cuuint64_t)cin * 4, (cuuint64_t)W * cin * 4, (cuuint64_t)H * W * cin * 4};
+  const cuuint32_t box[4] = {16, 130, 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int CIN, int COUT, int MODE>
-void launch_wide(const WArgs& a, cudaStream_t st) {
+void launch_wide(const WArgs& a, const CUtensorMap& tm, cudaStream_t st) {
   using C = WCfg<CIN, COUT, MODE>;
   static int sms = 0;
   if (!sms) {
@@ -561,7 +622,7 @@ void launch_wide(const WArgs& a, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_conv_wide<CIN, COUT, MODE>, a);
+  cudaLaunchKernelEx(&cfg, k_conv_wide<CIN, COUT, MODE>, a, tm);
 }
 
 }  // namespace
@@ -623,12 +684,17 @@ bool conv_wide_launch(const float* x, int H, int W, int cin, float* y, int Ho, i
   }
   WArgs a{static_cast<const unsigned char*>(split), x, H, W, y, Ho, Wo, w, bias, softplus, addend, addend_bstride,
           addend_per_model, model_of, residual, active, B, planar};
+  CUtensorMap tm;
+  if (!make_tmap(&tm, x, cin, H, W, B)) {
+    if (tmp) cudaFreeAsync(tmp, st);
+    return false;
+  }
   const int mode = transposed ? 2 : (stride == 2 ? 1 : 0);
-  if (mode == 0 && cin == 64) launch_wide<64, 64, 0>(a, st);
-  else if (mode == 0 && cin == 128) launch_wide<128, 128, 0>(a, st);
-  else if (mode == 1 && cin == 64) launch_wide<64, 128, 1>(a, st);
-  else if (mode == 1 && cin == 128) launch_wide<128, 128, 1>(a, st);
-  else if (mode == 2 && cout == 64) launch_wide<128, 64, 2>(a, st);
+  if (mode == 0 && cin == 64) launch_wide<64, 64, 0>(a, tm, st);
+  else if (mode == 0 && cin == 128) launch_wide<128, 128, 0>(a, tm, st);
+  else if (mode == 1 && cin == 64) launch_wide<64, 128, 1>(a, tm, st);
+  else if (mode == 1 && cin == 128) launch_wide<128, 128, 1>(a, tm, st);
+  else if (mode == 2 && cout == 64) launch_wide<128, 64, 2>(a, tm, st);
   if (tmp) cudaFreeAsync(tmp, st);
   return true;
 }

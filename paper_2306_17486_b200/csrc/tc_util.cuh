@@ -7,6 +7,10 @@
 
 #include "common.cuh"
 
+#ifndef HS_MBAR_SUSPEND_NS
+#define HS_MBAR_SUSPEND_NS 20000
+#endif
+
 namespace hs {
 namespace tc {
 
@@ -52,7 +56,7 @@ HS_DEV void mbar_wait(uint32_t mbar, uint32_t phase) {
       "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}\n" ::"r"(mbar),
-      "r"(phase), "n"(20000));  // suspend-time hint (ns): waiting warps sleep instead of spinning
+      "r"(phase), "n"(HS_MBAR_SUSPEND_NS));  // suspend-time hint (ns): waiting warps sleep instead of spinning
 }
 
 HS_DEV void mbar_arrive(uint32_t mbar) {
