@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
     }
     for (int i = 0; i < C::NA; ++i) {
       mbar_init(smem_u32(&acc_full[i]), 1);
-      mbar_init(smem_u32(&acc_empty[i]), kEpiWarps);  // one arrival per epilogue warp
+      mbar_init(smem_u32(&acc_empty[i]), C::ATM ? kEpiWarps / 2 : kEpiWarps);  // one arrival per draining warp
     }
     for (int i = 0; i < C::NSA; ++i) {
       mbar_init(smem_u32(&a_full[i]), C::NCVT_BASE);
@@ -684,6 +684,111 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
       }
     }
   } else {
+    if constexpr (C::ATM) {
+      // ================= epilogue of the 16-channel stride-1 layers: warp group hg = warp / 4 drains
+      // the tiles with tile % 2 == hg (TMEM accumulator hg), all 16 channels of its lane quarter's 32
+      // pixels.  A 4x4 transpose of 16-byte chunks inside each group of four lanes (shuffles) makes
+      // every store instruction write whole 64-byte pixels (two full sectors each): the per-lane
+      // layout wrote half sectors, which measured 0.38 ms of a 1.73 ms C3 level-0 conv.
+      static_assert(CS == 16 && COUT == 16 && C::NACC == 1 && C::NA == 2, "tile-split epilogue");
+      const int q4 = warp & 3, hg = warp >> 2;
+      const int m = q4 * 32 + lane;
+      const int gi = lane & 3;  // position inside the group of four lanes
+      long long tile = 0;
+      for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
+        Unit U;
+        if (!unit_at<MODE, MT>(a, NSPLIT, u, U)) continue;
+        const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[U.b] : 0) : U.b) *
+                                                     a.addend_bstride
+                                    : nullptr;
+        for (int oy = U.oy0; oy < U.oy1; ++oy, ++tile) {
+          if ((int)(tile & 1) != hg) continue;
+          const int acc = hg;
+          const size_t pix = (size_t)oy * a.Wo + (size_t)U.xb * MT + m;
+          // side inputs of this pixel (16 channels), requested before the accumulator wait
+          float4 sd[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) sd[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (add && !(kProbe & 256)) {
+            const float4* ap = reinterpret_cast<const float4*>(add + pix * COUT);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) sd[q] = __ldg(ap + q);
+          }
+          if (a.residual) {
+            const float4* rp = reinterpret_cast<const float4*>(a.residual + ((size_t)U.b * a.Ho * a.Wo + pix) * COUT);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 r = __ldg(rp + q);
+              const uint64_t s01 = add2(pkf(sd[q].x, sd[q].y), pkf(r.x, r.y)), s23 = add2(pkf(sd[q].z, sd[q].w), pkf(r.z, r.w));
+              sd[q] = make_float4(lo_f(s01), hi_f(s01), lo_f(s23), hi_f(s23));
+            }
+          }
+          mbar_wait(smem_u32(&acc_full[acc]), (uint32_t)((tile / C::NA) & 1));
+          tc_fence_after();
+          float o[16];
+#pragma unroll
+          for (int n0 = 0; n0 < 16; n0 += 8) {
+            uint32_t r0[8], r1[8], r2[8];
+            const uint32_t col = tmem + ((uint32_t)(q4 * 32) << 16) + acc * C::ACOLS + n0;
+            tmem_ld8(col, r0);
+            tmem_ld8(col + CS, r1);
+            tmem_ld8(col + 2 * CS, r2);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 8; j += 2) {  // (x0 + x1) + x2 partial sums, channel pairs packed (FADD2)
+              const uint64_t sm = add2(add2(pk2(r0[j], r0[j + 1]), pk2(r1[j], r1[j + 1])), pk2(r2[j], r2[j + 1]));
+              o[n0 + j] = __uint_as_float((uint32_t)sm);
+              o[n0 + j + 1] = __uint_as_float((uint32_t)(sm >> 32));
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&acc_empty[acc]));  // TMEM free; finish from registers
+          if (kProbe & 4) continue;
+          float4 ch[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 bs = *reinterpret_cast<const float4*>(s_bias + 4 * q);
+            const uint64_t o01 = add2(pkf(o[4 * q], o[4 * q + 1]), pkf(bs.x, bs.y));
+            const uint64_t o23 = add2(pkf(o[4 * q + 2], o[4 * q + 3]), pkf(bs.z, bs.w));
+            float4 v = make_float4(lo_f(o01), hi_f(o01), lo_f(o23), hi_f(o23));
+            if (a.softplus) {
+              v.x = softplus_fast(v.x);
+              v.y = softplus_fast(v.y);
+              v.z = softplus_fast(v.z);
+              v.w = softplus_fast(v.w);
+            }
+            const uint64_t q01 = add2(pkf(v.x, v.y), pkf(sd[q].x, sd[q].y));
+            const uint64_t q23 = add2(pkf(v.z, v.w), pkf(sd[q].z, sd[q].w));
+            ch[q] = make_float4(lo_f(q01), hi_f(q01), lo_f(q23), hi_f(q23));
+          }
+          // 4x4 transpose inside the group: lane gi ends up with chunk gi of the group's four pixels
+          // (xor partner gi ^ k sends its chunk gi and receives ours for its position)
+#pragma unroll
+          for (int k = 1; k < 4; ++k) {
+            const int want = gi ^ k;
+            float4 send = ch[0];
+#pragma unroll
+            for (int q = 1; q < 4; ++q)
+              if (q == want) send = ch[q];
+            float4 got;
+            got.x = __shfl_xor_sync(0xffffffffu, send.x, k);
+            got.y = __shfl_xor_sync(0xffffffffu, send.y, k);
+            got.z = __shfl_xor_sync(0xffffffffu, send.z, k);
+            got.w = __shfl_xor_sync(0xffffffffu, send.w, k);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (q == want) ch[q] = got;
+          }
+          // now ch[j] holds chunk gi of pixel (lane & ~3) + j: store j writes whole pixels
+          if (!(kProbe & 64)) {
+            float4* yb = reinterpret_cast<float4*>(a.y + ((size_t)U.b * a.Ho * a.Wo + pix - lane + (lane & ~3)) * COUT);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) yb[j * 4 + gi] = ch[j];  // pixel j of the group, chunk gi
+          }
+        }
+      }
+    } else {
     // ================= epilogue warps 0-7: TMEM lane quarter q = warp % 4 (the
     // only lanes a warp may read), channel half h = warp / 4 of the slice.
     // M = 128: tile row m = TMEM lane m.  M = 64: rows 16q..16q+15 sit in the
@@ -803,6 +908,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
             if constexpr (SPLIT) pre_r[k][q] = nxt_r[k][q];
           }
       }
+    }
     }
   }
   tc_fence_before();
