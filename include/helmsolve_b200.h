@@ -208,6 +208,9 @@ HS_API int hs_net_forward(const hs_net_t* net, const void* r, void* u0, const in
 /* green.green_function (green.py:55-82): kernel complex64 (C, 3, 3) ->
  * spectrum complex128 (C, 2h, 2w), the reference's numpy-2 dtype flow. */
 HS_API int hs_green_spectrum(const void* kernel, int C, int h, int w, void* spectrum, void* stream);
+/* the same with the regulariser as an argument (green.py:55, green_function(..., eps=SPECTRUM_EPS));
+ * hs_green_spectrum is this with eps = 1e-5 (green.py:19) */
+HS_API int hs_green_spectrum_eps(const void* kernel, int C, int h, int w, double eps, void* spectrum, void* stream);
 /* green.implicit_apply (green.py:85-107): x complex64 (B, C, h, w),
  * spectrum complex64 (C, 2h, 2w) -> y complex64 (B, C, h, w). */
 HS_API int hs_implicit_apply(const void* x, const void* spectrum, void* y, int B, int C, int h, int w,

@@ -138,6 +138,7 @@ SIGNATURES = {
     "hs_net_workspace_bytes": (_SZ, [_VP, _I]),
     "hs_net_forward": (_I, [_VP, _VP, _VP, _VP, _I, _VP, _SZ, _VP]),
     "hs_green_spectrum": (_I, [_VP, _I, _I, _I, _VP, _VP]),
+    "hs_green_spectrum_eps": (_I, [_VP, _I, _I, _I, ctypes.c_double, _VP, _VP]),
     "hs_implicit_apply": (_I, [_VP, _VP, _VP, _I, _I, _I, _I, _VP]),
     "hs_conv2d": (_I, [_VP, ctypes.POINTER(HsConv), _VP, _VP, _VP, _I, _I, _I, _VP]),
     "hs_profile_enable": (None, [ctypes.c_uint]),

@@ -1061,7 +1061,8 @@ size_t cnn_workspace_bytes(const hs_net_t* net, int B) {
   return fwd_layout(net->d, B, net->spec_perm != nullptr).total;
 }
 
-static int green_spectrum_c128(const float2* kern, int C, int h, int w, cufftDoubleComplex* out, cudaStream_t st) {
+static int green_spectrum_c128(const float2* kern, int C, int h, int w, cufftDoubleComplex* out, cudaStream_t st,
+                               double eps = 1e-5) {
   const int gh = 2 * h, gw = 2 * w, bh = 3 * gh, bw = 3 * gw;
   cufftDoubleComplex* big = nullptr;
   const long long nb = (long long)C * bh * bw;
@@ -1078,7 +1079,7 @@ static int green_spectrum_c128(const float2* kern, int C, int h, int w, cufftDou
     cufftSetStream(p2, st);
     k_green_embed<<<grid1(nb), 256, 0, st>>>(kern, big, C, bh, bw);
     cufftExecZ2Z(p1, big, big, CUFFT_FORWARD);
-    k_green_divide<<<grid1(nb), 256, 0, st>>>(big, nb, bh, bw, 1e-5);
+    k_green_divide<<<grid1(nb), 256, 0, st>>>(big, nb, bh, bw, eps);
     cufftExecZ2Z(p1, big, big, CUFFT_INVERSE);
     k_green_crop_shift<<<grid1((long long)C * gh * gw), 256, 0, st>>>(big, out, C, bh, bw, gh, gw);
     cufftExecZ2Z(p2, out, out, CUFFT_FORWARD);
@@ -1373,9 +1374,14 @@ HS_API int hs_net_forward(const hs_net_t* net, const void* r, void* u0, const in
 }
 
 HS_API int hs_green_spectrum(const void* kernel, int C, int h, int w, void* spectrum, void* stream) {
+  return hs_green_spectrum_eps(kernel, C, h, w, 1e-5, spectrum, stream);
+}
+
+HS_API int hs_green_spectrum_eps(const void* kernel, int C, int h, int w, double eps, void* spectrum, void* stream) {
   if (h < 3 || w < 3) return cfail(HS_EDIMENSION, "coarse size too small");
+  if (!(eps >= 0.0)) return cfail(HS_ECONFIG, "eps must be >= 0");
   int rc = hs::green_spectrum_c128(static_cast<const float2*>(kernel), C, h, w,
-                                   static_cast<cufftDoubleComplex*>(spectrum), (cudaStream_t)stream);
+                                   static_cast<cufftDoubleComplex*>(spectrum), (cudaStream_t)stream, eps);
   return rc == HS_OK ? ccheck("hs_green_spectrum") : cfail(rc, "cufft");
 }
 

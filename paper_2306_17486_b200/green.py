@@ -48,19 +48,17 @@ def green_function(kernel, coarse_size: tuple[int, int], eps: float = SPECTRUM_E
     from . import _lib
     from .device import stream_handle, to_device
 
-    if eps != SPECTRUM_EPS:
-        raise NotImplementedError("the device Green spectrum is built with SPECTRUM_EPS")
     h, w = coarse_size
     if h < 3 or w < 3:
         raise DimensionError(f"coarse size {coarse_size} too small")
-    k = np.asarray(kernel)
+    k = np.asarray(kernel.data if isinstance(kernel, KernelWeights) else kernel)
     if k.shape[-2:] != (3, 3):
         raise DimensionError(f"kernel must be 3x3 per channel, got {k.shape}")
     squeeze = k.ndim == 2
     kd = to_device(k.reshape(-1, 3, 3), torch.complex64)
     C = kd.shape[0]
     out = torch.empty((C, 2 * h, 2 * w), dtype=torch.complex128, device=kd.device)
-    _lib.check(_lib.load().hs_green_spectrum(kd.data_ptr(), C, h, w, out.data_ptr(), stream_handle()),
+    _lib.check(_lib.load().hs_green_spectrum_eps(kd.data_ptr(), C, h, w, float(eps), out.data_ptr(), stream_handle()),
                "green_function")
     res = out.cpu().numpy()
     return res[0] if squeeze else res
@@ -105,18 +103,47 @@ def circular_conv(kernel, x):
     return out.cpu().numpy()
 
 
+class KernelWeights:
+    """The implicit kernels as a versioned array: the part of the reference's autodiff ``Tensor``
+    that ``ImplicitKernel`` relies on (``.data``, ``.version``, ``.bump_version()``; autodiff.py's
+    Tensor, used at green.py:131, 139-146).  Change ``data`` in place, then ``bump_version()``."""
+
+    def __init__(self, data):
+        self.data = np.asarray(data)
+        self.version = 0
+
+    def bump_version(self):
+        self.version += 1
+
+    @property
+    def shape(self):
+        return self.data.shape
+
+    @property
+    def dtype(self):
+        return self.data.dtype
+
+    def __array__(self, dtype=None, copy=None):
+        return self.data if dtype is None else self.data.astype(dtype)
+
+    def __getitem__(self, idx):
+        return self.data[idx]
+
+    def __setitem__(self, idx, value):
+        self.data[idx] = value
+
+
 class ImplicitKernel:
     """Per-channel 3x3 complex kernels with a cached spectrum (green.py:120-149).
 
-    The cache is keyed on (size, weights version); call ``bump_version`` after
-    changing ``weights`` in place.
+    The cache is keyed on (size, weights.version) like the reference's; call
+    ``weights.bump_version()`` (or ``bump_version()`` here) after changing the weights in place.
     """
 
     def __init__(self, channels: int, dtype=np.complex64, weights=None):
         if weights is None:
             weights = laplacian_plus_i_kernel(channels, dtype)
-        self.weights = np.array(weights, dtype=dtype)
-        self.version = 0
+        self.weights = KernelWeights(np.array(weights, dtype=dtype))
         self._cache = None
         self._cache_key = None
 
@@ -124,13 +151,17 @@ class ImplicitKernel:
     def channels(self) -> int:
         return int(self.weights.shape[0])
 
+    @property
+    def version(self) -> int:
+        return self.weights.version
+
     def bump_version(self):
-        self.version += 1
+        self.weights.bump_version()
 
     def spectrum(self, coarse_size: tuple[int, int]) -> np.ndarray:
-        key = (tuple(coarse_size), self.version)
+        key = (tuple(coarse_size), self.weights.version)
         if self._cache_key != key:
-            self._cache = green_function(self.weights, tuple(coarse_size))
+            self._cache = green_function(self.weights.data, tuple(coarse_size))
             self._cache_key = key
         return self._cache
 

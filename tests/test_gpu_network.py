@@ -163,6 +163,25 @@ def test_implicit_kernel_cache():
     k.weights[0, 1, 1] += 0.5
     k.bump_version()
     assert k.spectrum((8, 8)) is not s1
+    # the reference's form (test_green.py:210-220): weights is a versioned tensor, the cache key
+    # (size, weights.version)
+    s2 = k.spectrum((8, 8))
+    k.weights.data[1, 1, 1] += 0.25
+    k.weights.bump_version()
+    assert k._cache_key == ((8, 8), 1)
+    s3 = k.spectrum((8, 8))
+    assert s3 is not s2 and k._cache_key == ((8, 8), 2)
+    assert relerr(s3, no.green_function(k.weights.data, (8, 8))) < 1e-6
+
+
+@pytest.mark.parametrize("eps", [1e-3, 0.0])
+def test_green_function_eps(eps):
+    # green.py:55 green_function(kernel, coarse_size, eps=SPECTRUM_EPS): any regulariser
+    rng = np.random.default_rng(41)
+    kern = (green.laplacian_plus_i_kernel(3) + 0.1 * (rng.standard_normal((3, 3, 3)) +
+                                                      1j * rng.standard_normal((3, 3, 3)))).astype(np.complex64)
+    S = green.green_function(kern, (8, 16), eps=eps)
+    assert relerr(S, no.green_function(kern, (8, 16), eps=eps)) < 1e-6
 
 
 @pytest.mark.parametrize("L", [2, 3])
