@@ -22,6 +22,8 @@
 // c = 32 k1 + l holds frequency k1 + E br5(l)); the spectrum is permuted into
 // the same order once, at network setup.  Twiddles come from a per-CTA table
 // built with sincospif (full fp32 accuracy).
+#include <cooperative_groups.h>
+
 #include <cstdlib>
 
 #include "common.cuh"
@@ -413,6 +415,213 @@ void launch_imp2(const ImpArgs& a, int B, cudaStream_t st) {
   k_implicit2<E><<<dim3((unsigned)a.C, (unsigned)B), Imp2<E>::THREADS, sm, st>>>(a);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Four-step transform on a 2-CTA cluster (rectangular grids, and 128 x 128): the (RHS, channel)
+// pair is split by spectrum COLUMNS between the two CTAs of a cluster, so each CTA keeps only
+// h x (W2 / 2) row spectra in shared memory (the single-CTA kernels keep h x W2, which left 8 warps
+// per SM at C3's 64 x 128 coarsest grid and did not fit 128 x 128 at all).
+//   1. CTA r transforms the rows [r h/2, (r+1) h/2) (four-step, length W2 = 32 EW); each thread's
+//      32 outputs are column frequencies k1 + EW m, written to the owning CTA's shared memory
+//      (distributed shared memory for the partner's half)                       -> cluster barrier
+//   2. each CTA runs forward column FFT, spectrum multiply, inverse column FFT on its W2 / 2 columns
+//      (length H2 = 32 EH, h rows kept), all local                               -> cluster barrier
+//   3. CTA r inverse-transforms its rows, reading the partner's columns through DSMEM, and writes
+//      the w kept outputs                                                         -> cluster barrier
+// The spectrum is used in its natural [C][H2][W2] order, like k_implicit2.
+template <int EW, int EH>
+struct ImpC {
+  static constexpr int THREADS = 128, NWARP = THREADS / 32;
+  static constexpr int W2 = 32 * EW, H2 = 32 * EH, h = H2 / 2, w = W2 / 2;
+  static constexpr int HALF = W2 / 2, LDS = HALF + 1;  // columns per CTA, S row pitch (odd: conflict-free)
+  static constexpr int RL = THREADS / EW, CL = THREADS / EH, TL = 33;
+  static constexpr size_t SMEM = ((size_t)h * LDS + (size_t)THREADS * TL + W2 + H2) * sizeof(float2);
+};
+
+template <int EW, int EH>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ImpC<EW, EH>::THREADS) k_implicit_cl(ImpArgs a) {
+  using G = ImpC<EW, EH>;
+  constexpr int W2 = G::W2, H2 = G::H2, h = G::h, HALF = G::HALF, LDS = G::LDS, RL = G::RL, CL = G::CL,
+                TL = G::TL, NT = G::THREADS, NWP = G::NWARP;
+  constexpr int NZW = EW / 2, NZH = EH / 2;  // non-zero 32-blocks of a padded row / column
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int r = (int)cluster.block_rank();
+  extern __shared__ float2 smem_cl[];
+  float2* S = smem_cl;                      // [h][LDS]: this CTA's HALF spectrum columns, all rows
+  float2* T = S + h * LDS;                  // [E][lines][TL] four-step transpose buffer
+  float2* twW = T + NT * TL;                // W_W2^m
+  float2* twH = twW + W2;                   // W_H2^m
+  float2* Sp[2];
+  Sp[r] = S;
+  Sp[1 - r] = cluster.map_shared_rank(S, 1 - r);
+  const int b = blockIdx.y, k = blockIdx.x >> 1;
+  const bool skip = a.active && a.active[b] == nullptr;  // both CTAs of the pair agree
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int m = threadIdx.x; m < W2; m += NT) {
+    float sn, cs;
+    sincospif(-2.f * m / W2, &sn, &cs);
+    twW[m] = make_float2(cs, sn);
+  }
+  for (int m = threadIdx.x; m < H2; m += NT) {
+    float sn, cs;
+    sincospif(-2.f * m / H2, &sn, &cs);
+    twH[m] = make_float2(cs, sn);
+  }
+  __syncthreads();
+  if (!skip) {
+    const float2* xin = a.x + b * a.xb + k * a.xk;
+    const int row0 = r * (h / 2);
+    // ---- 1. forward row transforms of rows [row0, row0 + h/2)
+    for (int c0 = 0; c0 < h / 2; c0 += RL) {
+      const int nl = min(RL, h / 2 - c0);  // rows of this chunk (RL may exceed the CTA's h / 2 rows)
+      for (int line = warp; line < nl; line += NWP) {  // step (a): E-point DFT over j, twiddle
+        const int row = row0 + c0 + line;
+        float2 q[EW];
+#pragma unroll
+        for (int j = 0; j < EW; ++j)
+          q[j] = j < NZW ? xin[(long long)(row * G::w + lane + 32 * j) * a.xp] : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k1 = 0; k1 < EW; ++k1) {
+          float2 sm = q[0];
+#pragma unroll
+          for (int j = 1; j < NZW; ++j) sm = cadd(sm, mul_wE<EW>(q[j], j * k1));
+          T[(k1 * RL + line) * TL + lane] = k1 == 0 ? sm : cmul(sm, twW[lane * k1]);
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x % RL < nl) {  // step (c): 32-point DFT over l per (k1, line); column f = k1 + EW m
+        const int tk = threadIdx.x / RL, tl = threadIdx.x % RL;
+        float2 v[32];
+#pragma unroll
+        for (int l = 0; l < 32; ++l) v[l] = T[(tk * RL + tl) * TL + l];
+        fft32<false>(v);
+        const int row = row0 + c0 + tl;
+#pragma unroll
+        for (int m = 0; m < 32; ++m) {
+          const int f = tk + EW * m;
+          Sp[f / HALF][row * LDS + f % HALF] = v[m];
+        }
+      }
+      __syncthreads();
+    }
+  }
+  cluster.sync();  // every row spectrum is in its owner's shared memory
+  if (!skip) {
+    // ---- 2. this CTA's columns: forward, spectrum, inverse (rows < h kept)
+    const float2* sp = a.spec + (long long)k * H2 * W2;
+    const int tk = threadIdx.x / CL, tl = threadIdx.x % CL;
+    static_assert(HALF % CL == 0, "column chunks");
+    for (int c0 = 0; c0 < HALF; c0 += CL) {
+      float2 spv[32];  // requested before the barrier
+      {
+        const float2* spc = sp + r * HALF + c0 + tl;
+#pragma unroll
+        for (int m = 0; m < 32; ++m) spv[m] = __ldg(spc + (long long)(tk + EH * m) * W2);
+      }
+      for (int cc = warp; cc < CL; cc += NWP) {
+        float2 q[EH];
+#pragma unroll
+        for (int j = 0; j < EH; ++j) q[j] = j < NZH ? S[(lane + 32 * j) * LDS + c0 + cc] : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k1 = 0; k1 < EH; ++k1) {
+          float2 sm = q[0];
+#pragma unroll
+          for (int j = 1; j < NZH; ++j) sm = cadd(sm, mul_wE<EH>(q[j], j * k1));
+          T[(k1 * CL + cc) * TL + lane] = k1 == 0 ? sm : cmul(sm, twH[lane * k1]);
+        }
+      }
+      __syncthreads();
+      {
+        float2 v[32];
+#pragma unroll
+        for (int l = 0; l < 32; ++l) v[l] = T[(tk * CL + tl) * TL + l];
+        fft32<false>(v);
+#pragma unroll
+        for (int m = 0; m < 32; ++m) v[m] = cmul(v[m], spv[m]);
+        fft32<true>(v);
+#pragma unroll
+        for (int l = 0; l < 32; ++l) T[(tk * CL + tl) * TL + l] = v[l];
+      }
+      __syncthreads();
+      for (int cc = warp; cc < CL; cc += NWP) {  // inverse step (a): rows < h kept
+        float2 y[EH];
+#pragma unroll
+        for (int k1 = 0; k1 < EH; ++k1) {
+          y[k1] = T[(k1 * CL + cc) * TL + lane];
+          if (k1) y[k1] = cmulc(y[k1], twH[lane * k1]);
+        }
+#pragma unroll
+        for (int j = 0; j < NZH; ++j) {
+          float2 sm = y[0];
+#pragma unroll
+          for (int k1 = 1; k1 < EH; ++k1) sm = cadd(sm, mul_wE<EH>(y[k1], (EH - (j * k1) % EH) % EH));
+          S[(lane + 32 * j) * LDS + c0 + cc] = sm;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  cluster.sync();  // both halves of every kept row are final
+  if (!skip) {
+    // ---- 3. inverse row transforms of this CTA's rows, the partner's columns through DSMEM
+    float2* yout = a.y + b * a.yb + k * a.yk;
+    const float inv = 1.f / ((float)H2 * (float)W2);
+    const int row0 = r * (h / 2);
+    const int tk = threadIdx.x / RL, tl = threadIdx.x % RL;
+    for (int c0 = 0; c0 < h / 2; c0 += RL) {
+      const int nl = min(RL, h / 2 - c0);
+      if (tl < nl) {
+        const int row = row0 + c0 + tl;
+        float2 v[32];
+#pragma unroll
+        for (int m = 0; m < 32; ++m) {
+          const int f = tk + EW * m;
+          v[m] = Sp[f / HALF][row * LDS + f % HALF];
+        }
+        fft32<true>(v);
+#pragma unroll
+        for (int l = 0; l < 32; ++l) T[(tk * RL + tl) * TL + l] = v[l];
+      }
+      __syncthreads();
+      for (int line = warp; line < nl; line += NWP) {
+        const int row = row0 + c0 + line;
+        float2 y[EW];
+#pragma unroll
+        for (int k1 = 0; k1 < EW; ++k1) {
+          y[k1] = T[(k1 * RL + line) * TL + lane];
+          if (k1) y[k1] = cmulc(y[k1], twW[lane * k1]);
+        }
+#pragma unroll
+        for (int j = 0; j < NZW; ++j) {
+          float2 sm = y[0];
+#pragma unroll
+          for (int k1 = 1; k1 < EW; ++k1) sm = cadd(sm, mul_wE<EW>(y[k1], (EW - (j * k1) % EW) % EW));
+          yout[(long long)(row * G::w + lane + 32 * j) * a.yp] = make_float2(sm.x * inv, sm.y * inv);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  cluster.sync();  // the partner may still be reading this CTA's shared memory
+}
+
+template <int EW, int EH>
+void launch_imp_cl(const ImpArgs& a, int B, cudaStream_t st) {
+  const size_t sm = ImpC<EW, EH>::SMEM;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_implicit_cl<EW, EH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  k_implicit_cl<EW, EH><<<dim3(2 * (unsigned)a.C, (unsigned)B), ImpC<EW, EH>::THREADS, sm, st>>>(a);
+}
+
+// the cluster kernel: non-square grids with sides in {32, 64, 128}, and 128 x 128
+bool use_cl(int h, int w) {
+  auto ok = [](int n) { return n == 32 || n == 64 || n == 128; };
+  return ok(h) && ok(w) && (h != w || h == 128) && !(h == 128 && w == 32) && !(h == 32 && w == 128);
+}
+
 // the four-step kernel where it applies (square 64^2 / 128^2 padded grids)
 bool use_v2(int h, int w) { return h == w && (h == 32 || h == 64); }
 
@@ -449,12 +658,12 @@ void launch_imp(const ImpArgs& a, int B, cudaStream_t st) {
 
 bool implicit_fused_supported(int h, int w) {
   auto ok = [](int n) { return n == 32 || n == 64 || n == 128; };  // E = 2n / 32 in {2, 4, 8}
-  return ok(h) && ok(w) && smem_bytes(h, w) <= 200 * 1024;
+  return ok(h) && ok(w) && (use_cl(h, w) || use_v2(h, w) || smem_bytes(h, w) <= 200 * 1024);
 }
 
 void implicit_permute_spectrum(const void* spec, void* spec_perm, int C, int h, int w, cudaStream_t st) {
   const long long n = (long long)C * 4 * h * w;
-  if (use_v2(h, w)) {  // the four-step kernel reads the natural order
+  if (use_v2(h, w) || use_cl(h, w)) {  // the four-step kernels read the natural order
     cudaMemcpyAsync(spec_perm, spec, n * sizeof(float2), cudaMemcpyDeviceToDevice, st);
     return;
   }
@@ -470,6 +679,16 @@ int implicit_fused(const void* x, long long xb, long long xk, long long xp, void
   ImpArgs a{static_cast<const float2*>(x), xb, xk, xp, static_cast<float2*>(y), yb, yk, yp,
             static_cast<const float2*>(spec_perm), active, C};
   const int EW = w / 16, EH = h / 16;
+  if (use_cl(h, w)) {
+#define HS_IMPC(A, Bq) \
+  if (EW == A && EH == Bq) return launch_imp_cl<A, Bq>(a, B, st), HS_OK;
+    HS_IMPC(8, 4)
+    HS_IMPC(4, 8)
+    HS_IMPC(4, 2)
+    HS_IMPC(2, 4)
+    HS_IMPC(8, 8)
+#undef HS_IMPC
+  }
   if (use_v2(h, w)) {
     if (EW == 2) return launch_imp2<2>(a, B, st), HS_OK;
     if (EW == 4) return launch_imp2<4>(a, B, st), HS_OK;

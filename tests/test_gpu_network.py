@@ -136,7 +136,8 @@ def test_green_function_and_implicit_apply_match_reference():
         assert relerr(y, g[f"iy_{tag}"]) < 2e-6
 
 
-@pytest.mark.parametrize("hh,ww", [(32, 32), (64, 64), (32, 64), (64, 32), (128, 64), (64, 128), (128, 256)])
+@pytest.mark.parametrize("hh,ww", [(32, 32), (64, 64), (32, 64), (64, 32), (128, 64), (64, 128), (128, 128), (32, 128),
+                                   (128, 256)])
 def test_fused_implicit_layer_matches_oracle(hh, ww):
     # the fused one-kernel path (implicit.cu) and, at 128 x 256 (the C4 / C5 coarsest level), the batched
     # cuFFT path; the oracle is green.py's pad/fft2/ifft2/crop
