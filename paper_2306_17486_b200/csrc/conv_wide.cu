@@ -106,13 +106,20 @@ struct WCfg {
   // B ring slots (measured: a deeper ring is slower, the weight copies are not the limiter); the
   // stride-2 layers' 257-pixel rows need the space
   static constexpr int NBS = MODE == 1 ? 4 : 6;
+  // staged drain: with one accumulator set, the epilogue copies the pass's group-summed accumulators
+  // into shared memory and releases TMEM before its math and stores, so the next pass's MMAs overlap
+  // them (cout 64 stride 1 only: the staging is R x 128 pixels x (cout + 4) floats, 70 KB)
+  static constexpr int STG_PITCH = COUT + 4;  // floats per staged pixel (16-byte skew: conflict-free)
+  static constexpr bool STG = NSETS == 1 && MODE == 0 && COUT == 64;
+  static constexpr size_t STG_BYTES = STG ? (size_t)R * NACC * 128 * STG_PITCH * 4 : 0;
   static constexpr int pick_rd() {
     for (int n = HS_WIDE_RD_MAX; n > 2; --n)
-      if (1024 + (size_t)n * RAW_SLOT + (size_t)NBS * B_SLOT + (size_t)(NROWS + 2) * A_SLOT <= kWSmemMax) return n;
+      if (1024 + STG_BYTES + (size_t)n * RAW_SLOT + (size_t)NBS * B_SLOT + (size_t)(NROWS + 2) * A_SLOT <= kWSmemMax)
+        return n;
     return 2;
   }
   static constexpr int RD = pick_rd();
-  static constexpr size_t BASE = 1024 + RD * RAW_SLOT;  // raw ring, barriers (512 B), bias (<= 512 B)
+  static constexpr size_t BASE = 1024 + STG_BYTES + RD * RAW_SLOT;  // staging, raw ring, barriers, bias
   static constexpr size_t FIXED = BASE + (size_t)NBS * B_SLOT;
   static constexpr int pick_nas() {
     for (int n = NROWS + HS_WIDE_NAS_EXTRA; n > NROWS; --n)
@@ -217,7 +224,8 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(const __grid_constan
   constexpr int R = C::R, NCH = C::NCH, NAS = C::NAS, NBS = C::NBS, NROWS = C::NROWS, RD = C::RD;
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* araw = smem;  // TMA destinations first: 128-byte aligned
-  unsigned char* bring = araw + (size_t)RD * C::RAW_SLOT;
+  float* stg = reinterpret_cast<float*>(araw + (size_t)RD * C::RAW_SLOT);  // staged drain (C::STG)
+  unsigned char* bring = araw + (size_t)RD * C::RAW_SLOT + C::STG_BYTES;
   unsigned char* aring = bring + (size_t)NBS * C::B_SLOT;
   uint64_t* bars = reinterpret_cast<uint64_t*>(aring + (size_t)NAS * C::A_SLOT);
   uint64_t* a_full = bars;
@@ -447,6 +455,33 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(const __grid_constan
       const uint32_t set = pass % C::NSETS;
       mbar_wait(smem_u32(&acc_full[set]), (pass / C::NSETS) & 1);
       tc_fence_after();
+      if constexpr (C::STG) {
+        // drain: group-summed accumulators of every tile into this thread's staging rows, then TMEM is free
+#pragma unroll 1
+        for (int rk = 0; rk < R * C::NACC; ++rk)
+#pragma unroll
+          for (int n0 = 0; n0 < EH; n0 += 8) {
+            uint32_t v[8], v1[8], v2[8];
+            const uint32_t col = tmem + ((uint32_t)(32 * q4) << 16) + set * C::SET_COLS +
+                                 (uint32_t)(rk * C::ACC_COLS) + hc * EH + n0;
+            tmem_ld8(col, v);
+            tmem_ld8(col + COUT, v1);
+            if constexpr (C::G == 3) tmem_ld8(col + 2 * COUT, v2);
+            tmem_wait_ld();
+            float gs[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float corr = C::G == 3 ? __uint_as_float(v1[j]) + __uint_as_float(v2[j]) : __uint_as_float(v1[j]);
+              gs[j] = __uint_as_float(v[j]) + corr;
+            }
+            float4* dp = reinterpret_cast<float4*>(stg + ((size_t)rk * 128 + m) * C::STG_PITCH + hc * EH + n0);
+            dp[0] = make_float4(gs[0], gs[1], gs[2], gs[3]);
+            dp[1] = make_float4(gs[4], gs[5], gs[6], gs[7]);
+          }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&acc_empty[set]));
+      }
       const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[P.b] : 0) : P.b) *
                                                    a.addend_bstride
                                   : nullptr;
@@ -488,17 +523,30 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(const __grid_constan
         float o[SEG];
 #pragma unroll
         for (int n0 = 0; n0 < SEG; n0 += 8) {
-          uint32_t v[8], v1[8], v2[8];
-          const uint32_t col = tmem + ((uint32_t)(32 * q4) << 16) + set * C::SET_COLS +
-                               (uint32_t)((r * C::NACC + k) * C::ACC_COLS) + hc * EH + sg * SEG + n0;
-          tmem_ld8(col, v);
-          tmem_ld8(col + COUT, v1);
-          if constexpr (C::G == 3) tmem_ld8(col + 2 * COUT, v2);
-          tmem_wait_ld();
+          float gs[8];  // g0 + (g1 [+ g2]): the corrections are summed first
+          if constexpr (C::STG) {
+            const float4* sp4 = reinterpret_cast<const float4*>(
+                stg + ((size_t)(r * C::NACC + k) * 128 + m) * C::STG_PITCH + hc * EH + sg * SEG + n0);
+            const float4 g0 = sp4[0], g1 = sp4[1];
+            gs[0] = g0.x, gs[1] = g0.y, gs[2] = g0.z, gs[3] = g0.w, gs[4] = g1.x, gs[5] = g1.y, gs[6] = g1.z,
+            gs[7] = g1.w;
+          } else {
+            uint32_t v[8], v1[8], v2[8];
+            const uint32_t col = tmem + ((uint32_t)(32 * q4) << 16) + set * C::SET_COLS +
+                                 (uint32_t)((r * C::NACC + k) * C::ACC_COLS) + hc * EH + sg * SEG + n0;
+            tmem_ld8(col, v);
+            tmem_ld8(col + COUT, v1);
+            if constexpr (C::G == 3) tmem_ld8(col + 2 * COUT, v2);
+            tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {  // g0 + (g1 [+ g2]): the corrections are summed first
-            const float corr = C::G == 3 ? __uint_as_float(v1[j]) + __uint_as_float(v2[j]) : __uint_as_float(v1[j]);
-            float x = (__uint_as_float(v[j]) + corr) + s_bias[hc * EH + sg * SEG + n0 + j];
+            for (int j = 0; j < 8; ++j) {
+              const float corr = C::G == 3 ? __uint_as_float(v1[j]) + __uint_as_float(v2[j]) : __uint_as_float(v1[j]);
+              gs[j] = __uint_as_float(v[j]) + corr;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float x = gs[j] + s_bias[hc * EH + sg * SEG + n0 + j];
             if (a.softplus) x = softplus_fast(x);
             o[n0 + j] = x;
           }
@@ -527,9 +575,11 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(const __grid_constan
           for (int q = 0; q < SEG / 4; ++q) yp[q] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&acc_empty[set]));
+      if constexpr (!C::STG) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&acc_empty[set]));
+      }
       ++pass;
     }
   }
