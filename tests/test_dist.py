@@ -160,3 +160,21 @@ def test_gloo_data_parallel_gradient_average():
         assert np.allclose(vec, want, rtol=1e-6, atol=1e-7)
         assert mean_loss == pytest.approx(np.mean(losses), rel=1e-12)
     assert np.array_equal(res[0][1], res[1][1])  # every rank holds the same averaged vector
+
+
+def test_bench_gpus_relaunches_under_torchrun(monkeypatch):
+    # `python bench.py --gpus N` without a torchrun environment re-launches itself with N ranks
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+
+    calls = []
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: calls.append(cmd) or 0)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "2", "--warmup", "3"])
+    assert bench.main() == 0
+    cmd = calls[0]
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=4" in cmd and "127.0.0.1" in cmd
+    assert cmd[-6:] == ["--gpus", "4", "--steps", "2", "--warmup", "3"]
