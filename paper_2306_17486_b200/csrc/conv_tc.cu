@@ -168,8 +168,11 @@ struct Cfg {
   static constexpr int SLOT_COLS = 9 * 8;
   // accumulators in flight; ATM keeps two and gives TMEM to five A slots (a tile
   // reads three rows, so the converters run two rows ahead of the MMAs)
-  static constexpr int NA = ATM ? HS_TC_ATM_NA : (4 * ACOLS <= 512 ? 4 : 2);
-  static constexpr int AOFF = NA * ACOLS;                                         // first A slot column
+  // ATM: two barrier pairs (the two epilogue groups alternate tiles) over NTA TMEM accumulators; with
+  // one accumulator TMEM holds six A slots instead of five (the converters run three rows ahead)
+  static constexpr int NA = ATM ? 2 : (4 * ACOLS <= 512 ? 4 : 2);
+  static constexpr int NTA = ATM ? HS_TC_ATM_NA : NA;                             // TMEM accumulators
+  static constexpr int AOFF = NTA * ACOLS;                                        // first A slot column
   static constexpr int NSA = ATM ? (512 - AOFF) / SLOT_COLS : 0;                  // TMEM A slots
   static_assert(!ATM || (NSA >= 4 && NSA <= 6), "a tile reads three rows; spare slots keep writes ahead");
   static constexpr int NCOLS_RAW = ATM ? 512 : NA * ACOLS;
@@ -611,11 +614,14 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
               mbar_wait(smem_u32(&a_full[sq % C::NSA]), (sq / C::NSA) & 1);
             }
             loaded = max(loaded, hi);
-            const uint32_t acc = tile % C::NA;
-            const uint32_t ause = tile / C::NA;
-            if (ause > 0) mbar_wait(smem_u32(&acc_empty[acc]), (ause - 1) & 1);
+            const uint32_t acc = tile % C::NA;  // barrier pair / epilogue group
+            // the TMEM accumulator was last written by tile - NTA: wait until its group drained it
+            if (tile >= (uint32_t)C::NTA) {
+              const uint32_t prev = tile - C::NTA;
+              mbar_wait(smem_u32(&acc_empty[prev % C::NA]), (prev / C::NA) & 1);
+            }
             tc_fence_after();
-            const uint32_t d0 = tm + acc * C::ACOLS;
+            const uint32_t d0 = tm + (tile % C::NTA) * C::ACOLS;
             if (!(kProbe & 2)) {
 #pragma unroll
               for (int ky = 0; ky < 3; ++ky)
@@ -703,7 +709,8 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
                                     : nullptr;
         for (int oy = U.oy0; oy < U.oy1; ++oy, ++tile) {
           if ((int)(tile & 1) != hg) continue;
-          const int acc = hg;
+          const int acc = hg;                                  // barrier pair
+          const uint32_t tcol = (uint32_t)(tile % C::NTA) * C::ACOLS;  // TMEM accumulator
           const size_t pix = (size_t)oy * a.Wo + (size_t)U.xb * MT + m;
           // side inputs of this pixel (16 channels), requested before the accumulator wait
           float4 sd[4];
@@ -729,7 +736,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
 #pragma unroll
           for (int n0 = 0; n0 < 16; n0 += 8) {
             uint32_t r0[8], r1[8], r2[8];
-            const uint32_t col = tmem + ((uint32_t)(q4 * 32) << 16) + acc * C::ACOLS + n0;
+            const uint32_t col = tmem + ((uint32_t)(q4 * 32) << 16) + tcol + n0;
             tmem_ld8(col, r0);
             tmem_ld8(col + CS, r1);
             tmem_ld8(col + 2 * CS, r2);

@@ -1,0 +1,64 @@
+"""Time the network forward alone (hs_net_forward) at a config's shape: CUDA events, no profiling tags.
+
+    python tools/cnn_probe.py [--config C3] [--B 64] [--iters 10]
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2306_17486_b200 import _lib, network, problems  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--B", type=int, default=64)
+    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--profile", action="store_true", help="also report the per-tag breakdown (events per launch)")
+    a = ap.parse_args()
+    cfg = problems.make_config(a.config)
+    net = network.EncoderSolverNet.seeded(cfg.cnn_channels, seed=0)
+    dn, enc = network.device_network(net, cfg.models, None, None)
+    shape = cfg.models[0].shape
+    rng = np.random.default_rng(1)
+    r = (rng.standard_normal((a.B,) + shape) + 1j * rng.standard_normal((a.B,) + shape)).astype(np.complex64)
+    rd = torch.from_numpy(r).cuda()
+    od = torch.zeros(a.B, dtype=torch.int32, device="cuda")
+    dn.set_encodings(enc)
+    for _ in range(3):
+        dn.forward(rd, od)
+    torch.cuda.synchronize()
+    lib = _lib.load()
+    best = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.iters):
+            dn.forward(rd, od)
+        e1.record()
+        torch.cuda.synchronize()
+        best.append(e0.elapsed_time(e1) / a.iters)
+    print(f"{a.config} network forward, {a.B} RHS: {min(best):.2f} ms per application (best of 3 x {a.iters})")
+    if a.profile:
+        tags = {"convs": _lib.PROF_CONV, "l0": _lib.PROF_CONV_L0, "wide": _lib.PROF_CONV_WIDE, "cnn": _lib.PROF_CNN,
+                "implicit": _lib.PROF_IMPLICIT}
+        lib.hs_profile_reset()
+        lib.hs_profile_enable(sum(1 << t for t in tags.values()))
+        for _ in range(a.iters):
+            dn.forward(rd, od)
+        torch.cuda.synchronize()
+        for n, t in tags.items():
+            ms, work, cnt = _lib.profile_query(t)
+            print(f"  {n}: {ms / a.iters:.2f} ms per application ({cnt // a.iters} launches)")
+        lib.hs_profile_enable(0)
+
+
+if __name__ == "__main__":
+    main()
