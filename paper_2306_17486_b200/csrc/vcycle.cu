@@ -18,6 +18,8 @@
 #include "common.cuh"
 #include "level.cuh"
 #include "prof.h"
+#include <cooperative_groups.h>
+
 #include "vcycle.h"
 
 namespace hs {
@@ -848,9 +850,311 @@ __global__ void __launch_bounds__(kCoarseThreads, 1)
 }
 
 // the reference's coarse solve runs 10 steps (multigrid.py:243); 16 is the supported maximum
+// ---------------------------------------------------------------------------------------------
+// The same GMRES-Jacobi coarse solve (multigrid.py:232-244) on a 2-CTA cluster per RHS.  One CTA
+// per RHS left most SMs idle at C3 (64 RHS on 148 SMs) with each CTA walking 8192 nodes serially;
+// here CTA r owns the rows [r nx0, ...) of the coarsest grid, reads the partner's boundary row of
+// z_j through distributed shared memory for the stencil, and every reduction is a block sum
+// followed by an exchange of the two block totals (added in rank order in both CTAs, so both hold
+// bit-identical coefficients and run identical Givens / stopping logic).
+namespace cgc = cooperative_groups;
+#ifndef HS_COARSE_CLUSTER
+#define HS_COARSE_CLUSTER 0
+#endif
+
+template <int MI>
+struct ClRed {  // double-buffered exchange slots for the cluster reductions
+  static constexpr int NMAX = 2 * (MI + 1) + 2;
+};
+
+// (all N_ entries, compile-time indices: the accumulators stay in registers)
+template <int N_, int MI>
+HS_DEV void cluster_sum(double (&v)[N_], double* red, double* cred, int& parity, cgc::cluster_group& cl, int r) {
+  static_assert(N_ <= ClRed<MI>::NMAX, "exchange slots");
+  block_sum<N_>(v, red);  // every thread holds this CTA's totals
+  double* mine = cred + parity * ClRed<MI>::NMAX;
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int i = 0; i < N_; ++i) mine[i] = v[i];
+  cl.sync();
+  const double* other = cl.map_shared_rank(cred, 1 - r) + parity * ClRed<MI>::NMAX;
+#pragma unroll
+  for (int i = 0; i < N_; ++i) v[i] = r == 0 ? mine[i] + other[i] : other[i] + mine[i];
+  parity ^= 1;
+}
+
+template <int MI, int NPT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCoarseThreads, 1)
+    k_coarse_gmres_cl(LevelDev L, const float2* __restrict__ rhs_base, float2* __restrict__ x_out, float2* vws,
+                      const float2* const* active, const int* model_of, int m, float damping, int* status) {
+  constexpr int NACC = 2 * (MI + 1) + 2;  // |w|^2, the dots, and the non-finite count
+  __shared__ double red[NACC * (kCoarseThreads / 32 + 1)];
+  __shared__ double cred[2 * ClRed<MI>::NMAX];
+  extern __shared__ __align__(16) float2 coarse_dyn[];
+  float2* zs = coarse_dyn;                         // z_j = S v_j / h_j on this CTA's rows
+  float2* ws = coarse_dyn + kCoarseThreads * NPT;  // unnormalised V_j, then w
+  __shared__ double2 H[(MI + 1) * MI];
+  __shared__ double2 gv[MI + 1], sn[MI], yv[MI];
+  __shared__ double cs[MI], vs[MI + 1];
+  __shared__ double2 hc[MI + 1];
+  __shared__ float2 scoef[MI + 1];
+  __shared__ int s_flag, s_jend;
+  cgc::cluster_group cl = cgc::this_cluster();
+  const int r = (int)cl.block_rank();
+  const int b = blockIdx.x >> 1;
+  if (active && active[b] == nullptr) return;  // both CTAs of the pair
+  const int nx = L.nx, ny = L.ny, N = nx * ny;
+  const int nx0 = nx / 2, rows = r ? nx - nx0 : nx0, row0 = r ? nx0 : 0;
+  const int Nr = rows * ny, p0 = row0 * ny;  // this CTA's nodes [p0, p0 + Nr)
+  const float ih2 = L.inv_h2;
+  const float2* rhs = rhs_base + (long long)b * N;
+  float2* V = vws + (long long)b * (m + 1) * N;  // slots 1..m used
+  float2* x = x_out + (long long)b * N;
+  const long long moff = (long long)(model_of ? model_of[b] : 0) * N;
+  const float2* __restrict__ dg = L.diag + moff;
+  const float2* __restrict__ di = L.dinv + moff;
+  const float2* zo = cl.map_shared_rank(zs, 1 - r);  // the partner's z (its boundary row)
+  const int orows = r ? nx0 : nx - nx0;
+  auto vec = [&](int k) -> const float2* { return k == 0 ? rhs : V + (long long)k * N; };
+  const int t = threadIdx.x;
+  int par = 0;
+
+  double acc[NACC];
+#pragma unroll
+  for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
+#pragma unroll
+  for (int u = 0; u < NPT; ++u) {
+    const int pl = t + u * kCoarseThreads;
+    const float2 v = pl < Nr ? rhs[p0 + pl] : make_float2(0.f, 0.f);
+    if (pl < Nr) ws[pl] = v;
+    acc[0] += (double)v.x * v.x + (double)v.y * v.y;
+  }
+  cluster_sum<NACC, MI>(acc, red, cred, par, cl, r);
+  const double beta0 = sqrt(acc[0]);
+  if (beta0 == 0.0) {
+#pragma unroll
+    for (int u = 0; u < NPT; ++u) {
+      const int pl = t + u * kCoarseThreads;
+      if (pl < Nr) x[p0 + pl] = make_float2(0.f, 0.f);
+    }
+    cl.sync();
+    return;
+  }
+  if (t == 0) {
+    vs[0] = 1.0 / beta0;
+    gv[0] = make_double2(beta0, 0.0);
+    s_flag = 0;
+    s_jend = m;
+  }
+  __syncthreads();
+
+  for (int j = 0; j < m; ++j) {
+    const float sj = (float)vs[j];
+#pragma unroll
+    for (int u = 0; u < NPT; ++u) {
+      const int pl = t + u * kCoarseThreads;
+      if (pl < Nr) zs[pl] = cscale(cmul(di[p0 + pl], ws[pl]), damping * sj);
+    }
+    cl.sync();  // both halves of z_j written (the partner reads this CTA's boundary row)
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
+    double bad = 0.0;
+#pragma unroll
+    for (int u = 0; u < NPT; ++u) {
+      const int pl = t + u * kCoarseThreads;
+      float2 w = make_float2(0.f, 0.f);
+      if (pl < Nr) {
+        const int il = pl / ny, q = pl - il * ny, i = row0 + il;
+        const float2 zero = make_float2(0.f, 0.f);
+        const float2 xp = i + 1 < nx ? (il + 1 < rows ? zs[pl + ny] : zo[q]) : zero;
+        const float2 xm = i > 0 ? (il > 0 ? zs[pl - ny] : zo[(orows - 1) * ny + q]) : zero;
+        const float2 yp = q + 1 < ny ? zs[pl + 1] : zero, ym = q > 0 ? zs[pl - 1] : zero;
+        const float2 nb = make_float2((xp.x + xm.x) + (yp.x + ym.x), (xp.y + xm.y) + (yp.y + ym.y));
+        w = apply_dd(dg[p0 + pl], ih2, zs[pl], nb);
+      }
+      if (!isfinite(w.x) || !isfinite(w.y)) bad = 1.0;
+      if (pl < Nr) ws[pl] = w;
+      acc[0] += (double)w.x * w.x + (double)w.y * w.y;
+    }
+    // dots with v_0..v_j over this CTA's nodes
+#pragma unroll 1
+    for (int u = 0; u < NPT; ++u) {
+      const int pl = t + u * kCoarseThreads;
+      if (pl >= Nr) continue;
+      const double2 wd = f2d(ws[pl]);
+#pragma unroll
+      for (int k = 0; k <= MI; ++k)
+        if (k <= j) {
+          const double2 d = zcmul(f2d(vec(k)[p0 + pl]), wd);
+          acc[1 + 2 * k] += d.x;
+          acc[2 + 2 * k] += d.y;
+        }
+    }
+    acc[NACC - 1] = bad;
+    cluster_sum<NACC, MI>(acc, red, cred, par, cl, r);
+    if (acc[NACC - 1] > 0.0) {  // non-finite A z in either half: both CTAs stop here
+      if (t == 0 && r == 0) atomicCAS(status + b, 0, HS_ENONFINITE);
+      cl.sync();
+      return;
+    }
+    const double wn = sqrt(acc[0]);
+    if (t == 0)
+#pragma unroll
+      for (int k = 0; k <= MI; ++k)
+        if (k <= j) {
+          hc[k] = make_double2(acc[1 + 2 * k] * vs[k], acc[2 + 2 * k] * vs[k]);
+          H[k * MI + j] = hc[k];
+        }
+    __syncthreads();
+    double hn2 = 0.0;
+    for (int pass = 0; pass < 2; ++pass) {
+      // w -= sum_k hc_k v_k ; ||w||^2
+      if (t <= j) scoef[t] = make_float2((float)(hc[t].x * vs[t]), (float)(hc[t].y * vs[t]));
+      __syncthreads();
+      double nn[1] = {0.0};
+#pragma unroll 1
+      for (int u = 0; u < NPT; ++u) {
+        const int pl = t + u * kCoarseThreads;
+        if (pl >= Nr) continue;
+        float2 wv = ws[pl];
+#pragma unroll
+        for (int k = 0; k <= MI; ++k)
+          if (k <= j) wv = csub(wv, cmul(scoef[k], vec(k)[p0 + pl]));
+        ws[pl] = wv;
+        nn[0] += (double)wv.x * wv.x + (double)wv.y * wv.y;
+      }
+      cluster_sum<1, MI>(nn, red, cred, par, cl, r);
+      hn2 = nn[0];
+      if (pass == 1 || sqrt(hn2) >= 0.25 * wn) break;
+      // one re-orthogonalisation pass (krylov.py:105-111): extra = V^H w
+#pragma unroll
+      for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
+#pragma unroll 1
+      for (int u = 0; u < NPT; ++u) {
+        const int pl = t + u * kCoarseThreads;
+        if (pl >= Nr) continue;
+        const double2 wd = f2d(ws[pl]);
+#pragma unroll
+        for (int k = 0; k <= MI; ++k)
+          if (k <= j) {
+            const double2 d = zcmul(f2d(vec(k)[p0 + pl]), wd);
+            acc[2 * k] += d.x;
+            acc[2 * k + 1] += d.y;
+          }
+      }
+      cluster_sum<NACC, MI>(acc, red, cred, par, cl, r);
+      if (t == 0)
+#pragma unroll
+        for (int k = 0; k <= MI; ++k)
+          if (k <= j) {
+            hc[k] = make_double2(acc[2 * k] * vs[k], acc[2 * k + 1] * vs[k]);
+            H[k * MI + j] = zadd(H[k * MI + j], hc[k]);
+          }
+      __syncthreads();
+    }
+    // the unnormalised V_{j+1} (this CTA's rows) for the later passes and the solution
+    if (j + 1 < m) {
+#pragma unroll
+      for (int u = 0; u < NPT; ++u) {
+        const int pl = t + u * kCoarseThreads;
+        if (pl < Nr) V[(long long)(j + 1) * N + p0 + pl] = ws[pl];
+      }
+    }
+    if (t == 0) {  // identical inputs in both CTAs: identical rotations and decisions
+      const double hn = sqrt(hn2);
+      double2 col[MI + 1];
+      for (int k = 0; k <= j; ++k) col[k] = H[k * MI + j];
+      for (int k = 0; k < j; ++k) {
+        double2 a = col[k], bb = col[k + 1];
+        double2 sk = sn[k];
+        col[k] = zadd(zscale(a, cs[k]), zmul(sk, bb));
+        col[k + 1] = zadd(zmul(make_double2(-sk.x, sk.y), a), zscale(bb, cs[k]));
+      }
+      double2 a = col[j];
+      double c;
+      double2 sv, rr;
+      double mag = hypot(a.x, a.y);
+      if (mag == 0.0) {
+        c = 0.0;
+        sv = make_double2(1.0, 0.0);
+        rr = make_double2(hn, 0.0);
+      } else {
+        double tt = hypot(mag, hn);
+        double2 ph = make_double2(a.x / mag, a.y / mag);
+        c = mag / tt;
+        sv = zscale(ph, hn / tt);
+        rr = zscale(ph, tt);
+      }
+      cs[j] = c;
+      sn[j] = sv;
+      col[j] = rr;
+      for (int k = 0; k <= j; ++k) H[k * MI + j] = col[k];
+      double2 gj = gv[j];
+      gv[j] = zscale(gj, c);
+      gv[j + 1] = zmul(make_double2(-sv.x, sv.y), gj);
+      const double est = hypot(gv[j + 1].x, gv[j + 1].y) / beta0;
+      if (est <= 1e-12) {
+        s_jend = j + 1;
+        s_flag = 2;
+      } else if (hn <= 1e-14 * fmax(1.0, wn)) {
+        s_flag = 3;
+      }
+      vs[j + 1] = 1.0 / hn;
+    }
+    __syncthreads();
+    if (s_flag == 2) break;
+    if (s_flag == 3) {
+      if (t == 0 && r == 0) atomicCAS(status + b, 0, HS_EBREAKDOWN);
+      cl.sync();
+      return;
+    }
+  }
+  // y = R^{-1} g ; x = S sum_k y_k v_k on this CTA's rows
+  const int jend = s_jend;
+  if (t == 0) {
+    for (int i = jend - 1; i >= 0; --i) {
+      double2 acc2 = gv[i];
+      for (int k = i + 1; k < jend; ++k) acc2 = zsub(acc2, zmul(H[i * MI + k], yv[k]));
+      double2 d = H[i * MI + i];
+      double den = d.x * d.x + d.y * d.y;
+      yv[i] = make_double2((acc2.x * d.x + acc2.y * d.y) / den, (acc2.y * d.x - acc2.x * d.y) / den);
+    }
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int u = 0; u < NPT; ++u) {
+    const int pl = t + u * kCoarseThreads;
+    if (pl >= Nr) continue;
+    float2 sum = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < MI; ++k)
+      if (k < jend) {
+        const float2 yk = make_float2((float)(yv[k].x * vs[k]), (float)(yv[k].y * vs[k]));
+        sum = cadd(sum, cmul(yk, vec(k)[p0 + pl]));
+      }
+    x[p0 + pl] = cmul(cscale(di[p0 + pl], damping), sum);
+  }
+  cl.sync();  // the partner may still read this CTA's exchange slots
+}
+
 void launch_coarse(LevelDev L, const float2* rhs, float2* x, float2* vws, float2* sws, const float2* const* active,
                    const int* model_of, int m, float damping, int* status, int B, cudaStream_t stream) {
   const long long nc = (long long)L.nx * L.ny;
+  // 2-CTA clusters once a half fits 8 nodes per thread: a measurement variant only (HS_COARSE_CLUSTER=1).
+  // Measured at C3 (64 RHS, 64 x 128): 352 us per V-cycle vs 301 us for one CTA per RHS -- the per-step
+  // chain of reductions, now with cluster barriers, sets the pace, not the node loops.
+  if (HS_COARSE_CLUSTER && m <= 10 && L.dinv && nc >= 2048 &&
+      (L.nx - L.nx / 2) * (long long)L.ny <= kCoarseThreads * 8 && L.nx >= 2) {
+    const int smem = 2 * kCoarseThreads * 8 * (int)sizeof(float2);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_coarse_gmres_cl<10, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr = true;
+    }
+    k_coarse_gmres_cl<10, 8><<<2 * B, kCoarseThreads, smem, stream>>>(L, rhs, x, vws, active, model_of, m, damping,
+                                                                       status);
+    return;
+  }
   if (m <= 10 && L.dinv && nc <= kCoarseFastMax) {
     auto launch = [&](auto kern, int npt) {
       const int smem = 2 * kCoarseThreads * npt * (int)sizeof(float2);

@@ -146,3 +146,18 @@ def test_vcycle_large_coarse_grid_matches_oracle(rng, n, levels):
     O = ho.build_hierarchy(ho.Model(m.kappa_sq, m.gamma, m.omega, m.h), damping=(0.8, 0.8), num_levels=levels)
     for i in range(2):
         assert relerr(out[i], ho.v_cycle(rhs[i], u0[i], O)) < 2e-5
+
+
+@pytest.mark.parametrize("shape", [(64, 64), (64, 128), (65, 64), (45, 50)])
+def test_coarse_solve_at_config_sizes_matches_oracle(rng, shape):
+    # the coarsest grids of C2 / C3 (fast on-chip kernel, 4096 / 8192 nodes) and odd / irregular sizes
+    # (the L2-basis kernel); batched, three RHS
+    m = fields.slowness_model(rng.uniform(0.25, 1.0, shape), layer_width=4)
+    H = multigrid.build_hierarchy(m, num_levels=1)
+    O = ho.build_hierarchy(ho.Model(m.kappa_sq, m.gamma, m.omega, m.h), num_levels=1)
+    b = complex_noise(rng, (3,) + shape)
+    import torch
+
+    out = multigrid.coarse_solve(torch.from_numpy(b).cuda(), H.levels[0], 10).cpu().numpy()
+    for i in range(3):
+        assert relerr(out[i], ho.coarse_solve(b[i], O.levels[0], 10)) < 2e-5
