@@ -67,6 +67,9 @@ constexpr int kProbe = HS_TC_PROBE;
 #ifndef HS_TC_PDL
 #define HS_TC_PDL 1
 #endif
+#ifndef HS_TC_BAND_MAX
+#define HS_TC_BAND_MAX 32  // output rows per work unit before the launcher halves it for load balance
+#endif
 #ifndef HS_TC_ATM_NA
 #define HS_TC_ATM_NA 2
 #endif
@@ -947,7 +950,7 @@ void launch_tc(const TcArgs& a, cudaStream_t st) {
   TcArgs b = a;
   const double act = prof::active_hint(a.B);
   const int xblocks = MODE == 2 ? a.W / MT : a.Wo / MT;
-  b.band = 32;
+  b.band = HS_TC_BAND_MAX;
   while (b.band > 8 && C::NSPLIT * act * xblocks * ((a.Ho + b.band - 1) / b.band) < 6.0 * grid) b.band /= 2;
   const long long nunits = num_units<MODE, MT>(b, C::NSPLIT);
   if (nunits < grid) grid = nunits;
