@@ -220,7 +220,7 @@ def cmd_train(args) -> int:
     net = _load_net(args.init) if args.init else network.EncoderSolverNet.seeded(channels, seed=config.seed)
     corpora = _corpora(config, args.models)
     os.makedirs(args.out, exist_ok=True)
-    ck = os.path.join(args.out, "checkpoint.npz")
+    ck = os.path.join(args.out, "checkpoint.ckpt")
     trained, hist = tr.train(net, config, corpora, checkpoint=ck)
     tr.save_checkpoint(ck, hist.state, trained.channels)
     with open(os.path.join(args.out, "loss.csv"), "w") as f:
@@ -250,7 +250,7 @@ def cmd_retrain(args) -> int:
                             batch_size=min(args.batch_size, args.pairs), seed=args.seed)
     trained, hist = tr.train(net, config, {model.shape[0]: ([model], r, e, np.zeros(args.pairs, dtype=int))})
     os.makedirs(args.out, exist_ok=True)
-    ck = os.path.join(args.out, "checkpoint.npz")
+    ck = os.path.join(args.out, "checkpoint.ckpt")
     tr.save_checkpoint(ck, hist.state, trained.channels)
     with open(os.path.join(args.out, "loss.csv"), "w") as f:
         f.write(hist.csv())

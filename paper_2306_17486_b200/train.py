@@ -199,21 +199,79 @@ class Trainer:
         self.steps = int(state["step"])
 
 
+CHECKPOINT_FORMAT = "helmsolve-checkpoint v1"
+
+
+def _arch_hash(channels) -> str:
+    import hashlib
+
+    spec = netparams.param_spec(tuple(channels))
+    text = ";".join(f"{n}:{'x'.join(map(str, s))}:{k}" for n, s, k, _ in spec)
+    return hashlib.sha256(text.encode()).hexdigest()[:16]
+
+
 def save_checkpoint(path: str, state: dict, channels):
-    """Atomic checkpoint write (SPEC trainer concurrency model: write-temp, rename)."""
+    """SPEC.md:384 checkpoint: a text manifest (key: value lines -- format, architecture hash, training
+    metadata, then every tensor's name, shape, dtype and offset) plus ``<path>.bin``, one flat
+    little-endian float32 blob in manifest order: the parameters (netparams.param_spec order, complex
+    kernels as (re, im) pairs, running batch-norm statistics included), then Adam's m and v.
+    Atomic (SPEC trainer concurrency model): both files are written to temporaries and renamed, the
+    manifest last, so a reader never sees a manifest without its blob."""
     import os
 
-    tmp = path + ".tmp"
-    with open(tmp, "wb") as f:
-        np.savez(f, params=state["params"], m=state["m"], v=state["v"], step=state["step"], lr=state["lr"],
-                 channels=np.asarray(channels))
-    os.replace(tmp, path)
+    channels = tuple(int(c) for c in channels)
+    params, m, v = (np.ascontiguousarray(state[k], dtype="<f4") for k in ("params", "m", "v"))
+    lines = [f"format: {CHECKPOINT_FORMAT}", f"architecture: {_arch_hash(channels)}",
+             f"channels: {','.join(map(str, channels))}", f"step: {int(state['step'])}", f"lr: {float(state['lr'])!r}",
+             f"blob: {os.path.basename(path)}.bin", "blob_dtype: float32 little-endian",
+             f"blob_floats: {params.size + m.size + v.size}"]
+    off = 0
+    for group, vec in (("param", params), ("adam_m", m), ("adam_v", v)):
+        goff = 0
+        for name, shape, kind, _ in netparams.param_spec(channels):
+            n = int(np.prod(shape)) * (2 if kind == "implicit" else 1)
+            dtype = "complex64 as (re, im) float32 pairs" if kind == "implicit" else "float32"
+            lines.append(f"tensor: {group} {name} shape={'x'.join(map(str, shape))} dtype={dtype} offset={off + goff}")
+            goff += n
+        if goff != vec.size:
+            raise DimensionError(f"{group}: {vec.size} floats, layout needs {goff}")
+        off += goff
+    for suffix, payload in ((".bin", np.concatenate([params, m, v]).tobytes()),
+                            ("", ("\n".join(lines) + "\n").encode())):
+        tmp = path + suffix + ".tmp"
+        with open(tmp, "wb") as f:
+            f.write(payload)
+        os.replace(tmp, path + suffix)
 
 
 def load_checkpoint(path: str) -> dict:
-    with np.load(path) as z:
-        return {"params": z["params"], "m": z["m"], "v": z["v"], "step": int(z["step"]), "lr": float(z["lr"]),
-                "channels": tuple(int(c) for c in z["channels"])}
+    """Read a SPEC manifest + blob checkpoint (``save_checkpoint``); round-1 ``.npz`` files still load."""
+    import os
+
+    with open(path, "rb") as f:
+        head = f.read(len(CHECKPOINT_FORMAT) + 8)
+    if not head.startswith(b"format:"):
+        with np.load(path) as z:
+            return {"params": z["params"], "m": z["m"], "v": z["v"], "step": int(z["step"]), "lr": float(z["lr"]),
+                    "channels": tuple(int(c) for c in z["channels"])}
+    meta = {}
+    with open(path) as f:
+        for line in f:
+            k, _, val = line.rstrip("\n").partition(": ")
+            if k != "tensor":
+                meta[k] = val
+    if meta.get("format") != CHECKPOINT_FORMAT:
+        raise ConfigurationError(f"{path}: unknown checkpoint format {meta.get('format')!r}")
+    channels = tuple(int(c) for c in meta["channels"].split(","))
+    if meta["architecture"] != _arch_hash(channels):
+        raise ConfigurationError(f"{path}: architecture hash does not match channels {channels}")
+    blob = np.fromfile(os.path.join(os.path.dirname(path), meta["blob"]), dtype="<f4")
+    if blob.size != int(meta["blob_floats"]) or blob.size % 3:
+        raise DimensionError(f"{path}: blob holds {blob.size} floats, manifest says {meta['blob_floats']}")
+    n = blob.size // 3
+    return {"params": blob[:n].astype(np.float32), "m": blob[n : 2 * n].astype(np.float32),
+            "v": blob[2 * n :].astype(np.float32), "step": int(meta["step"]), "lr": float(meta["lr"]),
+            "channels": channels}
 
 
 # ---------------------------------------------------------------- SPEC train schedule
@@ -265,6 +323,15 @@ def train(net: EncoderSolverNet, config: TrainConfig, corpora: dict, checkpoint=
     Parameters and Adam state move between the per-size trainers at every size switch.
     Returns (trained EncoderSolverNet, History).
     """
+    # data parallel (one process per GPU): every rank draws the same seeded epoch order and takes every
+    # world-th batch of it; Trainer.step averages the gradients over ranks, so the parameters stay
+    # identical and only the running batch-norm statistics (per rank, like PyTorch DDP) are averaged
+    # at the end of every epoch before validation and checkpoints
+    rank, world = 0, hdist.world_size()
+    if world > 1:
+        import torch.distributed as tdist
+
+        rank = tdist.get_rank()
     rng = np.random.default_rng(config.seed)
     hist = History()
     trainers, splits, media = {}, {}, {}
@@ -291,12 +358,21 @@ def train(net: EncoderSolverNet, config: TrainConfig, corpora: dict, checkpoint=
         order = rng.permutation(train_idx)
         order = np.resize(order, max(n_samples, config.batch_size))
         losses = []
-        for s in range(0, len(order) - config.batch_size + 1, config.batch_size):
+        nb = (len(order) // config.batch_size) // world * world  # equal batch counts on every rank
+        for bi in range(rank, nb, world):
+            s = bi * config.batch_size
             b = order[s : s + config.batch_size]
             loss = tr.step(media[size], r[b], e[b], owner[b])
             if not np.isfinite(loss):
                 raise NumericalError(f"non-finite loss at epoch {epoch}, batch {s // config.batch_size}")
             losses.append(loss)
+        if world > 1:  # one running-statistics state for validation, checkpoints and the returned net
+            import torch
+
+            keep = torch.as_tensor(tr._read(WHICH_PARAMS)).cuda()
+            hdist.allreduce_mean(keep)
+            tr._write(WHICH_PARAMS, keep.cpu().numpy())
+            losses = [hdist.reduce_scalar(float(np.mean(losses)), "sum") / world]
         # validation MSE (batch statistics, no update); the running statistics are restored after
         val = []
         vb = np.resize(val_idx, max(len(val_idx), config.batch_size)) if len(val_idx) else []

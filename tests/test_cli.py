@@ -88,3 +88,32 @@ def test_errors_are_machine_readable(capsys, tmp_path):
     assert rc == 2
     rc = cli.main(["solve", "--tol", "0", "--out", str(tmp_path / "x")])
     assert rc == 2
+
+
+def test_checkpoint_manifest_and_blob(tmp_path):
+    # text manifest (names, shapes, dtypes, architecture hash, training metadata) + a flat
+    # little-endian float32 blob in manifest order; atomic; round-1 .npz checkpoints still load
+    from paper_2306_17486_b200 import netparams
+    from paper_2306_17486_b200 import train as tr
+
+    ch = (4, 8, 8)
+    params = tr.flatten(netparams.init_params(ch, seed=3), ch)
+    rng = np.random.default_rng(0)
+    state = {"params": params, "m": rng.standard_normal(params.size).astype(np.float32),
+             "v": rng.random(params.size).astype(np.float32), "step": 7, "lr": 1e-3}
+    path = str(tmp_path / "ck.ckpt")
+    tr.save_checkpoint(path, state, ch)
+    text = open(path).read()
+    assert text.startswith("format: helmsolve-checkpoint v1")
+    assert "tensor: param sol.implicit.w shape=4x3x3 dtype=complex64 as (re, im) float32 pairs" in text
+    blob = np.fromfile(path + ".bin", dtype="<f4")
+    assert blob.size == 3 * params.size and np.array_equal(blob[: params.size], params)
+    back = tr.load_checkpoint(path)
+    assert back["channels"] == ch and back["step"] == 7 and back["lr"] == 1e-3
+    for k in ("params", "m", "v"):
+        assert np.array_equal(back[k], state[k])
+    with pytest.raises(Exception):
+        tr.save_checkpoint(path, {**state, "params": params[:-1]}, ch)
+    old = str(tmp_path / "old.npz")
+    np.savez(old, params=params, m=state["m"], v=state["v"], step=3, lr=0.5, channels=np.asarray(ch))
+    assert np.array_equal(tr.load_checkpoint(old)["params"], params)

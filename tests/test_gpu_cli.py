@@ -66,7 +66,7 @@ def test_train_lr_zero_checkpoint_equals_init(tmp_path):
     rc = cli.main(["train", "--sizes", "33", "--samples-per-epoch", "8", "--batch-size", "4", "--max-epochs", "3",
                    "--lr", "0", "--channels", "8,16", "--models", "1", "--out", out])
     assert rc == 0
-    ck = tr.load_checkpoint(os.path.join(out, "checkpoint.npz"))
+    ck = tr.load_checkpoint(os.path.join(out, "checkpoint.ckpt"))
     from paper_2306_17486_b200 import netparams
 
     p0 = tr.flatten(netparams.init_params((8, 16), 0), (8, 16))
@@ -84,14 +84,14 @@ def test_retrain_runs(tmp_path):
     out = str(tmp_path / "t")
     assert cli.main(["train", "--sizes", "33", "--samples-per-epoch", "8", "--batch-size", "4", "--max-epochs", "1",
                      "--channels", "8,16", "--models", "1", "--out", out]) == 0
-    ck = os.path.join(out, "checkpoint.npz")
+    ck = os.path.join(out, "checkpoint.ckpt")
     out2 = str(tmp_path / "r")
     assert cli.main(["retrain", "--checkpoint", ck, "--synthetic", "33", "--seed", "5", "--pairs", "8",
                      "--epochs", "2", "--batch-size", "4", "--out", out2]) == 0
-    assert os.path.exists(os.path.join(out2, "checkpoint.npz"))
+    assert os.path.exists(os.path.join(out2, "checkpoint.ckpt"))
     # the retrained network drives a learned solve through the CLI
     out3 = str(tmp_path / "s")
     assert cli.main(["solve", "--synthetic", "33", "--preconditioner", "implicit_net", "--checkpoint",
-                     os.path.join(out2, "checkpoint.npz"), "--tol", "1e-6", "--out", out3]) == 0
+                     os.path.join(out2, "checkpoint.ckpt"), "--tol", "1e-6", "--out", out3]) == 0
     rep = formats.read_json(out3 + ".report.json", "report")
     assert rep["converged"]
