@@ -21,6 +21,8 @@ ap.add_argument("--stride", type=int, default=1)
 ap.add_argument("--transposed", type=int, default=0)
 ap.add_argument("--tc", type=int, default=1)
 ap.add_argument("--iters", type=int, default=10)
+ap.add_argument("--side", default="addend", choices=["addend", "residual", "none"])
+ap.add_argument("--softplus", type=int, default=1)
 ap.add_argument("--lib", default="", help="a measurement variant (tools/_variants/*.so) instead of the product")
 a = ap.parse_args()
 if a.lib:
@@ -34,9 +36,12 @@ b = torch.randn(a.cout, device=dev)
 Ho, Wo = (2 * a.H, 2 * a.W) if a.transposed else ((a.H - 1) // a.stride + 1, (a.W - 1) // a.stride + 1)
 y = torch.empty(a.B, Ho, Wo, a.cout, device=dev)
 add = torch.randn_like(y)
-c = _lib.HsConv(a.cin, a.cout, a.stride if not a.transposed else 2, a.transposed, 1, w.data_ptr(), b.data_ptr())
+c = _lib.HsConv(a.cin, a.cout, a.stride if not a.transposed else 2, a.transposed, a.softplus, w.data_ptr(),
+                b.data_ptr())
+addp = add.data_ptr() if a.side == "addend" else None
+resp = add.data_ptr() if a.side == "residual" else None
 def run():
-    _lib.check(lib.hs_conv2d(x.data_ptr(), ctypes.byref(c), add.data_ptr(), None, y.data_ptr(), a.B, a.H, a.W,
+    _lib.check(lib.hs_conv2d(x.data_ptr(), ctypes.byref(c), addp, resp, y.data_ptr(), a.B, a.H, a.W,
                              stream_handle()), "conv")
 print("launch", flush=True)
 for _ in range(3):
@@ -56,6 +61,6 @@ print("synced", flush=True)
 ms = min(best)
 pix = (a.B * a.H * a.W) if a.transposed else (a.B * Ho * Wo)
 flops = 2 * 9 * a.cin * a.cout * pix
-byts = 4 * (a.B * a.H * a.W * a.cin + 2 * a.B * Ho * Wo * a.cout)
+byts = 4 * (a.B * a.H * a.W * a.cin + (1 + (a.side != "none")) * a.B * Ho * Wo * a.cout)
 print(f"cin {a.cin} cout {a.cout} s{a.stride} t{a.transposed} tc{a.tc}: {ms:.3f} ms  {flops / ms / 1e9:.1f} TFLOP/s  "
-      f"{byts / ms / 1e6:.0f} GB/s (x + addend + y)")
+      f"{byts / ms / 1e6:.0f} GB/s (x + {a.side} + y)")
