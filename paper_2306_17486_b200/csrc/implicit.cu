@@ -36,21 +36,40 @@ constexpr int kImpThreads = 256;
 
 HS_DEV int br5(int l) { return __brev(l) >> 27; }
 
-// a * W_E^m, W_E = exp(-2 pi i / E), E in {2, 4, 8}, m a compile-time constant
+// a * W_E^m, W_E = exp(-2 pi i / E), E in {2, 4, 8, 16}, m a compile-time constant
 // after unrolling: multiples of pi/2 are swaps / negations, odd multiples of
-// pi/4 one scaled add (no multiplications by 0 or 1 survive)
+// pi/4 one scaled add (no multiplications by 0 or 1 survive), odd multiples of
+// pi/8 (E = 16) one complex multiply by a constant
 template <int E>
 HS_DEV float2 mul_wE(float2 a, int m) {
-  constexpr float s = 0.70710678118654752f;
-  switch ((m * (8 / E)) & 7) {  // in units of 2 pi / 8
-    case 0: return a;
-    case 1: return make_float2(s * (a.x + a.y), s * (a.y - a.x));    // (1 - i) / sqrt2
-    case 2: return make_float2(a.y, -a.x);                          // -i
-    case 3: return make_float2(s * (a.y - a.x), -s * (a.x + a.y));   // (-1 - i) / sqrt2
-    case 4: return make_float2(-a.x, -a.y);                         // -1
-    case 5: return make_float2(-s * (a.x + a.y), s * (a.x - a.y));   // (-1 + i) / sqrt2
-    case 6: return make_float2(-a.y, a.x);                          // i
-    default: return make_float2(s * (a.x - a.y), s * (a.x + a.y));  // (1 + i) / sqrt2
+  if constexpr (E == 16) {
+    const int k = m & 15;
+    if ((k & 1) == 0) return mul_wE<8>(a, k >> 1);
+    constexpr float C1 = 0.92387953251128675613f, S1 = 0.38268343236508977173f;  // cos, sin of pi/8
+    float c, sn;
+    switch (k) {  // W_16^k = cos(pi k / 8) - i sin(pi k / 8)
+      case 1: c = C1, sn = S1; break;
+      case 3: c = S1, sn = C1; break;
+      case 5: c = -S1, sn = C1; break;
+      case 7: c = -C1, sn = S1; break;
+      case 9: c = -C1, sn = -S1; break;
+      case 11: c = -S1, sn = -C1; break;
+      case 13: c = S1, sn = -C1; break;
+      default: c = C1, sn = -S1; break;
+    }
+    return make_float2(a.x * c + a.y * sn, a.y * c - a.x * sn);
+  } else {
+    constexpr float s = 0.70710678118654752f;
+    switch ((m * (8 / E)) & 7) {  // in units of 2 pi / 8
+      case 0: return a;
+      case 1: return make_float2(s * (a.x + a.y), s * (a.y - a.x));    // (1 - i) / sqrt2
+      case 2: return make_float2(a.y, -a.x);                          // -i
+      case 3: return make_float2(s * (a.y - a.x), -s * (a.x + a.y));   // (-1 - i) / sqrt2
+      case 4: return make_float2(-a.x, -a.y);                         // -1
+      case 5: return make_float2(-s * (a.x + a.y), s * (a.x - a.y));   // (-1 + i) / sqrt2
+      case 6: return make_float2(-a.y, a.x);                          // i
+      default: return make_float2(s * (a.x - a.y), s * (a.x + a.y));  // (1 + i) / sqrt2
+    }
   }
 }
 
@@ -428,18 +447,19 @@ void launch_imp2(const ImpArgs& a, int B, cudaStream_t st) {
 //   3. CTA r inverse-transforms its rows, reading the partner's columns through DSMEM, and writes
 //      the w kept outputs                                                         -> cluster barrier
 // The spectrum is used in its natural [C][H2][W2] order, like k_implicit2.
-template <int EW, int EH>
+template <int EW, int EH, int NCL>
 struct ImpC {
   static constexpr int THREADS = 128, NWARP = THREADS / 32;
   static constexpr int W2 = 32 * EW, H2 = 32 * EH, h = H2 / 2, w = W2 / 2;
-  static constexpr int HALF = W2 / 2, LDS = HALF + 1;  // columns per CTA, S row pitch (odd: conflict-free)
+  static constexpr int HALF = W2 / NCL, LDS = HALF + 1;  // columns per CTA, S row pitch (odd: conflict-free)
+  static constexpr int HR = h / NCL;                     // rows per CTA in the row passes
   static constexpr int RL = THREADS / EW, CL = THREADS / EH, TL = 33;
   static constexpr size_t SMEM = ((size_t)h * LDS + (size_t)THREADS * TL + W2 + H2) * sizeof(float2);
 };
 
-template <int EW, int EH>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ImpC<EW, EH>::THREADS) k_implicit_cl(ImpArgs a) {
-  using G = ImpC<EW, EH>;
+template <int EW, int EH, int NCL>
+__global__ void __cluster_dims__(NCL, 1, 1) __launch_bounds__(ImpC<EW, EH, NCL>::THREADS) k_implicit_cl(ImpArgs a) {
+  using G = ImpC<EW, EH, NCL>;
   constexpr int W2 = G::W2, H2 = G::H2, h = G::h, HALF = G::HALF, LDS = G::LDS, RL = G::RL, CL = G::CL,
                 TL = G::TL, NT = G::THREADS, NWP = G::NWARP;
   constexpr int NZW = EW / 2, NZH = EH / 2;  // non-zero 32-blocks of a padded row / column
@@ -451,10 +471,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ImpC<EW, EH>::THREAD
   float2* T = S + h * LDS;                  // [E][lines][TL] four-step transpose buffer
   float2* twW = T + NT * TL;                // W_W2^m
   float2* twH = twW + W2;                   // W_H2^m
-  float2* Sp[2];
-  Sp[r] = S;
-  Sp[1 - r] = cluster.map_shared_rank(S, 1 - r);
-  const int b = blockIdx.y, k = blockIdx.x >> 1;
+  float2* Sp[NCL];  // every CTA's column slice
+#pragma unroll
+  for (int q = 0; q < NCL; ++q) Sp[q] = q == r ? S : cluster.map_shared_rank(S, q);
+  const int b = blockIdx.y, k = blockIdx.x / NCL;
   const bool skip = a.active && a.active[b] == nullptr;  // both CTAs of the pair agree
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int m = threadIdx.x; m < W2; m += NT) {
@@ -470,10 +490,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ImpC<EW, EH>::THREAD
   __syncthreads();
   if (!skip) {
     const float2* xin = a.x + b * a.xb + k * a.xk;
-    const int row0 = r * (h / 2);
-    // ---- 1. forward row transforms of rows [row0, row0 + h/2)
-    for (int c0 = 0; c0 < h / 2; c0 += RL) {
-      const int nl = min(RL, h / 2 - c0);  // rows of this chunk (RL may exceed the CTA's h / 2 rows)
+    const int row0 = r * G::HR;
+    // ---- 1. forward row transforms of rows [row0, row0 + HR)
+    for (int c0 = 0; c0 < G::HR; c0 += RL) {
+      const int nl = min(RL, G::HR - c0);  // rows of this chunk (RL may exceed the CTA's HR rows)
       for (int line = warp; line < nl; line += NWP) {  // step (a): E-point DFT over j, twiddle
         const int row = row0 + c0 + line;
         float2 q[EW];
@@ -566,10 +586,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ImpC<EW, EH>::THREAD
     // ---- 3. inverse row transforms of this CTA's rows, the partner's columns through DSMEM
     float2* yout = a.y + b * a.yb + k * a.yk;
     const float inv = 1.f / ((float)H2 * (float)W2);
-    const int row0 = r * (h / 2);
+    const int row0 = r * G::HR;
     const int tk = threadIdx.x / RL, tl = threadIdx.x % RL;
-    for (int c0 = 0; c0 < h / 2; c0 += RL) {
-      const int nl = min(RL, h / 2 - c0);
+    for (int c0 = 0; c0 < G::HR; c0 += RL) {
+      const int nl = min(RL, G::HR - c0);
       if (tl < nl) {
         const int row = row0 + c0 + tl;
         float2 v[32];
@@ -605,19 +625,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ImpC<EW, EH>::THREAD
   cluster.sync();  // the partner may still be reading this CTA's shared memory
 }
 
-template <int EW, int EH>
+template <int EW, int EH, int NCL>
 void launch_imp_cl(const ImpArgs& a, int B, cudaStream_t st) {
-  const size_t sm = ImpC<EW, EH>::SMEM;
+  using G = ImpC<EW, EH, NCL>;
+  static_assert(G::HR % 1 == 0 && G::h % NCL == 0 && G::HALF % G::CL == 0, "cluster split");
+  const size_t sm = G::SMEM;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_implicit_cl<EW, EH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_implicit_cl<EW, EH, NCL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
-  k_implicit_cl<EW, EH><<<dim3(2 * (unsigned)a.C, (unsigned)B), ImpC<EW, EH>::THREADS, sm, st>>>(a);
+  k_implicit_cl<EW, EH, NCL><<<dim3(NCL * (unsigned)a.C, (unsigned)B), G::THREADS, sm, st>>>(a);
 }
 
-// the cluster kernel: non-square grids with sides in {32, 64, 128}, and 128 x 128
+// the cluster kernel: non-square grids with sides in {32, 64, 128}, 128 x 128 (2-CTA clusters), and
+// the 128 x 256 coarsest grid of C4 / C5 (512-point rows, 4-CTA clusters)
 bool use_cl(int h, int w) {
+  if ((h == 128 && w == 256) || (h == 256 && w == 128)) return true;
   auto ok = [](int n) { return n == 32 || n == 64 || n == 128; };
   return ok(h) && ok(w) && (h != w || h == 128) && !(h == 128 && w == 32) && !(h == 32 && w == 128);
 }
@@ -657,8 +681,9 @@ void launch_imp(const ImpArgs& a, int B, cudaStream_t st) {
 }  // namespace
 
 bool implicit_fused_supported(int h, int w) {
+  if (use_cl(h, w)) return true;
   auto ok = [](int n) { return n == 32 || n == 64 || n == 128; };  // E = 2n / 32 in {2, 4, 8}
-  return ok(h) && ok(w) && (use_cl(h, w) || use_v2(h, w) || smem_bytes(h, w) <= 200 * 1024);
+  return ok(h) && ok(w) && (use_v2(h, w) || smem_bytes(h, w) <= 200 * 1024);
 }
 
 void implicit_permute_spectrum(const void* spec, void* spec_perm, int C, int h, int w, cudaStream_t st) {
@@ -680,13 +705,15 @@ int implicit_fused(const void* x, long long xb, long long xk, long long xp, void
             static_cast<const float2*>(spec_perm), active, C};
   const int EW = w / 16, EH = h / 16;
   if (use_cl(h, w)) {
-#define HS_IMPC(A, Bq) \
-  if (EW == A && EH == Bq) return launch_imp_cl<A, Bq>(a, B, st), HS_OK;
-    HS_IMPC(8, 4)
-    HS_IMPC(4, 8)
-    HS_IMPC(4, 2)
-    HS_IMPC(2, 4)
-    HS_IMPC(8, 8)
+#define HS_IMPC(A, Bq, NC) \
+  if (EW == A && EH == Bq) return launch_imp_cl<A, Bq, NC>(a, B, st), HS_OK;
+    HS_IMPC(8, 4, 2)
+    HS_IMPC(4, 8, 2)
+    HS_IMPC(4, 2, 2)
+    HS_IMPC(2, 4, 2)
+    HS_IMPC(8, 8, 2)
+    HS_IMPC(16, 8, 4)
+    HS_IMPC(8, 16, 4)
 #undef HS_IMPC
   }
   if (use_v2(h, w)) {
