@@ -14,6 +14,8 @@
 // a damped-Jacobi preconditioner (coarse_solve, :232-244), one CTA per RHS,
 // basis kept in an L2-resident workspace, fp64 reductions.
 #include <algorithm>
+#include <map>
+#include <mutex>
 
 #include "common.cuh"
 #include "level.cuh"
@@ -91,7 +93,13 @@ HS_DEV Pair mask_pair(Pair v, bool row_ok, bool oka, bool okb) {
 constexpr int kVcWarps = 4;          // warps per block (independent)
 constexpr int kDownQ = 29;           // coarse columns per down-leg warp (lanes 1..29)
 constexpr int kUpCols = 60;          // fine columns per up-leg warp (lanes 1..30)
-constexpr int kRing = 4;             // rows in flight per warp (cp.async ring depth)
+#ifndef HS_VC_RING
+#define HS_VC_RING 6
+#endif
+#ifndef HS_VC_WAVES
+#define HS_VC_WAVES 0  // 0: ~32 warps per SM heuristic; n > 0: bands sized for n full waves of resident warps
+#endif
+constexpr int kRing = HS_VC_RING;    // rows in flight per warp (cp.async ring depth)
 
 // Row staging: every lane copies its own two columns of a row into a per-warp
 // shared-memory ring with 8-byte cp.async (zero-filled outside the grid) and
@@ -567,9 +575,16 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_gmres(LevelDev L, con
 // the number of basis vectors JJ a compile-time constant (dispatched on the
 // window position), so every loop is unrolled without guards.
 // dots: acc[1 + 2k] + i acc[2 + 2k] += conj(v_k) w, k < JJ (v_0 = rhs)
+#ifndef HS_COARSE_UNROLL
+#define HS_COARSE_UNROLL 1  // measured: 1, 2, 4 and 8 equal at C3 (the coarse solve is issue-bound, not L2-latency-bound)
+#endif
+constexpr int kCoarseUnroll = HS_COARSE_UNROLL;
+// The node loop is unrolled (HS_COARSE_UNROLL nodes per trip) so the basis loads of several nodes are
+// in flight together: the basis lives in L2, and a trip per node paid one L2 round trip each.
 template <int JJ, int NACC>
 HS_DEV void coarse_dots(double (&acc)[NACC], const float2* __restrict__ rhs, const float2* __restrict__ V, int N,
                         const float2* ws) {
+#pragma unroll kCoarseUnroll
   for (int p = threadIdx.x; p < N; p += blockDim.x) {
     float2 q[JJ];
     q[0] = rhs[p];
@@ -592,6 +607,7 @@ HS_DEV double coarse_orth(const float2* __restrict__ rhs, const float2* __restri
 #pragma unroll
   for (int k = 0; k < JJ; ++k) c[k] = coef[k];
   double nn = 0.0;
+#pragma unroll kCoarseUnroll
   for (int p = threadIdx.x; p < N; p += blockDim.x) {
     float2 q[JJ];
     q[0] = rhs[p];
@@ -1186,10 +1202,24 @@ constexpr int kUpSmem = kVcWarps * kRing * kUpSlot * 8;
 // rows per warp band: enough (column block, band) warps to fill every SM
 // ~32 warps deep over the batch, but never bands shorter than `min_rows`
 // (each band re-reads a few halo rows)
-int band_rows(int rows, int ncb, int B, int min_rows) {
-  const long target = 148L * 32;
-  long nb = (target + (long)ncb * B - 1) / ((long)ncb * B);
-  long cap = rows / min_rows;
+int band_rows(int rows, int ncb, int B, int min_rows, const void* kern, int smem) {
+  static std::mutex mu;
+  static std::map<const void*, int> cache;  // resident blocks per SM of each leg kernel
+  int resident;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(kern);
+    if (it == cache.end()) {
+      int nb = 0;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kVcWarps * 32, smem);
+      it = cache.emplace(kern, nb > 0 ? nb : 1).first;
+    }
+    resident = it->second;
+  }
+  const long target = HS_VC_WAVES > 0 ? (long)HS_VC_WAVES * 148 * resident * kVcWarps : 148L * 32;
+  long nb = HS_VC_WAVES > 0 ? target / ((long)ncb * B) : (target + (long)ncb * B - 1) / ((long)ncb * B);
+  const long cap = rows / min_rows;
   if (nb > cap) nb = cap;
   if (nb < 1) nb = 1;
   return (int)((rows + nb - 1) / nb);
@@ -1314,7 +1344,7 @@ void vcycle(const Hierarchy& H_in, VecIn rhs, VecIn u0, VecOut out, const float2
     VecIn in = l == 0 ? rhs : VecIn{nullptr, lrhs[l], (long long)F.nx * F.ny, nullptr};
     VecIn uz = l == 0 ? u0 : VecIn{nullptr, nullptr, 0, nullptr};
     const int ncb = (int)cdiv_u(ncy, kDownQ);
-    const int band = band_rows(ncx, ncb, B, 4);
+    const int band = band_rows(ncx, ncb, B, 4, (uz.tab || uz.base) ? (const void*)k_vc_down<true> : (const void*)k_vc_down<false>, kDownSmem);
     dim3 g(B, cdiv_u((long)ncb * cdiv_u(ncx, band), kVcWarps));  // RHS fastest: the planes stay L2-hot
     if (uz.tab || uz.base)
       k_vc_down<true><<<g, kVcWarps * 32, kDownSmem, stream>>>(F, ncx, ncy, in, uz, active, model_of, H.w_pre, lrhs[l + 1],
@@ -1336,7 +1366,7 @@ void vcycle(const Hierarchy& H_in, VecIn rhs, VecIn u0, VecOut out, const float2
     VecIn uz = l == 0 ? u0 : VecIn{nullptr, nullptr, 0, nullptr};
     VecOut o = l == 0 ? out : VecOut{nullptr, lerr[l], (long long)F.nx * F.ny};
     const int ncb = (int)cdiv_u(F.ny, kUpCols);
-    const int band = band_rows(F.nx, ncb, B, 8);
+    const int band = band_rows(F.nx, ncb, B, 8, (uz.tab || uz.base) ? (const void*)k_vc_up<true> : (const void*)k_vc_up<false>, kUpSmem);
     dim3 g(B, cdiv_u((long)ncb * cdiv_u(F.nx, band), kVcWarps));
     const double N = (double)F.nx * F.ny;
     const double up_bytes = nact * (18.0 * N + ((l == 0 && has_u0) ? 8.0 * N : 0.0)) + H.n_models * 8.0 * N;
