@@ -181,6 +181,8 @@ HS_API void hs_profile_reset(void);
 HS_API int hs_profile_query(int tag, double* total_ms, double* total_work, long long* count);
 /* kernels launched by the library since the last hs_profile_reset */
 HS_API long long hs_launch_count(void);
+/* per-launch records of the enabled tags (tracing; no reference counterpart) */
+HS_API int hs_profile_records(int* tags, int* labels, double* ms, int max);
 /* 1 (default): tcgen05 BF16x3 convolutions (exact three-way bf16 split, fp32 accumulate) where the shape
    allows; 0: SIMT fp32 only (a test switch for A/B parity; it never skips work) */
 HS_API void hs_set_conv_path(int tensor_cores);

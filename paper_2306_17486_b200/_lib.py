@@ -145,6 +145,7 @@ SIGNATURES = {
     "hs_profile_reset": (None, []),
     "hs_profile_query": (_I, [_I, c_double_p, c_double_p, ctypes.POINTER(ctypes.c_longlong)]),
     "hs_launch_count": (ctypes.c_longlong, []),
+    "hs_profile_records": (_I, [c_int_p, c_int_p, c_double_p, _I]),
     "hs_set_conv_path": (None, [_I]),
     "hs_resize_bilinear": (_I, [_VP, _VP, _I, _I, _I, _I, _I, _VP]),
     "hs_gaussian_smooth": (_I, [_VP, _VP, _VP, _I, _I, _I, _D, _VP]),
@@ -192,6 +193,17 @@ def profile_query(tag: int):
     ms, work, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong()
     check(load().hs_profile_query(tag, ctypes.byref(ms), ctypes.byref(work), ctypes.byref(n)), "profile")
     return ms.value, work.value, n.value
+
+
+def profile_records(max_records: int = 100000):
+    """[(tag, label, ms)] of every timed launch since the last reset, in launch order."""
+    tags = (ctypes.c_int * max_records)()
+    labels = (ctypes.c_int * max_records)()
+    ms = (ctypes.c_double * max_records)()
+    n = load().hs_profile_records(tags, labels, ms, max_records)
+    if n < 0:
+        check(-n, "profile records")
+    return [(tags[i], labels[i], ms[i]) for i in range(n)]
 
 
 def last_error() -> str:

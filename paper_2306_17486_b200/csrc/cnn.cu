@@ -832,6 +832,7 @@ int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* 
       prof::stop(s1, st, w1);
     }
   };
+  prof::set_label(c.cin * 100000 + c.cout * 100 + (c.transposed ? 2 : c.stride - 1));
   Scope2 scope{prof::start(prof::CONV, st),
                l0 ? prof::start(prof::CONV_L0, st) : (wide ? prof::start(prof::CONV_WIDE, st) : -1), st, flops,
                l0 ? l0_bytes : flops};

@@ -715,22 +715,25 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
           const int acc = hg;                                  // barrier pair
           const uint32_t tcol = (uint32_t)(tile % C::NTA) * C::ACOLS;  // TMEM accumulator
           const size_t pix = (size_t)oy * a.Wo + (size_t)U.xb * MT + m;
-          // side inputs of this pixel (16 channels), requested before the accumulator wait
+          // side inputs in the layout the stores use after the 4x4 transpose below (chunk gi of the four
+          // pixels of this lane's group): each load instruction reads whole 64-byte pixels, coalesced,
+          // and they are requested before the accumulator wait
+          const size_t gpix = pix - lane + (lane & ~3);
           float4 sd[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) sd[q] = make_float4(0.f, 0.f, 0.f, 0.f);
           if (add && !(kProbe & 256)) {
-            const float4* ap = reinterpret_cast<const float4*>(add + pix * COUT);
+            const float4* ap = reinterpret_cast<const float4*>(add + gpix * COUT);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) sd[q] = __ldg(ap + q);
+            for (int j = 0; j < 4; ++j) sd[j] = __ldg(ap + j * 4 + gi);
           }
           if (a.residual) {
-            const float4* rp = reinterpret_cast<const float4*>(a.residual + ((size_t)U.b * a.Ho * a.Wo + pix) * COUT);
+            const float4* rp = reinterpret_cast<const float4*>(a.residual + ((size_t)U.b * a.Ho * a.Wo + gpix) * COUT);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float4 r = __ldg(rp + q);
-              const uint64_t s01 = add2(pkf(sd[q].x, sd[q].y), pkf(r.x, r.y)), s23 = add2(pkf(sd[q].z, sd[q].w), pkf(r.z, r.w));
-              sd[q] = make_float4(lo_f(s01), hi_f(s01), lo_f(s23), hi_f(s23));
+            for (int j = 0; j < 4; ++j) {
+              const float4 r = __ldg(rp + j * 4 + gi);
+              const uint64_t s01 = add2(pkf(sd[j].x, sd[j].y), pkf(r.x, r.y)), s23 = add2(pkf(sd[j].z, sd[j].w), pkf(r.z, r.w));
+              sd[j] = make_float4(lo_f(s01), hi_f(s01), lo_f(s23), hi_f(s23));
             }
           }
           mbar_wait(smem_u32(&acc_full[acc]), (uint32_t)((tile / C::NA) & 1));
@@ -768,29 +771,34 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
               v.z = softplus_fast(v.z);
               v.w = softplus_fast(v.w);
             }
-            const uint64_t q01 = add2(pkf(v.x, v.y), pkf(sd[q].x, sd[q].y));
-            const uint64_t q23 = add2(pkf(v.z, v.w), pkf(sd[q].z, sd[q].w));
-            ch[q] = make_float4(lo_f(q01), hi_f(q01), lo_f(q23), hi_f(q23));
+            ch[q] = v;
           }
-          // 4x4 transpose inside the group: lane gi ends up with chunk gi of the group's four pixels
-          // (xor partner gi ^ k sends its chunk gi and receives ours for its position)
+          // 4x4 transpose inside the group: lane gi ends up with chunk gi of the group's four pixels.
+          // Two butterfly stages (partner lane gi ^ 1, then gi ^ 2): each swaps the chunks whose index
+          // bit differs from the lane's bit with the partner's mirrored chunk
+          auto xchg = [&](float4& keep_lo, float4& keep_hi, bool hi_lane, int mask) {
+            float4 send = hi_lane ? keep_lo : keep_hi, got;
+            got.x = __shfl_xor_sync(0xffffffffu, send.x, mask);
+            got.y = __shfl_xor_sync(0xffffffffu, send.y, mask);
+            got.z = __shfl_xor_sync(0xffffffffu, send.z, mask);
+            got.w = __shfl_xor_sync(0xffffffffu, send.w, mask);
+            if (hi_lane)
+              keep_lo = got;
+            else
+              keep_hi = got;
+          };
+          xchg(ch[0], ch[1], gi & 1, 1);
+          xchg(ch[2], ch[3], gi & 1, 1);
+          xchg(ch[0], ch[2], gi & 2, 2);
+          xchg(ch[1], ch[3], gi & 2, 2);
+          // now ch[j] holds chunk gi of pixel (lane & ~3) + j: add the side inputs (same layout), and
+          // store j writes whole pixels
 #pragma unroll
-          for (int k = 1; k < 4; ++k) {
-            const int want = gi ^ k;
-            float4 send = ch[0];
-#pragma unroll
-            for (int q = 1; q < 4; ++q)
-              if (q == want) send = ch[q];
-            float4 got;
-            got.x = __shfl_xor_sync(0xffffffffu, send.x, k);
-            got.y = __shfl_xor_sync(0xffffffffu, send.y, k);
-            got.z = __shfl_xor_sync(0xffffffffu, send.z, k);
-            got.w = __shfl_xor_sync(0xffffffffu, send.w, k);
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (q == want) ch[q] = got;
+          for (int j = 0; j < 4; ++j) {
+            const uint64_t q01 = add2(pkf(ch[j].x, ch[j].y), pkf(sd[j].x, sd[j].y));
+            const uint64_t q23 = add2(pkf(ch[j].z, ch[j].w), pkf(sd[j].z, sd[j].w));
+            ch[j] = make_float4(lo_f(q01), hi_f(q01), lo_f(q23), hi_f(q23));
           }
-          // now ch[j] holds chunk gi of pixel (lane & ~3) + j: store j writes whole pixels
           if (!(kProbe & 64)) {
             float4* yb = reinterpret_cast<float4*>(a.y + ((size_t)U.b * a.Ho * a.Wo + pix - lane + (lane & ~3)) * COUT);
 #pragma unroll

@@ -12,7 +12,7 @@ std::atomic<int> active_now{0};
 
 namespace {
 struct Rec {
-  int tag;
+  int tag, label;
   cudaEvent_t a, b;
   double work;
 };
@@ -20,6 +20,7 @@ std::mutex mu;
 unsigned mask = 0;
 std::vector<Rec> recs;
 std::vector<cudaEvent_t> pool;
+thread_local int cur_label = 0;
 
 cudaEvent_t get_event() {
   if (!pool.empty()) {
@@ -35,10 +36,12 @@ cudaEvent_t get_event() {
 
 bool on(int tag) { return (mask >> tag) & 1u; }
 
+void set_label(int label) { cur_label = label; }
+
 int start(int tag, cudaStream_t st) {
   if (!on(tag)) return -1;
   std::lock_guard<std::mutex> g(mu);
-  Rec r{tag, get_event(), get_event(), 0.0};
+  Rec r{tag, cur_label, get_event(), get_event(), 0.0};
   cudaEventRecord(r.a, st);
   recs.push_back(r);
   return (int)recs.size() - 1;
@@ -72,6 +75,25 @@ HS_API void hs_profile_reset(void) {
 }
 
 HS_API long long hs_launch_count(void) { return launches.load(); }
+
+/* Per-launch records of the timed tags, in launch order: tag, label (convolutions: cin * 100000 +
+   cout * 100 + mode, mode 0/1 = stride 1/2, 2 = transposed), milliseconds.  Returns the record count
+   (at most max are written). */
+HS_API int hs_profile_records(int* tags, int* labels, double* ms, int max) {
+  std::lock_guard<std::mutex> g(mu);
+  int n = 0;
+  for (auto& r : recs) {
+    if (n >= max) break;
+    if (cudaEventSynchronize(r.b) != cudaSuccess) return -HS_ECUDA;
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    tags[n] = r.tag;
+    labels[n] = r.label;
+    ms[n] = t;
+    ++n;
+  }
+  return n;
+}
 
 HS_API int hs_profile_query(int tag, double* total_ms, double* total_work, long long* count) {
   std::lock_guard<std::mutex> g(mu);

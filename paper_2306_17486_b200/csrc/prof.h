@@ -36,6 +36,8 @@ inline double active_hint(int B) {
 }
 
 bool on(int tag);
+// label attached to the records this thread starts next (per-layer breakdowns)
+void set_label(int label);
 // returns an opaque slot (or -1) to close with stop()
 int start(int tag, cudaStream_t st);
 void stop(int slot, cudaStream_t st, double work);

@@ -58,6 +58,21 @@ def main():
             ms, work, cnt = _lib.profile_query(t)
             print(f"  {n}: {ms / a.iters:.2f} ms per application ({cnt // a.iters} launches)")
         lib.hs_profile_enable(0)
+        # per layer (label = cin * 100000 + cout * 100 + mode): hot time per launch, CUDA events
+        lib.hs_profile_reset()
+        lib.hs_profile_enable(1 << _lib.PROF_CONV)
+        for _ in range(a.iters):
+            dn.forward(rd, od)
+        torch.cuda.synchronize()
+        lib.hs_profile_enable(0)
+        recs = _lib.profile_records()
+        per = len(recs) // a.iters
+        print(f"  per layer ({per} convs per application, mean of {a.iters}):")
+        for k in range(per):
+            _, lab, _ = recs[k]
+            ms = sum(recs[i * per + k][2] for i in range(a.iters)) / a.iters
+            cin, cout, mode = lab // 100000, (lab // 100) % 1000, lab % 100
+            print(f"    {k:2d}  {cin:3d} -> {cout:3d} {('s1', 's2', 't')[mode]:>2}  {ms:.3f} ms")
 
 
 if __name__ == "__main__":
