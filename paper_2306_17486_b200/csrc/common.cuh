@@ -62,6 +62,29 @@ HS_DEV float softplus_fast(float x) {
   return fmaf(l, 0.69314718055994531f, fmaxf(x, 0.f));
 }
 
+// 4x4 transpose of 16-byte chunks inside each group of four lanes: lane gi (= lane & 3) holds
+// chunks ch[0..3] of its own pixel and ends with chunk gi of the group's pixels 0..3, so store j of a
+// warp writes whole 64-byte pixels.  Two butterfly stages (partner gi ^ 1, then gi ^ 2): each swaps the
+// chunks whose index bit differs from the lane's bit with the partner's mirrored chunk.
+HS_DEV void group4_transpose(float4 (&ch)[4], int gi) {
+  auto xchg = [](float4& keep_lo, float4& keep_hi, bool hi_lane, int mask) {
+    const float4 send = hi_lane ? keep_lo : keep_hi;
+    float4 got;
+    got.x = __shfl_xor_sync(0xffffffffu, send.x, mask);
+    got.y = __shfl_xor_sync(0xffffffffu, send.y, mask);
+    got.z = __shfl_xor_sync(0xffffffffu, send.z, mask);
+    got.w = __shfl_xor_sync(0xffffffffu, send.w, mask);
+    if (hi_lane)
+      keep_lo = got;
+    else
+      keep_hi = got;
+  };
+  xchg(ch[0], ch[1], gi & 1, 1);
+  xchg(ch[2], ch[3], gi & 1, 1);
+  xchg(ch[0], ch[2], gi & 2, 2);
+  xchg(ch[1], ch[3], gi & 2, 2);
+}
+
 HS_DEV float warp_sumf(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -536,19 +536,42 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
         mbar_wait(smem_u32(&raw_full[rs]), (uint32_t)((seq / NR) & 1));
         const bool row_ok = g >= 0 && g < a.H;
         const unsigned char* src = raw + (size_t)rs * C::RAW_BYTES;
-        for (int e = ct; e < ((kProbe & 1) ? 0 : C::RW * KC); e += C::GCVT_THREADS) {
-          const int p = e / KC, c = e - p * KC;  // chunk fastest: conflict-free raw reads
-          float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-          if (row_ok && p >= clo && p < chi) {
-            const float4* s4 = reinterpret_cast<const float4*>(src + ((size_t)p * CIN + 8 * c) * 4);
-            const float4 v0 = s4[0], v1 = s4[1];
-            v[0] = v0.x, v[1] = v0.y, v[2] = v0.z, v[3] = v0.w, v[4] = v1.x, v[5] = v1.y, v[6] = v1.z, v[7] = v1.w;
-          }
-          uint4 p3[3];
-          split_bf16x3(v, p3[0], p3[1], p3[2]);
-          const size_t off = ((size_t)c * C::XPL + ss * C::RW + staged_px<MODE, MT>(p)) * 16;
+        // elements (pixel, 8-channel chunk) in batches of up to three per thread: the batch's raw-row
+        // loads are issued before any of its conversions and stores (a rolled loop paid one
+        // shared-memory round trip per element, and the compiler cannot hoist loads across the stores
+        // to the staged ring; one converter warp per SM sub-partition has no other warps to hide it)
+        constexpr int NEL = (kProbe & 1) ? 0 : C::RW * KC;
+        constexpr int TRIPS = (NEL + C::GCVT_THREADS - 1) / C::GCVT_THREADS;
+        constexpr int NBW = (MODE == 2 || MT == 64) ? 1 : 3;  // batch width (the M = 64 and transposed tiles: no registers to spare)
+        constexpr int NB = TRIPS < NBW ? (TRIPS > 0 ? TRIPS : 1) : NBW;
+#pragma unroll 1
+        for (int t0 = 0; t0 < TRIPS; t0 += NB) {
+          float4 va[NB][2];
 #pragma unroll
-          for (int part = 0; part < 3; ++part) *reinterpret_cast<uint4*>(xp[part] + off) = p3[part];
+          for (int t = 0; t < NB; ++t) {
+            const int e = ct + (t0 + t) * C::GCVT_THREADS;
+            const int p = e / KC, c = e - p * KC;  // chunk fastest: conflict-free raw reads
+            va[t][0] = va[t][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (t0 + t < TRIPS && e < NEL && row_ok && p >= clo && p < chi) {
+              const float4* s4 = reinterpret_cast<const float4*>(src + ((size_t)p * CIN + 8 * c) * 4);
+              va[t][0] = s4[0];
+              va[t][1] = s4[1];
+            }
+          }
+#pragma unroll
+          for (int t = 0; t < NB; ++t) {
+            const int e = ct + (t0 + t) * C::GCVT_THREADS;
+            if (t0 + t < TRIPS && e < NEL) {
+              const int p = e / KC, c = e - p * KC;
+              const float v[8] = {va[t][0].x, va[t][0].y, va[t][0].z, va[t][0].w,
+                                  va[t][1].x, va[t][1].y, va[t][1].z, va[t][1].w};
+              uint4 p3[3];
+              split_bf16x3(v, p3[0], p3[1], p3[2]);
+              const size_t off = ((size_t)c * C::XPL + ss * C::RW + staged_px<MODE, MT>(p)) * 16;
+#pragma unroll
+              for (int part = 0; part < 3; ++part) *reinterpret_cast<uint4*>(xp[part] + off) = p3[part];
+            }
+          }
         }
         if constexpr (C::ATM) {
           // every converter thread owns TMEM lane m = tile row m (a warp may only
@@ -773,24 +796,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
             }
             ch[q] = v;
           }
-          // 4x4 transpose inside the group: lane gi ends up with chunk gi of the group's four pixels.
-          // Two butterfly stages (partner lane gi ^ 1, then gi ^ 2): each swaps the chunks whose index
-          // bit differs from the lane's bit with the partner's mirrored chunk
-          auto xchg = [&](float4& keep_lo, float4& keep_hi, bool hi_lane, int mask) {
-            float4 send = hi_lane ? keep_lo : keep_hi, got;
-            got.x = __shfl_xor_sync(0xffffffffu, send.x, mask);
-            got.y = __shfl_xor_sync(0xffffffffu, send.y, mask);
-            got.z = __shfl_xor_sync(0xffffffffu, send.z, mask);
-            got.w = __shfl_xor_sync(0xffffffffu, send.w, mask);
-            if (hi_lane)
-              keep_lo = got;
-            else
-              keep_hi = got;
-          };
-          xchg(ch[0], ch[1], gi & 1, 1);
-          xchg(ch[2], ch[3], gi & 1, 1);
-          xchg(ch[0], ch[2], gi & 2, 2);
-          xchg(ch[1], ch[3], gi & 2, 2);
+          group4_transpose(ch, gi);  // lane gi: chunk gi of the group's four pixels
           // now ch[j] holds chunk gi of pixel (lane & ~3) + j: add the side inputs (same layout), and
           // store j writes whole pixels
 #pragma unroll

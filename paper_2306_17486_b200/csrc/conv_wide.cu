@@ -339,14 +339,26 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(const __grid_constan
           if (use > 0) mbar_wait(smem_u32(&a_empty[s]), (use - 1) & 1);
           unsigned char* slot = aring + (size_t)s * C::A_SLOT;
           const unsigned char* raw = araw + (size_t)rs * C::RAW_SLOT;
+          // every item's raw loads first, then the conversions and stores (the compiler cannot hoist
+          // the loads of a later item over the earlier item's stores to the A ring)
+          constexpr int NI = (HS_WIDE_PROBE & 4) ? 0 : IPT;
+          float4 va[NI > 0 ? NI : 1][2];
 #pragma unroll
-          for (int k = 0; k < ((HS_WIDE_PROBE & 4) ? 0 : IPT); ++k) {
+          for (int k = 0; k < NI; ++k) {
+            const int e = t + k * NT;
+            const int p = e % C::RW, h = e / C::RW;
+            if (e < 2 * C::RW) {
+              va[k][0] = *reinterpret_cast<const float4*>(raw + (size_t)p * 64 + h * 32);
+              va[k][1] = *reinterpret_cast<const float4*>(raw + (size_t)p * 64 + h * 32 + 16);
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < NI; ++k) {
             const int e = t + k * NT;
             if (e >= 2 * C::RW) break;
             const int p = e % C::RW, h = e / C::RW;
-            const float4 v0 = *reinterpret_cast<const float4*>(raw + (size_t)p * 64 + h * 32);
-            const float4 v1 = *reinterpret_cast<const float4*>(raw + (size_t)p * 64 + h * 32 + 16);
-            const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+            const float v[8] = {va[k][0].x, va[k][0].y, va[k][0].z, va[k][0].w,
+                                va[k][1].x, va[k][1].y, va[k][1].z, va[k][1].w};
             uint4 q0, q1, q2;
             split_bf16x3(v, q0, q1, q2);
             const size_t off = (size_t)h * C::A_PLANE + (size_t)staged<MODE>(p) * 16;
