@@ -175,8 +175,11 @@ HS_DEV void arn_dispatch(int nv, const SolveDims& d, const ArnArgs& g, double (&
   arn_sweep<MODE, NVMAX>(d, g, acc, bad);
 }
 
+#ifndef HS_ARN_MINB
+#define HS_ARN_MINB 1
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(NT) k_arnoldi(SolveDims d, SolveBuffers s, int nchunks) {
+__global__ void __launch_bounds__(NT, HS_ARN_MINB) k_arnoldi(SolveDims d, SolveBuffers s, int nchunks) {
   __shared__ double red[PST * (NT / 32 + 1)];
   __shared__ double2 s_coef[kMaxRestart + 1];
   const int blk = blockIdx.x, chunk = blockIdx.y, b = blockIdx.z;
