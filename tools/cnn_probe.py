@@ -22,7 +22,10 @@ def main():
     ap.add_argument("--B", type=int, default=64)
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--profile", action="store_true", help="also report the per-tag breakdown (events per launch)")
+    ap.add_argument("--lib", default="", help="a measurement variant instead of the product library")
     a = ap.parse_args()
+    if a.lib:
+        _lib.LIB_PATH = os.path.abspath(a.lib)
     cfg = problems.make_config(a.config)
     net = network.EncoderSolverNet.seeded(cfg.cnn_channels, seed=0)
     dn, enc = network.device_network(net, cfg.models, None, None)

@@ -17,7 +17,10 @@ ap.add_argument("--C", type=int, default=32)
 ap.add_argument("--h", type=int, default=64)
 ap.add_argument("--w", type=int, default=64)
 ap.add_argument("--iters", type=int, default=10)
+ap.add_argument("--lib", default="", help="a measurement variant instead of the product library")
 a = ap.parse_args()
+if a.lib:
+    _lib.LIB_PATH = os.path.abspath(a.lib)
 lib = _lib.load()
 x = torch.randn(a.B, a.C, a.h, a.w, dtype=torch.complex64, device="cuda")
 spec = torch.randn(a.C, 2 * a.h, 2 * a.w, dtype=torch.complex64, device="cuda")
