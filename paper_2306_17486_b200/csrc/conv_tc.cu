@@ -835,7 +835,26 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
       // (wide transposed tiles have no registers to spare: there the two are summed at load)
       constexpr bool SPLIT = C::NACC * EH <= 16;
       constexpr int RK = SPLIT ? C::NACC : 1, RQ = SPLIT ? EH / 4 : 1;
+      // TR (16 channels per warp-half at M = 128, one accumulator): the four lanes of a group transpose
+      // their pixels' 16-byte chunks before storing, so every store writes whole 64-byte pixel halves,
+      // and the side inputs are loaded in that layout (lane: chunk gi of the group's pixels 0..3)
+      constexpr bool TR = EH == 16 && C::NACC == 1 && MT == 128;
+      const bool tr = TR && !a.planar;
+      const int gi = lane & 3;
       auto fetch = [&](int oy, float4(&pa)[C::NACC][EH / 4], float4(&pr)[RK][RQ]) {
+        if (TR && tr) {
+          const size_t gpix = (size_t)oy * a.Wo + U.xb * MT + m - gi;
+#pragma unroll
+          for (int j = 0; j < EH / 4; ++j) {
+            const size_t off = (gpix + j) * COUT + n_base + 4 * gi;
+            pa[0][j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (add && !(kProbe & 256)) pa[0][j] = __ldg(reinterpret_cast<const float4*>(add + off));
+            float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (a.residual) r = __ldg(reinterpret_cast<const float4*>(a.residual + (size_t)U.b * a.Ho * a.Wo * COUT + off));
+            pr[0][SPLIT ? j : 0] = r;
+          }
+          return;
+        }
 #pragma unroll
         for (int k = 0; k < C::NACC; ++k) {
           const int ox = MODE == 2 ? 2 * (U.xb * MT + m) + k : U.xb * MT + m;
@@ -888,7 +907,35 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&acc_empty[acc]));  // TMEM free; finish from registers
-        if (lane_ok && !(kProbe & 4)) {
+        if (TR && tr && !(kProbe & 4)) {
+          float4 ch[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 bs = *reinterpret_cast<const float4*>(s_bias + h * EH + 4 * q);
+            const uint64_t o01 = add2(pkf(t[0][4 * q], t[0][4 * q + 1]), pkf(bs.x, bs.y));
+            const uint64_t o23 = add2(pkf(t[0][4 * q + 2], t[0][4 * q + 3]), pkf(bs.z, bs.w));
+            float4 o = make_float4(lo_f(o01), hi_f(o01), lo_f(o23), hi_f(o23));
+            if (a.softplus) {
+              o.x = softplus_fast(o.x);
+              o.y = softplus_fast(o.y);
+              o.z = softplus_fast(o.z);
+              o.w = softplus_fast(o.w);
+            }
+            ch[q] = o;
+          }
+          group4_transpose(ch, gi);
+          const size_t gpix = (size_t)oy * a.Wo + U.xb * MT + m - gi;
+          float* yb = a.y + (size_t)U.b * a.Ho * a.Wo * COUT + n_base + 4 * gi;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 ad = pre_a[0][j];
+            const float4 rs = SPLIT ? pre_r[0][SPLIT ? j : 0] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const uint64_t a01 = add2(pkf(ad.x, ad.y), pkf(rs.x, rs.y)), a23 = add2(pkf(ad.z, ad.w), pkf(rs.z, rs.w));
+            const uint64_t q01 = add2(pkf(ch[j].x, ch[j].y), a01), q23 = add2(pkf(ch[j].z, ch[j].w), a23);
+            if (!(kProbe & 64))
+              *reinterpret_cast<float4*>(yb + (gpix + j) * COUT) = make_float4(lo_f(q01), hi_f(q01), lo_f(q23), hi_f(q23));
+          }
+        } else if (lane_ok && !(kProbe & 4)) {
 #pragma unroll
           for (int k = 0; k < C::NACC; ++k) {
             const int ox = MODE == 2 ? 2 * (U.xb * MT + m) + k : U.xb * MT + m;
