@@ -838,10 +838,27 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
       // TR (16 channels per warp-half at M = 128, one accumulator): the four lanes of a group transpose
       // their pixels' 16-byte chunks before storing, so every store writes whole 64-byte pixel halves,
       // and the side inputs are loaded in that layout (lane: chunk gi of the group's pixels 0..3)
-      constexpr bool TR = EH == 16 && C::NACC == 1 && MT == 128;
-      const bool tr = TR && !a.planar;
-      const int gi = lane & 3;
+      // (M = 64: lanes 16-31 mirror lanes 0-15 and do not store).
+      // TR2 (transposed, 8 channels per warp-half, two output-column accumulators): lane pairs swap
+      // chunks so that each store writes whole 32-byte pixel halves (a full sector per lane pair)
+      constexpr bool TR = EH == 16 && C::NACC == 1;
+      constexpr bool TR2 = MODE == 2 && EH == 8 && C::NACC == 2 && MT == 128;
+      const bool tr = (TR || TR2) && !a.planar;
+      const int gi = lane & 3, pi = lane & 1;
       auto fetch = [&](int oy, float4(&pa)[C::NACC][EH / 4], float4(&pr)[RK][RQ]) {
+        if (TR2 && tr) {  // pixel P + j (P = the pair's first output column), chunk pi
+          const size_t prow = (size_t)oy * a.Wo + 2 * (U.xb * MT + m - pi);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const size_t off = (prow + j) * COUT + n_base + 4 * pi;
+            float4 ad = make_float4(0.f, 0.f, 0.f, 0.f), r = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (add && !(kProbe & 256)) ad = __ldg(reinterpret_cast<const float4*>(add + off));
+            if (a.residual) r = __ldg(reinterpret_cast<const float4*>(a.residual + (size_t)U.b * a.Ho * a.Wo * COUT + off));
+            pa[(j >> 1) % C::NACC][(j & 1) % (EH / 4)] = ad;
+            pr[SPLIT ? (j >> 1) % RK : 0][SPLIT ? (j & 1) % RQ : 0] = r;
+          }
+          return;
+        }
         if (TR && tr) {
           const size_t gpix = (size_t)oy * a.Wo + U.xb * MT + m - gi;
 #pragma unroll
@@ -907,7 +924,54 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&acc_empty[acc]));  // TMEM free; finish from registers
-        if (TR && tr && !(kProbe & 4)) {
+        if (TR2 && tr && !(kProbe & 4)) {
+          // chunks A, B (column 2m: channels 0-3, 4-7 of the half) and C, D (column 2m + 1)
+          float4 ch[4];
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int k2 = k % C::NACC;
+              const float4 bs = *reinterpret_cast<const float4*>(s_bias + h * EH + 4 * q);
+              const uint64_t o01 = add2(pkf(t[k2][4 * q], t[k2][4 * q + 1]), pkf(bs.x, bs.y));
+              const uint64_t o23 = add2(pkf(t[k2][4 * q + 2], t[k2][4 * q + 3]), pkf(bs.z, bs.w));
+              float4 o = make_float4(lo_f(o01), hi_f(o01), lo_f(o23), hi_f(o23));
+              if (a.softplus) {
+                o.x = softplus_fast(o.x);
+                o.y = softplus_fast(o.y);
+                o.z = softplus_fast(o.z);
+                o.w = softplus_fast(o.w);
+              }
+              ch[2 * k + q] = o;
+            }
+          // even lane keeps A, C and receives the odd lane's A, C; odd keeps B, D and receives the even's
+          float4 s0 = pi ? ch[0] : ch[1], s1 = pi ? ch[2] : ch[3], g0, g1;
+          g0.x = __shfl_xor_sync(0xffffffffu, s0.x, 1);
+          g0.y = __shfl_xor_sync(0xffffffffu, s0.y, 1);
+          g0.z = __shfl_xor_sync(0xffffffffu, s0.z, 1);
+          g0.w = __shfl_xor_sync(0xffffffffu, s0.w, 1);
+          g1.x = __shfl_xor_sync(0xffffffffu, s1.x, 1);
+          g1.y = __shfl_xor_sync(0xffffffffu, s1.y, 1);
+          g1.z = __shfl_xor_sync(0xffffffffu, s1.z, 1);
+          g1.w = __shfl_xor_sync(0xffffffffu, s1.w, 1);
+          float4 outv[4];  // chunk pi of output columns P .. P + 3
+          outv[0] = pi ? g0 : ch[0];
+          outv[1] = pi ? g1 : ch[2];
+          outv[2] = pi ? ch[1] : g0;
+          outv[3] = pi ? ch[3] : g1;
+          const size_t prow = (size_t)oy * a.Wo + 2 * (U.xb * MT + m - pi);
+          float* yb = a.y + (size_t)U.b * a.Ho * a.Wo * COUT + n_base + 4 * pi;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 ad = pre_a[(j >> 1) % C::NACC][(j & 1) % (EH / 4)];
+            const float4 rs = SPLIT ? pre_r[SPLIT ? (j >> 1) % RK : 0][SPLIT ? (j & 1) % RQ : 0]
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+            const uint64_t a01 = add2(pkf(ad.x, ad.y), pkf(rs.x, rs.y)), a23 = add2(pkf(ad.z, ad.w), pkf(rs.z, rs.w));
+            const uint64_t q01 = add2(pkf(outv[j].x, outv[j].y), a01), q23 = add2(pkf(outv[j].z, outv[j].w), a23);
+            if (!(kProbe & 64))
+              *reinterpret_cast<float4*>(yb + (prow + j) * COUT) = make_float4(lo_f(q01), hi_f(q01), lo_f(q23), hi_f(q23));
+          }
+        } else if (TR && tr && !(kProbe & 4)) {
           float4 ch[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -932,7 +996,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
             const float4 rs = SPLIT ? pre_r[0][SPLIT ? j : 0] : make_float4(0.f, 0.f, 0.f, 0.f);
             const uint64_t a01 = add2(pkf(ad.x, ad.y), pkf(rs.x, rs.y)), a23 = add2(pkf(ad.z, ad.w), pkf(rs.z, rs.w));
             const uint64_t q01 = add2(pkf(ch[j].x, ch[j].y), a01), q23 = add2(pkf(ch[j].z, ch[j].w), a23);
-            if (!(kProbe & 64))
+            if (lane_ok && !(kProbe & 64))
               *reinterpret_cast<float4*>(yb + (gpix + j) * COUT) = make_float4(lo_f(q01), hi_f(q01), lo_f(q23), hi_f(q23));
           }
         } else if (lane_ok && !(kProbe & 4)) {
