@@ -505,9 +505,14 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(const __grid_constan
       constexpr int SEG = 16, NSEG = EH / SEG;
       const float* side = add ? add : a.residual;
       const bool side_res = !add;  // addend rows are indexed by pixel, residual rows by (b, pixel)
-      auto side_ptr = [&](int r, int k, int sg) -> const float4* {
-        const int ox = MODE == 2 ? 2 * (128 * P.xb + m) + k : 128 * P.xb + m;
-        const size_t pix = (size_t)(P.oy0 + r) * a.Wo + ox;
+      // NHWC stores: the four lanes of a group transpose their pixels' 16-byte chunks (group4_transpose),
+      // so every store / side load instruction moves whole 64-byte segments; lane gi then owns chunk gi
+      // of the group's pixels j = 0..3 (tile pixel m - gi + j)
+      const bool tr = !a.planar;
+      const int gi = lane & 3;
+      auto ox_of = [&](int mm, int k) { return MODE == 2 ? 2 * (128 * P.xb + mm) + k : 128 * P.xb + mm; };
+      auto side_ptr = [&](int r, int k, int sg, int mm) -> const float4* {
+        const size_t pix = (size_t)(P.oy0 + r) * a.Wo + ox_of(mm, k);
         const size_t base = side_res ? ((size_t)P.b * a.Ho * a.Wo + pix) * COUT : pix * COUT;
         return reinterpret_cast<const float4*>(side + base + hc * EH + sg * SEG);
       };
@@ -516,9 +521,14 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(const __grid_constan
 #pragma unroll
         for (int q = 0; q < SEG / 4; ++q) dst[q] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (side && P.oy0 + r < a.Ho) {
-          const float4* sp = side_ptr(r, k, sg);
+          if (tr) {
 #pragma unroll
-          for (int q = 0; q < SEG / 4; ++q) dst[q] = __ldg(sp + q);
+            for (int j = 0; j < SEG / 4; ++j) dst[j] = __ldg(side_ptr(r, k, sg, m - gi + j) + gi);
+          } else {
+            const float4* sp = side_ptr(r, k, sg, m);
+#pragma unroll
+            for (int q = 0; q < SEG / 4; ++q) dst[q] = __ldg(sp + q);
+          }
         }
       };
       if (HS_WIDE_PROBE & 1) side = nullptr;  // probe build only
@@ -567,6 +577,24 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(const __grid_constan
           }
         }
         if (oy >= a.Ho || (HS_WIDE_PROBE & 1)) continue;  // (warp-uniform: every lane has the same row)
+        if (tr) {
+          float4 ch[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) ch[q] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+          group4_transpose(ch, gi);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            ch[j].x += sd[j].x, ch[j].y += sd[j].y, ch[j].z += sd[j].z, ch[j].w += sd[j].w;
+            const size_t pj = (size_t)oy * a.Wo + ox_of(m - gi + j, k);
+            const size_t oj = ((size_t)P.b * a.Ho * a.Wo + pj) * COUT + hc * EH + sg * SEG + 4 * gi;
+            if (add && a.residual) {
+              const float4 rv = __ldg(reinterpret_cast<const float4*>(a.residual + oj));
+              ch[j].x += rv.x, ch[j].y += rv.y, ch[j].z += rv.z, ch[j].w += rv.w;
+            }
+            *reinterpret_cast<float4*>(a.y + oj) = ch[j];
+          }
+          continue;
+        }
 #pragma unroll
         for (int q = 0; q < SEG / 4; ++q) {
           o[4 * q] += sd[q].x, o[4 * q + 1] += sd[q].y, o[4 * q + 2] += sd[q].z, o[4 * q + 3] += sd[q].w;
