@@ -23,10 +23,7 @@ namespace hs {
 namespace {
 
 constexpr int NT = 128;
-#ifndef HS_ARN_KC
-#define HS_ARN_KC 10
-#endif
-constexpr int KC = HS_ARN_KC;     // basis vectors per chunk in a dot pass (registers vs w recomputes)
+constexpr int KC = 10;            // basis vectors per chunk in a dot pass (registers vs w recomputes)
 constexpr int PST = 2 * KC + 1;   // doubles per partial record
 constexpr int kChunks = (kMaxRestart + KC - 1) / KC;
 
@@ -88,98 +85,52 @@ struct ArnArgs {
 // together: DOT / REDOT dot v_{k0} .. v_{k0+NV-1} (REDOT first subtracts every
 // k < J with a runtime loop; it runs only where krylov.py:105 triggers), ORTH /
 // ORTH2 subtract v_0 .. v_{NV-1} (NV = 0: runtime J).
-// The grid-stride walk keeps the node's (row, column) by stepping (no integer
-// division per node), and U nodes are processed per trip so U x NV basis loads
-// are in flight together.
-#ifndef HS_ARN_UNROLL
-#define HS_ARN_UNROLL 1
-#endif
-template <int MODE, int NV>
-HS_DEV void arn_node(const SolveDims& d, const ArnArgs& g, double (&acc)[PST], int& bad, int p, int i, int jj) {
-  const long long N = g.N;
-  auto ldz_b = [&](int q) { return ldz(g.zb + q); };
-  if constexpr (MODE == DOT || MODE == REDOT || MODE == ORTH) {
-    const float2* vp = g.Vb + (long long)g.k0 * N + p;
-    float2 v[NV > 0 ? NV : 1];
-#pragma unroll
-    for (int kk = 0; kk < NV; ++kk) v[kk] = vp[kk * N];
-    double2 w = apply_true(ldz_b, g.c, d.nx, d.ny, p, i, jj, d.h2, d.inv_h2);
-    if (MODE == DOT) {
-      if (!isfinite(w.x) || !isfinite(w.y)) bad = 1;
-      if (g.chunk == 0) acc[2 * KC] += w.x * w.x + w.y * w.y;
-    } else {
-      for (int k = 0; k < g.J; ++k) w = zsub(w, zmul(g.coef[k], ldz(g.Vb + (long long)k * N + p)));
-      if (MODE == ORTH && g.chunk == 0) {
-        const_cast<float2*>(g.Vb)[(long long)g.J * N + p] = d2f(w);
-        acc[2 * KC] += w.x * w.x + w.y * w.y;
-      }
-    }
-#pragma unroll
-    for (int kk = 0; kk < NV; ++kk) {
-      const double2 dv = zcmul(f2d(v[kk]), w);
-      acc[2 * kk] += dv.x;
-      acc[2 * kk + 1] += dv.y;
-    }
-  } else {
-    double2 w = apply_true(ldz_b, g.c, d.nx, d.ny, p, i, jj, d.h2, d.inv_h2);
-    if constexpr (NV > 0) {
-      float2 v[NV > 0 ? NV : 1];
-#pragma unroll
-      for (int k = 0; k < NV; ++k) v[k] = g.Vb[(long long)k * N + p];
-#pragma unroll
-      for (int k = 0; k < NV; ++k) w = zsub(w, zmul(g.coef[k], f2d(v[k])));
-    } else {
-      for (int k = 0; k < g.J; ++k) w = zsub(w, zmul(g.coef[k], ldz(g.Vb + (long long)k * N + p)));
-    }
-    const_cast<float2*>(g.Vb)[(long long)g.J * N + p] = d2f(w);
-    acc[2 * KC] += w.x * w.x + w.y * w.y;
-  }
-}
-
 template <int MODE, int NV>
 HS_DEV void arn_sweep(const SolveDims& d, const ArnArgs& g, double (&acc)[PST], int& bad) {
-  const int ny = d.ny, st = g.stride;
-  const int sq = st / ny, sr = st - sq * ny;  // the stride as (rows, columns)
-  int p = g.p0, i = p / ny, jj = p - i * ny;
-  auto step = [&](int& pp, int& ii, int& jc) {
-    pp += st;
-    ii += sq;
-    jc += sr;
-    if (jc >= ny) {
-      jc -= ny;
-      ++ii;
-    }
-  };
-  if constexpr (HS_ARN_UNROLL == 2) {
-    for (; p + st < g.N;) {
-      int p1 = p, i1 = i, j1 = jj;
-      step(p1, i1, j1);
-      arn_node<MODE, NV>(d, g, acc, bad, p, i, jj);
-      arn_node<MODE, NV>(d, g, acc, bad, p1, i1, j1);
-      p = p1, i = i1, jj = j1;
-      step(p, i, jj);
+  const long long N = g.N;
+  auto ldz_b = [&](int q) { return ldz(g.zb + q); };
+  for (int p = g.p0; p < g.N; p += g.stride) {
+    const int i = p / d.ny, jj = p - i * d.ny;
+    if constexpr (MODE == DOT || MODE == REDOT || MODE == ORTH) {
+      float2 v[NV > 0 ? NV : 1];
+#pragma unroll
+      for (int kk = 0; kk < NV; ++kk) v[kk] = g.Vb[(long long)(g.k0 + kk) * N + p];
+      double2 w = apply_true(ldz_b, g.c, d.nx, d.ny, p, i, jj, d.h2, d.inv_h2);
+      if (MODE == DOT) {
+        if (!isfinite(w.x) || !isfinite(w.y)) bad = 1;
+        if (g.chunk == 0) acc[2 * KC] += w.x * w.x + w.y * w.y;
+      } else {
+        for (int k = 0; k < g.J; ++k) w = zsub(w, zmul(g.coef[k], ldz(g.Vb + (long long)k * N + p)));
+        if (MODE == ORTH && g.chunk == 0) {
+          const_cast<float2*>(g.Vb)[(long long)g.J * N + p] = d2f(w);
+          acc[2 * KC] += w.x * w.x + w.y * w.y;
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < NV; ++kk) {
+        const double2 dv = zcmul(f2d(v[kk]), w);
+        acc[2 * kk] += dv.x;
+        acc[2 * kk + 1] += dv.y;
+      }
+    } else {
+      double2 w = apply_true(ldz_b, g.c, d.nx, d.ny, p, i, jj, d.h2, d.inv_h2);
+      if constexpr (NV > 0) {
+        float2 v[NV > 0 ? NV : 1];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) v[k] = g.Vb[(long long)k * N + p];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) w = zsub(w, zmul(g.coef[k], f2d(v[k])));
+      } else {
+        for (int k = 0; k < g.J; ++k) w = zsub(w, zmul(g.coef[k], ldz(g.Vb + (long long)k * N + p)));
+      }
+      const_cast<float2*>(g.Vb)[(long long)g.J * N + p] = d2f(w);
+      acc[2 * KC] += w.x * w.x + w.y * w.y;
     }
   }
-  for (; p < g.N; step(p, i, jj)) arn_node<MODE, NV>(d, g, acc, bad, p, i, jj);
 }
 
-// arn_sweep with the chunk's vector count as a compile-time constant (1..NVMAX)
-template <int MODE, int NVMAX>
-HS_DEV void arn_dispatch(int nv, const SolveDims& d, const ArnArgs& g, double (&acc)[PST], int& bad) {
-  if constexpr (NVMAX > 1) {
-    if (nv < NVMAX) {
-      arn_dispatch<MODE, NVMAX - 1>(nv, d, g, acc, bad);
-      return;
-    }
-  }
-  arn_sweep<MODE, NVMAX>(d, g, acc, bad);
-}
-
-#ifndef HS_ARN_MINB
-#define HS_ARN_MINB 1
-#endif
 template <int MODE>
-__global__ void __launch_bounds__(NT, HS_ARN_MINB) k_arnoldi(SolveDims d, SolveBuffers s, int nchunks) {
+__global__ void __launch_bounds__(NT) k_arnoldi(SolveDims d, SolveBuffers s, int nchunks) {
   __shared__ double red[PST * (NT / 32 + 1)];
   __shared__ double2 s_coef[kMaxRestart + 1];
   const int blk = blockIdx.x, chunk = blockIdx.y, b = blockIdx.z;
@@ -211,7 +162,18 @@ __global__ void __launch_bounds__(NT, HS_ARN_MINB) k_arnoldi(SolveDims d, SolveB
   ArnArgs g{Vb, zb, c, s_coef, N, J, k0, chunk, blk * NT + (int)threadIdx.x, d.nblk * NT};
   if (MODE == DOT || MODE == REDOT || MODE == ORTH) {
     // vectors of this chunk, a compile-time count
-    arn_dispatch<MODE, KC>(min(KC, J - k0), d, g, acc, bad);
+    switch (min(KC, J - k0)) {
+      case 1: arn_sweep<MODE, 1>(d, g, acc, bad); break;
+      case 2: arn_sweep<MODE, 2>(d, g, acc, bad); break;
+      case 3: arn_sweep<MODE, 3>(d, g, acc, bad); break;
+      case 4: arn_sweep<MODE, 4>(d, g, acc, bad); break;
+      case 5: arn_sweep<MODE, 5>(d, g, acc, bad); break;
+      case 6: arn_sweep<MODE, 6>(d, g, acc, bad); break;
+      case 7: arn_sweep<MODE, 7>(d, g, acc, bad); break;
+      case 8: arn_sweep<MODE, 8>(d, g, acc, bad); break;
+      case 9: arn_sweep<MODE, 9>(d, g, acc, bad); break;
+      default: arn_sweep<MODE, 10>(d, g, acc, bad); break;
+    }
   } else {
     // w -= sum_k coef_k v_k over every k < J: the runtime loop measured faster
     // than the fully unrolled one (159 vs 139 us per pass at C2)
