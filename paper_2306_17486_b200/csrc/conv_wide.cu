@@ -391,6 +391,9 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(const __grid_constan
     }
   } else if (warp == kWarpMma) {
     // ================= MMA issuer
+    // The per-row bookkeeping is hoisted out of the tap loops: the A descriptors of a chunk's rows are
+    // formed once, the staged-row waits happen once per tap row, and the taps (fully unrolled) issue
+    // each tile's three (G = 3) or five (G = 2) MMAs from one asm block with one elect.
     constexpr uint32_t I1 = idesc_bf16(128, COUT), I2 = idesc_bf16(128, 2 * COUT), I3 = idesc_bf16(128, 3 * COUT);
     constexpr uint32_t WROW = (uint32_t)COUT * 16;  // byte offset of weight part p: p * WROW
     const uint32_t a_base = smem_u32(aring), b_base = smem_u32(bring);
@@ -404,54 +407,75 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(const __grid_constan
       const uint32_t dset = tmem + set * C::SET_COLS;
       uint32_t started = 0;  // bit (r * NACC + k): accumulator written
       for (int c = 0; c < NCH; ++c) {
+        uint32_t arow[NROWS];  // descriptor low word of each row's part 0, pixel 0
+#pragma unroll
+        for (int i = 0; i < NROWS; ++i) arow[i] = desc_lo(a_base + ((aseq + (uint32_t)i) % NAS) * C::A_SLOT, C::A_PLANE);
         int have = -1;  // highest input row of this chunk known to be staged
+#pragma unroll
         for (int ky = 0; ky < 3; ++ky) {
+          int need = -1;
+#pragma unroll
+          for (int r = 0; r < R; ++r) need = tap_row<MODE>(r, ky) > need ? tap_row<MODE>(r, ky) : need;
+          for (; have < need; ++have) {
+            const uint32_t sq = aseq + (uint32_t)(have + 1);
+            mbar_wait(smem_u32(&a_full[sq % NAS]), (sq / NAS) & 1);
+          }
+          tc_fence_after();
+#pragma unroll
           for (int kx = 0; kx < 3; ++kx, ++bseq) {
             const uint32_t bs = bseq % NBS;
             if (!(HS_WIDE_PROBE & 8)) mbar_wait(smem_u32(&b_full[bs]), (bseq / NBS) & 1);
-            const uint32_t bsl = b_base + bs * C::B_SLOT;
+            const uint32_t w0 = desc_lo(b_base + bs * C::B_SLOT, C::B_PLANE);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
               const int i = tap_row<MODE>(r, ky);
               if (i < 0) continue;
-              for (; have < i; ++have) {
-                const uint32_t sq = aseq + (uint32_t)(have + 1);
-                mbar_wait(smem_u32(&a_full[sq % NAS]), (sq / NAS) & 1);
-              }
-              tc_fence_after();
-              const uint32_t asl = a_base + ((aseq + (uint32_t)i) % NAS) * C::A_SLOT + (uint32_t)tap_px<MODE>(kx) * 16;
               const int k = tap_acc<MODE>(kx);
               const uint32_t bit = 1u << (r * C::NACC + k);
               const uint32_t d = dset + (uint32_t)((r * C::NACC + k) * C::ACC_COLS);
-              const uint32_t a0 = desc_lo(asl, C::A_PLANE), a1 = desc_lo(asl + 2 * C::A_PLANE, C::A_PLANE),
-                             a2 = desc_lo(asl + 4 * C::A_PLANE, C::A_PLANE);
-              const uint32_t w0 = desc_lo(bsl, C::B_PLANE), w1 = desc_lo(bsl + WROW, C::B_PLANE),
-                             w2 = desc_lo(bsl + 2 * WROW, C::B_PLANE);
+              const uint32_t a0 = arow[i] + (uint32_t)tap_px<MODE>(kx);  // 16-byte pixel steps
+              const uint32_t acc = (started & bit) ? 1u : 0u;
               if constexpr ((HS_WIDE_PROBE & 2) != 0) {
               } else if constexpr (C::G == 3) {
-                mma_bf16(d, a0, kDescHi, w0, kDescHi, I3, (started & bit) ? 1u : 0u);  // g0 g1 g2 += a0 [w0 w1 w2]
-                mma_bf16(d + COUT, a1, kDescHi, w0, kDescHi, I2, 1u);                  // g1 g2 += a1 [w0 w1]
-                mma_bf16(d + 2 * COUT, a2, kDescHi, w0, kDescHi, I1, 1u);              // g2 += a2 w0
+                // g0 g1 g2 += a0 [w0 w1 w2];  g1 g2 += a1 [w0 w1];  g2 += a2 w0
+                asm volatile(
+                    "{\n\t.reg .pred p, t, e;\n\t.reg .b64 da, db;\n\t.reg .b32 al, dd;\n\t"
+                    "setp.ne.b32 p, %3, 0;\n\tsetp.eq.b32 t, %3, %3;\n\telect.sync _|e, 0xffffffff;\n\t"
+                    "mov.b64 db, {%2, %4};\n\tmov.b64 da, {%1, %4};\n\t"
+                    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, p;\n\t"
+                    "add.u32 al, %1, %8;\n\tmov.b64 da, {al, %4};\n\tadd.u32 dd, %0, %10;\n\t"
+                    "@e tcgen05.mma.cta_group::1.kind::f16 [dd], da, db, %6, t;\n\t"
+                    "add.u32 al, %1, %9;\n\tmov.b64 da, {al, %4};\n\tadd.u32 dd, %0, %11;\n\t"
+                    "@e tcgen05.mma.cta_group::1.kind::f16 [dd], da, db, %7, t;\n\t}\n" ::"r"(d),
+                    "r"(a0), "r"(w0), "r"(acc), "n"(kDescHi), "n"(I3), "n"(I2), "n"(I1),
+                    "n"((2 * C::A_PLANE) >> 4), "n"((4 * C::A_PLANE) >> 4), "n"(COUT), "n"(2 * COUT));
               } else {
-                mma_bf16(d, a0, kDescHi, w0, kDescHi, I2, (started & bit) ? 1u : 0u);  // g0 g1 += a0 [w0 w1]
-                mma_bf16(d + COUT, a0, kDescHi, w2, kDescHi, I1, 1u);                  // g1 += a0 w2
-                mma_bf16(d + COUT, a1, kDescHi, w0, kDescHi, I1, 1u);                  // g1 += a1 w0
-                mma_bf16(d + COUT, a1, kDescHi, w1, kDescHi, I1, 1u);                  // g1 += a1 w1
-                mma_bf16(d + COUT, a2, kDescHi, w0, kDescHi, I1, 1u);                  // g1 += a2 w0
+                // g0 g1 += a0 [w0 w1];  g1 += a0 w2, a1 w0, a1 w1, a2 w0
+                asm volatile(
+                    "{\n\t.reg .pred p, t, e;\n\t.reg .b64 da, db;\n\t.reg .b32 al, bl, dd;\n\t"
+                    "setp.ne.b32 p, %3, 0;\n\tsetp.eq.b32 t, %3, %3;\n\telect.sync _|e, 0xffffffff;\n\t"
+                    "mov.b64 db, {%2, %4};\n\tmov.b64 da, {%1, %4};\n\tadd.u32 dd, %0, %10;\n\t"
+                    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, p;\n\t"
+                    "add.u32 bl, %2, %9;\n\tmov.b64 db, {bl, %4};\n\t"
+                    "@e tcgen05.mma.cta_group::1.kind::f16 [dd], da, db, %6, t;\n\t"
+                    "add.u32 al, %1, %7;\n\tmov.b64 da, {al, %4};\n\tmov.b64 db, {%2, %4};\n\t"
+                    "@e tcgen05.mma.cta_group::1.kind::f16 [dd], da, db, %6, t;\n\t"
+                    "add.u32 bl, %2, %11;\n\tmov.b64 db, {bl, %4};\n\t"
+                    "@e tcgen05.mma.cta_group::1.kind::f16 [dd], da, db, %6, t;\n\t"
+                    "add.u32 al, %1, %8;\n\tmov.b64 da, {al, %4};\n\tmov.b64 db, {%2, %4};\n\t"
+                    "@e tcgen05.mma.cta_group::1.kind::f16 [dd], da, db, %6, t;\n\t}\n" ::"r"(d),
+                    "r"(a0), "r"(w0), "r"(acc), "n"(kDescHi), "n"(I2), "n"(I1),
+                    "n"((2 * C::A_PLANE) >> 4), "n"((4 * C::A_PLANE) >> 4), "n"((2 * WROW) >> 4), "n"(COUT),
+                    "n"(WROW >> 4));
               }
               started |= bit;
             }
             if (!(HS_WIDE_PROBE & 8)) mma_commit(smem_u32(&b_empty[bs]));  // the piece is free once its MMAs completed
           }
           // input rows whose last reader was this tap row go back to the converters
+#pragma unroll
           for (int i = 0; i < NROWS; ++i)
-            if (last_ky<MODE, R>(i) == ky) {
-              for (; have < i; ++have) {  // (a row no tap reads yet must still be seen staged first)
-                const uint32_t sq = aseq + (uint32_t)(have + 1);
-                mbar_wait(smem_u32(&a_full[sq % NAS]), (sq / NAS) & 1);
-              }
-              mma_commit(smem_u32(&a_empty[(aseq + (uint32_t)i) % NAS]));
-            }
+            if (last_ky<MODE, R>(i) == ky) mma_commit(smem_u32(&a_empty[(aseq + (uint32_t)i) % NAS]));
         }
         aseq += NROWS;
       }
