@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
   if (warp == C::PROD) {
     // ================= producer: raw row segments, global -> smem (bulk copies)
     if (lane == 0) {
-      long long seq = 0;
+      uint32_t seq = 0;  // 32-bit ring bookkeeping: divisions by the ring depths stay cheap
       for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
         Unit U;
         if (!unit_at<MODE, MT>(a, NSPLIT, u, U)) continue;
@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
           prefetch_in(g + kPrefetch);
           prefetch_out(U.oy0 + (MODE == 0 ? i : (MODE == 1 ? i / 2 : 2 * i)) + kPrefetch);
           const int s = (int)(seq % NR);
-          const long long use = seq / NR;
+          const uint32_t use = seq / NR;
           if (use > 0) mbar_wait(smem_u32(&raw_empty[s]), (uint32_t)((use - 1) & 1));
           const uint32_t bar = smem_u32(&raw_full[s]);
           if (g >= 0 && g < a.H && chi > clo && !(kProbe & 128)) {
@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
     // ================= converters: raw fp32 -> staged bf16x3
     const int cg = (warp - kCvtWarp0) / C::NCVT_BASE;              // converter group: rows seq % NCG == cg
     const int ct = tid - 32 * kCvtWarp0 - cg * C::GCVT_THREADS;    // thread within the group
-    long long seq = 0;
+    uint32_t seq = 0;  // 32-bit ring bookkeeping
     for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
       if (!unit_at<MODE, MT>(a, NSPLIT, u, U)) continue;
@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
         if (C::NCG > 1 && (int)(seq % C::NCG) != cg) continue;
         const int rs = (int)(seq % NR);
         const int ss = C::ATM ? (int)(2 * cg + (seq / C::NCG) % 2) : (int)(seq % NS);
-        const long long suse = seq / NS;
+        const uint32_t suse = seq / NS;
         if (!C::ATM && suse > 0) mbar_wait(smem_u32(&stg_empty[ss]), (uint32_t)((suse - 1) & 1));
         mbar_wait(smem_u32(&raw_full[rs]), (uint32_t)((seq / NR) & 1));
         const bool row_ok = g >= 0 && g < a.H;
@@ -726,7 +726,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
       const int q4 = warp & 3, hg = warp >> 2;
       const int m = q4 * 32 + lane;
       const int gi = lane & 3;  // position inside the group of four lanes
-      long long tile = 0;
+      uint32_t tile = 0;
       for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
         Unit U;
         if (!unit_at<MODE, MT>(a, NSPLIT, u, U)) continue;
@@ -821,7 +821,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
     const int q4 = warp & 3, h = warp >> 2;
     const bool lane_ok = MT == 128 || lane < 16;
     const int m = MT == 128 ? q4 * 32 + lane : q4 * 16 + (lane & 15);
-    long long tile = 0;
+    uint32_t tile = 0;
     for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
       if (!unit_at<MODE, MT>(a, NSPLIT, u, U)) continue;
