@@ -66,7 +66,10 @@ using namespace tc;
 #define HS_WIDE_G64 3
 #endif
 #ifndef HS_WIDE_EXTRA
-#define HS_WIDE_EXTRA 0  // also 32 -> 64 stride 2 and 64 -> 32 transposed (measurement variant)
+#define HS_WIDE_EXTRA 0  // also 64 -> 32 transposed (measurement variant: 1.40 vs 1.09 ms on the resident-weight kernel)
+#endif
+#ifndef HS_WIDE_S2_32
+#define HS_WIDE_S2_32 1  // 32 -> 64 stride 2 on this kernel (measured at C3: 0.85 vs 1.14 ms on the resident-weight kernel)
 #endif
 #ifndef HS_WIDE_RD_MAX
 #define HS_WIDE_RD_MAX 8
@@ -686,8 +689,10 @@ cudaError_t run_split(const float* w, int cin, int cout, void* out, cudaStream_t
   else if (cin == 128 && cout == 128) k_wide_split<128, 128><<<blocks, 256, 0, st>>>(w, static_cast<uint4*>(out));
   else if (cin == 64 && cout == 128) k_wide_split<64, 128><<<blocks, 256, 0, st>>>(w, static_cast<uint4*>(out));
   else if (cin == 128 && cout == 64) k_wide_split<128, 64><<<blocks, 256, 0, st>>>(w, static_cast<uint4*>(out));
-#if HS_WIDE_EXTRA
+#if HS_WIDE_S2_32
   else if (cin == 32 && cout == 64) k_wide_split<32, 64><<<blocks, 256, 0, st>>>(w, static_cast<uint4*>(out));
+#endif
+#if HS_WIDE_EXTRA
   else if (cin == 64 && cout == 32) k_wide_split<64, 32><<<blocks, 256, 0, st>>>(w, static_cast<uint4*>(out));
 #endif
   else return cudaErrorInvalidValue;
@@ -755,13 +760,14 @@ bool conv_wide_supported(int cin, int cout, int stride, int transposed, int H, i
   if ((mode == 2 ? W : Wo) % 128) return false;
   return (mode == 0 && ((cin == 64 && cout == 64) || (cin == 128 && cout == 128))) ||
          (mode == 1 && ((cin == 64 && cout == 128) || (cin == 128 && cout == 128) ||
-                        (HS_WIDE_EXTRA && cin == 32 && cout == 64))) ||
+                        (HS_WIDE_S2_32 && cin == 32 && cout == 64))) ||
          (mode == 2 && ((cin == 128 && cout == 64) || (HS_WIDE_EXTRA && cin == 64 && cout == 32)));
 }
 
 bool conv_wide_eligible(int cin, int cout) {
   return (cin == 64 && cout == 64) || (cin == 128 && cout == 128) || (cin == 64 && cout == 128) ||
-         (cin == 128 && cout == 64) || (HS_WIDE_EXTRA && ((cin == 32 && cout == 64) || (cin == 64 && cout == 32)));
+         (cin == 128 && cout == 64) || (HS_WIDE_S2_32 && cin == 32 && cout == 64) ||
+         (HS_WIDE_EXTRA && cin == 64 && cout == 32);
 }
 
 int conv_wide_register(const float* w, int cin, int cout, cudaStream_t st) {
@@ -817,8 +823,10 @@ bool conv_wide_launch(const float* x, int H, int W, int cin, float* y, int Ho, i
   else if (mode == 1 && cin == 64) launch_wide<64, 128, 1>(a, tm, st);
   else if (mode == 1 && cin == 128) launch_wide<128, 128, 1>(a, tm, st);
   else if (mode == 2 && cout == 64) launch_wide<128, 64, 2>(a, tm, st);
-#if HS_WIDE_EXTRA
+#if HS_WIDE_S2_32
   else if (mode == 1 && cin == 32) launch_wide<32, 64, 1>(a, tm, st);
+#endif
+#if HS_WIDE_EXTRA
   else if (mode == 2 && cout == 32) launch_wide<64, 32, 2>(a, tm, st);
 #endif
   if (tmp) cudaFreeAsync(tmp, st);

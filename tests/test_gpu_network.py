@@ -83,7 +83,8 @@ def test_tconv_shapes(rng, cin, cout, hw):
                                                # multiples of 128; odd row counts leave partial passes
                                                (64, 64, 0, (5, 128)), (64, 64, 0, (9, 256)), (128, 128, 0, (5, 128)),
                                                (128, 128, 0, (3, 256)), (64, 128, 1, (7, 256)), (128, 128, 1, (5, 256)),
-                                               (128, 64, 2, (3, 128)), (128, 128, 2, (3, 128)), (128, 64, 2, (2, 256))])
+                                               (128, 64, 2, (3, 128)), (128, 128, 2, (3, 128)), (128, 64, 2, (2, 256)),
+                                               (32, 64, 1, (7, 256)), (32, 64, 1, (4, 512))])
 def test_tcgen05_conv_matches_oracle(rng, cin, cout, mode, hw):
     """The tcgen05 BF16x3 paths (conv_tc.cu at widths that are multiples of 64, conv_wide.cu for the
     >= 64-channel layers at multiples of 128) against the fp64 oracle, and the SIMT fp32 path."""
