@@ -52,6 +52,12 @@ namespace {
 using namespace tc;
 
 constexpr int kPrefetch = 4;  // rows pulled into L2 ahead of the bulk copies / epilogue loads
+#ifndef HS_TC_PREF_OUT
+#define HS_TC_PREF_OUT 0  // bulk L2 prefetch of the epilogue's side rows (measured: off is faster, 32->16 t 1.37 -> 1.25 ms at C3)
+#endif
+#ifndef HS_TC_PREF_IN
+#define HS_TC_PREF_IN 1  // bulk L2 prefetch of the input rows
+#endif
 constexpr int kNA = 4;    // TMEM accumulators in flight
 constexpr int kEpiWarps = 8, kCvtWarp0 = 8;  // epilogue warps 0-7, converters from warp 8
 constexpr size_t kSmemMax = 232448;
@@ -485,15 +491,15 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
         const int ox0 = MODE == 2 ? 2 * U.xb * MT : U.xb * MT;
         const uint32_t out_bytes = (uint32_t)(MODE == 2 ? 2 * MT : MT) * COUT * 4;
         auto prefetch_in = [&](int g) {
-          if (g <= U.ghi && g >= 0 && g < a.H && chi > clo)
+          if (HS_TC_PREF_IN && g <= U.ghi && g >= 0 && g < a.H && chi > clo)
             prefetch_l2(img + ((size_t)g * a.W + clo) * CIN, (uint32_t)(chi - clo) * CIN * 4);
         };
         int next_out = U.oy0;
         auto prefetch_out = [&](int upto) {
           for (; next_out < min(upto, U.oy1); ++next_out) {
             const size_t off = ((size_t)next_out * a.Wo + ox0) * COUT;
-            if (add) prefetch_l2(add + off, out_bytes);
-            if (res) prefetch_l2(res + off, out_bytes);
+            if (HS_TC_PREF_OUT && add) prefetch_l2(add + off, out_bytes);
+            if (HS_TC_PREF_OUT && res) prefetch_l2(res + off, out_bytes);
           }
         };
         for (int g = U.glo; g < U.glo + kPrefetch; ++g) prefetch_in(g);
