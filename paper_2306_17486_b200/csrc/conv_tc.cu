@@ -181,6 +181,9 @@ struct Cfg {
   // one accumulator TMEM holds six A slots instead of five (the converters run three rows ahead)
   static constexpr int NA = ATM ? 2 : (4 * ACOLS <= 512 ? 4 : 2);
   static constexpr int NTA = ATM ? HS_TC_ATM_NA : NA;                             // TMEM accumulators
+  // more accumulators than barrier pairs would let the MMA warp complete a pair's phase twice ahead of
+  // the epilogue's parity wait (a deadlock)
+  static_assert(NTA <= NA, "one acc_full / acc_empty pair per TMEM accumulator at most");
   static constexpr int AOFF = NTA * ACOLS;                                        // first A slot column
   static constexpr int NSA = ATM ? (512 - AOFF) / SLOT_COLS : 0;                  // TMEM A slots
   static_assert(!ATM || (NSA >= 4 && NSA <= 6), "a tile reads three rows; spare slots keep writes ahead");
