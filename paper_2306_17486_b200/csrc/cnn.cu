@@ -645,12 +645,122 @@ __global__ void __launch_bounds__(kThinThreads) k_conv_thin1(ConvArgs a, const _
   }
 }
 
+// The stem (2 -> 16) as one thread per output pixel: the nine complex inputs come from L1 (neighbouring
+// threads and rows share them), so no rolling three-row window of accumulators is kept and the kernel
+// runs at full occupancy; the weights are in the kernel-parameter constant bank as in k_conv_thin1.
+#ifndef HS_STEM_TR
+#define HS_STEM_TR 0  // measured: the group-of-four transposed stores are slower here (1.17 vs 0.94 ms at C3)
+#endif
+#ifndef HS_STEM_PX
+#define HS_STEM_PX 1
+#endif
+template <int COUT>
+__global__ void __launch_bounds__(256) k_conv_stem_px(ConvArgs a, const __grid_constant__ ThinW<2, COUT> wt) {
+  const int b = blockIdx.z;
+  if (a.active && a.active[b] == nullptr) return;
+  const int x = blockIdx.x * 256 + threadIdx.x, oy = blockIdx.y;
+  // TR: each group of four lanes transposes its pixels' 16-byte chunks so every store / side load
+  // moves whole 64-byte pixels (all lanes stay for the shuffles)
+  constexpr bool TR = HS_STEM_TR && COUT == 16;
+  if (!TR && x >= a.Wo) return;
+  const int gi = threadIdx.x & 3, xg = x - gi;
+  const bool cin_c = a.cx_ld > 0;
+  const float* xb = a.x ? a.x + (long long)b * a.H * a.W * 2 : nullptr;
+  const float2* xc = cin_c ? (a.cx.tab ? a.cx.tab[b] : a.cx.base + (long long)b * a.cx.bstride) : nullptr;
+  const float xcs = cin_c && a.cx.scale ? a.cx.scale[b] : 1.f;
+  const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[b] : 0) : b) * a.addend_bstride
+                              : nullptr;
+  const long long p = (long long)oy * a.Wo + x;
+  float sd[COUT];
+#pragma unroll
+  for (int n = 0; n < COUT; ++n) sd[n] = 0.f;
+  if (TR) {  // chunk gi of pixels xg .. xg + 3
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (xg + j >= a.Wo) continue;
+      const long long pj = ((long long)oy * a.Wo + xg + j) * COUT + 4 * gi;
+      if (add) load_vec<4>(add + pj, &sd[4 * j]);
+      if (a.residual) {
+        float u[4];
+        load_vec<4>(a.residual + (long long)b * a.Ho * a.Wo * COUT + pj, u);
+#pragma unroll
+        for (int n = 0; n < 4; ++n) sd[4 * j + n] += u[n];
+      }
+    }
+  } else if (add) {
+    load_vec<COUT>(add + p * COUT, sd);
+  }
+  if (!TR && a.residual) {
+    float u[COUT];
+    load_vec<COUT>(a.residual + (long long)b * a.Ho * a.Wo * COUT + p * COUT, u);
+#pragma unroll
+    for (int n = 0; n < COUT; ++n) sd[n] += u[n];
+  }
+  float2 xv[3][3];
+#pragma unroll
+  for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+    for (int kx = 0; kx < 3; ++kx) {
+      const int iy = oy + ky - 1, ix = x + kx - 1;
+      float2 v = make_float2(0.f, 0.f);
+      if (iy >= 0 && iy < a.H && ix >= 0 && ix < a.W) {
+        if (cin_c) {
+          const float2 c = xc[(long long)iy * a.cx_ld + ix];
+          v = make_float2(c.x * xcs, c.y * xcs);
+        } else {
+          v = *reinterpret_cast<const float2*>(xb + ((long long)iy * a.W + ix) * 2);
+        }
+      }
+      xv[ky][kx] = v;
+    }
+  unsigned long long acc[COUT / 2];
+#pragma unroll
+  for (int n = 0; n < COUT / 2; ++n) acc[n] = 0ull;
+#pragma unroll
+  for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+    for (int kx = 0; kx < 3; ++kx)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int n = 0; n < COUT / 2; ++n)
+          ffma2(acc[n], c ? xv[ky][kx].y : xv[ky][kx].x, wt.w[((ky * 3 + kx) * 2 + c) * COUT + 2 * n],
+                wt.w[((ky * 3 + kx) * 2 + c) * COUT + 2 * n + 1]);
+  float v[COUT];
+#pragma unroll
+  for (int n = 0; n < COUT; ++n) {
+    float t = ((n & 1) ? hi32(acc[n / 2]) : lo32(acc[n / 2])) + wt.b[n];
+    if (a.softplus) t = softplus_fast(t);
+    v[n] = TR ? t : t + sd[n];
+  }
+  if constexpr (TR) {
+    float4 ch[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ch[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    group4_transpose(ch, gi);
+    float* yrow = a.y + (long long)b * a.Ho * a.Wo * COUT + (long long)oy * a.Wo * COUT;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (xg + j < a.Wo)
+        *reinterpret_cast<float4*>(yrow + (long long)(xg + j) * COUT + 4 * gi) =
+            make_float4(ch[j].x + sd[4 * j], ch[j].y + sd[4 * j + 1], ch[j].z + sd[4 * j + 2], ch[j].w + sd[4 * j + 3]);
+  } else {
+    store_vec<COUT>(a.y + (long long)b * a.Ho * a.Wo * COUT + p * COUT, v);
+  }
+}
+
 template <int CIN, int COUT>
 void launch_thin1(const ConvArgs& a, const float* host_w, int B, cudaStream_t st) {
   ThinW<CIN, COUT> wt;
   for (int i = 0; i < 9 * CIN * COUT; ++i) wt.w[i] = host_w[i];
   for (int n = 0; n < COUT; ++n) wt.b[n] = host_w[9 * CIN * COUT + n];
   const int Hl = a.cy ? a.cy_h : a.Ho, Wl = a.cy ? a.cy_w : a.Wo;
+  if constexpr (CIN == 2 && COUT == 16 && HS_STEM_PX) {
+    if (!a.cy) {
+      k_conv_stem_px<COUT><<<dim3((unsigned)((a.Wo + 255) / 256), (unsigned)a.Ho, (unsigned)B), 256, 0, st>>>(a, wt);
+      return;
+    }
+  }
   const dim3 grid((unsigned)((Wl + kThinThreads - 1) / kThinThreads), (unsigned)((Hl + kThinRows - 1) / kThinRows),
                   (unsigned)B);
   k_conv_thin1<CIN, COUT><<<grid, kThinThreads, 0, st>>>(a, wt);
