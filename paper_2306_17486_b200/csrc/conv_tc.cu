@@ -82,6 +82,9 @@ constexpr int kProbe = HS_TC_PROBE;
 #ifndef HS_TC_S2_CVT
 #define HS_TC_S2_CVT 6
 #endif
+#ifndef HS_TC_PAIR
+#define HS_TC_PAIR 1  // 16-channel stride-1 layers: the converter group takes input rows two at a time
+#endif
 #ifndef HS_TC_CVT_GROUPS
 #define HS_TC_CVT_GROUPS 1  // measured round 2 (C3 and C2 level-0 shapes): one group of four converter warps is 9-10% faster than two
 #endif
@@ -141,7 +144,10 @@ struct Cfg {
   // converter group alternates between two slots, so a thread may convert the
   // group's next row while a slower one still reads the previous (the group
   // barrier of the next row orders the reuse)
-  static constexpr int NS_MIN = ATM ? 2 * NCG_ : 3, NS_MAX = ATM ? 2 * NCG_ : (MODE == 0 ? 10 : (MODE == 1 ? 8 : 6));
+  // PAIR (one converter group): rows are converted two at a time into four staged slots
+  static constexpr bool PAIR = ATM && NCG_ == 1 && HS_TC_PAIR;
+  static constexpr int NS_MIN = ATM ? (PAIR ? 4 : 2 * NCG_) : 3,
+                       NS_MAX = ATM ? (PAIR ? 4 : 2 * NCG_) : (MODE == 0 ? 10 : (MODE == 1 ? 8 : 6));
   static constexpr size_t row_stage_bytes(int ns) {
     return (size_t)3 * KC * 16 * (ns * RW + ((9 - ((ns * RW) & 7)) & 7));
   }
@@ -531,6 +537,92 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
     const int cg = (warp - kCvtWarp0) / C::NCVT_BASE;              // converter group: rows seq % NCG == cg
     const int ct = tid - 32 * kCvtWarp0 - cg * C::GCVT_THREADS;    // thread within the group
     uint32_t seq = 0;  // 32-bit ring bookkeeping
+    if constexpr (C::PAIR) {
+      // Two input rows per round: both rows' raw loads and conversions interleave, one group barrier
+      // covers both, and both rows' TMEM writes follow (the converters had one warp per SM
+      // sub-partition and spent most of a row in load / conversion latencies and the barrier)
+      constexpr int NEL = (kProbe & 1) ? 0 : C::RW * KC;
+      constexpr int TRIPS = (NEL + C::GCVT_THREADS - 1) / C::GCVT_THREADS;
+      const int q = warp & 3, m = 32 * q + lane;
+      for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
+        Unit U;
+        if (!unit_at<MODE, MT>(a, NSPLIT, u, U)) continue;
+        const int x0 = raw_x0<MODE, MT>(U.xb);
+        const int clo = max(x0, 0) - x0, chi = min(x0 + C::RW, a.W) - x0;
+        for (int g = U.glo; g <= U.ghi;) {
+          const int np = g + 1 <= U.ghi ? 2 : 1;
+          float4 va[2][TRIPS > 0 ? TRIPS : 1][2];
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            if (r >= np) break;
+            const uint32_t sq = seq + r;
+            mbar_wait(smem_u32(&raw_full[sq % NR]), (sq / NR) & 1);
+            const bool row_ok = g + r >= 0 && g + r < a.H;
+            const unsigned char* src = raw + (size_t)(sq % NR) * C::RAW_BYTES;
+#pragma unroll
+            for (int t = 0; t < TRIPS; ++t) {
+              const int e = ct + t * C::GCVT_THREADS;
+              const int p = e / KC, c = e - p * KC;
+              va[r][t][0] = va[r][t][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (e < NEL && row_ok && p >= clo && p < chi) {
+                const float4* s4 = reinterpret_cast<const float4*>(src + ((size_t)p * CIN + 8 * c) * 4);
+                va[r][t][0] = s4[0];
+                va[r][t][1] = s4[1];
+              }
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            if (r >= np) break;
+            const int ss = (int)((seq + r) % NS);
+#pragma unroll
+            for (int t = 0; t < TRIPS; ++t) {
+              const int e = ct + t * C::GCVT_THREADS;
+              if (e < NEL) {
+                const int p = e / KC, c = e - p * KC;
+                const float v[8] = {va[r][t][0].x, va[r][t][0].y, va[r][t][0].z, va[r][t][0].w,
+                                    va[r][t][1].x, va[r][t][1].y, va[r][t][1].z, va[r][t][1].w};
+                uint4 p3[3];
+                split_bf16x3(v, p3[0], p3[1], p3[2]);
+                const size_t off = ((size_t)c * C::XPL + ss * C::RW + p) * 16;
+#pragma unroll
+                for (int part = 0; part < 3; ++part) *reinterpret_cast<uint4*>(xp[part] + off) = p3[part];
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0)
+            for (int r = 0; r < np; ++r) mbar_arrive(smem_u32(&raw_empty[(seq + r) % NR]));
+          asm volatile("bar.sync %0, %1;" ::"r"(1), "n"(C::GCVT_THREADS) : "memory");  // staged rows complete
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            if (r >= np) break;
+            const uint32_t sq = seq + r, as = sq % C::NSA, ause = sq / C::NSA;
+            if (ause > 0) mbar_wait(smem_u32(&a_empty[as]), (ause - 1) & 1);
+            tc_fence_after();
+            const int ss = (int)(sq % NS);
+            const uint32_t tcol = tmem + ((uint32_t)(32 * q) << 16) + C::AOFF + as * C::SLOT_COLS;
+#pragma unroll
+            for (int kx = 0; kx < 3; ++kx)
+#pragma unroll
+              for (int part = 0; part < 3; ++part) {
+                const unsigned char* b0 = xp[part] + ((size_t)ss * C::RW + m + kx) * 16;
+                const uint4 lo = *reinterpret_cast<const uint4*>(b0);
+                const uint4 hi = *reinterpret_cast<const uint4*>(b0 + (size_t)C::XPL * 16);
+                asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                                 tcol + (kx * 3 + part) * 8),
+                             "r"(lo.x), "r"(lo.y), "r"(lo.z), "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w));
+              }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&a_full[as]));
+          }
+          seq += np;
+          g += np;
+        }
+      }
+    } else
     for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
       if (!unit_at<MODE, MT>(a, NSPLIT, u, U)) continue;
