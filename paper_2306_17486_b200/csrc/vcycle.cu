@@ -119,6 +119,12 @@ HS_DEV void issue_pair(uint32_t dst, const float2* __restrict__ g, int nx, int n
   cpa8(dst + 8, okb ? g + off + 1 : g, okb);
 }
 
+// the same from a running row offset `off` (= i * ny + ja) and the row's validity
+HS_DEV void issue_pair_at(uint32_t dst, const float2* __restrict__ g, int off, bool rok, bool oka, bool okb) {
+  cpa8(dst, (rok && oka) ? g + off : g, rok && oka);
+  cpa8(dst + 8, (rok && okb) ? g + off + 1 : g, rok && okb);
+}
+
 HS_DEV Pair read_pair(const float2* slot, float s) {
   const float4 v = *reinterpret_cast<const float4*>(slot);
   return Pair{make_float2(v.x * s, v.y * s), make_float2(v.z * s, v.w * s)};
@@ -169,18 +175,27 @@ __global__ void __launch_bounds__(kVcWarps * 32) k_vc_down(LevelDev L, int ncx, 
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring) + lane * 16;
 
   const int s0 = 2 * K0 - 1, s1 = 2 * K1 + 1;  // u1 rows
-  auto issue = [&](int s) {
-    if (s <= s1) {
-      const uint32_t d = ring_s + (((unsigned)(s - s0) % kRing) * kDownSlot * 8);
-      issue_pair(d, rhs, nx, ny, s, ja);
-      issue_pair(d + 512, dg, nx, ny, s, ja);
-      issue_pair(d + 1024, di, nx, ny, s, ja);
-      if (U0) issue_pair(d + 1536, u0, nx, ny, s + 1, ja);
+  // issue side: the next row, its ring slot and its in-field offset advance by one row per call
+  // (no per-row multiplies or divisions by the ring depth)
+  int is = s0, ioff = s0 * ny + ja;
+  uint32_t islot = 0;
+  auto issue_next = [&]() {
+    if (is <= s1) {
+      const uint32_t d = ring_s + islot * (kDownSlot * 8);
+      const bool rok = is >= 0 && is < nx;
+      issue_pair_at(d, rhs, ioff, rok, oka, okb);
+      issue_pair_at(d + 512, dg, ioff, rok, oka, okb);
+      issue_pair_at(d + 1024, di, ioff, rok, oka, okb);
+      if (U0) issue_pair_at(d + 1536, u0, ioff + ny, is + 1 >= 0 && is + 1 < nx, oka, okb);
     }
     cpa_commit();
+    ++is;
+    ioff += ny;
+    islot = islot + 1 == kRing ? 0 : islot + 1;
   };
 #pragma unroll
-  for (int k = 0; k < kRing - 1; ++k) issue(s0 + k);
+  for (int k = 0; k < kRing - 1; ++k) issue_next();
+  uint32_t cslot = 0;  // consume side
   const Pair z{make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
   Pair u0m = z, u0c = z, u0p = z;
   if (U0) {
@@ -190,9 +205,10 @@ __global__ void __launch_bounds__(kVcWarps * 32) k_vc_down(LevelDev L, int ncx, 
   Pair rh_m = z, dg_m = z, u1m2 = z, u1m1 = z;
   float2 acc = make_float2(0.f, 0.f);
   for (int s = s0; s <= s1; ++s) {
-    issue(s + kRing - 1);
+    issue_next();
     cpa_wait_ring();
-    const float2* slot = ring + ((unsigned)(s - s0) % kRing) * kDownSlot + 2 * lane;
+    const float2* slot = ring + cslot * kDownSlot + 2 * lane;
+    cslot = cslot + 1 == kRing ? 0 : cslot + 1;
     const Pair rh_c = read_pair(slot, rs), dg_c = read_pair(slot + 64, 1.f), di_c = read_pair(slot + 128, 1.f);
     if (U0) {
       u0m = u0c;
@@ -274,22 +290,29 @@ __global__ void __launch_bounds__(kVcWarps * 32) k_vc_up(LevelDev L, int ncx, in
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring) + lane * 16;
 
   const int s0 = R0 - 1, s1 = R1;  // u2 rows
-  auto issue = [&](int s) {
-    if (s <= s1) {
-      const uint32_t d = ring_s + (((unsigned)(s - s0) % kRing) * kUpSlot * 8);
-      issue_pair(d, rhs, nx, ny, s, ja);
-      issue_pair(d + 512, di, nx, ny, s, ja);
-      if (U0) issue_pair(d + 1024, u0, nx, ny, s + 1, ja);
-      if ((s & 1) == 0) {
-        const int K = s / 2;
+  int is = s0, ioff = s0 * ny + ja;
+  uint32_t islot = 0;
+  auto issue_next = [&]() {
+    if (is <= s1) {
+      const uint32_t d = ring_s + islot * (kUpSlot * 8);
+      const bool rok = is >= 0 && is < nx;
+      issue_pair_at(d, rhs, ioff, rok, oka, okb);
+      issue_pair_at(d + 512, di, ioff, rok, oka, okb);
+      if (U0) issue_pair_at(d + 1024, u0, ioff + ny, is + 1 >= 0 && is + 1 < nx, oka, okb);
+      if ((is & 1) == 0) {
+        const int K = is / 2;
         const bool ok = okq && K < ncx;
         cpa8(d + 1536, ok ? e + (long long)K * ncy + Q : e, ok);
       }
     }
     cpa_commit();
+    ++is;
+    ioff += ny;
+    islot = islot + 1 == kRing ? 0 : islot + 1;
   };
 #pragma unroll
-  for (int k = 0; k < kRing - 1; ++k) issue(s0 + k);
+  for (int k = 0; k < kRing - 1; ++k) issue_next();
+  uint32_t cslot = 0;
   const Pair z{make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
   Pair u0m = z, u0c = z, u0p = z;
   if (U0) {
@@ -307,9 +330,10 @@ __global__ void __launch_bounds__(kVcWarps * 32) k_vc_up(LevelDev L, int ncx, in
     hcur = prolong_pair(v);
   }
   for (int s = s0; s <= s1; ++s) {
-    issue(s + kRing - 1);
+    issue_next();
     cpa_wait_ring();
-    const float2* slot = ring + ((unsigned)(s - s0) % kRing) * kUpSlot + 2 * lane;
+    const float2* slot = ring + cslot * kUpSlot + 2 * lane;
+    cslot = cslot + 1 == kRing ? 0 : cslot + 1;
     const Pair rh_c = read_pair(slot, rs), di_c = read_pair(slot + 64, 1.f);
     if (U0) {
       u0m = u0c;
