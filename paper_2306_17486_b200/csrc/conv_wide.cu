@@ -159,6 +159,8 @@ struct WArgs {
   const void* const* active;
   int B;
   int planar;
+  int ldc;   // channels per pixel of y / addend / residual (COUT, or the full width for a cout slice)
+  int coff;  // first channel of this launch's slice (bias is already offset)
 };
 
 struct Pass {
@@ -540,8 +542,8 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(const __grid_constan
       auto ox_of = [&](int mm, int k) { return MODE == 2 ? 2 * (128 * P.xb + mm) + k : 128 * P.xb + mm; };
       auto side_ptr = [&](int r, int k, int sg, int mm) -> const float4* {
         const size_t pix = (size_t)(P.oy0 + r) * a.Wo + ox_of(mm, k);
-        const size_t base = side_res ? ((size_t)P.b * a.Ho * a.Wo + pix) * COUT : pix * COUT;
-        return reinterpret_cast<const float4*>(side + base + hc * EH + sg * SEG);
+        const size_t base = side_res ? ((size_t)P.b * a.Ho * a.Wo + pix) * a.ldc : pix * a.ldc;
+        return reinterpret_cast<const float4*>(side + base + a.coff + hc * EH + sg * SEG);
       };
       float4 sd[SEG / 4], sn[SEG / 4];
       auto load_side = [&](int r, int k, int sg, float4 (&dst)[SEG / 4]) {
@@ -571,7 +573,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(const __grid_constan
         const int oy = P.oy0 + r;
         const int ox = MODE == 2 ? 2 * (128 * P.xb + m) + k : 128 * P.xb + m;
         const size_t pix = (size_t)oy * a.Wo + ox;
-        const size_t obase = ((size_t)P.b * a.Ho * a.Wo + pix) * COUT + hc * EH + sg * SEG;
+        const size_t obase = ((size_t)P.b * a.Ho * a.Wo + pix) * a.ldc + a.coff + hc * EH + sg * SEG;
         float o[SEG];
 #pragma unroll
         for (int n0 = 0; n0 < SEG; n0 += 8) {
@@ -613,7 +615,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_conv_wide(const __grid_constan
           for (int j = 0; j < 4; ++j) {
             ch[j].x += sd[j].x, ch[j].y += sd[j].y, ch[j].z += sd[j].z, ch[j].w += sd[j].w;
             const size_t pj = (size_t)oy * a.Wo + ox_of(m - gi + j, k);
-            const size_t oj = ((size_t)P.b * a.Ho * a.Wo + pj) * COUT + hc * EH + sg * SEG + 4 * gi;
+            const size_t oj = ((size_t)P.b * a.Ho * a.Wo + pj) * a.ldc + a.coff + hc * EH + sg * SEG + 4 * gi;
             if (add && a.residual) {
               const float4 rv = __ldg(reinterpret_cast<const float4*>(a.residual + oj));
               ch[j].x += rv.x, ch[j].y += rv.y, ch[j].z += rv.z, ch[j].w += rv.w;
@@ -703,6 +705,10 @@ cudaError_t run_split(const float* w, int cin, int cout, void* out, cudaStream_t
 // weights registered by hs_net_create: device weight pointer -> its split pieces
 std::mutex reg_mu;
 std::map<const float*, void*> reg;
+// 128 -> 128 layers also keep the bf16x3 split of each 64-output-channel slice: a transposed 128 -> 128
+// layer runs as two 128 -> 64 launches (its two parity accumulators of 256 columns do not fit TMEM)
+std::map<std::pair<const float*, int>, void*> reg_slice;
+constexpr size_t kSlice128 = (size_t)64 * 9 * 128;  // floats of one 64-channel weight slice
 
 // TMA descriptor of the NHWC activation x: 4-D (channel, column, row, RHS), box 16 channels x 130
 // columns x 1 x 1, fp32, zero fill outside the tensor (the convolution's padding and halo)
@@ -761,7 +767,8 @@ bool conv_wide_supported(int cin, int cout, int stride, int transposed, int H, i
   return (mode == 0 && ((cin == 64 && cout == 64) || (cin == 128 && cout == 128))) ||
          (mode == 1 && ((cin == 64 && cout == 128) || (cin == 128 && cout == 128) ||
                         (HS_WIDE_S2_32 && cin == 32 && cout == 64))) ||
-         (mode == 2 && ((cin == 128 && cout == 64) || (HS_WIDE_EXTRA && cin == 64 && cout == 32)));
+         (mode == 2 && ((cin == 128 && cout == 64) || (cin == 128 && cout == 128) ||
+                        (HS_WIDE_EXTRA && cin == 64 && cout == 32)));
 }
 
 bool conv_wide_eligible(int cin, int cout) {
@@ -778,15 +785,34 @@ int conv_wide_register(const float* w, int cin, int cout, cudaStream_t st) {
     cudaFree(buf);
     return 1;
   }
+  void* half[2] = {nullptr, nullptr};
+  if (cin == 128 && cout == 128)
+    for (int h = 0; h < 2; ++h)
+      if (cudaMalloc(&half[h], split_bytes(128, 64)) != cudaSuccess ||
+          run_split(w + h * kSlice128, 128, 64, half[h], st) != cudaSuccess)
+        return 1;
   std::lock_guard<std::mutex> g(reg_mu);
   auto it = reg.find(w);
   if (it != reg.end()) cudaFree(it->second);
   reg[w] = buf;
+  for (int h = 0; h < 2; ++h)
+    if (half[h]) {
+      auto is = reg_slice.find({w, h});
+      if (is != reg_slice.end()) cudaFree(is->second);
+      reg_slice[{w, h}] = half[h];
+    }
   return 0;
 }
 
 void conv_wide_unregister(const float* w) {
   std::lock_guard<std::mutex> g(reg_mu);
+  for (int h = 0; h < 2; ++h) {
+    auto is = reg_slice.find({w, h});
+    if (is != reg_slice.end()) {
+      cudaFree(is->second);
+      reg_slice.erase(is);
+    }
+  }
   auto it = reg.find(w);
   if (it == reg.end()) return;
   cudaFree(it->second);  // synchronises the device: only at network destruction
@@ -798,6 +824,31 @@ bool conv_wide_launch(const float* x, int H, int W, int cin, float* y, int Ho, i
                       long long addend_bstride, int addend_per_model, const int* model_of, const float* residual,
                       const void* const* active, int B, cudaStream_t st, int planar) {
   if (!conv_wide_supported(cin, cout, stride, transposed, H, W, Wo)) return false;
+  if (transposed && cin == 128 && cout == 128) {
+    // two 64-channel output slices, each a 128 -> 64 transposed launch writing its half of every pixel
+    if (planar) return false;
+    CUtensorMap tm;
+    if (!make_tmap(&tm, x, cin, H, W, B)) return false;
+    for (int h = 0; h < 2; ++h) {
+      const void* split = nullptr;
+      {
+        std::lock_guard<std::mutex> g(reg_mu);
+        auto it = reg_slice.find({w, h});
+        if (it != reg_slice.end()) split = it->second;
+      }
+      void* tmp = nullptr;
+      if (!split) {
+        if (cudaMallocAsync(&tmp, split_bytes(128, 64), st) != cudaSuccess) return false;
+        if (run_split(w + h * kSlice128, 128, 64, tmp, st) != cudaSuccess) return false;
+        split = tmp;
+      }
+      WArgs a{static_cast<const unsigned char*>(split), x, H, W, y, Ho, Wo, w + h * kSlice128, bias + 64 * h, softplus,
+              addend, addend_bstride, addend_per_model, model_of, residual, active, B, 0, 128, 64 * h};
+      launch_wide<128, 64, 2>(a, tm, st);
+      if (tmp) cudaFreeAsync(tmp, st);
+    }
+    return true;
+  }
   const void* split = nullptr;
   {
     std::lock_guard<std::mutex> g(reg_mu);
@@ -811,7 +862,7 @@ bool conv_wide_launch(const float* x, int H, int W, int cin, float* y, int Ho, i
     split = tmp;
   }
   WArgs a{static_cast<const unsigned char*>(split), x, H, W, y, Ho, Wo, w, bias, softplus, addend, addend_bstride,
-          addend_per_model, model_of, residual, active, B, planar};
+          addend_per_model, model_of, residual, active, B, planar, cout, 0};
   CUtensorMap tm;
   if (!make_tmap(&tm, x, cin, H, W, B)) {
     if (tmp) cudaFreeAsync(tmp, st);
