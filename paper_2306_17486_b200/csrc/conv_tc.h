@@ -10,8 +10,8 @@ bool conv_tc_launch(const float* x, int H, int W, int cin, float* y, int Ho, int
                     long long addend_bstride, int addend_per_model, const int* model_of, const float* residual,
                     const void* const* active, int B, cudaStream_t st, int planar = 0);
 // K-streamed tcgen05 kernel for the >= 64-channel layers (conv_wide.cu): 64->64 / 128->128 stride 1,
-// 64->128 / 128->128 stride 2, 128->64 transposed, widths (transposed: input widths) that are
-// multiples of 128.  Same arguments and epilogue as conv_tc_launch.
+// 32->64 / 64->128 / 128->128 stride 2, 128->64 and 128->128 (two 64-channel slices) transposed, widths
+// (transposed: input widths) that are multiples of 128.  Same arguments and epilogue as conv_tc_launch.
 bool conv_wide_supported(int cin, int cout, int stride, int transposed, int H, int W, int Wo);
 bool conv_wide_launch(const float* x, int H, int W, int cin, float* y, int Ho, int Wo, int cout, int stride,
                       int transposed, const float* w, const float* bias, int softplus, const float* addend,
