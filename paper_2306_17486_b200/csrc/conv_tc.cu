@@ -51,7 +51,10 @@ namespace hs {
 namespace {
 using namespace tc;
 
-constexpr int kPrefetch = 4;  // rows pulled into L2 ahead of the bulk copies / epilogue loads
+#ifndef HS_TC_PREFETCH
+#define HS_TC_PREFETCH 4
+#endif
+constexpr int kPrefetch = HS_TC_PREFETCH;  // rows pulled into L2 ahead of the bulk copies / epilogue loads
 #ifndef HS_TC_PREF_OUT
 #define HS_TC_PREF_OUT 0  // bulk L2 prefetch of the epilogue's side rows (measured: off is faster, 32->16 t 1.37 -> 1.25 ms at C3)
 #endif

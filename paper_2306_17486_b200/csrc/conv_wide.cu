@@ -111,7 +111,10 @@ struct WCfg {
   static constexpr size_t RAW_SLOT = (size_t)NLOAD * BOXW * 64;  // a multiple of 128 (TMA destination)
   // B ring slots (measured: a deeper ring is slower, the weight copies are not the limiter); the
   // stride-2 layers' 257-pixel rows need the space
-  static constexpr int NBS = MODE == 1 ? 4 : 6;
+#ifndef HS_WIDE_NBS
+#define HS_WIDE_NBS 6
+#endif
+  static constexpr int NBS = MODE == 1 ? 4 : HS_WIDE_NBS;
   // staged drain: with one accumulator set, the epilogue copies the pass's group-summed accumulators
   // into shared memory and releases TMEM before its math and stores, so the next pass's MMAs overlap
   // them (cout 64 stride 1 only: the staging is R x 128 pixels x (cout + 4) floats, 70 KB)
