@@ -88,6 +88,9 @@ constexpr int kProbe = HS_TC_PROBE;
 #ifndef HS_TC_PAIR
 #define HS_TC_PAIR 1  // 16-channel stride-1 layers: the converter group takes input rows two at a time
 #endif
+#ifndef HS_TC_T_CVT
+#define HS_TC_T_CVT 2  // converter warps of the wide transposed tiles (64 -> 32 t at M = 64)
+#endif
 #ifndef HS_TC_CVT_GROUPS
 #define HS_TC_CVT_GROUPS 1  // measured round 2 (C3 and C2 level-0 shapes): one group of four converter warps is 9-10% faster than two
 #endif
@@ -132,7 +135,7 @@ struct Cfg {
   // needs the registers a 14-warp CTA cannot give
   // stride-2 layers convert two input rows per output row: six converter warps at M = 128
   // (measured; the M = 64 ones with two MMA warps would spill)
-  static constexpr int NCVT_BASE = (MODE == 2 && CS * NACC > 32) ? 2 : (MODE == 1 && MT == 128 ? HS_TC_S2_CVT : 4);
+  static constexpr int NCVT_BASE = (MODE == 2 && CS * NACC > 32) ? HS_TC_T_CVT : (MODE == 1 && MT == 128 ? HS_TC_S2_CVT : 4);
   // ATM: two groups of four converter warps (one per TMEM lane quarter each)
   // take alternate input rows, so two rows' convert -> stage -> TMEM chains
   // overlap instead of running back to back
