@@ -185,7 +185,7 @@ def load():
 
 
 (PROF_CONV, PROF_CONV_L0, PROF_VCYCLE, PROF_ARNOLDI, PROF_CNN, PROF_IMPLICIT, PROF_VC_UP0, PROF_TRAIN_WGRAD,
- PROF_CONV_WIDE) = range(9)
+ PROF_CONV_WIDE, PROF_KRYLOV) = range(10)
 
 
 def profile_query(tag: int):

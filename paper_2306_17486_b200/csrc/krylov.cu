@@ -85,8 +85,8 @@ struct ArnArgs {
 // together: DOT / REDOT dot v_{k0} .. v_{k0+NV-1} (REDOT first subtracts every
 // k < J with a runtime loop; it runs only where krylov.py:105 triggers), ORTH /
 // ORTH2 subtract v_0 .. v_{NV-1} (NV = 0: runtime J).
-template <int MODE, int NV>
-HS_DEV void arn_sweep(const SolveDims& d, const ArnArgs& g, double (&acc)[PST], int& bad) {
+template <int MODE, int NV, int KCT = KC>
+HS_DEV void arn_sweep(const SolveDims& d, const ArnArgs& g, double (&acc)[2 * KCT + 1], int& bad) {
   const long long N = g.N;
   auto ldz_b = [&](int q) { return ldz(g.zb + q); };
   for (int p = g.p0; p < g.N; p += g.stride) {
@@ -98,12 +98,12 @@ HS_DEV void arn_sweep(const SolveDims& d, const ArnArgs& g, double (&acc)[PST], 
       double2 w = apply_true(ldz_b, g.c, d.nx, d.ny, p, i, jj, d.h2, d.inv_h2);
       if (MODE == DOT) {
         if (!isfinite(w.x) || !isfinite(w.y)) bad = 1;
-        if (g.chunk == 0) acc[2 * KC] += w.x * w.x + w.y * w.y;
+        if (g.chunk == 0) acc[2 * KCT] += w.x * w.x + w.y * w.y;
       } else {
         for (int k = 0; k < g.J; ++k) w = zsub(w, zmul(g.coef[k], ldz(g.Vb + (long long)k * N + p)));
         if (MODE == ORTH && g.chunk == 0) {
           const_cast<float2*>(g.Vb)[(long long)g.J * N + p] = d2f(w);
-          acc[2 * KC] += w.x * w.x + w.y * w.y;
+          acc[2 * KCT] += w.x * w.x + w.y * w.y;
         }
       }
 #pragma unroll
@@ -124,14 +124,32 @@ HS_DEV void arn_sweep(const SolveDims& d, const ArnArgs& g, double (&acc)[PST], 
         for (int k = 0; k < g.J; ++k) w = zsub(w, zmul(g.coef[k], ldz(g.Vb + (long long)k * N + p)));
       }
       const_cast<float2*>(g.Vb)[(long long)g.J * N + p] = d2f(w);
-      acc[2 * KC] += w.x * w.x + w.y * w.y;
+      acc[2 * KCT] += w.x * w.x + w.y * w.y;
     }
   }
 }
 
-template <int MODE>
+// arn_sweep with the chunk's vector count as a compile-time constant 1..NV (the 20-vector fused pass)
+template <int MODE, int KCT, int NV>
+HS_DEV void arn_dispatch(int nv, const SolveDims& d, const ArnArgs& g, double (&acc)[2 * KCT + 1], int& bad) {
+  if constexpr (NV > 1) {
+    if (nv < NV) {
+      arn_dispatch<MODE, KCT, NV - 1>(nv, d, g, acc, bad);
+      return;
+    }
+  }
+  arn_sweep<MODE, NV, KCT>(d, g, acc, bad);
+}
+
+// The fused orthogonalisation + re-dot pass for windows of KC < J <= KCF vectors runs as ONE chunk of
+// KCF (k_arnoldi<ORTH, KCF>): with chunks of KC every chunk's blocks recomputed w from all J vectors,
+// so each vector was read once per chunk; one chunk reads each once (more registers, fewer warps).
+constexpr int KCF = 20;
+
+template <int MODE, int KCT = KC>
 __global__ void __launch_bounds__(NT) k_arnoldi(SolveDims d, SolveBuffers s, int nchunks) {
-  __shared__ double red[PST * (NT / 32 + 1)];
+  constexpr int PT = 2 * KCT + 1;  // doubles per partial record
+  __shared__ double red[PT * (NT / 32 + 1)];
   __shared__ double2 s_coef[kMaxRestart + 1];
   const int blk = blockIdx.x, chunk = blockIdx.y, b = blockIdx.z;
   RhsState& S = s.st[b];
@@ -142,9 +160,10 @@ __global__ void __launch_bounds__(NT) k_arnoldi(SolveDims d, SolveBuffers s, int
   if (MODE == REDOT && S.fused) return;  // the fused ORTH pass already added the re-dot
   if ((MODE == ORTH && !S.fuse) || (MODE == ORTHP && S.fuse)) return;
   const int j = S.j, J = j + 1, m = d.restart;
+  if (MODE == ORTH && ((J > KC && J <= KCF) != (KCT == KCF))) return;  // the other fused-pass kernel's RHS
   // dot passes: only the chunks holding v_0..v_j do work (and take part in the
   // last-block count); the rest exit before touching memory
-  const int live = (MODE == DOT || MODE == REDOT || MODE == ORTH) ? min(nchunks, (J + KC - 1) / KC) : nchunks;
+  const int live = (MODE == DOT || MODE == REDOT || MODE == ORTH) ? min(nchunks, (J + KCT - 1) / KCT) : nchunks;
   if (chunk >= live) return;
   const int N = (int)d.N;
   const float2* Vb = s.V + (long long)b * (m + 1) * N;
@@ -154,14 +173,17 @@ __global__ void __launch_bounds__(NT) k_arnoldi(SolveDims d, SolveBuffers s, int
     for (int k = threadIdx.x; k < J; k += NT) s_coef[k] = zscale(S.hcol[k], S.vscale[k]);
     __syncthreads();
   }
-  const int k0 = chunk * KC;
-  double acc[PST];
+  const int k0 = chunk * KCT;
+  double acc[PT];
 #pragma unroll
-  for (int t = 0; t < PST; ++t) acc[t] = 0.0;
+  for (int t = 0; t < PT; ++t) acc[t] = 0.0;
   int bad = 0;
   ArnArgs g{Vb, zb, c, s_coef, N, J, k0, chunk, blk * NT + (int)threadIdx.x, d.nblk * NT};
   if (MODE == DOT || MODE == REDOT || MODE == ORTH) {
     // vectors of this chunk, a compile-time count
+    if constexpr (KCT != KC) {
+      arn_dispatch<MODE, KCT, KCT>(min(KCT, J - k0), d, g, acc, bad);
+    } else
     switch (min(KC, J - k0)) {
       case 1: arn_sweep<MODE, 1>(d, g, acc, bad); break;
       case 2: arn_sweep<MODE, 2>(d, g, acc, bad); break;
@@ -177,27 +199,27 @@ __global__ void __launch_bounds__(NT) k_arnoldi(SolveDims d, SolveBuffers s, int
   } else {
     // w -= sum_k coef_k v_k over every k < J: the runtime loop measured faster
     // than the fully unrolled one (159 vs 139 us per pass at C2)
-    arn_sweep<MODE, 0>(d, g, acc, bad);
+    arn_sweep<MODE, 0, KCT>(d, g, acc, bad);
   }
   if (MODE == DOT && bad) atomicOr(&S.nonfinite, 1);
-  block_sum<PST>(acc, red);
-  double* part = s.partial + (((long long)b * nchunks + chunk) * d.nblk + blk) * PST;
+  block_sum<PT>(acc, red);
+  double* part = s.partial + (((long long)b * nchunks + chunk) * d.nblk + blk) * PT;
 #pragma unroll
-  for (int t = 0; t < PST; ++t)  // constant indices keep acc[] in registers
+  for (int t = 0; t < PT; ++t)  // constant indices keep acc[] in registers
     if (threadIdx.x == t) part[t] = acc[t];
   if (!arrive_last(&s.counter[b], live * d.nblk)) return;
   // ---- finish (one block per RHS)
-  const double* pb = s.partial + (long long)b * nchunks * d.nblk * PST;
+  const double* pb = s.partial + (long long)b * nchunks * d.nblk * PT;
   if (MODE == DOT || MODE == REDOT) {
     for (int t = threadIdx.x; t < 2 * J; t += NT) {
-      const int k = t >> 1, ch = k / KC, slot = 2 * (k % KC) + (t & 1);
+      const int k = t >> 1, ch = k / KCT, slot = 2 * (k % KCT) + (t & 1);
       double sum = 0.0;
-      for (int q = 0; q < d.nblk; ++q) sum += pb[((long long)ch * d.nblk + q) * PST + slot];
+      for (int q = 0; q < d.nblk; ++q) sum += pb[((long long)ch * d.nblk + q) * PT + slot];
       red[t] = sum * S.vscale[k];
     }
     if (MODE == DOT && threadIdx.x == 0) {
       double nn = 0.0;
-      for (int q = 0; q < d.nblk; ++q) nn += pb[(long long)q * PST + 2 * KC];
+      for (int q = 0; q < d.nblk; ++q) nn += pb[(long long)q * PT + 2 * KCT];
       S.wn = sqrt(nn);
     }
     __syncthreads();
@@ -210,14 +232,14 @@ __global__ void __launch_bounds__(NT) k_arnoldi(SolveDims d, SolveBuffers s, int
     // the second-pass coefficients V^H w: this pass formed exactly the w the
     // re-dot would recompute (same operations, same order), so it dots it here
     for (int t = threadIdx.x; t < 2 * J; t += NT) {
-      const int k = t >> 1, ch = k / KC, slot = 2 * (k % KC) + (t & 1);
+      const int k = t >> 1, ch = k / KCT, slot = 2 * (k % KCT) + (t & 1);
       double sum = 0.0;
-      for (int q = 0; q < d.nblk; ++q) sum += pb[((long long)ch * d.nblk + q) * PST + slot];
+      for (int q = 0; q < d.nblk; ++q) sum += pb[((long long)ch * d.nblk + q) * PT + slot];
       red[t] = sum * S.vscale[k];
     }
     if (threadIdx.x == 0) {
       double nn = 0.0;
-      for (int q = 0; q < d.nblk; ++q) nn += pb[(long long)q * PST + 2 * KC];
+      for (int q = 0; q < d.nblk; ++q) nn += pb[(long long)q * PT + 2 * KCT];
       S.hn = sqrt(nn);
       S.reorth = S.hn < 0.25 * S.wn;
       S.fused = 1;
@@ -227,7 +249,7 @@ __global__ void __launch_bounds__(NT) k_arnoldi(SolveDims d, SolveBuffers s, int
       for (int k = threadIdx.x; k < J; k += NT) S.hcol[k] = zadd(S.hcol[k], make_double2(red[2 * k], red[2 * k + 1]));
   } else if (threadIdx.x == 0) {
     double nn = 0.0;
-    for (int q = 0; q < d.nblk; ++q) nn += pb[(long long)q * PST + 2 * KC];
+    for (int q = 0; q < d.nblk; ++q) nn += pb[(long long)q * PT + 2 * KCT];
     S.hn = sqrt(nn);
     if (MODE == ORTHP) {
       S.reorth = S.hn < 0.25 * S.wn;  // krylov.py:105
@@ -488,13 +510,24 @@ void krylov_after_precond(const SolveDims& d, const SolveBuffers& s, int j_hint,
   k_arnoldi<DOT><<<dim3(d.nblk, nch, d.B), NT, 0, stream>>>(d, s, nch);
   prof::stop(slot, stream, dot_bytes);
   prof::count(8);
-  k_arnoldi<ORTH><<<dim3(d.nblk, nch, d.B), NT, 0, stream>>>(d, s, nch);  // + the re-dot (see its finish)
-  k_arnoldi<ORTHP><<<dim3(d.nblk, 1, d.B), NT, 0, stream>>>(d, s, 1);
-  k_arnoldi<REDOT><<<dim3(d.nblk, nch, d.B), NT, 0, stream>>>(d, s, nch);
-  k_arnoldi<ORTH2><<<dim3(d.nblk, 1, d.B), NT, 0, stream>>>(d, s, 1);
-  k_givens<<<cdiv_u(d.B, 64), 64, 0, stream>>>(d, s);
-  k_xupdate<<<dim3(d.nblk, d.B), NT, 0, stream>>>(d, s);
-  k_residual<false><<<dim3(d.nblk, d.B), NT, 0, stream>>>(d, s, 1);
+  // the other kernels of the step, each timed under tag KRYLOV with its own label when profiling is on
+  auto timed = [&](int label, auto&& launch) {
+    prof::set_label(label);
+    const int sl = prof::start(prof::KRYLOV, stream);
+    launch();
+    prof::stop(sl, stream, 0.0);
+  };
+  timed(ORTH, [&] {  // + the re-dot (windows of up to KC vectors, and beyond KCF)
+    k_arnoldi<ORTH><<<dim3(d.nblk, nch, d.B), NT, 0, stream>>>(d, s, nch);
+  });
+  if (d.restart > KC)  // windows of KC < J <= KCF vectors: one 20-vector chunk
+    timed(5, [&] { k_arnoldi<ORTH, KCF><<<dim3(d.nblk, 1, d.B), NT, 0, stream>>>(d, s, 1); });
+  timed(ORTHP, [&] { k_arnoldi<ORTHP><<<dim3(d.nblk, 1, d.B), NT, 0, stream>>>(d, s, 1); });
+  timed(REDOT, [&] { k_arnoldi<REDOT><<<dim3(d.nblk, nch, d.B), NT, 0, stream>>>(d, s, nch); });
+  timed(ORTH2, [&] { k_arnoldi<ORTH2><<<dim3(d.nblk, 1, d.B), NT, 0, stream>>>(d, s, 1); });
+  timed(10, [&] { k_givens<<<cdiv_u(d.B, 64), 64, 0, stream>>>(d, s); });
+  timed(11, [&] { k_xupdate<<<dim3(d.nblk, d.B), NT, 0, stream>>>(d, s); });
+  timed(12, [&] { k_residual<false><<<dim3(d.nblk, d.B), NT, 0, stream>>>(d, s, 1); });
 }
 
 void krylov_count_active(const SolveDims& d, const SolveBuffers& s, cudaStream_t stream) {

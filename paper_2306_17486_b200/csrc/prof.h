@@ -21,7 +21,8 @@ enum Tag {
   VC_UP0 = 6,     // finest-level up-leg kernel (work = algorithmic bytes)
   TRAIN_WGRAD = 7,  // training weight-gradient reductions (work = flops)
   CONV_WIDE = 8,  // 3x3 convolutions with >= 64 input or output channels, tensor-bound (work = flops)
-  NTAGS = 9
+  KRYLOV = 9,     // the other Krylov kernels of a step (orthogonalisation passes, Givens, x update, residual)
+  NTAGS = 10
 };
 
 extern std::atomic<long long> launches;
