@@ -26,6 +26,11 @@ constexpr int NT = 128;
 constexpr int KC = 10;            // basis vectors per chunk in a dot pass (registers vs w recomputes)
 constexpr int PST = 2 * KC + 1;   // doubles per partial record
 constexpr int kChunks = (kMaxRestart + KC - 1) / KC;
+// The fused orthogonalisation + re-dot pass for windows of KC < J <= KCF vectors runs as ONE chunk of
+// KCF (k_arnoldi<ORTH, KCF>): with chunks of KC every chunk's blocks recomputed w from all J vectors,
+// so each vector was read once per chunk; one chunk reads each once, and w is formed from the same
+// registers the dots use (more registers, fewer warps).
+constexpr int KCF = 20;
 
 // ORTH is the orthogonalisation pass fused with the re-dot (for RHS predicted
 // to re-orthogonalise), ORTHP the plain one (the rest)
@@ -100,7 +105,16 @@ HS_DEV void arn_sweep(const SolveDims& d, const ArnArgs& g, double (&acc)[2 * KC
         if (!isfinite(w.x) || !isfinite(w.y)) bad = 1;
         if (g.chunk == 0) acc[2 * KCT] += w.x * w.x + w.y * w.y;
       } else {
-        for (int k = 0; k < g.J; ++k) w = zsub(w, zmul(g.coef[k], ldz(g.Vb + (long long)k * N + p)));
+        bool done = false;
+        if constexpr (KCT == KCF && NV > 0) {  // the 20-vector chunk holds every vector: subtract from registers
+          if (NV == g.J) {
+#pragma unroll
+            for (int k = 0; k < NV; ++k) w = zsub(w, zmul(g.coef[k], f2d(v[k])));
+            done = true;
+          }
+        }
+        if (!done)
+          for (int k = 0; k < g.J; ++k) w = zsub(w, zmul(g.coef[k], ldz(g.Vb + (long long)k * N + p)));
         if (MODE == ORTH && g.chunk == 0) {
           const_cast<float2*>(g.Vb)[(long long)g.J * N + p] = d2f(w);
           acc[2 * KCT] += w.x * w.x + w.y * w.y;
@@ -141,10 +155,6 @@ HS_DEV void arn_dispatch(int nv, const SolveDims& d, const ArnArgs& g, double (&
   arn_sweep<MODE, NV, KCT>(d, g, acc, bad);
 }
 
-// The fused orthogonalisation + re-dot pass for windows of KC < J <= KCF vectors runs as ONE chunk of
-// KCF (k_arnoldi<ORTH, KCF>): with chunks of KC every chunk's blocks recomputed w from all J vectors,
-// so each vector was read once per chunk; one chunk reads each once (more registers, fewer warps).
-constexpr int KCF = 20;
 
 template <int MODE, int KCT = KC>
 __global__ void __launch_bounds__(NT) k_arnoldi(SolveDims d, SolveBuffers s, int nchunks) {
