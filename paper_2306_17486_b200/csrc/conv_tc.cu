@@ -91,6 +91,12 @@ constexpr int kProbe = HS_TC_PROBE;
 #ifndef HS_TC_T_CVT
 #define HS_TC_T_CVT 2  // converter warps of the wide transposed tiles (64 -> 32 t at M = 64)
 #endif
+#ifndef HS_TC_XPL_SKEW
+#define HS_TC_XPL_SKEW 1  // staged chunk-plane pitch chosen per KC (see Cfg::XPL)
+#endif
+#ifndef HS_TC_RAW_SWZ
+#define HS_TC_RAW_SWZ 1  // converters' raw-row loads: halves in swizzled order (no 2-way bank conflict)
+#endif
 #ifndef HS_TC_CVT_GROUPS
 #define HS_TC_CVT_GROUPS 1  // measured round 2 (C3 and C2 level-0 shapes): one group of four converter warps is 9-10% faster than two
 #endif
@@ -154,9 +160,9 @@ struct Cfg {
   static constexpr bool PAIR = ATM && NCG_ == 1 && HS_TC_PAIR;
   static constexpr int NS_MIN = ATM ? (PAIR ? 4 : 2 * NCG_) : 3,
                        NS_MAX = ATM ? (PAIR ? 4 : 2 * NCG_) : (MODE == 0 ? 10 : (MODE == 1 ? 8 : 6));
-  static constexpr size_t row_stage_bytes(int ns) {
-    return (size_t)3 * KC * 16 * (ns * RW + ((9 - ((ns * RW) & 7)) & 7));
-  }
+  static constexpr int XP_RES = (HS_TC_XPL_SKEW && MODE != 1 && KC < 8) ? 8 / KC : 1;
+  static constexpr int pitch(int ns) { return ns * RW + ((8 + XP_RES - ((ns * RW) & 7)) & 7); }
+  static constexpr size_t row_stage_bytes(int ns) { return (size_t)3 * KC * 16 * pitch(ns); }
   static constexpr size_t total(int ns, int nr) {
     return W_BYTES + row_stage_bytes(ns) + (size_t)nr * RAW_BYTES + 8 * (2 * nr + 2 * ns + 2 * kNA + 12) + 16 +
            4 * CS;
@@ -174,8 +180,11 @@ struct Cfg {
     return NS_MIN;
   }
   static constexpr int NS = pick_ns();
-  static constexpr int XPL0 = NS * RW;
-  static constexpr int XPL = XPL0 + ((9 - (XPL0 & 7)) & 7);  // == 1 mod 8: conflict-free chunk planes
+  // chunk-plane pitch mod 8 (16-byte bank groups): the converters' staged stores put the KC chunks of
+  // 8 / KC consecutive pixels in one quarter-warp wavefront, so a pitch == 8 / KC (mod 8) lands them in
+  // eight distinct bank groups (ncu at the C3 level-0 shape: == 1 gave every 16-channel store a 2-way
+  // conflict).  Stride 2 de-interleaves the pixels, where no pitch removes the conflict: it keeps 1.
+  static constexpr int XPL = pitch(NS);
   static constexpr size_t XP_BYTES = (size_t)KC * XPL * 16;   // one activation part
   static constexpr size_t R_BYTES = (size_t)NR * RAW_BYTES;
   static constexpr size_t TOTAL = total(NS, NR);
@@ -233,6 +242,25 @@ template <int MODE, int MT>
 HS_DEV int staged_px(int p) {
   if (MODE != 1) return p;
   return (p & 1) ? (p - 1) >> 1 : MT + (p >> 1);  // column 2x0-1+p: odd p is an even column
+}
+
+// One 8-channel chunk (32 bytes) of a raw fp32 row, element e = pixel * KC + chunk.  Consecutive
+// elements sit 32 bytes apart, so loading every lane's first half and then its second half puts lanes e
+// and e + 4 of a quarter warp on the same banks; lanes with bit 2 of e set load their halves in the
+// other order, so each wavefront covers 128 distinct bytes.  Measured at C3: stride 2 / transposed
+// 1-3.5% faster; the 16-channel stride-1 (A-in-TMEM) converters 8-16% SLOWER, so they keep the plain order.
+template <bool SWZ>
+HS_DEV void load_chunk(const unsigned char* p, int e, float4& lo, float4& hi) {
+  const float4* s4 = reinterpret_cast<const float4*>(p);
+  if (SWZ) {
+    const int sw = (e >> 2) & 1;
+    const float4 a = s4[sw], b = s4[sw ^ 1];
+    lo = sw ? b : a;
+    hi = sw ? a : b;
+  } else {
+    lo = s4[0];
+    hi = s4[1];
+  }
 }
 
 struct Unit {
@@ -571,9 +599,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
               const int p = e / KC, c = e - p * KC;
               va[r][t][0] = va[r][t][1] = make_float4(0.f, 0.f, 0.f, 0.f);
               if (e < NEL && row_ok && p >= clo && p < chi) {
-                const float4* s4 = reinterpret_cast<const float4*>(src + ((size_t)p * CIN + 8 * c) * 4);
-                va[r][t][0] = s4[0];
-                va[r][t][1] = s4[1];
+                load_chunk<HS_TC_RAW_SWZ && !C::ATM>(src + ((size_t)p * CIN + 8 * c) * 4, e, va[r][t][0], va[r][t][1]);
               }
             }
           }
@@ -660,9 +686,7 @@ __global__ void __launch_bounds__(Cfg<CIN, COUT, MODE, MT, CS>::NT, 1) k_conv_tc
             const int p = e / KC, c = e - p * KC;  // chunk fastest: conflict-free raw reads
             va[t][0] = va[t][1] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (t0 + t < TRIPS && e < NEL && row_ok && p >= clo && p < chi) {
-              const float4* s4 = reinterpret_cast<const float4*>(src + ((size_t)p * CIN + 8 * c) * 4);
-              va[t][0] = s4[0];
-              va[t][1] = s4[1];
+              load_chunk<HS_TC_RAW_SWZ && !C::ATM>(src + ((size_t)p * CIN + 8 * c) * 4, e, va[t][0], va[t][1]);
             }
           }
 #pragma unroll
