@@ -97,6 +97,9 @@ constexpr int kProbe = HS_TC_PROBE;
 #ifndef HS_TC_RAW_SWZ
 #define HS_TC_RAW_SWZ 1  // converters' raw-row loads: halves in swizzled order (no 2-way bank conflict)
 #endif
+#ifndef HS_TC_SHIFT
+#define HS_TC_SHIFT 1  // 16 -> 16 stride-1 layers on the tcgen05.shift kernel (conv_shift.cu); 0 keeps the tap-view kernel below
+#endif
 #ifndef HS_TC_CVT_GROUPS
 #define HS_TC_CVT_GROUPS 1  // measured round 2 (C3 and C2 level-0 shapes): one group of four converter warps is 9-10% faster than two
 #endif
@@ -1256,6 +1259,9 @@ bool conv_tc_launch(const float* x, int H, int W, int cin, float* y, int Ho, int
   TcArgs a{x, H, W, y, Ho, Wo, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual,
            active, B, 32, planar};
   const int mode = transposed ? 2 : (stride == 2 ? 1 : 0);
+  if (HS_TC_SHIFT && mode == 0 && cin == 16 && cout == 16 && !planar && !kProbe)
+    return conv_shift_launch(x, H, W, y, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of,
+                             residual, active, B, st);
   const bool m128 = ((mode == 2 ? W : Wo) % 128) == 0 && !(kProbe & 32);
 #define HS_TC(CI, CO, MD, CSL)                                           \
   if (mode == MD && cin == CI && cout == CO) {                           \

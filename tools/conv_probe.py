@@ -58,6 +58,8 @@ for _ in range(3):  # best of three batches (clocks vary under the power cap)
     torch.cuda.synchronize()
     best.append(e0.elapsed_time(e1) / a.iters)
 print("synced", flush=True)
+if os.environ.get("HS_DBG"):
+    print("dbg y[0:4]", y.flatten()[:4].tolist())
 ms = min(best)
 pix = (a.B * a.H * a.W) if a.transposed else (a.B * Ho * Wo)
 flops = 2 * 9 * a.cin * a.cout * pix

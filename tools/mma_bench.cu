@@ -280,9 +280,130 @@ void run_row9(long long* d) {
          cudaGetErrorString(cudaDeviceSynchronize()));
 }
 
-int main() {
+
+// the tcgen05.shift conv's issue pattern (conv_shift.cu): per input row 27 MMAs (N = 48 / 32 / 16) into three
+// accumulators and 6 shifts of the row's TMEM A slot, all from one elected thread
+constexpr uint32_t WT = 96;
+#define HS_SH_TAP(D, E, P0, WOFF)                                                   \
+  "add.u32 bl, %4, " WOFF ";\n\tmov.b64 db, {bl, hi};\n\t"                         \
+  "@" E " tcgen05.mma.cta_group::1.kind::f16 [" D "], [%3], db, i0, " P0 ";\n\t"    \
+  "@" E " tcgen05.mma.cta_group::1.kind::f16 [" D "], [ta1], db, i1, pt;\n\t"       \
+  "@" E " tcgen05.mma.cta_group::1.kind::f16 [" D "], [ta2], db, i2, pt;\n\t"
+#define HS_SH_SHIFT                                                                 \
+  "@es tcgen05.shift.cta_group::1.down [%3];\n\t"                                   \
+  "@es tcgen05.shift.cta_group::1.down [ta1];\n\t"                                  \
+  "@es tcgen05.shift.cta_group::1.down [ta2];\n\t"
+#define HS_SH_KX(E0, E1, E2, P0, W0, W1, W2, SH) \
+  HS_SH_TAP("%0", E0, P0, W0) HS_SH_TAP("%1", E1, "pt", W1) HS_SH_TAP("%2", E2, "pt", W2) SH
+#define HS_SH_ROW(E0, E1, E2)                                                       \
+  HS_SH_KX(E0, E1, E2, "pz", "%10", "%13", "%16", HS_SH_SHIFT)                      \
+  HS_SH_KX(E0, E1, E2, "pt", "%11", "%14", "%17", HS_SH_SHIFT)                      \
+  HS_SH_KX(E0, E1, E2, "pt", "%12", "%15", "%18", "")
+#define HS_SH_OPERANDS                                                                                          \
+  "r"(d0), "r"(d1), "r"(d2), "r"(abase), "r"(wlo), "r"(valid), "n"(kDescHi), "n"(I0), "n"(I1), "n"(I2), "n"(0 * WT), \
+      "n"(1 * WT), "n"(2 * WT), "n"(3 * WT), "n"(4 * WT), "n"(5 * WT), "n"(6 * WT), "n"(7 * WT), "n"(8 * WT)
+#define HS_SH_HEAD                                                                                              \
+  "{\n\t.reg .pred e, es, e0, e1, e2, pz, pt;\n\t.reg .b64 db;\n\t.reg .b32 hi, i0, i1, i2, ta1, ta2, bl, m;\n\t" \
+  "mov.b32 hi, %6;\n\tmov.b32 i0, %7;\n\tmov.b32 i1, %8;\n\tmov.b32 i2, %9;\n\t"                                  \
+  "elect.sync _|e, 0xffffffff;\n\t"                                                                             \
+  "setp.ne.b32 pz, %5, %5;\n\tsetp.eq.b32 pt, %5, %5;\n\t"                                                       \
+  "add.u32 ta1, %3, 8;\n\tadd.u32 ta2, %3, 16;\n\t"
+
+
+template <int SAMEACC, int NOSHIFT, int NCOMMIT = 0>
+__global__ void k_rowpat(long long* out, int rows) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint32_t s_tmem;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t cbar[2];
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    for (int i = 0; i < 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&cbar[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s_tmem;
+  if (warp == 0) {
+    constexpr uint32_t I0 = idesc_bf16(128, 48), I1 = idesc_bf16(128, 32), I2 = idesc_bf16(128, 16);
+    const uint32_t wlo = (uint32_t)(desc(smem_u32(smem), 48 * 16, 128) & 0xffffffffu);
+    const uint32_t valid = NOSHIFT ? 0u : 1u;
+    long long t0 = clock64();
+    uint32_t s = 0, as = 0;
+#pragma unroll 1
+    for (int r = 0; r < rows; ++r) {
+      const uint32_t d0 = tmem + s * 48, d1 = SAMEACC ? d0 : tmem + ((s + 5) % 6) * 48, d2 = SAMEACC ? d0 : tmem + ((s + 4) % 6) * 48;
+      const uint32_t abase = tmem + 288 + as * 24;
+      asm volatile(HS_SH_HEAD
+                   "@!e bra SH_SKIP_%=;\n\t"
+                   "setp.ne.b32 es, %5, 0;\n\t" HS_SH_ROW("pt", "pt", "pt") "SH_SKIP_%=:\n\t}\n" ::HS_SH_OPERANDS
+                   : "memory");
+      __syncwarp();
+      for (int c = 0; c < NCOMMIT; ++c)
+        asm volatile(
+            "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(&cbar[c]))
+            : "memory");
+      s = s + 1 == 6 ? 0 : s + 1;
+      as = as + 1 == 9 ? 0 : as + 1;
+    }
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(&bar))
+        : "memory");
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tW2:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t@P1 bra D2;\n\tbra W2;\n\tD2:\n\t}\n" ::"r"(
+            smem_u32(&bar)));
+    long long t1 = clock64();
+    if (threadIdx.x == 0) out[0] = t1 - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+template <int SAMEACC, int NOSHIFT, int NCOMMIT = 0>
+void run_rowpat(long long* d) {
+  auto k = k_rowpat<SAMEACC, NOSHIFT, NCOMMIT>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  k<<<1, 128, 64 * 1024>>>(d, 2000);
+  k<<<1, 128, 64 * 1024>>>(d, 2000);
+  long long h = 0;
+  cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaError_t e = cudaDeviceSynchronize();
+  printf("shift-conv row pattern (27 MMAs + 6 shifts), same accumulator %d, no shifts %d, commits per row %d: %.1f cycles per row (%s)\n", SAMEACC,
+         NOSHIFT, NCOMMIT, (double)h / 2000, cudaGetErrorString(e));
+}
+
+int main(int argc, char** argv) {
   long long* d;
   cudaMalloc(&d, 1024 * sizeof(long long));
+  if (argc > 1) {  // "tm": A in TMEM, cycles per MMA against N (one accumulator, back to back)
+    run_rowpat<0, 0>(d);
+    run_rowpat<0, 0, 1>(d);
+    run_rowpat<0, 0, 2>(d);
+    run_rowpat<1, 0>(d);
+    run_rowpat<0, 1>(d);
+    run_rowpat<1, 1>(d);
+    run<128, 16, true>(d);
+    run<128, 32, true>(d);
+    run<128, 48, true>(d);
+    run<128, 64, true>(d);
+    run<128, 96, true>(d);
+    run<128, 128, true>(d);
+    run<128, 144, true>(d);
+    run<128, 192, true>(d);
+    run<128, 256, true>(d);
+    return 0;
+  }
   run_row9<16>(d);
   run_row9<32>(d);
   run_row9<32, 6>(d);
