@@ -966,7 +966,7 @@ int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* 
                        a.softplus, a.addend, a.addend_bstride, a.addend_per_model, a.model_of, a.residual, a.active, B,
                        st, planar_out ? 1 : 0))
     return HS_OK;
-  if (conv_tc_supported(c.cin, c.cout, c.stride, c.transposed, H, W, a.Wo) &&
+  if (conv_tc_supported(c.cin, c.cout, c.stride, c.transposed, H, W, a.Wo, planar_out ? 1 : 0) &&
       conv_tc_launch(a.x, a.H, a.W, a.cin, a.y, a.Ho, a.Wo, a.cout, c.stride, c.transposed, a.w, a.bias, a.softplus,
                      a.addend, a.addend_bstride, a.addend_per_model, a.model_of, a.residual, a.active, B, st,
                      planar_out ? 1 : 0))
@@ -1246,7 +1246,7 @@ static bool coarse_planar(const hs_net_t* net, int h, int w) {
   const hs_conv_t& c = net->d.sol_res_b[net->d.levels - 1];
   return net->spec_perm != nullptr && !c.transposed && c.stride == 1 &&
          (conv_wide_supported(c.cin, c.cout, c.stride, c.transposed, h, w, w) ||
-          conv_tc_supported(c.cin, c.cout, c.stride, c.transposed, h, w, w));
+          conv_tc_supported(c.cin, c.cout, c.stride, c.transposed, h, w, w, 1));
 }
 
 static int solver_forward(const hs_net_t* net, const float* in, float* head, const ThinIO* io, char* ws,

@@ -52,7 +52,7 @@ using namespace tc;
 
 // Stage-removal probes for a separate measurement build only (`make variant DEFS=-DHS_SH_PROBE=<mask>`): 1 no shifts,
 // 2 no MMAs, 4 no split / TMEM writes, 8 no epilogue math and stores, 16 one accumulator for a row's three output rows,
-// 32 no TMEM drain, 64 MMA-warp cycle counts into y[0..2] (waiting, issuing, rows).  The product build compiles with 0.
+// 32 no TMEM drain, 64 MMA-warp cycle counts into y[0..3] (waiting for A slots, issuing, rows, waiting for accumulators).  The product build compiles with 0.
 #ifndef HS_SH_PROBE
 #define HS_SH_PROBE 0
 #endif
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(NT, 1) k_conv16_shift(ShArgs a) {
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
     uint32_t as = 0, a_par = 0;        // A slot of the next input row and the parity of its a_full phase
     uint32_t s_next = 0, epoch = 0;    // accumulator slot of the next output row to open, completed wraps
-    long long dbg_wait = 0, dbg_issue = 0, dbg_rows = 0;  // kShProbe & 64: cycles per row waiting / issuing
+    long long dbg_wait = 0, dbg_wait2 = 0, dbg_issue = 0, dbg_rows = 0;  // kShProbe & 64: cycles per row waiting / issuing
     for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
       if (!unit_at(a, u, U)) continue;
@@ -323,6 +323,7 @@ __global__ void __launch_bounds__(NT, 1) k_conv16_shift(ShArgs a) {
         const bool v_new = g + 1 < U.oy1, v_cur = g >= U.oy0 && g < U.oy1, v_old = g - 1 >= U.oy0;
         s_old = s_cur;
         s_cur = s_new;
+        const long long tq01 = (kShProbe & 64) ? clock64() : 0;
         if (v_new) {  // output row g + 1 opens its accumulator: the previous user must have drained it
           s_new = s_next;
           if (epoch > 0) mbar_wait(smem_u32(&acc_empty[s_new]), (epoch - 1) & 1);
@@ -349,7 +350,8 @@ __global__ void __launch_bounds__(NT, 1) k_conv16_shift(ShArgs a) {
         }
         if (kShProbe & 64) {
           const long long tq2 = clock64();
-          dbg_wait += tq1 - tq0;
+          dbg_wait += tq01 - tq0;
+          dbg_wait2 += tq1 - tq01;
           dbg_issue += tq2 - tq1;
           ++dbg_rows;
         }
@@ -359,6 +361,7 @@ __global__ void __launch_bounds__(NT, 1) k_conv16_shift(ShArgs a) {
       a.y[0] = (float)dbg_wait / (float)dbg_rows;
       a.y[1] = (float)dbg_issue / (float)dbg_rows;
       a.y[2] = (float)dbg_rows;
+      a.y[3] = (float)dbg_wait2 / (float)dbg_rows;
     }
   } else {
     // ================= epilogue: group hg drains the output rows with tile % 2 == hg; warp q4 its lane quarter

@@ -1243,11 +1243,12 @@ int slice_for(int cin, int cout, int mode) {
 
 bool conv_tc_enabled = true;
 
-bool conv_tc_supported(int cin, int cout, int stride, int transposed, int H, int W, int Wo) {
+bool conv_tc_supported(int cin, int cout, int stride, int transposed, int H, int W, int Wo, int planar) {
   (void)H;
   if (!conv_tc_enabled) return false;
   const int mode = transposed ? 2 : (stride == 2 ? 1 : 0);
   const int width = mode == 2 ? W : Wo;
+  if (HS_TC_SHIFT && !planar && mode == 0 && cin == 16 && cout == 16) return true;  // conv_shift.cu: 30-pixel segments, any width
   if (width % 64) return false;
   return slice_for(cin, cout, mode) > 0;
 }

@@ -4,7 +4,7 @@
 
 namespace hs {
 extern bool conv_tc_enabled;  // hs_set_conv_path() toggles it (tests compare both paths)
-bool conv_tc_supported(int cin, int cout, int stride, int transposed, int H, int W, int Wo);
+bool conv_tc_supported(int cin, int cout, int stride, int transposed, int H, int W, int Wo, int planar = 0);
 bool conv_tc_launch(const float* x, int H, int W, int cin, float* y, int Ho, int Wo, int cout, int stride,
                     int transposed, const float* w, const float* bias, int softplus, const float* addend,
                     long long addend_bstride, int addend_per_model, const int* model_of, const float* residual,
