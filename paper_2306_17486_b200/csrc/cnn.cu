@@ -929,8 +929,10 @@ int launch_conv(const hs_conv_t& c, const float* x, int B, int H, int W, float* 
   const double flops =
       2.0 * 9.0 * c.cin * c.cout * (c.transposed ? (double)H * W : (double)a.Ho * a.Wo) * prof::active_hint(B);
   const bool l0 = c.cin == 16 && c.cout == 16 && c.stride == 1 && !c.transposed;
-  // CONV_L0 records algorithmic HBM bytes: input + output (+ addend) (+ residual), once each
-  const double l0_bytes = 4.0 * 16 * (double)H * W * (2 + (addend ? 1 : 0) + (residual ? 1 : 0)) *
+  // CONV_L0 records algorithmic HBM bytes: input + output (+ per-RHS addend) (+ residual), once each; an
+  // addend shared by a model's RHS (the encoder features) is read from DRAM once per model, not per RHS,
+  // and is not counted
+  const double l0_bytes = 4.0 * 16 * (double)H * W * (2 + (addend && !model_of_addend ? 1 : 0) + (residual ? 1 : 0)) *
                           prof::active_hint(B);
   const bool wide = (c.cin >= 64 || c.cout >= 64) && c.cin > 2 && c.cout > 2;
   struct Scope2 {

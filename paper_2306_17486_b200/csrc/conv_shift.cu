@@ -1,4 +1,4 @@
-// 16 -> 16 stride-1 3x3 convolution (the level-0 residual blocks) on tcgen05 with the A operand in
+// 16 -> 16 and 32 -> 32 stride-1 3x3 convolutions (the level-0 and level-1 residual blocks) on tcgen05 with the A operand in
 // TMEM and the horizontal taps made by tcgen05.shift -- no im2col, no tap views, no staged copy.
 //
 // Replaces the A-in-TMEM variant of conv_tc.cu (Cfg::ATM) for this layer shape.  There the converters
@@ -28,6 +28,11 @@
 // warp 13 MMA issuer.  Precision and results follow conv_tc.cu: six bf16 products per fp32 product,
 // the three column groups summed in the epilogue, bias, softplus, addend / residual, NHWC stores as whole
 // 64-byte pixels (group-of-four transpose).
+// 32 channels (template C = 32): a slot is 48 columns (three parts x two K steps), an accumulator 96, so TMEM
+// holds four accumulators and two A slots (the converters keep the next row split in registers while they
+// wait for a slot); the two epilogue groups take the two 16-channel halves of every output row instead of
+// alternate rows; the converters read their 128-byte pixels in rotated order (no bank conflicts).  With A in
+// shared memory this layer was bound by the MMAs' operand reads (36 KB per tile and tap).
 // Reference: helmsolve.autodiff.conv2d (/root/reference/pkg/src/helmsolve/autodiff.py:472-507).
 #include <cuda_bf16.h>
 
@@ -43,37 +48,43 @@ using namespace tc;
 #ifndef HS_SH_BAND_MAX
 #define HS_SH_BAND_MAX 32
 #endif
-#ifndef HS_SH_X
-#define HS_SH_X 1  // 1: a raw slot is released after its row is in TMEM (see the converter); other bits: measurement builds
+#ifndef HS_SH_ROT
+#define HS_SH_ROT 0  // 16 channels: converters read their pixel's four 16-byte pieces in rotated order (measured equal)
 #endif
 #ifndef HS_SH_NR
 #define HS_SH_NR 12
 #endif
 
 // Stage-removal probes for a separate measurement build only (`make variant DEFS=-DHS_SH_PROBE=<mask>`): 1 no shifts,
-// 2 no MMAs, 4 no split / TMEM writes, 8 no epilogue math and stores, 16 one accumulator for a row's three output rows,
-// 32 no TMEM drain, 64 MMA-warp cycle counts into y[0..3] (waiting for A slots, issuing, rows, waiting for accumulators).  The product build compiles with 0.
+// 2 no MMAs, 4 no split / TMEM writes, 8 no epilogue math and stores, 32 no TMEM drain, 64 MMA-warp cycle counts into
+// y[0..3] (waiting for A slots, issuing, rows, waiting for accumulators).  The product build compiles with 0.
 #ifndef HS_SH_PROBE
 #define HS_SH_PROBE 0
 #endif
 constexpr int kShProbe = HS_SH_PROBE;
-constexpr int CIN = 16, COUT = 16;
 constexpr int SEG = 30;                 // output pixels per lane quarter
-constexpr int TPX = 4 * SEG;            // output pixels per tile
-constexpr int RAWPX = TPX + 2;          // input pixels per raw row
-constexpr int RAW_BYTES = RAWPX * CIN * 4;
-constexpr int NW = 48, KC = 2;          // stacked weight rows [W0; W1; W2], 16-byte chunks per part
-constexpr uint32_t WT = KC * NW;        // weight units (16 B) per tap
-constexpr int W_BYTES = 9 * KC * NW * 16;
-constexpr int NR = HS_SH_NR;            // raw ring depth (rows in flight per SM)
-constexpr int NACC = 6, ACOLS = 48;     // TMEM accumulators
-constexpr int AOFF = NACC * ACOLS;      // first A slot column
-constexpr int SLOT_COLS = 24;           // three parts x 8 columns
-constexpr int NSA = (512 - AOFF) / SLOT_COLS;
-constexpr int kEpi = 8, kCvt0 = 8, kProd = 12, kMma = 13, NT = 32 * 14;
-constexpr size_t SMEM = W_BYTES + (size_t)NR * RAW_BYTES + 8 * (2 * NR + 2 * NSA + 2 * NACC) + 16 + 4 * COUT;
-static_assert(NSA >= 4, "A slots");
-static_assert(RAW_BYTES % 128 == 0, "raw slots stay 128-byte aligned");
+constexpr int RAWPX = 128;              // input pixels per raw row: 32 per lane quarter (30 + the two halo columns)
+constexpr int kCvt0 = 8, kProd = 12, kMma = 13, NT = 32 * 14;
+
+template <int C>
+struct Cfg {
+  static constexpr int KC = C / 8;                 // 16-byte chunks per part
+  static constexpr int KSTEPS = C / 16;            // MMA K steps per tap
+  static constexpr int NW = 3 * C;                 // stacked weight rows [W0; W1; W2]
+  static constexpr uint32_t WT = KC * NW;          // weight units (16 B) per tap
+  static constexpr int W_BYTES = 9 * KC * NW * 16;
+  static constexpr int RAW_BYTES = RAWPX * C * 4;
+  static constexpr int NR = C == 16 ? HS_SH_NR : 8;        // raw ring depth (rows in flight per SM)
+  static constexpr int NACC = C == 16 ? 6 : 4, ACOLS = 3 * C;  // TMEM accumulators
+  static constexpr int AOFF = NACC * ACOLS;        // first A slot column
+  static constexpr int SLOT_COLS = 3 * (C / 2);    // three parts x C bf16
+  static constexpr int NSA = (512 - AOFF) / SLOT_COLS;
+  static constexpr bool HALVES = C == 32;          // epilogue groups: channel halves of every row (else alternate rows)
+  static constexpr size_t SMEM = W_BYTES + (size_t)NR * RAW_BYTES + 8 * (2 * NR + 2 * NSA + 2 * NACC) + 16 + 4 * C;
+  static_assert(NSA >= 2, "A slots");
+  static_assert(RAW_BYTES % 128 == 0, "raw slots stay 128-byte aligned");
+  static_assert(SMEM <= 232448, "shared memory budget");
+};
 
 struct ShArgs {
   const float* x;
@@ -89,95 +100,131 @@ struct ShArgs {
   const float* residual;
   const void* const* active;
   int B;
-  int band, ntile, nbands;
+  // Work units.  A row of the image is nseg segments of 30 output pixels; a unit is one tile (four segments, one per
+  // lane quarter) of a group of nb bands of one image, the group's nb * nseg segments taken in order.  The four
+  // quarters of a tile may therefore sit in different bands; they walk their bands' rows in lockstep.  nb is
+  // chosen by the launcher so that few quarters stay empty (W = 512: 18 segments per row, nb = 2 fills 9 tiles).
+  int band, nseg, nb, ntile, ngroups;
 };
 
 struct Unit {
-  int b, t, oy0, oy1;
+  int b, t, grp, bh;  // image, tile of the band group, band group, rows per band
 };
 
 HS_DEV bool unit_at(const ShArgs& a, long long u, Unit& U) {
   U.t = (int)(u % a.ntile);
-  const int band = (int)((u / a.ntile) % a.nbands);
-  U.b = (int)(u / ((long long)a.ntile * a.nbands));
-  U.oy0 = band * a.band;
-  U.oy1 = min(a.H, U.oy0 + a.band);
+  U.grp = (int)((u / a.ntile) % a.ngroups);
+  U.b = (int)(u / ((long long)a.ntile * a.ngroups));
+  U.bh = min(a.H - U.grp * a.nb * a.band, a.band);  // nb > 1 only when the band height divides H
   return !(a.active && a.active[U.b] == nullptr);
 }
 
+// lane quarter q of unit U: first output row and segment, or false if the quarter is empty
+HS_DEV bool quarter_at(const ShArgs& a, const Unit& U, int q, int& oy0, int& seg) {
+  const int s = 4 * U.t + q;
+  const int bl = s / a.nseg;
+  seg = s - bl * a.nseg;
+  oy0 = (U.grp * a.nb + bl) * a.band;
+  return s < a.nb * a.nseg;
+}
+
 // All tcgen05 work of one input row: for kx = 0, 1, 2 the taps (ky, kx) into the accumulators of output
-// rows g + 1 (ky 0, d0; its very first MMA overwrites), g (ky 1, d1) and g - 1 (ky 2, d2), each tap as
-// parts a0 [W0|W1|W2] (N 48), a1 [W0|W1] (N 32), a2 [W0] (N 16); the A slot is shifted one lane down
+// rows g + 1 (ky 0, d0; its very first MMA overwrites), g (ky 1, d1) and g - 1 (ky 2, d2), each tap and K
+// step as parts a0 [W0|W1|W2] (N 3C), a1 [W0|W1] (N 2C), a2 [W0] (N C); the A slot is shifted one lane down
 // after kx = 0 and kx = 1.  One asm block, one elect: the issuing warp is the pipeline's pace-setter once
 // the converters and the epilogue are out of the way (every instruction between two MMAs costs).
-// E0 / E1 / E2: the predicates of the MMAs of output rows g + 1 / g / g - 1.
-#define HS_SH_TAP(D, E, P0, WOFF)                                                   \
-  "add.u32 bl, %4, " WOFF ";\n\tmov.b64 db, {bl, hi};\n\t"                         \
-  "@" E " tcgen05.mma.cta_group::1.kind::f16 [" D "], [%3], db, i0, " P0 ";\n\t"    \
-  "@" E " tcgen05.mma.cta_group::1.kind::f16 [" D "], [ta1], db, i1, pt;\n\t"       \
-  "@" E " tcgen05.mma.cta_group::1.kind::f16 [" D "], [ta2], db, i2, pt;\n\t"
-#define HS_SH_SHIFT                                                                 \
-  "@es tcgen05.shift.cta_group::1.down [%3];\n\t"                                   \
-  "@es tcgen05.shift.cta_group::1.down [ta1];\n\t"                                  \
-  "@es tcgen05.shift.cta_group::1.down [ta2];\n\t"
-#define HS_SH_KX(E0, E1, E2, P0, W0, W1, W2, SH) \
-  HS_SH_TAP("%0", E0, P0, W0) HS_SH_TAP("%1", E1, "pt", W1) HS_SH_TAP("%2", E2, "pt", W2) SH
-#define HS_SH_ROW(E0, E1, E2)                                                       \
-  HS_SH_KX(E0, E1, E2, "pz", "%10", "%13", "%16", HS_SH_SHIFT)                      \
-  HS_SH_KX(E0, E1, E2, "pt", "%11", "%14", "%17", HS_SH_SHIFT)                      \
-  HS_SH_KX(E0, E1, E2, "pt", "%12", "%15", "%18", "")
+// E0 / E1 / E2: the predicates of the MMAs of output rows g + 1 / g / g - 1.  A slot columns: part p, K step
+// k at 8 (KSTEPS p + k), registers %3, ta1 .. ta5.
+#define HS_SH_MMA3(D, E, P0, A0, A1, A2)                                            \
+  "@" E " tcgen05.mma.cta_group::1.kind::f16 [" D "], [" A0 "], db, i0, " P0 ";\n\t" \
+  "@" E " tcgen05.mma.cta_group::1.kind::f16 [" D "], [" A1 "], db, i1, pt;\n\t"     \
+  "@" E " tcgen05.mma.cta_group::1.kind::f16 [" D "], [" A2 "], db, i2, pt;\n\t"
+#define HS_SH_TAP16(D, E, P0, WOFF) \
+  "add.u32 bl, %4, " WOFF ";\n\tmov.b64 db, {bl, hi};\n\t" HS_SH_MMA3(D, E, P0, "%3", "ta1", "ta2")
+#define HS_SH_TAP32(D, E, P0, WOFF)                                                                   \
+  "add.u32 bl, %4, " WOFF ";\n\tmov.b64 db, {bl, hi};\n\t" HS_SH_MMA3(D, E, P0, "%3", "ta2", "ta4")  \
+  "add.u32 bl, bl, %19;\n\tmov.b64 db, {bl, hi};\n\t" HS_SH_MMA3(D, E, "pt", "ta1", "ta3", "ta5")
+#define HS_SH_S(A) "@es tcgen05.shift.cta_group::1.down [" A "];\n\t"
+#define HS_SH_SHIFT16 HS_SH_S("%3") HS_SH_S("ta1") HS_SH_S("ta2")
+#define HS_SH_SHIFT32 HS_SH_S("%3") HS_SH_S("ta1") HS_SH_S("ta2") HS_SH_S("ta3") HS_SH_S("ta4") HS_SH_S("ta5")
+#define HS_SH_KX(TAP, E0, E1, E2, P0, W0, W1, W2, SH) TAP("%0", E0, P0, W0) TAP("%1", E1, "pt", W1) TAP("%2", E2, "pt", W2) SH
+#define HS_SH_ROW(TAP, SH, E0, E1, E2)                                              \
+  HS_SH_KX(TAP, E0, E1, E2, "pz", "%10", "%13", "%16", SH)                          \
+  HS_SH_KX(TAP, E0, E1, E2, "pt", "%11", "%14", "%17", SH)                          \
+  HS_SH_KX(TAP, E0, E1, E2, "pt", "%12", "%15", "%18", "")
 #define HS_SH_OPERANDS                                                                                          \
   "r"(d0), "r"(d1), "r"(d2), "r"(abase), "r"(wlo), "r"(valid), "n"(kDescHi), "n"(I0), "n"(I1), "n"(I2), "n"(0 * WT), \
-      "n"(1 * WT), "n"(2 * WT), "n"(3 * WT), "n"(4 * WT), "n"(5 * WT), "n"(6 * WT), "n"(7 * WT), "n"(8 * WT)
+      "n"(1 * WT), "n"(2 * WT), "n"(3 * WT), "n"(4 * WT), "n"(5 * WT), "n"(6 * WT), "n"(7 * WT), "n"(8 * WT), "n"(KK)
 #define HS_SH_HEAD                                                                                              \
-  "{\n\t.reg .pred e, es, e0, e1, e2, pz, pt;\n\t.reg .b64 db;\n\t.reg .b32 hi, i0, i1, i2, ta1, ta2, bl, m;\n\t" \
+  "{\n\t.reg .pred e, es, e0, e1, e2, pz, pt;\n\t.reg .b64 db;\n\t.reg .b32 hi, i0, i1, i2, ta1, ta2, ta3, ta4, ta5, bl, m;\n\t" \
   "mov.b32 hi, %6;\n\tmov.b32 i0, %7;\n\tmov.b32 i1, %8;\n\tmov.b32 i2, %9;\n\t"                                  \
   "elect.sync _|e, 0xffffffff;\n\t"                                                                             \
   "setp.ne.b32 pz, %5, %5;\n\tsetp.eq.b32 pt, %5, %5;\n\t"                                                       \
-  "add.u32 ta1, %3, 8;\n\tadd.u32 ta2, %3, 16;\n\t"
+  "add.u32 ta1, %3, 8;\n\tadd.u32 ta2, %3, 16;\n\tadd.u32 ta3, %3, 24;\n\tadd.u32 ta4, %3, 32;\n\tadd.u32 ta5, %3, 40;\n\t"
 
 // interior rows: all three output rows lie inside the band.  The elected lane branches into an
 // unpredicated block (predicated tcgen05 instructions made ptxas re-materialise the uniform operands of
 // every MMA: two R2UR, a VOTEU and three UMOV each).
+template <int C>
 HS_DEV void row_mmas_all(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t abase, uint32_t wlo) {
-  constexpr uint32_t I0 = idesc_bf16(128, 48), I1 = idesc_bf16(128, 32), I2 = idesc_bf16(128, 16);
+  constexpr uint32_t I0 = idesc_bf16(128, 3 * C), I1 = idesc_bf16(128, 2 * C), I2 = idesc_bf16(128, C);
+  constexpr uint32_t WT = Cfg<C>::WT, KK = 2 * Cfg<C>::NW;  // KK: weight units between K steps (two chunks)
   const uint32_t valid = (kShProbe & 1) ? 0u : 1u;
   if (kShProbe & 2) return;
-  asm volatile(HS_SH_HEAD
-               "@!e bra SH_SKIP_%=;\n\t"
-               "setp.ne.b32 es, %5, 0;\n\t" HS_SH_ROW("pt", "pt", "pt") "SH_SKIP_%=:\n\t}\n" ::HS_SH_OPERANDS
-               : "memory");
+  if constexpr (C == 16)
+    asm volatile(HS_SH_HEAD "@!e bra SH_SKIP_%=;\n\tsetp.ne.b32 es, %5, 0;\n\t"
+                 HS_SH_ROW(HS_SH_TAP16, HS_SH_SHIFT16, "pt", "pt", "pt") "SH_SKIP_%=:\n\t}\n" ::HS_SH_OPERANDS
+                 : "memory");
+  else
+    asm volatile(HS_SH_HEAD "@!e bra SH_SKIP_%=;\n\tsetp.ne.b32 es, %5, 0;\n\t"
+                 HS_SH_ROW(HS_SH_TAP32, HS_SH_SHIFT32, "pt", "pt", "pt") "SH_SKIP_%=:\n\t}\n" ::HS_SH_OPERANDS
+                 : "memory");
   __syncwarp();
 }
 
 // band edges: valid bit 0 / 1 / 2 = output row g + 1 / g / g - 1 lies inside the band
+#define HS_SH_EDGE_PREDS                                                              \
+  "and.b32 m, %5, 1;\n\tsetp.ne.b32 e0, m, 0;\n\tand.pred e0, e0, e;\n\t"             \
+  "and.b32 m, %5, 2;\n\tsetp.ne.b32 e1, m, 0;\n\tand.pred e1, e1, e;\n\t"             \
+  "and.b32 m, %5, 4;\n\tsetp.ne.b32 e2, m, 0;\n\tand.pred e2, e2, e;\n\t"             \
+  "and.pred es, e, e;\n\t"
+template <int C>
 HS_DEV void row_mmas_edge(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t abase, uint32_t wlo, uint32_t valid) {
-  constexpr uint32_t I0 = idesc_bf16(128, 48), I1 = idesc_bf16(128, 32), I2 = idesc_bf16(128, 16);
+  constexpr uint32_t I0 = idesc_bf16(128, 3 * C), I1 = idesc_bf16(128, 2 * C), I2 = idesc_bf16(128, C);
+  constexpr uint32_t WT = Cfg<C>::WT, KK = 2 * Cfg<C>::NW;
   if (kShProbe & 2) return;
-  asm volatile(HS_SH_HEAD
-               "and.b32 m, %5, 1;\n\tsetp.ne.b32 e0, m, 0;\n\tand.pred e0, e0, e;\n\t"
-               "and.b32 m, %5, 2;\n\tsetp.ne.b32 e1, m, 0;\n\tand.pred e1, e1, e;\n\t"
-               "and.b32 m, %5, 4;\n\tsetp.ne.b32 e2, m, 0;\n\tand.pred e2, e2, e;\n\t"
-               "and.pred es, e, e;\n\t" HS_SH_ROW("e0", "e1", "e2") "}\n" ::HS_SH_OPERANDS
-               : "memory");
+  if constexpr (C == 16)
+    asm volatile(HS_SH_HEAD HS_SH_EDGE_PREDS HS_SH_ROW(HS_SH_TAP16, HS_SH_SHIFT16, "e0", "e1", "e2") "}\n" ::HS_SH_OPERANDS
+                 : "memory");
+  else
+    asm volatile(HS_SH_HEAD HS_SH_EDGE_PREDS HS_SH_ROW(HS_SH_TAP32, HS_SH_SHIFT32, "e0", "e1", "e2") "}\n" ::HS_SH_OPERANDS
+                 : "memory");
 }
-#undef HS_SH_TAP
-#undef HS_SH_SHIFT
+#undef HS_SH_MMA3
+#undef HS_SH_TAP16
+#undef HS_SH_TAP32
+#undef HS_SH_S
+#undef HS_SH_SHIFT16
+#undef HS_SH_SHIFT32
 #undef HS_SH_KX
 #undef HS_SH_ROW
 #undef HS_SH_OPERANDS
 #undef HS_SH_HEAD
+#undef HS_SH_EDGE_PREDS
 
 HS_DEV void tmem_st8(uint32_t taddr, const uint4& lo, const uint4& hi) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(lo.x),
                "r"(lo.y), "r"(lo.z), "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w));
 }
 
-__global__ void __launch_bounds__(NT, 1) k_conv16_shift(ShArgs a) {
+template <int C>
+__global__ void __launch_bounds__(NT, 1) k_conv_shift(ShArgs a) {
+  using F = Cfg<C>;
+  constexpr int KC = F::KC, NW = F::NW, NR = F::NR, NACC = F::NACC, NSA = F::NSA, ACOLS = F::ACOLS;
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* wst = smem;
-  unsigned char* raw = smem + W_BYTES;
-  uint64_t* raw_full = reinterpret_cast<uint64_t*>(raw + (size_t)NR * RAW_BYTES);
+  unsigned char* raw = smem + F::W_BYTES;
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(raw + (size_t)NR * F::RAW_BYTES);
   uint64_t* raw_empty = raw_full + NR;
   uint64_t* a_full = raw_empty + NR;
   uint64_t* a_empty = a_full + NSA;
@@ -186,21 +233,21 @@ __global__ void __launch_bounds__(NT, 1) k_conv16_shift(ShArgs a) {
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(acc_empty + NACC);
   float* s_bias = reinterpret_cast<float*>(s_tmem + 4);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const long long nunits = (long long)a.B * a.ntile * a.nbands;
+  const long long nunits = (long long)a.B * a.ntile * a.ngroups;
 
   // ---- setup: resident weight stack [W0; W1; W2], layout (tap, chunk, row) x 16 B (as conv_tc.cu)
-  for (int e = tid; e < 9 * KC * COUT; e += NT) {
-    const int n = e % COUT, c = (e / COUT) % KC, t = e / (COUT * KC);
-    const float* src = a.w + ((size_t)n * 9 + t) * CIN + 8 * c;
+  for (int e = tid; e < 9 * KC * C; e += NT) {
+    const int n = e % C, c = (e / C) % KC, t = e / (C * KC);
+    const float* src = a.w + ((size_t)n * 9 + t) * C + 8 * c;
     const float4 v0 = __ldg(reinterpret_cast<const float4*>(src)), v1 = __ldg(reinterpret_cast<const float4*>(src + 4));
     const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
     uint4 p[3];
     split_bf16x3(v, p[0], p[1], p[2]);
 #pragma unroll
     for (int part = 0; part < 3; ++part)
-      *reinterpret_cast<uint4*>(wst + ((size_t)(t * KC + c) * NW + part * COUT + n) * 16) = p[part];
+      *reinterpret_cast<uint4*>(wst + ((size_t)(t * KC + c) * NW + part * C + n) * 16) = p[part];
   }
-  if (tid < COUT) s_bias[tid] = a.bias[tid];
+  if (tid < C) s_bias[tid] = a.bias[tid];
   if (tid == 0) {
     for (int i = 0; i < NR; ++i) {
       mbar_init(smem_u32(&raw_full[i]), 1);
@@ -212,7 +259,7 @@ __global__ void __launch_bounds__(NT, 1) k_conv16_shift(ShArgs a) {
     }
     for (int i = 0; i < NACC; ++i) {
       mbar_init(smem_u32(&acc_full[i]), 1);
-      mbar_init(smem_u32(&acc_empty[i]), 4);  // the four warps of the draining group
+      mbar_init(smem_u32(&acc_empty[i]), F::HALVES ? 8 : 4);  // the warps that drain one output row
     }
     fence_mbar_init();
   }
@@ -230,24 +277,40 @@ __global__ void __launch_bounds__(NT, 1) k_conv16_shift(ShArgs a) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == kProd) {
-    // ================= producer: one bulk copy per input row (122 pixels x 64 B, clipped to the image)
+    // ================= producer: per input row one bulk copy per lane quarter (32 pixels, clipped to the image)
     if (lane == 0) {
       uint32_t seq = 0;
       for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
         Unit U;
         if (!unit_at(a, u, U)) continue;
-        const int x0 = TPX * U.t - 1;
-        const int clo = max(x0, 0), chi = min(x0 + RAWPX, a.W);
-        const float* img = a.x + (size_t)U.b * a.H * a.W * CIN;
-        for (int g = U.oy0 - 1; g <= U.oy1; ++g, ++seq) {
+        const float* img = a.x + (size_t)U.b * a.H * a.W * C;
+        int qy0[4], qx0[4];
+        bool qv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          int seg;
+          qv[q] = quarter_at(a, U, q, qy0[q], seg);
+          qx0[q] = SEG * seg - 1;
+        }
+        for (int i = -1; i <= U.bh; ++i, ++seq) {
           const uint32_t s = seq % NR, use = seq / NR;
           if (use > 0) mbar_wait(smem_u32(&raw_empty[s]), (use - 1) & 1);
           const uint32_t bar = smem_u32(&raw_full[s]);
-          if (g >= 0 && g < a.H && chi > clo) {
-            const uint32_t bytes = (uint32_t)(chi - clo) * CIN * 4;
-            mbar_arrive_tx(bar, bytes);
-            bulk_g2s(smem_u32(raw + (size_t)s * RAW_BYTES + (size_t)(clo - x0) * CIN * 4),
-                     img + ((size_t)g * a.W + clo) * CIN, bytes, bar);
+          uint32_t total = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int g = qy0[q] + i, clo = max(qx0[q], 0), chi = min(qx0[q] + 32, a.W);
+            if (qv[q] && g >= 0 && g < a.H && chi > clo) total += (uint32_t)(chi - clo) * C * 4;
+          }
+          if (total) {
+            mbar_arrive_tx(bar, total);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int g = qy0[q] + i, clo = max(qx0[q], 0), chi = min(qx0[q] + 32, a.W);
+              if (qv[q] && g >= 0 && g < a.H && chi > clo)
+                bulk_g2s(smem_u32(raw + (size_t)s * F::RAW_BYTES + (size_t)(32 * q + clo - qx0[q]) * C * 4),
+                         img + ((size_t)g * a.W + clo) * C, (uint32_t)(chi - clo) * C * 4, bar);
+            }
           } else {
             mbar_arrive(bar);
           }
@@ -255,59 +318,86 @@ __global__ void __launch_bounds__(NT, 1) k_conv16_shift(ShArgs a) {
       }
     }
   } else if (warp >= kCvt0 && warp < kCvt0 + 4) {
-    // ================= converters: warp q owns TMEM lane quarter q; lane j holds input pixel x0 + 30 q + j
+    // ================= converters: warp q owns TMEM lane quarter q; lane j holds input pixel 30 seg - 1 + j of its segment
     const int q = warp - kCvt0;
     uint32_t seq = 0;
     for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
       if (!unit_at(a, u, U)) continue;
-      const int prel = SEG * q + lane;              // pixel within the raw row
-      const int xin = TPX * U.t - 1 + prel;
-      const bool xok = xin >= 0 && xin < a.W;
-      for (int g = U.oy0 - 1; g <= U.oy1; ++g, ++seq) {
+      const int prel = 32 * q + lane;               // pixel within the raw row
+      int qy0, seg;
+      const bool qv = quarter_at(a, U, q, qy0, seg);
+      const int xin = SEG * seg - 1 + lane;
+      const bool xok = qv && xin >= 0 && xin < a.W;
+      for (int i = -1; i <= U.bh; ++i, ++seq) {
+        const int g = qy0 + i;
         const uint32_t s = seq % NR;
         mbar_wait(smem_u32(&raw_full[s]), (seq / NR) & 1);
-        float4 v[4];
+        constexpr int NP = C / 4;  // 16-byte pieces of a pixel
+        float4 v[NP];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i = 0; i < NP; ++i) v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (xok && g >= 0 && g < a.H) {
-          const float4* src = reinterpret_cast<const float4*>(raw + (size_t)s * RAW_BYTES + (size_t)prel * CIN * 4);
+          const float4* src = reinterpret_cast<const float4*>(raw + (size_t)s * F::RAW_BYTES + (size_t)prel * C * 4);
+          if constexpr (C == 32 || HS_SH_ROT) {
+            // a lane's pixel is 4 C bytes, so eight lanes reading piece i of their pixels would hit one or two
+            // bank groups; lane L reads its pieces rotated by r instead -- eight distinct bank groups per
+            // wavefront -- and rotates them back in registers (log2(NP) select stages)
+            const int r = C == 32 ? (lane & 7) : ((lane >> 1) & 3);
+            float4 w4[NP];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) v[i] = src[i];
+            for (int i = 0; i < NP; ++i) w4[i] = src[(i + r) & (NP - 1)];
+#pragma unroll
+            for (int st = 1; st < NP; st <<= 1) {
+              float4 t4[NP];
+#pragma unroll
+              for (int i = 0; i < NP; ++i) t4[i] = (r & st) ? w4[(i + NP - st) & (NP - 1)] : w4[i];
+#pragma unroll
+              for (int i = 0; i < NP; ++i) w4[i] = t4[i];
+            }
+#pragma unroll
+            for (int i = 0; i < NP; ++i) v[i] = w4[i];
+          } else {
+#pragma unroll
+            for (int i = 0; i < NP; ++i) v[i] = src[i];
+          }
         }
-        uint4 lo[3] = {}, hi[3] = {};
+        // part p of the row: chunk c (8 channels) at words 4 c .. 4 c + 3
+        uint4 pw[3][KC] = {};
         if (!(kShProbe & 4)) {
-          const float f0[8] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y, v[1].z, v[1].w};
-          const float f1[8] = {v[2].x, v[2].y, v[2].z, v[2].w, v[3].x, v[3].y, v[3].z, v[3].w};
-          split_bf16x3(f0, lo[0], lo[1], lo[2]);
-          split_bf16x3(f1, hi[0], hi[1], hi[2]);
+#pragma unroll
+          for (int c = 0; c < KC; ++c) {
+            const float f[8] = {v[2 * c].x, v[2 * c].y, v[2 * c].z, v[2 * c].w,
+                                v[2 * c + 1].x, v[2 * c + 1].y, v[2 * c + 1].z, v[2 * c + 1].w};
+            split_bf16x3(f, pw[0][c], pw[1][c], pw[2][c]);
+          }
         }
-#if !(HS_SH_X & 1)
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&raw_empty[s]));
-#endif
         const uint32_t as = seq % NSA, ause = seq / NSA;
         if (ause > 0) mbar_wait(smem_u32(&a_empty[as]), (ause - 1) & 1);
         tc_fence_after();
-        const uint32_t tcol = tmem + ((uint32_t)(32 * q) << 16) + AOFF + as * SLOT_COLS;
+        const uint32_t tcol = tmem + ((uint32_t)(32 * q) << 16) + F::AOFF + as * F::SLOT_COLS;
+        if (!(kShProbe & 4)) {
 #pragma unroll
-        for (int part = 0; part < 3; ++part)
-          if (!(kShProbe & 4)) tmem_st8(tcol + 8 * part, lo[part], hi[part]);
+          for (int part = 0; part < 3; ++part)
+#pragma unroll
+            for (int c = 0; c < KC; c += 2) tmem_st8(tcol + (C / 2) * part + 4 * c, pw[part][c], pw[part][c + 1]);
+        }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&a_full[as]));
-#if HS_SH_X & 1
+        // The raw slot is released only now: released right after the loads (before the split), the producer's
+        // next bulk copy overwrote pixels of rows whose bank-conflicted loads were still replaying (rare wrong
+        // pixels, caught by tests/test_gpu_determinism.py); here the TMEM writes depend on the loaded values.
         fence_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&raw_empty[s]));
-#endif
       }
     }
   } else if (warp == kMma) {
     // ================= MMA issuer: input-row stationary, two shifts per row.  The whole warp walks the
     // schedule with warp-uniform incremental bookkeeping (no divisions); one asm block per input row
-    // issues its 27 MMAs and 6 shifts from the elected lane.
+    // issues its MMAs and shifts from the elected lane.
     const uint32_t wlo = desc_lo(smem_u32(wst), NW * 16);
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
     uint32_t as = 0, a_par = 0;        // A slot of the next input row and the parity of its a_full phase
@@ -317,10 +407,10 @@ __global__ void __launch_bounds__(NT, 1) k_conv16_shift(ShArgs a) {
       Unit U;
       if (!unit_at(a, u, U)) continue;
       uint32_t s_new = 0, s_cur = 0, s_old = 0;
-      for (int g = U.oy0 - 1; g <= U.oy1; ++g) {
+      for (int g = -1; g <= U.bh; ++g) {  // g: input row relative to the quarters' bands
         const long long tq0 = (kShProbe & 64) ? clock64() : 0;
         mbar_wait(smem_u32(&a_full[as]), a_par);
-        const bool v_new = g + 1 < U.oy1, v_cur = g >= U.oy0 && g < U.oy1, v_old = g - 1 >= U.oy0;
+        const bool v_new = g + 1 < U.bh, v_cur = g >= 0 && g < U.bh, v_old = g - 1 >= 0;
         s_old = s_cur;
         s_cur = s_new;
         const long long tq01 = (kShProbe & 64) ? clock64() : 0;
@@ -334,14 +424,12 @@ __global__ void __launch_bounds__(NT, 1) k_conv16_shift(ShArgs a) {
         }
         tc_fence_after();
         const long long tq1 = (kShProbe & 64) ? clock64() : 0;
-        const uint32_t abase = tm + AOFF + as * SLOT_COLS;
-        if ((kShProbe & 16) && v_new && v_cur && v_old)  // timing probe: one accumulator for all three output rows
-          row_mmas_all(tm + s_new * ACOLS, tm + s_new * ACOLS, tm + s_new * ACOLS, abase, wlo);
-        else if (v_new && v_cur && v_old)
-          row_mmas_all(tm + s_new * ACOLS, tm + s_cur * ACOLS, tm + s_old * ACOLS, abase, wlo);
+        const uint32_t abase = tm + F::AOFF + as * F::SLOT_COLS;
+        if (v_new && v_cur && v_old)
+          row_mmas_all<C>(tm + s_new * ACOLS, tm + s_cur * ACOLS, tm + s_old * ACOLS, abase, wlo);
         else
-          row_mmas_edge(tm + s_new * ACOLS, tm + s_cur * ACOLS, tm + s_old * ACOLS, abase, wlo,
-                        (v_new ? 1u : 0u) | (v_cur ? 2u : 0u) | (v_old ? 4u : 0u));
+          row_mmas_edge<C>(tm + s_new * ACOLS, tm + s_cur * ACOLS, tm + s_old * ACOLS, abase, wlo,
+                           (v_new ? 1u : 0u) | (v_cur ? 2u : 0u) | (v_old ? 4u : 0u));
         mma_commit(smem_u32(&a_empty[as]));
         if (v_old) mma_commit(smem_u32(&acc_full[s_old]));
         if (++as == (uint32_t)NSA) {
@@ -364,9 +452,12 @@ __global__ void __launch_bounds__(NT, 1) k_conv16_shift(ShArgs a) {
       a.y[3] = (float)dbg_wait2 / (float)dbg_rows;
     }
   } else {
-    // ================= epilogue: group hg drains the output rows with tile % 2 == hg; warp q4 its lane quarter
+    // ================= epilogue: warp q4 drains its lane quarter.  16 channels: group hg takes the output rows
+    // with tile % 2 == hg; 32 channels: group hg takes channels 16 hg .. 16 hg + 15 of every output row.
     const int q4 = warp & 3, hg = warp >> 2;
     const int gi = lane & 3, gb = lane & ~3;
+    const int ch0 = F::HALVES ? 16 * hg : 0;  // first channel of this warp
+    constexpr int STEP = F::HALVES ? 1 : 2;   // output rows between two rows of this group
     uint32_t tile = 0;
     for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
@@ -374,43 +465,46 @@ __global__ void __launch_bounds__(NT, 1) k_conv16_shift(ShArgs a) {
       const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[U.b] : 0) : U.b) *
                                                    a.addend_bstride
                                   : nullptr;
-      const float* res = a.residual ? a.residual + (size_t)U.b * a.H * a.W * COUT : nullptr;
-      float* yimg = a.y + (size_t)U.b * a.H * a.W * COUT;
-      const int xg0 = SEG * (4 * U.t + q4) + gb;  // output pixel of this lane group's first lane
+      const float* res = a.residual ? a.residual + (size_t)U.b * a.H * a.W * C : nullptr;
+      float* yimg = a.y + (size_t)U.b * a.H * a.W * C;
+      int qy0, seg;
+      const bool qv = quarter_at(a, U, q4, qy0, seg);
+      const int xg0 = SEG * seg + gb;  // output pixel of this lane group's first lane
+      const int oy_end = qy0 + U.bh;
       bool ok[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) ok[j] = gb + j < SEG && xg0 + j < a.W;
+      for (int j = 0; j < 4; ++j) ok[j] = qv && gb + j < SEG && xg0 + j < a.W;
       // side inputs (addend, residual) in the post-transpose layout (chunk gi of the group's four pixels).
-      // A row's side inputs are requested as soon as the group's previous row has used its own (two output
-      // rows ahead) and are only touched at the store, so their DRAM latency runs under the next accumulator
-      // wait, drain and softplus.  (Requested right before the accumulator wait, their first use held 28% of
-      // all stall samples in ncu; summing addend and residual at load time stalls on the loads just the same.)
+      // A row's side inputs are requested as soon as the group's previous row has used its own and are only
+      // touched at the store, so their DRAM latency runs under the next accumulator wait, drain and softplus.
+      // (Requested right before the accumulator wait, their first use held 28% of all stall samples in ncu;
+      // summing addend and residual at load time stalls on the loads just the same.)
       float4 sa[4], sr[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) sa[j] = sr[j] = make_float4(0.f, 0.f, 0.f, 0.f);
       auto issue_side = [&](int oy) {
-        const size_t gp = (size_t)oy * a.W + xg0;
+        const size_t gp = ((size_t)oy * a.W + xg0) * C + ch0;
         if (add) {
-          const float4* ap = reinterpret_cast<const float4*>(add + gp * COUT);
+          const float4* ap = reinterpret_cast<const float4*>(add + gp);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            if (ok[j]) sa[j] = __ldg(ap + j * 4 + gi);
+            if (ok[j]) sa[j] = __ldg(ap + j * (C / 4) + gi);
         }
         if (res) {
-          const float4* rp = reinterpret_cast<const float4*>(res + gp * COUT);
+          const float4* rp = reinterpret_cast<const float4*>(res + gp);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            if (ok[j]) sr[j] = __ldg(rp + j * 4 + gi);
+            if (ok[j]) sr[j] = __ldg(rp + j * (C / 4) + gi);
         }
       };
       {
-        const int first = U.oy0 + (int)((tile ^ (uint32_t)hg) & 1);  // this group's first row of the unit
-        if (first < U.oy1) issue_side(first);
+        const int first = F::HALVES ? qy0 : qy0 + (int)((tile ^ (uint32_t)hg) & 1);  // this group's first row
+        if (first < oy_end) issue_side(first);
       }
-      for (int oy = U.oy0; oy < U.oy1; ++oy, ++tile) {
-        if ((int)(tile & 1) != hg) continue;
+      for (int oy = qy0; oy < oy_end; ++oy, ++tile) {
+        if (!F::HALVES && (int)(tile & 1) != hg) continue;
         const uint32_t acc = tile % NACC;
-        const size_t gpix = (size_t)oy * a.W + xg0;
+        const size_t gpix = ((size_t)oy * a.W + xg0) * C + ch0;
         mbar_wait(smem_u32(&acc_full[acc]), (tile / NACC) & 1);
         tc_fence_after();
         float o[16] = {};
@@ -418,10 +512,10 @@ __global__ void __launch_bounds__(NT, 1) k_conv16_shift(ShArgs a) {
         for (int n0 = 0; n0 < 16; n0 += 8) {
           if (kShProbe & 32) break;
           uint32_t r0[8], r1[8], r2[8];
-          const uint32_t col = tmem + ((uint32_t)(q4 * 32) << 16) + acc * ACOLS + n0;
+          const uint32_t col = tmem + ((uint32_t)(q4 * 32) << 16) + acc * ACOLS + ch0 + n0;
           tmem_ld8(col, r0);
-          tmem_ld8(col + COUT, r1);
-          tmem_ld8(col + 2 * COUT, r2);
+          tmem_ld8(col + C, r1);
+          tmem_ld8(col + 2 * C, r2);
           tmem_wait_ld();
 #pragma unroll
           for (int j = 0; j < 8; j += 2) {  // (x0 + x1) + x2 partial sums, channel pairs packed (FADD2)
@@ -434,13 +528,13 @@ __global__ void __launch_bounds__(NT, 1) k_conv16_shift(ShArgs a) {
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&acc_empty[acc]));  // TMEM free; finish from registers
         if (kShProbe & 8) {
-          if (oy + 2 < U.oy1) issue_side(oy + 2);
+          if (oy + STEP < oy_end) issue_side(oy + STEP);
           continue;
         }
         float4 ch[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const float4 bs = *reinterpret_cast<const float4*>(s_bias + 4 * q);
+          const float4 bs = *reinterpret_cast<const float4*>(s_bias + ch0 + 4 * q);
           const uint64_t o01 = add2(pkf(o[4 * q], o[4 * q + 1]), pkf(bs.x, bs.y));
           const uint64_t o23 = add2(pkf(o[4 * q + 2], o[4 * q + 3]), pkf(bs.z, bs.w));
           float4 v = make_float4(lo_f(o01), hi_f(o01), lo_f(o23), hi_f(o23));
@@ -453,15 +547,15 @@ __global__ void __launch_bounds__(NT, 1) k_conv16_shift(ShArgs a) {
           ch[q] = v;
         }
         group4_transpose(ch, gi);  // lane gi: chunk gi of the group's four pixels
-        float4* yb = reinterpret_cast<float4*>(yimg + gpix * COUT);
+        float4* yb = reinterpret_cast<float4*>(yimg + gpix);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {  // o + (addend + residual), as conv_tc.cu
           const uint64_t s01 = add2(pkf(sa[j].x, sa[j].y), pkf(sr[j].x, sr[j].y));
           const uint64_t s23 = add2(pkf(sa[j].z, sa[j].w), pkf(sr[j].z, sr[j].w));
           const uint64_t q01 = add2(pkf(ch[j].x, ch[j].y), s01), q23 = add2(pkf(ch[j].z, ch[j].w), s23);
-          if (ok[j]) yb[j * 4 + gi] = make_float4(lo_f(q01), hi_f(q01), lo_f(q23), hi_f(q23));
+          if (ok[j]) yb[j * (C / 4) + gi] = make_float4(lo_f(q01), hi_f(q01), lo_f(q23), hi_f(q23));
         }
-        if (oy + 2 < U.oy1) issue_side(oy + 2);
+        if (oy + STEP < oy_end) issue_side(oy + STEP);
       }
     }
   }
@@ -473,38 +567,64 @@ __global__ void __launch_bounds__(NT, 1) k_conv16_shift(ShArgs a) {
   }
 }
 
-}  // namespace
-
-bool conv_shift_launch(const float* x, int H, int W, float* y, const float* w, const float* bias, int softplus,
-                       const float* addend, long long addend_bstride, int addend_per_model, const int* model_of,
-                       const float* residual, const void* const* active, int B, cudaStream_t st) {
+template <int C>
+bool launch_shift(ShArgs a, cudaStream_t st) {
+  using F = Cfg<C>;
   static int sms = 0;
   if (!sms) {
-    cudaFuncSetAttribute(k_conv16_shift, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    cudaFuncSetAttribute(k_conv_shift<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F::SMEM);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  ShArgs a{x, H, W, y, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual, active, B,
-           HS_SH_BAND_MAX, (W + TPX - 1) / TPX, 0};
+  a.band = HS_SH_BAND_MAX;
+  a.nseg = (a.W + SEG - 1) / SEG;
   // band height as conv_tc.cu: halve it until the RHS still iterating give every CTA >= 6 units
-  const double act = prof::active_hint(B);
+  const double act = prof::active_hint(a.B);
   long long grid = sms;
-  while (a.band > 8 && act * a.ntile * ((H + a.band - 1) / a.band) < 6.0 * grid) a.band /= 2;
-  a.nbands = (H + a.band - 1) / a.band;
-  const long long nunits = (long long)B * a.ntile * a.nbands;
+  while (a.band > 8 && act * ((a.nseg + 3) / 4) * ((a.H + a.band - 1) / a.band) < 6.0 * grid) a.band /= 2;
+  const int nbands = (a.H + a.band - 1) / a.band;
+  // bands per unit group: the smallest of 1, 2, 4 that leaves the fewest empty lane quarters
+  a.nb = 1;
+  if (a.H % a.band == 0) {
+    double best = (double)a.nseg / (4 * ((a.nseg + 3) / 4));
+    for (int nb = 2; nb <= 4; nb *= 2) {
+      if (nbands % nb) break;
+      const double eff = (double)(nb * a.nseg) / (4 * ((nb * a.nseg + 3) / 4));
+      if (eff > best + 1e-9) {
+        best = eff;
+        a.nb = nb;
+      }
+    }
+  }
+  a.ntile = (a.nb * a.nseg + 3) / 4;
+  a.ngroups = nbands / a.nb;
+  const long long nunits = (long long)a.B * a.ntile * a.ngroups;
   if (nunits < grid) grid = nunits;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(NT);
-  cfg.dynamicSmemBytes = SMEM;
+  cfg.dynamicSmemBytes = F::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_conv16_shift, a) == cudaSuccess;
+  return cudaLaunchKernelEx(&cfg, k_conv_shift<C>, a) == cudaSuccess;
+}
+
+}  // namespace
+
+bool conv_shift_launch(int channels, const float* x, int H, int W, float* y, const float* w, const float* bias,
+                       int softplus, const float* addend, long long addend_bstride, int addend_per_model,
+                       const int* model_of, const float* residual, const void* const* active, int B,
+                       cudaStream_t st) {
+  ShArgs a{x, H, W, y, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual, active, B,
+           0, 0, 0, 0, 0};
+  if (channels == 16) return launch_shift<16>(a, st);
+  if (channels == 32) return launch_shift<32>(a, st);
+  return false;
 }
 
 }  // namespace hs

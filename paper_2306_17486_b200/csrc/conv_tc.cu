@@ -100,6 +100,9 @@ constexpr int kProbe = HS_TC_PROBE;
 #ifndef HS_TC_SHIFT
 #define HS_TC_SHIFT 1  // 16 -> 16 stride-1 layers on the tcgen05.shift kernel (conv_shift.cu); 0 keeps the tap-view kernel below
 #endif
+#ifndef HS_TC_SHIFT32
+#define HS_TC_SHIFT32 1  // 32 -> 32 stride-1 layers on the tcgen05.shift kernel as well
+#endif
 #ifndef HS_TC_CVT_GROUPS
 #define HS_TC_CVT_GROUPS 1  // measured round 2 (C3 and C2 level-0 shapes): one group of four converter warps is 9-10% faster than two
 #endif
@@ -1248,7 +1251,8 @@ bool conv_tc_supported(int cin, int cout, int stride, int transposed, int H, int
   if (!conv_tc_enabled) return false;
   const int mode = transposed ? 2 : (stride == 2 ? 1 : 0);
   const int width = mode == 2 ? W : Wo;
-  if (HS_TC_SHIFT && !planar && mode == 0 && cin == 16 && cout == 16) return true;  // conv_shift.cu: 30-pixel segments, any width
+  if (!planar && mode == 0 && cin == cout && ((HS_TC_SHIFT && cin == 16) || (HS_TC_SHIFT32 && cin == 32)))
+    return true;  // conv_shift.cu: 30-pixel segments, any width
   if (width % 64) return false;
   return slice_for(cin, cout, mode) > 0;
 }
@@ -1260,8 +1264,8 @@ bool conv_tc_launch(const float* x, int H, int W, int cin, float* y, int Ho, int
   TcArgs a{x, H, W, y, Ho, Wo, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual,
            active, B, 32, planar};
   const int mode = transposed ? 2 : (stride == 2 ? 1 : 0);
-  if (HS_TC_SHIFT && mode == 0 && cin == 16 && cout == 16 && !planar && !kProbe)
-    return conv_shift_launch(x, H, W, y, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of,
+  if (!planar && !kProbe && mode == 0 && cin == cout && ((HS_TC_SHIFT && cin == 16) || (HS_TC_SHIFT32 && cin == 32)))
+    return conv_shift_launch(cin, x, H, W, y, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of,
                              residual, active, B, st);
   const bool m128 = ((mode == 2 ? W : Wo) % 128) == 0 && !(kProbe & 32);
 #define HS_TC(CI, CO, MD, CSL)                                           \

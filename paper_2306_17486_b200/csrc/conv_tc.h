@@ -9,11 +9,12 @@ bool conv_tc_launch(const float* x, int H, int W, int cin, float* y, int Ho, int
                     int transposed, const float* w, const float* bias, int softplus, const float* addend,
                     long long addend_bstride, int addend_per_model, const int* model_of, const float* residual,
                     const void* const* active, int B, cudaStream_t st, int planar = 0);
-// 16 -> 16 stride-1 layers (conv_shift.cu): A operand in TMEM, horizontal taps by tcgen05.shift; any width.
-// conv_tc_launch routes that shape here (NHWC output only).
-bool conv_shift_launch(const float* x, int H, int W, float* y, const float* w, const float* bias, int softplus,
-                       const float* addend, long long addend_bstride, int addend_per_model, const int* model_of,
-                       const float* residual, const void* const* active, int B, cudaStream_t st);
+// 16 -> 16 and 32 -> 32 stride-1 layers (conv_shift.cu): A operand in TMEM, horizontal taps by tcgen05.shift; any
+// width.  conv_tc_launch routes those shapes here (NHWC output only).
+bool conv_shift_launch(int channels, const float* x, int H, int W, float* y, const float* w, const float* bias,
+                       int softplus, const float* addend, long long addend_bstride, int addend_per_model,
+                       const int* model_of, const float* residual, const void* const* active, int B,
+                       cudaStream_t st);
 // K-streamed tcgen05 kernel for the >= 64-channel layers (conv_wide.cu): 64->64 / 128->128 stride 1,
 // 32->64 / 64->128 / 128->128 stride 2, 128->64 and 128->128 (two 64-channel slices) transposed, widths
 // (transposed: input widths) that are multiples of 128.  Same arguments and epilogue as conv_tc_launch.

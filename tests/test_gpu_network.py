@@ -77,6 +77,8 @@ def test_tconv_shapes(rng, cin, cout, hw):
                                                # segment / tile, one-segment images, bands of 1 and 33+ rows
                                                (16, 16, 0, (7, 100)), (16, 16, 0, (1, 33)), (16, 16, 0, (33, 30)),
                                                (16, 16, 0, (3, 121)), (16, 16, 0, (40, 250)),
+                                               (32, 32, 0, (7, 100)), (32, 32, 0, (1, 33)), (32, 32, 0, (35, 150)),
+                                               (32, 32, 0, (9, 256)),
                                                (32, 32, 0, (4, 128)),
                                                (16, 32, 1, (6, 256)), (32, 16, 2, (3, 128)), (32, 16, 2, (2, 256)),
                                                # M = 64 tiles (64-wide levels) and cout split across CTAs
