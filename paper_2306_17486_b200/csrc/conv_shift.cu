@@ -14,8 +14,9 @@
 //   by one thread run in issue order (tools/shift_probe.cu, measured on B200).
 // A quarter of 32 lanes therefore serves 30 output pixels: lane j starts with input pixel P0 + j
 // (tap kx = 0 of output pixel P0 + j + 1), holds P0 + j + 1 after one shift and P0 + j + 2 after two;
-// lanes 30 and 31 end up stale and are never stored.  A tile is four such segments of one row (120
-// output pixels, 122 input pixels).
+// lanes 30 and 31 end up stale and are never stored.  A tile is four such segments, taken in order from
+// the segments of a group of 1, 2 or 4 bands of rows (so few lane quarters stay empty whatever the width);
+// its quarters walk their bands' rows in lockstep.
 //
 // The schedule is input-row stationary: input row g (one TMEM slot) feeds output rows g + 1 (ky = 0),
 // g (ky = 1) and g - 1 (ky = 2) while it is shifted twice, so three accumulators are open at a time and
@@ -24,7 +25,7 @@
 //
 // Warp roles (one persistent CTA per SM): warps 0-7 epilogue (two groups of four alternate output rows,
 // one warp per lane quarter), warps 8-11 converters (one per lane quarter: raw fp32 pixel -> exact
-// bf16x3 split -> tcgen05.st), warp 12 producer (one bulk copy per input row into a 12-deep raw ring),
+// bf16x3 split -> tcgen05.st), warp 12 producer (per input row one bulk copy per lane quarter into a 12-deep raw ring),
 // warp 13 MMA issuer.  Precision and results follow conv_tc.cu: six bf16 products per fp32 product,
 // the three column groups summed in the epilogue, bias, softplus, addend / residual, NHWC stores as whole
 // 64-byte pixels (group-of-four transpose).
