@@ -101,6 +101,7 @@ struct ShArgs {
   const float* residual;
   const void* const* active;
   int B;
+  int Ho, Wo;  // output size (the stride-2 kernel; stride 1: H, W)
   // Work units.  A row of the image is nseg segments of 30 output pixels; a unit is one tile (four segments, one per
   // lane quarter) of a group of nb bands of one image, the group's nb * nseg segments taken in order.  The four
   // quarters of a tile may therefore sit in different bands; they walk their bands' rows in lockstep.  nb is
@@ -116,7 +117,7 @@ HS_DEV bool unit_at(const ShArgs& a, long long u, Unit& U) {
   U.t = (int)(u % a.ntile);
   U.grp = (int)((u / a.ntile) % a.ngroups);
   U.b = (int)(u / ((long long)a.ntile * a.ngroups));
-  U.bh = min(a.H - U.grp * a.nb * a.band, a.band);  // nb > 1 only when the band height divides H
+  U.bh = min(a.Ho - U.grp * a.nb * a.band, a.band);  // output rows; nb > 1 only when the band height divides Ho
   return !(a.active && a.active[U.b] == nullptr);
 }
 
@@ -568,26 +569,371 @@ __global__ void __launch_bounds__(NT, 1) k_conv_shift(ShArgs a) {
   }
 }
 
-template <int C>
-bool launch_shift(ShArgs a, cudaStream_t st) {
-  using F = Cfg<C>;
-  static int sms = 0;
-  if (!sms) {
-    cudaFuncSetAttribute(k_conv_shift<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F::SMEM);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+// ---------------------------------------------------------------------------------------------------------------
+// 16 -> 32 stride-2 layer on the same scheme.  A TMEM lane holds the PAIR of input pixels (2 ox, 2 ox + 1) of its
+// output pixel ox: 32 floats, split and written exactly like a 32-channel pixel (part p: even pixel at columns
+// 16 p, odd pixel at 16 p + 8).  Taps kx = 1 / 2 read the even / odd columns; tap kx = 0 needs the odd pixel of
+// output ox - 1, so the lanes of a quarter hold DESCENDING ox (lane j: ox = 31 seg + 30 - j) and one shift of the
+// odd columns brings it in (lane 31 goes stale: 31 output pixels per quarter, 64 input pixels per raw segment).
+// Rows: input row 2 oy - 1 + i of a band: even i closes output row i / 2 - 1 (ky 2) and opens i / 2 (ky 0), odd i
+// adds ky 1 to output row (i - 1) / 2.  TMEM: four 96-column accumulators, two 48-column A slots.  The two
+// epilogue groups take the two 16-channel halves of every output row.
+constexpr int SEG2 = 31;
+struct S2 {
+  static constexpr int CIN = 16, COUT = 32, KC = 2, NW = 3 * COUT;
+  static constexpr uint32_t WT = KC * NW;
+  static constexpr int W_BYTES = 9 * KC * NW * 16;
+  static constexpr int QBYTES = 64 * CIN * 4;          // raw bytes of one lane quarter's 64 input pixels
+  static constexpr int RAW_BYTES = 4 * QBYTES;
+  static constexpr int NR = 8, NACC = 4, ACOLS = 3 * COUT, AOFF = NACC * ACOLS, SLOT_COLS = 48;
+  static constexpr int NSA = (512 - AOFF) / SLOT_COLS;
+  static constexpr size_t SMEM = W_BYTES + (size_t)NR * RAW_BYTES + 8 * (2 * NR + 2 * NSA + 2 * NACC) + 16 + 4 * COUT;
+  static_assert(SMEM <= 232448, "shared memory budget");
+};
+
+// the tcgen05 work of one input row: target X (accumulator dx, weight taps of its ky at wx, all accumulating)
+// and target Y (dy, wy; its first MMA overwrites); valid bit 0 / 1 enables X / Y
+HS_DEV void s2_row_mmas(uint32_t dx, uint32_t dy, uint32_t abase, uint32_t wx, uint32_t wy, uint32_t valid) {
+  constexpr uint32_t I0 = idesc_bf16(128, 96), I1 = idesc_bf16(128, 64), I2 = idesc_bf16(128, 32);
+  if (kShProbe & 2) return;
+#define HS_S2_MMA3(D, E, P0, A0, A1, A2)                                            \
+  "@" E " tcgen05.mma.cta_group::1.kind::f16 [" D "], [" A0 "], db, i0, " P0 ";\n\t" \
+  "@" E " tcgen05.mma.cta_group::1.kind::f16 [" D "], [" A1 "], db, i1, pt;\n\t"     \
+  "@" E " tcgen05.mma.cta_group::1.kind::f16 [" D "], [" A2 "], db, i2, pt;\n\t"
+#define HS_S2_TAP(WR, KOFF, D, E, P0, A0, A1, A2) \
+  "add.u32 bl, " WR ", " KOFF ";\n\tmov.b64 db, {bl, hi};\n\t" HS_S2_MMA3(D, E, P0, A0, A1, A2)
+  asm volatile(
+      "{\n\t.reg .pred e, ex, ey, pz, pt;\n\t.reg .b64 db;\n\t.reg .b32 hi, i0, i1, i2, e1, e2, o0, o1, o2, bl, m;\n\t"
+      "mov.b32 hi, %6;\n\tmov.b32 i0, %7;\n\tmov.b32 i1, %8;\n\tmov.b32 i2, %9;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "and.b32 m, %5, 1;\n\tsetp.ne.b32 ex, m, 0;\n\tand.pred ex, ex, e;\n\t"
+      "and.b32 m, %5, 2;\n\tsetp.ne.b32 ey, m, 0;\n\tand.pred ey, ey, e;\n\t"
+      "setp.ne.b32 pz, %5, %5;\n\tsetp.eq.b32 pt, %5, %5;\n\t"
+      "add.u32 e1, %2, 16;\n\tadd.u32 e2, %2, 32;\n\tadd.u32 o0, %2, 8;\n\tadd.u32 o1, %2, 24;\n\tadd.u32 o2, %2, 40;\n\t"
+      HS_S2_TAP("%3", "%10", "%0", "ex", "pt", "%2", "e1", "e2") HS_S2_TAP("%4", "%10", "%1", "ey", "pz", "%2", "e1", "e2")
+      HS_S2_TAP("%3", "%11", "%0", "ex", "pt", "o0", "o1", "o2") HS_S2_TAP("%4", "%11", "%1", "ey", "pt", "o0", "o1", "o2")
+      "@e tcgen05.shift.cta_group::1.down [o0];\n\t@e tcgen05.shift.cta_group::1.down [o1];\n\t"
+      "@e tcgen05.shift.cta_group::1.down [o2];\n\t"
+      HS_S2_TAP("%3", "0", "%0", "ex", "pt", "o0", "o1", "o2") HS_S2_TAP("%4", "0", "%1", "ey", "pt", "o0", "o1", "o2")
+      "}\n" ::"r"(dx), "r"(dy), "r"(abase), "r"(wx), "r"(wy), "r"(valid), "n"(kDescHi), "n"(I0), "n"(I1), "n"(I2),
+      "n"(1 * S2::WT), "n"(2 * S2::WT)
+      : "memory");
+#undef HS_S2_MMA3
+#undef HS_S2_TAP
+}
+
+__global__ void __launch_bounds__(NT, 1) k_conv_shift_s2(ShArgs a) {
+  using F = S2;
+  constexpr int C = F::CIN, CO = F::COUT, KC = F::KC, NW = F::NW, NR = F::NR, NACC = F::NACC, NSA = F::NSA,
+                ACOLS = F::ACOLS;
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* wst = smem;
+  unsigned char* raw = smem + F::W_BYTES;
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(raw + (size_t)NR * F::RAW_BYTES);
+  uint64_t* raw_empty = raw_full + NR;
+  uint64_t* a_full = raw_empty + NR;
+  uint64_t* a_empty = a_full + NSA;
+  uint64_t* acc_full = a_empty + NSA;
+  uint64_t* acc_empty = acc_full + NACC;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(acc_empty + NACC);
+  float* s_bias = reinterpret_cast<float*>(s_tmem + 4);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long nunits = (long long)a.B * a.ntile * a.ngroups;
+
+  for (int e = tid; e < 9 * KC * CO; e += NT) {  // resident weight stack, layout (tap, chunk, row) x 16 B
+    const int n = e % CO, c = (e / CO) % KC, t = e / (CO * KC);
+    const float* src = a.w + ((size_t)n * 9 + t) * C + 8 * c;
+    const float4 v0 = __ldg(reinterpret_cast<const float4*>(src)), v1 = __ldg(reinterpret_cast<const float4*>(src + 4));
+    const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    uint4 p[3];
+    split_bf16x3(v, p[0], p[1], p[2]);
+#pragma unroll
+    for (int part = 0; part < 3; ++part)
+      *reinterpret_cast<uint4*>(wst + ((size_t)(t * KC + c) * NW + part * CO + n) * 16) = p[part];
   }
+  if (tid < CO) s_bias[tid] = a.bias[tid];
+  if (tid == 0) {
+    for (int i = 0; i < NR; ++i) {
+      mbar_init(smem_u32(&raw_full[i]), 1);
+      mbar_init(smem_u32(&raw_empty[i]), 4);
+    }
+    for (int i = 0; i < NSA; ++i) {
+      mbar_init(smem_u32(&a_full[i]), 4);
+      mbar_init(smem_u32(&a_empty[i]), 1);
+    }
+    for (int i = 0; i < NACC; ++i) {
+      mbar_init(smem_u32(&acc_full[i]), 1);
+      mbar_init(smem_u32(&acc_empty[i]), 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *s_tmem;
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  if (warp == kProd) {
+    if (lane == 0) {
+      uint32_t seq = 0;
+      for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
+        Unit U;
+        if (!unit_at(a, u, U)) continue;
+        const float* img = a.x + (size_t)U.b * a.H * a.W * C;
+        int qy0[4], qx0[4];
+        bool qv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          int seg;
+          qv[q] = quarter_at(a, U, q, qy0[q], seg);
+          qx0[q] = 2 * SEG2 * seg - 2;  // first input pixel of the quarter's raw segment
+        }
+        for (int i = 0; i <= 2 * U.bh; ++i, ++seq) {
+          const uint32_t s = seq % NR, use = seq / NR;
+          if (use > 0) mbar_wait(smem_u32(&raw_empty[s]), (use - 1) & 1);
+          const uint32_t bar = smem_u32(&raw_full[s]);
+          uint32_t total = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int g = 2 * qy0[q] - 1 + i, clo = max(qx0[q], 0), chi = min(qx0[q] + 64, a.W);
+            if (qv[q] && g >= 0 && g < a.H && chi > clo) total += (uint32_t)(chi - clo) * C * 4;
+          }
+          if (total) {
+            mbar_arrive_tx(bar, total);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int g = 2 * qy0[q] - 1 + i, clo = max(qx0[q], 0), chi = min(qx0[q] + 64, a.W);
+              if (qv[q] && g >= 0 && g < a.H && chi > clo)
+                bulk_g2s(smem_u32(raw + (size_t)s * F::RAW_BYTES + (size_t)q * F::QBYTES + (size_t)(clo - qx0[q]) * C * 4),
+                         img + ((size_t)g * a.W + clo) * C, (uint32_t)(chi - clo) * C * 4, bar);
+            }
+          } else {
+            mbar_arrive(bar);
+          }
+        }
+      }
+    }
+  } else if (warp >= kCvt0 && warp < kCvt0 + 4) {
+    const int q = warp - kCvt0;
+    uint32_t seq = 0;
+    for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
+      Unit U;
+      if (!unit_at(a, u, U)) continue;
+      int qy0, seg;
+      const bool qv = quarter_at(a, U, q, qy0, seg);
+      const int xe = 2 * (SEG2 * seg + 30 - lane);  // even input pixel of this lane's pair
+      const bool oke = qv && xe >= 0 && xe < a.W, oko = qv && xe + 1 >= 0 && xe + 1 < a.W;
+      for (int i = 0; i <= 2 * U.bh; ++i, ++seq) {
+        const int g = 2 * qy0 - 1 + i;
+        const uint32_t s = seq % NR;
+        mbar_wait(smem_u32(&raw_full[s]), (seq / NR) & 1);
+        float4 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if ((oke || oko) && g >= 0 && g < a.H) {
+          const float4* src = reinterpret_cast<const float4*>(raw + (size_t)s * F::RAW_BYTES + (size_t)q * F::QBYTES +
+                                                              (size_t)(31 - lane) * 128);
+          const int r = lane & 7;  // rotated piece order: eight bank groups per quarter-warp wavefront
+          float4 w4[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) w4[k] = src[(k + r) & 7];
+#pragma unroll
+          for (int st = 1; st < 8; st <<= 1) {
+            float4 t4[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) t4[k] = (r & st) ? w4[(k + 8 - st) & 7] : w4[k];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) w4[k] = t4[k];
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (k < 4 ? oke : oko) v[k] = w4[k];
+        }
+        uint4 pw[3][4] = {};
+        if (!(kShProbe & 4)) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float f[8] = {v[2 * c].x, v[2 * c].y, v[2 * c].z, v[2 * c].w,
+                                v[2 * c + 1].x, v[2 * c + 1].y, v[2 * c + 1].z, v[2 * c + 1].w};
+            split_bf16x3(f, pw[0][c], pw[1][c], pw[2][c]);
+          }
+        }
+        const uint32_t as = seq % NSA, ause = seq / NSA;
+        if (ause > 0) mbar_wait(smem_u32(&a_empty[as]), (ause - 1) & 1);
+        tc_fence_after();
+        const uint32_t tcol = tmem + ((uint32_t)(32 * q) << 16) + F::AOFF + as * F::SLOT_COLS;
+        if (!(kShProbe & 4)) {
+#pragma unroll
+          for (int part = 0; part < 3; ++part) {
+            tmem_st8(tcol + 16 * part, pw[part][0], pw[part][1]);      // even pixel
+            tmem_st8(tcol + 16 * part + 8, pw[part][2], pw[part][3]);  // odd pixel
+          }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&a_full[as]));
+        fence_async_smem();  // the raw slot is released after the row is in TMEM (see k_conv_shift)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&raw_empty[s]));
+      }
+    }
+  } else if (warp == kMma) {
+    const uint32_t wlo = desc_lo(smem_u32(wst), NW * 16);
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    uint32_t as = 0, a_par = 0, s_next = 0, epoch = 0;
+    for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
+      Unit U;
+      if (!unit_at(a, u, U)) continue;
+      uint32_t s_new = 0, s_old = 0;  // accumulator of the newest open output row and of the one before it
+      for (int i = 0; i <= 2 * U.bh; ++i) {
+        mbar_wait(smem_u32(&a_full[as]), a_par);
+        const uint32_t abase = tm + F::AOFF + as * F::SLOT_COLS;
+        if ((i & 1) == 0) {
+          // input row 2 r - 1 (r = i / 2): ky 2 of output row r - 1 (closes it), ky 0 of output row r (opens it)
+          const bool v_old = i > 0, v_new = i < 2 * U.bh;
+          s_old = s_new;
+          if (v_new) {
+            s_new = s_next;
+            if (epoch > 0) mbar_wait(smem_u32(&acc_empty[s_new]), (epoch - 1) & 1);
+            if (++s_next == (uint32_t)NACC) {
+              s_next = 0;
+              ++epoch;
+            }
+          }
+          tc_fence_after();
+          s2_row_mmas(tm + s_old * ACOLS, tm + s_new * ACOLS, abase, wlo + 6 * F::WT, wlo,
+                      (v_old ? 1u : 0u) | (v_new ? 2u : 0u));
+          mma_commit(smem_u32(&a_empty[as]));
+          if (v_old) mma_commit(smem_u32(&acc_full[s_old]));
+        } else {
+          // input row 2 r: ky 1 of output row r = (i - 1) / 2
+          tc_fence_after();
+          s2_row_mmas(tm + s_new * ACOLS, tm + s_new * ACOLS, abase, wlo + 3 * F::WT, wlo, 1u);
+          mma_commit(smem_u32(&a_empty[as]));
+        }
+        if (++as == (uint32_t)NSA) {
+          as = 0;
+          a_par ^= 1;
+        }
+      }
+    }
+  } else {
+    // epilogue: warp q4 drains its lane quarter; group hg takes channels 16 hg .. 16 hg + 15 of every output row
+    const int q4 = warp & 3, hg = warp >> 2;
+    const int gi = lane & 3, gb = lane & ~3;
+    const int ch0 = 16 * hg;
+    uint32_t tile = 0;
+    for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
+      Unit U;
+      if (!unit_at(a, u, U)) continue;
+      const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[U.b] : 0) : U.b) *
+                                                   a.addend_bstride
+                                  : nullptr;
+      const float* res = a.residual ? a.residual + (size_t)U.b * a.Ho * a.Wo * CO : nullptr;
+      float* yimg = a.y + (size_t)U.b * a.Ho * a.Wo * CO;
+      int qy0, seg;
+      const bool qv = quarter_at(a, U, q4, qy0, seg);
+      const int xg0 = SEG2 * seg + 30 - gb;  // output pixel of this lane group's first lane; the group's pixel j is xg0 - j
+      const int oy_end = qy0 + U.bh;
+      bool ok[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) ok[j] = qv && gb + j < SEG2 && xg0 - j >= 0 && xg0 - j < a.Wo;
+      float4 sa[4], sr[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) sa[j] = sr[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      auto issue_side = [&](int oy) {
+        const long long gp = ((long long)oy * a.Wo + xg0) * CO + ch0;
+        if (add) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (ok[j]) sa[j] = __ldg(reinterpret_cast<const float4*>(add + gp - (long long)j * CO) + gi);
+        }
+        if (res) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (ok[j]) sr[j] = __ldg(reinterpret_cast<const float4*>(res + gp - (long long)j * CO) + gi);
+        }
+      };
+      if (qy0 < oy_end) issue_side(qy0);
+      for (int oy = qy0; oy < oy_end; ++oy, ++tile) {
+        const uint32_t acc = tile % NACC;
+        const long long gpix = ((long long)oy * a.Wo + xg0) * CO + ch0;
+        mbar_wait(smem_u32(&acc_full[acc]), (tile / NACC) & 1);
+        tc_fence_after();
+        float o[16] = {};
+#pragma unroll
+        for (int n0 = 0; n0 < 16; n0 += 8) {
+          uint32_t r0[8], r1[8], r2[8];
+          const uint32_t col = tmem + ((uint32_t)(q4 * 32) << 16) + acc * ACOLS + ch0 + n0;
+          tmem_ld8(col, r0);
+          tmem_ld8(col + CO, r1);
+          tmem_ld8(col + 2 * CO, r2);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 8; j += 2) {
+            const uint64_t sm = add2(add2(pk2(r0[j], r0[j + 1]), pk2(r1[j], r1[j + 1])), pk2(r2[j], r2[j + 1]));
+            o[n0 + j] = __uint_as_float((uint32_t)sm);
+            o[n0 + j + 1] = __uint_as_float((uint32_t)(sm >> 32));
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&acc_empty[acc]));
+        float4 ch[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 bs = *reinterpret_cast<const float4*>(s_bias + ch0 + 4 * q);
+          const uint64_t o01 = add2(pkf(o[4 * q], o[4 * q + 1]), pkf(bs.x, bs.y));
+          const uint64_t o23 = add2(pkf(o[4 * q + 2], o[4 * q + 3]), pkf(bs.z, bs.w));
+          float4 v = make_float4(lo_f(o01), hi_f(o01), lo_f(o23), hi_f(o23));
+          if (a.softplus) {
+            v.x = softplus_fast(v.x);
+            v.y = softplus_fast(v.y);
+            v.z = softplus_fast(v.z);
+            v.w = softplus_fast(v.w);
+          }
+          ch[q] = v;
+        }
+        group4_transpose(ch, gi);  // lane gi: chunk gi of the group's four pixels (pixel j at xg0 - j)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint64_t s01 = add2(pkf(sa[j].x, sa[j].y), pkf(sr[j].x, sr[j].y));
+          const uint64_t s23 = add2(pkf(sa[j].z, sa[j].w), pkf(sr[j].z, sr[j].w));
+          const uint64_t q01 = add2(pkf(ch[j].x, ch[j].y), s01), q23 = add2(pkf(ch[j].z, ch[j].w), s23);
+          if (ok[j])
+            reinterpret_cast<float4*>(yimg + gpix - (long long)j * CO)[gi] = make_float4(lo_f(q01), hi_f(q01), lo_f(q23), hi_f(q23));
+        }
+        if (oy + 1 < oy_end) issue_side(oy + 1);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// band height and band groups for a layer with Ho output rows of nseg segments (both kernels)
+void plan_units(ShArgs& a, int Ho, int nseg, int sms, long long& grid) {
   a.band = HS_SH_BAND_MAX;
-  a.nseg = (a.W + SEG - 1) / SEG;
+  a.nseg = nseg;
   // band height as conv_tc.cu: halve it until the RHS still iterating give every CTA >= 6 units
   const double act = prof::active_hint(a.B);
-  long long grid = sms;
-  while (a.band > 8 && act * ((a.nseg + 3) / 4) * ((a.H + a.band - 1) / a.band) < 6.0 * grid) a.band /= 2;
-  const int nbands = (a.H + a.band - 1) / a.band;
+  grid = sms;
+  while (a.band > 8 && act * ((a.nseg + 3) / 4) * ((Ho + a.band - 1) / a.band) < 6.0 * grid) a.band /= 2;
+  const int nbands = (Ho + a.band - 1) / a.band;
   // bands per unit group: the smallest of 1, 2, 4 that leaves the fewest empty lane quarters
   a.nb = 1;
-  if (a.H % a.band == 0) {
+  if (Ho % a.band == 0) {
     double best = (double)a.nseg / (4 * ((a.nseg + 3) / 4));
     for (int nb = 2; nb <= 4; nb *= 2) {
       if (nbands % nb) break;
@@ -602,17 +948,36 @@ bool launch_shift(ShArgs a, cudaStream_t st) {
   a.ngroups = nbands / a.nb;
   const long long nunits = (long long)a.B * a.ntile * a.ngroups;
   if (nunits < grid) grid = nunits;
+}
+
+template <typename K>
+bool launch_pdl(K kernel, const ShArgs& a, long long grid, size_t smem_bytes, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(NT);
-  cfg.dynamicSmemBytes = F::SMEM;
+  cfg.dynamicSmemBytes = smem_bytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_conv_shift<C>, a) == cudaSuccess;
+  return cudaLaunchKernelEx(&cfg, kernel, a) == cudaSuccess;
+}
+
+template <int C>
+bool launch_shift(ShArgs a, cudaStream_t st) {
+  using F = Cfg<C>;
+  static int sms = 0;
+  if (!sms) {
+    cudaFuncSetAttribute(k_conv_shift<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F::SMEM);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  long long grid;
+  plan_units(a, a.H, (a.W + SEG - 1) / SEG, sms, grid);
+  return launch_pdl(k_conv_shift<C>, a, grid, F::SMEM, st);
 }
 
 }  // namespace
@@ -622,10 +987,28 @@ bool conv_shift_launch(int channels, const float* x, int H, int W, float* y, con
                        const int* model_of, const float* residual, const void* const* active, int B,
                        cudaStream_t st) {
   ShArgs a{x, H, W, y, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual, active, B,
-           0, 0, 0, 0, 0};
+           H, W, 0, 0, 0, 0, 0};
   if (channels == 16) return launch_shift<16>(a, st);
   if (channels == 32) return launch_shift<32>(a, st);
   return false;
+}
+
+bool conv_shift_s2_launch(const float* x, int H, int W, float* y, int Ho, int Wo, const float* w, const float* bias,
+                          int softplus, const float* addend, long long addend_bstride, int addend_per_model,
+                          const int* model_of, const float* residual, const void* const* active, int B,
+                          cudaStream_t st) {
+  static int sms = 0;
+  if (!sms) {
+    cudaFuncSetAttribute(k_conv_shift_s2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S2::SMEM);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  ShArgs a{x, H, W, y, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual, active, B,
+           Ho, Wo, 0, 0, 0, 0, 0};
+  long long grid;
+  plan_units(a, Ho, (Wo + SEG2 - 1) / SEG2, sms, grid);
+  return launch_pdl(k_conv_shift_s2, a, grid, S2::SMEM, st);
 }
 
 }  // namespace hs

@@ -79,6 +79,9 @@ def test_tconv_shapes(rng, cin, cout, hw):
                                                (16, 16, 0, (3, 121)), (16, 16, 0, (40, 250)),
                                                (32, 32, 0, (7, 100)), (32, 32, 0, (1, 33)), (32, 32, 0, (35, 150)),
                                                (32, 32, 0, (9, 256)),
+                                               # stride-2 tcgen05.shift kernel: odd and even sizes, partial segments
+                                               (16, 32, 1, (7, 100)), (16, 32, 1, (1, 33)), (16, 32, 1, (34, 63)),
+                                               (16, 32, 1, (9, 129)), (16, 32, 1, (66, 250)),
                                                (32, 32, 0, (4, 128)),
                                                (16, 32, 1, (6, 256)), (32, 16, 2, (3, 128)), (32, 16, 2, (2, 256)),
                                                # M = 64 tiles (64-wide levels) and cout split across CTAs
