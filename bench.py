@@ -730,7 +730,7 @@ def roofline(breakdown, learned, hbm, bf16_sus, src):
         name = "vc_up_l0"
     row = breakdown.get(name, {})
     ach = row.get("achieved", 0.0)
-    l0 = hbm_row("convs_l0_16ch", "k_conv16_shift (tcgen05 BF16x3 3x3 conv, A in TMEM + tcgen05.shift, level 0 16->16)")
+    l0 = hbm_row("convs_l0_16ch", "k_conv_shift<16> (tcgen05 BF16x3 3x3 conv, A in TMEM + tcgen05.shift, level 0 16->16)")
     l0.update(traffic=traffic.get("dram_bytes_per_launch"), traffic_note=traffic.get("note"))
     wide_peak = bf16_sus / 6.0
     wrow = breakdown.get("convs_wide", {})

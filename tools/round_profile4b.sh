@@ -6,8 +6,9 @@ cap() {  # name, kernel regex, skip, command...
     -o gpurun_out/$name -f "$@" > gpurun_out/$name.log 2>&1
   tail -2 gpurun_out/$name.log
 }
-cap r2g_shift16 'k_conv_shift<16>' 4 python tools/step_probe.py --iters 6
-cap r2g_shift32 'k_conv_shift<32>' 4 python tools/step_probe.py --iters 6
-cap r2g_wide6464 'k_conv_wide<64, 64' 4 python tools/step_probe.py --iters 6
-cap r2g_shift16_resid 'k_conv_shift<16>' 5 python tools/conv_probe.py --B 64 --H 512 --W 1024 --side residual --softplus 0 --iters 3
+cap r2g_shift16 'k_conv_shift<.int.16>' 4 python tools/step_probe.py --iters 6
+cap r2g_shift32 'k_conv_shift<.int.32>' 4 python tools/step_probe.py --iters 6
+cap r2g_wide6464 'k_conv_wide<.int.64, .int.64' 4 python tools/step_probe.py --iters 6
+cap r2g_shift_s2 'k_conv_shift_s2' 2 python tools/step_probe.py --iters 6
+cap r2g_shift16_resid 'k_conv_shift<.int.16>' 5 python tools/conv_probe.py --B 64 --H 512 --W 1024 --side residual --softplus 0 --iters 3
 ls -la gpurun_out | grep r2g
