@@ -101,7 +101,8 @@ struct ShArgs {
   const float* residual;
   const void* const* active;
   int B;
-  int Ho, Wo;  // output size (the stride-2 kernel; stride 1: H, W)
+  int Ho, Wo;  // output size (stride 1: H, W)
+  int rows;    // the banded dimension: output rows, or input rows for the transposed kernel
   // Work units.  A row of the image is nseg segments of 30 output pixels; a unit is one tile (four segments, one per
   // lane quarter) of a group of nb bands of one image, the group's nb * nseg segments taken in order.  The four
   // quarters of a tile may therefore sit in different bands; they walk their bands' rows in lockstep.  nb is
@@ -117,7 +118,7 @@ HS_DEV bool unit_at(const ShArgs& a, long long u, Unit& U) {
   U.t = (int)(u % a.ntile);
   U.grp = (int)((u / a.ntile) % a.ngroups);
   U.b = (int)(u / ((long long)a.ntile * a.ngroups));
-  U.bh = min(a.Ho - U.grp * a.nb * a.band, a.band);  // output rows; nb > 1 only when the band height divides Ho
+  U.bh = min(a.rows - U.grp * a.nb * a.band, a.band);  // nb > 1 only when the band height divides the row count
   return !(a.active && a.active[U.b] == nullptr);
 }
 
@@ -922,6 +923,362 @@ __global__ void __launch_bounds__(NT, 1) k_conv_shift_s2(ShArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------------------------------------------
+// 32 -> 16 transposed (stride-2) layer on the same scheme.  Lanes hold INPUT pixels p (ascending, 31 valid per
+// quarter); output (2 q + a, 2 p + b) takes, as conv_tc.cu's transposed tiles,
+//   rows:  a = 0: (ky 1, input row q);  a = 1: (ky 0, row q + 1), (ky 2, row q)
+//   cols:  b = 0: (kx 1, pixel p);      b = 1: (kx 0, pixel p + 1), (kx 2, pixel p)
+// so input row r feeds output rows 2 r - 1 (ky 0, closes it), 2 r (ky 1, opens and closes it) and 2 r + 1 (ky 2,
+// opens it), each with two column-parity accumulators of 48 columns (96 per output row); the taps kx 1 and kx 2
+// read the row as written, kx 0 after one shift.  Bands run over input rows; a band reads one input row past its
+// end (ky 0 of its last odd output row).  TMEM: four 96-column accumulators, two 48-column A slots.  The two
+// epilogue groups take the even and the odd output columns of every output row: a lane's 16 channels are one
+// 64-byte pixel, and the group-of-four transpose makes every store write whole pixels.
+struct ST {
+  static constexpr int CIN = 32, COUT = 16, KC = 4, NW = 3 * COUT;
+  static constexpr uint32_t WT = KC * NW, KK = 2 * NW;
+  static constexpr int W_BYTES = 9 * KC * NW * 16;
+  static constexpr int QBYTES = 32 * CIN * 4;          // raw bytes of one lane quarter's 32 input pixels
+  static constexpr int RAW_BYTES = 4 * QBYTES;
+  static constexpr int NR = 8, NACC = 4, ACOLS = 6 * COUT, AOFF = NACC * ACOLS, SLOT_COLS = 48;
+  static constexpr int NSA = (512 - AOFF) / SLOT_COLS;
+  static constexpr size_t SMEM = W_BYTES + (size_t)NR * RAW_BYTES + 8 * (2 * NR + 2 * NSA + 2 * NACC) + 16 + 4 * COUT;
+  static_assert(SMEM <= 232448, "shared memory budget");
+};
+
+// the tcgen05 work of one input row: targets a (output row 2 r - 1, ky 0, accumulating), b (2 r, ky 1) and
+// c (2 r + 1, ky 2), both opened here (their first MMA per column parity overwrites); valid bits 0 / 1 / 2
+HS_DEV void t_row_mmas(uint32_t da, uint32_t db_, uint32_t dc, uint32_t abase, uint32_t wlo, uint32_t valid) {
+  constexpr uint32_t I0 = idesc_bf16(128, 48), I1 = idesc_bf16(128, 32), I2 = idesc_bf16(128, 16);
+  if (kShProbe & 2) return;
+#define HS_T_MMA3(D, E, P0, A0, A1, A2)                                             \
+  "@" E " tcgen05.mma.cta_group::1.kind::f16 [" D "], [" A0 "], db, i0, " P0 ";\n\t" \
+  "@" E " tcgen05.mma.cta_group::1.kind::f16 [" D "], [" A1 "], db, i1, pt;\n\t"     \
+  "@" E " tcgen05.mma.cta_group::1.kind::f16 [" D "], [" A2 "], db, i2, pt;\n\t"
+#define HS_T_TAP(WOFF, D, E, P0)                                                                          \
+  "add.u32 bl, %4, " WOFF ";\n\tmov.b64 db, {bl, hi};\n\t" HS_T_MMA3(D, E, P0, "%3", "a10", "a20")        \
+  "add.u32 bl, bl, %19;\n\tmov.b64 db, {bl, hi};\n\t" HS_T_MMA3(D, E, "pt", "a01", "a11", "a21")
+  asm volatile(
+      "{\n\t.reg .pred e, ea, eb, ec, pz, pt;\n\t.reg .b64 db;\n\t"
+      ".reg .b32 hi, i0, i1, i2, a01, a10, a11, a20, a21, da1, db1, dc1, bl, m;\n\t"
+      "mov.b32 hi, %6;\n\tmov.b32 i0, %7;\n\tmov.b32 i1, %8;\n\tmov.b32 i2, %9;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "and.b32 m, %5, 1;\n\tsetp.ne.b32 ea, m, 0;\n\tand.pred ea, ea, e;\n\t"
+      "and.b32 m, %5, 2;\n\tsetp.ne.b32 eb, m, 0;\n\tand.pred eb, eb, e;\n\t"
+      "and.b32 m, %5, 4;\n\tsetp.ne.b32 ec, m, 0;\n\tand.pred ec, ec, e;\n\t"
+      "setp.ne.b32 pz, %5, %5;\n\tsetp.eq.b32 pt, %5, %5;\n\t"
+      "add.u32 a01, %3, 8;\n\tadd.u32 a10, %3, 16;\n\tadd.u32 a11, %3, 24;\n\tadd.u32 a20, %3, 32;\n\tadd.u32 a21, %3, 40;\n\t"
+      "add.u32 da1, %0, 48;\n\tadd.u32 db1, %1, 48;\n\tadd.u32 dc1, %2, 48;\n\t"
+      // row as written: kx 1 -> even output columns, kx 2 -> odd output columns
+      HS_T_TAP("%11", "%0", "ea", "pt") HS_T_TAP("%14", "%1", "eb", "pz") HS_T_TAP("%17", "%2", "ec", "pz")
+      HS_T_TAP("%12", "da1", "ea", "pt") HS_T_TAP("%15", "db1", "eb", "pz") HS_T_TAP("%18", "dc1", "ec", "pz")
+      "@e tcgen05.shift.cta_group::1.down [%3];\n\t@e tcgen05.shift.cta_group::1.down [a01];\n\t"
+      "@e tcgen05.shift.cta_group::1.down [a10];\n\t@e tcgen05.shift.cta_group::1.down [a11];\n\t"
+      "@e tcgen05.shift.cta_group::1.down [a20];\n\t@e tcgen05.shift.cta_group::1.down [a21];\n\t"
+      // shifted row (pixel p + 1): kx 0 -> odd output columns
+      HS_T_TAP("%10", "da1", "ea", "pt") HS_T_TAP("%13", "db1", "eb", "pt") HS_T_TAP("%16", "dc1", "ec", "pt")
+      "}\n" ::"r"(da), "r"(db_), "r"(dc), "r"(abase), "r"(wlo), "r"(valid), "n"(kDescHi), "n"(I0), "n"(I1), "n"(I2),
+      "n"(0 * ST::WT), "n"(1 * ST::WT), "n"(2 * ST::WT), "n"(3 * ST::WT), "n"(4 * ST::WT), "n"(5 * ST::WT),
+      "n"(6 * ST::WT), "n"(7 * ST::WT), "n"(8 * ST::WT), "n"(ST::KK)
+      : "memory");
+#undef HS_T_MMA3
+#undef HS_T_TAP
+}
+
+__global__ void __launch_bounds__(NT, 1) k_conv_shift_t(ShArgs a) {
+  using F = ST;
+  constexpr int C = F::CIN, CO = F::COUT, KC = F::KC, NW = F::NW, NR = F::NR, NACC = F::NACC, NSA = F::NSA,
+                ACOLS = F::ACOLS;
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* wst = smem;
+  unsigned char* raw = smem + F::W_BYTES;
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(raw + (size_t)NR * F::RAW_BYTES);
+  uint64_t* raw_empty = raw_full + NR;
+  uint64_t* a_full = raw_empty + NR;
+  uint64_t* a_empty = a_full + NSA;
+  uint64_t* acc_full = a_empty + NSA;
+  uint64_t* acc_empty = acc_full + NACC;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(acc_empty + NACC);
+  float* s_bias = reinterpret_cast<float*>(s_tmem + 4);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long nunits = (long long)a.B * a.ntile * a.ngroups;
+
+  for (int e = tid; e < 9 * KC * CO; e += NT) {  // resident weight stack, layout (tap, chunk, row) x 16 B
+    const int n = e % CO, c = (e / CO) % KC, t = e / (CO * KC);
+    const float* src = a.w + ((size_t)n * 9 + t) * C + 8 * c;
+    const float4 v0 = __ldg(reinterpret_cast<const float4*>(src)), v1 = __ldg(reinterpret_cast<const float4*>(src + 4));
+    const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    uint4 p[3];
+    split_bf16x3(v, p[0], p[1], p[2]);
+#pragma unroll
+    for (int part = 0; part < 3; ++part)
+      *reinterpret_cast<uint4*>(wst + ((size_t)(t * KC + c) * NW + part * CO + n) * 16) = p[part];
+  }
+  if (tid < CO) s_bias[tid] = a.bias[tid];
+  if (tid == 0) {
+    for (int i = 0; i < NR; ++i) {
+      mbar_init(smem_u32(&raw_full[i]), 1);
+      mbar_init(smem_u32(&raw_empty[i]), 4);
+    }
+    for (int i = 0; i < NSA; ++i) {
+      mbar_init(smem_u32(&a_full[i]), 4);
+      mbar_init(smem_u32(&a_empty[i]), 1);
+    }
+    for (int i = 0; i < NACC; ++i) {
+      mbar_init(smem_u32(&acc_full[i]), 1);
+      mbar_init(smem_u32(&acc_empty[i]), 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *s_tmem;
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  if (warp == kProd) {
+    if (lane == 0) {
+      uint32_t seq = 0;
+      for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
+        Unit U;
+        if (!unit_at(a, u, U)) continue;
+        const float* img = a.x + (size_t)U.b * a.H * a.W * C;
+        int qy0[4], qx0[4];
+        bool qv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          int seg;
+          qv[q] = quarter_at(a, U, q, qy0[q], seg);
+          qx0[q] = SEG2 * seg;  // first input pixel of the quarter
+        }
+        for (int i = 0; i <= U.bh; ++i, ++seq) {
+          const uint32_t s = seq % NR, use = seq / NR;
+          if (use > 0) mbar_wait(smem_u32(&raw_empty[s]), (use - 1) & 1);
+          const uint32_t bar = smem_u32(&raw_full[s]);
+          uint32_t total = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int g = qy0[q] + i, chi = min(qx0[q] + 32, a.W);
+            if (qv[q] && g < a.H && chi > qx0[q]) total += (uint32_t)(chi - qx0[q]) * C * 4;
+          }
+          if (total) {
+            mbar_arrive_tx(bar, total);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int g = qy0[q] + i, chi = min(qx0[q] + 32, a.W);
+              if (qv[q] && g < a.H && chi > qx0[q])
+                bulk_g2s(smem_u32(raw + (size_t)s * F::RAW_BYTES + (size_t)q * F::QBYTES),
+                         img + ((size_t)g * a.W + qx0[q]) * C, (uint32_t)(chi - qx0[q]) * C * 4, bar);
+            }
+          } else {
+            mbar_arrive(bar);
+          }
+        }
+      }
+    }
+  } else if (warp >= kCvt0 && warp < kCvt0 + 4) {
+    const int q = warp - kCvt0;
+    uint32_t seq = 0;
+    for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
+      Unit U;
+      if (!unit_at(a, u, U)) continue;
+      int qy0, seg;
+      const bool qv = quarter_at(a, U, q, qy0, seg);
+      const bool xok = qv && SEG2 * seg + lane < a.W;
+      for (int i = 0; i <= U.bh; ++i, ++seq) {
+        const int g = qy0 + i;
+        const uint32_t s = seq % NR;
+        mbar_wait(smem_u32(&raw_full[s]), (seq / NR) & 1);
+        float4 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (xok && g < a.H) {
+          const float4* src = reinterpret_cast<const float4*>(raw + (size_t)s * F::RAW_BYTES + (size_t)q * F::QBYTES +
+                                                              (size_t)lane * 128);
+          const int r = lane & 7;  // rotated piece order: eight bank groups per quarter-warp wavefront
+          float4 w4[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) w4[k] = src[(k + r) & 7];
+#pragma unroll
+          for (int st = 1; st < 8; st <<= 1) {
+            float4 t4[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) t4[k] = (r & st) ? w4[(k + 8 - st) & 7] : w4[k];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) w4[k] = t4[k];
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] = w4[k];
+        }
+        uint4 pw[3][4] = {};
+        if (!(kShProbe & 4)) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float f[8] = {v[2 * c].x, v[2 * c].y, v[2 * c].z, v[2 * c].w,
+                                v[2 * c + 1].x, v[2 * c + 1].y, v[2 * c + 1].z, v[2 * c + 1].w};
+            split_bf16x3(f, pw[0][c], pw[1][c], pw[2][c]);
+          }
+        }
+        const uint32_t as = seq % NSA, ause = seq / NSA;
+        if (ause > 0) mbar_wait(smem_u32(&a_empty[as]), (ause - 1) & 1);
+        tc_fence_after();
+        const uint32_t tcol = tmem + ((uint32_t)(32 * q) << 16) + F::AOFF + as * F::SLOT_COLS;
+        if (!(kShProbe & 4)) {
+#pragma unroll
+          for (int part = 0; part < 3; ++part) {
+            tmem_st8(tcol + 16 * part, pw[part][0], pw[part][1]);      // channels 0-15 (K step 0)
+            tmem_st8(tcol + 16 * part + 8, pw[part][2], pw[part][3]);  // channels 16-31 (K step 1)
+          }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&a_full[as]));
+        fence_async_smem();  // the raw slot is released after the row is in TMEM (see k_conv_shift)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&raw_empty[s]));
+      }
+    }
+  } else if (warp == kMma) {
+    const uint32_t wlo = desc_lo(smem_u32(wst), NW * 16);
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    uint32_t as = 0, a_par = 0, s_next = 0, epoch = 0;
+    auto open_acc = [&]() {  // next output row's accumulator: its previous user must have drained it
+      const uint32_t sl = s_next;
+      if (epoch > 0) mbar_wait(smem_u32(&acc_empty[sl]), (epoch - 1) & 1);
+      if (++s_next == (uint32_t)NACC) {
+        s_next = 0;
+        ++epoch;
+      }
+      return sl;
+    };
+    for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
+      Unit U;
+      if (!unit_at(a, u, U)) continue;
+      uint32_t s_a = 0, s_b = 0, s_c = 0;
+      for (int i = 0; i <= U.bh; ++i) {
+        mbar_wait(smem_u32(&a_full[as]), a_par);
+        const bool v_a = i > 0, v_bc = i < U.bh;
+        s_a = s_c;  // output row 2 r - 1 was opened as the previous input row's target c
+        if (v_bc) {
+          s_b = open_acc();
+          s_c = open_acc();
+        }
+        tc_fence_after();
+        t_row_mmas(tm + s_a * ACOLS, tm + s_b * ACOLS, tm + s_c * ACOLS, tm + F::AOFF + as * F::SLOT_COLS, wlo,
+                   (v_a ? 1u : 0u) | (v_bc ? 6u : 0u));
+        mma_commit(smem_u32(&a_empty[as]));
+        if (v_a) mma_commit(smem_u32(&acc_full[s_a]));
+        if (v_bc) mma_commit(smem_u32(&acc_full[s_b]));
+        if (++as == (uint32_t)NSA) {
+          as = 0;
+          a_par ^= 1;
+        }
+      }
+    }
+  } else {
+    // epilogue: warp q4 drains its lane quarter; group hg takes the output columns 2 p + hg of every output row
+    const int q4 = warp & 3, hg = warp >> 2;
+    const int gi = lane & 3, gb = lane & ~3;
+    uint32_t tile = 0;
+    for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
+      Unit U;
+      if (!unit_at(a, u, U)) continue;
+      const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[U.b] : 0) : U.b) *
+                                                   a.addend_bstride
+                                  : nullptr;
+      const float* res = a.residual ? a.residual + (size_t)U.b * a.Ho * a.Wo * CO : nullptr;
+      float* yimg = a.y + (size_t)U.b * a.Ho * a.Wo * CO;
+      int qy0, seg;
+      const bool qv = quarter_at(a, U, q4, qy0, seg);
+      const int pg0 = SEG2 * seg + gb;  // input pixel of this lane group's first lane; the group's pixel j is pg0 + j
+      bool ok[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) ok[j] = qv && gb + j < SEG2 && pg0 + j < a.W;
+      const int oy_first = 2 * qy0, oy_end = 2 * (qy0 + U.bh);
+      float4 sa[4], sr[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) sa[j] = sr[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      auto issue_side = [&](int oy) {
+        const size_t gp = ((size_t)oy * a.Wo + 2 * pg0 + hg) * CO;
+        if (add) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (ok[j]) sa[j] = __ldg(reinterpret_cast<const float4*>(add + gp + (size_t)j * 2 * CO) + gi);
+        }
+        if (res) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (ok[j]) sr[j] = __ldg(reinterpret_cast<const float4*>(res + gp + (size_t)j * 2 * CO) + gi);
+        }
+      };
+      if (oy_first < oy_end) issue_side(oy_first);
+      for (int oy = oy_first; oy < oy_end; ++oy, ++tile) {
+        const uint32_t acc = tile % NACC;
+        const size_t gpix = ((size_t)oy * a.Wo + 2 * pg0 + hg) * CO;
+        mbar_wait(smem_u32(&acc_full[acc]), (tile / NACC) & 1);
+        tc_fence_after();
+        float o[16] = {};
+#pragma unroll
+        for (int n0 = 0; n0 < 16; n0 += 8) {
+          uint32_t r0[8], r1[8], r2[8];
+          const uint32_t col = tmem + ((uint32_t)(q4 * 32) << 16) + acc * ACOLS + 48 * hg + n0;
+          tmem_ld8(col, r0);
+          tmem_ld8(col + CO, r1);
+          tmem_ld8(col + 2 * CO, r2);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 8; j += 2) {
+            const uint64_t sm = add2(add2(pk2(r0[j], r0[j + 1]), pk2(r1[j], r1[j + 1])), pk2(r2[j], r2[j + 1]));
+            o[n0 + j] = __uint_as_float((uint32_t)sm);
+            o[n0 + j + 1] = __uint_as_float((uint32_t)(sm >> 32));
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&acc_empty[acc]));
+        float4 ch[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 bs = *reinterpret_cast<const float4*>(s_bias + 4 * q);
+          const uint64_t o01 = add2(pkf(o[4 * q], o[4 * q + 1]), pkf(bs.x, bs.y));
+          const uint64_t o23 = add2(pkf(o[4 * q + 2], o[4 * q + 3]), pkf(bs.z, bs.w));
+          float4 v = make_float4(lo_f(o01), hi_f(o01), lo_f(o23), hi_f(o23));
+          if (a.softplus) {
+            v.x = softplus_fast(v.x);
+            v.y = softplus_fast(v.y);
+            v.z = softplus_fast(v.z);
+            v.w = softplus_fast(v.w);
+          }
+          ch[q] = v;
+        }
+        group4_transpose(ch, gi);  // lane gi: chunk gi of the group's four pixels (output pixel 2 (pg0 + j) + hg)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint64_t s01 = add2(pkf(sa[j].x, sa[j].y), pkf(sr[j].x, sr[j].y));
+          const uint64_t s23 = add2(pkf(sa[j].z, sa[j].w), pkf(sr[j].z, sr[j].w));
+          const uint64_t q01 = add2(pkf(ch[j].x, ch[j].y), s01), q23 = add2(pkf(ch[j].z, ch[j].w), s23);
+          if (ok[j])
+            reinterpret_cast<float4*>(yimg + gpix + (size_t)j * 2 * CO)[gi] = make_float4(lo_f(q01), hi_f(q01), lo_f(q23), hi_f(q23));
+        }
+        if (oy + 1 < oy_end) issue_side(oy + 1);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 // band height and band groups for a layer with Ho output rows of nseg segments (both kernels)
 void plan_units(ShArgs& a, int Ho, int nseg, int sms, long long& grid) {
   a.band = HS_SH_BAND_MAX;
@@ -987,7 +1344,7 @@ bool conv_shift_launch(int channels, const float* x, int H, int W, float* y, con
                        const int* model_of, const float* residual, const void* const* active, int B,
                        cudaStream_t st) {
   ShArgs a{x, H, W, y, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual, active, B,
-           H, W, 0, 0, 0, 0, 0};
+           H, W, H, 0, 0, 0, 0, 0};
   if (channels == 16) return launch_shift<16>(a, st);
   if (channels == 32) return launch_shift<32>(a, st);
   return false;
@@ -1005,10 +1362,27 @@ bool conv_shift_s2_launch(const float* x, int H, int W, float* y, int Ho, int Wo
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   ShArgs a{x, H, W, y, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual, active, B,
-           Ho, Wo, 0, 0, 0, 0, 0};
+           Ho, Wo, Ho, 0, 0, 0, 0, 0};
   long long grid;
   plan_units(a, Ho, (Wo + SEG2 - 1) / SEG2, sms, grid);
   return launch_pdl(k_conv_shift_s2, a, grid, S2::SMEM, st);
+}
+
+bool conv_shift_t_launch(const float* x, int H, int W, float* y, const float* w, const float* bias, int softplus,
+                         const float* addend, long long addend_bstride, int addend_per_model, const int* model_of,
+                         const float* residual, const void* const* active, int B, cudaStream_t st) {
+  static int sms = 0;
+  if (!sms) {
+    cudaFuncSetAttribute(k_conv_shift_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ST::SMEM);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  ShArgs a{x, H, W, y, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual, active, B,
+           2 * H, 2 * W, H, 0, 0, 0, 0, 0};
+  long long grid;
+  plan_units(a, H, (W + SEG2 - 1) / SEG2, sms, grid);
+  return launch_pdl(k_conv_shift_t, a, grid, ST::SMEM, st);
 }
 
 }  // namespace hs

@@ -16,8 +16,10 @@ torch = pytest.importorskip("torch")
 
 
 @pytest.mark.parametrize("cin,cout,H,W,stride", [(16, 16, 256, 256, 1), (32, 32, 128, 128, 1), (64, 64, 64, 64, 1),
-                                                  (16, 32, 256, 256, 2), (16, 16, 250, 250, 1)])
+                                                  (16, 32, 256, 256, 2), (16, 16, 250, 250, 1), (32, 16, 128, 128, -2)])
 def test_tc_conv_bitwise_repeatable(cin, cout, H, W, stride):
+    transposed = stride < 0  # stride -2: transposed conv, output 2H x 2W
+    stride = abs(stride)
     from paper_2306_17486_b200 import _lib
     from paper_2306_17486_b200.device import stream_handle
 
@@ -27,10 +29,10 @@ def test_tc_conv_bitwise_repeatable(cin, cout, H, W, stride):
     x = torch.randn(B, H, W, cin, device="cuda", generator=g)
     w = torch.randn(cout, 3, 3, cin, device="cuda", generator=g) / np.sqrt(9 * cin)
     b = torch.randn(cout, device="cuda", generator=g)
-    Ho, Wo = (H - 1) // stride + 1, (W - 1) // stride + 1
+    Ho, Wo = (2 * H, 2 * W) if transposed else ((H - 1) // stride + 1, (W - 1) // stride + 1)
     add = torch.randn(B, Ho, Wo, cout, device="cuda", generator=g)
     y = torch.empty_like(add)
-    c = _lib.HsConv(cin, cout, stride, 0, 1, w.data_ptr(), b.data_ptr())
+    c = _lib.HsConv(cin, cout, stride, int(transposed), 1, w.data_ptr(), b.data_ptr())
     ref = None
     for _ in range(8):
         y.fill_(float("nan"))

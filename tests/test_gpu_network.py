@@ -82,6 +82,9 @@ def test_tconv_shapes(rng, cin, cout, hw):
                                                # stride-2 tcgen05.shift kernel: odd and even sizes, partial segments
                                                (16, 32, 1, (7, 100)), (16, 32, 1, (1, 33)), (16, 32, 1, (34, 63)),
                                                (16, 32, 1, (9, 129)), (16, 32, 1, (66, 250)),
+                                               # transposed tcgen05.shift kernel: partial segments, one-row and 33-row inputs
+                                               (32, 16, 2, (5, 50)), (32, 16, 2, (1, 31)), (32, 16, 2, (33, 65)),
+                                               (32, 16, 2, (7, 125)),
                                                (32, 32, 0, (4, 128)),
                                                (16, 32, 1, (6, 256)), (32, 16, 2, (3, 128)), (32, 16, 2, (2, 256)),
                                                # M = 64 tiles (64-wide levels) and cout split across CTAs
