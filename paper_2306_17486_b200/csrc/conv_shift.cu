@@ -1309,6 +1309,7 @@ void plan_units(ShArgs& a, int Ho, int nseg, int sms, long long& grid) {
 
 template <typename K>
 bool launch_pdl(K kernel, const ShArgs& a, long long grid, size_t smem_bytes, cudaStream_t st) {
+  if (grid <= 0) return true;  // empty batch or image: nothing to do
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(NT);
