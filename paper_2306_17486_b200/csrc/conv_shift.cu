@@ -934,20 +934,28 @@ __global__ void __launch_bounds__(NT, 1) k_conv_shift_s2(ShArgs a) {
 // end (ky 0 of its last odd output row).  TMEM: four 96-column accumulators, two 48-column A slots.  The two
 // epilogue groups take the even and the odd output columns of every output row: a lane's 16 channels are one
 // 64-byte pixel, and the group-of-four transpose makes every store write whole pixels.
+// 64 -> 32 (template CIN = 64): a CTA computes one 16-channel half of the output (units of the two halves run
+// side by side, so the input rows are shared in L2) and takes a row's 64 input channels as two 32-channel halves
+// through the two A slots in turn: the second half accumulates onto the first, and the converters refill one slot
+// while the MMAs read the other.
+template <int CIN_>
 struct ST {
-  static constexpr int CIN = 32, COUT = 16, KC = 4, NW = 3 * COUT;
-  static constexpr uint32_t WT = KC * NW, KK = 2 * NW;
+  static constexpr int CIN = CIN_, COUT = 16, COUT_T = CIN / 2, NSPLIT = COUT_T / COUT, KH = CIN / 32;
+  static constexpr int KC = CIN / 8, NW = 3 * COUT;
+  static constexpr uint32_t WT = KC * NW, KK = 2 * NW, WH = 4 * NW;  // weight units per tap / K step / K half
   static constexpr int W_BYTES = 9 * KC * NW * 16;
   static constexpr int QBYTES = 32 * CIN * 4;          // raw bytes of one lane quarter's 32 input pixels
   static constexpr int RAW_BYTES = 4 * QBYTES;
-  static constexpr int NR = 8, NACC = 4, ACOLS = 6 * COUT, AOFF = NACC * ACOLS, SLOT_COLS = 48;
+  static constexpr int NR = CIN == 32 ? 8 : 4, NACC = 4, ACOLS = 6 * COUT, AOFF = NACC * ACOLS, SLOT_COLS = 48;
   static constexpr int NSA = (512 - AOFF) / SLOT_COLS;
   static constexpr size_t SMEM = W_BYTES + (size_t)NR * RAW_BYTES + 8 * (2 * NR + 2 * NSA + 2 * NACC) + 16 + 4 * COUT;
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
 // the tcgen05 work of one input row: targets a (output row 2 r - 1, ky 0, accumulating), b (2 r, ky 1) and
-// c (2 r + 1, ky 2), both opened here (their first MMA per column parity overwrites); valid bits 0 / 1 / 2
+// c (2 r + 1, ky 2), both opened here (their first MMA per column parity overwrites unless valid bit 3 says
+// this is a later K half); valid bits 0 / 1 / 2 enable a / b / c
+template <typename F>
 HS_DEV void t_row_mmas(uint32_t da, uint32_t db_, uint32_t dc, uint32_t abase, uint32_t wlo, uint32_t valid) {
   constexpr uint32_t I0 = idesc_bf16(128, 48), I1 = idesc_bf16(128, 32), I2 = idesc_bf16(128, 16);
   if (kShProbe & 2) return;
@@ -966,7 +974,7 @@ HS_DEV void t_row_mmas(uint32_t da, uint32_t db_, uint32_t dc, uint32_t abase, u
       "and.b32 m, %5, 1;\n\tsetp.ne.b32 ea, m, 0;\n\tand.pred ea, ea, e;\n\t"
       "and.b32 m, %5, 2;\n\tsetp.ne.b32 eb, m, 0;\n\tand.pred eb, eb, e;\n\t"
       "and.b32 m, %5, 4;\n\tsetp.ne.b32 ec, m, 0;\n\tand.pred ec, ec, e;\n\t"
-      "setp.ne.b32 pz, %5, %5;\n\tsetp.eq.b32 pt, %5, %5;\n\t"
+      "and.b32 m, %5, 8;\n\tsetp.ne.b32 pz, m, 0;\n\tsetp.eq.b32 pt, %5, %5;\n\t"
       "add.u32 a01, %3, 8;\n\tadd.u32 a10, %3, 16;\n\tadd.u32 a11, %3, 24;\n\tadd.u32 a20, %3, 32;\n\tadd.u32 a21, %3, 40;\n\t"
       "add.u32 da1, %0, 48;\n\tadd.u32 db1, %1, 48;\n\tadd.u32 dc1, %2, 48;\n\t"
       // row as written: kx 1 -> even output columns, kx 2 -> odd output columns
@@ -978,16 +986,17 @@ HS_DEV void t_row_mmas(uint32_t da, uint32_t db_, uint32_t dc, uint32_t abase, u
       // shifted row (pixel p + 1): kx 0 -> odd output columns
       HS_T_TAP("%10", "da1", "ea", "pt") HS_T_TAP("%13", "db1", "eb", "pt") HS_T_TAP("%16", "dc1", "ec", "pt")
       "}\n" ::"r"(da), "r"(db_), "r"(dc), "r"(abase), "r"(wlo), "r"(valid), "n"(kDescHi), "n"(I0), "n"(I1), "n"(I2),
-      "n"(0 * ST::WT), "n"(1 * ST::WT), "n"(2 * ST::WT), "n"(3 * ST::WT), "n"(4 * ST::WT), "n"(5 * ST::WT),
-      "n"(6 * ST::WT), "n"(7 * ST::WT), "n"(8 * ST::WT), "n"(ST::KK)
+      "n"(0 * F::WT), "n"(1 * F::WT), "n"(2 * F::WT), "n"(3 * F::WT), "n"(4 * F::WT), "n"(5 * F::WT),
+      "n"(6 * F::WT), "n"(7 * F::WT), "n"(8 * F::WT), "n"(F::KK)
       : "memory");
 #undef HS_T_MMA3
 #undef HS_T_TAP
 }
 
+template <int CIN_>
 __global__ void __launch_bounds__(NT, 1) k_conv_shift_t(ShArgs a) {
-  using F = ST;
-  constexpr int C = F::CIN, CO = F::COUT, KC = F::KC, NW = F::NW, NR = F::NR, NACC = F::NACC, NSA = F::NSA,
+  using F = ST<CIN_>;
+  constexpr int C = F::CIN, CO = F::COUT, CT = F::COUT_T, KH = F::KH, NSPLIT = F::NSPLIT, KC = F::KC, NW = F::NW, NR = F::NR, NACC = F::NACC, NSA = F::NSA,
                 ACOLS = F::ACOLS;
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* wst = smem;
@@ -1001,11 +1010,13 @@ __global__ void __launch_bounds__(NT, 1) k_conv_shift_t(ShArgs a) {
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(acc_empty + NACC);
   float* s_bias = reinterpret_cast<float*>(s_tmem + 4);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const long long nunits = (long long)a.B * a.ntile * a.ngroups;
+  // units: the cout halves of one tile run side by side; a persistent CTA keeps one half (grid is a multiple of NSPLIT)
+  const long long nunits = (long long)a.B * a.ntile * a.ngroups * NSPLIT;
+  const int split = (int)(blockIdx.x % NSPLIT);
 
-  for (int e = tid; e < 9 * KC * CO; e += NT) {  // resident weight stack, layout (tap, chunk, row) x 16 B
+  for (int e = tid; e < 9 * KC * CO; e += NT) {  // resident weight stack of this half, layout (tap, chunk, row) x 16 B
     const int n = e % CO, c = (e / CO) % KC, t = e / (CO * KC);
-    const float* src = a.w + ((size_t)n * 9 + t) * C + 8 * c;
+    const float* src = a.w + ((size_t)(split * CO + n) * 9 + t) * C + 8 * c;
     const float4 v0 = __ldg(reinterpret_cast<const float4*>(src)), v1 = __ldg(reinterpret_cast<const float4*>(src + 4));
     const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
     uint4 p[3];
@@ -1014,7 +1025,7 @@ __global__ void __launch_bounds__(NT, 1) k_conv_shift_t(ShArgs a) {
     for (int part = 0; part < 3; ++part)
       *reinterpret_cast<uint4*>(wst + ((size_t)(t * KC + c) * NW + part * CO + n) * 16) = p[part];
   }
-  if (tid < CO) s_bias[tid] = a.bias[tid];
+  if (tid < CO) s_bias[tid] = a.bias[split * CO + tid];
   if (tid == 0) {
     for (int i = 0; i < NR; ++i) {
       mbar_init(smem_u32(&raw_full[i]), 1);
@@ -1047,7 +1058,7 @@ __global__ void __launch_bounds__(NT, 1) k_conv_shift_t(ShArgs a) {
       uint32_t seq = 0;
       for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
         Unit U;
-        if (!unit_at(a, u, U)) continue;
+        if (!unit_at(a, u / NSPLIT, U)) continue;
         const float* img = a.x + (size_t)U.b * a.H * a.W * C;
         int qy0[4], qx0[4];
         bool qv[4];
@@ -1087,7 +1098,7 @@ __global__ void __launch_bounds__(NT, 1) k_conv_shift_t(ShArgs a) {
     uint32_t seq = 0;
     for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
-      if (!unit_at(a, u, U)) continue;
+      if (!unit_at(a, u / NSPLIT, U)) continue;
       int qy0, seg;
       const bool qv = quarter_at(a, U, q, qy0, seg);
       const bool xok = qv && SEG2 * seg + lane < a.W;
@@ -1095,51 +1106,54 @@ __global__ void __launch_bounds__(NT, 1) k_conv_shift_t(ShArgs a) {
         const int g = qy0 + i;
         const uint32_t s = seq % NR;
         mbar_wait(smem_u32(&raw_full[s]), (seq / NR) & 1);
-        float4 v[8];
+#pragma unroll 1
+        for (int h = 0; h < KH; ++h) {  // 32 input channels at a time, one A slot each
+          float4 v[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (xok && g < a.H) {
-          const float4* src = reinterpret_cast<const float4*>(raw + (size_t)s * F::RAW_BYTES + (size_t)q * F::QBYTES +
-                                                              (size_t)lane * 128);
-          const int r = lane & 7;  // rotated piece order: eight bank groups per quarter-warp wavefront
-          float4 w4[8];
+          for (int k = 0; k < 8; ++k) v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (xok && g < a.H) {
+            const float4* src = reinterpret_cast<const float4*>(raw + (size_t)s * F::RAW_BYTES + (size_t)q * F::QBYTES +
+                                                                (size_t)lane * (C * 4) + (size_t)h * 128);
+            const int r = lane & 7;  // rotated piece order: eight bank groups per quarter-warp wavefront
+            float4 w4[8];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) w4[k] = src[(k + r) & 7];
+            for (int k = 0; k < 8; ++k) w4[k] = src[(k + r) & 7];
 #pragma unroll
-          for (int st = 1; st < 8; st <<= 1) {
-            float4 t4[8];
+            for (int st = 1; st < 8; st <<= 1) {
+              float4 t4[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) t4[k] = (r & st) ? w4[(k + 8 - st) & 7] : w4[k];
+              for (int k = 0; k < 8; ++k) t4[k] = (r & st) ? w4[(k + 8 - st) & 7] : w4[k];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) w4[k] = t4[k];
+              for (int k = 0; k < 8; ++k) w4[k] = t4[k];
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = w4[k];
           }
+          uint4 pw[3][4] = {};
+          if (!(kShProbe & 4)) {
 #pragma unroll
-          for (int k = 0; k < 8; ++k) v[k] = w4[k];
-        }
-        uint4 pw[3][4] = {};
-        if (!(kShProbe & 4)) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const float f[8] = {v[2 * c].x, v[2 * c].y, v[2 * c].z, v[2 * c].w,
-                                v[2 * c + 1].x, v[2 * c + 1].y, v[2 * c + 1].z, v[2 * c + 1].w};
-            split_bf16x3(f, pw[0][c], pw[1][c], pw[2][c]);
+            for (int c = 0; c < 4; ++c) {
+              const float f[8] = {v[2 * c].x, v[2 * c].y, v[2 * c].z, v[2 * c].w,
+                                  v[2 * c + 1].x, v[2 * c + 1].y, v[2 * c + 1].z, v[2 * c + 1].w};
+              split_bf16x3(f, pw[0][c], pw[1][c], pw[2][c]);
+            }
           }
-        }
-        const uint32_t as = seq % NSA, ause = seq / NSA;
-        if (ause > 0) mbar_wait(smem_u32(&a_empty[as]), (ause - 1) & 1);
-        tc_fence_after();
-        const uint32_t tcol = tmem + ((uint32_t)(32 * q) << 16) + F::AOFF + as * F::SLOT_COLS;
-        if (!(kShProbe & 4)) {
+          const uint32_t aseq = seq * KH + h, as = aseq % NSA, ause = aseq / NSA;
+          if (ause > 0) mbar_wait(smem_u32(&a_empty[as]), (ause - 1) & 1);
+          tc_fence_after();
+          const uint32_t tcol = tmem + ((uint32_t)(32 * q) << 16) + F::AOFF + as * F::SLOT_COLS;
+          if (!(kShProbe & 4)) {
 #pragma unroll
-          for (int part = 0; part < 3; ++part) {
-            tmem_st8(tcol + 16 * part, pw[part][0], pw[part][1]);      // channels 0-15 (K step 0)
-            tmem_st8(tcol + 16 * part + 8, pw[part][2], pw[part][3]);  // channels 16-31 (K step 1)
+            for (int part = 0; part < 3; ++part) {
+              tmem_st8(tcol + 16 * part, pw[part][0], pw[part][1]);      // channels 0-15 of the half (K step 0)
+              tmem_st8(tcol + 16 * part + 8, pw[part][2], pw[part][3]);  // channels 16-31 (K step 1)
+            }
           }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&a_full[as]));
         }
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&a_full[as]));
         fence_async_smem();  // the raw slot is released after the row is in TMEM (see k_conv_shift)
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&raw_empty[s]));
@@ -1160,26 +1174,31 @@ __global__ void __launch_bounds__(NT, 1) k_conv_shift_t(ShArgs a) {
     };
     for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
-      if (!unit_at(a, u, U)) continue;
+      if (!unit_at(a, u / NSPLIT, U)) continue;
       uint32_t s_a = 0, s_b = 0, s_c = 0;
       for (int i = 0; i <= U.bh; ++i) {
-        mbar_wait(smem_u32(&a_full[as]), a_par);
         const bool v_a = i > 0, v_bc = i < U.bh;
-        s_a = s_c;  // output row 2 r - 1 was opened as the previous input row's target c
-        if (v_bc) {
-          s_b = open_acc();
-          s_c = open_acc();
+#pragma unroll 1
+        for (int h = 0; h < KH; ++h) {
+          mbar_wait(smem_u32(&a_full[as]), a_par);
+          if (h == 0) {
+            s_a = s_c;  // output row 2 r - 1 was opened as the previous input row's target c
+            if (v_bc) {
+              s_b = open_acc();
+              s_c = open_acc();
+            }
+          }
+          tc_fence_after();
+          t_row_mmas<F>(tm + s_a * ACOLS, tm + s_b * ACOLS, tm + s_c * ACOLS, tm + F::AOFF + as * F::SLOT_COLS,
+                        wlo + (uint32_t)h * F::WH, (v_a ? 1u : 0u) | (v_bc ? 6u : 0u) | (h ? 8u : 0u));
+          mma_commit(smem_u32(&a_empty[as]));
+          if (++as == (uint32_t)NSA) {
+            as = 0;
+            a_par ^= 1;
+          }
         }
-        tc_fence_after();
-        t_row_mmas(tm + s_a * ACOLS, tm + s_b * ACOLS, tm + s_c * ACOLS, tm + F::AOFF + as * F::SLOT_COLS, wlo,
-                   (v_a ? 1u : 0u) | (v_bc ? 6u : 0u));
-        mma_commit(smem_u32(&a_empty[as]));
         if (v_a) mma_commit(smem_u32(&acc_full[s_a]));
         if (v_bc) mma_commit(smem_u32(&acc_full[s_b]));
-        if (++as == (uint32_t)NSA) {
-          as = 0;
-          a_par ^= 1;
-        }
       }
     }
   } else {
@@ -1189,12 +1208,12 @@ __global__ void __launch_bounds__(NT, 1) k_conv_shift_t(ShArgs a) {
     uint32_t tile = 0;
     for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
-      if (!unit_at(a, u, U)) continue;
+      if (!unit_at(a, u / NSPLIT, U)) continue;
       const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[U.b] : 0) : U.b) *
                                                    a.addend_bstride
                                   : nullptr;
-      const float* res = a.residual ? a.residual + (size_t)U.b * a.Ho * a.Wo * CO : nullptr;
-      float* yimg = a.y + (size_t)U.b * a.Ho * a.Wo * CO;
+      const float* res = a.residual ? a.residual + (size_t)U.b * a.Ho * a.Wo * CT : nullptr;
+      float* yimg = a.y + (size_t)U.b * a.Ho * a.Wo * CT;
       int qy0, seg;
       const bool qv = quarter_at(a, U, q4, qy0, seg);
       const int pg0 = SEG2 * seg + gb;  // input pixel of this lane group's first lane; the group's pixel j is pg0 + j
@@ -1206,22 +1225,22 @@ __global__ void __launch_bounds__(NT, 1) k_conv_shift_t(ShArgs a) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) sa[j] = sr[j] = make_float4(0.f, 0.f, 0.f, 0.f);
       auto issue_side = [&](int oy) {
-        const size_t gp = ((size_t)oy * a.Wo + 2 * pg0 + hg) * CO;
+        const size_t gp = ((size_t)oy * a.Wo + 2 * pg0 + hg) * CT + split * CO;
         if (add) {
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            if (ok[j]) sa[j] = __ldg(reinterpret_cast<const float4*>(add + gp + (size_t)j * 2 * CO) + gi);
+            if (ok[j]) sa[j] = __ldg(reinterpret_cast<const float4*>(add + gp + (size_t)j * 2 * CT) + gi);
         }
         if (res) {
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            if (ok[j]) sr[j] = __ldg(reinterpret_cast<const float4*>(res + gp + (size_t)j * 2 * CO) + gi);
+            if (ok[j]) sr[j] = __ldg(reinterpret_cast<const float4*>(res + gp + (size_t)j * 2 * CT) + gi);
         }
       };
       if (oy_first < oy_end) issue_side(oy_first);
       for (int oy = oy_first; oy < oy_end; ++oy, ++tile) {
         const uint32_t acc = tile % NACC;
-        const size_t gpix = ((size_t)oy * a.Wo + 2 * pg0 + hg) * CO;
+        const size_t gpix = ((size_t)oy * a.Wo + 2 * pg0 + hg) * CT + split * CO;
         mbar_wait(smem_u32(&acc_full[acc]), (tile / NACC) & 1);
         tc_fence_after();
         float o[16] = {};
@@ -1265,7 +1284,7 @@ __global__ void __launch_bounds__(NT, 1) k_conv_shift_t(ShArgs a) {
           const uint64_t s23 = add2(pkf(sa[j].z, sa[j].w), pkf(sr[j].z, sr[j].w));
           const uint64_t q01 = add2(pkf(ch[j].x, ch[j].y), s01), q23 = add2(pkf(ch[j].z, ch[j].w), s23);
           if (ok[j])
-            reinterpret_cast<float4*>(yimg + gpix + (size_t)j * 2 * CO)[gi] = make_float4(lo_f(q01), hi_f(q01), lo_f(q23), hi_f(q23));
+            reinterpret_cast<float4*>(yimg + gpix + (size_t)j * 2 * CT)[gi] = make_float4(lo_f(q01), hi_f(q01), lo_f(q23), hi_f(q23));
         }
         if (oy + 1 < oy_end) issue_side(oy + 1);
       }
@@ -1369,21 +1388,30 @@ bool conv_shift_s2_launch(const float* x, int H, int W, float* y, int Ho, int Wo
   return launch_pdl(k_conv_shift_s2, a, grid, S2::SMEM, st);
 }
 
-bool conv_shift_t_launch(const float* x, int H, int W, float* y, const float* w, const float* bias, int softplus,
-                         const float* addend, long long addend_bstride, int addend_per_model, const int* model_of,
-                         const float* residual, const void* const* active, int B, cudaStream_t st) {
+template <int CIN_>
+static bool launch_shift_t(ShArgs a, cudaStream_t st) {
+  using F = ST<CIN_>;
   static int sms = 0;
   if (!sms) {
-    cudaFuncSetAttribute(k_conv_shift_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ST::SMEM);
+    cudaFuncSetAttribute(k_conv_shift_t<CIN_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F::SMEM);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
+  long long grid;
+  plan_units(a, a.H, (a.W + SEG2 - 1) / SEG2, sms / F::NSPLIT, grid);  // grid: tiles; each has NSPLIT cout halves
+  return launch_pdl(k_conv_shift_t<CIN_>, a, grid * F::NSPLIT, F::SMEM, st);
+}
+
+bool conv_shift_t_launch(int cin, const float* x, int H, int W, float* y, const float* w, const float* bias,
+                         int softplus, const float* addend, long long addend_bstride, int addend_per_model,
+                         const int* model_of, const float* residual, const void* const* active, int B,
+                         cudaStream_t st) {
   ShArgs a{x, H, W, y, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of, residual, active, B,
            2 * H, 2 * W, H, 0, 0, 0, 0, 0};
-  long long grid;
-  plan_units(a, H, (W + SEG2 - 1) / SEG2, sms, grid);
-  return launch_pdl(k_conv_shift_t, a, grid, ST::SMEM, st);
+  if (cin == 32) return launch_shift_t<32>(a, st);
+  if (cin == 64) return launch_shift_t<64>(a, st);
+  return false;
 }
 
 }  // namespace hs

@@ -100,6 +100,9 @@ constexpr int kProbe = HS_TC_PROBE;
 #ifndef HS_TC_SHIFT
 #define HS_TC_SHIFT 1  // 16 -> 16 stride-1 layers on the tcgen05.shift kernel (conv_shift.cu); 0 keeps the tap-view kernel below
 #endif
+#ifndef HS_TC_SHIFT_T64
+#define HS_TC_SHIFT_T64 1  // 64 -> 32 transposed layer on the tcgen05.shift kernel (cout halves per CTA, two K halves)
+#endif
 #ifndef HS_TC_SHIFT_T
 #define HS_TC_SHIFT_T 1  // 32 -> 16 transposed layer on the tcgen05.shift kernel
 #endif
@@ -1261,6 +1264,7 @@ bool conv_tc_supported(int cin, int cout, int stride, int transposed, int H, int
     return true;  // conv_shift.cu: 30-pixel segments, any width
   if (HS_TC_SHIFT_S2 && !planar && mode == 1 && cin == 16 && cout == 32) return true;
   if (HS_TC_SHIFT_T && !planar && mode == 2 && cin == 32 && cout == 16) return true;
+  if (HS_TC_SHIFT_T64 && !planar && mode == 2 && cin == 64 && cout == 32) return true;
   if (width % 64) return false;
   return slice_for(cin, cout, mode) > 0;
 }
@@ -1278,8 +1282,8 @@ bool conv_tc_launch(const float* x, int H, int W, int cin, float* y, int Ho, int
   if (HS_TC_SHIFT_S2 && !planar && !kProbe && mode == 1 && cin == 16 && cout == 32)
     return conv_shift_s2_launch(x, H, W, y, Ho, Wo, w, bias, softplus, addend, addend_bstride, addend_per_model,
                                 model_of, residual, active, B, st);
-  if (HS_TC_SHIFT_T && !planar && !kProbe && mode == 2 && cin == 32 && cout == 16)
-    return conv_shift_t_launch(x, H, W, y, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of,
+  if (!planar && !kProbe && mode == 2 && ((HS_TC_SHIFT_T && cin == 32 && cout == 16) || (HS_TC_SHIFT_T64 && cin == 64 && cout == 32)))
+    return conv_shift_t_launch(cin, x, H, W, y, w, bias, softplus, addend, addend_bstride, addend_per_model, model_of,
                                residual, active, B, st);
   const bool m128 = ((mode == 2 ? W : Wo) % 128) == 0 && !(kProbe & 32);
 #define HS_TC(CI, CO, MD, CSL)                                           \

@@ -20,10 +20,12 @@ bool conv_shift_s2_launch(const float* x, int H, int W, float* y, int Ho, int Wo
                           int softplus, const float* addend, long long addend_bstride, int addend_per_model,
                           const int* model_of, const float* residual, const void* const* active, int B,
                           cudaStream_t st);
-// 32 -> 16 transposed layer on the same scheme (lanes hold input pixels; one shift for the odd output columns)
-bool conv_shift_t_launch(const float* x, int H, int W, float* y, const float* w, const float* bias, int softplus,
-                         const float* addend, long long addend_bstride, int addend_per_model, const int* model_of,
-                         const float* residual, const void* const* active, int B, cudaStream_t st);
+// 32 -> 16 and 64 -> 32 transposed layers on the same scheme (lanes hold input pixels; one shift for the odd output
+// columns; 64 -> 32: one 16-channel output half per CTA, the input channels in two halves)
+bool conv_shift_t_launch(int cin, const float* x, int H, int W, float* y, const float* w, const float* bias,
+                         int softplus, const float* addend, long long addend_bstride, int addend_per_model,
+                         const int* model_of, const float* residual, const void* const* active, int B,
+                         cudaStream_t st);
 // K-streamed tcgen05 kernel for the >= 64-channel layers (conv_wide.cu): 64->64 / 128->128 stride 1,
 // 32->64 / 64->128 / 128->128 stride 2, 128->64 and 128->128 (two 64-channel slices) transposed, widths
 // (transposed: input widths) that are multiples of 128.  Same arguments and epilogue as conv_tc_launch.

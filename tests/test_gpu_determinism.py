@@ -16,7 +16,7 @@ torch = pytest.importorskip("torch")
 
 
 @pytest.mark.parametrize("cin,cout,H,W,stride", [(16, 16, 256, 256, 1), (32, 32, 128, 128, 1), (64, 64, 64, 64, 1),
-                                                  (16, 32, 256, 256, 2), (16, 16, 250, 250, 1), (32, 16, 128, 128, -2)])
+                                                  (16, 32, 256, 256, 2), (16, 16, 250, 250, 1), (32, 16, 128, 128, -2), (64, 32, 64, 64, -2)])
 def test_tc_conv_bitwise_repeatable(cin, cout, H, W, stride):
     transposed = stride < 0  # stride -2: transposed conv, output 2H x 2W
     stride = abs(stride)

@@ -85,6 +85,8 @@ def test_tconv_shapes(rng, cin, cout, hw):
                                                # transposed tcgen05.shift kernel: partial segments, one-row and 33-row inputs
                                                (32, 16, 2, (5, 50)), (32, 16, 2, (1, 31)), (32, 16, 2, (33, 65)),
                                                (32, 16, 2, (7, 125)),
+                                               (64, 32, 2, (5, 50)), (64, 32, 2, (1, 31)), (64, 32, 2, (33, 65)),
+                                               (64, 32, 2, (4, 128)),
                                                (32, 32, 0, (4, 128)),
                                                (16, 32, 1, (6, 256)), (32, 16, 2, (3, 128)), (32, 16, 2, (2, 256)),
                                                # M = 64 tiles (64-wide levels) and cout split across CTAs
