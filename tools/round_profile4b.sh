@@ -10,5 +10,8 @@ cap r2g_shift16 'k_conv_shift<.int.16>' 4 python tools/step_probe.py --iters 6
 cap r2g_shift32 'k_conv_shift<.int.32>' 4 python tools/step_probe.py --iters 6
 cap r2g_wide6464 'k_conv_wide<.int.64, .int.64' 4 python tools/step_probe.py --iters 6
 cap r2g_shift_s2 'k_conv_shift_s2' 2 python tools/step_probe.py --iters 6
+cap r2g_shift_t32 'k_conv_shift_t<.int.32>' 2 python tools/step_probe.py --iters 6
+cap r2g_shift_t64 'k_conv_shift_t<.int.64>' 2 python tools/step_probe.py --iters 6
 cap r2g_shift16_resid 'k_conv_shift<.int.16>' 5 python tools/conv_probe.py --B 64 --H 512 --W 1024 --side residual --softplus 0 --iters 3
-ls -la gpurun_out | grep r2g
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2l_launches_c3_learned.csv python tools/step_probe.py --iters 6 > /dev/null 2>&1
+ls -la gpurun_out | grep -E 'r2g|r2l'
