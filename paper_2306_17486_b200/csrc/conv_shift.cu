@@ -52,6 +52,9 @@ using namespace tc;
 #ifndef HS_SH_ROT
 #define HS_SH_ROT 0  // 16 channels: converters read their pixel's four 16-byte pieces in rotated order (measured equal)
 #endif
+#ifndef HS_SH_FRAG
+#define HS_SH_FRAG 0  // stride-1 epilogue drains TMEM as 16x256b fragments (no transposes; 8-byte stores, full sectors): measured equal, in isolation and in the network
+#endif
 #ifndef HS_SH_NR
 #define HS_SH_NR 12
 #endif
@@ -218,6 +221,14 @@ HS_DEV void row_mmas_edge(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t abase,
 HS_DEV void tmem_st8(uint32_t taddr, const uint4& lo, const uint4& hi) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(lo.x),
                "r"(lo.y), "r"(lo.z), "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w));
+}
+
+// tcgen05.ld 16x256b.x2: 16 TMEM lanes x 16 columns as an MMA-style fragment.  Measured (tools/ld_probe.cu): register
+// j of lane l holds TMEM lane (lane base) + l / 4 + 8 ((j / 2) % 2), column (column base) + 8 (j / 4) + 2 (l % 4) + j % 2.
+HS_DEV void tmem_ld_frag16(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
 }
 
 template <int C>
@@ -457,6 +468,107 @@ __global__ void __launch_bounds__(NT, 1) k_conv_shift(ShArgs a) {
   } else {
     // ================= epilogue: warp q4 drains its lane quarter.  16 channels: group hg takes the output rows
     // with tile % 2 == hg; 32 channels: group hg takes channels 16 hg .. 16 hg + 15 of every output row.
+#if HS_SH_FRAG
+    // The accumulator is read as 16x256b fragments (tmem_ld_frag16): a thread holds, of each 16-lane half hh, the
+    // rows l / 4 and l / 4 + 8 and the channel pairs 2 (l % 4) + {0, 1} of both 8-channel blocks, so four lanes
+    // cover 32 contiguous bytes of a pixel and every 8-byte store (and side-input load) instruction moves whole
+    // sectors -- without the 4x4 transposes the lane-per-pixel layout needed (64 shuffles and selects per row).
+    const int q4 = warp & 3, hg = warp >> 2;
+    const int l4 = lane >> 2, c2 = 2 * (lane & 3);
+    const int ch0 = (F::HALVES ? 16 * hg : 0) + c2;  // this thread's first channel (block 0); block 1 at + 8
+    constexpr int STEP = F::HALVES ? 1 : 2;          // output rows between two rows of this group
+    uint32_t tile = 0;
+    for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
+      Unit U;
+      if (!unit_at(a, u, U)) continue;
+      const float* add = a.addend ? a.addend + (a.addend_per_model ? (a.model_of ? a.model_of[U.b] : 0) : U.b) *
+                                                   a.addend_bstride
+                                  : nullptr;
+      const float* res = a.residual ? a.residual + (size_t)U.b * a.H * a.W * C : nullptr;
+      float* yimg = a.y + (size_t)U.b * a.H * a.W * C;
+      int qy0, seg;
+      const bool qv = quarter_at(a, U, q4, qy0, seg);
+      const int oy_end = qy0 + U.bh;
+      // this thread's four pixels: row (hh, rh) = 16 hh + 8 rh + l4 of the segment
+      int px[4];
+      bool ok[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int row = 16 * (k >> 1) + 8 * (k & 1) + l4;
+        px[k] = SEG * seg + row;
+        ok[k] = qv && row < SEG && px[k] < a.W;
+      }
+      const float2 bs0 = *reinterpret_cast<const float2*>(s_bias + ch0), bs1 = *reinterpret_cast<const float2*>(s_bias + ch0 + 8);
+      // side inputs: requested when the group's previous row has stored, first touched at the store
+      float2 sa[4][2], sr[4][2];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) sa[k][0] = sa[k][1] = sr[k][0] = sr[k][1] = make_float2(0.f, 0.f);
+      auto issue_side = [&](int oy) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (!ok[k]) continue;
+          const size_t gp = ((size_t)oy * a.W + px[k]) * C + ch0;
+          if (add) {
+            sa[k][0] = __ldg(reinterpret_cast<const float2*>(add + gp));
+            sa[k][1] = __ldg(reinterpret_cast<const float2*>(add + gp + 8));
+          }
+          if (res) {
+            sr[k][0] = __ldg(reinterpret_cast<const float2*>(res + gp));
+            sr[k][1] = __ldg(reinterpret_cast<const float2*>(res + gp + 8));
+          }
+        }
+      };
+      {
+        const int first = F::HALVES ? qy0 : qy0 + (int)((tile ^ (uint32_t)hg) & 1);  // this group's first row
+        if (first < oy_end) issue_side(first);
+      }
+      for (int oy = qy0; oy < oy_end; ++oy, ++tile) {
+        if (!F::HALVES && (int)(tile & 1) != hg) continue;
+        const uint32_t acc = tile % NACC;
+        mbar_wait(smem_u32(&acc_full[acc]), (tile / NACC) & 1);
+        tc_fence_after();
+        uint64_t o[2][4];  // [hh][j / 2]: (rh, block) = (0, 0), (1, 0), (0, 1), (1, 1), channel pairs packed
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t r0[8], r1[8], r2[8];
+          const uint32_t col = tmem + ((uint32_t)(q4 * 32 + 16 * hh) << 16) + acc * ACOLS + (F::HALVES ? 16 * hg : 0);
+          if (!(kShProbe & 32)) {
+            tmem_ld_frag16(col, r0);
+            tmem_ld_frag16(col + C, r1);
+            tmem_ld_frag16(col + 2 * C, r2);
+            tmem_wait_ld();
+          }
+#pragma unroll
+          for (int j = 0; j < 8; j += 2)  // (x0 + x1) + x2 partial sums (FADD2)
+            o[hh][j / 2] = add2(add2(pk2(r0[j], r0[j + 1]), pk2(r1[j], r1[j + 1])), pk2(r2[j], r2[j + 1]));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&acc_empty[acc]));  // TMEM free; finish from registers
+        if (!(kShProbe & 8)) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {  // pixel (hh, rh) = (k >> 1, k & 1)
+#pragma unroll
+            for (int blk = 0; blk < 2; ++blk) {
+              const float2 bs = blk ? bs1 : bs0;
+              const uint64_t v = add2(o[k >> 1][2 * blk + (k & 1)], pkf(bs.x, bs.y));
+              float vx = lo_f(v), vy = hi_f(v);
+              if (a.softplus) {
+                vx = softplus_fast(vx);
+                vy = softplus_fast(vy);
+              }
+              const uint64_t sd = add2(pkf(sa[k][blk].x, sa[k][blk].y), pkf(sr[k][blk].x, sr[k][blk].y));
+              const uint64_t q = add2(pkf(vx, vy), sd);  // o + (addend + residual), as conv_tc.cu
+              if (ok[k])
+                *reinterpret_cast<float2*>(yimg + ((size_t)oy * a.W + px[k]) * C + ch0 + 8 * blk) = make_float2(lo_f(q), hi_f(q));
+            }
+          }
+        }
+        if (oy + STEP < oy_end) issue_side(oy + STEP);
+      }
+    }
+  }
+#else
     const int q4 = warp & 3, hg = warp >> 2;
     const int gi = lane & 3, gb = lane & ~3;
     const int ch0 = F::HALVES ? 16 * hg : 0;  // first channel of this warp
@@ -562,6 +674,7 @@ __global__ void __launch_bounds__(NT, 1) k_conv_shift(ShArgs a) {
       }
     }
   }
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
