@@ -189,22 +189,26 @@ HS_DEV void row_mmas_all(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t abase, 
 }
 
 // band edges: valid bit 0 / 1 / 2 = output row g + 1 / g / g - 1 lies inside the band
+// (the elected lane branches in, as in row_mmas_all; the row predicates come from `valid` alone, so they are
+// warp-uniform and cost no per-MMA operand re-materialisation)
 #define HS_SH_EDGE_PREDS                                                              \
-  "and.b32 m, %5, 1;\n\tsetp.ne.b32 e0, m, 0;\n\tand.pred e0, e0, e;\n\t"             \
-  "and.b32 m, %5, 2;\n\tsetp.ne.b32 e1, m, 0;\n\tand.pred e1, e1, e;\n\t"             \
-  "and.b32 m, %5, 4;\n\tsetp.ne.b32 e2, m, 0;\n\tand.pred e2, e2, e;\n\t"             \
-  "and.pred es, e, e;\n\t"
+  "@!e bra SH_SKIPE_%=;\n\t"                                                           \
+  "and.b32 m, %5, 1;\n\tsetp.ne.b32 e0, m, 0;\n\t"                                     \
+  "and.b32 m, %5, 2;\n\tsetp.ne.b32 e1, m, 0;\n\t"                                     \
+  "and.b32 m, %5, 4;\n\tsetp.ne.b32 e2, m, 0;\n\t"                                     \
+  "setp.eq.b32 es, %5, %5;\n\t"
 template <int C>
 HS_DEV void row_mmas_edge(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t abase, uint32_t wlo, uint32_t valid) {
   constexpr uint32_t I0 = idesc_bf16(128, 3 * C), I1 = idesc_bf16(128, 2 * C), I2 = idesc_bf16(128, C);
   constexpr uint32_t WT = Cfg<C>::WT, KK = 2 * Cfg<C>::NW;
   if (kShProbe & 2) return;
   if constexpr (C == 16)
-    asm volatile(HS_SH_HEAD HS_SH_EDGE_PREDS HS_SH_ROW(HS_SH_TAP16, HS_SH_SHIFT16, "e0", "e1", "e2") "}\n" ::HS_SH_OPERANDS
+    asm volatile(HS_SH_HEAD HS_SH_EDGE_PREDS HS_SH_ROW(HS_SH_TAP16, HS_SH_SHIFT16, "e0", "e1", "e2") "SH_SKIPE_%=:\n\t}\n" ::HS_SH_OPERANDS
                  : "memory");
   else
-    asm volatile(HS_SH_HEAD HS_SH_EDGE_PREDS HS_SH_ROW(HS_SH_TAP32, HS_SH_SHIFT32, "e0", "e1", "e2") "}\n" ::HS_SH_OPERANDS
+    asm volatile(HS_SH_HEAD HS_SH_EDGE_PREDS HS_SH_ROW(HS_SH_TAP32, HS_SH_SHIFT32, "e0", "e1", "e2") "SH_SKIPE_%=:\n\t}\n" ::HS_SH_OPERANDS
                  : "memory");
+  __syncwarp();
 }
 #undef HS_SH_MMA3
 #undef HS_SH_TAP16
@@ -719,21 +723,22 @@ HS_DEV void s2_row_mmas(uint32_t dx, uint32_t dy, uint32_t abase, uint32_t wx, u
   asm volatile(
       "{\n\t.reg .pred e, ex, ey, pz, pt;\n\t.reg .b64 db;\n\t.reg .b32 hi, i0, i1, i2, e1, e2, o0, o1, o2, bl, m;\n\t"
       "mov.b32 hi, %6;\n\tmov.b32 i0, %7;\n\tmov.b32 i1, %8;\n\tmov.b32 i2, %9;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "and.b32 m, %5, 1;\n\tsetp.ne.b32 ex, m, 0;\n\tand.pred ex, ex, e;\n\t"
-      "and.b32 m, %5, 2;\n\tsetp.ne.b32 ey, m, 0;\n\tand.pred ey, ey, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t@!e bra S2_SKIP_%=;\n\t"  // the elected lane branches in: uniform predicates below
+      "and.b32 m, %5, 1;\n\tsetp.ne.b32 ex, m, 0;\n\t"
+      "and.b32 m, %5, 2;\n\tsetp.ne.b32 ey, m, 0;\n\t"
       "setp.ne.b32 pz, %5, %5;\n\tsetp.eq.b32 pt, %5, %5;\n\t"
       "add.u32 e1, %2, 16;\n\tadd.u32 e2, %2, 32;\n\tadd.u32 o0, %2, 8;\n\tadd.u32 o1, %2, 24;\n\tadd.u32 o2, %2, 40;\n\t"
       HS_S2_TAP("%3", "%10", "%0", "ex", "pt", "%2", "e1", "e2") HS_S2_TAP("%4", "%10", "%1", "ey", "pz", "%2", "e1", "e2")
       HS_S2_TAP("%3", "%11", "%0", "ex", "pt", "o0", "o1", "o2") HS_S2_TAP("%4", "%11", "%1", "ey", "pt", "o0", "o1", "o2")
-      "@e tcgen05.shift.cta_group::1.down [o0];\n\t@e tcgen05.shift.cta_group::1.down [o1];\n\t"
-      "@e tcgen05.shift.cta_group::1.down [o2];\n\t"
+      "tcgen05.shift.cta_group::1.down [o0];\n\ttcgen05.shift.cta_group::1.down [o1];\n\t"
+      "tcgen05.shift.cta_group::1.down [o2];\n\t"
       HS_S2_TAP("%3", "0", "%0", "ex", "pt", "o0", "o1", "o2") HS_S2_TAP("%4", "0", "%1", "ey", "pt", "o0", "o1", "o2")
-      "}\n" ::"r"(dx), "r"(dy), "r"(abase), "r"(wx), "r"(wy), "r"(valid), "n"(kDescHi), "n"(I0), "n"(I1), "n"(I2),
+      "S2_SKIP_%=:\n\t}\n" ::"r"(dx), "r"(dy), "r"(abase), "r"(wx), "r"(wy), "r"(valid), "n"(kDescHi), "n"(I0), "n"(I1), "n"(I2),
       "n"(1 * S2::WT), "n"(2 * S2::WT)
       : "memory");
 #undef HS_S2_MMA3
 #undef HS_S2_TAP
+  __syncwarp();
 }
 
 __global__ void __launch_bounds__(NT, 1) k_conv_shift_s2(ShArgs a) {
@@ -1083,27 +1088,28 @@ HS_DEV void t_row_mmas(uint32_t da, uint32_t db_, uint32_t dc, uint32_t abase, u
       "{\n\t.reg .pred e, ea, eb, ec, pz, pt;\n\t.reg .b64 db;\n\t"
       ".reg .b32 hi, i0, i1, i2, a01, a10, a11, a20, a21, da1, db1, dc1, bl, m;\n\t"
       "mov.b32 hi, %6;\n\tmov.b32 i0, %7;\n\tmov.b32 i1, %8;\n\tmov.b32 i2, %9;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "and.b32 m, %5, 1;\n\tsetp.ne.b32 ea, m, 0;\n\tand.pred ea, ea, e;\n\t"
-      "and.b32 m, %5, 2;\n\tsetp.ne.b32 eb, m, 0;\n\tand.pred eb, eb, e;\n\t"
-      "and.b32 m, %5, 4;\n\tsetp.ne.b32 ec, m, 0;\n\tand.pred ec, ec, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t@!e bra T_SKIP_%=;\n\t"  // the elected lane branches in: uniform predicates below
+      "and.b32 m, %5, 1;\n\tsetp.ne.b32 ea, m, 0;\n\t"
+      "and.b32 m, %5, 2;\n\tsetp.ne.b32 eb, m, 0;\n\t"
+      "and.b32 m, %5, 4;\n\tsetp.ne.b32 ec, m, 0;\n\t"
       "and.b32 m, %5, 8;\n\tsetp.ne.b32 pz, m, 0;\n\tsetp.eq.b32 pt, %5, %5;\n\t"
       "add.u32 a01, %3, 8;\n\tadd.u32 a10, %3, 16;\n\tadd.u32 a11, %3, 24;\n\tadd.u32 a20, %3, 32;\n\tadd.u32 a21, %3, 40;\n\t"
       "add.u32 da1, %0, 48;\n\tadd.u32 db1, %1, 48;\n\tadd.u32 dc1, %2, 48;\n\t"
       // row as written: kx 1 -> even output columns, kx 2 -> odd output columns
       HS_T_TAP("%11", "%0", "ea", "pt") HS_T_TAP("%14", "%1", "eb", "pz") HS_T_TAP("%17", "%2", "ec", "pz")
       HS_T_TAP("%12", "da1", "ea", "pt") HS_T_TAP("%15", "db1", "eb", "pz") HS_T_TAP("%18", "dc1", "ec", "pz")
-      "@e tcgen05.shift.cta_group::1.down [%3];\n\t@e tcgen05.shift.cta_group::1.down [a01];\n\t"
-      "@e tcgen05.shift.cta_group::1.down [a10];\n\t@e tcgen05.shift.cta_group::1.down [a11];\n\t"
-      "@e tcgen05.shift.cta_group::1.down [a20];\n\t@e tcgen05.shift.cta_group::1.down [a21];\n\t"
+      "tcgen05.shift.cta_group::1.down [%3];\n\ttcgen05.shift.cta_group::1.down [a01];\n\t"
+      "tcgen05.shift.cta_group::1.down [a10];\n\ttcgen05.shift.cta_group::1.down [a11];\n\t"
+      "tcgen05.shift.cta_group::1.down [a20];\n\ttcgen05.shift.cta_group::1.down [a21];\n\t"
       // shifted row (pixel p + 1): kx 0 -> odd output columns
       HS_T_TAP("%10", "da1", "ea", "pt") HS_T_TAP("%13", "db1", "eb", "pt") HS_T_TAP("%16", "dc1", "ec", "pt")
-      "}\n" ::"r"(da), "r"(db_), "r"(dc), "r"(abase), "r"(wlo), "r"(valid), "n"(kDescHi), "n"(I0), "n"(I1), "n"(I2),
+      "T_SKIP_%=:\n\t}\n" ::"r"(da), "r"(db_), "r"(dc), "r"(abase), "r"(wlo), "r"(valid), "n"(kDescHi), "n"(I0), "n"(I1), "n"(I2),
       "n"(0 * F::WT), "n"(1 * F::WT), "n"(2 * F::WT), "n"(3 * F::WT), "n"(4 * F::WT), "n"(5 * F::WT),
       "n"(6 * F::WT), "n"(7 * F::WT), "n"(8 * F::WT), "n"(F::KK)
       : "memory");
 #undef HS_T_MMA3
 #undef HS_T_TAP
+  __syncwarp();
 }
 
 template <int CIN_>
