@@ -55,6 +55,9 @@ using namespace tc;
 #ifndef HS_SH_FRAG
 #define HS_SH_FRAG 0  // stride-1 epilogue drains TMEM as 16x256b fragments (no transposes; 8-byte stores, full sectors): measured equal, in isolation and in the network
 #endif
+#ifndef HS_SH_NOROT
+#define HS_SH_NOROT 0  // 1: plain piece order in the 128-byte-pixel converters (8-way bank conflicts, no select stages)
+#endif
 #ifndef HS_SH_NR
 #define HS_SH_NR 12
 #endif
@@ -361,7 +364,7 @@ __global__ void __launch_bounds__(NT, 1) k_conv_shift(ShArgs a) {
             // a lane's pixel is 4 C bytes, so eight lanes reading piece i of their pixels would hit one or two
             // bank groups; lane L reads its pieces rotated by r instead -- eight distinct bank groups per
             // wavefront -- and rotates them back in registers (log2(NP) select stages)
-            const int r = C == 32 ? (lane & 7) : ((lane >> 1) & 3);
+            const int r = HS_SH_NOROT ? 0 : (C == 32 ? (lane & 7) : ((lane >> 1) & 3));
             float4 w4[NP];
 #pragma unroll
             for (int i = 0; i < NP; ++i) w4[i] = src[(i + r) & (NP - 1)];
@@ -858,7 +861,7 @@ __global__ void __launch_bounds__(NT, 1) k_conv_shift_s2(ShArgs a) {
         if ((oke || oko) && g >= 0 && g < a.H) {
           const float4* src = reinterpret_cast<const float4*>(raw + (size_t)s * F::RAW_BYTES + (size_t)q * F::QBYTES +
                                                               (size_t)(31 - lane) * 128);
-          const int r = lane & 7;  // rotated piece order: eight bank groups per quarter-warp wavefront
+          const int r = HS_SH_NOROT ? 0 : (lane & 7);  // rotated piece order: eight bank groups per quarter-warp wavefront
           float4 w4[8];
 #pragma unroll
           for (int k = 0; k < 8; ++k) w4[k] = src[(k + r) & 7];
@@ -1233,7 +1236,7 @@ __global__ void __launch_bounds__(NT, 1) k_conv_shift_t(ShArgs a) {
           if (xok && g < a.H) {
             const float4* src = reinterpret_cast<const float4*>(raw + (size_t)s * F::RAW_BYTES + (size_t)q * F::QBYTES +
                                                                 (size_t)lane * (C * 4) + (size_t)h * 128);
-            const int r = lane & 7;  // rotated piece order: eight bank groups per quarter-warp wavefront
+            const int r = HS_SH_NOROT ? 0 : (lane & 7);  // rotated piece order: eight bank groups per quarter-warp wavefront
             float4 w4[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) w4[k] = src[(k + r) & 7];
